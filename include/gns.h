@@ -1,0 +1,262 @@
+/*
+ * gns.h — C ABI of the B200-native Global Neighbor Sampling hot path.
+ *
+ * libgns.so (paper_2106_06150_b200/libgns.so, sm_100a) exports exactly these
+ * symbols.  All array arguments are DEVICE pointers unless stated; every call
+ * is asynchronous on `stream` (a cudaStream_t passed as void*) and writes only
+ * into caller-owned buffers.  Functions that need scratch take a caller-given
+ * workspace whose size is queried first with the matching *_workspace_size().
+ * Counts that are produced on the device (cache size, edges, unique sources)
+ * are returned through device pointers so a whole mini-batch can be captured
+ * in a CUDA graph; the host reads them once per batch.
+ *
+ * Node ids are int32 (ogbn-papers100M has 111M < 2^31 nodes), CSR offsets are
+ * int64 (3.2B directed entries > 2^31), importance weights are float64 exactly
+ * as the reference computes them.
+ *
+ * Each entry point names the reference function it replaces (paths relative
+ * to /root/reference/pkg/src/gnsbench).  The reference is a Python package, so
+ * "replaces" means: the Python facade paper_2106_06150_b200/ keeps the
+ * reference signature and calls this function where the reference ran numpy.
+ *
+ * Status codes: GNS_OK, or an error whose message gns_last_error() returns.
+ * The facade maps GNS_EINVAL / GNS_EZEROPROB to ValueError (sampling.py:161,
+ * 202-207, 255-256; cache.py:34-37,49,57), GNS_ECAPACITY to InvariantError
+ * (graph.py:48) and GNS_ECUDA to RuntimeError.
+ */
+#ifndef GNS_B200_H_
+#define GNS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define GNS_API __attribute__((visibility("default")))
+#else
+#define GNS_API
+#endif
+
+#define GNS_OK 0
+#define GNS_EINVAL 1
+#define GNS_ECAPACITY 2
+#define GNS_ECUDA 3
+#define GNS_EZEROPROB 4
+
+/* Device-side error flags raised by kernels (bit set in a block's counts[GNS_CNT_ERR]). */
+#define GNS_ERRBIT_ZEROPROB 1u  /* cached draw with inclusion 0 (sampling.py:255-256) */
+#define GNS_ERRBIT_CAPACITY 2u  /* selection buffer could not converge */
+
+/* Layout of the per-block device counter array (int32[8]). */
+#define GNS_CNT_DST 0      /* number of dst rows (seeds)                    */
+#define GNS_CNT_EDGES 1    /* sampled edges (cached + fill)                 */
+#define GNS_CNT_CACHED 2   /* cached-phase edges                            */
+#define GNS_CNT_SRC 3      /* unique src nodes after relabel                */
+#define GNS_CNT_HUBS 4     /* rows routed to the CTA-per-row sampler        */
+#define GNS_CNT_ERR 5      /* GNS_ERRBIT_* flags                             */
+#define GNS_CNT_N 8
+
+/* CSR graph (graph.py:52-104): indptr int64[N+1], indices int32[E]. */
+typedef struct gns_graph {
+  int64_t num_nodes;
+  int64_t num_edges;
+  const int64_t* indptr;
+  const int32_t* indices;
+} gns_graph_t;
+
+/* Cache state (cache.py:130-157): cached CSR N(v)∩C, membership bitmap over
+ * node ids (bit v of word v>>5), per-node inclusion probability (Eq. 9). */
+typedef struct gns_cache {
+  const int64_t* cached_indptr;   /* int64[N+1] */
+  const int32_t* cached_indices;  /* int32[nnz_C] */
+  const uint32_t* mask_bits;      /* uint32[ceil(N/32)] */
+  const double* inclusion;        /* float64[N] */
+} gns_cache_t;
+
+/* Philox4x32-10 key (oracle/philox.py): key = (seed, epoch), counter =
+ * (pos>>1, node, tag<<24|layer<<16|phase<<8, batch). */
+typedef struct gns_rng {
+  uint32_t seed;
+  uint32_t epoch;
+  uint32_t batch;
+  uint32_t layer;
+} gns_rng_t;
+
+/* One sampled layer (sampling.py:32-60 LayerBlock) in capacity-sized buffers. */
+typedef struct gns_block {
+  /* per dst row, capacity max_dst (+1 for row_scan) */
+  uint64_t* row_scan;      /* exclusive scan, packed (cached_prefix<<32 | fill_prefix); [n] = totals */
+  int32_t* dst_degree;     /* deg(dst) (sampling.py:149)                              */
+  int32_t* self_pos;       /* searchsorted(src_nodes, dst_nodes) (model.py:137)       */
+  int32_t* hub_rows;       /* rows handled by the CTA-per-row kernel                   */
+  /* per edge, capacity max_edges; order = cached edges then fill edges, each by (dst row, key) */
+  int32_t* edge_node;      /* global id of the sampled neighbour                       */
+  int32_t* edge_src;       /* relabelled: index into src_nodes (sampling.py:145)       */
+  int32_t* edge_dst;       /* dst row (sampling.py:146)                                */
+  double* edge_weight;     /* importance weight (sampling.py:168,252-258)              */
+  uint8_t* edge_cached;    /* cached-phase flag (sampling.py:263)                      */
+  /* src set, capacity max_src */
+  int32_t* src_nodes;      /* sorted unique seeds ∪ neighbours (sampling.py:141)        */
+  int32_t* counts;         /* int32[GNS_CNT_N] device counters                           */
+} gns_block_t;
+
+/* ---- library ------------------------------------------------------------ */
+GNS_API const char* gns_last_error(void);
+GNS_API int gns_version(void);
+
+/* ---- cache engine (cache.py) ------------------------------------------- */
+
+/* degree_probs (cache.py:53-58): out[i] = deg(i) / E in float64. */
+GNS_API int gns_degree_probs(const gns_graph_t* g, double* out_probs, void* stream);
+
+/* sample_cache (cache.py:87-103) + NodeSet.from_ids (graph.py:118-125):
+ * exponential race keys -log(1-U)/p over p>0, smallest min(cache_size,
+ * |support|) by (key, id) via radix select, emitted as sorted ids + bitmap.
+ * out_ids int32[cache_size]; out_mask_bits uint32[ceil(N/32)];
+ * out_counts int64[2] = {|C|, |support|} (device). */
+GNS_API size_t gns_cache_draw_workspace_size(int64_t num_nodes);
+GNS_API int gns_cache_draw(const double* probs, int64_t num_nodes, int64_t cache_size,
+                   uint32_t seed, uint32_t epoch, int32_t* out_ids,
+                   uint32_t* out_mask_bits, int64_t* out_counts, void* ws,
+                   size_t ws_bytes, void* stream);
+
+/* inclusion_prob (cache.py:106-117) and the forced-case pin of build_cache
+ * (cache.py:174-177).  cache_size_dev / support_dev (device int64, may be
+ * NULL) override cache_size and enable the pin when |C| >= |support|. */
+GNS_API int gns_inclusion(const double* probs, int64_t n, int64_t cache_size,
+                  const int64_t* cache_size_dev, const int64_t* support_dev,
+                  double* out, void* stream);
+
+/* Induced cached-neighbour CSR (cache.py:185-197) by filtering the full CSR
+ * with the cache bitmap (rows stay ascending).  Two phases: count (writes
+ * out_c_indptr and *out_nnz_dev), then fill (needs c_indices capacity >= nnz). */
+GNS_API size_t gns_cached_csr_workspace_size(int64_t num_nodes);
+GNS_API int gns_cached_csr_count(const gns_graph_t* g, const uint32_t* mask_bits,
+                         int64_t* out_c_indptr, int64_t* out_nnz_dev, void* ws,
+                         size_t ws_bytes, void* stream);
+GNS_API int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits,
+                        const int64_t* c_indptr, int32_t* out_c_indices,
+                        void* stream);
+
+/* ---- sampler (sampling.py) --------------------------------------------- */
+
+/* sample_neighbors_gns (sampling.py:189-266, policy gns-paper) when cache !=
+ * NULL, sample_neighbors_uniform (sampling.py:155-170) when cache == NULL.
+ * seeds: sorted unique int32 (count in *n_seeds_dev, <= max_dst).  Writes
+ * row_scan, dst_degree, edge_node/edge_dst/edge_weight/edge_cached and counts
+ * DST/EDGES/CACHED/HUBS/ERR.  Edge capacity must be >= max_dst * k. */
+GNS_API size_t gns_sample_workspace_size(int64_t max_dst);
+GNS_API int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache,
+                     const int32_t* seeds, const int32_t* n_seeds_dev,
+                     int64_t max_dst, int32_t k, int32_t cache_only,
+                     const gns_rng_t* rng, gns_block_t* block, void* ws,
+                     size_t ws_bytes, void* stream);
+
+/* _assemble (sampling.py:139-152): src_nodes = sorted unique(seeds ∪
+ * edge_node), edge_src = rank of edge_node, self_pos = rank of each seed.
+ * Bitmap dedup over node ids; the workspace bitmap must be zero on entry
+ * and is left zero.  Writes counts[GNS_CNT_SRC]. */
+GNS_API size_t gns_relabel_workspace_size(int64_t num_nodes);
+GNS_API int gns_relabel(int64_t num_nodes, const int32_t* seeds, const int32_t* n_seeds_dev,
+                int64_t max_dst, gns_block_t* block, int64_t max_edges,
+                void* ws, size_t ws_bytes, void* stream);
+
+/* np.unique of an id list (sampling.py:208,312): sorted unique ids of
+ * ids[0..n) (n = *n_dev if n_dev else n_host) into out, count into *out_n_dev. */
+GNS_API int gns_unique_sorted(int64_t num_nodes, const int32_t* ids, const int32_t* n_dev,
+                      int64_t n_host, int32_t* out, int32_t* out_n_dev, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/* ---- data loader (pool.py) --------------------------------------------- */
+
+/* epoch_targets (pool.py:60-66): out[j] = train_ids[perm(begin + j)] for
+ * j < count, perm = 4-round Feistel bijection keyed on (seed, epoch). */
+GNS_API int gns_epoch_targets(const int32_t* train_ids, int64_t n_train, uint32_t seed,
+                      uint32_t epoch, int64_t begin, int64_t count, int32_t* out,
+                      void* stream);
+
+/* ---- model side (model.py) --------------------------------------------- */
+
+/* features[input_nodes] (model.py:146): out[i,:] = table[rows[i],:], D
+ * columns.  dtype_in/out: 0 = float32, 1 = float64 (float32 -> float64 for
+ * the reference-parity mode).  ld_* are row strides in elements. */
+GNS_API int gns_gather_rows(const void* table, int64_t ld_in, int32_t dtype_in,
+                    const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
+                    int32_t dim, void* out, int64_t ld_out, int32_t dtype_out,
+                    void* stream);
+
+/* Mixed CPU-GPU placement (paper §3.1): cached rows from an HBM cache table
+ * (slot = rank of the node in the cache bitmap), the rest from a pinned host
+ * table through UVA. */
+GNS_API int gns_gather_rows_mixed(const float* host_table, const float* cache_table,
+                          const uint32_t* mask_bits, const int32_t* mask_word_rank,
+                          int64_t ld, const int32_t* rows, const int32_t* n_rows_dev,
+                          int64_t max_rows, int32_t dim, float* out, int64_t ld_out,
+                          void* stream);
+
+/* Refresh of the HBM cache table from the pinned host table (paper §3.1;
+ * modeled by metrics.py:83-86): cache_table[j,:] = host_table[ids[j],:]. */
+GNS_API int gns_cache_refresh_rows(const float* host_table, int64_t ld, const int32_t* ids,
+                           const int64_t* n_dev, int64_t max_rows, int32_t dim,
+                           float* cache_table, void* stream);
+
+/* Per-word exclusive popcount rank of a bitmap (slot lookup for the cache). */
+GNS_API int gns_bitmap_rank(const uint32_t* bits, int64_t nwords, int32_t* out_rank,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* Weighted mean aggregation + self concat (model.py:131-138,153-154):
+ * cat[r, 0:D]  = h[self_pos[r], :]
+ * cat[r, D:2D] = (sum_e w_e * h[edge_src_e, :]) / max(deg(r), 1)
+ * accumulated in ascending edge_src order (scipy CSR order).  dtype 0 =
+ * float32 (production), 1 = float64 bit-exact vs scipy (no FMA). */
+GNS_API int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim,
+                 const gns_block_t* block, int64_t max_dst, void* cat, int64_t ld_cat,
+                 void* stream);
+
+/* Backward of the above (model.py:223-225):
+ * dh[s,:] = sum_{e: src=s, ascending dst} w_e * (dcat[dst_e, D:2D] / max(deg,1))
+ *           (+ dcat[d, 0:D] where self_pos[d] == s).
+ * Builds the transposed block CSR in the workspace. */
+GNS_API size_t gns_spmm_bwd_workspace_size(int64_t max_src, int64_t max_edges);
+GNS_API int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim,
+                 const gns_block_t* block, int64_t max_dst, int64_t max_src,
+                 int64_t max_edges, void* dh, int64_t ld_dh, void* ws,
+                 size_t ws_bytes, void* stream);
+
+/* Softmax cross-entropy (model.py:189-200) over rows of logits for the
+ * sorted targets; labels gathered as labels[targets[r]].  Writes grad_out
+ * (same layout) and loss_out[0] = mean loss (device, float64). */
+GNS_API int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, const int32_t* n_dev,
+                     int64_t max_rows, int32_t num_classes, const int32_t* labels,
+                     const int32_t* targets, void* grad_out, double* loss_out,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* Bias-corrected Adam over a flat parameter buffer (model.py:229-242);
+ * grad_scale multiplies the gradient first (1/W after an allreduce). */
+GNS_API int gns_adam(int32_t dtype, void* params, const void* grads, void* m, void* v,
+             int64_t n, double lr, double beta1, double beta2, double eps,
+             int64_t step, double grad_scale, void* stream);
+
+/* ---- synthetic graphs (graph.py:172-205 analogue, device generator) ---- */
+
+/* Power-law (Chung-Lu style) random graph with the graph.py:142-169 contract:
+ * symmetric, no self loops, no duplicate edges, rows sorted ascending.
+ * num_pairs undirected endpoint pairs are drawn from Philox; endpoint rank x
+ * follows P(x) ~ (x + offset)^-alpha, ranks are scattered over ids by a
+ * Feistel bijection.  Two phases: count (builds sorted rows in the workspace,
+ * writes the final indptr and *out_nnz_dev) then fill (compacts unique
+ * neighbours into out_indices, capacity >= nnz). */
+GNS_API size_t gns_gen_workspace_size(int64_t num_nodes, int64_t num_pairs);
+GNS_API int gns_gen_powerlaw_count(int64_t num_nodes, int64_t num_pairs, double alpha, double offset,
+                           uint32_t seed, int64_t* out_indptr, int64_t* out_nnz_dev, void* ws,
+                           size_t ws_bytes, void* stream);
+GNS_API int gns_gen_powerlaw_fill(int64_t num_nodes, int64_t num_pairs, const int64_t* indptr,
+                          int32_t* out_indices, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNS_B200_H_ */

@@ -1,0 +1,20 @@
+"""B200-native Global Neighbor Sampling (arXiv 2106.06150) hot path.
+
+Drop-in for the sampler / data-loader API of the reference package
+``gnsbench`` (``/root/reference/pkg/src/gnsbench/__init__.py:5-22``): the cache
+engine, the NS/GNS neighbour samplers, ``build_minibatch``, ``SamplerPool`` and
+the GraphSAGE aggregation path, all running as hand-written sm_100a kernels in
+``libgns.so`` behind the C ABI in ``include/gns.h``.
+"""
+
+from ._lib import GraphFormatError, InvariantError
+from .cache import (CacheState, ProbVector, build_cache, degree_probs, inclusion_prob,
+                    sample_cache)
+from .graph import Graph, NodeSet, generate_powerlaw_device
+from .model import GraphSAGE, TrainConfig, init_params_numpy, micro_f1
+from .pool import BatchItem, SamplerPool, epoch_targets
+from .sampling import (BatchRng, LayerBlock, MiniBatch, MiniBatchSampler, SamplerConfig,
+                       build_minibatch, gns_weight_paper, isolated_fraction,
+                       sample_neighbors_gns, sample_neighbors_uniform, validate_minibatch)
+
+__version__ = "0.1.0"

@@ -1,0 +1,177 @@
+"""ctypes binding of libgns.so (include/gns.h).
+
+The extension lives in-tree (``paper_2106_06150_b200/libgns.so``), built for
+sm_100a by ``build.py``.  There is no fallback: if the library is missing or a
+CUDA device is absent, every product entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, Structure, c_double, c_int32, c_int64, c_size_t, c_uint32, c_void_p
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgns.so")
+
+GNS_OK = 0
+GNS_EINVAL = 1
+GNS_ECAPACITY = 2
+GNS_ECUDA = 3
+GNS_EZEROPROB = 4
+
+ERRBIT_ZEROPROB = 1
+ERRBIT_CAPACITY = 2
+
+CNT_DST, CNT_EDGES, CNT_CACHED, CNT_SRC, CNT_HUBS, CNT_ERR, CNT_N = 0, 1, 2, 3, 4, 5, 8
+
+
+class GraphFormatError(ValueError):
+    """graph.py:44 GraphFormatError."""
+
+
+class InvariantError(RuntimeError):
+    """graph.py:48 InvariantError."""
+
+
+class GnsGraph(Structure):
+    _fields_ = [("num_nodes", c_int64), ("num_edges", c_int64), ("indptr", c_void_p),
+                ("indices", c_void_p)]
+
+
+class GnsCache(Structure):
+    _fields_ = [("cached_indptr", c_void_p), ("cached_indices", c_void_p),
+                ("mask_bits", c_void_p), ("inclusion", c_void_p)]
+
+
+class GnsRng(Structure):
+    _fields_ = [("seed", c_uint32), ("epoch", c_uint32), ("batch", c_uint32),
+                ("layer", c_uint32)]
+
+
+class GnsBlock(Structure):
+    _fields_ = [("row_scan", c_void_p), ("dst_degree", c_void_p), ("self_pos", c_void_p),
+                ("hub_rows", c_void_p), ("edge_node", c_void_p), ("edge_src", c_void_p),
+                ("edge_dst", c_void_p), ("edge_weight", c_void_p), ("edge_cached", c_void_p),
+                ("src_nodes", c_void_p), ("counts", c_void_p)]
+
+
+_SIGS = {
+    "gns_last_error": (ctypes.c_char_p, []),
+    "gns_version": (c_int32, []),
+    "gns_degree_probs": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p]),
+    "gns_cache_draw_workspace_size": (c_size_t, [c_int64]),
+    "gns_cache_draw": (c_int32, [c_void_p, c_int64, c_int64, c_uint32, c_uint32, c_void_p,
+                                 c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "gns_inclusion": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                c_void_p]),
+    "gns_cached_csr_workspace_size": (c_size_t, [c_int64]),
+    "gns_cached_csr_count": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_size_t, c_void_p]),
+    "gns_cached_csr_fill": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p, c_void_p,
+                                      c_void_p]),
+    "gns_sample_workspace_size": (c_size_t, [c_int64]),
+    "gns_sample_layer": (c_int32, [POINTER(GnsGraph), POINTER(GnsCache), c_void_p, c_void_p,
+                                   c_int64, c_int32, c_int32, POINTER(GnsRng),
+                                   POINTER(GnsBlock), c_void_p, c_size_t, c_void_p]),
+    "gns_relabel_workspace_size": (c_size_t, [c_int64]),
+    "gns_relabel": (c_int32, [c_int64, c_void_p, c_void_p, c_int64, POINTER(GnsBlock), c_int64,
+                              c_void_p, c_size_t, c_void_p]),
+    "gns_unique_sorted": (c_int32, [c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                                    c_void_p, c_size_t, c_void_p]),
+    "gns_epoch_targets": (c_int32, [c_void_p, c_int64, c_uint32, c_uint32, c_int64, c_int64,
+                                    c_void_p, c_void_p]),
+    "gns_gather_rows": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_int64,
+                                  c_int32, c_void_p, c_int64, c_int32, c_void_p]),
+    "gns_gather_rows_mixed": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+                                        c_void_p, c_void_p, c_int64, c_int32, c_void_p,
+                                        c_int64, c_void_p]),
+    "gns_cache_refresh_rows": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+                                         c_int32, c_void_p, c_void_p]),
+    "gns_bitmap_rank": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "gns_spmm_fwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, POINTER(GnsBlock),
+                               c_int64, c_void_p, c_int64, c_void_p]),
+    "gns_spmm_bwd_workspace_size": (c_size_t, [c_int64, c_int64]),
+    "gns_spmm_bwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, POINTER(GnsBlock), c_int64,
+                               c_int64, c_int64, c_void_p, c_int64, c_void_p, c_size_t,
+                               c_void_p]),
+    "gns_softmax_xent": (c_int32, [c_int32, c_void_p, c_int64, c_void_p, c_int64, c_int32,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                   c_void_p]),
+    "gns_adam": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_double,
+                           c_double, c_double, c_double, c_int64, c_double, c_void_p]),
+    "gns_gen_workspace_size": (c_size_t, [c_int64, c_int64]),
+    "gns_gen_powerlaw_count": (c_int32, [c_int64, c_int64, c_double, c_double, c_uint32,
+                                         c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "gns_gen_powerlaw_fill": (c_int32, [c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                        c_size_t, c_void_p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libgns.so and declare every C-ABI signature (no CUDA needed)."""
+    global _lib
+    if _lib is not None and path == LIB_PATH:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"libgns.so not found at {path}; build it with "
+            "`python -m paper_2106_06150_b200.build` (nvcc, sm_100a)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path == LIB_PATH:
+        _lib = lib
+    return lib
+
+
+def lib():
+    return _lib if _lib is not None else load()
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2106_06150_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+
+
+def check(rc: int, what: str = ""):
+    if rc == GNS_OK:
+        return
+    msg = lib().gns_last_error().decode(errors="replace")
+    if rc in (GNS_EINVAL, GNS_EZEROPROB):
+        raise ValueError(f"{what}: {msg}" if what else msg)
+    if rc == GNS_ECAPACITY:
+        raise InvariantError(f"{what}: {msg}" if what else msg)
+    raise RuntimeError(f"{what}: {msg}" if what else msg)
+
+
+def call(name: str, *args):
+    check(getattr(lib(), name)(*args), name)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def workspace(nbytes: int, device, zero: bool = False) -> torch.Tensor:
+    nbytes = max(int(nbytes), 256)
+    if zero:
+        return torch.zeros(nbytes, dtype=torch.uint8, device=device)
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)

@@ -1,0 +1,217 @@
+"""Cache engine on B200 (reference: cache.py).
+
+Same API as the reference: ``ProbVector``, ``degree_probs``, ``sample_cache``,
+``inclusion_prob``, ``CacheState``, ``build_cache``.  Every array lives in
+HBM and every computation is a libgns.so kernel:
+
+* ``degree_probs``  -> gns_degree_probs            (cache.py:53-58)
+* ``sample_cache``  -> gns_cache_draw              (cache.py:87-103): Philox
+  exponential race + 11-bit radix select + ordered compaction
+* ``inclusion_prob``-> gns_inclusion               (cache.py:106-117)
+* ``build_cache``   -> draw + inclusion + gns_cached_csr_count/fill
+  (cache.py:160-197; the induced CSR is built by filtering the full CSR with
+  the cache bitmap, which yields the same ascending rows)
+
+``rng_seed`` follows the reference's call sites: ``[seed, 33, epoch]`` (pool.py:117)
+keys Philox with (seed, epoch); a bare int is (seed, 0).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graph import Graph, NodeSet
+
+_CACHE_TAG = 33
+
+
+def seed_epoch(rng_seed) -> tuple[int, int]:
+    """Map the reference's ``rng_seed`` forms to the Philox key (seed, epoch)."""
+    if np.isscalar(rng_seed):
+        return int(rng_seed) & 0xFFFFFFFF, 0
+    s = [int(x) for x in rng_seed]
+    if len(s) == 3:           # [seed, tag, epoch]  (pool.py:117)
+        return s[0] & 0xFFFFFFFF, s[2] & 0xFFFFFFFF
+    if len(s) == 2:
+        return s[0] & 0xFFFFFFFF, s[1] & 0xFFFFFFFF
+    if len(s) == 1:
+        return s[0] & 0xFFFFFFFF, 0
+    h = 0
+    for x in s:
+        h = (h * 1000003 + x) & 0xFFFFFFFF
+    return h, 0
+
+
+@dataclass(frozen=True, eq=False)
+class ProbVector:
+    """Non-negative per-node weights on the device (cache.py:25-50)."""
+
+    weights: torch.Tensor
+    normalized: bool = False
+
+    def __post_init__(self):
+        w = self.weights
+        if not torch.is_tensor(w):
+            w = torch.as_tensor(np.asarray(w, dtype=np.float64), device="cuda")
+        w = w.to(torch.float64)
+        bad = torch.logical_or(w < 0, ~torch.isfinite(w)).any()
+        if bool(bad):
+            raise ValueError("probability weights must be finite and >= 0")
+        if self.normalized and abs(float(w.sum()) - 1.0) > 1e-9:
+            raise ValueError("normalized ProbVector must sum to 1")
+        object.__setattr__(self, "weights", w)
+
+    def __len__(self) -> int:
+        return int(self.weights.shape[0])
+
+    def normalize(self) -> "ProbVector":
+        if self.normalized:
+            return self
+        total = float(self.weights.sum())
+        if total <= 0:
+            raise ValueError("cannot normalize an all-zero weight vector")
+        return ProbVector(self.weights / total, normalized=True)
+
+
+def degree_probs(g: Graph) -> ProbVector:
+    """cache.py:53-58: p_i = deg(i) / sum deg."""
+    _lib.require_cuda()
+    if g.num_edges == 0:
+        raise ValueError("graph has no edges; degree distribution undefined")
+    out = torch.empty(g.num_nodes, dtype=torch.float64, device=g.device)
+    _lib.call("gns_degree_probs", g.cstruct(), out.data_ptr(), _lib.stream_ptr())
+    return ProbVector(out, normalized=True)
+
+
+class _DrawWorkspace:
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, n: int, device) -> torch.Tensor:
+        key = (n, str(device))
+        ws = cls._cache.get(key)
+        if ws is None:
+            cls._cache.clear()
+            ws = _lib.workspace(_lib.lib().gns_cache_draw_workspace_size(n), device)
+            cls._cache[key] = ws
+        return ws
+
+
+def _draw(probs: ProbVector, cache_size: int, seed: int, epoch: int, stream=None):
+    w = probs.weights
+    n = int(w.shape[0])
+    dev = w.device
+    cs = max(int(cache_size), 0)
+    ids = torch.empty(max(cs, 1), dtype=torch.int32, device=dev)
+    bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws = _DrawWorkspace.get(n, dev)
+    _lib.call("gns_cache_draw", w.data_ptr(), n, cs, seed, epoch, ids.data_ptr(), bits.data_ptr(),
+              counts.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(stream))
+    return ids, bits, counts
+
+
+def sample_cache(probs: ProbVector, cache_size: int, rng_seed) -> NodeSet:
+    """cache.py:87-103: min(cache_size, #positive) ids drawn without replacement
+    with probability proportional to the weights (exponential race)."""
+    _lib.require_cuda()
+    seed, epoch = seed_epoch(rng_seed)
+    ids, bits, counts = _draw(probs, cache_size, seed, epoch)
+    k = int(counts[0])
+    return NodeSet(ids=ids[:k], mask_bits=bits, num_nodes=len(probs))
+
+
+def inclusion_prob(p, cache_size: int):
+    """cache.py:106-117: 1 - (1 - p)^|C| as -expm1(|C| log1p(-min(p, 1-1e-15)))."""
+    _lib.require_cuda()
+    scalar = np.isscalar(p)
+    host = not torch.is_tensor(p)
+    t = torch.as_tensor(np.asarray(p, dtype=np.float64) if host else p.to(torch.float64),
+                        device="cuda").reshape(-1).contiguous()
+    out = torch.empty_like(t)
+    _lib.call("gns_inclusion", t.data_ptr(), t.numel(), int(cache_size), None, None,
+              out.data_ptr(), _lib.stream_ptr())
+    if scalar:
+        return float(out[0])
+    if host:
+        return out.cpu().numpy().reshape(np.shape(p))
+    return out.reshape(p.shape)
+
+
+@dataclass(frozen=True, eq=False)
+class CacheState:
+    """cache.py:130-157: cache set + what samplers need, all in HBM."""
+
+    nodes: NodeSet
+    inclusion: torch.Tensor       # float64[N]
+    cached_indptr: torch.Tensor   # int64[N+1]
+    cached_indices: torch.Tensor  # int32[nnz]
+    epoch: int
+    source_probs: ProbVector
+
+    def __len__(self) -> int:
+        return len(self.nodes)
+
+    def num_cached_neighbors(self, v: int) -> int:
+        return int(self.cached_indptr[v + 1] - self.cached_indptr[v])
+
+    def cached_neighbors(self, v: int) -> torch.Tensor:
+        return self.cached_indices[int(self.cached_indptr[v]):int(self.cached_indptr[v + 1])]
+
+    def cstruct(self):
+        c = getattr(self, "_c", None)
+        if c is None:
+            c = _lib.GnsCache(self.cached_indptr.data_ptr(), self.cached_indices.data_ptr(),
+                              self.nodes.mask_bits.data_ptr(), self.inclusion.data_ptr())
+            object.__setattr__(self, "_c", c)
+        return c
+
+    def mask_word_rank(self) -> torch.Tensor:
+        """Per-word popcount rank of the cache bitmap (cache-slot lookup)."""
+        r = getattr(self, "_rank", None)
+        if r is None:
+            bits = self.nodes.mask_bits
+            r = torch.empty_like(bits)
+            ws = _lib.workspace(1 << 20, bits.device)
+            _lib.call("gns_bitmap_rank", bits.data_ptr(), bits.numel(), r.data_ptr(), ws.data_ptr(),
+                      ws.numel(), _lib.stream_ptr())
+            object.__setattr__(self, "_rank", r)
+        return r
+
+
+def build_cache(g: Graph, probs: ProbVector, cache_size: int, epoch: int = 0, rng_seed=0,
+                inclusion_mode: str = "analytic", resamples: int = 64) -> CacheState:
+    """cache.py:160-197 (analytic inclusion)."""
+    _lib.require_cuda()
+    if inclusion_mode == "empirical":
+        raise NotImplementedError("empirical inclusion (cache.py:178-181) is outside the B200 "
+                                  "hot path (SURVEY.md §8(f)3)")
+    if inclusion_mode != "analytic":
+        raise ValueError(f"unknown inclusion_mode {inclusion_mode!r}")
+    probs = probs.normalize()
+    stream = _lib.stream_ptr()
+    seed, ep = seed_epoch(rng_seed)
+    ids, bits, counts = _draw(probs, cache_size, seed, ep)
+    n = g.num_nodes
+    incl = torch.empty(n, dtype=torch.float64, device=g.device)
+    # |C| and |support| stay on the device (counts[0], counts[1])
+    _lib.call("gns_inclusion", probs.weights.data_ptr(), n, 0, counts.data_ptr(),
+              counts[1:].data_ptr(), incl.data_ptr(), stream)
+    c_indptr = torch.empty(n + 1, dtype=torch.int64, device=g.device)
+    nnz = torch.zeros(1, dtype=torch.int64, device=g.device)
+    ws = _lib.workspace(_lib.lib().gns_cached_csr_workspace_size(n), g.device)
+    _lib.call("gns_cached_csr_count", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
+              nnz.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    host = counts.cpu()  # one sync per refresh: |C| and nnz_C size the outputs
+    nnz_h = int(nnz.item())
+    c_indices = torch.empty(max(nnz_h, 1), dtype=torch.int32, device=g.device)
+    _lib.call("gns_cached_csr_fill", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
+              c_indices.data_ptr(), stream)
+    k = int(host[0])
+    nodes = NodeSet(ids=ids[:k], mask_bits=bits, num_nodes=n)
+    return CacheState(nodes=nodes, inclusion=incl, cached_indptr=c_indptr,
+                      cached_indices=c_indices[:nnz_h], epoch=epoch, source_probs=probs)

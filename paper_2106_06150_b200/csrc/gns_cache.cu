@@ -1,0 +1,347 @@
+// Cache engine on B200: the degree-proportional cache draw (cache.py:87-103)
+// and the induced cached-neighbour CSR (cache.py:185-197).
+//
+// Draw = exponential race.  key(i) = -log(1 - U_i) / p_i over p_i > 0, U_i from
+// Philox at (tag 33, node 0, pos = i).  The |C| smallest (key, id) pairs are
+// found with an 11-bit-digit radix select over the key bit patterns (positive
+// doubles order like their uint64 bits), then one ordered stream compaction
+// emits sorted ids and the membership bitmap.  Ties at the threshold key are
+// broken by node id (oracle/gns.py:sample_cache).
+#include "gns_common.cuh"
+
+namespace gns {
+
+static constexpr int kDigitBits[6] = {11, 11, 11, 11, 11, 9};
+static constexpr int kDigitShift[6] = {53, 42, 31, 20, 9, 0};
+static constexpr uint64_t kNoKey = ~0ull;  // non-support sentinel (> +inf bits)
+
+struct SelectState {
+  unsigned long long prefix;       // selected high bits so far
+  unsigned long long prefix_mask;  // which bits are fixed
+  long long remaining;             // rank (1-based) still to find inside the prefix
+  long long k_eff;                 // min(cache_size, support)
+  unsigned long long support;      // |{p > 0}|
+  long long pad[3];
+};
+
+__global__ void cache_keys_kernel(const double* __restrict__ probs, int64_t n, uint32_t seed,
+                                  uint32_t epoch, uint64_t* __restrict__ keys,
+                                  SelectState* __restrict__ st) {
+  const uint32_t stream = stream_word(33, 0, 0);
+  unsigned long long local = 0;
+  // each thread handles pairs (2q, 2q+1) so one Philox block serves two nodes
+  const int64_t npairs = (n + 1) >> 1;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npairs;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t ke, ko;
+    key53_pair(seed, epoch, 0u, stream, 0u, (uint32_t)q, ke, ko);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      int64_t i = 2 * q + j;
+      if (i >= n) break;
+      double p = probs[i];
+      uint64_t out = kNoKey;
+      if (p > 0.0) {
+        uint64_t k53 = j ? ko : ke;
+        double u = (double)k53 * 0x1p-53;   // exact
+        double e = -det_log(DSUB(1.0, u));  // Exp(1); 1-u exact
+        double key = DDIV(e, p);
+        out = (uint64_t)__double_as_longlong(key);
+        ++local;
+      }
+      keys[i] = out;
+    }
+  }
+  local = warp_sum(local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(&st->support, local);
+}
+
+__global__ void select_init_kernel(SelectState* st, int64_t cache_size) {
+  long long sup = (long long)st->support;
+  long long k = cache_size < sup ? cache_size : sup;
+  if (k < 0) k = 0;
+  st->k_eff = k;
+  st->remaining = k;
+  st->prefix = 0;
+  st->prefix_mask = 0;
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) radix_hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                                           const SelectState* __restrict__ st, int shift,
+                                                           int bits, unsigned int* __restrict__ hist) {
+  __shared__ unsigned int sh[2048];
+  const int nb = 1 << bits;
+  for (int i = threadIdx.x; i < nb; i += BLOCK) sh[i] = 0;
+  __syncthreads();
+  const unsigned long long prefix = st->prefix, pmask = st->prefix_mask;
+  if (st->remaining > 0) {
+    for (int64_t i = blockIdx.x * (int64_t)BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
+      uint64_t k = keys[i];
+      if (k != kNoKey && (k & pmask) == prefix) atomicAdd(&sh[(k >> shift) & (nb - 1)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += BLOCK)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// one block of 1024 threads: find the digit that contains rank `remaining`.
+__global__ void radix_pick_kernel(SelectState* st, int shift, int bits, unsigned int* hist) {
+  __shared__ unsigned long long part[1024];
+  __shared__ int s_bin;
+  __shared__ unsigned long long s_below;
+  const int nb = 1 << bits;
+  const int per = (nb + 1023) / 1024;  // 2 for 2048 bins
+  const long long rem = st->remaining;
+  unsigned long long c[2] = {0, 0};
+  unsigned long long tsum = 0;
+  for (int j = 0; j < per; ++j) {
+    int b = threadIdx.x * per + j;
+    c[j] = (b < nb) ? hist[b] : 0;
+    tsum += c[j];
+  }
+  part[threadIdx.x] = tsum;
+  __syncthreads();
+  // Hillis-Steele inclusive scan over 1024 partials
+  for (int o = 1; o < 1024; o <<= 1) {
+    unsigned long long t = (threadIdx.x >= o) ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += t;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { s_bin = -1; s_below = 0; }
+  __syncthreads();
+  if (rem > 0) {
+    unsigned long long run = part[threadIdx.x] - tsum;  // exclusive
+    for (int j = 0; j < per; ++j) {
+      int b = threadIdx.x * per + j;
+      if (b < nb && run < (unsigned long long)rem && run + c[j] >= (unsigned long long)rem) {
+        s_bin = b;
+        s_below = run;
+      }
+      run += c[j];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && rem > 0 && s_bin >= 0) {
+    unsigned long long dmask = ((unsigned long long)(nb - 1)) << shift;
+    st->prefix |= ((unsigned long long)s_bin) << shift;
+    st->prefix_mask |= dmask;
+    st->remaining = rem - (long long)s_below;
+  }
+  for (int b = threadIdx.x; b < nb; b += 1024) hist[b] = 0;  // ready for next pass
+}
+
+// classify: per 32-node word, bits of keys < T and keys == T.
+__global__ void classify_kernel(const uint64_t* __restrict__ keys, int64_t n, const SelectState* __restrict__ st,
+                                uint32_t* __restrict__ less_bits, uint32_t* __restrict__ eq_bits) {
+  const bool any = st->k_eff > 0;
+  const unsigned long long T = st->prefix;
+  const int64_t nw = (n + 31) >> 5;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw * 32;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = (i < n) ? keys[i] : kNoKey;
+    bool lt = any && k != kNoKey && k < T;
+    bool eq = any && k != kNoKey && k == T;
+    unsigned bl = __ballot_sync(GNS_FULL, lt);
+    unsigned be = __ballot_sync(GNS_FULL, eq);
+    if ((threadIdx.x & 31) == 0) {
+      less_bits[i >> 5] = bl;
+      eq_bits[i >> 5] = be;
+    }
+  }
+}
+
+// ordered compaction over words: value = (popc(less) << 32) | popc(eq)
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) cache_compact_kernel(ScanStatus ss, const uint32_t* __restrict__ less_bits,
+                                                              const uint32_t* __restrict__ eq_bits, int64_t nw,
+                                                              const SelectState* __restrict__ st,
+                                                              int32_t* __restrict__ out_ids,
+                                                              uint32_t* __restrict__ out_mask,
+                                                              int64_t* __restrict__ out_counts) {
+  const long long need_eq = st->remaining;  // equal keys still to take, in id order
+  scan_tiles<BLOCK, ITEMS>(
+      ss, nw,
+      [&](long long w) {
+        return ((unsigned long long)__popc(less_bits[w]) << 32) | (unsigned long long)__popc(eq_bits[w]);
+      },
+      [&](long long w, unsigned long long ex, unsigned long long) {
+        long long a_ex = (long long)(ex >> 32), b_ex = (long long)(ex & 0xffffffffull);
+        uint32_t lt = less_bits[w], eq = eq_bits[w];
+        uint32_t sel = lt;
+        long long taken_eq = b_ex < need_eq ? b_ex : need_eq;
+        long long cnt_eq = b_ex;
+        while (eq) {
+          int b = __ffs(eq) - 1;
+          eq &= eq - 1;
+          if (cnt_eq < need_eq) sel |= 1u << b;
+          ++cnt_eq;
+        }
+        out_mask[w] = sel;
+        long long pos = a_ex + taken_eq;
+        uint32_t s = sel;
+        while (s) {
+          int b = __ffs(s) - 1;
+          s &= s - 1;
+          out_ids[pos++] = (int32_t)(w * 32 + b);
+        }
+      },
+      [&](unsigned long long tot) {
+        long long a = (long long)(tot >> 32), b = (long long)(tot & 0xffffffffull);
+        out_counts[0] = a + (b < need_eq ? b : need_eq);
+        out_counts[1] = (long long)st->support;
+      });
+}
+
+// ---- cached CSR --------------------------------------------------------------
+// count: per node, number of neighbours in the cache (one warp per row)
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) ccsr_count_scan_kernel(ScanStatus ss, const int64_t* __restrict__ rowcnt,
+                                                                int64_t n, int64_t* __restrict__ c_indptr,
+                                                                int64_t* __restrict__ nnz_dev) {
+  scan_tiles<BLOCK, ITEMS>(
+      ss, n, [&](long long i) { return (unsigned long long)rowcnt[i]; },
+      [&](long long i, unsigned long long ex, unsigned long long) { c_indptr[i] = (int64_t)ex; },
+      [&](unsigned long long tot) {
+        c_indptr[n] = (int64_t)tot;
+        nnz_dev[0] = (int64_t)tot;
+      });
+}
+
+__device__ __forceinline__ bool in_mask(const uint32_t* __restrict__ mask, int32_t v) {
+  return (__ldg(mask + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+__global__ void ccsr_rowcount_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                                     int64_t n, const uint32_t* __restrict__ mask, int64_t* __restrict__ rowcnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    int64_t b = indptr[r], e = indptr[r + 1];
+    unsigned c = 0;
+    for (int64_t p = b + lane; p < e; p += 32) c += in_mask(mask, __ldg(indices + p));
+    c = warp_sum(c);
+    if (lane == 0) rowcnt[r] = c;
+  }
+}
+
+__global__ void ccsr_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                                 int64_t n, const uint32_t* __restrict__ mask,
+                                 const int64_t* __restrict__ c_indptr, int32_t* __restrict__ c_indices) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    int64_t b = indptr[r], e = indptr[r + 1];
+    int64_t out = c_indptr[r];
+    if (c_indptr[r + 1] == out) continue;
+    for (int64_t base = b; base < e; base += 32) {
+      int64_t p = base + lane;
+      int32_t v = (p < e) ? __ldg(indices + p) : 0;
+      bool keep = (p < e) && in_mask(mask, v);
+      unsigned bal = __ballot_sync(GNS_FULL, keep);
+      if (keep) c_indices[out + __popc(bal & ((1u << lane) - 1))] = v;
+      out += __popc(bal);
+    }
+  }
+}
+
+}  // namespace gns
+
+using namespace gns;
+
+static size_t cache_draw_ws(int64_t n, char* base, size_t cap, uint64_t** keys, uint32_t** lt,
+                            uint32_t** eq, unsigned** hist, SelectState** st, void** scan,
+                            long long* tiles) {
+  Workspace w(base, cap);
+  int64_t nw = (n + 31) / 32;
+  *keys = w.take<uint64_t>(n > 0 ? n : 1);
+  *lt = w.take<uint32_t>(nw + 1);
+  *eq = w.take<uint32_t>(nw + 1);
+  *hist = w.take<unsigned>(2048);
+  *st = w.take<SelectState>(1);
+  *tiles = (nw + 256 * 8 - 1) / (256 * 8) + 1;
+  *scan = (void*)w.take<char>(scan_status_bytes(*tiles));
+  return w.off;
+}
+
+extern "C" {
+
+size_t gns_cache_draw_workspace_size(int64_t num_nodes) {
+  uint64_t* k; uint32_t *a, *b; unsigned* h; SelectState* s; void* sc; long long t;
+  return cache_draw_ws(num_nodes, nullptr, 0, &k, &a, &b, &h, &s, &sc, &t);
+}
+
+int gns_cache_draw(const double* probs, int64_t n, int64_t cache_size, uint32_t seed, uint32_t epoch,
+                   int32_t* out_ids, uint32_t* out_mask_bits, int64_t* out_counts, void* ws,
+                   size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (n <= 0) {
+    set_error("cache_draw: empty graph");
+    return GNS_EINVAL;
+  }
+  uint64_t* keys; uint32_t *lt, *eq; unsigned* hist; SelectState* st; void* scan; long long tiles;
+  size_t need = cache_draw_ws(n, (char*)ws, ws_bytes, &keys, &lt, &eq, &hist, &st, &scan, &tiles);
+  if (need > ws_bytes) {
+    set_error("cache_draw: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  if (cache_size < 0) cache_size = 0;
+  const int sms = num_sms();
+  GNS_CUDA(cudaMemsetAsync(hist, 0, 2048 * sizeof(unsigned), stream));
+  GNS_CUDA(cudaMemsetAsync(st, 0, sizeof(SelectState), stream));
+  cache_keys_kernel<<<sms * 8, 256, 0, stream>>>(probs, n, seed, epoch, keys, st);
+  GNS_TRY(check_launch("cache_keys"));
+  select_init_kernel<<<1, 1, 0, stream>>>(st, cache_size);
+  for (int pass = 0; pass < 6; ++pass) {
+    radix_hist_kernel<256><<<sms * 4, 256, 0, stream>>>(keys, n, st, kDigitShift[pass], kDigitBits[pass], hist);
+    radix_pick_kernel<<<1, 1024, 0, stream>>>(st, kDigitShift[pass], kDigitBits[pass], hist);
+  }
+  GNS_TRY(check_launch("radix_select"));
+  int64_t nw = (n + 31) / 32;
+  classify_kernel<<<sms * 8, 256, 0, stream>>>(keys, n, st, lt, eq);
+  ScanStatus ss = make_scan_status(scan, tiles);
+  GNS_CUDA(cudaMemsetAsync(scan, 0, scan_status_bytes(tiles), stream));
+  cache_compact_kernel<256, 8><<<(unsigned)tiles, 256, 0, stream>>>(ss, lt, eq, nw, st, out_ids, out_mask_bits,
+                                                                    out_counts);
+  return check_launch("cache_compact");
+}
+
+size_t gns_cached_csr_workspace_size(int64_t num_nodes) {
+  long long tiles = (num_nodes + 256 * 16 - 1) / (256 * 16) + 1;
+  return (((size_t)num_nodes * 8 + 255) & ~(size_t)255) + scan_status_bytes(tiles);
+}
+
+int gns_cached_csr_count(const gns_graph_t* g, const uint32_t* mask_bits, int64_t* out_c_indptr,
+                         int64_t* out_nnz_dev, void* ws, size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int64_t n = g->num_nodes;
+  size_t need = gns_cached_csr_workspace_size(n);
+  if (ws_bytes < need) {
+    set_error("cached_csr: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  int64_t* rowcnt = (int64_t*)ws;
+  char* scan = (char*)ws + (((size_t)n * 8 + 255) & ~(size_t)255);
+  long long tiles = (n + 256 * 16 - 1) / (256 * 16) + 1;
+  const int sms = num_sms();
+  ccsr_rowcount_kernel<<<sms * 8, 256, 0, stream>>>(g->indptr, g->indices, n, mask_bits, rowcnt);
+  GNS_TRY(check_launch("ccsr_rowcount"));
+  GNS_CUDA(cudaMemsetAsync(scan, 0, scan_status_bytes(tiles), stream));
+  ccsr_count_scan_kernel<256, 16><<<(unsigned)tiles, 256, 0, stream>>>(make_scan_status(scan, tiles), rowcnt, n,
+                                                                       out_c_indptr, out_nnz_dev);
+  return check_launch("ccsr_scan");
+}
+
+int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits, const int64_t* c_indptr,
+                        int32_t* out_c_indices, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  ccsr_fill_kernel<<<num_sms() * 8, 256, 0, stream>>>(g->indptr, g->indices, g->num_nodes, mask_bits, c_indptr,
+                                                      out_c_indices);
+  return check_launch("ccsr_fill");
+}
+
+}  // extern "C"

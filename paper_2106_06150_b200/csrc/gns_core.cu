@@ -1,0 +1,158 @@
+// Library plumbing + small kernels: error state, degree_probs (cache.py:53-58),
+// Eq. 9 inclusion (cache.py:106-117, 174-177), Feistel epoch targets
+// (pool.py:60-66), bitmap rank.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "gns_common.cuh"
+
+namespace gns {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return GNS_ECUDA;
+  }
+  return GNS_OK;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+  }
+  return sms;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void degree_probs_kernel(const int64_t* __restrict__ indptr, int64_t n, double total,
+                                    double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = DDIV((double)(indptr[i + 1] - indptr[i]), total);
+  }
+}
+
+__global__ void inclusion_kernel(const double* __restrict__ p_in, int64_t n, int64_t cache_size,
+                                 const int64_t* __restrict__ cs_dev,
+                                 const int64_t* __restrict__ support_dev, double* __restrict__ out) {
+  const int64_t cs = cs_dev ? cs_dev[0] : cache_size;
+  const bool pin = support_dev ? (cs >= support_dev[0]) : false;
+  const double csd = (double)cs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double p = p_in[i];
+    p = fmin(fmax(p, 0.0), 1.0);  // np.clip
+    double r;
+    if (p >= 1.0) {
+      r = cs >= 1 ? 1.0 : 0.0;
+    } else {
+      double x = -fmin(p, GNS_ONE_MINUS_1EM15);
+      r = -det_expm1(DMUL(csd, det_log1p(x)));
+    }
+    if (pin && p_in[i] > 0.0) r = 1.0;
+    out[i] = r;
+  }
+}
+
+__global__ void epoch_targets_kernel(const int32_t* __restrict__ train_ids, int64_t n_train, int h,
+                                     uint32_t seed, uint32_t epoch, int64_t begin, int64_t count,
+                                     int32_t* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < count;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t y = (uint64_t)(begin + j);
+    if (n_train > 1) {
+      y = feistel_once(y, h, seed, epoch);
+      while (y >= (uint64_t)n_train) y = feistel_once(y, h, seed, epoch);
+    }
+    out[j] = train_ids[y];
+  }
+}
+
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) bitmap_rank_kernel(ScanStatus st, const uint32_t* __restrict__ bits,
+                                                            int64_t nwords, int32_t* __restrict__ rank) {
+  scan_tiles<BLOCK, ITEMS>(
+      st, nwords, [&](long long i) { return (unsigned long long)__popc(bits[i]); },
+      [&](long long i, unsigned long long ex, unsigned long long) { rank[i] = (int32_t)ex; },
+      [&](unsigned long long) {});
+}
+
+}  // namespace gns
+
+using namespace gns;
+
+extern "C" {
+
+const char* gns_last_error(void) { return g_err; }
+
+int gns_version(void) { return 1; }
+
+int gns_degree_probs(const gns_graph_t* g, double* out_probs, void* stream) {
+  if (!g || g->num_edges <= 0) {
+    set_error("graph has no edges; degree distribution undefined");
+    return GNS_EINVAL;
+  }
+  int grid = num_sms() * 8;
+  degree_probs_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(g->indptr, g->num_nodes,
+                                                              (double)g->num_edges, out_probs);
+  return check_launch("degree_probs");
+}
+
+int gns_inclusion(const double* probs, int64_t n, int64_t cache_size, const int64_t* cache_size_dev,
+                  const int64_t* support_dev, double* out, void* stream) {
+  if (n <= 0) return GNS_OK;
+  int grid = num_sms() * 8;
+  inclusion_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(probs, n, cache_size, cache_size_dev,
+                                                           support_dev, out);
+  return check_launch("inclusion");
+}
+
+int gns_epoch_targets(const int32_t* train_ids, int64_t n_train, uint32_t seed, uint32_t epoch,
+                      int64_t begin, int64_t count, int32_t* out, void* stream) {
+  if (count <= 0) return GNS_OK;
+  if (begin < 0 || begin + count > n_train) {
+    set_error("epoch_targets: range [%lld, %lld) outside [0, %lld)", (long long)begin,
+              (long long)(begin + count), (long long)n_train);
+    return GNS_EINVAL;
+  }
+  int bits = 2;
+  while ((1ll << bits) < n_train) ++bits;
+  bits += bits & 1;
+  int grid = (int)div_up(count, 256);
+  if (grid > num_sms() * 8) grid = num_sms() * 8;
+  epoch_targets_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(train_ids, n_train, bits / 2, seed,
+                                                               epoch, begin, count, out);
+  return check_launch("epoch_targets");
+}
+
+int gns_bitmap_rank(const uint32_t* bits, int64_t nwords, int32_t* out_rank, void* ws,
+                    size_t ws_bytes, void* stream) {
+  constexpr int B = 256, I = 16;
+  long long tiles = (nwords + B * I - 1) / (B * I);
+  size_t need = scan_status_bytes(tiles + 1);
+  if (ws_bytes < need) {
+    set_error("bitmap_rank: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  ScanStatus st = make_scan_status(ws, tiles + 1);
+  GNS_CUDA(cudaMemsetAsync(ws, 0, need, (cudaStream_t)stream));
+  int grid = (int)(tiles > 0 ? tiles : 1);
+  bitmap_rank_kernel<B, I><<<grid, B, 0, (cudaStream_t)stream>>>(st, bits, nwords, out_rank);
+  return check_launch("bitmap_rank");
+}
+
+}  // extern "C"

@@ -1,0 +1,616 @@
+// Model-side hot ops on B200: input-feature gather (model.py:146), the weighted
+// mean aggregation + self concat (model.py:131-138,153-154) and its backward
+// (model.py:223-225), softmax cross-entropy (model.py:189-200) and Adam
+// (model.py:229-242).  All HBM-bound; no tensor cores (the GraphSAGE linear
+// layers are cuBLAS GEMMs issued by the Python side).
+#include <algorithm>
+
+#include "gns_common.cuh"
+
+namespace gns {
+
+// ---- gather ------------------------------------------------------------------
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// out[i, :] = table[rows[i], :] with 16-byte vectors; flattened (row, chunk)
+// index space so any D % 4 == 0 is fully coalesced; 4 chunks in flight per thread.
+__global__ void gather_f32x4_kernel(const float* __restrict__ table, int64_t ld_in, const int32_t* __restrict__ rows,
+                                    const int32_t* __restrict__ n_dev, int64_t n_host, int dim4,
+                                    float* __restrict__ out, int64_t ld_out) {
+  const int64_t n = n_dev ? n_dev[0] : n_host;
+  const int64_t total = n * dim4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < total; i += 4 * stride) {
+    float4 v[4];
+    int64_t orow[4];
+    int oc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int64_t ii = i + u * stride;
+      int64_t r = ii / dim4;
+      int c = (int)(ii - r * dim4);
+      int32_t src = __ldg(rows + r);
+      v[u] = ld_stream_f4(reinterpret_cast<const float4*>(table + (int64_t)src * ld_in) + c);
+      orow[u] = r;
+      oc[u] = c;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) reinterpret_cast<float4*>(out + orow[u] * ld_out)[oc[u]] = v[u];
+  }
+  for (; i < total; i += stride) {
+    int64_t r = i / dim4;
+    int c = (int)(i - r * dim4);
+    int32_t src = __ldg(rows + r);
+    reinterpret_cast<float4*>(out + r * ld_out)[c] =
+        ld_stream_f4(reinterpret_cast<const float4*>(table + (int64_t)src * ld_in) + c);
+  }
+}
+
+template <typename TI, typename TO>
+__global__ void gather_scalar_kernel(const TI* __restrict__ table, int64_t ld_in, const int32_t* __restrict__ rows,
+                                     const int32_t* __restrict__ n_dev, int64_t n_host, int dim,
+                                     TO* __restrict__ out, int64_t ld_out) {
+  const int64_t n = n_dev ? n_dev[0] : n_host;
+  const int64_t total = n * dim;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / dim;
+    int c = (int)(i - r * dim);
+    out[r * ld_out + c] = (TO)table[(int64_t)rows[r] * ld_in + c];
+  }
+}
+
+__global__ void gather_mixed_kernel(const float* __restrict__ host_table, const float* __restrict__ cache_table,
+                                    const uint32_t* __restrict__ mask, const int32_t* __restrict__ wrank, int64_t ld,
+                                    const int32_t* __restrict__ rows, const int32_t* __restrict__ n_dev, int dim4,
+                                    float* __restrict__ out, int64_t ld_out) {
+  const int64_t n = n_dev[0];
+  const int64_t total = n * dim4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / dim4;
+    int c = (int)(i - r * dim4);
+    int32_t v = __ldg(rows + r);
+    uint32_t w = __ldg(mask + (v >> 5));
+    const float4* src;
+    if ((w >> (v & 31)) & 1u) {
+      int32_t slot = __ldg(wrank + (v >> 5)) + __popc(w & ((1u << (v & 31)) - 1u));
+      src = reinterpret_cast<const float4*>(cache_table + (int64_t)slot * ld) + c;
+    } else {
+      src = reinterpret_cast<const float4*>(host_table + (int64_t)v * ld) + c;
+    }
+    reinterpret_cast<float4*>(out + r * ld_out)[c] = *src;
+  }
+}
+
+__global__ void refresh_rows_kernel(const float* __restrict__ host_table, int64_t ld, const int32_t* __restrict__ ids,
+                                    const int64_t* __restrict__ n_dev, int dim4, float* __restrict__ cache_table) {
+  const int64_t n = n_dev[0];
+  const int64_t total = n * dim4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / dim4;
+    int c = (int)(i - r * dim4);
+    reinterpret_cast<float4*>(cache_table + r * ld)[c] =
+        reinterpret_cast<const float4*>(host_table + (int64_t)ids[r] * ld)[c];
+  }
+}
+
+// ---- SpMM forward --------------------------------------------------------------
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int W = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int W = 2; };
+
+template <typename V, typename T> __device__ __forceinline__ void vzero(V& v);
+__device__ __forceinline__ void vzero(float4& v) { v = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void vzero(double2& v) { v = make_double2(0.0, 0.0); }
+
+template <bool EXACT>
+__device__ __forceinline__ void vfma(float4& acc, float w, const float4& x) {
+  acc.x = fmaf(w, x.x, acc.x); acc.y = fmaf(w, x.y, acc.y);
+  acc.z = fmaf(w, x.z, acc.z); acc.w = fmaf(w, x.w, acc.w);
+}
+template <bool EXACT>
+__device__ __forceinline__ void vfma(double2& acc, double w, const double2& x) {
+  acc.x = DADD(acc.x, DMUL(w, x.x));
+  acc.y = DADD(acc.y, DMUL(w, x.y));
+}
+__device__ __forceinline__ float4 vdiv(const float4& a, float d) {
+  return make_float4(__fdiv_rn(a.x, d), __fdiv_rn(a.y, d), __fdiv_rn(a.z, d), __fdiv_rn(a.w, d));
+}
+__device__ __forceinline__ double2 vdiv(const double2& a, double d) { return make_double2(DDIV(a.x, d), DDIV(a.y, d)); }
+
+constexpr int kRowCap = 128;  // max edges per dst row (fanout <= 128)
+constexpr int kSpmmBlock = 256;
+
+struct BlockView {
+  const uint64_t* row_scan;
+  const int32_t* dst_degree;
+  const int32_t* self_pos;
+  const int32_t* edge_src;
+  const int32_t* edge_dst;
+  const double* edge_weight;
+  const int32_t* counts;
+};
+
+__host__ static inline BlockView view_of(const gns_block_t* b) {
+  return {b->row_scan, b->dst_degree, b->self_pos, b->edge_src, b->edge_dst, b->edge_weight, b->counts};
+}
+
+// one warp per dst row: sort the row's (<= k) edges by src index (the scipy
+// CSR order, model.py:133-135), then cat[r] = [h[self], sum w*h[src] / norm]
+template <typename T>
+__global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restrict__ h, int64_t ld_h, int dim,
+                                                              BlockView bv, T* __restrict__ cat, int64_t ld_cat) {
+  using V = typename Vec<T>::type;
+  constexpr int VW = Vec<T>::W;
+  __shared__ int32_t s_idx[kSpmmBlock / 32][kRowCap];
+  __shared__ T s_w[kSpmmBlock / 32][kRowCap];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t n = bv.counts[GNS_CNT_DST];
+  const uint64_t tot = bv.row_scan[n];
+  const int64_t tm = (int64_t)(tot >> 32);
+  const int dv = dim / VW;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < n; r += nw) {
+    const uint64_t s0 = bv.row_scan[r], s1 = bv.row_scan[r + 1];
+    const int64_t cb = (int64_t)(s0 >> 32), ce = (int64_t)(s1 >> 32);
+    const int64_t fb = tm + (int64_t)(s0 & 0xffffffffull), fe = tm + (int64_t)(s1 & 0xffffffffull);
+    const int nc = (int)(ce - cb), L = nc + (int)(fe - fb);
+    // load + rank-sort by src index (distinct within a row)
+    int32_t my_idx[kRowCap / 32];
+    T my_w[kRowCap / 32];
+#pragma unroll
+    for (int j = 0; j < kRowCap / 32; ++j) {
+      int i = lane + 32 * j;
+      my_idx[j] = INT32_MAX;
+      my_w[j] = 0;
+      if (i < L) {
+        int64_t e = i < nc ? cb + i : fb + (i - nc);
+        my_idx[j] = bv.edge_src[e];
+        my_w[j] = (T)bv.edge_weight[e];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kRowCap / 32; ++j) {
+      if (32 * j < L) {
+        if (lane + 32 * j < L) s_idx[wib][lane + 32 * j] = my_idx[j];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < kRowCap / 32; ++j) {
+      int i = lane + 32 * j;
+      if (i < L) {
+        int rank = 0;
+        for (int t = 0; t < L; ++t) rank += s_idx[wib][t] < my_idx[j];
+        my_idx[j] = rank;  // reuse as rank
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < kRowCap / 32; ++j) {
+      int i = lane + 32 * j;
+      if (i < L) {
+        int64_t e = i < nc ? cb + i : fb + (i - nc);
+        s_idx[wib][my_idx[j]] = bv.edge_src[e];
+        s_w[wib][my_idx[j]] = my_w[j];
+      }
+    }
+    __syncwarp();
+    const T norm = (T)max(bv.dst_degree[r], 1);
+    const V* hs = reinterpret_cast<const V*>(h + (int64_t)bv.self_pos[r] * ld_h);
+    V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
+    for (int c = lane; c < dv; c += 32) crow[c] = hs[c];
+    for (int c = lane; c < dv; c += 32) {
+      V acc;
+      vzero(acc);
+      int t = 0;
+      for (; t + 4 <= L; t += 4) {
+        V x0 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t] * ld_h)[c];
+        V x1 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t + 1] * ld_h)[c];
+        V x2 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t + 2] * ld_h)[c];
+        V x3 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t + 3] * ld_h)[c];
+        vfma<true>(acc, s_w[wib][t], x0);
+        vfma<true>(acc, s_w[wib][t + 1], x1);
+        vfma<true>(acc, s_w[wib][t + 2], x2);
+        vfma<true>(acc, s_w[wib][t + 3], x3);
+      }
+      for (; t < L; ++t) vfma<true>(acc, s_w[wib][t], reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t] * ld_h)[c]);
+      crow[dv + c] = vdiv(acc, norm);
+    }
+    __syncwarp();
+  }
+}
+
+// ---- SpMM backward -------------------------------------------------------------
+__global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of) {
+  const int64_t ne = bv.counts[GNS_CNT_EDGES], nd = bv.counts[GNS_CNT_DST];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne + nd; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < ne)
+      atomicAdd(tcount + bv.edge_src[i], 1);
+    else
+      self_of[bv.self_pos[i - ne]] = (int32_t)(i - ne);
+  }
+}
+
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) tscan_kernel(ScanStatus ss, BlockView bv, int32_t* __restrict__ tcount,
+                                                      int32_t* __restrict__ tptr) {
+  const int64_t n = bv.counts[GNS_CNT_SRC];
+  scan_tiles<BLOCK, ITEMS>(
+      ss, n, [&](long long i) { return (unsigned long long)tcount[i]; },
+      [&](long long i, unsigned long long ex, unsigned long long) {
+        tptr[i] = (int32_t)ex;
+        tcount[i] = 0;  // becomes the scatter cursor
+      },
+      [&](unsigned long long tot) { tptr[n] = (int32_t)tot; });
+}
+
+__global__ void tscatter_kernel(BlockView bv, int32_t* __restrict__ cursor, const int32_t* __restrict__ tptr,
+                                uint64_t* __restrict__ tkeys) {
+  const int64_t ne = bv.counts[GNS_CNT_EDGES];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = bv.edge_src[e];
+    int slot = atomicAdd(cursor + s, 1);
+    tkeys[tptr[s] + slot] = ((uint64_t)(uint32_t)bv.edge_dst[e] << 32) | (uint64_t)(uint32_t)e;
+  }
+}
+
+// sort each transposed row by dst (ascending): registers for <= 32 entries,
+// an all-ascending bitonic network in place otherwise
+__global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uint64_t* __restrict__ tkeys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = bv.counts[GNS_CNT_SRC];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = gw; s < n; s += nw) {
+    const int b = tptr[s], L = tptr[s + 1] - b;
+    if (L <= 1) continue;
+    uint64_t* a = tkeys + b;
+    if (L <= 32) {
+      uint64_t x = lane < L ? a[lane] : ~0ull;
+      int rank = 0;
+      for (int j = 0; j < L; ++j) rank += __shfl_sync(GNS_FULL, x, j) < x;
+      __syncwarp();
+      if (lane < L) a[rank] = x;
+      __syncwarp();
+      continue;
+    }
+    int P = 1;
+    while (P < L) P <<= 1;
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int t = lane; t < P / 2; t += 32) {
+        int half = k >> 1;
+        int i = (t / half) * k + (t % half);
+        int j = i ^ (k - 1);
+        if (j < L && a[j] < a[i]) { uint64_t x = a[i]; a[i] = a[j]; a[j] = x; }
+      }
+      __syncwarp();
+      for (int st = k >> 2; st >= 1; st >>= 1) {
+        for (int t = lane; t < P / 2; t += 32) {
+          int i = (t / st) * 2 * st + (t % st);
+          int j = i + st;
+          if (j < L && a[j] < a[i]) { uint64_t x = a[i]; a[i] = a[j]; a[j] = x; }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+template <typename T, bool EXACT>
+__device__ __forceinline__ T div_norm(T x, T d);
+template <> __device__ __forceinline__ float div_norm<float, false>(float x, float d) { return __fdiv_rn(x, d); }
+template <> __device__ __forceinline__ double div_norm<double, true>(double x, double d) { return DDIV(x, d); }
+
+template <typename T>
+__global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restrict__ dcat, int64_t ld_dcat, int dim,
+                                                              BlockView bv, const int32_t* __restrict__ tptr,
+                                                              const uint64_t* __restrict__ tkeys,
+                                                              const int32_t* __restrict__ self_of,
+                                                              T* __restrict__ dh, int64_t ld_dh) {
+  using V = typename Vec<T>::type;
+  constexpr int VW = Vec<T>::W;
+  constexpr bool EXACT = sizeof(T) == 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = bv.counts[GNS_CNT_SRC];
+  const int dv = dim / VW;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = gw; s < n; s += nw) {
+    const int b = tptr[s], e_end = tptr[s + 1];
+    const int sd = self_of[s];
+    for (int c = lane; c < dv; c += 32) {
+      T acc[VW];
+#pragma unroll
+      for (int q = 0; q < VW; ++q) acc[q] = (T)0;
+      for (int t = b; t < e_end; ++t) {
+        const uint64_t key = tkeys[t];
+        const int32_t d = (int32_t)(key >> 32), e = (int32_t)(key & 0xffffffffu);
+        const T w = (T)bv.edge_weight[e];
+        const T nrm = (T)max(bv.dst_degree[d], 1);
+        V g = reinterpret_cast<const V*>(dcat + (int64_t)d * ld_dcat + dim)[c];
+        const T* gp = reinterpret_cast<const T*>(&g);
+#pragma unroll
+        for (int q = 0; q < VW; ++q) {
+          T y = div_norm<T, EXACT>(gp[q], nrm);
+          if constexpr (EXACT) acc[q] = DADD(acc[q], DMUL(w, y));
+          else acc[q] = fmaf(w, y, acc[q]);
+        }
+      }
+      if (sd >= 0) {
+        V g = reinterpret_cast<const V*>(dcat + (int64_t)sd * ld_dcat)[c];
+        const T* gp = reinterpret_cast<const T*>(&g);
+#pragma unroll
+        for (int q = 0; q < VW; ++q) {
+          if constexpr (EXACT) acc[q] = DADD(acc[q], gp[q]);
+          else acc[q] = acc[q] + gp[q];
+        }
+      }
+      V out;
+      T* op = reinterpret_cast<T*>(&out);
+#pragma unroll
+      for (int q = 0; q < VW; ++q) op[q] = acc[q];
+      reinterpret_cast<V*>(dh + s * ld_dh)[c] = out;
+    }
+  }
+}
+
+struct BwdWs {
+  int32_t* tcount;
+  int32_t* tptr;
+  int32_t* self_of;
+  uint64_t* tkeys;
+  void* scan;
+  long long tiles;
+};
+
+static size_t bwd_ws(int64_t max_src, int64_t max_edges, void* base, size_t cap, BwdWs* w) {
+  Workspace ws(base, cap);
+  w->tcount = ws.take<int32_t>(max_src + 1);
+  w->tptr = ws.take<int32_t>(max_src + 1);
+  w->self_of = ws.take<int32_t>(max_src + 1);
+  w->tkeys = ws.take<uint64_t>(max_edges + 1);
+  w->tiles = (max_src + 256 * 8 - 1) / (256 * 8) + 1;
+  w->scan = (void*)ws.take<char>(scan_status_bytes(w->tiles));
+  return ws.off;
+}
+
+// ---- softmax cross-entropy ------------------------------------------------------
+template <typename T>
+__global__ void xent_kernel(const T* __restrict__ logits, int64_t ld, const int32_t* __restrict__ n_dev, int C,
+                            const int32_t* __restrict__ labels, const int32_t* __restrict__ targets,
+                            T* __restrict__ grad, double* __restrict__ row_loss) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = n_dev[0];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < n; r += nw) {
+    const T* z = logits + r * ld;
+    T mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = max(mx, z[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(GNS_FULL, mx, o));
+    T s = 0;
+    for (int c = lane; c < C; c += 32) s += exp(z[c] - mx);
+    s = warp_sum(s);
+    const T lse = log(s);
+    const int lab = labels[targets[r]];
+    const T inv_n = (T)1 / (T)n;
+    for (int c = lane; c < C; c += 32) {
+      T lp = (z[c] - mx) - lse;
+      T g = exp(lp);
+      if (c == lab) g -= (T)1;
+      grad[r * ld + c] = g * inv_n;
+      if (c == lab) row_loss[r] = -(double)lp;
+    }
+  }
+}
+
+__global__ void mean_kernel(const double* __restrict__ x, const int32_t* __restrict__ n_dev, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int64_t n = n_dev[0];
+  double s = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) out[0] = n > 0 ? v / (double)n : 0.0;
+  }
+}
+
+// ---- Adam ---------------------------------------------------------------------------
+template <typename T>
+__global__ void adam_kernel(T* __restrict__ p, const T* __restrict__ g, T* __restrict__ m, T* __restrict__ v,
+                            int64_t n, T lr, T b1, T b2, T eps, T bc1, T bc2, T gs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T gr = g[i] * gs;
+    T mi = b1 * m[i] + ((T)1 - b1) * gr;
+    T vi = b2 * v[i] + ((T)1 - b2) * gr * gr;
+    m[i] = mi;
+    v[i] = vi;
+    T mh = mi / bc1, vh = vi / bc2;
+    p[i] -= lr * mh / (sqrt(vh) + eps);
+  }
+}
+
+}  // namespace gns
+
+using namespace gns;
+
+extern "C" {
+
+int gns_gather_rows(const void* table, int64_t ld_in, int32_t dtype_in, const int32_t* rows,
+                    const int32_t* n_rows_dev, int64_t max_rows, int32_t dim, void* out, int64_t ld_out,
+                    int32_t dtype_out, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (max_rows <= 0 || dim <= 0) return GNS_OK;
+  const int sms = num_sms();
+  if (dtype_in == 0 && dtype_out == 0) {
+    bool vec = (dim % 4 == 0) && (ld_in % 4 == 0) && (ld_out % 4 == 0) && ((uintptr_t)table % 16 == 0) &&
+               ((uintptr_t)out % 16 == 0);
+    if (vec) {
+      long long want = (max_rows * (dim / 4) + 255) / 256;
+      int grid = grid_for(want, (long long)sms * 16);
+      gather_f32x4_kernel<<<grid, 256, 0, stream>>>((const float*)table, ld_in, rows, n_rows_dev, max_rows, dim / 4,
+                                                    (float*)out, ld_out);
+      return check_launch("gather_f32x4");
+    }
+    gather_scalar_kernel<float, float><<<sms * 16, 256, 0, stream>>>((const float*)table, ld_in, rows, n_rows_dev,
+                                                                     max_rows, dim, (float*)out, ld_out);
+    return check_launch("gather_f32");
+  }
+  if (dtype_in == 0 && dtype_out == 1) {
+    gather_scalar_kernel<float, double><<<sms * 16, 256, 0, stream>>>((const float*)table, ld_in, rows, n_rows_dev,
+                                                                      max_rows, dim, (double*)out, ld_out);
+    return check_launch("gather_f32_f64");
+  }
+  if (dtype_in == 1 && dtype_out == 1) {
+    gather_scalar_kernel<double, double><<<sms * 16, 256, 0, stream>>>((const double*)table, ld_in, rows, n_rows_dev,
+                                                                       max_rows, dim, (double*)out, ld_out);
+    return check_launch("gather_f64");
+  }
+  set_error("gather_rows: unsupported dtype pair %d->%d", dtype_in, dtype_out);
+  return GNS_EINVAL;
+}
+
+int gns_gather_rows_mixed(const float* host_table, const float* cache_table, const uint32_t* mask_bits,
+                          const int32_t* mask_word_rank, int64_t ld, const int32_t* rows, const int32_t* n_rows_dev,
+                          int64_t max_rows, int32_t dim, float* out, int64_t ld_out, void* stream_) {
+  if (dim % 4 || ld % 4 || ld_out % 4) {
+    set_error("gather_rows_mixed: dim and strides must be multiples of 4");
+    return GNS_EINVAL;
+  }
+  if (max_rows <= 0) return GNS_OK;
+  long long want = (max_rows * (dim / 4) + 255) / 256;
+  int grid = grid_for(want, (long long)num_sms() * 16);
+  gather_mixed_kernel<<<grid, 256, 0, (cudaStream_t)stream_>>>(host_table, cache_table, mask_bits, mask_word_rank, ld,
+                                                               rows, n_rows_dev, dim / 4, out, ld_out);
+  return check_launch("gather_mixed");
+}
+
+int gns_cache_refresh_rows(const float* host_table, int64_t ld, const int32_t* ids, const int64_t* n_dev,
+                           int64_t max_rows, int32_t dim, float* cache_table, void* stream_) {
+  if (dim % 4 || ld % 4) {
+    set_error("cache_refresh_rows: dim and ld must be multiples of 4");
+    return GNS_EINVAL;
+  }
+  if (max_rows <= 0) return GNS_OK;
+  long long want = (max_rows * (dim / 4) + 255) / 256;
+  int grid = grid_for(want, (long long)num_sms() * 16);
+  refresh_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream_>>>(host_table, ld, ids, n_dev, dim / 4, cache_table);
+  return check_launch("cache_refresh_rows");
+}
+
+int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, const gns_block_t* block, int64_t max_dst,
+                 void* cat, int64_t ld_cat, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (max_dst <= 0) return GNS_OK;
+  const int sms = num_sms();
+  long long want = (max_dst * 32 + kSpmmBlock - 1) / kSpmmBlock;
+  int grid = grid_for(want, (long long)sms * 8);
+  BlockView bv = view_of(block);
+  if (dtype == 0) {
+    if (dim % 4 || ld_h % 4 || ld_cat % 4) {
+      set_error("spmm_fwd(f32): dim/strides must be multiples of 4");
+      return GNS_EINVAL;
+    }
+    spmm_fwd_kernel<float><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv, (float*)cat, ld_cat);
+  } else {
+    if (dim % 2 || ld_h % 2 || ld_cat % 2) {
+      set_error("spmm_fwd(f64): dim/strides must be even");
+      return GNS_EINVAL;
+    }
+    spmm_fwd_kernel<double><<<grid, kSpmmBlock, 0, stream>>>((const double*)h, ld_h, dim, bv, (double*)cat, ld_cat);
+  }
+  return check_launch("spmm_fwd");
+}
+
+size_t gns_spmm_bwd_workspace_size(int64_t max_src, int64_t max_edges) {
+  BwdWs w;
+  return bwd_ws(max_src, max_edges, nullptr, 0, &w);
+}
+
+int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, const gns_block_t* block,
+                 int64_t max_dst, int64_t max_src, int64_t max_edges, void* dh, int64_t ld_dh, void* ws,
+                 size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  BwdWs w;
+  size_t need = bwd_ws(max_src, max_edges, ws, ws_bytes, &w);
+  if (need > ws_bytes) {
+    set_error("spmm_bwd: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  const int VW = dtype == 0 ? 4 : 2;
+  if (dim % VW || ld_dcat % VW || ld_dh % VW) {
+    set_error("spmm_bwd: dim/strides must be multiples of %d", VW);
+    return GNS_EINVAL;
+  }
+  const int sms = num_sms();
+  BlockView bv = view_of(block);
+  GNS_CUDA(cudaMemsetAsync(w.tcount, 0, (max_src + 1) * sizeof(int32_t), stream));
+  GNS_CUDA(cudaMemsetAsync(w.self_of, 0xff, (max_src + 1) * sizeof(int32_t), stream));
+  GNS_CUDA(cudaMemsetAsync(w.scan, 0, scan_status_bytes(w.tiles), stream));
+  int g1 = grid_for((max_edges + max_dst + 255) / 256, (long long)sms * 8);
+  tcount_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.self_of);
+  tscan_kernel<256, 8><<<(unsigned)w.tiles, 256, 0, stream>>>(make_scan_status(w.scan, w.tiles), bv, w.tcount, w.tptr);
+  tscatter_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.tptr, w.tkeys);
+  int g2 = grid_for((max_src * 32 + 255) / 256, (long long)sms * 8);
+  tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys);
+  GNS_TRY(check_launch("spmm_bwd transpose"));
+  if (dtype == 0)
+    spmm_bwd_kernel<float><<<g2, kSpmmBlock, 0, stream>>>((const float*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,
+                                                          w.self_of, (float*)dh, ld_dh);
+  else
+    spmm_bwd_kernel<double><<<g2, kSpmmBlock, 0, stream>>>((const double*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,
+                                                           w.self_of, (double*)dh, ld_dh);
+  return check_launch("spmm_bwd");
+}
+
+int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, const int32_t* n_dev, int64_t max_rows,
+                     int32_t num_classes, const int32_t* labels, const int32_t* targets, void* grad_out,
+                     double* loss_out, void* ws, size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if ((size_t)max_rows * sizeof(double) > ws_bytes) {
+    set_error("softmax_xent: workspace %zu < %zu", ws_bytes, (size_t)max_rows * 8);
+    return GNS_EINVAL;
+  }
+  double* row_loss = (double*)ws;
+  const int sms = num_sms();
+  int grid = grid_for((max_rows * 32 + 255) / 256, (long long)sms * 8);
+  if (dtype == 0)
+    xent_kernel<float><<<grid, 256, 0, stream>>>((const float*)logits, ld, n_dev, num_classes, labels, targets,
+                                                 (float*)grad_out, row_loss);
+  else
+    xent_kernel<double><<<grid, 256, 0, stream>>>((const double*)logits, ld, n_dev, num_classes, labels, targets,
+                                                  (double*)grad_out, row_loss);
+  mean_kernel<<<1, 1024, 0, stream>>>(row_loss, n_dev, loss_out);
+  return check_launch("softmax_xent");
+}
+
+int gns_adam(int32_t dtype, void* params, const void* grads, void* m, void* v, int64_t n, double lr, double beta1,
+             double beta2, double eps, int64_t step, double grad_scale, void* stream_) {
+  if (n <= 0) return GNS_OK;
+  double bc1 = 1.0 - pow(beta1, (double)step), bc2 = 1.0 - pow(beta2, (double)step);
+  int grid = grid_for((n + 255) / 256, (long long)num_sms() * 8);
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (dtype == 0)
+    adam_kernel<float><<<grid, 256, 0, stream>>>((float*)params, (const float*)grads, (float*)m, (float*)v, n,
+                                                 (float)lr, (float)beta1, (float)beta2, (float)eps, (float)bc1,
+                                                 (float)bc2, (float)grad_scale);
+  else
+    adam_kernel<double><<<grid, 256, 0, stream>>>((double*)params, (const double*)grads, (double*)m, (double*)v, n,
+                                                  lr, beta1, beta2, eps, bc1, bc2, grad_scale);
+  return check_launch("adam");
+}
+
+}  // extern "C"

@@ -1,0 +1,524 @@
+// Per-layer NS/GNS neighbour sampler and the frontier dedup/relabel on B200.
+//
+// Reference: sampling.py:155-170 (NS), :189-266 (GNS, gns-paper weights),
+// :129-136 (_select_per_row), :139-152 (_assemble), graph.py:399-415
+// (gather_rows).
+//
+// Selection per dst row and phase: the `take` smallest (key53, position)
+// pairs among the row's valid candidates, keys from Philox at
+// (node, layer, phase, position).  Keys are uniform, so a threshold T with
+// E[#{key < T}] = take + 4 sqrt(take) + 8 keeps ~take+ candidates in one pass;
+// T is bisected if the count falls outside [take, CAP] (rare).  The kept
+// candidates are ranked exactly by (key, pos) — ties break by position like
+// the reference's stable lexsort — so the result equals the full sort.  In the
+// fill phase the cache-bitmap probe and the neighbour-id load happen only for
+// positions whose key is under T, so a hub row costs Philox ALU, not HBM.
+//
+// Rows whose scan length exceeds kHubLen go to a CTA-per-row kernel.
+//
+// Dedup/relabel: one bit per node id (N/8 bytes, L2-resident), atomicOr the
+// seeds and sampled neighbours, a single-pass scan over the bitmap words emits
+// the sorted unique src set and per-word ranks, and edge_src = word rank +
+// popc(prefix bits).  The bits are cleared by walking src_nodes.
+#include <algorithm>
+
+#include "gns_common.cuh"
+
+namespace gns {
+
+constexpr int kSampBlock = 256;
+constexpr int kWarpCap = 256;
+constexpr int kHubLen = 2048;
+constexpr int kHubBlock = 512;
+constexpr int kHubCap = 512;
+constexpr int kMaxFanout = 128;
+constexpr uint64_t kTwo53 = 1ull << 53;
+
+struct LayerArgs {
+  const int64_t* indptr;
+  const int32_t* indices;
+  const int64_t* cindptr;
+  const int32_t* cindices;
+  const uint32_t* mask;
+  const double* incl;
+  const int32_t* seeds;
+  const int32_t* n_dev;
+  int k;
+  int cache_only;
+  int gns;
+  uint32_t seed, epoch, batch, layer;
+  gns_block_t b;
+};
+
+struct RowInfo {
+  int64_t start, cstart;
+  int32_t node, deg, nc, m, fill;
+};
+
+__device__ __forceinline__ RowInfo row_info(const LayerArgs& a, int64_t r) {
+  RowInfo ri;
+  ri.node = a.seeds[r];
+  ri.start = a.indptr[ri.node];
+  ri.deg = (int32_t)(a.indptr[ri.node + 1] - ri.start);
+  if (a.gns) {
+    ri.cstart = a.cindptr[ri.node];
+    ri.nc = (int32_t)(a.cindptr[ri.node + 1] - ri.cstart);
+    ri.m = min(a.k, ri.nc);
+    ri.fill = a.cache_only ? 0 : min(a.k - ri.m, ri.deg - ri.nc);
+  } else {
+    ri.cstart = 0;
+    ri.nc = 0;
+    ri.m = 0;
+    ri.fill = min(a.k, ri.deg);
+  }
+  return ri;
+}
+
+__device__ __forceinline__ bool is_hub(const RowInfo& ri) {
+  int sc = ri.m > 0 ? ri.nc : 0;
+  int sf = ri.fill > 0 ? ri.deg : 0;
+  return max(sc, sf) > kHubLen;
+}
+
+__device__ __forceinline__ bool cached_bit(const uint32_t* __restrict__ mask, int32_t v) {
+  return (__ldg(mask + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+// ---- pass 1: per-row counts + exclusive scan --------------------------------
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) layer_count_kernel(ScanStatus ss, LayerArgs a) {
+  const long long n = a.n_dev[0];
+  scan_tiles<BLOCK, ITEMS>(
+      ss, n,
+      [&](long long r) {
+        RowInfo ri = row_info(a, r);
+        return ((unsigned long long)ri.m << 32) | (unsigned long long)ri.fill;
+      },
+      [&](long long r, unsigned long long ex, unsigned long long) {
+        RowInfo ri = row_info(a, r);
+        a.b.row_scan[r] = ex;
+        a.b.dst_degree[r] = ri.deg;
+        if (is_hub(ri)) {
+          int h = atomicAdd(a.b.counts + GNS_CNT_HUBS, 1);
+          a.b.hub_rows[h] = (int32_t)r;
+        }
+      },
+      [&](unsigned long long tot) {
+        a.b.row_scan[n] = tot;
+        a.b.counts[GNS_CNT_DST] = (int32_t)n;
+        a.b.counts[GNS_CNT_EDGES] = (int32_t)((tot >> 32) + (tot & 0xffffffffull));
+        a.b.counts[GNS_CNT_CACHED] = (int32_t)(tot >> 32);
+      });
+}
+
+// ---- selection helpers ------------------------------------------------------
+struct PhaseDesc {
+  int phase;          // 0 cached, 1 fill, 2 uniform
+  int take, cnt, len; // selections, valid candidates, positions to scan
+  const int32_t* ids; // neighbour ids of this row/phase (position-indexed)
+  bool filter;        // fill phase: skip cached neighbours
+  int64_t out_base;   // first output slot
+};
+
+__device__ __forceinline__ uint64_t initial_threshold(int take, int cnt) {
+  if (take >= cnt) return kTwo53;
+  double mu = (double)take + 4.0 * sqrt((double)take) + 8.0;
+  if (mu >= (double)cnt) return kTwo53;
+  uint64_t t = (uint64_t)(mu / (double)cnt * 9007199254740992.0);
+  return t < 1 ? 1 : t;
+}
+
+__device__ __forceinline__ void emit_edge(const LayerArgs& a, const RowInfo& ri, int64_t r,
+                                          const PhaseDesc& ph, int rank, uint32_t pos) {
+  const int64_t o = ph.out_base + rank;
+  const int32_t u = __ldg(ph.ids + pos);
+  double w;
+  if (ph.phase == 0) {
+    double q = DDIV((double)a.k, (double)min(a.k, max(ri.nc, 1)));
+    double coeff = DMUL(a.incl[u], q);
+    if (!(coeff > 0.0)) atomicOr((unsigned*)(a.b.counts + GNS_CNT_ERR), GNS_ERRBIT_ZEROPROB);
+    w = DDIV(1.0, coeff);
+  } else if (ph.phase == 1) {
+    w = DDIV((double)(ri.deg - ri.nc), (double)max(ri.fill, 1));
+  } else {
+    w = DDIV((double)ri.deg, (double)max(ri.fill, 1));
+  }
+  a.b.edge_node[o] = u;
+  a.b.edge_dst[o] = (int32_t)r;
+  a.b.edge_weight[o] = w;
+  a.b.edge_cached[o] = ph.phase == 0 ? 1 : 0;
+}
+
+// warp-cooperative selection of one phase of one row
+__device__ void warp_select(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
+                            uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpos) {
+  const int lane = lane_id();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint32_t stream = stream_word(32, a.layer, ph.phase);
+  uint64_t T = initial_threshold(ph.take, ph.cnt);
+  uint64_t lo = 0, hi = kTwo53 + 1;
+  const int64_t npairs = ((int64_t)ph.len + 1) >> 1;
+  int found = 0;
+  for (int iter = 0; iter < 64; ++iter) {
+    found = 0;
+    for (int64_t qb = 0; qb < npairs; qb += 32) {
+      const int64_t q = qb + lane;
+      uint64_t k0 = kTwo53, k1 = kTwo53;
+      if (q < npairs) key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t p = 2 * q + j;
+        const uint64_t key = j ? k1 : k0;
+        bool pred = (q < npairs) && (p < ph.len) && (key < T);
+        if (pred && ph.filter) pred = !cached_bit(a.mask, __ldg(ph.ids + p));
+        unsigned bal = __ballot_sync(GNS_FULL, pred);
+        if (pred) {
+          int o = found + __popc(bal & lt_mask);
+          if (o < kWarpCap) {
+            bkey[o] = key;
+            bpos[o] = (uint32_t)p;
+          }
+        }
+        found += __popc(bal);
+      }
+    }
+    if (found > kWarpCap) {
+      hi = T;
+      uint64_t nt = lo + (T - lo) / 2;
+      if (nt <= lo) break;
+      T = nt;
+    } else if (found < ph.take) {
+      lo = T;
+      uint64_t nt = (hi > kTwo53) ? (T * 2 > kTwo53 ? kTwo53 : T * 2) : T + (hi - T) / 2;
+      if (nt <= T) break;
+      T = nt;
+    } else {
+      break;
+    }
+  }
+  __syncwarp();
+  if (found < ph.take || found > kWarpCap) {
+    if (lane == 0) atomicOr((unsigned*)(a.b.counts + GNS_CNT_ERR), GNS_ERRBIT_CAPACITY);
+    return;
+  }
+  for (int i = lane; i < found; i += 32) {
+    const uint64_t ki = bkey[i];
+    const uint32_t pi = bpos[i];
+    int rank = 0;
+    for (int j = 0; j < found; ++j) {
+      const uint64_t kj = bkey[j];
+      rank += (kj < ki) || (kj == ki && bpos[j] < pi);
+    }
+    if (rank < ph.take) emit_edge(a, ri, r, ph, rank, pi);
+  }
+  __syncwarp();
+}
+
+// CTA-cooperative selection for hub rows
+__device__ void block_select(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
+                             uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpos, int* s_found) {
+  const uint32_t stream = stream_word(32, a.layer, ph.phase);
+  uint64_t T = initial_threshold(ph.take, ph.cnt);
+  uint64_t lo = 0, hi = kTwo53 + 1;
+  const int64_t npairs = ((int64_t)ph.len + 1) >> 1;
+  int found = 0;
+  for (int iter = 0; iter < 64; ++iter) {
+    if (threadIdx.x == 0) *s_found = 0;
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < npairs; q += kHubBlock) {
+      uint64_t k0, k1;
+      key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t p = 2 * q + j;
+        const uint64_t key = j ? k1 : k0;
+        bool pred = (p < ph.len) && (key < T);
+        if (pred && ph.filter) pred = !cached_bit(a.mask, __ldg(ph.ids + p));
+        if (pred) {
+          int o = atomicAdd(s_found, 1);
+          if (o < kHubCap) {
+            bkey[o] = key;
+            bpos[o] = (uint32_t)p;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    found = *s_found;
+    __syncthreads();
+    if (found > kHubCap) {
+      hi = T;
+      uint64_t nt = lo + (T - lo) / 2;
+      if (nt <= lo) break;
+      T = nt;
+    } else if (found < ph.take) {
+      lo = T;
+      uint64_t nt = (hi > kTwo53) ? (T * 2 > kTwo53 ? kTwo53 : T * 2) : T + (hi - T) / 2;
+      if (nt <= T) break;
+      T = nt;
+    } else {
+      break;
+    }
+  }
+  if (found < ph.take || found > kHubCap) {
+    if (threadIdx.x == 0) atomicOr((unsigned*)(a.b.counts + GNS_CNT_ERR), GNS_ERRBIT_CAPACITY);
+    __syncthreads();
+    return;
+  }
+  for (int i = threadIdx.x; i < found; i += kHubBlock) {
+    const uint64_t ki = bkey[i];
+    const uint32_t pi = bpos[i];
+    int rank = 0;
+    for (int j = 0; j < found; ++j) {
+      const uint64_t kj = bkey[j];
+      rank += (kj < ki) || (kj == ki && bpos[j] < pi);
+    }
+    if (rank < ph.take) emit_edge(a, ri, r, ph, rank, pi);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void make_phases(const LayerArgs& a, const RowInfo& ri, int64_t r,
+                                            PhaseDesc& pc, PhaseDesc& pf) {
+  const uint64_t scan_r = a.b.row_scan[r];
+  const uint64_t n = (uint64_t)a.n_dev[0];
+  const uint64_t tm = a.b.row_scan[n] >> 32;
+  pc.phase = 0;
+  pc.take = ri.m;
+  pc.cnt = ri.nc;
+  pc.len = ri.nc;
+  pc.ids = a.cindices + ri.cstart;
+  pc.filter = false;
+  pc.out_base = (int64_t)(scan_r >> 32);
+  pf.phase = a.gns ? 1 : 2;
+  pf.take = ri.fill;
+  pf.cnt = a.gns ? ri.deg - ri.nc : ri.deg;
+  pf.len = ri.deg;
+  pf.ids = a.indices + ri.start;
+  pf.filter = a.gns != 0;
+  pf.out_base = (int64_t)(tm + (scan_r & 0xffffffffull));
+}
+
+__global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a) {
+  __shared__ uint64_t s_key[kSampBlock / 32][kWarpCap];
+  __shared__ uint32_t s_pos[kSampBlock / 32][kWarpCap];
+  const int w = threadIdx.x >> 5;
+  const int64_t n = a.n_dev[0];
+  const int64_t gw = (blockIdx.x * (int64_t)kSampBlock + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * kSampBlock) >> 5;
+  for (int64_t r = gw; r < n; r += nw) {
+    RowInfo ri = row_info(a, r);
+    if (is_hub(ri)) continue;
+    PhaseDesc pc, pf;
+    make_phases(a, ri, r, pc, pf);
+    if (pc.take > 0) warp_select(a, ri, r, pc, s_key[w], s_pos[w]);
+    if (pf.take > 0) warp_select(a, ri, r, pf, s_key[w], s_pos[w]);
+  }
+}
+
+__global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(LayerArgs a) {
+  __shared__ uint64_t s_key[kHubCap];
+  __shared__ uint32_t s_pos[kHubCap];
+  __shared__ int s_found;
+  const int nh = a.b.counts[GNS_CNT_HUBS];
+  for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+    const int64_t r = a.b.hub_rows[h];
+    RowInfo ri = row_info(a, r);
+    PhaseDesc pc, pf;
+    make_phases(a, ri, r, pc, pf);
+    if (pc.take > 0) block_select(a, ri, r, pc, s_key, s_pos, &s_found);
+    if (pf.take > 0) block_select(a, ri, r, pf, s_key, s_pos, &s_found);
+  }
+}
+
+// ---- dedup / relabel ----------------------------------------------------------
+__global__ void setbits_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ na_dev, int64_t na_host,
+                               const int32_t* __restrict__ b, const int32_t* __restrict__ nb_dev,
+                               uint32_t* __restrict__ bits) {
+  const int64_t na = na_dev ? na_dev[0] : na_host;
+  const int64_t nb = (b && nb_dev) ? nb_dev[0] : 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < na + nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = i < na ? a[i] : b[i - na];
+    atomicOr(bits + (v >> 5), 1u << (v & 31));
+  }
+}
+
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) enumerate_kernel(ScanStatus ss, const uint32_t* __restrict__ bits, int64_t nw,
+                                                          int32_t* __restrict__ rank, int32_t* __restrict__ out,
+                                                          int32_t* __restrict__ out_n) {
+  scan_tiles<BLOCK, ITEMS>(
+      ss, nw, [&](long long w) { return (unsigned long long)__popc(bits[w]); },
+      [&](long long w, unsigned long long ex, unsigned long long val) {
+        if (!val) return;
+        rank[w] = (int32_t)ex;
+        uint32_t s = bits[w];
+        int32_t pos = (int32_t)ex;
+        while (s) {
+          int bb = __ffs(s) - 1;
+          s &= s - 1;
+          out[pos++] = (int32_t)(w * 32 + bb);
+        }
+      },
+      [&](unsigned long long tot) { out_n[0] = (int32_t)tot; });
+}
+
+__device__ __forceinline__ int32_t bit_rank(const uint32_t* __restrict__ bits, const int32_t* __restrict__ rank,
+                                            int32_t v) {
+  const uint32_t w = bits[v >> 5];
+  return rank[v >> 5] + __popc(w & ((1u << (v & 31)) - 1u));
+}
+
+__global__ void relabel_kernel(const uint32_t* __restrict__ bits, const int32_t* __restrict__ rank,
+                               const int32_t* __restrict__ seeds, const int32_t* __restrict__ n_seeds_dev,
+                               const int32_t* __restrict__ edge_node, const int32_t* __restrict__ counts,
+                               int32_t* __restrict__ self_pos, int32_t* __restrict__ edge_src) {
+  const int64_t ns = n_seeds_dev[0];
+  const int64_t ne = counts[GNS_CNT_EDGES];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns + ne;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < ns)
+      self_pos[i] = bit_rank(bits, rank, seeds[i]);
+    else
+      edge_src[i - ns] = bit_rank(bits, rank, edge_node[i - ns]);
+  }
+}
+
+__global__ void clearbits_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ n_dev,
+                                 uint32_t* __restrict__ bits) {
+  const int64_t n = n_dev[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bits[ids[i] >> 5] = 0u;
+}
+
+struct RelabelWs {
+  uint32_t* bits;
+  int32_t* rank;
+  void* scan;
+  long long tiles;
+};
+
+static size_t relabel_ws(int64_t num_nodes, void* base, size_t cap, RelabelWs* r) {
+  Workspace w(base, cap);
+  int64_t nw = (num_nodes + 31) / 32;
+  r->bits = w.take<uint32_t>(nw + 1);
+  r->rank = w.take<int32_t>(nw + 1);
+  r->tiles = (nw + 256 * 16 - 1) / (256 * 16) + 1;
+  r->scan = (void*)w.take<char>(scan_status_bytes(r->tiles));
+  return w.off;
+}
+
+static int run_enumerate(const RelabelWs& r, int64_t num_nodes, int32_t* out, int32_t* out_n, cudaStream_t stream) {
+  int64_t nw = (num_nodes + 31) / 32;
+  GNS_CUDA(cudaMemsetAsync(r.scan, 0, scan_status_bytes(r.tiles), stream));
+  enumerate_kernel<256, 16><<<(unsigned)r.tiles, 256, 0, stream>>>(make_scan_status(r.scan, r.tiles), r.bits, nw,
+                                                                   r.rank, out, out_n);
+  return check_launch("enumerate");
+}
+
+}  // namespace gns
+
+using namespace gns;
+
+extern "C" {
+
+size_t gns_sample_workspace_size(int64_t max_dst) {
+  long long tiles = (max_dst + 256 * 4 - 1) / (256 * 4) + 1;
+  return scan_status_bytes(tiles);
+}
+
+int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32_t* seeds,
+                     const int32_t* n_seeds_dev, int64_t max_dst, int32_t k, int32_t cache_only,
+                     const gns_rng_t* rng, gns_block_t* block, void* ws, size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (k < 1) {
+    set_error("fanout must be >= 1");
+    return GNS_EINVAL;
+  }
+  if (k > kMaxFanout) {
+    set_error("fanout %d exceeds the supported maximum %d", k, kMaxFanout);
+    return GNS_EINVAL;
+  }
+  size_t need = gns_sample_workspace_size(max_dst);
+  if (ws_bytes < need) {
+    set_error("sample_layer: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  LayerArgs a;
+  a.indptr = g->indptr;
+  a.indices = g->indices;
+  a.gns = cache != nullptr;
+  a.cindptr = cache ? cache->cached_indptr : nullptr;
+  a.cindices = cache ? cache->cached_indices : nullptr;
+  a.mask = cache ? cache->mask_bits : nullptr;
+  a.incl = cache ? cache->inclusion : nullptr;
+  a.seeds = seeds;
+  a.n_dev = n_seeds_dev;
+  a.k = k;
+  a.cache_only = cache_only;
+  a.seed = rng->seed;
+  a.epoch = rng->epoch;
+  a.batch = rng->batch;
+  a.layer = rng->layer;
+  a.b = *block;
+  long long tiles = (max_dst + 256 * 4 - 1) / (256 * 4) + 1;
+  GNS_CUDA(cudaMemsetAsync(ws, 0, scan_status_bytes(tiles), stream));
+  GNS_CUDA(cudaMemsetAsync(block->counts, 0, GNS_CNT_N * sizeof(int32_t), stream));
+  layer_count_kernel<256, 4><<<(unsigned)tiles, 256, 0, stream>>>(make_scan_status(ws, tiles), a);
+  GNS_TRY(check_launch("layer_count"));
+  const int sms = num_sms();
+  long long want = (max_dst * 32 + kSampBlock - 1) / kSampBlock;
+  int grid = (int)(want < sms * 8 ? (want > 0 ? want : 1) : sms * 8);
+  sample_warp_kernel<<<grid, kSampBlock, 0, stream>>>(a);
+  GNS_TRY(check_launch("sample_warp"));
+  sample_hub_kernel<<<sms, kHubBlock, 0, stream>>>(a);
+  return check_launch("sample_hub");
+}
+
+size_t gns_relabel_workspace_size(int64_t num_nodes) {
+  RelabelWs r;
+  return relabel_ws(num_nodes, nullptr, 0, &r);
+}
+
+int gns_relabel(int64_t num_nodes, const int32_t* seeds, const int32_t* n_seeds_dev, int64_t max_dst,
+                gns_block_t* block, int64_t max_edges, void* ws, size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  RelabelWs r;
+  size_t need = relabel_ws(num_nodes, ws, ws_bytes, &r);
+  if (need > ws_bytes) {
+    set_error("relabel: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  const int sms = num_sms();
+  int grid = grid_for((max_dst + max_edges + 255) / 256 + 1, (long long)sms * 16);
+  setbits_kernel<<<grid, 256, 0, stream>>>(seeds, n_seeds_dev, 0, block->edge_node, block->counts + GNS_CNT_EDGES,
+                                           r.bits);
+  GNS_TRY(check_launch("setbits"));
+  GNS_TRY(run_enumerate(r, num_nodes, block->src_nodes, block->counts + GNS_CNT_SRC, stream));
+  relabel_kernel<<<grid, 256, 0, stream>>>(r.bits, r.rank, seeds, n_seeds_dev, block->edge_node, block->counts,
+                                           block->self_pos, block->edge_src);
+  GNS_TRY(check_launch("relabel"));
+  clearbits_kernel<<<grid, 256, 0, stream>>>(block->src_nodes, block->counts + GNS_CNT_SRC, r.bits);
+  return check_launch("clearbits");
+}
+
+int gns_unique_sorted(int64_t num_nodes, const int32_t* ids, const int32_t* n_dev, int64_t n_host, int32_t* out,
+                      int32_t* out_n_dev, void* ws, size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  RelabelWs r;
+  size_t need = relabel_ws(num_nodes, ws, ws_bytes, &r);
+  if (need > ws_bytes) {
+    set_error("unique_sorted: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  const int sms = num_sms();
+  int grid = grid_for((n_host + 255) / 256 + 1, (long long)sms * 16);
+  setbits_kernel<<<grid, 256, 0, stream>>>(ids, n_dev, n_host, nullptr, nullptr, r.bits);
+  GNS_TRY(check_launch("setbits"));
+  GNS_TRY(run_enumerate(r, num_nodes, out, out_n_dev, stream));
+  clearbits_kernel<<<grid, 256, 0, stream>>>(out, out_n_dev, r.bits);
+  return check_launch("clearbits");
+}
+
+}  // extern "C"

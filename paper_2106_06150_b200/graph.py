@@ -1,0 +1,205 @@
+"""HBM-resident CSR graph and node sets (reference: graph.py:52-139).
+
+``Graph`` mirrors the reference's immutable CSR (``graph.py:52-104``): rows
+sorted ascending, symmetric, no self loops.  On B200 it lives in HBM:
+``indptr`` int64[N+1], ``indices`` int32[E] (ids < 2^31), features float32
+[N, D] row-major (rows padded to a 16-byte multiple for 128-bit gathers),
+labels int32, masks bool.  ``NodeSet`` keeps sorted int32 ids plus a packed
+membership bitmap (bit v of word v>>5, N/8 bytes — L2-resident at 111M nodes)
+instead of the reference's bool[N] mask (``graph.py:107-139``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import GraphFormatError, InvariantError  # noqa: F401  (re-export)
+
+
+def _dev(device):
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+class Graph:
+    """Undirected CSR graph resident in HBM (graph.py:52-104)."""
+
+    def __init__(self, num_nodes: int, indptr: torch.Tensor, indices: torch.Tensor,
+                 features: torch.Tensor | None = None, labels: torch.Tensor | None = None,
+                 train_mask: torch.Tensor | None = None, val_mask: torch.Tensor | None = None,
+                 test_mask: torch.Tensor | None = None, feature_dim: int | None = None):
+        if indptr.dtype != torch.int64 or indices.dtype != torch.int32:
+            raise ValueError("Graph needs indptr int64 and indices int32 device tensors")
+        if num_nodes >= 2 ** 31:
+            raise ValueError("node ids must fit in int32")
+        self.num_nodes = int(num_nodes)
+        self.indptr = indptr
+        self.indices = indices
+        self.features = features              # [N, ld] float32, ld % 4 == 0
+        self._feature_dim = feature_dim if feature_dim is not None else (
+            0 if features is None else int(features.shape[1]))
+        self.labels = labels
+        self.train_mask = train_mask
+        self.val_mask = val_mask
+        self.test_mask = test_mask
+        self.degrees = (indptr[1:] - indptr[:-1]).to(torch.int32)
+        self._train_ids = None
+        self._cstruct = _lib.GnsGraph(self.num_nodes, int(indices.shape[0]), indptr.data_ptr(),
+                                      indices.data_ptr())
+
+    # -- reference properties ------------------------------------------------
+    @property
+    def num_edges(self) -> int:
+        """Directed edge entries (graph.py:78-80)."""
+        return int(self.indices.shape[0])
+
+    @property
+    def feature_dim(self) -> int:
+        return self._feature_dim
+
+    @property
+    def device(self):
+        return self.indptr.device
+
+    def degree(self, v: int) -> int:
+        return int(self.degrees[v])
+
+    def neighbors(self, v: int) -> torch.Tensor:
+        return self.indices[int(self.indptr[v]):int(self.indptr[v + 1])]
+
+    def cstruct(self):
+        return self._cstruct
+
+    def train_ids(self) -> torch.Tensor:
+        """graph.py:418-422: sorted train ids (all nodes without a mask), int32."""
+        if self._train_ids is None:
+            if self.train_mask is None:
+                self._train_ids = torch.arange(self.num_nodes, dtype=torch.int32, device=self.device)
+            else:
+                self._train_ids = torch.nonzero(self.train_mask).flatten().to(torch.int32)
+        return self._train_ids
+
+    @property
+    def feature_ld(self) -> int:
+        return 0 if self.features is None else int(self.features.stride(0))
+
+    # -- construction -----------------------------------------------------------
+    @classmethod
+    def from_numpy(cls, num_nodes, indptr, indices, features=None, labels=None, train_mask=None,
+                   val_mask=None, test_mask=None, device=None) -> "Graph":
+        dev = _dev(device)
+        ip = torch.as_tensor(np.asarray(indptr, dtype=np.int64)).to(dev)
+        ix = torch.as_tensor(np.asarray(indices).astype(np.int32, copy=False)).to(dev)
+        feats, fdim = None, None
+        if features is not None:
+            f = np.asarray(features, dtype=np.float32)
+            fdim = f.shape[1]
+            ld = (fdim + 3) // 4 * 4
+            feats = torch.zeros((f.shape[0], ld), dtype=torch.float32, device=dev)
+            feats[:, :fdim] = torch.as_tensor(f).to(dev)
+        lab = None if labels is None else torch.as_tensor(np.asarray(labels, dtype=np.int32)).to(dev)
+
+        def m(x):
+            return None if x is None else torch.as_tensor(np.asarray(x, dtype=bool)).to(dev)
+
+        return cls(int(num_nodes), ip, ix, feats, lab, m(train_mask), m(val_mask), m(test_mask),
+                   feature_dim=fdim)
+
+    @classmethod
+    def from_reference(cls, g, device=None) -> "Graph":
+        """Upload any reference-shaped graph (gnsbench.Graph, oracle OGraph)."""
+        return cls.from_numpy(g.num_nodes, g.indptr, g.indices, getattr(g, "features", None),
+                              getattr(g, "labels", None), getattr(g, "train_mask", None),
+                              getattr(g, "val_mask", None), getattr(g, "test_mask", None),
+                              device=device)
+
+    def to_host(self):
+        """numpy copy in the reference's layout (for oracle checks / CPU baseline)."""
+        from types import SimpleNamespace
+        f = None
+        if self.features is not None:
+            f = self.features[:, :self.feature_dim].cpu().numpy()
+        return SimpleNamespace(
+            num_nodes=self.num_nodes, indptr=self.indptr.cpu().numpy(),
+            indices=self.indices.cpu().numpy(), features=f,
+            labels=None if self.labels is None else self.labels.cpu().numpy(),
+            train_mask=None if self.train_mask is None else self.train_mask.cpu().numpy(),
+            val_mask=None if self.val_mask is None else self.val_mask.cpu().numpy(),
+            test_mask=None if self.test_mask is None else self.test_mask.cpu().numpy())
+
+
+@dataclass(eq=False)
+class NodeSet:
+    """Sorted unique ids + packed membership bitmap (graph.py:107-139)."""
+
+    ids: torch.Tensor        # int32 sorted unique
+    mask_bits: torch.Tensor  # int32 words (bit v of word v >> 5)
+    num_nodes: int
+
+    def __len__(self) -> int:
+        return int(self.ids.shape[0])
+
+    @property
+    def mask(self) -> torch.Tensor:
+        """bool[N] view of the bitmap (materialised on demand)."""
+        shifts = torch.arange(32, device=self.mask_bits.device, dtype=torch.int32)
+        bits = (self.mask_bits.unsqueeze(1) >> shifts) & 1
+        return bits.flatten()[:self.num_nodes].bool()
+
+    def __contains__(self, v) -> bool:
+        v = int(v)
+        return bool((int(self.mask_bits[v >> 5]) >> (v & 31)) & 1)
+
+    def contains(self, nodes) -> torch.Tensor:
+        nodes = torch.as_tensor(nodes, device=self.mask_bits.device).long()
+        return ((self.mask_bits[nodes >> 5] >> (nodes & 31).int()) & 1).bool()
+
+
+# ---------------------------------------------------------------------------
+# Synthetic power-law graphs on the device (graph.py:172-205 analogue)
+# ---------------------------------------------------------------------------
+
+def generate_powerlaw_device(num_nodes: int, num_pairs: int, alpha: float = 0.6,
+                             offset: float = 1000.0, seed: int = 0, feature_dim: int = 0,
+                             num_classes: int = 2, train_frac: float = 1.0,
+                             feature_noise: float = 3.0, device=None) -> Graph:
+    """Symmetric power-law CSR generated on the GPU (gns_gen_powerlaw_*), with
+    class-mean + noise features (graph.py:249-253 scheme) and random masks."""
+    _lib.require_cuda()
+    dev = _dev(device)
+    stream = _lib.stream_ptr()
+    ws = _lib.workspace(_lib.lib().gns_gen_workspace_size(num_nodes, num_pairs), dev)
+    indptr = torch.empty(num_nodes + 1, dtype=torch.int64, device=dev)
+    nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.call("gns_gen_powerlaw_count", num_nodes, num_pairs, float(alpha), float(offset),
+              seed & 0xFFFFFFFF, indptr.data_ptr(), nnz.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    e = int(nnz.item())
+    indices = torch.empty(max(e, 1), dtype=torch.int32, device=dev)[:e]
+    _lib.call("gns_gen_powerlaw_fill", num_nodes, num_pairs, indptr.data_ptr(), indices.data_ptr(),
+              ws.data_ptr(), ws.numel(), stream)
+    del ws
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    labels = torch.randint(0, num_classes, (num_nodes,), generator=gen, device=dev, dtype=torch.int32)
+    feats = None
+    if feature_dim > 0:
+        ld = (feature_dim + 3) // 4 * 4
+        means = torch.randn((num_classes, ld), generator=gen, device=dev)
+        feats = torch.empty((num_nodes, ld), dtype=torch.float32, device=dev)
+        chunk = 1 << 22
+        for s in range(0, num_nodes, chunk):
+            t = min(num_nodes, s + chunk)
+            feats[s:t] = means[labels[s:t].long()]
+            feats[s:t].add_(torch.randn((t - s, ld), generator=gen, device=dev), alpha=feature_noise)
+        if ld != feature_dim:
+            feats[:, feature_dim:] = 0
+    r = torch.rand(num_nodes, generator=gen, device=dev)
+    train = r < train_frac
+    rest = (1.0 - train_frac) / 2
+    val = (r >= train_frac) & (r < train_frac + rest)
+    test = r >= train_frac + rest
+    return Graph(num_nodes, indptr, indices, feats, labels, train, val, test,
+                 feature_dim=feature_dim if feature_dim else None)

@@ -1,0 +1,425 @@
+"""Mini-batch construction on B200 (reference: sampling.py).
+
+Drop-in names: ``SamplerConfig``, ``LayerBlock``, ``MiniBatch``,
+``sample_neighbors_uniform``, ``sample_neighbors_gns``, ``build_minibatch``,
+``gns_weight_paper``, ``isolated_fraction``, ``validate_minibatch``.
+
+The ``rng`` argument is a :class:`BatchRng` — the Philox key (seed, epoch,
+batch[, layer]) — instead of a numpy ``Generator``: the B200 kernels draw
+their own counter-based keys per (node, layer, phase, position), which is the
+SPEC's "deterministic per (seed, epoch, batch_index, layer, dst node id)"
+contract.  ``SamplerPool`` derives it from (seed, epoch, index)
+exactly where the reference derives ``default_rng([seed, 32, epoch, index])``
+(pool.py:70).
+
+``MiniBatchSampler`` is the engine: capacity-sized HBM buffers for every
+layer (static bounds from the fanout product) so a whole
+batch is sampled with device-side counts and no host synchronisation; the
+host reads all counts once per batch (``DeviceMiniBatch.sync``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from ._lib import InvariantError
+from .cache import CacheState
+from .graph import Graph
+
+STRATEGIES = ("NS", "GNS", "LADIES")
+WEIGHT_POLICIES = ("uniform", "gns-paper", "gns-exact", "ladies")
+
+
+@dataclass(frozen=True)
+class SamplerConfig:
+    """sampling.py:80-126 (same fields, defaults and validation)."""
+
+    strategy: str = "NS"
+    fanouts: tuple = (15, 10, 5)
+    layer_size: int = 512
+    cache_frac: float = 0.01
+    cache_period: int = 1
+    cache_mode: str = "auto"
+    input_layer_cache_only: bool = True
+    batch_size: int = 1000
+    seed: int = 0
+    weight_policy: str = ""
+    exact_resamples: int = 64
+
+    def __post_init__(self):
+        if self.strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {self.strategy!r}")
+        if len(self.fanouts) < 1 or any(k < 1 for k in self.fanouts):
+            raise ValueError("fanouts must be a non-empty tuple of counts >= 1")
+        if not (0.0 < self.cache_frac <= 1.0):
+            raise ValueError("cache_frac must be in (0, 1]")
+        if self.cache_period < 1:
+            raise ValueError("cache_period must be >= 1")
+        if self.cache_mode not in ("auto", "degree", "walk"):
+            raise ValueError(f"unknown cache_mode {self.cache_mode!r}")
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+        if self.layer_size < 1:
+            raise ValueError("layer_size must be >= 1")
+        if not self.weight_policy:
+            default = {"NS": "uniform", "GNS": "gns-paper", "LADIES": "ladies"}[self.strategy]
+            object.__setattr__(self, "weight_policy", default)
+        if self.weight_policy not in WEIGHT_POLICIES:
+            raise ValueError(f"unknown weight_policy {self.weight_policy!r}")
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.fanouts)
+
+
+@dataclass(frozen=True)
+class BatchRng:
+    """Philox key of one mini-batch: (seed, epoch, batch); ``layer`` is only
+    used by the single-layer entry points."""
+
+    seed: int = 0
+    epoch: int = 0
+    batch: int = 0
+    layer: int = 0
+
+    def cstruct(self, layer=None):
+        return _lib.GnsRng(self.seed & 0xFFFFFFFF, self.epoch & 0xFFFFFFFF, self.batch & 0xFFFFFFFF,
+                           (self.layer if layer is None else layer) & 0xFF)
+
+
+def _as_rng(rng) -> BatchRng:
+    if isinstance(rng, BatchRng):
+        return rng
+    raise TypeError("the B200 sampler draws counter-based Philox keys: pass "
+                    "paper_2106_06150_b200.BatchRng(seed, epoch, batch) as rng")
+
+
+@dataclass(eq=False)
+class LayerBlock:
+    """sampling.py:32-60, device tensors (ids int32, weights float64)."""
+
+    dst_nodes: torch.Tensor
+    src_nodes: torch.Tensor
+    edge_src: torch.Tensor
+    edge_dst: torch.Tensor
+    edge_weight: torch.Tensor
+    edge_cached: torch.Tensor
+    dst_degree: torch.Tensor
+    fanout: int | None
+    policy: str
+    self_pos: torch.Tensor | None = None
+    edge_node: torch.Tensor | None = None
+    row_scan: torch.Tensor | None = None
+    _c: object = None  # gns_block_t of the engine buffers
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.edge_src.shape[0])
+
+    def to_numpy(self):
+        """Reference dtypes (int64 / float64 / bool) on the host."""
+        from types import SimpleNamespace
+        return SimpleNamespace(
+            dst_nodes=self.dst_nodes.long().cpu().numpy(), src_nodes=self.src_nodes.long().cpu().numpy(),
+            edge_src=self.edge_src.long().cpu().numpy(), edge_dst=self.edge_dst.long().cpu().numpy(),
+            edge_weight=self.edge_weight.cpu().numpy(), edge_cached=self.edge_cached.bool().cpu().numpy(),
+            dst_degree=self.dst_degree.long().cpu().numpy(), fanout=self.fanout, policy=self.policy,
+            num_edges=self.num_edges)
+
+
+@dataclass(eq=False)
+class MiniBatch:
+    """sampling.py:63-77: blocks input layer first."""
+
+    blocks: tuple
+    targets: torch.Tensor
+    input_nodes: torch.Tensor
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.blocks)
+
+
+# ---------------------------------------------------------------------------
+# engine
+# ---------------------------------------------------------------------------
+
+@dataclass
+class _LayerBuffers:
+    k: int
+    layer: int
+    cache_only: bool
+    max_dst: int
+    max_edges: int
+    max_src: int
+    row_scan: torch.Tensor
+    dst_degree: torch.Tensor
+    self_pos: torch.Tensor
+    hub_rows: torch.Tensor
+    edge_node: torch.Tensor
+    edge_src: torch.Tensor
+    edge_dst: torch.Tensor
+    edge_weight: torch.Tensor
+    edge_cached: torch.Tensor
+    src_nodes: torch.Tensor
+    counts: torch.Tensor
+    cblock: object = None
+
+
+class MiniBatchSampler:
+    """Static-capacity device buffers + the L-layer sampling chain.
+
+    Layer buffers are ordered output layer first (the reference's loop order
+    ``layer = L..1``, sampling.py:314).  Capacities: the top layer has at most
+    ``batch_size`` dst rows; each layer's edges <= dst * k; src <= min(N, dst +
+    edges), which is the next layer's dst bound.
+    """
+
+    def __init__(self, g: Graph, config: SamplerConfig, max_targets: int | None = None):
+        _lib.require_cuda()
+        if config.strategy == "LADIES":
+            raise NotImplementedError("LADIES is a baseline outside the GNS hot path (SURVEY.md §2)")
+        if config.strategy == "GNS" and config.weight_policy != "gns-paper":
+            raise NotImplementedError("gns-exact weights are SURVEY.md §8(f)3, not built yet")
+        self.g = g
+        self.config = config
+        dev = g.device
+        self.device = dev
+        L = config.num_layers
+        self.max_targets = int(max_targets or config.batch_size)
+        n = g.num_nodes
+        # all per-layer device counters in one tensor -> one D2H per batch
+        self.counts = torch.zeros((L, _lib.CNT_N), dtype=torch.int32, device=dev)
+        self.counts_host = torch.zeros((L, _lib.CNT_N), dtype=torch.int32).pin_memory()
+        self.layers: list[_LayerBuffers] = []
+        dst_cap = self.max_targets
+        for i, layer in enumerate(range(L, 0, -1)):
+            k = int(config.fanouts[L - layer])
+            edge_cap = dst_cap * k
+            src_cap = min(n, dst_cap + edge_cap)
+            lb = _LayerBuffers(
+                k=k, layer=layer,
+                cache_only=(config.strategy == "GNS" and config.input_layer_cache_only and layer == 1),
+                max_dst=dst_cap, max_edges=edge_cap, max_src=src_cap,
+                row_scan=torch.empty(dst_cap + 1, dtype=torch.int64, device=dev),
+                dst_degree=torch.empty(dst_cap, dtype=torch.int32, device=dev),
+                self_pos=torch.empty(dst_cap, dtype=torch.int32, device=dev),
+                hub_rows=torch.empty(dst_cap, dtype=torch.int32, device=dev),
+                edge_node=torch.empty(max(edge_cap, 1), dtype=torch.int32, device=dev),
+                edge_src=torch.empty(max(edge_cap, 1), dtype=torch.int32, device=dev),
+                edge_dst=torch.empty(max(edge_cap, 1), dtype=torch.int32, device=dev),
+                edge_weight=torch.empty(max(edge_cap, 1), dtype=torch.float64, device=dev),
+                edge_cached=torch.empty(max(edge_cap, 1), dtype=torch.uint8, device=dev),
+                src_nodes=torch.empty(max(src_cap, 1), dtype=torch.int32, device=dev),
+                counts=self.counts[i],
+            )
+            lb.cblock = _lib.GnsBlock(*(t.data_ptr() for t in (
+                lb.row_scan, lb.dst_degree, lb.self_pos, lb.hub_rows, lb.edge_node, lb.edge_src,
+                lb.edge_dst, lb.edge_weight, lb.edge_cached, lb.src_nodes, lb.counts)))
+            self.layers.append(lb)
+            dst_cap = src_cap
+        lib = _lib.lib()
+        self.targets = torch.empty(max(self.max_targets, 1), dtype=torch.int32, device=dev)
+        self.seeds0 = torch.empty(max(self.max_targets, 1), dtype=torch.int32, device=dev)
+        self.n_seeds0 = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ws_sample = _lib.workspace(lib.gns_sample_workspace_size(max(l.max_dst for l in self.layers)), dev)
+        # bitmap must start zeroed; every relabel leaves it zeroed
+        self.ws_relabel = _lib.workspace(lib.gns_relabel_workspace_size(n), dev, zero=True)
+
+    # -- device-side chain -------------------------------------------------------
+    def sample_async(self, targets: torch.Tensor | None, n_targets: int, rng: BatchRng,
+                     cache: CacheState | None, stream=None):
+        """Enqueue the whole L-layer chain on ``stream``; targets (int32 device,
+        any order, may repeat) are deduplicated+sorted first (sampling.py:312).
+        If ``targets`` is None the caller already wrote ``self.targets``."""
+        s = _lib.stream_ptr(stream)
+        if targets is not None:
+            if targets.numel() > self.max_targets:
+                raise ValueError(f"{targets.numel()} targets exceed capacity {self.max_targets}")
+            self.targets[:targets.numel()].copy_(targets.to(torch.int32), non_blocking=True)
+            n_targets = targets.numel()
+        _lib.call("gns_unique_sorted", self.g.num_nodes, self.targets.data_ptr(), None, int(n_targets),
+                  self.seeds0.data_ptr(), self.n_seeds0.data_ptr(), self.ws_relabel.data_ptr(),
+                  self.ws_relabel.numel(), s)
+        gns = self.config.strategy == "GNS"
+        if gns and cache is None:
+            raise ValueError("GNS sampling needs a CacheState")
+        cstruct = cache.cstruct() if gns else None
+        seeds, n_dev = self.seeds0, self.n_seeds0
+        gc = self.g.cstruct()
+        for lb in self.layers:
+            _lib.call("gns_sample_layer", gc, cstruct, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
+                      lb.k, int(lb.cache_only), rng.cstruct(lb.layer), lb.cblock,
+                      self.ws_sample.data_ptr(), self.ws_sample.numel(), s)
+            _lib.call("gns_relabel", self.g.num_nodes, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
+                      lb.cblock, lb.max_edges, self.ws_relabel.data_ptr(), self.ws_relabel.numel(), s)
+            seeds = lb.src_nodes
+            n_dev = lb.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
+        self.counts_host.copy_(self.counts, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream if stream is not None else torch.cuda.current_stream())
+        return ev
+
+    def collect(self, event=None, policy_ns="uniform", policy_gns="gns-paper") -> MiniBatch:
+        """Wait for the counts of the last ``sample_async`` and wrap the buffers
+        as a MiniBatch (views sized to the real counts; blocks input first)."""
+        if event is not None:
+            event.synchronize()
+        else:
+            torch.cuda.current_stream().synchronize()
+        c = self.counts_host.tolist()
+        err = 0
+        blocks = []
+        seeds_n = None
+        for i, lb in enumerate(self.layers):
+            nd, ne, nsrc, e = c[i][_lib.CNT_DST], c[i][_lib.CNT_EDGES], c[i][_lib.CNT_SRC], c[i][_lib.CNT_ERR]
+            err |= e
+            dst = self.seeds0[:nd] if i == 0 else self.layers[i - 1].src_nodes[:nd]
+            blocks.append(LayerBlock(
+                dst_nodes=dst, src_nodes=lb.src_nodes[:nsrc], edge_src=lb.edge_src[:ne],
+                edge_dst=lb.edge_dst[:ne], edge_weight=lb.edge_weight[:ne],
+                edge_cached=lb.edge_cached[:ne], dst_degree=lb.dst_degree[:nd], fanout=lb.k,
+                policy=policy_gns if self.config.strategy == "GNS" else policy_ns,
+                self_pos=lb.self_pos[:nd], edge_node=lb.edge_node[:ne], row_scan=lb.row_scan[:nd + 1],
+                _c=lb.cblock))
+            seeds_n = nsrc
+        if err & _lib.ERRBIT_ZEROPROB:
+            raise ValueError("inclusion probability is zero for a cached draw")
+        if err & _lib.ERRBIT_CAPACITY:
+            raise InvariantError("neighbour selection did not converge (capacity)")
+        blocks.reverse()
+        return MiniBatch(blocks=tuple(blocks), targets=blocks[-1].dst_nodes,
+                         input_nodes=blocks[0].src_nodes)
+
+    def sample(self, targets, rng: BatchRng, cache: CacheState | None = None) -> MiniBatch:
+        t = torch.as_tensor(targets, device=self.device)
+        ev = self.sample_async(t, t.numel(), rng, cache)
+        return self.collect(ev)
+
+
+_ENGINES: dict = {}
+
+
+def _engine(g: Graph, config: SamplerConfig, n_targets: int) -> MiniBatchSampler:
+    key = (id(g), config, )
+    eng = _ENGINES.get(key)
+    if eng is None or eng.max_targets < n_targets:
+        eng = MiniBatchSampler(g, config, max_targets=max(n_targets, config.batch_size))
+        _ENGINES.clear()
+        _ENGINES[key] = eng
+    return eng
+
+
+def build_minibatch(g: Graph, cache: CacheState | None, targets, config: SamplerConfig, rng,
+                    exact_tables: dict | None = None) -> MiniBatch:
+    """sampling.py:299-336.  Returned tensors are views of engine buffers that
+    the next call on the same (graph, config) overwrites; clone to keep."""
+    rng = _as_rng(rng)
+    if config.strategy == "LADIES":
+        raise NotImplementedError("LADIES is outside the GNS hot path (SURVEY.md §2)")
+    if config.strategy == "GNS" and cache is None:
+        raise ValueError("GNS sampling needs a CacheState")
+    t = torch.as_tensor(targets, device=g.device)
+    eng = _engine(g, config, t.numel())
+    return eng.sample(t, rng, cache if config.strategy == "GNS" else None)
+
+
+def _single_layer(g, cache, seeds, k, cache_only, rng, strategy):
+    rng = _as_rng(rng)
+    if k < 1:
+        raise ValueError("fanout must be >= 1")
+    cfg = SamplerConfig(strategy=strategy, fanouts=(int(k),),
+                        input_layer_cache_only=bool(cache_only), batch_size=max(1, len(seeds)))
+    t = torch.as_tensor(seeds, device=g.device)
+    eng = MiniBatchSampler(g, cfg, max_targets=max(1, t.numel()))
+    eng.layers[0].layer = rng.layer
+    eng.layers[0].cache_only = bool(cache_only) and strategy == "GNS"
+    mb = eng.sample(t, rng, cache)
+    return mb.blocks[0]
+
+
+def sample_neighbors_uniform(g: Graph, seeds, k: int, rng) -> LayerBlock:
+    """sampling.py:155-170: min(k, deg) uniform neighbours, weight deg/min(k, deg)."""
+    return _single_layer(g, None, seeds, k, False, rng, "NS")
+
+
+def sample_neighbors_gns(g: Graph, cache: CacheState, seeds, k: int, cache_only: bool, rng,
+                         policy: str = "gns-paper", exact_weights=None) -> LayerBlock:
+    """sampling.py:189-266 (gns-paper policy)."""
+    if k < 1:
+        raise ValueError("fanout must be >= 1")
+    if policy not in ("gns-paper", "gns-exact"):
+        raise ValueError(f"unsupported GNS weight policy {policy!r}")
+    if policy == "gns-exact":
+        if exact_weights is None:
+            raise ValueError("gns-exact policy needs an edge-inclusion table")
+        raise NotImplementedError("gns-exact is SURVEY.md §8(f)3, not built yet")
+    return _single_layer(g, cache, seeds, k, cache_only, rng, "GNS")
+
+
+def gns_weight_paper(p_v: float, cache_size: int, k: int, n_cached: int) -> float:
+    """sampling.py:173-186 (scalar helper; Eq. 9 from the device kernel)."""
+    if n_cached < 1 or k < 1:
+        raise ValueError("need n_cached >= 1 and k >= 1")
+    from .cache import inclusion_prob
+    p_c = inclusion_prob(p_v, cache_size)
+    if p_c <= 0.0:
+        raise ValueError("inclusion probability is zero; cannot weight draw")
+    return min(k, n_cached) / (k * p_c)
+
+
+def isolated_fraction(mb: MiniBatch) -> float:
+    """sampling.py:413-425 on the device."""
+    block = mb.blocks[0]
+    if mb.targets.numel() == 0:
+        return 0.0
+    indeg = torch.bincount(block.edge_dst.long(), minlength=block.dst_nodes.numel())
+    tpos = torch.searchsorted(block.dst_nodes, mb.targets)
+    return float((indeg[tpos] == 0).float().mean())
+
+
+def validate_minibatch(g: Graph, mb: MiniBatch) -> None:
+    """sampling.py:428-470 structural invariants, evaluated with device ops."""
+    for i, block in enumerate(mb.blocks):
+        d, s = block.dst_nodes, block.src_nodes
+        if (d[1:] <= d[:-1]).any() or (s[1:] <= s[:-1]).any():
+            raise InvariantError(f"block {i}: node arrays must be sorted unique")
+        if not torch.isin(d, s).all():
+            raise InvariantError(f"block {i}: dst nodes missing from src")
+        if block.num_edges:
+            if int(block.edge_src.max()) >= s.numel() or int(block.edge_dst.max()) >= d.numel():
+                raise InvariantError(f"block {i}: edge index out of range")
+            srcs = s[block.edge_src.long()].long()
+            dsts = d[block.edge_dst.long()].long()
+            # (src, dst) is an edge iff dst is in src's sorted row
+            lo = g.indptr[srcs]
+            hi = g.indptr[srcs + 1]
+            # binary search per edge in its row
+            l, h = lo.clone(), hi.clone()
+            for _ in range(40):
+                mid = (l + h) // 2
+                v = g.indices[torch.clamp(mid, max=g.num_edges - 1)].long()
+                go = v < dsts
+                l = torch.where(go & (l < h), mid + 1, l)
+                h = torch.where(~go & (l < h), mid, h)
+            ok = (l < hi) & (g.indices[torch.clamp(l, max=g.num_edges - 1)].long() == dsts)
+            if not ok.all():
+                raise InvariantError(f"block {i}: sampled a non-edge")
+            w = block.edge_weight
+            if not torch.isfinite(w).all() or (w <= 0).any():
+                raise InvariantError(f"block {i}: edge weights must be finite > 0")
+            if block.fanout is not None:
+                indeg = torch.bincount(block.edge_dst.long(), minlength=d.numel())
+                if int(indeg.max()) > block.fanout:
+                    raise InvariantError(f"block {i}: fanout bound {block.fanout} exceeded")
+        if not torch.equal(block.dst_degree.long(), g.degrees[d.long()].long()):
+            raise InvariantError(f"block {i}: stale dst degrees")
+        if i + 1 < len(mb.blocks) and not torch.equal(d, mb.blocks[i + 1].src_nodes):
+            raise InvariantError(f"block {i}: dst set does not chain into block {i + 1} src")
+    if not torch.equal(mb.targets, mb.blocks[-1].dst_nodes):
+        raise InvariantError("targets must equal the last block's dst set")
+    if not torch.equal(mb.input_nodes, mb.blocks[0].src_nodes):
+        raise InvariantError("input_nodes must equal the first block's src set")

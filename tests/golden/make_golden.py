@@ -1,0 +1,146 @@
+"""Generate golden fixtures by running the REFERENCE (gnsbench) in this container.
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The reference is Python and cannot travel to the GPU box, so its outputs on
+small inputs are committed here (``golden_*.npz``).  Each fixture records the
+inputs (graph CSR, cache ids, targets, Philox key) and the reference's outputs
+when fed the build's Philox keys through its duck-typed ``rng.random(n)``
+(``sampling.py:166,214,233``) via ``oracle.gns.ReplayRng``.  GPU tests compare
+the B200 kernels against these arrays bit for bit.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import gnsbench as gb  # noqa: E402
+
+from oracle import gns as O  # noqa: E402
+
+
+def _block_arrays(prefix, mb, out):
+    for i, b in enumerate(mb.blocks):
+        for f in ("dst_nodes", "src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached",
+                  "dst_degree"):
+            out[f"{prefix}_b{i}_{f}"] = np.asarray(getattr(b, f))
+
+
+def make_sampler_golden():
+    out = {}
+    g = gb.generate_powerlaw(2000, 4, 0)
+    out["indptr"], out["indices"] = g.indptr, g.indices
+    probs = gb.degree_probs(g)
+    out["probs"] = probs.weights
+    cs = 40
+    # reference cache draw under its own numpy stream (statistical reference)
+    ref_cache = gb.build_cache(g, probs, cs, epoch=0, rng_seed=[0, 33, 0])
+    out["ref_cache_ids_numpy"] = ref_cache.nodes.ids
+    # the build's Philox cache draw, injected into the reference (cache replay)
+    w = O.degree_probs(g)
+    ids = O.sample_cache(w, cs, seed=0, epoch=0)
+    out["philox_cache_ids"] = ids
+    orig = gb.cache.sample_cache
+    gb.cache.sample_cache = lambda probs_, size_, seed_: gb.NodeSet.from_ids(ids, g.num_nodes)
+    try:
+        cache = gb.build_cache(g, probs, cs, epoch=0, rng_seed=[0, 33, 0])
+    finally:
+        gb.cache.sample_cache = orig
+    out["cache_inclusion_ref"] = cache.inclusion
+    out["cached_indptr"] = cache.cached_indptr
+    out["cached_indices"] = cache.cached_indices
+    oc = O.OCache(ids=cache.nodes.ids, mask=cache.nodes.mask, inclusion=cache.inclusion,
+                  cached_indptr=cache.cached_indptr, cached_indices=cache.cached_indices)
+    cases = [("gns", gb.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=64,
+                                      cache_mode="degree", seed=0)),
+             ("gnsfill", gb.SamplerConfig(strategy="GNS", fanouts=(6, 4), batch_size=64,
+                                          cache_mode="degree", input_layer_cache_only=False, seed=3)),
+             ("ns", gb.SamplerConfig(strategy="NS", fanouts=(15, 10, 5), batch_size=64, seed=0))]
+    rs = np.random.default_rng(7)
+    for name, cfg in cases:
+        targets = rs.choice(g.num_nodes, size=64, replace=False)
+        out[f"{name}_targets"] = targets
+        for epoch, index in ((0, 0), (2, 5)):
+            rec = []
+            O.build_minibatch(g, oc if cfg.strategy == "GNS" else None, targets, cfg,
+                              O.PhiloxKeys(cfg.seed, epoch, index, record=rec))
+            mb = gb.build_minibatch(g, cache if cfg.strategy == "GNS" else None, targets, cfg,
+                                    O.ReplayRng(rec))
+            _block_arrays(f"{name}_e{epoch}_i{index}", mb, out)
+            out[f"{name}_e{epoch}_i{index}_nblocks"] = np.array(len(mb.blocks))
+    np.savez_compressed(os.path.join(HERE, "golden_sampler.npz"), **out)
+
+
+def make_kat_golden():
+    out = {
+        "inclusion_0p01_100": np.array(gb.inclusion_prob(0.01, 100)),
+        "gns_weight_0p01_100_10_4": np.array(gb.gns_weight_paper(0.01, 100, 10, 4)),
+        "gns_weight_pc_half": np.array(1.0 / (0.5 * 5 / 5)),
+        "star_probs": gb.degree_probs(gb.build_csr([(0, 1), (0, 2), (0, 3)], 4)).weights,
+    }
+    p = np.concatenate([10.0 ** -np.linspace(0, 12, 200), [0.0, 1.0, 0.5]])
+    out["incl_p"] = p
+    for cs in (1, 100, 111000):
+        out[f"incl_ref_{cs}"] = gb.inclusion_prob(p, cs)
+    np.savez_compressed(os.path.join(HERE, "golden_kat.npz"), **out)
+
+
+def make_model_golden():
+    """Reference fp64 trainer (model.py:279-285 loop body) for 6 steps on an SBM
+    graph with replayed Philox keys and a Philox cache."""
+    out = {}
+    g = gb.generate_sbm(400, 4, 0.05, 0.005, seed=1, feature_dim=16)
+    out["indptr"], out["indices"] = g.indptr, g.indices
+    out["features"], out["labels"] = g.features, g.labels
+    out["train_mask"] = g.train_mask
+    cfg = gb.SamplerConfig(strategy="GNS", fanouts=(5, 3), batch_size=50, cache_frac=0.1,
+                           cache_mode="degree", seed=0)
+    w = O.degree_probs(g)
+    cs = int(round(cfg.cache_frac * g.num_nodes))
+    ids = O.sample_cache(w, cs, seed=0, epoch=0)
+    probs = gb.degree_probs(g)
+    orig = gb.cache.sample_cache
+    gb.cache.sample_cache = lambda probs_, size_, seed_: gb.NodeSet.from_ids(ids, g.num_nodes)
+    try:
+        cache = gb.build_cache(g, probs, cs, epoch=0, rng_seed=[0, 33, 0])
+    finally:
+        gb.cache.sample_cache = orig
+    oc = O.OCache(ids=cache.nodes.ids, mask=cache.nodes.mask, inclusion=cache.inclusion,
+                  cached_indptr=cache.cached_indptr, cached_indices=cache.cached_indices)
+    dims = (16, 32, 4)
+    params = gb.init_params(dims, seed=0)
+    state = gb.AdamState.zeros_like(params)
+    tc = gb.TrainConfig(lr=0.003)
+    batches = O.epoch_targets(g, cfg.batch_size, cfg.seed, 0)
+    losses = []
+    for index, targets in enumerate(batches[:6]):
+        rec = []
+        O.build_minibatch(g, oc, targets, cfg, O.PhiloxKeys(cfg.seed, 0, index, record=rec))
+        mb = gb.build_minibatch(g, cache, targets, cfg, O.ReplayRng(rec))
+        logits = gb.forward(mb, g.features, params)
+        loss, grad = gb.loss_and_grad(logits, g.labels[mb.targets])
+        grads = gb.backward(mb, g.features, params, grad)
+        gb.adam_step(params, grads, state, tc)
+        losses.append(loss)
+    out["losses"] = np.array(losses)
+    for i, (wt, b) in enumerate(zip(params.weights, params.biases)):
+        out[f"final_w{i}"], out[f"final_b{i}"] = wt, b
+    out["cache_ids"] = ids
+    np.savez_compressed(os.path.join(HERE, "golden_model.npz"), **out)
+
+
+if __name__ == "__main__":
+    make_kat_golden()
+    make_sampler_golden()
+    make_model_golden()
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))

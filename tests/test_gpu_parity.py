@@ -1,0 +1,496 @@
+"""GPU parity: libgns.so kernels vs the reference's golden outputs and the oracle.
+
+Bit-exact for ids, offsets, relabel maps, float64 weights, cached CSR and the
+float64 SpMM; statistical tests for the draws; tolerance-stated for training.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import detmath, philox
+from oracle import gns as O
+from oracle import model as OM
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("dst_nodes", "src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached", "dst_degree")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2106_06150_b200 as P
+    return P
+
+
+def _golden_graph(P, gold):
+    n = len(gold["indptr"]) - 1
+    og = O.OGraph(num_nodes=n, indptr=gold["indptr"], indices=gold["indices"])
+    return og, P.Graph.from_numpy(n, gold["indptr"], gold["indices"])
+
+
+def assert_mb_equal(mb_gpu, mb_ref, tag=""):
+    assert len(mb_gpu.blocks) == len(mb_ref.blocks), tag
+    for i, (bg, br) in enumerate(zip(mb_gpu.blocks, mb_ref.blocks)):
+        h = bg.to_numpy()
+        for f in FIELDS:
+            a, b = getattr(h, f), np.asarray(getattr(br, f))
+            assert a.shape == b.shape, (tag, i, f, a.shape, b.shape)
+            assert np.array_equal(a, b), (tag, i, f)
+        # relabel map: self_pos = searchsorted(src_nodes, dst_nodes) (model.py:137)
+        sp = np.searchsorted(h.src_nodes, h.dst_nodes)
+        assert np.array_equal(bg.self_pos.cpu().numpy(), sp), (tag, i, "self_pos")
+        assert np.array_equal(bg.edge_node.cpu().numpy(), h.src_nodes[h.edge_src]), (tag, i, "edge_node")
+
+
+# ---- cache engine -----------------------------------------------------------------
+
+def test_degree_probs_bit_exact(P, golden):
+    gold = golden["sampler"]
+    og, g = _golden_graph(P, gold)
+    probs = P.degree_probs(g)
+    assert np.array_equal(probs.weights.cpu().numpy(), O.degree_probs(og))
+    assert np.array_equal(probs.weights.cpu().numpy(), gold["probs"])
+
+
+def test_cache_draw_matches_oracle(P, golden):
+    gold = golden["sampler"]
+    og, g = _golden_graph(P, gold)
+    probs = P.degree_probs(g)
+    ns = P.sample_cache(probs, 40, [0, 33, 0])
+    assert np.array_equal(ns.ids.cpu().numpy(), gold["philox_cache_ids"])
+    mask = ns.mask.cpu().numpy()
+    assert np.array_equal(np.flatnonzero(mask), gold["philox_cache_ids"])
+    w = O.degree_probs(og)
+    for cs, (seed, epoch) in [(1, (3, 0)), (7, (0, 9)), (500, (1, 1)), (1999, (2, 2))]:
+        got = P.sample_cache(probs, cs, [seed, 33, epoch]).ids.cpu().numpy()
+        assert np.array_equal(got, O.sample_cache(w, cs, seed=seed, epoch=epoch)), cs
+
+
+def test_cache_draw_edge_cases(P):
+    # empty draw, saturation returns exactly the positive support
+    w = torch.tensor([0.0, 0.5, 0.25, 0.0, 0.25], dtype=torch.float64, device="cuda")
+    pv = P.ProbVector(w, normalized=True)
+    assert P.sample_cache(pv, 0, 0).ids.numel() == 0
+    assert P.sample_cache(pv, 3, 0).ids.tolist() == [1, 2, 4]
+    assert P.sample_cache(pv, 10, 0).ids.tolist() == [1, 2, 4]
+    # ties: uniform weights -> identical p; (key, id) order decides
+    n = 100_003
+    wu = np.full(n, 1.0 / n)
+    pu = P.ProbVector(torch.as_tensor(wu, device="cuda"), normalized=True)
+    got = P.sample_cache(pu, 12_345, [5, 33, 2]).ids.cpu().numpy()
+    assert np.array_equal(got, O.sample_cache(wu, 12_345, seed=5, epoch=2))
+
+
+def test_inclusion_bit_exact(P, golden):
+    kat = golden["kat"]
+    rng = np.random.default_rng(3)
+    p = np.concatenate([10.0 ** -rng.uniform(0, 12, 20000), [0.0, 1.0, 0.5, 0.999999999999999]])
+    for cs in (0, 1, 100, 111_000, 1_110_000):
+        got = P.inclusion_prob(p, cs)
+        assert np.array_equal(got, detmath.inclusion_prob(p, cs)), cs
+    assert abs(P.inclusion_prob(0.01, 100) - 0.63397) < 1e-5
+    for cs in (1, 100, 111000):
+        ref = kat[f"incl_ref_{cs}"]
+        got = P.inclusion_prob(kat["incl_p"], cs)
+        assert np.max(np.abs(got - ref) / np.spacing(np.maximum(np.abs(ref), 1e-300))) <= 4
+
+
+def test_build_cache_matches_reference(P, golden):
+    gold = golden["sampler"]
+    og, g = _golden_graph(P, gold)
+    cache = P.build_cache(g, P.degree_probs(g), 40, epoch=0, rng_seed=[0, 33, 0])
+    assert np.array_equal(cache.nodes.ids.cpu().numpy(), gold["philox_cache_ids"])
+    assert np.array_equal(cache.cached_indptr.cpu().numpy(), gold["cached_indptr"])
+    assert np.array_equal(cache.cached_indices.cpu().numpy(), gold["cached_indices"])
+    oc = O.build_cache(og, O.degree_probs(og), 40, ids=gold["philox_cache_ids"])
+    assert np.array_equal(cache.inclusion.cpu().numpy(), oc.inclusion)
+    ref = gold["cache_inclusion_ref"]
+    inc = cache.inclusion.cpu().numpy()
+    assert np.max(np.abs(inc - ref) / np.spacing(np.maximum(np.abs(ref), 1e-300))) <= 4
+
+
+def test_build_cache_full_and_empty(P):
+    # C = V -> cached CSR equals the full CSR; C = {} -> empty rows
+    og = O.build_csr(np.random.default_rng(0).integers(0, 300, size=(1500, 2)), 300)
+    g = P.Graph.from_numpy(300, og.indptr, og.indices)
+    probs = P.degree_probs(g)
+    full = P.build_cache(g, probs, 300)
+    support = np.flatnonzero(np.diff(og.indptr) > 0)
+    assert np.array_equal(full.nodes.ids.cpu().numpy(), support)
+    assert np.array_equal(full.cached_indptr.cpu().numpy(), og.indptr)
+    assert np.array_equal(full.cached_indices.cpu().numpy(), og.indices)
+    inc = full.inclusion.cpu().numpy()
+    assert np.all(inc[support] == 1.0)
+    empty = P.build_cache(g, probs, 0)
+    assert len(empty) == 0 and int(empty.cached_indptr[-1]) == 0
+
+
+# ---- sampler --------------------------------------------------------------------
+
+CASES = {"gns": dict(strategy="GNS", fanouts=(15, 10, 5), input_layer_cache_only=True, seed=0),
+         "gnsfill": dict(strategy="GNS", fanouts=(6, 4), input_layer_cache_only=False, seed=3),
+         "ns": dict(strategy="NS", fanouts=(15, 10, 5), input_layer_cache_only=True, seed=0)}
+
+
+def test_minibatch_bit_exact_vs_reference_golden(P, golden):
+    """The reference's own outputs (Philox keys replayed into gnsbench)."""
+    gold = golden["sampler"]
+    og, g = _golden_graph(P, gold)
+    cache = P.build_cache(g, P.degree_probs(g), 40, epoch=0, rng_seed=[0, 33, 0])
+    for name, kw in CASES.items():
+        cfg = P.SamplerConfig(batch_size=64, cache_mode="degree", **kw)
+        for epoch, index in ((0, 0), (2, 5)):
+            mb = P.build_minibatch(g, cache if cfg.strategy == "GNS" else None,
+                                   gold[f"{name}_targets"], cfg, P.BatchRng(cfg.seed, epoch, index))
+            pre = f"{name}_e{epoch}_i{index}"
+
+            class R:
+                pass
+            ref = R()
+            ref.blocks = []
+            for i in range(int(gold[f"{pre}_nblocks"])):
+                b = R()
+                for f in FIELDS:
+                    setattr(b, f, gold[f"{pre}_b{i}_{f}"])
+                ref.blocks.append(b)
+            assert_mb_equal(mb, ref, pre)
+            P.validate_minibatch(g, mb)
+
+
+def _hub_graph(n=6000, seed=0):
+    """Power-law-ish graph with hub rows > 2048 (exercises the CTA-per-row path)."""
+    rng = np.random.default_rng(seed)
+    hubs = np.arange(8)
+    e1 = np.stack([rng.choice(hubs, 30000), rng.integers(0, n, 30000)], 1)
+    e2 = rng.integers(0, n, size=(40000, 2))
+    return O.build_csr(np.concatenate([e1, e2]), n)
+
+
+@pytest.mark.parametrize("strategy,cache_only,frac", [("GNS", True, 0.02), ("GNS", False, 0.02),
+                                                      ("GNS", False, 0.3), ("NS", False, 0.0)])
+def test_minibatch_bit_exact_vs_oracle_hubs(P, strategy, cache_only, frac):
+    og = _hub_graph()
+    assert np.diff(og.indptr).max() > 2048
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy=strategy, fanouts=(15, 10, 5), batch_size=500,
+                          input_layer_cache_only=cache_only, cache_mode="degree",
+                          cache_frac=max(frac, 0.01), seed=11)
+    cache = oc = None
+    if strategy == "GNS":
+        cs = O.cache_size_for(og, frac)
+        cache = P.build_cache(g, P.degree_probs(g), cs, rng_seed=[11, 33, 1])
+        oc = O.build_cache(og, O.degree_probs(og), cs, seed=11, epoch=1)
+        assert np.array_equal(cache.nodes.ids.cpu().numpy(), oc.ids)
+        assert np.array_equal(cache.cached_indptr.cpu().numpy(), oc.cached_indptr)
+        assert np.array_equal(cache.cached_indices.cpu().numpy(), oc.cached_indices)
+        assert np.array_equal(cache.inclusion.cpu().numpy(), oc.inclusion)
+    targets = np.concatenate([np.arange(8), np.random.default_rng(1).choice(og.num_nodes, 480, replace=False)])
+    for index in range(3):
+        mb = P.build_minibatch(g, cache, targets, cfg, P.BatchRng(11, 1, index))
+        ref = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(11, 1, index))
+        assert_mb_equal(mb, ref, f"{strategy}-{cache_only}-{index}")
+
+
+def test_single_layer_entry_points(P):
+    og = _hub_graph(2000, 3)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    seeds = np.array([5, 3, 3, 1999, 0, 7, 100])
+    b = P.sample_neighbors_uniform(g, seeds, 4, P.BatchRng(1, 2, 3, layer=2))
+    r = O.sample_neighbors_uniform(og, seeds, 4, O.PhiloxKeys(1, 2, 3), layer=2)
+    for f in FIELDS:
+        assert np.array_equal(getattr(b.to_numpy(), f), getattr(r, f)), f
+    cache = P.build_cache(g, P.degree_probs(g), 50, rng_seed=[1, 33, 0])
+    oc = O.build_cache(og, O.degree_probs(og), 50, seed=1, epoch=0)
+    for co in (True, False):
+        b = P.sample_neighbors_gns(g, cache, seeds, 6, co, P.BatchRng(1, 2, 3, layer=1))
+        r = O.sample_neighbors_gns(og, oc, seeds, 6, co, O.PhiloxKeys(1, 2, 3), layer=1)
+        for f in FIELDS:
+            assert np.array_equal(getattr(b.to_numpy(), f), getattr(r, f)), (co, f)
+    with pytest.raises(ValueError):
+        P.sample_neighbors_uniform(g, seeds, 0, P.BatchRng())
+    with pytest.raises(TypeError):
+        P.sample_neighbors_uniform(g, seeds, 3, np.random.default_rng(0))
+
+
+def test_zero_degree_and_repeated_targets(P):
+    # d = 0 -> no sampled edges, src contains only the seed
+    og = O.build_csr([(0, 1), (1, 2)], 6)
+    g = P.Graph.from_numpy(6, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy="NS", fanouts=(3, 2), batch_size=8)
+    mb = P.build_minibatch(g, None, [5, 4, 4, 0, 5], cfg, P.BatchRng(0, 0, 0))
+    ref = O.build_minibatch(og, None, [5, 4, 4, 0, 5], cfg, O.PhiloxKeys(0, 0, 0))
+    assert_mb_equal(mb, ref, "zero-degree")
+    assert mb.targets.tolist() == [0, 4, 5]
+
+
+def test_epoch_targets_feistel(P):
+    og = O.build_csr(np.random.default_rng(0).integers(0, 5000, size=(20000, 2)), 5000)
+    mask = np.random.default_rng(1).random(5000) < 0.3
+    g = P.Graph.from_numpy(5000, og.indptr, og.indices, train_mask=mask)
+    og.train_mask = mask
+    cfg = P.SamplerConfig(strategy="NS", batch_size=97, seed=4)
+    got = [t.cpu().numpy() for t in P.epoch_targets(g, cfg, 3)]
+    ref = O.epoch_targets(og, 97, 4, 3)
+    assert len(got) == len(ref)
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+    allv = np.concatenate(got)
+    assert np.array_equal(np.sort(allv), np.flatnonzero(mask))
+
+
+def test_pool_deterministic_and_complete(P):
+    og = _hub_graph(3000, 5)
+    mask = np.random.default_rng(2).random(3000) < 0.5
+    g = P.Graph.from_numpy(3000, og.indptr, og.indices, train_mask=mask)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=128, cache_mode="degree", seed=2,
+                          cache_frac=0.05)
+
+    def run(workers):
+        pool = P.SamplerPool(g, cfg, num_workers=workers)
+        out = []
+        for epoch in range(2):
+            for it in pool.iter_epoch(epoch):
+                out.append((it.epoch, it.index, [b.to_numpy() for b in it.minibatch.blocks],
+                            it.minibatch.targets.cpu().numpy().copy()))
+                assert it.sample_ms >= 0
+        return out
+
+    a, b = run(1), run(3)
+    assert [x[:2] for x in a] == [x[:2] for x in b]
+    for x, y in zip(a, b):
+        for bx, by in zip(x[2], y[2]):
+            for f in FIELDS:
+                assert np.array_equal(getattr(bx, f), getattr(by, f))
+    targets = np.concatenate([x[3] for x in a if x[0] == 0])
+    assert np.array_equal(np.sort(targets), np.flatnonzero(mask))
+
+
+# ---- gather / SpMM ---------------------------------------------------------------
+
+def _mb_and_features(P, dim=24, strategy="GNS"):
+    og = _hub_graph(4000, 9)
+    feats = np.random.default_rng(0).normal(size=(og.num_nodes, dim)).astype(np.float32)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices, features=feats)
+    cfg = P.SamplerConfig(strategy=strategy, fanouts=(8, 5, 3), batch_size=300, cache_mode="degree",
+                          input_layer_cache_only=False, seed=1)
+    cache = P.build_cache(g, P.degree_probs(g), 200, rng_seed=[1, 33, 0]) if strategy == "GNS" else None
+    oc = O.build_cache(og, O.degree_probs(og), 200, seed=1, epoch=0) if strategy == "GNS" else None
+    targets = np.random.default_rng(4).choice(og.num_nodes, 300, replace=False)
+    mb = P.build_minibatch(g, cache, targets, cfg, P.BatchRng(1, 0, 0))
+    ref = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(1, 0, 0))
+    return og, g, feats, mb, ref
+
+
+def test_gather_rows_exact(P):
+    og, g, feats, mb, ref = _mb_and_features(P, dim=24)
+    model = P.GraphSAGE((24, 8, 3))
+    h = model.gather_inputs(mb, g)
+    assert torch.equal(h.cpu(), torch.as_tensor(feats[ref.input_nodes]))
+    m64 = P.GraphSAGE((24, 8, 3), dtype=torch.float64)
+    h64 = m64.gather_inputs(mb, g)
+    assert np.array_equal(h64.cpu().numpy(), feats[ref.input_nodes].astype(np.float64))
+
+
+@pytest.mark.parametrize("dim", [2, 6, 64, 130])
+def test_spmm_fwd_f64_bit_exact(P, dim):
+    from paper_2106_06150_b200 import _lib
+    og, g, feats, mb, ref = _mb_and_features(P, dim=16)
+    for li, (bg, br) in enumerate(zip(mb.blocks, ref.blocks)):
+        nsrc, ndst = len(br.src_nodes), len(br.dst_nodes)
+        h = np.random.default_rng(li).normal(size=(nsrc, dim))
+        ht = torch.as_tensor(h, device="cuda")
+        cat = torch.empty((ndst, 2 * dim), dtype=torch.float64, device="cuda")
+        _lib.call("gns_spmm_fwd", 1, ht.data_ptr(), dim, dim, bg._c, ndst, cat.data_ptr(), 2 * dim,
+                  _lib.stream_ptr())
+        agg = OM.spmm_mean_fwd(br, h)
+        self_pos = np.searchsorted(br.src_nodes, br.dst_nodes)
+        c = cat.cpu().numpy()
+        assert np.array_equal(c[:, :dim], h[self_pos])
+        assert np.array_equal(c[:, dim:], agg), li
+        # float32 production path: same order, FMA; tolerance 1e-5 relative-to-scale
+        h32 = torch.as_tensor(h.astype(np.float32), device="cuda")
+        if dim % 4 == 0:
+            cat32 = torch.empty((ndst, 2 * dim), dtype=torch.float32, device="cuda")
+            _lib.call("gns_spmm_fwd", 0, h32.data_ptr(), dim, dim, bg._c, ndst, cat32.data_ptr(), 2 * dim,
+                      _lib.stream_ptr())
+            np.testing.assert_allclose(cat32.cpu().numpy()[:, dim:], agg, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("dim", [2, 8, 64])
+def test_spmm_bwd_f64_bit_exact(P, dim):
+    from paper_2106_06150_b200 import _lib
+    og, g, feats, mb, ref = _mb_and_features(P, dim=16)
+    ws = _lib.workspace(1 << 24, "cuda")
+    for li, (bg, br) in enumerate(zip(mb.blocks, ref.blocks)):
+        nsrc, ndst = len(br.src_nodes), len(br.dst_nodes)
+        dcat = np.random.default_rng(10 + li).normal(size=(ndst, 2 * dim))
+        dt = torch.as_tensor(dcat, device="cuda")
+        dh = torch.empty((nsrc, dim), dtype=torch.float64, device="cuda")
+        _lib.call("gns_spmm_bwd", 1, dt.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges,
+                  dh.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        expect = OM.spmm_mean_bwd(br, dcat, dim)
+        assert np.array_equal(dh.cpu().numpy(), expect), li
+        if dim % 4 == 0:
+            dt32 = torch.as_tensor(dcat.astype(np.float32), device="cuda")
+            dh32 = torch.empty((nsrc, dim), dtype=torch.float32, device="cuda")
+            _lib.call("gns_spmm_bwd", 0, dt32.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges,
+                      dh32.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+            np.testing.assert_allclose(dh32.cpu().numpy(), expect, rtol=1e-5, atol=1e-5)
+
+
+def test_full_batch_equivalence(P):
+    """with k >= max degree the sampled forward equals the
+    full-neighbourhood forward (NS keeps every neighbour, weight 1)."""
+    og = O.build_csr(np.random.default_rng(0).integers(0, 200, size=(600, 2)), 200)
+    feats = np.random.default_rng(1).normal(size=(200, 8)).astype(np.float32)
+    g = P.Graph.from_numpy(200, og.indptr, og.indices, features=feats)
+    kmax = int(np.diff(og.indptr).max())
+    cfg = P.SamplerConfig(strategy="NS", fanouts=(kmax, kmax), batch_size=200)
+    mb = P.build_minibatch(g, None, np.arange(200), cfg, P.BatchRng())
+    model = P.GraphSAGE((8, 16, 4), dtype=torch.float64)
+    logits = model.logits(mb, g).cpu().numpy()
+    w, b = model.export()
+    h = feats.astype(np.float64)
+    norm = np.maximum(np.diff(og.indptr), 1).astype(np.float64)
+    import scipy.sparse as sp
+    adj = sp.csr_matrix((np.ones(og.num_edges), og.indices, og.indptr), shape=(200, 200))
+    for li in range(2):
+        agg = (adj @ h) / norm[:, None]
+        z = np.concatenate([h, agg], 1) @ w[li] + b[li]
+        h = np.maximum(z, 0) if li == 0 else z
+    np.testing.assert_allclose(logits, h, rtol=1e-10, atol=1e-10)
+
+
+# ---- training parity ------------------------------------------------------------
+
+def test_training_loss_matches_reference_fp64(P, golden):
+    """6 reference steps (golden, fp64 numpy) vs the B200 fp64 mode; tolerance
+    1e-9 relative on every loss (GEMM summation order differs from BLAS)."""
+    gold = golden["model"]
+    n = len(gold["indptr"]) - 1
+    g = P.Graph.from_numpy(n, gold["indptr"], gold["indices"], features=gold["features"],
+                           labels=gold["labels"], train_mask=gold["train_mask"])
+    og = O.OGraph(num_nodes=n, indptr=gold["indptr"], indices=gold["indices"], train_mask=gold["train_mask"])
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(5, 3), batch_size=50, cache_frac=0.1, cache_mode="degree",
+                          seed=0)
+    cache = P.build_cache(g, P.degree_probs(g), 40, rng_seed=[0, 33, 0])
+    assert np.array_equal(cache.nodes.ids.cpu().numpy(), gold["cache_ids"])
+    model = P.GraphSAGE((16, 32, 4), dtype=torch.float64, seed=0)
+    tc = P.TrainConfig(lr=0.003)
+    batches = O.epoch_targets(og, 50, 0, 0)
+    losses = []
+    for index, targets in enumerate(batches[:6]):
+        mb = P.build_minibatch(g, cache, targets, cfg, P.BatchRng(0, 0, index))
+        losses.append(float(model.train_step(mb, g, tc)))
+    np.testing.assert_allclose(losses, gold["losses"], rtol=1e-9)
+    w, b = model.export()
+    for i in range(2):
+        np.testing.assert_allclose(w[i], gold[f"final_w{i}"], rtol=1e-7, atol=1e-10)
+        np.testing.assert_allclose(b[i], gold[f"final_b{i}"], rtol=1e-7, atol=1e-10)
+
+
+def test_training_fp32_tracks_fp64(P, golden):
+    gold = golden["model"]
+    n = len(gold["indptr"]) - 1
+    g = P.Graph.from_numpy(n, gold["indptr"], gold["indices"], features=gold["features"],
+                           labels=gold["labels"], train_mask=gold["train_mask"])
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(5, 3), batch_size=50, cache_frac=0.1, cache_mode="degree",
+                          seed=0)
+    pool = P.SamplerPool(g, cfg, num_workers=2)
+    model = P.GraphSAGE((16, 32, 4), dtype=torch.float32, seed=0)
+    tc = P.TrainConfig(lr=0.003)
+    losses = [float(model.train_step(it.minibatch, g, tc)) for it in pool.iter_epoch(0)]
+    np.testing.assert_allclose(losses[:6], gold["losses"], rtol=1e-3)
+
+
+# ---- statistics -------------------------------------------------------------------
+
+def test_neighbor_draw_inclusion_frequencies(P):
+    """Per-edge inclusion frequency vs the exact probabilities min(k,nc)/nc
+    (cached) and fill/rest (uncached) — sampling.py:287-295 — over T
+    independent Philox batches; per-edge |z| < 4.5 (Bonferroni)."""
+    og = O.build_csr(np.random.default_rng(5).integers(0, 60, size=(300, 2)), 60)
+    g = P.Graph.from_numpy(60, og.indptr, og.indices)
+    cache = P.build_cache(g, P.degree_probs(g), 12, rng_seed=[0, 33, 0])
+    mask = cache.nodes.mask.cpu().numpy()
+    seeds = np.arange(60)
+    T = 3000
+    k = 4
+    for cache_only in (False, True):
+        cfg = P.SamplerConfig(strategy="GNS", fanouts=(k,), batch_size=60, input_layer_cache_only=cache_only,
+                              cache_mode="degree")
+        counts = {}
+        for t in range(T):
+            mb = P.build_minibatch(g, cache, seeds, cfg, P.BatchRng(0, 0, t))
+            b = mb.blocks[0]
+            d = b.dst_nodes.cpu().numpy()[b.edge_dst.cpu().numpy()]
+            s = b.edge_node.cpu().numpy()
+            key = d.astype(np.int64) * 60 + s
+            for x in key:
+                counts[x] = counts.get(x, 0) + 1
+        zmax = 0.0
+        for v in range(60):
+            nb = og.indices[og.indptr[v]:og.indptr[v + 1]]
+            c_nb = nb[mask[nb]]
+            u_nb = nb[~mask[nb]]
+            m = min(k, len(c_nb))
+            fill = 0 if cache_only else min(k - m, len(u_nb))
+            for u in nb:
+                p = (m / len(c_nb)) if mask[u] else (fill / len(u_nb) if len(u_nb) else 0.0)
+                f = counts.get(v * 60 + u, 0)
+                if p in (0.0, 1.0):
+                    assert f == p * T, (v, u, p, f)
+                    continue
+                z = (f - T * p) / np.sqrt(T * p * (1 - p))
+                zmax = max(zmax, abs(z))
+        assert zmax < 4.5, zmax
+
+
+def test_cache_draw_distribution(P):
+    """|C| = 1: the draw is exactly p-proportional; chi-square over R epochs."""
+    og = O.build_csr(np.random.default_rng(7).integers(0, 40, size=(150, 2)), 40)
+    g = P.Graph.from_numpy(40, og.indptr, og.indices)
+    probs = P.degree_probs(g)
+    p = probs.weights.cpu().numpy()
+    R = 6000
+    hits = np.zeros(40)
+    for e in range(R):
+        hits[P.sample_cache(probs, 1, [0, 33, e]).ids.cpu().numpy()] += 1
+    sup = p > 0
+    exp = R * p[sup]
+    chi2 = float(((hits[sup] - exp) ** 2 / exp).sum())
+    dof = int(sup.sum()) - 1
+    from scipy.stats import chi2 as C
+    assert C.sf(chi2, dof) > 1e-3, (chi2, dof)
+    # |C| > 1: Spearman(frequency, degree) high
+    freq = np.zeros(40)
+    for e in range(1500):
+        freq[P.sample_cache(probs, 8, [1, 33, e]).ids.cpu().numpy()] += 1
+    from scipy.stats import spearmanr
+    assert spearmanr(freq[sup], p[sup]).correlation > 0.9
+
+
+# ---- device generator (graph.py:142-169 contract) ---------------------------------
+
+def test_device_generator_contract(P):
+    g = P.generate_powerlaw_device(20000, 150000, alpha=0.6, offset=50.0, seed=3, feature_dim=12,
+                                   num_classes=5, train_frac=0.5)
+    ip = g.indptr.cpu().numpy()
+    ix = g.indices.cpu().numpy().astype(np.int64)
+    n = g.num_nodes
+    assert ip[0] == 0 and ip[-1] == len(ix) and np.all(np.diff(ip) >= 0)
+    rows = np.repeat(np.arange(n), np.diff(ip))
+    assert not np.any(rows == ix), "self loop"
+    same = rows[1:] == rows[:-1]
+    assert not np.any(same & (np.diff(ix) <= 0)), "rows must be sorted + dedup"
+    keys = rows * n + ix
+    assert np.array_equal(keys, np.sort(ix * n + rows)), "symmetric"
+    deg = np.diff(ip)
+    assert deg.max() > 20 * max(deg.mean(), 1), "power-law tail"
+    assert g.features.shape == (n, 12) and g.feature_dim == 12
+    # determinism
+    g2 = P.generate_powerlaw_device(20000, 150000, alpha=0.6, offset=50.0, seed=3)
+    assert torch.equal(g.indices, g2.indices)

@@ -1,0 +1,78 @@
+"""CPU tests of the C-ABI boundary: libgns.so loads without a GPU, exports every
+symbol include/gns.h declares, and carries sm_100a code."""
+
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "gns.h")
+LIB = os.path.join(ROOT, "paper_2106_06150_b200", "libgns.so")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^GNS_API\s+[\w\s\*]+?\b(gns_\w+)\s*\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_2106_06150_b200 import build
+        build.build()
+    from paper_2106_06150_b200 import _lib
+    return _lib.load()
+
+
+def test_header_declares_api():
+    syms = declared_symbols()
+    assert "gns_sample_layer" in syms and "gns_cache_draw" in syms and len(syms) >= 25
+
+
+def test_every_declared_symbol_is_exported(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s+(gns_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    for s in declared_symbols():
+        assert hasattr(lib, s)
+
+
+def test_python_binding_covers_header():
+    from paper_2106_06150_b200 import _lib
+    assert sorted(_lib.EXPORTED) == declared_symbols()
+
+
+def test_workspace_queries_without_gpu(lib):
+    assert lib.gns_version() == 1
+    assert lib.gns_cache_draw_workspace_size(1000) > 8000
+    assert lib.gns_relabel_workspace_size(111_000_000) > 111_000_000 // 8
+    assert lib.gns_spmm_bwd_workspace_size(1000, 10000) > 80000
+    assert lib.gns_gen_workspace_size(1000, 5000) > 40000
+
+
+def test_error_mapping_without_gpu(lib):
+    from paper_2106_06150_b200 import _lib
+    g = _lib.GnsGraph(10, 0, None, None)
+    rc = lib.gns_degree_probs(g, None, None)
+    assert rc == _lib.GNS_EINVAL
+    assert b"no edges" in lib.gns_last_error()
+    with pytest.raises(ValueError):
+        _lib.check(rc)
+
+
+def test_sm100a_code_present():
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_product_path_has_no_oracle_import():
+    """The package must never route through the CPU oracle."""
+    pkg = os.path.join(ROOT, "paper_2106_06150_b200")
+    for f in os.listdir(pkg):
+        if f.endswith(".py"):
+            src = open(os.path.join(pkg, f)).read()
+            assert "import oracle" not in src and "from oracle" not in src, f

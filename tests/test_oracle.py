@@ -1,0 +1,209 @@
+"""CPU tests: the oracle against known answers, golden fixtures and (when the
+reference is mounted) the reference itself."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import detmath, philox
+from oracle import gns as O
+from oracle import model as OM
+
+from conftest import ROOT
+
+
+# ---- Philox / Feistel ----------------------------------------------------------
+
+@pytest.mark.parametrize("ctr,key,expect", [
+    ((0, 0, 0, 0), (0, 0), (0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8)),
+    ((0xffffffff,) * 4, (0xffffffff,) * 2, (0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd)),
+    ((0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344), (0xa4093822, 0x299f31d0),
+     (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1)),
+])
+def test_philox_kat(ctr, key, expect):
+    """Random123 kat_vectors for philox4x32-10."""
+    assert tuple(int(x) for x in philox.philox4x32_10(*ctr, *key)) == expect
+
+
+def test_uniform_is_key53_scaled():
+    k = philox.key53(1, 2, 3, philox.stream_word(32, 1, 0), 4, np.arange(100))
+    u = philox.uniform(1, 2, 3, philox.stream_word(32, 1, 0), 4, np.arange(100))
+    assert np.all(k < 2 ** 53)
+    assert np.array_equal(u, k.astype(np.float64) / 2.0 ** 53)
+    assert np.all((u >= 0) & (u < 1))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 1000, 4097])
+def test_feistel_is_bijection(n):
+    p = philox.feistel_permute(np.arange(n), n, 7, 3)
+    assert sorted(p.tolist()) == list(range(n))
+
+
+# ---- deterministic transcendental functions -------------------------------------
+
+def _ulps(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.max(np.abs(a - b) / np.spacing(np.maximum(np.abs(a), np.abs(b))))
+
+
+def test_detmath_close_to_libm():
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.random(50000), 10 ** -rng.uniform(0, 16, 50000), [1.0, 2 ** -53]])
+    x = x[x > 0]
+    assert _ulps(detmath.det_log(x), np.log(x)) <= 4
+    x1 = -np.concatenate([rng.random(50000), 10 ** -rng.uniform(0, 16, 50000), [0.999999999999999, .5]])
+    assert _ulps(detmath.det_log1p(x1), np.log1p(x1)) <= 4
+    y = -np.concatenate([rng.random(50000) * 50, 10 ** -rng.uniform(0, 16, 50000), [0.5, 40, 45]])
+    assert _ulps(detmath.det_expm1(y), np.expm1(y)) <= 4
+
+
+def test_cuda_constants_match_oracle():
+    """The .cuh coefficient tables are the oracle's correctly rounded values."""
+    src = open(os.path.join(ROOT, "paper_2106_06150_b200", "csrc", "gns_common.cuh")).read()
+
+    def table(name):
+        body = re.search(name + r"\[\d+\] = \{(.*?)\};", src, re.S).group(1)
+        return [float.fromhex(t.strip()) for t in body.split(",") if t.strip()]
+
+    assert table("kAtanhC") == detmath.ATANH_C
+    assert table("kExpC") == detmath.EXP_C
+    for name, val in [("GNS_LN2_HI", detmath.LN2_HI), ("GNS_LN2_LO", detmath.LN2_LO),
+                      ("GNS_INV_LN2", detmath.INV_LN2), ("GNS_SQRT_HALF", detmath.SQRT_HALF),
+                      ("GNS_ONE_MINUS_1EM15", detmath.ONE_MINUS_1EM15)]:
+        m = re.search(r"#define " + name + r" (\S+)", src)
+        assert float.fromhex(m.group(1)) == val, name
+
+
+# ---- KATs (SPEC.md examples) -----------------------------------------------------
+
+def test_spec_kats(golden):
+    kat = golden["kat"]
+    assert abs(detmath.inclusion_prob(0.01, 100) - 0.63397) < 1e-5
+    assert _ulps(detmath.inclusion_prob(0.01, 100), kat["inclusion_0p01_100"]) <= 4
+    star = O.build_csr([(0, 1), (0, 2), (0, 3)], 4)
+    assert np.array_equal(O.degree_probs(star), kat["star_probs"])
+    g = O.build_csr([(0, 1)], 2)
+    assert g.indptr.tolist() == [0, 1, 2] and g.indices.tolist() == [1, 0]
+    p = kat["incl_p"]
+    for cs in (1, 100, 111000):
+        assert _ulps(detmath.inclusion_prob(p, cs), kat[f"incl_ref_{cs}"]) <= 4
+
+
+def test_sample_cache_edge_cases():
+    w = np.array([0.0, 0.5, 0.25, 0.25])
+    assert O.sample_cache(w, 0).tolist() == []
+    assert O.sample_cache(w, 3).tolist() == [1, 2, 3]
+    assert O.sample_cache(w, 10).tolist() == [1, 2, 3]
+    assert len(O.sample_cache(w, 2, seed=5, epoch=1)) == 2
+
+
+# ---- oracle vs golden reference outputs -----------------------------------------
+
+def _graph_from(gold):
+    return O.OGraph(num_nodes=len(gold["indptr"]) - 1, indptr=gold["indptr"], indices=gold["indices"])
+
+
+def _cache_from(g, gold, ids):
+    mask = np.zeros(g.num_nodes, dtype=bool)
+    mask[ids] = True
+    return O.OCache(ids=ids, mask=mask, inclusion=gold["cache_inclusion_ref"],
+                    cached_indptr=gold["cached_indptr"], cached_indices=gold["cached_indices"])
+
+
+CASES = {"gns": dict(strategy="GNS", fanouts=(15, 10, 5), input_layer_cache_only=True, seed=0),
+         "gnsfill": dict(strategy="GNS", fanouts=(6, 4), input_layer_cache_only=False, seed=3),
+         "ns": dict(strategy="NS", fanouts=(15, 10, 5), input_layer_cache_only=True, seed=0)}
+
+
+class _Cfg:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def test_oracle_matches_golden_sampler(golden):
+    gold = golden["sampler"]
+    g = _graph_from(gold)
+    ids = gold["philox_cache_ids"]
+    assert np.array_equal(O.sample_cache(O.degree_probs(g), 40, seed=0, epoch=0), ids)
+    oc = O.build_cache(g, O.degree_probs(g), 40, ids=ids)
+    assert np.array_equal(oc.cached_indptr, gold["cached_indptr"])
+    assert np.array_equal(oc.cached_indices, gold["cached_indices"])
+    assert _ulps(oc.inclusion, gold["cache_inclusion_ref"]) <= 4
+    ci, cx = O.cached_csr_by_filter(g, oc.mask)
+    assert np.array_equal(ci, oc.cached_indptr) and np.array_equal(cx, oc.cached_indices)
+    cache = _cache_from(g, gold, ids)
+    for name, kw in CASES.items():
+        cfg = _Cfg(**kw)
+        for epoch, index in ((0, 0), (2, 5)):
+            mb = O.build_minibatch(g, cache if cfg.strategy == "GNS" else None, gold[f"{name}_targets"], cfg,
+                                   O.PhiloxKeys(cfg.seed, epoch, index))
+            pre = f"{name}_e{epoch}_i{index}"
+            assert len(mb.blocks) == int(gold[f"{pre}_nblocks"])
+            for i, b in enumerate(mb.blocks):
+                for f in ("dst_nodes", "src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached",
+                          "dst_degree"):
+                    assert np.array_equal(getattr(b, f), gold[f"{pre}_b{i}_{f}"]), (pre, i, f)
+            O.validate_minibatch(g, mb)
+
+
+def test_oracle_model_matches_golden(golden):
+    gold = golden["model"]
+    g = O.OGraph(num_nodes=len(gold["indptr"]) - 1, indptr=gold["indptr"], indices=gold["indices"],
+                 features=gold["features"], labels=gold["labels"], train_mask=gold["train_mask"])
+    w = O.degree_probs(g)
+    oc = O.build_cache(g, w, 40, ids=gold["cache_ids"])
+    cfg = _Cfg(strategy="GNS", fanouts=(5, 3), input_layer_cache_only=True, seed=0)
+    params = OM.init_params((16, 32, 4), seed=0)
+    st = OM.OAdam.zeros_like(params)
+    batches = O.epoch_targets(g, 50, 0, 0)
+    losses = []
+    for index, targets in enumerate(batches[:6]):
+        mb = O.build_minibatch(g, oc, targets, cfg, O.PhiloxKeys(0, 0, index))
+        losses.append(OM.train_step(mb, g.features, g.labels, params, st))
+    np.testing.assert_allclose(losses, gold["losses"], rtol=1e-12)
+
+
+# ---- oracle vs the live reference (build container only) -------------------------
+
+def test_oracle_numpy_stream_equals_reference(gb):
+    """With the reference's own PCG64 streams the restatement is bit-exact."""
+    g = gb.generate_powerlaw(3000, 4, 0)
+    cfg = gb.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=100, cache_frac=0.05,
+                           cache_mode="degree", seed=0)
+    probs = gb.degree_probs(g)
+    cs = O.cache_size_for(g, 0.05)
+    rc = gb.build_cache(g, probs, cs, epoch=0, rng_seed=[0, 33, 0])
+    oc = O.build_cache(g, O.degree_probs(g), cs, numpy_seed=[0, 33, 0])
+    assert np.array_equal(oc.ids, rc.nodes.ids)
+    assert np.array_equal(oc.cached_indptr, rc.cached_indptr)
+    assert np.array_equal(oc.cached_indices, rc.cached_indices)
+    oc_ref = O.OCache(ids=rc.nodes.ids, mask=rc.nodes.mask, inclusion=rc.inclusion,
+                      cached_indptr=rc.cached_indptr, cached_indices=rc.cached_indices)
+    batches = gb.pool.epoch_targets(g, cfg, 0)
+    ob = O.epoch_targets(g, 100, 0, 0, numpy_mode=True)
+    assert all(np.array_equal(a, b) for a, b in zip(batches, ob))
+    for idx in range(2):
+        mr = gb.build_minibatch(g, rc, batches[idx], cfg, np.random.default_rng([0, 32, 0, idx]))
+        mo = O.build_minibatch(g, oc_ref, batches[idx], cfg, O.NumpyStream(np.random.default_rng([0, 32, 0, idx])))
+        for ba, bb in zip(mr.blocks, mo.blocks):
+            for f in ("dst_nodes", "src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached", "dst_degree"):
+                assert np.array_equal(getattr(ba, f), getattr(bb, f)), f
+
+
+def test_oracle_model_equals_reference(gb):
+    g = gb.generate_sbm(300, 3, 0.05, 0.01, seed=2, feature_dim=8)
+    cfg = gb.SamplerConfig(strategy="NS", fanouts=(4, 3), batch_size=40, seed=0)
+    mb = gb.build_minibatch(g, None, np.arange(0, 300, 7), cfg, np.random.default_rng(0))
+    p_ref = gb.init_params((8, 16, 3), seed=0)
+    p_or = OM.init_params((8, 16, 3), seed=0)
+    lr, _ = OM.forward_pass(mb, g.features, p_or)
+    assert np.array_equal(lr, gb.forward(mb, g.features, p_ref))
+    loss, grad = OM.loss_and_grad(lr, g.labels[mb.targets])
+    loss_r, grad_r = gb.loss_and_grad(lr, g.labels[mb.targets])
+    assert loss == loss_r and np.array_equal(grad, grad_r)
+    dw, db = OM.backward(mb, g.features, p_or, grad)
+    gr = gb.backward(mb, g.features, p_ref, grad)
+    for a, b in zip(dw + db, gr.weights + gr.biases):
+        assert np.array_equal(a, b)
