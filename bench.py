@@ -1,0 +1,344 @@
+"""GNS mini-batch training throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config papers100m]
+                    [--impl ours|reference] [--no-cpu-baseline]
+
+One step = sample one mini-batch (3-layer GNS, fanouts 15,10,5, batch 1000,
+input layer cache-only) + gather its input features + one GraphSAGE training
+step (forward, loss, backward, Adam), on a synthetic power-law graph of the
+named shape generated on the device.  N>1: one process per GPU (torchrun),
+rank r takes batches r, r+W, ... (pool.py:80 striding), NCCL gradient
+all-reduce; time = max over ranks.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GNS mini-batches/sec (sample+gather+train) at 1/2/4/8 B200; gather HBM GB/s"
+UNIT = "mini-batches/s"
+
+CONFIGS = {
+    # name: nodes, undirected pairs drawn, feature dim, classes, train fraction, hidden, cache frac, alpha, offset
+    "cfg1": dict(label="synthetic power-law 100K nodes / 2M directed edges, 64-d (BASELINE configs[0])",
+                 nodes=100_000, pairs=1_000_000, dim=64, classes=16, train=0.5, hidden=64, cache=0.01,
+                 alpha=0.6, offset=10.0, cpu_batches=12),
+    "products": dict(label="ogbn-products-shaped synthetic: 2.4M nodes, ~124M directed edges, 100-d",
+                     nodes=2_400_000, pairs=62_000_000, dim=100, classes=47, train=0.10, hidden=256,
+                     cache=0.01, alpha=0.6, offset=30.0, cpu_batches=6),
+    "papers100m": dict(label="ogbn-papers100M-shaped synthetic: 111M nodes, ~3.2B directed edges, 128-d",
+                       nodes=111_000_000, pairs=1_615_000_000, dim=128, classes=172, train=0.01,
+                       hidden=256, cache=0.01, alpha=0.6, offset=300.0, cpu_batches=4),
+    "oag": dict(label="OAG-paper-shaped synthetic: 15M nodes, ~220M directed edges, 768-d",
+                nodes=15_000_000, pairs=110_000_000, dim=768, classes=146, train=0.43, hidden=256,
+                cache=0.01, alpha=0.6, offset=100.0, cpu_batches=4),
+}
+FANOUTS = (15, 10, 5)
+BATCH = 1000
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_graph(P, c, seed=0):
+    t0 = time.perf_counter()
+    g = P.generate_powerlaw_device(c["nodes"], c["pairs"], alpha=c["alpha"], offset=c["offset"], seed=seed,
+                                   feature_dim=c["dim"], num_classes=c["classes"], train_frac=c["train"])
+    torch.cuda.synchronize()
+    return g, time.perf_counter() - t0
+
+
+def batch_stream(pool, start_epoch=0):
+    epoch = start_epoch
+    while True:
+        n = 0
+        for item in pool.iter_epoch(epoch):
+            n += 1
+            yield item
+        if n == 0:
+            raise RuntimeError("empty epoch")
+        epoch += 1
+
+
+def host_graph(g):
+    """Reference-layout numpy copy of the device graph (CPU baseline input)."""
+    from oracle import gns as O
+    h = g.to_host()
+    return O.OGraph(num_nodes=h.num_nodes, indptr=h.indptr, indices=h.indices, features=h.features,
+                    labels=h.labels, train_mask=h.train_mask)
+
+
+def host_cache(cache, n):
+    from oracle import gns as O
+    ids = cache.nodes.ids.cpu().numpy().astype(np.int64)
+    mask = np.zeros(n, dtype=bool)
+    mask[ids] = True
+    return O.OCache(ids=ids, mask=mask, inclusion=cache.inclusion.cpu().numpy(),
+                    cached_indptr=cache.cached_indptr.cpu().numpy(),
+                    cached_indices=cache.cached_indices.cpu().numpy())
+
+
+def cpu_reference_run(P, g, c, cfg, cache, n_batches, warmup=1):
+    """The reference's CPU algorithm (oracle port: pool.py fork workers + the
+    float64 trainer loop body) on this host's cores."""
+    from oracle import cpu_pipeline, gns as O
+    og = host_graph(g)
+    oc = host_cache(cache, g.num_nodes) if cache is not None else None
+    batches = O.epoch_targets(og, cfg.batch_size, cfg.seed, 0, numpy_mode=True)
+    batches = batches[:n_batches + warmup]
+    dims = (c["dim"], c["hidden"], c["hidden"], c["classes"])
+    r = cpu_pipeline.run(og, oc, cfg, dims, batches, epoch=0, warmup=warmup)
+    r["cores"] = r["workers"] + 1
+    return r
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=os.environ.get("GNS_BENCH_CONFIG", "papers100m"), choices=list(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--workers", type=int, default=2, help="sampling slots in flight (SamplerPool num_workers)")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    c = CONFIGS[args.config]
+
+    if args.impl == "reference" and rank != 0:
+        return
+    import paper_2106_06150_b200 as P
+    from paper_2106_06150_b200 import _lib
+
+    torch.cuda.set_device(local)
+    if world > 1 and args.impl == "ours":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    g, gen_s = make_graph(P, c, seed=0)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=FANOUTS, batch_size=BATCH, cache_frac=c["cache"],
+                          cache_mode="degree", input_layer_cache_only=True, seed=0)
+    dims = (c["dim"], c["hidden"], c["hidden"], c["classes"])
+    config = {"workload": c["label"], "config": args.config, "nodes": g.num_nodes, "edges": g.num_edges,
+              "feature_dim": c["dim"], "fanouts": list(FANOUTS), "global_batch": BATCH * world,
+              "cache_frac": c["cache"], "cache_mode": "degree", "hidden": c["hidden"],
+              "classes": c["classes"], "parallelism": f"dp{world}",
+              "l2": "inputs larger than L2 (feature table + CSR >> 126 MB); no flush",
+              "graph_gen_s": round(gen_s, 2)}
+
+    if args.impl == "reference":
+        pool = P.SamplerPool(g, cfg)
+        pool._refresh_cache(0)
+        n = max(1, min(args.steps, c["cpu_batches"] * 2))
+        r = cpu_reference_run(P, g, c, cfg, pool.cache, n, warmup=min(args.warmup, 1))
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+               "sample": f"{r['steps']} mini-batches of the same workload (epoch 0), oracle port of pool.py "
+                         f"fork workers ({r['workers']}) + float64 trainer loop body; "
+                         f"sample {r['sample_ms']:.0f} ms/batch/worker, train {r['train_ms']:.0f} ms/batch"}
+        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
+                "steps": r["steps"], "warmup": 1, "ms_per_step": 1e3 / r["value"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "cpu_baseline": cpu,
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    model = P.GraphSAGE(dims, dtype=torch.float32, seed=0)
+    tc = P.TrainConfig(lr=0.003, hidden_dim=c["hidden"])
+    pool = P.SamplerPool(g, cfg, num_workers=args.workers, rank=rank, world_size=world)
+
+    def allreduce(grad):
+        dist.all_reduce(grad)
+        return 1.0 / world
+
+    ar = allreduce if world > 1 else None
+    it = batch_stream(pool)
+    ev_pairs = []
+
+    def step(timed):
+        item = next(it)
+        mb = item.minibatch
+        if timed:
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+        h = model.gather_inputs(mb, g)
+        if timed:
+            e1.record()
+        logits, saved = model.forward(mb, h)
+        if timed:
+            e2.record()
+            ev_pairs.append((e0, e1, e2, mb.input_nodes.numel(),
+                             sum(b.num_edges for b in mb.blocks), mb.blocks[0].dst_nodes.numel()))
+        dl = model.loss_and_grad(logits, g.labels, mb)
+        model.backward(mb, saved, dl)
+        scale = ar(model.grad) if ar else 1.0
+        model.adam_step(tc, grad_scale=scale)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = _lib.launch_counter[0]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for _ in range(args.steps):
+        step(True)
+    t_end.record()
+    t_end.synchronize()
+    launches = _lib.launch_counter[0] - l0
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = args.steps * world / (ms / 1e3)
+
+    # gather roofline (algorithmic bytes: rows read + rows written + ids)
+    peak, peak_kind = load_peaks()
+    gather_ms = [a.elapsed_time(b) for a, b, _, _, _, _ in ev_pairs]
+    fwd_ms = [b.elapsed_time(cc) for _, b, cc, _, _, _ in ev_pairs]
+    n_in = np.array([p[3] for p in ev_pairs], dtype=np.float64)
+    row_bytes = 4 * c["dim"]
+    gbytes = n_in * (2 * row_bytes + 4)
+    gather_gbs = float(gbytes.sum() / (np.sum(gather_ms) / 1e3) / 1e9)
+    roofline = {"kernel": "gns_gather_rows (gather_f32x4_kernel)", "bound": "hbm",
+                "achieved": round(gather_gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": round(gather_gbs / peak, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": float(gbytes.mean()),
+                "avg_launch_ms": float(np.mean(gather_ms)),
+                "share_of_step": float(np.sum(gather_ms) / ms)}
+    prof_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof_path):
+        try:
+            tr = json.load(open(prof_path)).get(args.config, {}).get("gather_f32x4_kernel")
+            roofline["traffic"] = tr
+        except Exception:
+            pass
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if rank == 0 and world == 1:
+        k2 = args.e2e_steps if args.e2e_steps is not None else max(5, args.steps // 2)
+        ids_host = g.train_ids().cpu().numpy().astype(np.int64)
+        perm = np.random.default_rng(1).permutation(ids_host)
+        tgt = torch.empty(BATCH, dtype=torch.int64).pin_memory()
+        eng = P.MiniBatchSampler(g, cfg)
+        cache = pool.cache
+        lossh = torch.empty(1, dtype=torch.float64).pin_memory()
+        for i in range(2):
+            tgt.copy_(torch.from_numpy(perm[i * BATCH:(i + 1) * BATCH]))
+            mb = eng.sample(tgt.to("cuda", non_blocking=True), P.BatchRng(0, 99, i), cache)
+            lossh.copy_(model.train_step(mb, g, tc))
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for i in range(k2):
+            j = (i + 2) % (len(perm) // BATCH)
+            tgt.copy_(torch.from_numpy(perm[j * BATCH:(j + 1) * BATCH]))
+            mb = eng.sample(tgt.to("cuda", non_blocking=True), P.BatchRng(0, 99, i + 2), cache)
+            lossh.copy_(model.train_step(mb, g, tc))
+            float(lossh[0])
+        s1.record()
+        s1.synchronize()
+        e_ms = s0.elapsed_time(s1)
+        e2e = {"value": k2 / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": BATCH * 8,
+               "d2h_bytes_per_step": 8 + 4 * 8 * len(FANOUTS), "steps": k2,
+               "path": "MiniBatchSampler.sample(host int64 targets) + GraphSAGE.train_step + loss.item()"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_run(P, g, c, cfg, pool.cache, c["cpu_batches"])
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+               "sample": f"{r['steps']} mini-batches of this workload (epoch 0, after 1 warm-up), oracle port "
+                         f"of pool.py fork workers ({r['workers']}) + float64 trainer loop body; sample "
+                         f"{r['sample_ms']:.0f} ms/batch/worker, train {r['train_ms']:.0f} ms/batch"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "gpu_launches_per_step": launches / args.steps, "clocks": clk,
+                "per_step": {"input_nodes": float(n_in.mean()),
+                             "sampled_edges": float(np.mean([p[4] for p in ev_pairs])),
+                             "gather_ms": float(np.mean(gather_ms)), "fwd_ms": float(np.mean(fwd_ms))}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -27,6 +27,16 @@ import gnsbench as gb  # noqa: E402
 from oracle import gns as O  # noqa: E402
 
 
+def _with_det_inclusion(gb, cache, w):
+    from oracle import detmath
+    incl = detmath.inclusion_prob(w, len(cache.nodes))
+    if len(cache.nodes) >= int((w > 0).sum()):
+        incl = np.where(w > 0, 1.0, incl)
+    return gb.CacheState(nodes=cache.nodes, inclusion=np.asarray(incl, dtype=np.float64),
+                         cached_indptr=cache.cached_indptr, cached_indices=cache.cached_indices,
+                         epoch=cache.epoch, source_probs=cache.source_probs)
+
+
 def _block_arrays(prefix, mb, out):
     for i, b in enumerate(mb.blocks):
         for f in ("dst_nodes", "src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached",
@@ -55,6 +65,10 @@ def make_sampler_golden():
     finally:
         gb.cache.sample_cache = orig
     out["cache_inclusion_ref"] = cache.inclusion
+    # "bit-exact given the same inclusion vector": the reference samples with the
+    # build's Eq. 9 values (libm vs the deterministic series differ by <= 4 ulp)
+    cache = _with_det_inclusion(gb, cache, w)
+    out["cache_inclusion_det"] = cache.inclusion
     out["cached_indptr"] = cache.cached_indptr
     out["cached_indices"] = cache.cached_indices
     oc = O.OCache(ids=cache.nodes.ids, mask=cache.nodes.mask, inclusion=cache.inclusion,
@@ -113,6 +127,7 @@ def make_model_golden():
         cache = gb.build_cache(g, probs, cs, epoch=0, rng_seed=[0, 33, 0])
     finally:
         gb.cache.sample_cache = orig
+    cache = _with_det_inclusion(gb, cache, w)
     oc = O.OCache(ids=cache.nodes.ids, mask=cache.nodes.mask, inclusion=cache.inclusion,
                   cached_indptr=cache.cached_indptr, cached_indices=cache.cached_indices)
     dims = (16, 32, 4)
