@@ -226,6 +226,15 @@ GNS_API int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32
                  int64_t max_edges, void* dh, int64_t ld_dh, void* ws,
                  size_t ws_bytes, void* stream);
 
+/* relu backward fused with the bias gradient (model.py:218,220):
+ * dz = (z > 0) ? dh : 0 (skipped when z == NULL: the output layer), db[c] =
+ * sum over rows of dz[:, c] in a fixed order (deterministic).  n = *n_dev if
+ * n_dev else n_rows; dh, z, dz share the row stride ld. */
+GNS_API size_t gns_dense_bwd_workspace_size(int64_t max_rows, int32_t ncols);
+GNS_API int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int64_t ld,
+                               const int32_t* n_dev, int64_t n_rows, int32_t ncols, void* dz,
+                               void* db, void* ws, size_t ws_bytes, void* stream);
+
 /* Softmax cross-entropy (model.py:189-200) over rows of logits for the
  * sorted targets; labels gathered as labels[targets[r]].  Writes grad_out
  * (same layout) and loss_out[0] = mean loss (device, float64). */

@@ -143,7 +143,7 @@ __host__ static inline BlockView view_of(const gns_block_t* b) {
 
 // one warp per dst row: sort the row's (<= k) edges by src index (the scipy
 // CSR order, model.py:133-135), then cat[r] = [h[self], sum w*h[src] / norm]
-template <typename T>
+template <typename T, int CH>
 __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restrict__ h, int64_t ld_h, int dim,
                                                               BlockView bv, T* __restrict__ cat, int64_t ld_cat) {
   using V = typename Vec<T>::type;
@@ -207,22 +207,41 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
     const V* hs = reinterpret_cast<const V*>(h + (int64_t)bv.self_pos[r] * ld_h);
     V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
     for (int c = lane; c < dv; c += 32) crow[c] = hs[c];
-    for (int c = lane; c < dv; c += 32) {
-      V acc;
-      vzero(acc);
+    for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
+      V acc[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) vzero(acc[j]);
       int t = 0;
-      for (; t + 4 <= L; t += 4) {
-        V x0 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t] * ld_h)[c];
-        V x1 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t + 1] * ld_h)[c];
-        V x2 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t + 2] * ld_h)[c];
-        V x3 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t + 3] * ld_h)[c];
-        vfma<true>(acc, s_w[wib][t], x0);
-        vfma<true>(acc, s_w[wib][t + 1], x1);
-        vfma<true>(acc, s_w[wib][t + 2], x2);
-        vfma<true>(acc, s_w[wib][t + 3], x3);
+      for (; t + 2 <= L; t += 2) {
+        const V* r0 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t] * ld_h);
+        const V* r1 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t + 1] * ld_h);
+        const T w0 = s_w[wib][t], w1 = s_w[wib][t + 1];
+        V x0[CH], x1[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int c = c0 + lane + 32 * j;
+          if (c < dv) { x0[j] = r0[c]; x1[j] = r1[c]; }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          vfma<true>(acc[j], w0, x0[j]);
+          vfma<true>(acc[j], w1, x1[j]);
+        }
       }
-      for (; t < L; ++t) vfma<true>(acc, s_w[wib][t], reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t] * ld_h)[c]);
-      crow[dv + c] = vdiv(acc, norm);
+      if (t < L) {
+        const V* r0 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t] * ld_h);
+        const T w0 = s_w[wib][t];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int c = c0 + lane + 32 * j;
+          if (c < dv) vfma<true>(acc[j], w0, r0[c]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = c0 + lane + 32 * j;
+        if (c < dv) crow[dv + c] = vdiv(acc[j], norm);
+      }
     }
     __syncwarp();
   }
@@ -309,7 +328,7 @@ __device__ __forceinline__ T div_norm(T x, T d);
 template <> __device__ __forceinline__ float div_norm<float, false>(float x, float d) { return __fdiv_rn(x, d); }
 template <> __device__ __forceinline__ double div_norm<double, true>(double x, double d) { return DDIV(x, d); }
 
-template <typename T>
+template <typename T, int CH>
 __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restrict__ dcat, int64_t ld_dcat, int dim,
                                                               BlockView bv, const int32_t* __restrict__ tptr,
                                                               const uint64_t* __restrict__ tkeys,
@@ -326,40 +345,102 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
   for (int64_t s = gw; s < n; s += nw) {
     const int b = tptr[s], e_end = tptr[s + 1];
     const int sd = self_of[s];
-    for (int c = lane; c < dv; c += 32) {
-      T acc[VW];
+    for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
+      T acc[CH][VW];
 #pragma unroll
-      for (int q = 0; q < VW; ++q) acc[q] = (T)0;
+      for (int j = 0; j < CH; ++j)
+#pragma unroll
+        for (int q = 0; q < VW; ++q) acc[j][q] = (T)0;
+      // transposed row in ascending dst order (csc_matvecs order, model.py:224)
       for (int t = b; t < e_end; ++t) {
         const uint64_t key = tkeys[t];
         const int32_t d = (int32_t)(key >> 32), e = (int32_t)(key & 0xffffffffu);
         const T w = (T)bv.edge_weight[e];
         const T nrm = (T)max(bv.dst_degree[d], 1);
-        V g = reinterpret_cast<const V*>(dcat + (int64_t)d * ld_dcat + dim)[c];
-        const T* gp = reinterpret_cast<const T*>(&g);
+        const V* grow = reinterpret_cast<const V*>(dcat + (int64_t)d * ld_dcat + dim);
+        V g[CH];
 #pragma unroll
-        for (int q = 0; q < VW; ++q) {
-          T y = div_norm<T, EXACT>(gp[q], nrm);
-          if constexpr (EXACT) acc[q] = DADD(acc[q], DMUL(w, y));
-          else acc[q] = fmaf(w, y, acc[q]);
+        for (int j = 0; j < CH; ++j) {
+          const int c = c0 + lane + 32 * j;
+          if (c < dv) g[j] = grow[c];
+        }
+        if constexpr (EXACT) {
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const T* gp = reinterpret_cast<const T*>(&g[j]);
+#pragma unroll
+            for (int q = 0; q < VW; ++q) acc[j][q] = DADD(acc[j][q], DMUL(w, DDIV(gp[q], nrm)));
+          }
+        } else {
+          const T wn = w / nrm;
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const T* gp = reinterpret_cast<const T*>(&g[j]);
+#pragma unroll
+            for (int q = 0; q < VW; ++q) acc[j][q] = fmaf(wn, gp[q], acc[j][q]);
+          }
         }
       }
-      if (sd >= 0) {
-        V g = reinterpret_cast<const V*>(dcat + (int64_t)sd * ld_dcat)[c];
-        const T* gp = reinterpret_cast<const T*>(&g);
+      const V* srow = sd >= 0 ? reinterpret_cast<const V*>(dcat + (int64_t)sd * ld_dcat) : nullptr;
 #pragma unroll
-        for (int q = 0; q < VW; ++q) {
-          if constexpr (EXACT) acc[q] = DADD(acc[q], gp[q]);
-          else acc[q] = acc[q] + gp[q];
+      for (int j = 0; j < CH; ++j) {
+        const int c = c0 + lane + 32 * j;
+        if (c >= dv) continue;
+        if (srow) {
+          V g = srow[c];
+          const T* gp = reinterpret_cast<const T*>(&g);
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            if constexpr (EXACT) acc[j][q] = DADD(acc[j][q], gp[q]);
+            else acc[j][q] = acc[j][q] + gp[q];
+          }
         }
-      }
-      V out;
-      T* op = reinterpret_cast<T*>(&out);
+        V out;
+        T* op = reinterpret_cast<T*>(&out);
 #pragma unroll
-      for (int q = 0; q < VW; ++q) op[q] = acc[q];
-      reinterpret_cast<V*>(dh + s * ld_dh)[c] = out;
+        for (int q = 0; q < VW; ++q) op[q] = acc[j][q];
+        reinterpret_cast<V*>(dh + s * ld_dh)[c] = out;
+      }
     }
   }
+}
+
+// dz = relu'(z) * dh (model.py:218) fused with the bias gradient db = sum_r dz
+// (model.py:220): per-block column partials, then a fixed-order reduction.
+template <typename T>
+__global__ void dense_bwd_partial_kernel(const T* __restrict__ dh, const T* __restrict__ z, int64_t ld,
+                                         const int32_t* __restrict__ n_dev, int64_t n_host, int ncols,
+                                         T* __restrict__ dz, T* __restrict__ partial, int rows_per_block) {
+  __shared__ T red[4][64];
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  const int c = blockIdx.y * 64 + tx;
+  const int64_t n = n_dev ? n_dev[0] : n_host;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(n, r0 + rows_per_block);
+  T sum = 0;
+  if (c < ncols) {
+    for (int64_t r = r0 + ty; r < r1; r += 4) {
+      T v = dh[r * ld + c];
+      if (z) {
+        v = z[r * ld + c] > (T)0 ? v : (T)0;
+        dz[r * ld + c] = v;
+      }
+      sum += v;
+    }
+  }
+  red[ty][tx] = sum;
+  __syncthreads();
+  if (ty == 0 && c < ncols)
+    partial[(int64_t)blockIdx.x * ncols + c] = (red[0][tx] + red[1][tx]) + (red[2][tx] + red[3][tx]);
+}
+
+template <typename T>
+__global__ void colsum_final_kernel(const T* __restrict__ partial, int nblocks, int ncols, T* __restrict__ db) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  T s = 0;
+  for (int b = 0; b < nblocks; ++b) s += partial[(int64_t)b * ncols + c];
+  db[c] = s;
 }
 
 struct BwdWs {
@@ -524,13 +605,25 @@ int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, const 
       set_error("spmm_fwd(f32): dim/strides must be multiples of 4");
       return GNS_EINVAL;
     }
-    spmm_fwd_kernel<float><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv, (float*)cat, ld_cat);
+    const int dv = dim / 4;
+    if (dv <= 32)
+      spmm_fwd_kernel<float, 1><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv, (float*)cat, ld_cat);
+    else if (dv <= 64)
+      spmm_fwd_kernel<float, 2><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv, (float*)cat, ld_cat);
+    else
+      spmm_fwd_kernel<float, 4><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv, (float*)cat, ld_cat);
   } else {
     if (dim % 2 || ld_h % 2 || ld_cat % 2) {
       set_error("spmm_fwd(f64): dim/strides must be even");
       return GNS_EINVAL;
     }
-    spmm_fwd_kernel<double><<<grid, kSpmmBlock, 0, stream>>>((const double*)h, ld_h, dim, bv, (double*)cat, ld_cat);
+    const int dv = dim / 2;
+    if (dv <= 32)
+      spmm_fwd_kernel<double, 1><<<grid, kSpmmBlock, 0, stream>>>((const double*)h, ld_h, dim, bv, (double*)cat,
+                                                                  ld_cat);
+    else
+      spmm_fwd_kernel<double, 2><<<grid, kSpmmBlock, 0, stream>>>((const double*)h, ld_h, dim, bv, (double*)cat,
+                                                                  ld_cat);
   }
   return check_launch("spmm_fwd");
 }
@@ -567,13 +660,53 @@ int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, 
   int g2 = grid_for((max_src * 32 + 255) / 256, (long long)sms * 8);
   tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys);
   GNS_TRY(check_launch("spmm_bwd transpose"));
-  if (dtype == 0)
-    spmm_bwd_kernel<float><<<g2, kSpmmBlock, 0, stream>>>((const float*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,
-                                                          w.self_of, (float*)dh, ld_dh);
-  else
-    spmm_bwd_kernel<double><<<g2, kSpmmBlock, 0, stream>>>((const double*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,
-                                                           w.self_of, (double*)dh, ld_dh);
+  const int dv = dim / VW;
+#define GNS_BWD(T, CH)                                                                                       \
+  spmm_bwd_kernel<T, CH><<<g2, kSpmmBlock, 0, stream>>>((const T*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys, \
+                                                        w.self_of, (T*)dh, ld_dh)
+  if (dtype == 0) {
+    if (dv <= 32) GNS_BWD(float, 1);
+    else if (dv <= 64) GNS_BWD(float, 2);
+    else GNS_BWD(float, 4);
+  } else {
+    if (dv <= 32) GNS_BWD(double, 1);
+    else if (dv <= 64) GNS_BWD(double, 2);
+    else GNS_BWD(double, 4);
+  }
+#undef GNS_BWD
   return check_launch("spmm_bwd");
+}
+
+size_t gns_dense_bwd_workspace_size(int64_t max_rows, int32_t ncols) {
+  return (size_t)((max_rows + 127) / 128 + 1) * (size_t)ncols * 8 + 256;
+}
+
+int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int64_t ld, const int32_t* n_dev,
+                       int64_t n_rows, int32_t ncols, void* dz, void* db, void* ws, size_t ws_bytes,
+                       void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int rpb = 128;
+  const int nblocks = (int)((n_rows + rpb - 1) / rpb);
+  if (ws_bytes < gns_dense_bwd_workspace_size(n_rows, ncols)) {
+    set_error("dense_bwd_bias: workspace too small");
+    return GNS_EINVAL;
+  }
+  if (nblocks == 0) {
+    GNS_CUDA(cudaMemsetAsync(db, 0, (size_t)ncols * (dtype == 0 ? 4 : 8), stream));
+    return GNS_OK;
+  }
+  dim3 grid(nblocks, (ncols + 63) / 64);
+  if (dtype == 0) {
+    dense_bwd_partial_kernel<float><<<grid, 256, 0, stream>>>((const float*)dh, (const float*)z, ld, n_dev, n_rows,
+                                                              ncols, (float*)dz, (float*)ws, rpb);
+    colsum_final_kernel<float><<<(ncols + 127) / 128, 128, 0, stream>>>((const float*)ws, nblocks, ncols, (float*)db);
+  } else {
+    dense_bwd_partial_kernel<double><<<grid, 256, 0, stream>>>((const double*)dh, (const double*)z, ld, n_dev,
+                                                               n_rows, ncols, (double*)dz, (double*)ws, rpb);
+    colsum_final_kernel<double><<<(ncols + 127) / 128, 128, 0, stream>>>((const double*)ws, nblocks, ncols,
+                                                                        (double*)db);
+  }
+  return check_launch("dense_bwd_bias");
 }
 
 int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, const int32_t* n_dev, int64_t max_rows,

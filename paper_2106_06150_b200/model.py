@@ -63,11 +63,29 @@ def _dt(dtype) -> int:
     return 0 if dtype == torch.float32 else 1
 
 
+class _TF32:
+    """Scoped torch.backends.cuda.matmul.allow_tf32."""
+
+    def __init__(self, on: bool):
+        self.on = on
+
+    def __enter__(self):
+        self.prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = self.on
+
+    def __exit__(self, *exc):
+        torch.backends.cuda.matmul.allow_tf32 = self.prev
+
+
 class GraphSAGE:
     """Flat-buffer GraphSAGE with a manual forward/backward (model.py:141-226)."""
 
-    def __init__(self, dims, dtype=torch.float32, device=None, seed: int = 0, weights=None, biases=None):
+    def __init__(self, dims, dtype=torch.float32, device=None, seed: int = 0, weights=None, biases=None,
+                 tf32: bool = True):
         _lib.require_cuda()
+        # float32 mode runs the linear layers on tensor cores (TF32, 10-bit
+        # mantissa); float64 mode is the reference-parity path
+        self.tf32 = bool(tf32) and dtype == torch.float32
         self.dims = tuple(int(d) for d in dims)
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -95,6 +113,7 @@ class GraphSAGE:
         self.load(weights, biases)
         self._ws_bwd = None
         self._ws_xent = None
+        self._ws_dense = None
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
 
     @property
@@ -124,8 +143,15 @@ class GraphSAGE:
                   _lib.stream_ptr(stream))
         return h[:n]
 
+    def _tf32(self):
+        return _TF32(self.tf32)
+
     def forward(self, mb: MiniBatch, h: torch.Tensor, stream=None):
         """Layer chain (model.py:141-159); returns logits and saved tensors."""
+        with self._tf32():
+            return self._forward(mb, h, stream)
+
+    def _forward(self, mb, h, stream):
         s = _lib.stream_ptr(stream)
         saved = []
         L = self.num_layers
@@ -158,14 +184,30 @@ class GraphSAGE:
         """model.py:209-226 into the flat gradient buffer.  The input layer's
         dh is not formed (features are not trainable; the reference computes
         and discards it)."""
+        with self._tf32():
+            self._backward(mb, saved, dlogits, stream)
+
+    def _backward(self, mb, saved, dlogits, stream):
         s = _lib.stream_ptr(stream)
         dh = dlogits
         L = self.num_layers
         for li in range(L - 1, -1, -1):
             cat, z = saved[li]
-            dz = dh if li == L - 1 else torch.ops.aten.threshold_backward(dh, z, 0)
+            n, d_out = dh.shape
+            need = _lib.lib().gns_dense_bwd_workspace_size(max(n, 1), d_out)
+            if self._ws_dense is None or self._ws_dense.numel() < need:
+                self._ws_dense = _lib.workspace(int(need * 1.5), self.device)
+            if li == L - 1:
+                dz = dh
+                _lib.call("gns_dense_bwd_bias", _dt(self.dtype), dh.data_ptr(), None, dh.stride(0), None, n,
+                          d_out, None, self.gbiases[li].data_ptr(), self._ws_dense.data_ptr(),
+                          self._ws_dense.numel(), s)
+            else:
+                dz = torch.empty_like(dh)
+                _lib.call("gns_dense_bwd_bias", _dt(self.dtype), dh.data_ptr(), z.data_ptr(), dh.stride(0), None,
+                          n, d_out, dz.data_ptr(), self.gbiases[li].data_ptr(), self._ws_dense.data_ptr(),
+                          self._ws_dense.numel(), s)
             torch.mm(cat.t(), dz, out=self.gweights[li])
-            torch.sum(dz, dim=0, out=self.gbiases[li])
             if li == 0:
                 break
             dcat = torch.mm(dz, self.weights[li].t())
