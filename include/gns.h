@@ -57,6 +57,7 @@ extern "C" {
 #define GNS_CNT_SRC 3      /* unique src nodes after relabel                */
 #define GNS_CNT_HUBS 4     /* rows routed to the CTA-per-row sampler        */
 #define GNS_CNT_ERR 5      /* GNS_ERRBIT_* flags                             */
+#define GNS_CNT_WARPROWS 6 /* rows routed to the warp-per-row sampler        */
 #define GNS_CNT_N 8
 
 /* CSR graph (graph.py:52-104): indptr int64[N+1], indices int32[E]. */
@@ -91,7 +92,7 @@ typedef struct gns_block {
   uint64_t* row_scan;      /* exclusive scan, packed (cached_prefix<<32 | fill_prefix); [n] = totals */
   int32_t* dst_degree;     /* deg(dst) (sampling.py:149)                              */
   int32_t* self_pos;       /* searchsorted(src_nodes, dst_nodes) (model.py:137)       */
-  int32_t* hub_rows;       /* rows handled by the CTA-per-row kernel                   */
+  int32_t* hub_rows;       /* tier lists: warp-per-row rows from the front, CTA-per-row rows from the back */
   /* per edge, capacity max_edges; order = cached edges then fill edges, each by (dst row, key) */
   int32_t* edge_node;      /* global id of the sampled neighbour                       */
   int32_t* edge_src;       /* relabelled: index into src_nodes (sampling.py:145)       */
@@ -208,13 +209,17 @@ GNS_API int gns_bitmap_rank(const uint32_t* bits, int64_t nwords, int32_t* out_r
                     void* ws, size_t ws_bytes, void* stream);
 
 /* Weighted mean aggregation + self concat (model.py:131-138,153-154):
- * cat[r, 0:D]  = h[self_pos[r], :]
- * cat[r, D:2D] = (sum_e w_e * h[edge_src_e, :]) / max(deg(r), 1)
- * accumulated in ascending edge_src order (scipy CSR order).  dtype 0 =
- * float32 (production), 1 = float64 bit-exact vs scipy (no FMA). */
-GNS_API int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim,
-                 const gns_block_t* block, int64_t max_dst, void* cat, int64_t ld_cat,
-                 void* stream);
+ * cat[r, 0:D]  = x(h[self_pos[r], :])
+ * cat[r, D:2D] = (sum_e w_e * x(h[edge_src_e, :])) / max(deg(r), 1)
+ * accumulated in ascending edge_src order (scipy CSR order); x = relu when
+ * flags & GNS_SPMM_RELU_INPUT (h holds the previous layer's pre-activations,
+ * model.py:156), identity otherwise.  Rows [n_dst, pad_rows) of cat are
+ * zero-filled.  dtype 0 = float32 (production), 1 = float64 bit-exact vs
+ * scipy (no FMA). */
+#define GNS_SPMM_RELU_INPUT 1
+GNS_API int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_t flags,
+                         const gns_block_t* block, int64_t max_dst, int64_t pad_rows, void* cat,
+                         int64_t ld_cat, void* stream);
 
 /* Backward of the above (model.py:223-225):
  * dh[s,:] = sum_{e: src=s, ascending dst} w_e * (dcat[dst_e, D:2D] / max(deg,1))

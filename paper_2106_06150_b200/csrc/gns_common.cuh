@@ -297,6 +297,7 @@ __device__ __forceinline__ void scan_tiles(ScanStatus st, long long n, Loader lo
                                            Totaler tot) {
   constexpr int TILE = BLOCK * ITEMS;
   __shared__ unsigned long long s_warp[BLOCK / 32 + 1];
+  __shared__ unsigned long long s_items[TILE + TILE / 32];
   __shared__ int s_tile;
   __shared__ unsigned long long s_prefix;
   const long long ntiles = (n + TILE - 1) / TILE;
@@ -307,13 +308,22 @@ __device__ __forceinline__ void scan_tiles(ScanStatus st, long long n, Loader lo
     if (n == 0 && tile == 0 && threadIdx.x == 0) tot(0ull);
     return;
   }
-  const long long base = (long long)tile * TILE + (long long)threadIdx.x * ITEMS;
+  // striped (coalesced) loads -> shared memory -> blocked per-thread items
+  const long long tbase = (long long)tile * TILE;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int li = j * BLOCK + threadIdx.x;
+    const long long i = tbase + li;
+    s_items[li + (li >> 5)] = (i < n) ? load(i) : 0ull;
+  }
+  __syncthreads();
+  const long long base = tbase + (long long)threadIdx.x * ITEMS;
   unsigned long long vals[ITEMS];
   unsigned long long tsum = 0;
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
-    long long i = base + j;
-    vals[j] = (i < n) ? load(i) : 0ull;
+    const int li = threadIdx.x * ITEMS + j;
+    vals[j] = s_items[li + (li >> 5)];
     tsum += vals[j];
   }
   unsigned long long block_total;

@@ -143,9 +143,25 @@ __host__ static inline BlockView view_of(const gns_block_t* b) {
 
 // one warp per dst row: sort the row's (<= k) edges by src index (the scipy
 // CSR order, model.py:133-135), then cat[r] = [h[self], sum w*h[src] / norm]
-template <typename T, int CH>
+__device__ __forceinline__ float4 vrelu(float4 v) {
+  return make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+}
+__device__ __forceinline__ double2 vrelu(double2 v) { return make_double2(fmax(v.x, 0.0), fmax(v.y, 0.0)); }
+
+template <typename V, bool RELU>
+__device__ __forceinline__ V ldv(const V* p) {
+  V v = *p;
+  if constexpr (RELU) v = vrelu(v);
+  return v;
+}
+
+// RELU: the input rows are the previous layer's pre-activations z and
+// relu(z) (model.py:156) is applied on load instead of being materialised.
+// Rows [n, pad_rows) of cat are zero-filled (static-capacity GEMMs).
+template <typename T, int CH, bool RELU>
 __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restrict__ h, int64_t ld_h, int dim,
-                                                              BlockView bv, T* __restrict__ cat, int64_t ld_cat) {
+                                                              BlockView bv, T* __restrict__ cat, int64_t ld_cat,
+                                                              int64_t pad_rows) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   __shared__ int32_t s_idx[kSpmmBlock / 32][kRowCap];
@@ -206,7 +222,7 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
     const T norm = (T)max(bv.dst_degree[r], 1);
     const V* hs = reinterpret_cast<const V*>(h + (int64_t)bv.self_pos[r] * ld_h);
     V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
-    for (int c = lane; c < dv; c += 32) crow[c] = hs[c];
+    for (int c = lane; c < dv; c += 32) crow[c] = ldv<V, RELU>(hs + c);
     for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
       V acc[CH];
 #pragma unroll
@@ -220,7 +236,7 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int c = c0 + lane + 32 * j;
-          if (c < dv) { x0[j] = r0[c]; x1[j] = r1[c]; }
+          if (c < dv) { x0[j] = ldv<V, RELU>(r0 + c); x1[j] = ldv<V, RELU>(r1 + c); }
         }
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
@@ -234,7 +250,7 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int c = c0 + lane + 32 * j;
-          if (c < dv) vfma<true>(acc[j], w0, r0[c]);
+          if (c < dv) vfma<true>(acc[j], w0, ldv<V, RELU>(r0 + c));
         }
       }
 #pragma unroll
@@ -244,6 +260,12 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
       }
     }
     __syncwarp();
+  }
+  for (int64_t r = n + gw; r < pad_rows; r += nw) {
+    V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
+    V zero;
+    vzero(zero);
+    for (int c = lane; c < 2 * dv; c += 32) crow[c] = zero;
   }
 }
 
@@ -434,13 +456,16 @@ __global__ void dense_bwd_partial_kernel(const T* __restrict__ dh, const T* __re
     partial[(int64_t)blockIdx.x * ncols + c] = (red[0][tx] + red[1][tx]) + (red[2][tx] + red[3][tx]);
 }
 
+// one warp per column: fixed lane-strided partial sums + shuffle tree (deterministic)
 template <typename T>
 __global__ void colsum_final_kernel(const T* __restrict__ partial, int nblocks, int ncols, T* __restrict__ db) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= ncols) return;
   T s = 0;
-  for (int b = 0; b < nblocks; ++b) s += partial[(int64_t)b * ncols + c];
-  db[c] = s;
+  for (int b = lane; b < nblocks; b += 32) s += partial[(int64_t)b * ncols + c];
+  s = warp_sum(s);
+  if (lane == 0) db[c] = s;
 }
 
 struct BwdWs {
@@ -592,39 +617,36 @@ int gns_cache_refresh_rows(const float* host_table, int64_t ld, const int32_t* i
   return check_launch("cache_refresh_rows");
 }
 
-int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, const gns_block_t* block, int64_t max_dst,
-                 void* cat, int64_t ld_cat, void* stream_) {
+int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_t flags, const gns_block_t* block,
+                 int64_t max_dst, int64_t pad_rows, void* cat, int64_t ld_cat, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
-  if (max_dst <= 0) return GNS_OK;
+  if (max_dst <= 0 && pad_rows <= 0) return GNS_OK;
   const int sms = num_sms();
-  long long want = (max_dst * 32 + kSpmmBlock - 1) / kSpmmBlock;
-  int grid = grid_for(want, (long long)sms * 8);
+  long long rows = max_dst > pad_rows ? max_dst : pad_rows;
+  int grid = grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)sms * 8);
   BlockView bv = view_of(block);
+  const bool relu = flags & GNS_SPMM_RELU_INPUT;
+#define GNS_FWD(T, CH, R)                                                                                      \
+  spmm_fwd_kernel<T, CH, R><<<grid, kSpmmBlock, 0, stream>>>((const T*)h, ld_h, dim, bv, (T*)cat, ld_cat, pad_rows)
   if (dtype == 0) {
     if (dim % 4 || ld_h % 4 || ld_cat % 4) {
       set_error("spmm_fwd(f32): dim/strides must be multiples of 4");
       return GNS_EINVAL;
     }
     const int dv = dim / 4;
-    if (dv <= 32)
-      spmm_fwd_kernel<float, 1><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv, (float*)cat, ld_cat);
-    else if (dv <= 64)
-      spmm_fwd_kernel<float, 2><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv, (float*)cat, ld_cat);
-    else
-      spmm_fwd_kernel<float, 4><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv, (float*)cat, ld_cat);
+    if (dv <= 32) { if (relu) GNS_FWD(float, 1, true); else GNS_FWD(float, 1, false); }
+    else if (dv <= 64) { if (relu) GNS_FWD(float, 2, true); else GNS_FWD(float, 2, false); }
+    else { if (relu) GNS_FWD(float, 4, true); else GNS_FWD(float, 4, false); }
   } else {
     if (dim % 2 || ld_h % 2 || ld_cat % 2) {
       set_error("spmm_fwd(f64): dim/strides must be even");
       return GNS_EINVAL;
     }
     const int dv = dim / 2;
-    if (dv <= 32)
-      spmm_fwd_kernel<double, 1><<<grid, kSpmmBlock, 0, stream>>>((const double*)h, ld_h, dim, bv, (double*)cat,
-                                                                  ld_cat);
-    else
-      spmm_fwd_kernel<double, 2><<<grid, kSpmmBlock, 0, stream>>>((const double*)h, ld_h, dim, bv, (double*)cat,
-                                                                  ld_cat);
+    if (dv <= 32) { if (relu) GNS_FWD(double, 1, true); else GNS_FWD(double, 1, false); }
+    else { if (relu) GNS_FWD(double, 2, true); else GNS_FWD(double, 2, false); }
   }
+#undef GNS_FWD
   return check_launch("spmm_fwd");
 }
 
@@ -678,14 +700,14 @@ int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, 
 }
 
 size_t gns_dense_bwd_workspace_size(int64_t max_rows, int32_t ncols) {
-  return (size_t)((max_rows + 127) / 128 + 1) * (size_t)ncols * 8 + 256;
+  return (size_t)((max_rows + 511) / 512 + 1) * (size_t)ncols * 8 + 256;
 }
 
 int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int64_t ld, const int32_t* n_dev,
                        int64_t n_rows, int32_t ncols, void* dz, void* db, void* ws, size_t ws_bytes,
                        void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
-  const int rpb = 128;
+  const int rpb = 512;
   const int nblocks = (int)((n_rows + rpb - 1) / rpb);
   if (ws_bytes < gns_dense_bwd_workspace_size(n_rows, ncols)) {
     set_error("dense_bwd_bias: workspace too small");
@@ -699,12 +721,12 @@ int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int64_t ld,
   if (dtype == 0) {
     dense_bwd_partial_kernel<float><<<grid, 256, 0, stream>>>((const float*)dh, (const float*)z, ld, n_dev, n_rows,
                                                               ncols, (float*)dz, (float*)ws, rpb);
-    colsum_final_kernel<float><<<(ncols + 127) / 128, 128, 0, stream>>>((const float*)ws, nblocks, ncols, (float*)db);
+    colsum_final_kernel<float><<<(ncols + 7) / 8, 256, 0, stream>>>((const float*)ws, nblocks, ncols, (float*)db);
   } else {
     dense_bwd_partial_kernel<double><<<grid, 256, 0, stream>>>((const double*)dh, (const double*)z, ld, n_dev,
                                                                n_rows, ncols, (double*)dz, (double*)ws, rpb);
-    colsum_final_kernel<double><<<(ncols + 127) / 128, 128, 0, stream>>>((const double*)ws, nblocks, ncols,
-                                                                        (double*)db);
+    colsum_final_kernel<double><<<(ncols + 7) / 8, 256, 0, stream>>>((const double*)ws, nblocks, ncols,
+                                                                     (double*)db);
   }
   return check_launch("dense_bwd_bias");
 }

@@ -29,6 +29,8 @@ namespace gns {
 constexpr int kSampBlock = 256;
 constexpr int kWarpCap = 256;
 constexpr int kHubLen = 2048;
+constexpr int kThreadLen = 64;    // rows scanning <= this many positions: one thread per row
+constexpr int kThreadFanout = 32; // and fanout <= this (register top-k list)
 constexpr int kHubBlock = 512;
 constexpr int kHubCap = 512;
 constexpr int kMaxFanout = 128;
@@ -46,6 +48,7 @@ struct LayerArgs {
   int k;
   int cache_only;
   int gns;
+  int64_t max_dst;
   uint32_t seed, epoch, batch, layer;
   gns_block_t b;
 };
@@ -74,10 +77,14 @@ __device__ __forceinline__ RowInfo row_info(const LayerArgs& a, int64_t r) {
   return ri;
 }
 
-__device__ __forceinline__ bool is_hub(const RowInfo& ri) {
+// 0 = thread per row, 1 = warp per row, 2 = CTA per row (hub)
+__device__ __forceinline__ int row_tier(const RowInfo& ri, int k) {
   int sc = ri.m > 0 ? ri.nc : 0;
   int sf = ri.fill > 0 ? ri.deg : 0;
-  return max(sc, sf) > kHubLen;
+  int len = max(sc, sf);
+  if (len > kHubLen) return 2;
+  if (len > kThreadLen || k > kThreadFanout) return 1;
+  return 0;
 }
 
 __device__ __forceinline__ bool cached_bit(const uint32_t* __restrict__ mask, int32_t v) {
@@ -98,9 +105,13 @@ __global__ void __launch_bounds__(BLOCK) layer_count_kernel(ScanStatus ss, Layer
         RowInfo ri = row_info(a, r);
         a.b.row_scan[r] = ex;
         a.b.dst_degree[r] = ri.deg;
-        if (is_hub(ri)) {
-          int h = atomicAdd(a.b.counts + GNS_CNT_HUBS, 1);
+        const int tier = row_tier(ri, a.k);
+        if (tier == 1) {  // warp-tier rows fill hub_rows from the front
+          int h = atomicAdd(a.b.counts + GNS_CNT_WARPROWS, 1);
           a.b.hub_rows[h] = (int32_t)r;
+        } else if (tier == 2) {  // hub rows from the back
+          int h = atomicAdd(a.b.counts + GNS_CNT_HUBS, 1);
+          a.b.hub_rows[a.max_dst - 1 - h] = (int32_t)r;
         }
       },
       [&](unsigned long long tot) {
@@ -299,16 +310,70 @@ __device__ __forceinline__ void make_phases(const LayerArgs& a, const RowInfo& r
   pf.out_base = (int64_t)(tm + (scan_r & 0xffffffffull));
 }
 
+// one thread per row: register-resident sorted top-`take` list, filled by a
+// compare-swap insertion chain in candidate (= position) order, so equal keys
+// keep position order like the reference's stable lexsort.
+template <int TMAX>
+__device__ __forceinline__ void thread_select(const LayerArgs& a, const RowInfo& ri, int64_t r,
+                                              const PhaseDesc& ph) {
+  uint64_t bk[TMAX];
+  uint32_t bp[TMAX];
+#pragma unroll
+  for (int i = 0; i < TMAX; ++i) { bk[i] = ~0ull; bp[i] = 0; }
+  uint64_t worst = ~0ull;
+  const uint32_t stream = stream_word(32, a.layer, ph.phase);
+  const int take = ph.take;
+  const int npairs = (ph.len + 1) >> 1;
+  for (int q = 0; q < npairs; ++q) {
+    uint64_t k2[2];
+    key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k2[0], k2[1]);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int p = 2 * q + j;
+      uint64_t xk = k2[j];
+      if (p >= ph.len || xk >= worst) continue;
+      if (ph.filter && cached_bit(a.mask, __ldg(ph.ids + p))) continue;
+      uint32_t xp = (uint32_t)p;
+#pragma unroll
+      for (int i = 0; i < TMAX; ++i) {
+        if (i < take && xk < bk[i]) {
+          uint64_t tk = bk[i]; bk[i] = xk; xk = tk;
+          uint32_t tp = bp[i]; bp[i] = xp; xp = tp;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TMAX; ++i)
+        if (i == take - 1) worst = bk[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TMAX; ++i)
+    if (i < take) emit_edge(a, ri, r, ph, i, bp[i]);
+}
+
+template <int TMAX>
+__global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a) {
+  const int64_t n = a.n_dev[0];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    RowInfo ri = row_info(a, r);
+    if (row_tier(ri, a.k) != 0) continue;
+    PhaseDesc pc, pf;
+    make_phases(a, ri, r, pc, pf);
+    if (pc.take > 0) thread_select<TMAX>(a, ri, r, pc);
+    if (pf.take > 0) thread_select<TMAX>(a, ri, r, pf);
+  }
+}
+
 __global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a) {
   __shared__ uint64_t s_key[kSampBlock / 32][kWarpCap];
   __shared__ uint32_t s_pos[kSampBlock / 32][kWarpCap];
   const int w = threadIdx.x >> 5;
-  const int64_t n = a.n_dev[0];
+  const int64_t nl = a.b.counts[GNS_CNT_WARPROWS];
   const int64_t gw = (blockIdx.x * (int64_t)kSampBlock + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSampBlock) >> 5;
-  for (int64_t r = gw; r < n; r += nw) {
+  for (int64_t j = gw; j < nl; j += nw) {
+    const int64_t r = a.b.hub_rows[j];
     RowInfo ri = row_info(a, r);
-    if (is_hub(ri)) continue;
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
     if (pc.take > 0) warp_select(a, ri, r, pc, s_key[w], s_pos[w]);
@@ -322,7 +387,7 @@ __global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(LayerArgs a) {
   __shared__ int s_found;
   const int nh = a.b.counts[GNS_CNT_HUBS];
   for (int h = blockIdx.x; h < nh; h += gridDim.x) {
-    const int64_t r = a.b.hub_rows[h];
+    const int64_t r = a.b.hub_rows[a.max_dst - 1 - h];
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
@@ -457,6 +522,7 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.n_dev = n_seeds_dev;
   a.k = k;
   a.cache_only = cache_only;
+  a.max_dst = max_dst;
   a.seed = rng->seed;
   a.epoch = rng->epoch;
   a.batch = rng->batch;
@@ -468,8 +534,13 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   layer_count_kernel<256, 4><<<(unsigned)tiles, 256, 0, stream>>>(make_scan_status(ws, tiles), a);
   GNS_TRY(check_launch("layer_count"));
   const int sms = num_sms();
-  long long want = (max_dst * 32 + kSampBlock - 1) / kSampBlock;
-  int grid = (int)(want < sms * 8 ? (want > 0 ? want : 1) : sms * 8);
+  int tgrid = grid_for((max_dst + 255) / 256, (long long)sms * 16);
+  if (k <= 16)
+    sample_thread_kernel<16><<<tgrid, 256, 0, stream>>>(a);
+  else
+    sample_thread_kernel<32><<<tgrid, 256, 0, stream>>>(a);
+  GNS_TRY(check_launch("sample_thread"));
+  int grid = grid_for((max_dst * 32 + kSampBlock - 1) / kSampBlock, (long long)sms * 8);
   sample_warp_kernel<<<grid, kSampBlock, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_warp"));
   sample_hub_kernel<<<sms, kHubBlock, 0, stream>>>(a);

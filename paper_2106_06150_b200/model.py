@@ -159,12 +159,13 @@ class GraphSAGE:
             d_in = self.dims[li]
             nd = block.dst_nodes.numel()
             cat = torch.empty((max(nd, 1), 2 * d_in), dtype=self.dtype, device=self.device)
-            _lib.call("gns_spmm_fwd", _dt(self.dtype), h.data_ptr(), h.stride(0), d_in, block._c, nd,
-                      cat.data_ptr(), cat.stride(0), s)
+            # layers > 0 read the previous pre-activation and apply relu on load
+            _lib.call("gns_spmm_fwd", _dt(self.dtype), h.data_ptr(), h.stride(0), d_in, 1 if li > 0 else 0,
+                      block._c, nd, 0, cat.data_ptr(), cat.stride(0), s)
             cat = cat[:nd]
             z = torch.addmm(self.biases[li], cat, self.weights[li])
             saved.append((cat, z))
-            h = torch.relu(z) if li + 1 < L else z
+            h = z
         return h, saved
 
     def loss_and_grad(self, logits: torch.Tensor, labels: torch.Tensor, mb: MiniBatch, stream=None):

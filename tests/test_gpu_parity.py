@@ -302,21 +302,30 @@ def test_spmm_fwd_f64_bit_exact(P, dim):
         nsrc, ndst = len(br.src_nodes), len(br.dst_nodes)
         h = np.random.default_rng(li).normal(size=(nsrc, dim))
         ht = torch.as_tensor(h, device="cuda")
-        cat = torch.empty((ndst, 2 * dim), dtype=torch.float64, device="cuda")
-        _lib.call("gns_spmm_fwd", 1, ht.data_ptr(), dim, dim, bg._c, ndst, cat.data_ptr(), 2 * dim,
-                  _lib.stream_ptr())
+        cat = torch.full((ndst + 3, 2 * dim), 7.0, dtype=torch.float64, device="cuda")
+        _lib.call("gns_spmm_fwd", 1, ht.data_ptr(), dim, dim, 0, bg._c, ndst, ndst + 3, cat.data_ptr(),
+                  2 * dim, _lib.stream_ptr())
         agg = OM.spmm_mean_fwd(br, h)
         self_pos = np.searchsorted(br.src_nodes, br.dst_nodes)
         c = cat.cpu().numpy()
+        assert np.all(c[ndst:] == 0)        # static-capacity zero padding
+        c = c[:ndst]
         assert np.array_equal(c[:, :dim], h[self_pos])
         assert np.array_equal(c[:, dim:], agg), li
         # float32 production path: same order, FMA; tolerance 1e-5 relative-to-scale
         h32 = torch.as_tensor(h.astype(np.float32), device="cuda")
         if dim % 4 == 0:
             cat32 = torch.empty((ndst, 2 * dim), dtype=torch.float32, device="cuda")
-            _lib.call("gns_spmm_fwd", 0, h32.data_ptr(), dim, dim, bg._c, ndst, cat32.data_ptr(), 2 * dim,
+            _lib.call("gns_spmm_fwd", 0, h32.data_ptr(), dim, dim, 0, bg._c, ndst, 0, cat32.data_ptr(), 2 * dim,
                       _lib.stream_ptr())
             np.testing.assert_allclose(cat32.cpu().numpy()[:, dim:], agg, rtol=1e-5, atol=1e-5)
+            # relu-on-load variant == spmm of relu(h)
+            _lib.call("gns_spmm_fwd", 1, ht.data_ptr(), dim, dim, 1, bg._c, ndst, 0, cat.data_ptr(), 2 * dim,
+                      _lib.stream_ptr())
+            hr = np.maximum(h, 0.0)
+            c = cat.cpu().numpy()[:ndst]
+            assert np.array_equal(c[:, :dim], hr[self_pos])
+            assert np.array_equal(c[:, dim:], OM.spmm_mean_fwd(br, hr))
 
 
 @pytest.mark.parametrize("dim", [2, 8, 64])
