@@ -161,9 +161,9 @@ def check(rc: int, what: str = ""):
 # how many of OUR kernels ran inside a timed region
 KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
-    "gns_cached_csr_fill": 1, "gns_sample_layer": 4, "gns_relabel": 4, "gns_unique_sorted": 3,
+    "gns_cached_csr_fill": 1, "gns_sample_layer": 5, "gns_relabel": 5, "gns_unique_sorted": 4,
     "gns_epoch_targets": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
-    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 5,
+    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 6,
     "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1,
 }
 launch_counter = [0]

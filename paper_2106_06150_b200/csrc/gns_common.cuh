@@ -364,4 +364,91 @@ __device__ __forceinline__ void scan_tiles(ScanStatus st, long long n, Loader lo
   }
 }
 
+// ---------------------------------------------------------------------------
+// Two-kernel scan for per-step sizes (<= a few thousand tiles): pass 1 writes
+// one sum per tile; pass 2 forms each tile's exclusive prefix by summing the
+// preceding tile sums directly (no look-back chain, no status memset) and
+// scans the tile locally.  Grid = tiles for the capacity; n may live on the
+// device and be smaller.
+// ---------------------------------------------------------------------------
+template <int BLOCK>
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* smem_warp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) smem_warp[warp] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+  if (threadIdx.x < 32) {
+    t = (lane < BLOCK / 32) ? smem_warp[lane] : 0ull;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) smem_warp[0] = t;
+  __syncthreads();
+  t = smem_warp[0];
+  __syncthreads();
+  return t;
+}
+
+template <int BLOCK, int ITEMS, typename Loader>
+__device__ __forceinline__ void scan2_reduce(long long n, Loader load, unsigned long long* __restrict__ tile_sums) {
+  constexpr int TILE = BLOCK * ITEMS;
+  __shared__ unsigned long long s_warp[BLOCK / 32 + 1];
+  const long long base = (long long)blockIdx.x * TILE;
+  unsigned long long s = 0;
+  if (base < n) {
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const long long i = base + j * BLOCK + threadIdx.x;
+      if (i < n) s += load(i);
+    }
+  }
+  s = block_sum<BLOCK>(s, s_warp);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = s;
+}
+
+template <int BLOCK, int ITEMS, typename Loader, typename Storer, typename Totaler>
+__device__ __forceinline__ void scan2_apply(long long n, Loader load, Storer store, Totaler tot,
+                                            const unsigned long long* __restrict__ tile_sums) {
+  constexpr int TILE = BLOCK * ITEMS;
+  __shared__ unsigned long long s_warp[BLOCK / 32 + 1];
+  __shared__ unsigned long long s_items[TILE + TILE / 32];
+  const long long ntiles = (n + TILE - 1) / TILE;
+  const long long tile = blockIdx.x;
+  if (n == 0) {
+    if (tile == 0 && threadIdx.x == 0) tot(0ull);
+    return;
+  }
+  if (tile >= ntiles) return;
+  unsigned long long pre = 0;
+  for (long long j = threadIdx.x; j < tile; j += BLOCK) pre += tile_sums[j];
+  pre = block_sum<BLOCK>(pre, s_warp);
+  const long long tbase = tile * TILE;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int li = j * BLOCK + threadIdx.x;
+    const long long i = tbase + li;
+    s_items[li + (li >> 5)] = (i < n) ? load(i) : 0ull;
+  }
+  __syncthreads();
+  unsigned long long vals[ITEMS];
+  unsigned long long tsum = 0;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int li = threadIdx.x * ITEMS + j;
+    vals[j] = s_items[li + (li >> 5)];
+    tsum += vals[j];
+  }
+  unsigned long long block_total;
+  unsigned long long run = pre + block_excl_scan<BLOCK>(tsum, s_warp, block_total);
+  if (tile == ntiles - 1 && threadIdx.x == 0) tot(pre + block_total);
+  const long long base = tbase + (long long)threadIdx.x * ITEMS;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const long long i = base + j;
+    if (i < n) store(i, run, vals[j]);
+    run += vals[j];
+  }
+}
+
 }  // namespace gns

@@ -280,17 +280,25 @@ __global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_
   }
 }
 
-template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) tscan_kernel(ScanStatus ss, BlockView bv, int32_t* __restrict__ tcount,
-                                                      int32_t* __restrict__ tptr) {
+constexpr int kTsBlock = 256, kTsItems = 8;
+
+__global__ void __launch_bounds__(kTsBlock) tscan_reduce_kernel(BlockView bv, const int32_t* __restrict__ tcount,
+                                                                unsigned long long* tile_sums) {
   const int64_t n = bv.counts[GNS_CNT_SRC];
-  scan_tiles<BLOCK, ITEMS>(
-      ss, n, [&](long long i) { return (unsigned long long)tcount[i]; },
+  scan2_reduce<kTsBlock, kTsItems>(n, [&](long long i) { return (unsigned long long)tcount[i]; }, tile_sums);
+}
+
+__global__ void __launch_bounds__(kTsBlock) tscan_apply_kernel(BlockView bv, int32_t* __restrict__ tcount,
+                                                               int32_t* __restrict__ tptr,
+                                                               const unsigned long long* tile_sums) {
+  const int64_t n = bv.counts[GNS_CNT_SRC];
+  scan2_apply<kTsBlock, kTsItems>(
+      n, [&](long long i) { return (unsigned long long)tcount[i]; },
       [&](long long i, unsigned long long ex, unsigned long long) {
         tptr[i] = (int32_t)ex;
         tcount[i] = 0;  // becomes the scatter cursor
       },
-      [&](unsigned long long tot) { tptr[n] = (int32_t)tot; });
+      [&](unsigned long long tot) { tptr[n] = (int32_t)tot; }, tile_sums);
 }
 
 __global__ void tscatter_kernel(BlockView bv, int32_t* __restrict__ cursor, const int32_t* __restrict__ tptr,
@@ -674,10 +682,11 @@ int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, 
   BlockView bv = view_of(block);
   GNS_CUDA(cudaMemsetAsync(w.tcount, 0, (max_src + 1) * sizeof(int32_t), stream));
   GNS_CUDA(cudaMemsetAsync(w.self_of, 0xff, (max_src + 1) * sizeof(int32_t), stream));
-  GNS_CUDA(cudaMemsetAsync(w.scan, 0, scan_status_bytes(w.tiles), stream));
   int g1 = grid_for((max_edges + max_dst + 255) / 256, (long long)sms * 8);
   tcount_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.self_of);
-  tscan_kernel<256, 8><<<(unsigned)w.tiles, 256, 0, stream>>>(make_scan_status(w.scan, w.tiles), bv, w.tcount, w.tptr);
+  const unsigned ttiles = (unsigned)((max_src + kTsBlock * kTsItems - 1) / (kTsBlock * kTsItems)) + 1;
+  tscan_reduce_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, (unsigned long long*)w.scan);
+  tscan_apply_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, w.tptr, (unsigned long long*)w.scan);
   tscatter_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.tptr, w.tkeys);
   int g2 = grid_for((max_src * 32 + 255) / 256, (long long)sms * 8);
   tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys);

@@ -29,8 +29,7 @@ namespace gns {
 constexpr int kSampBlock = 256;
 constexpr int kWarpCap = 256;
 constexpr int kHubLen = 2048;
-constexpr int kThreadLen = 64;    // rows scanning <= this many positions: one thread per row
-constexpr int kThreadFanout = 32; // and fanout <= this (register top-k list)
+constexpr int kThreadLen = 16;    // rows scanning <= 16 positions: one thread per row, register sort
 constexpr int kHubBlock = 512;
 constexpr int kHubCap = 512;
 constexpr int kMaxFanout = 128;
@@ -83,7 +82,7 @@ __device__ __forceinline__ int row_tier(const RowInfo& ri, int k) {
   int sf = ri.fill > 0 ? ri.deg : 0;
   int len = max(sc, sf);
   if (len > kHubLen) return 2;
-  if (len > kThreadLen || k > kThreadFanout) return 1;
+  if (len > kThreadLen) return 1;
   return 0;
 }
 
@@ -91,16 +90,31 @@ __device__ __forceinline__ bool cached_bit(const uint32_t* __restrict__ mask, in
   return (__ldg(mask + (v >> 5)) >> (v & 31)) & 1u;
 }
 
-// ---- pass 1: per-row counts + exclusive scan --------------------------------
-template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) layer_count_kernel(ScanStatus ss, LayerArgs a) {
+// ---- pass 1: per-row counts + exclusive scan (two kernels) ----------------------
+__device__ __forceinline__ unsigned long long row_counts(const LayerArgs& a, long long r) {
+  RowInfo ri = row_info(a, r);
+  return ((unsigned long long)ri.m << 32) | (unsigned long long)ri.fill;
+}
+
+constexpr int kCntBlock = 256, kCntItems = 4;
+
+__global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(LayerArgs a, unsigned long long* tile_sums) {
   const long long n = a.n_dev[0];
-  scan_tiles<BLOCK, ITEMS>(
-      ss, n,
+  // the per-row value is stashed in row_scan[r] for the apply pass
+  scan2_reduce<kCntBlock, kCntItems>(
+      n,
       [&](long long r) {
-        RowInfo ri = row_info(a, r);
-        return ((unsigned long long)ri.m << 32) | (unsigned long long)ri.fill;
+        unsigned long long v = row_counts(a, r);
+        a.b.row_scan[r] = v;
+        return v;
       },
+      tile_sums);
+}
+
+__global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(LayerArgs a, const unsigned long long* tile_sums) {
+  const long long n = a.n_dev[0];
+  scan2_apply<kCntBlock, kCntItems>(
+      n, [&](long long r) { return (unsigned long long)a.b.row_scan[r]; },
       [&](long long r, unsigned long long ex, unsigned long long) {
         RowInfo ri = row_info(a, r);
         a.b.row_scan[r] = ex;
@@ -119,7 +133,8 @@ __global__ void __launch_bounds__(BLOCK) layer_count_kernel(ScanStatus ss, Layer
         a.b.counts[GNS_CNT_DST] = (int32_t)n;
         a.b.counts[GNS_CNT_EDGES] = (int32_t)((tot >> 32) + (tot & 0xffffffffull));
         a.b.counts[GNS_CNT_CACHED] = (int32_t)(tot >> 32);
-      });
+      },
+      tile_sums);
 }
 
 // ---- selection helpers ------------------------------------------------------
@@ -310,48 +325,59 @@ __device__ __forceinline__ void make_phases(const LayerArgs& a, const RowInfo& r
   pf.out_base = (int64_t)(tm + (scan_r & 0xffffffffull));
 }
 
-// one thread per row: register-resident sorted top-`take` list, filled by a
-// compare-swap insertion chain in candidate (= position) order, so equal keys
-// keep position order like the reference's stable lexsort.
-template <int TMAX>
-__device__ __forceinline__ void thread_select(const LayerArgs& a, const RowInfo& ri, int64_t r,
-                                              const PhaseDesc& ph) {
-  uint64_t bk[TMAX];
-  uint32_t bp[TMAX];
+// Ascending bitonic sorting network over 16 packed keys, compile-time
+// indices only (stays in registers).
+__device__ __forceinline__ void sort16(uint64_t (&a)[16]) {
 #pragma unroll
-  for (int i = 0; i < TMAX; ++i) { bk[i] = ~0ull; bp[i] = 0; }
-  uint64_t worst = ~0ull;
-  const uint32_t stream = stream_word(32, a.layer, ph.phase);
-  const int take = ph.take;
-  const int npairs = (ph.len + 1) >> 1;
-  for (int q = 0; q < npairs; ++q) {
-    uint64_t k2[2];
-    key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k2[0], k2[1]);
+  for (int k = 2; k <= 16; k <<= 1) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int p = 2 * q + j;
-      uint64_t xk = k2[j];
-      if (p >= ph.len || xk >= worst) continue;
-      if (ph.filter && cached_bit(a.mask, __ldg(ph.ids + p))) continue;
-      uint32_t xp = (uint32_t)p;
+    for (int j = k >> 1; j > 0; j >>= 1) {
 #pragma unroll
-      for (int i = 0; i < TMAX; ++i) {
-        if (i < take && xk < bk[i]) {
-          uint64_t tk = bk[i]; bk[i] = xk; xk = tk;
-          uint32_t tp = bp[i]; bp[i] = xp; xp = tp;
+      for (int i = 0; i < 16; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const uint64_t x = a[i], y = a[l];
+          const bool sw = up ? (y < x) : (x < y);
+          a[i] = sw ? y : x;
+          a[l] = sw ? x : y;
         }
       }
-#pragma unroll
-      for (int i = 0; i < TMAX; ++i)
-        if (i == take - 1) worst = bk[i];
     }
   }
-#pragma unroll
-  for (int i = 0; i < TMAX; ++i)
-    if (i < take) emit_edge(a, ri, r, ph, i, bp[i]);
 }
 
-template <int TMAX>
+// One thread per row for rows scanning <= 16 positions (the bulk of the
+// cache-only input layer): every valid candidate gets the packed key
+// (key53 << 11 | position) — ordering = (key, position), exactly the
+// reference's stable lexsort — a 16-wide sorting network orders them and the
+// first `take` are emitted.
+__device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInfo& ri, int64_t r,
+                                                const PhaseDesc& ph) {
+  const uint32_t stream = stream_word(32, a.layer, ph.phase);
+  uint64_t v[16];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint64_t k0 = ~0ull, k1 = ~0ull;
+    if (2 * q < ph.len) {
+      key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
+      bool ok0 = true, ok1 = 2 * q + 1 < ph.len;
+      if (ph.filter) {
+        ok0 = !cached_bit(a.mask, __ldg(ph.ids + 2 * q));
+        if (ok1) ok1 = !cached_bit(a.mask, __ldg(ph.ids + 2 * q + 1));
+      }
+      k0 = ok0 ? ((k0 << 11) | (uint64_t)(2 * q)) : ~0ull;
+      k1 = ok1 ? ((k1 << 11) | (uint64_t)(2 * q + 1)) : ~0ull;
+    }
+    v[2 * q] = k0;
+    v[2 * q + 1] = k1;
+  }
+  sort16(v);
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (i < ph.take) emit_edge(a, ri, r, ph, i, (uint32_t)(v[i] & 2047u));
+}
+
 __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a) {
   const int64_t n = a.n_dev[0];
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
@@ -359,8 +385,8 @@ __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a) {
     if (row_tier(ri, a.k) != 0) continue;
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
-    if (pc.take > 0) thread_select<TMAX>(a, ri, r, pc);
-    if (pf.take > 0) thread_select<TMAX>(a, ri, r, pf);
+    if (pc.take > 0) thread_select16(a, ri, r, pc);
+    if (pf.take > 0) thread_select16(a, ri, r, pf);
   }
 }
 
@@ -409,12 +435,21 @@ __global__ void setbits_kernel(const int32_t* __restrict__ a, const int32_t* __r
   }
 }
 
-template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) enumerate_kernel(ScanStatus ss, const uint32_t* __restrict__ bits, int64_t nw,
-                                                          int32_t* __restrict__ rank, int32_t* __restrict__ out,
-                                                          int32_t* __restrict__ out_n) {
-  scan_tiles<BLOCK, ITEMS>(
-      ss, nw, [&](long long w) { return (unsigned long long)__popc(bits[w]); },
+constexpr int kEnumBlock = 256, kEnumItems = 16;
+
+__global__ void __launch_bounds__(kEnumBlock) enumerate_reduce_kernel(const uint32_t* __restrict__ bits, int64_t nw,
+                                                                      unsigned long long* tile_sums) {
+  scan2_reduce<kEnumBlock, kEnumItems>(nw, [&](long long w) { return (unsigned long long)__popc(bits[w]); },
+                                       tile_sums);
+}
+
+__global__ void __launch_bounds__(kEnumBlock) enumerate_apply_kernel(const uint32_t* __restrict__ bits, int64_t nw,
+                                                                     const unsigned long long* tile_sums,
+                                                                     int32_t* __restrict__ rank,
+                                                                     int32_t* __restrict__ out,
+                                                                     int32_t* __restrict__ out_n) {
+  scan2_apply<kEnumBlock, kEnumItems>(
+      nw, [&](long long w) { return (unsigned long long)__popc(bits[w]); },
       [&](long long w, unsigned long long ex, unsigned long long val) {
         if (!val) return;
         rank[w] = (int32_t)ex;
@@ -426,7 +461,7 @@ __global__ void __launch_bounds__(BLOCK) enumerate_kernel(ScanStatus ss, const u
           out[pos++] = (int32_t)(w * 32 + bb);
         }
       },
-      [&](unsigned long long tot) { out_n[0] = (int32_t)tot; });
+      [&](unsigned long long tot) { out_n[0] = (int32_t)tot; }, tile_sums);
 }
 
 __device__ __forceinline__ int32_t bit_rank(const uint32_t* __restrict__ bits, const int32_t* __restrict__ rank,
@@ -476,9 +511,10 @@ static size_t relabel_ws(int64_t num_nodes, void* base, size_t cap, RelabelWs* r
 
 static int run_enumerate(const RelabelWs& r, int64_t num_nodes, int32_t* out, int32_t* out_n, cudaStream_t stream) {
   int64_t nw = (num_nodes + 31) / 32;
-  GNS_CUDA(cudaMemsetAsync(r.scan, 0, scan_status_bytes(r.tiles), stream));
-  enumerate_kernel<256, 16><<<(unsigned)r.tiles, 256, 0, stream>>>(make_scan_status(r.scan, r.tiles), r.bits, nw,
-                                                                   r.rank, out, out_n);
+  const unsigned tiles = (unsigned)((nw + kEnumBlock * kEnumItems - 1) / (kEnumBlock * kEnumItems));
+  unsigned long long* tile_sums = (unsigned long long*)r.scan;
+  enumerate_reduce_kernel<<<tiles ? tiles : 1, kEnumBlock, 0, stream>>>(r.bits, nw, tile_sums);
+  enumerate_apply_kernel<<<tiles ? tiles : 1, kEnumBlock, 0, stream>>>(r.bits, nw, tile_sums, r.rank, out, out_n);
   return check_launch("enumerate");
 }
 
@@ -528,17 +564,14 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.batch = rng->batch;
   a.layer = rng->layer;
   a.b = *block;
-  long long tiles = (max_dst + 256 * 4 - 1) / (256 * 4) + 1;
-  GNS_CUDA(cudaMemsetAsync(ws, 0, scan_status_bytes(tiles), stream));
+  const unsigned tiles = (unsigned)((max_dst + kCntBlock * kCntItems - 1) / (kCntBlock * kCntItems)) + 1;
   GNS_CUDA(cudaMemsetAsync(block->counts, 0, GNS_CNT_N * sizeof(int32_t), stream));
-  layer_count_kernel<256, 4><<<(unsigned)tiles, 256, 0, stream>>>(make_scan_status(ws, tiles), a);
+  layer_count_reduce_kernel<<<tiles, kCntBlock, 0, stream>>>(a, (unsigned long long*)ws);
+  layer_count_apply_kernel<<<tiles, kCntBlock, 0, stream>>>(a, (unsigned long long*)ws);
   GNS_TRY(check_launch("layer_count"));
   const int sms = num_sms();
   int tgrid = grid_for((max_dst + 255) / 256, (long long)sms * 16);
-  if (k <= 16)
-    sample_thread_kernel<16><<<tgrid, 256, 0, stream>>>(a);
-  else
-    sample_thread_kernel<32><<<tgrid, 256, 0, stream>>>(a);
+  sample_thread_kernel<<<tgrid, 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_thread"));
   int grid = grid_for((max_dst * 32 + kSampBlock - 1) / kSampBlock, (long long)sms * 8);
   sample_warp_kernel<<<grid, kSampBlock, 0, stream>>>(a);
