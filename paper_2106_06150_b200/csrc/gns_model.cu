@@ -451,10 +451,8 @@ __global__ void dense_bwd_partial_kernel(const T* __restrict__ dh, const T* __re
   if (c < ncols) {
     for (int64_t r = r0 + ty; r < r1; r += 4) {
       T v = dh[r * ld + c];
-      if (z) {
-        v = z[r * ld + c] > (T)0 ? v : (T)0;
-        dz[r * ld + c] = v;
-      }
+      if (z) v = z[r * ld + c] > (T)0 ? v : (T)0;
+      if (dz) dz[r * ld + c] = v;
       sum += v;
     }
   }

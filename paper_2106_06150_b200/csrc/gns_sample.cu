@@ -351,15 +351,16 @@ __device__ __forceinline__ void sort16(uint64_t (&a)[16]) {
 // cache-only input layer): every valid candidate gets the packed key
 // (key53 << 11 | position) — ordering = (key, position), exactly the
 // reference's stable lexsort — a 16-wide sorting network orders them and the
-// first `take` are emitted.
-__device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInfo& ri, int64_t r,
-                                                const PhaseDesc& ph) {
+// first `take` are emitted.  Keys are staged per thread in shared memory so
+// the Philox and emit loops stay rolled (small code, no local memory).
+__device__ __noinline__ void thread_select16(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
+                                             uint64_t* __restrict__ slot) {
   const uint32_t stream = stream_word(32, a.layer, ph.phase);
-  uint64_t v[16];
-#pragma unroll
+  const int npairs = (ph.len + 1) >> 1;
+#pragma unroll 1
   for (int q = 0; q < 8; ++q) {
     uint64_t k0 = ~0ull, k1 = ~0ull;
-    if (2 * q < ph.len) {
+    if (q < npairs) {
       key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
       bool ok0 = true, ok1 = 2 * q + 1 < ph.len;
       if (ph.filter) {
@@ -369,24 +370,32 @@ __device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInf
       k0 = ok0 ? ((k0 << 11) | (uint64_t)(2 * q)) : ~0ull;
       k1 = ok1 ? ((k1 << 11) | (uint64_t)(2 * q + 1)) : ~0ull;
     }
-    v[2 * q] = k0;
-    v[2 * q + 1] = k1;
+    slot[(2 * q) * 32] = k0;
+    slot[(2 * q + 1) * 32] = k1;
   }
+  uint64_t v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = slot[i * 32];
   sort16(v);
 #pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if (i < ph.take) emit_edge(a, ri, r, ph, i, (uint32_t)(v[i] & 2047u));
+  for (int i = 0; i < 16; ++i) slot[i * 32] = v[i];
+#pragma unroll 1
+  for (int i = 0; i < ph.take; ++i) emit_edge(a, ri, r, ph, i, (uint32_t)(slot[i * 32] & 2047u));
 }
 
 __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a) {
+  // per-thread 16-entry key slots, interleaved by lane (bank-conflict free)
+  __shared__ uint64_t s_keys[256 / 32][16 * 32];
+  uint64_t* slot = &s_keys[threadIdx.x >> 5][threadIdx.x & 31];
   const int64_t n = a.n_dev[0];
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     RowInfo ri = row_info(a, r);
     if (row_tier(ri, a.k) != 0) continue;
-    PhaseDesc pc, pf;
-    make_phases(a, ri, r, pc, pf);
-    if (pc.take > 0) thread_select16(a, ri, r, pc);
-    if (pf.take > 0) thread_select16(a, ri, r, pf);
+    PhaseDesc ph[2];
+    make_phases(a, ri, r, ph[0], ph[1]);
+#pragma unroll 1
+    for (int j = 0; j < 2; ++j)
+      if (ph[j].take > 0) thread_select16(a, ri, r, ph[j], slot);
   }
 }
 

@@ -63,6 +63,30 @@ def _dt(dtype) -> int:
     return 0 if dtype == torch.float32 else 1
 
 
+_SPLIT_CHUNK = 2048
+_SPLIT_MIN = 8192
+
+
+def _split_rows(n: int) -> int:
+    """Row count padded for the split-K weight gradient (tall-skinny GEMM)."""
+    if n < _SPLIT_MIN:
+        return n
+    return (n + _SPLIT_CHUNK - 1) // _SPLIT_CHUNK * _SPLIT_CHUNK
+
+
+def _weight_grad(cat: torch.Tensor, dz: torch.Tensor, out: torch.Tensor):
+    """dW = cat^T dz (model.py:219).  K = rows is ~10^5 while the output is
+    only (2 d_in) x d_out, so a single GEMM has too few output tiles to fill
+    148 SMs: split K into 2048-row chunks (batched GEMM) and reduce."""
+    n = cat.shape[0]
+    if n < _SPLIT_MIN or n % _SPLIT_CHUNK:
+        torch.mm(cat.t(), dz, out=out)
+        return
+    s = n // _SPLIT_CHUNK
+    part = torch.bmm(cat.view(s, _SPLIT_CHUNK, -1).transpose(1, 2), dz.view(s, _SPLIT_CHUNK, -1))
+    torch.sum(part, dim=0, out=out)
+
+
 class _TF32:
     """Scoped torch.backends.cuda.matmul.allow_tf32."""
 
@@ -158,12 +182,14 @@ class GraphSAGE:
         for li, block in enumerate(mb.blocks):
             d_in = self.dims[li]
             nd = block.dst_nodes.numel()
-            cat = torch.empty((max(nd, 1), 2 * d_in), dtype=self.dtype, device=self.device)
-            # layers > 0 read the previous pre-activation and apply relu on load
+            npad = _split_rows(nd)
+            catp = torch.empty((max(npad, 1), 2 * d_in), dtype=self.dtype, device=self.device)
+            # layers > 0 read the previous pre-activation and apply relu on load;
+            # rows [nd, npad) are zero so the split-K weight gradient can use them
             _lib.call("gns_spmm_fwd", _dt(self.dtype), h.data_ptr(), h.stride(0), d_in, 1 if li > 0 else 0,
-                      block._c, nd, 0, cat.data_ptr(), cat.stride(0), s)
-            cat = cat[:nd]
-            z = torch.addmm(self.biases[li], cat, self.weights[li])
+                      block._c, nd, npad, catp.data_ptr(), catp.stride(0), s)
+            cat = catp[:npad]
+            z = torch.addmm(self.biases[li], cat[:nd], self.weights[li])
             saved.append((cat, z))
             h = z
         return h, saved
@@ -198,17 +224,22 @@ class GraphSAGE:
             need = _lib.lib().gns_dense_bwd_workspace_size(max(n, 1), d_out)
             if self._ws_dense is None or self._ws_dense.numel() < need:
                 self._ws_dense = _lib.workspace(int(need * 1.5), self.device)
-            if li == L - 1:
-                dz = dh
+            npad = cat.shape[0]
+            if li == L - 1 and npad == n:
+                dzp = dh
                 _lib.call("gns_dense_bwd_bias", _dt(self.dtype), dh.data_ptr(), None, dh.stride(0), None, n,
                           d_out, None, self.gbiases[li].data_ptr(), self._ws_dense.data_ptr(),
                           self._ws_dense.numel(), s)
             else:
-                dz = torch.empty_like(dh)
-                _lib.call("gns_dense_bwd_bias", _dt(self.dtype), dh.data_ptr(), z.data_ptr(), dh.stride(0), None,
-                          n, d_out, dz.data_ptr(), self.gbiases[li].data_ptr(), self._ws_dense.data_ptr(),
+                dzp = torch.empty((npad, d_out), dtype=self.dtype, device=self.device)
+                if npad > n:
+                    dzp[n:].zero_()
+                zz = z.data_ptr() if li < L - 1 else None
+                _lib.call("gns_dense_bwd_bias", _dt(self.dtype), dh.data_ptr(), zz, dh.stride(0), None,
+                          n, d_out, dzp.data_ptr(), self.gbiases[li].data_ptr(), self._ws_dense.data_ptr(),
                           self._ws_dense.numel(), s)
-            torch.mm(cat.t(), dz, out=self.gweights[li])
+            dz = dzp[:n]
+            _weight_grad(cat, dzp, self.gweights[li])
             if li == 0:
                 break
             dcat = torch.mm(dz, self.weights[li].t())
