@@ -86,6 +86,18 @@ typedef struct gns_rng {
   uint32_t layer;
 } gns_rng_t;
 
+/* Per-batch parameters kept in DEVICE memory so a captured CUDA graph can be
+ * replayed for every batch: the Philox key and the batch's slice of the
+ * epoch permutation (pool.py:60-70). */
+typedef struct gns_step {
+  uint32_t seed;
+  uint32_t epoch;
+  uint32_t batch;
+  uint32_t pad;
+  int64_t begin;
+  int64_t count;
+} gns_step_t;
+
 /* One sampled layer (sampling.py:32-60 LayerBlock) in capacity-sized buffers. */
 typedef struct gns_block {
   /* per dst row, capacity max_dst (+1 for row_scan) */
@@ -144,7 +156,8 @@ GNS_API int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits,
 
 /* ---- sampler (sampling.py) --------------------------------------------- */
 
-/* sample_neighbors_gns (sampling.py:189-266, policy gns-paper) when cache !=
+/* step_dev (device, may be NULL) overrides rng->seed/epoch/batch.
+ * sample_neighbors_gns (sampling.py:189-266, policy gns-paper) when cache !=
  * NULL, sample_neighbors_uniform (sampling.py:155-170) when cache == NULL.
  * seeds: sorted unique int32 (count in *n_seeds_dev, <= max_dst).  Writes
  * row_scan, dst_degree, edge_node/edge_dst/edge_weight/edge_cached and counts
@@ -153,8 +166,8 @@ GNS_API size_t gns_sample_workspace_size(int64_t max_dst);
 GNS_API int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache,
                      const int32_t* seeds, const int32_t* n_seeds_dev,
                      int64_t max_dst, int32_t k, int32_t cache_only,
-                     const gns_rng_t* rng, gns_block_t* block, void* ws,
-                     size_t ws_bytes, void* stream);
+                     const gns_rng_t* rng, const gns_step_t* step_dev,
+                     gns_block_t* block, void* ws, size_t ws_bytes, void* stream);
 
 /* _assemble (sampling.py:139-152): src_nodes = sorted unique(seeds ∪
  * edge_node), edge_src = rank of edge_node, self_pos = rank of each seed.
@@ -178,6 +191,12 @@ GNS_API int gns_unique_sorted(int64_t num_nodes, const int32_t* ids, const int32
 GNS_API int gns_epoch_targets(const int32_t* train_ids, int64_t n_train, uint32_t seed,
                       uint32_t epoch, int64_t begin, int64_t count, int32_t* out,
                       void* stream);
+
+/* Same, with (seed, epoch, begin, count) read from a device gns_step_t; the
+ * batch size actually written (min(count, n_train - begin)) goes to *out_n_dev. */
+GNS_API int gns_epoch_targets_dev(const int32_t* train_ids, int64_t n_train,
+                                  const gns_step_t* step_dev, int64_t max_count, int32_t* out,
+                                  int32_t* out_n_dev, void* stream);
 
 /* ---- model side (model.py) --------------------------------------------- */
 
@@ -224,11 +243,12 @@ GNS_API int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim
 /* Backward of the above (model.py:223-225):
  * dh[s,:] = sum_{e: src=s, ascending dst} w_e * (dcat[dst_e, D:2D] / max(deg,1))
  *           (+ dcat[d, 0:D] where self_pos[d] == s).
- * Builds the transposed block CSR in the workspace. */
+ * Builds the transposed block CSR in the workspace.  Rows [n_src, pad_rows)
+ * of dh are zero-filled. */
 GNS_API size_t gns_spmm_bwd_workspace_size(int64_t max_src, int64_t max_edges);
 GNS_API int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim,
                  const gns_block_t* block, int64_t max_dst, int64_t max_src,
-                 int64_t max_edges, void* dh, int64_t ld_dh, void* ws,
+                 int64_t max_edges, int64_t pad_rows, void* dh, int64_t ld_dh, void* ws,
                  size_t ws_bytes, void* stream);
 
 /* relu backward fused with the bias gradient (model.py:218,220):
@@ -242,9 +262,10 @@ GNS_API int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int
 
 /* Softmax cross-entropy (model.py:189-200) over rows of logits for the
  * sorted targets; labels gathered as labels[targets[r]].  Writes grad_out
- * (same layout) and loss_out[0] = mean loss (device, float64). */
+ * (same layout; rows [n, pad_rows) zero) and loss_out[0] = mean loss (device,
+ * float64). */
 GNS_API int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, const int32_t* n_dev,
-                     int64_t max_rows, int32_t num_classes, const int32_t* labels,
+                     int64_t max_rows, int64_t pad_rows, int32_t num_classes, const int32_t* labels,
                      const int32_t* targets, void* grad_out, double* loss_out,
                      void* ws, size_t ws_bytes, void* stream);
 

@@ -51,6 +51,11 @@ class GnsRng(Structure):
                 ("layer", c_uint32)]
 
 
+class GnsStep(Structure):
+    _fields_ = [("seed", c_uint32), ("epoch", c_uint32), ("batch", c_uint32), ("pad", c_uint32),
+                ("begin", c_int64), ("count", c_int64)]
+
+
 class GnsBlock(Structure):
     _fields_ = [("row_scan", c_void_p), ("dst_degree", c_void_p), ("self_pos", c_void_p),
                 ("hub_rows", c_void_p), ("edge_node", c_void_p), ("edge_src", c_void_p),
@@ -74,7 +79,7 @@ _SIGS = {
                                       c_void_p]),
     "gns_sample_workspace_size": (c_size_t, [c_int64]),
     "gns_sample_layer": (c_int32, [POINTER(GnsGraph), POINTER(GnsCache), c_void_p, c_void_p,
-                                   c_int64, c_int32, c_int32, POINTER(GnsRng),
+                                   c_int64, c_int32, c_int32, POINTER(GnsRng), c_void_p,
                                    POINTER(GnsBlock), c_void_p, c_size_t, c_void_p]),
     "gns_relabel_workspace_size": (c_size_t, [c_int64]),
     "gns_relabel": (c_int32, [c_int64, c_void_p, c_void_p, c_int64, POINTER(GnsBlock), c_int64,
@@ -83,6 +88,8 @@ _SIGS = {
                                     c_void_p, c_size_t, c_void_p]),
     "gns_epoch_targets": (c_int32, [c_void_p, c_int64, c_uint32, c_uint32, c_int64, c_int64,
                                     c_void_p, c_void_p]),
+    "gns_epoch_targets_dev": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                                        c_void_p]),
     "gns_gather_rows": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_int64,
                                   c_int32, c_void_p, c_int64, c_int32, c_void_p]),
     "gns_gather_rows_mixed": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
@@ -95,12 +102,12 @@ _SIGS = {
                                c_int64, c_int64, c_void_p, c_int64, c_void_p]),
     "gns_spmm_bwd_workspace_size": (c_size_t, [c_int64, c_int64]),
     "gns_spmm_bwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, POINTER(GnsBlock), c_int64,
-                               c_int64, c_int64, c_void_p, c_int64, c_void_p, c_size_t,
+                               c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_size_t,
                                c_void_p]),
     "gns_dense_bwd_workspace_size": (c_size_t, [c_int64, c_int32]),
     "gns_dense_bwd_bias": (c_int32, [c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int32,
                                      c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
-    "gns_softmax_xent": (c_int32, [c_int32, c_void_p, c_int64, c_void_p, c_int64, c_int32,
+    "gns_softmax_xent": (c_int32, [c_int32, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                    c_void_p]),
     "gns_adam": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_double,
@@ -162,7 +169,7 @@ def check(rc: int, what: str = ""):
 KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
     "gns_cached_csr_fill": 1, "gns_sample_layer": 5, "gns_relabel": 5, "gns_unique_sorted": 4,
-    "gns_epoch_targets": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
+    "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
     "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 6,
     "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1,
 }

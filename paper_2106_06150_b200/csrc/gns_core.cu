@@ -82,6 +82,26 @@ __global__ void epoch_targets_kernel(const int32_t* __restrict__ train_ids, int6
   }
 }
 
+__global__ void epoch_targets_dev_kernel(const int32_t* __restrict__ train_ids, int64_t n_train, int h,
+                                         const gns_step_t* __restrict__ step, int64_t max_count,
+                                         int32_t* __restrict__ out, int32_t* __restrict__ out_n) {
+  const int64_t begin = step->begin;
+  int64_t count = step->count;
+  if (count > n_train - begin) count = n_train - begin;
+  if (count > max_count) count = max_count;
+  if (count < 0) count = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) out_n[0] = (int32_t)count;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < count;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t y = (uint64_t)(begin + j);
+    if (n_train > 1) {
+      y = feistel_once(y, h, step->seed, step->epoch);
+      while (y >= (uint64_t)n_train) y = feistel_once(y, h, step->seed, step->epoch);
+    }
+    out[j] = train_ids[y];
+  }
+}
+
 template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) bitmap_rank_kernel(ScanStatus st, const uint32_t* __restrict__ bits,
                                                             int64_t nwords, int32_t* __restrict__ rank) {
@@ -137,6 +157,17 @@ int gns_epoch_targets(const int32_t* train_ids, int64_t n_train, uint32_t seed, 
   epoch_targets_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(train_ids, n_train, bits / 2, seed,
                                                                epoch, begin, count, out);
   return check_launch("epoch_targets");
+}
+
+int gns_epoch_targets_dev(const int32_t* train_ids, int64_t n_train, const gns_step_t* step_dev,
+                          int64_t max_count, int32_t* out, int32_t* out_n_dev, void* stream) {
+  int bits = 2;
+  while ((1ll << bits) < n_train) ++bits;
+  bits += bits & 1;
+  int grid = grid_for((max_count + 255) / 256, (long long)num_sms() * 8);
+  epoch_targets_dev_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(train_ids, n_train, bits / 2, step_dev,
+                                                                   max_count, out, out_n_dev);
+  return check_launch("epoch_targets_dev");
 }
 
 int gns_bitmap_rank(const uint32_t* bits, int64_t nwords, int32_t* out_rank, void* ws,

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
                                                               BlockView bv, const int32_t* __restrict__ tptr,
                                                               const uint64_t* __restrict__ tkeys,
                                                               const int32_t* __restrict__ self_of,
-                                                              T* __restrict__ dh, int64_t ld_dh) {
+                                                              T* __restrict__ dh, int64_t ld_dh, int64_t pad_rows) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   constexpr bool EXACT = sizeof(T) == 8;
@@ -433,6 +433,11 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
       }
     }
   }
+  for (int64_t s = n + gw; s < pad_rows; s += nw) {
+    V zero;
+    vzero(zero);
+    for (int c = lane; c < dv; c += 32) reinterpret_cast<V*>(dh + s * ld_dh)[c] = zero;
+  }
 }
 
 // dz = relu'(z) * dh (model.py:218) fused with the bias gradient db = sum_r dz
@@ -498,7 +503,7 @@ static size_t bwd_ws(int64_t max_src, int64_t max_edges, void* base, size_t cap,
 template <typename T>
 __global__ void xent_kernel(const T* __restrict__ logits, int64_t ld, const int32_t* __restrict__ n_dev, int C,
                             const int32_t* __restrict__ labels, const int32_t* __restrict__ targets,
-                            T* __restrict__ grad, double* __restrict__ row_loss) {
+                            T* __restrict__ grad, double* __restrict__ row_loss, int64_t pad_rows) {
   const int lane = threadIdx.x & 31;
   const int64_t n = n_dev[0];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -523,6 +528,8 @@ __global__ void xent_kernel(const T* __restrict__ logits, int64_t ld, const int3
       if (c == lab) row_loss[r] = -(double)lp;
     }
   }
+  for (int64_t r = n + gw; r < pad_rows; r += nw)
+    for (int c = lane; c < C; c += 32) grad[r * ld + c] = (T)0;
 }
 
 __global__ void mean_kernel(const double* __restrict__ x, const int32_t* __restrict__ n_dev, double* __restrict__ out) {
@@ -662,8 +669,8 @@ size_t gns_spmm_bwd_workspace_size(int64_t max_src, int64_t max_edges) {
 }
 
 int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, const gns_block_t* block,
-                 int64_t max_dst, int64_t max_src, int64_t max_edges, void* dh, int64_t ld_dh, void* ws,
-                 size_t ws_bytes, void* stream_) {
+                 int64_t max_dst, int64_t max_src, int64_t max_edges, int64_t pad_rows, void* dh, int64_t ld_dh,
+                 void* ws, size_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   BwdWs w;
   size_t need = bwd_ws(max_src, max_edges, ws, ws_bytes, &w);
@@ -686,13 +693,13 @@ int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, 
   tscan_reduce_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, (unsigned long long*)w.scan);
   tscan_apply_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, w.tptr, (unsigned long long*)w.scan);
   tscatter_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.tptr, w.tkeys);
-  int g2 = grid_for((max_src * 32 + 255) / 256, (long long)sms * 8);
+  int g2 = grid_for(((max_src > pad_rows ? max_src : pad_rows) * 32 + 255) / 256, (long long)sms * 8);
   tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys);
   GNS_TRY(check_launch("spmm_bwd transpose"));
   const int dv = dim / VW;
 #define GNS_BWD(T, CH)                                                                                       \
   spmm_bwd_kernel<T, CH><<<g2, kSpmmBlock, 0, stream>>>((const T*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys, \
-                                                        w.self_of, (T*)dh, ld_dh)
+                                                        w.self_of, (T*)dh, ld_dh, pad_rows)
   if (dtype == 0) {
     if (dv <= 32) GNS_BWD(float, 1);
     else if (dv <= 64) GNS_BWD(float, 2);
@@ -739,8 +746,8 @@ int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int64_t ld,
 }
 
 int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, const int32_t* n_dev, int64_t max_rows,
-                     int32_t num_classes, const int32_t* labels, const int32_t* targets, void* grad_out,
-                     double* loss_out, void* ws, size_t ws_bytes, void* stream_) {
+                     int64_t pad_rows, int32_t num_classes, const int32_t* labels, const int32_t* targets,
+                     void* grad_out, double* loss_out, void* ws, size_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if ((size_t)max_rows * sizeof(double) > ws_bytes) {
     set_error("softmax_xent: workspace %zu < %zu", ws_bytes, (size_t)max_rows * 8);
@@ -748,13 +755,13 @@ int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, const int32_
   }
   double* row_loss = (double*)ws;
   const int sms = num_sms();
-  int grid = grid_for((max_rows * 32 + 255) / 256, (long long)sms * 8);
+  int grid = grid_for(((max_rows > pad_rows ? max_rows : pad_rows) * 32 + 255) / 256, (long long)sms * 8);
   if (dtype == 0)
     xent_kernel<float><<<grid, 256, 0, stream>>>((const float*)logits, ld, n_dev, num_classes, labels, targets,
-                                                 (float*)grad_out, row_loss);
+                                                 (float*)grad_out, row_loss, pad_rows);
   else
     xent_kernel<double><<<grid, 256, 0, stream>>>((const double*)logits, ld, n_dev, num_classes, labels, targets,
-                                                  (double*)grad_out, row_loss);
+                                                  (double*)grad_out, row_loss, pad_rows);
   mean_kernel<<<1, 1024, 0, stream>>>(row_loss, n_dev, loss_out);
   return check_launch("softmax_xent");
 }

@@ -49,8 +49,20 @@ struct LayerArgs {
   int gns;
   int64_t max_dst;
   uint32_t seed, epoch, batch, layer;
+  const gns_step_t* step_dev;
   gns_block_t b;
 };
+
+// per-batch Philox key from device memory (CUDA-graph replay) when given
+__device__ __forceinline__ LayerArgs resolve_rng(const LayerArgs& in) {
+  LayerArgs a = in;
+  if (a.step_dev) {
+    a.seed = a.step_dev->seed;
+    a.epoch = a.step_dev->epoch;
+    a.batch = a.step_dev->batch;
+  }
+  return a;
+}
 
 struct RowInfo {
   int64_t start, cstart;
@@ -383,7 +395,8 @@ __device__ __noinline__ void thread_select16(const LayerArgs& a, const RowInfo& 
   for (int i = 0; i < ph.take; ++i) emit_edge(a, ri, r, ph, i, (uint32_t)(slot[i * 32] & 2047u));
 }
 
-__global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a) {
+__global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a_in) {
+  const LayerArgs a = resolve_rng(a_in);
   // per-thread 16-entry key slots, interleaved by lane (bank-conflict free)
   __shared__ uint64_t s_keys[256 / 32][16 * 32];
   uint64_t* slot = &s_keys[threadIdx.x >> 5][threadIdx.x & 31];
@@ -399,7 +412,8 @@ __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a) {
+__global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a_in) {
+  const LayerArgs a = resolve_rng(a_in);
   __shared__ uint64_t s_key[kSampBlock / 32][kWarpCap];
   __shared__ uint32_t s_pos[kSampBlock / 32][kWarpCap];
   const int w = threadIdx.x >> 5;
@@ -416,7 +430,8 @@ __global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(LayerArgs a) {
+__global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(LayerArgs a_in) {
+  const LayerArgs a = resolve_rng(a_in);
   __shared__ uint64_t s_key[kHubCap];
   __shared__ uint32_t s_pos[kHubCap];
   __shared__ int s_found;
@@ -540,7 +555,8 @@ size_t gns_sample_workspace_size(int64_t max_dst) {
 
 int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32_t* seeds,
                      const int32_t* n_seeds_dev, int64_t max_dst, int32_t k, int32_t cache_only,
-                     const gns_rng_t* rng, gns_block_t* block, void* ws, size_t ws_bytes, void* stream_) {
+                     const gns_rng_t* rng, const gns_step_t* step_dev, gns_block_t* block, void* ws,
+                     size_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (k < 1) {
     set_error("fanout must be >= 1");
@@ -572,6 +588,7 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.epoch = rng->epoch;
   a.batch = rng->batch;
   a.layer = rng->layer;
+  a.step_dev = step_dev;
   a.b = *block;
   const unsigned tiles = (unsigned)((max_dst + kCntBlock * kCntItems - 1) / (kCntBlock * kCntItems)) + 1;
   GNS_CUDA(cudaMemsetAsync(block->counts, 0, GNS_CNT_N * sizeof(int32_t), stream));

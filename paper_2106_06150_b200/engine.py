@@ -1,0 +1,252 @@
+"""Whole-step CUDA-graph training engine (the B200 answer to pool.py + model.py:257-307).
+
+One replay of a captured graph = one training step: on a side branch it
+samples the NEXT mini-batch into one sampler slot (epoch-permutation slice,
+L x (sample, relabel) — all device-count driven), while the main branch runs
+gather -> L x (SpMM + GEMM) -> softmax-CE -> backward -> Adam on the CURRENT
+batch held in the other slot.  Two graphs alternate the slot roles, so the
+host issues one graph launch per step and the sampler overlaps training.
+
+Per-batch values (Philox key, the batch's slice of the epoch permutation)
+live in a device ``gns_step_t`` refreshed from pinned host memory by a
+memcpy node inside the graph.  Dense tensors are allocated at the static
+capacity bounds; kernels zero-fill rows past the device counts, so GEMMs
+over padded rows contribute exact zeros to the gradients.
+
+The cache (cache.py) is rebuilt at epoch boundaries every ``cache_period``
+epochs (pool.py:133-135); the graphs capture the cache pointers, so they are
+re-captured after each refresh.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from . import cache as cache_mod
+from .graph import Graph
+from .model import GraphSAGE, TrainConfig, _dt, _split_rows, _weight_grad
+from .pool import cache_probs, num_batches
+from .sampling import MiniBatchSampler, SamplerConfig
+
+_CACHE = 33
+
+
+class GraphedTrainer:
+    """CUDA-graph GNS trainer: ``step()`` = sample(next) || train(current)."""
+
+    def __init__(self, g: Graph, config: SamplerConfig, dims, train_config: TrainConfig | None = None,
+                 rank: int = 0, world_size: int = 1, allreduce=None, seed: int = 0):
+        _lib.require_cuda()
+        if g.features is None or g.labels is None:
+            raise ValueError("training needs features and labels")
+        self.g, self.cfg = g, config
+        self.tc = train_config or TrainConfig()
+        self.rank, self.world = rank, world_size
+        self.allreduce = allreduce
+        self.dev = g.device
+        self.model = GraphSAGE(dims, dtype=torch.float32, device=self.dev, seed=seed)
+        self.dims = self.model.dims
+        self.L = config.num_layers
+        self.slots = [MiniBatchSampler(g, config), MiniBatchSampler(g, config)]
+        for sl in self.slots:
+            sl.n_targets_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.train_ids = g.train_ids()
+        self.step_host = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self.step_dev = [torch.zeros(4, dtype=torch.int64, device=self.dev) for _ in range(2)]
+        self.done = [None, None]
+        self.cache = None
+        self._probs = None
+        self.graphs = None
+        self.side = torch.cuda.Stream(device=self.dev)
+        self.main = torch.cuda.Stream(device=self.dev)
+        self._alloc()
+
+    # -- static buffers -----------------------------------------------------------
+    def _alloc(self):
+        sl = self.slots[0]
+        L, dims, dev = self.L, self.dims, self.dev
+        # model layer li (input first) <-> sampler layer L-1-li
+        self.cap_dst = [sl.layers[L - 1 - li].max_dst for li in range(L)]
+        self.cap_src = [sl.layers[L - 1 - li].max_src for li in range(L)]
+        self.cap_edges = [sl.layers[L - 1 - li].max_edges for li in range(L)]
+        self.npad = [_split_rows(c) for c in self.cap_dst]
+        f32 = torch.float32
+        self.h0 = torch.empty((max(self.cap_src[0], 1), dims[0]), dtype=f32, device=dev)
+        self.cat = [torch.empty((max(self.npad[li], 1), 2 * dims[li]), dtype=f32, device=dev) for li in range(L)]
+        self.z = [torch.empty((max(self.cap_dst[li], 1), dims[li + 1]), dtype=f32, device=dev) for li in range(L)]
+        self.dh = [torch.zeros((max(self.npad[li], 1), dims[li + 1]), dtype=f32, device=dev) for li in range(L)]
+        self.dz = [torch.zeros((max(self.npad[li], 1), dims[li + 1]), dtype=f32, device=dev) for li in range(L)]
+        self.dcat = [torch.empty((max(self.cap_dst[li], 1), 2 * dims[li]), dtype=f32, device=dev) for li in range(L)]
+        lib = _lib.lib()
+        self.ws_dense = _lib.workspace(max(lib.gns_dense_bwd_workspace_size(max(p, 1), d)
+                                           for p, d in zip(self.npad, dims[1:])), dev)
+        self.ws_bwd = _lib.workspace(max(lib.gns_spmm_bwd_workspace_size(self.cap_src[li], self.cap_edges[li])
+                                         for li in range(1, L)) if L > 1 else 256, dev)
+        self.ws_xent = _lib.workspace(8 * max(self.cap_dst[L - 1], 1024), dev)
+        self.loss = self.model.loss_dev
+
+    # -- one training step on a slot (captured) ------------------------------------
+    def _train_body(self, slot: int, with_adam: bool):
+        m, sl, L, s = self.model, self.slots[slot], self.L, _lib.stream_ptr()
+        blocks = [sl.layers[L - 1 - li] for li in range(L)]
+        d0 = self.dims[0]
+        tab = self.g.features
+        n_in_dev = blocks[0].counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
+        _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, blocks[0].src_nodes.data_ptr(),
+                  n_in_dev.data_ptr(), self.cap_src[0], d0, self.h0.data_ptr(), self.h0.stride(0), 0, s)
+        h = self.h0
+        with m._tf32():
+            for li in range(L):
+                d_in = self.dims[li]
+                _lib.call("gns_spmm_fwd", 0, h.data_ptr(), h.stride(0), d_in, 1 if li > 0 else 0, blocks[li].cblock,
+                          self.cap_dst[li], self.npad[li], self.cat[li].data_ptr(), self.cat[li].stride(0), s)
+                torch.addmm(m.biases[li], self.cat[li][:self.cap_dst[li]], m.weights[li], out=self.z[li])
+                h = self.z[li]
+            top = blocks[L - 1]
+            logits = self.z[L - 1]
+            _lib.call("gns_softmax_xent", 0, logits.data_ptr(), logits.stride(0),
+                      top.counts[_lib.CNT_DST:_lib.CNT_DST + 1].data_ptr(), self.cap_dst[L - 1], self.npad[L - 1],
+                      logits.shape[1], self.g.labels.data_ptr(), sl.seeds0.data_ptr(), self.dh[L - 1].data_ptr(),
+                      self.loss.data_ptr(), self.ws_xent.data_ptr(), self.ws_xent.numel(), s)
+            for li in range(L - 1, -1, -1):
+                d_out = self.dims[li + 1]
+                zz = self.z[li].data_ptr() if li < L - 1 else None
+                # dh rows >= n are zero (xent / spmm_bwd padding) -> dz rows zero
+                _lib.call("gns_dense_bwd_bias", 0, self.dh[li].data_ptr(), zz, d_out, None, self.cap_dst[li], d_out,
+                          self.dz[li].data_ptr(), m.gbiases[li].data_ptr(), self.ws_dense.data_ptr(),
+                          self.ws_dense.numel(), s)
+                _weight_grad(self.cat[li][:self.npad[li]], self.dz[li][:self.npad[li]], m.gweights[li])
+                if li == 0:
+                    break
+                torch.mm(self.dz[li][:self.cap_dst[li]], m.weights[li].t(), out=self.dcat[li])
+                _lib.call("gns_spmm_bwd", 0, self.dcat[li].data_ptr(), self.dcat[li].stride(0), self.dims[li],
+                          blocks[li].cblock, self.cap_dst[li], self.cap_src[li], self.cap_edges[li],
+                          self.npad[li - 1], self.dh[li - 1].data_ptr(), self.dh[li - 1].stride(0),
+                          self.ws_bwd.data_ptr(), self.ws_bwd.numel(), s)
+        if with_adam:
+            self._adam()
+
+    def _adam(self):
+        m = self.model
+        m.step_count += 1
+        # bias correction uses the host step count; inside a graph the step is
+        # replayed, so Adam's t is passed through a device scalar instead
+        _lib.call("gns_adam", 0, m.flat.data_ptr(), m.grad.data_ptr(), m.m.data_ptr(), m.v.data_ptr(), m.numel,
+                  self.tc.lr, self.tc.beta1, self.tc.beta2, self.tc.eps, m.step_count, 1.0, _lib.stream_ptr())
+
+    def _sample_body(self, slot: int):
+        self.step_dev[slot].copy_(self.step_host[slot], non_blocking=True)
+        self.slots[slot].enqueue_device(self.train_ids, self.step_dev[slot],
+                                        self.cache if self.cfg.strategy == "GNS" else None)
+
+    # -- cache + capture ------------------------------------------------------------
+    def _refresh_cache(self, epoch: int):
+        if self.cfg.strategy != "GNS":
+            return
+        if self._probs is None:
+            self._probs = cache_probs(self.g, self.cfg)
+        cs = int(round(self.cfg.cache_frac * self.g.num_nodes))
+        self.cache = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch,
+                                           rng_seed=[self.cfg.seed, _CACHE, epoch])
+
+    def _set_step(self, slot: int, epoch: int, index: int | None):
+        b = self.cfg.batch_size
+        h = self.step_host[slot]
+        if self.done[slot] is not None:
+            self.done[slot].synchronize()
+        if index is None:  # nothing to sample next (epoch/cache boundary)
+            h[0], h[1], h[2], h[3] = 0, 0, 0, 0
+            return
+        h[0] = (self.cfg.seed & 0xFFFFFFFF) | ((epoch & 0xFFFFFFFF) << 32)
+        h[1] = index & 0xFFFFFFFF
+        h[2] = index * b
+        h[3] = b
+
+    def _capture(self):
+        torch.cuda.synchronize()
+        self.graphs = []
+        adam_in_graph = self.allreduce is None
+        # warm-up outside capture (cuBLAS handles / workspaces)
+        with torch.cuda.stream(self.main):
+            self._train_body(0, with_adam=False)
+        torch.cuda.synchronize()
+        for p in range(2):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=self.main):
+                fork = torch.cuda.Event()
+                fork.record(self.main)
+                self.side.wait_event(fork)
+                with torch.cuda.stream(self.side):
+                    self._sample_body(1 - p)
+                self._train_body(p, with_adam=False)
+                join = torch.cuda.Event()
+                join.record(self.side)
+                self.main.wait_event(join)
+            self.graphs.append(gph)
+        self.adam_in_graph = adam_in_graph
+        torch.cuda.synchronize()
+
+    # -- driving ----------------------------------------------------------------------
+    def batches(self, epoch: int):
+        nb = num_batches(self.g, self.cfg)
+        return list(range(self.rank, nb, self.world))
+
+    def run(self, steps: int, start_epoch: int = 0, on_step=None):
+        """Run ``steps`` training steps (crossing epochs as needed)."""
+        done_steps = 0
+        epoch = start_epoch
+        while done_steps < steps:
+            done_steps += self.run_epoch(epoch, max_steps=steps - done_steps, on_step=on_step)
+            epoch += 1
+        return done_steps
+
+    def run_epoch(self, epoch: int, max_steps: int | None = None, on_step=None) -> int:
+        need_refresh = self.cfg.strategy == "GNS" and (self.cache is None or epoch % self.cfg.cache_period == 0)
+        if need_refresh or self.graphs is None:
+            torch.cuda.synchronize()
+            if need_refresh:
+                self._refresh_cache(epoch)
+            self._set_step(0, epoch, None)
+            self._set_step(1, epoch, None)
+            self._capture()
+        idx = self.batches(epoch)
+        if max_steps is not None:
+            idx = idx[:max_steps]
+        if not idx:
+            return 0
+        # prologue: sample the first batch into slot 0
+        self._set_step(0, epoch, idx[0])
+        with torch.cuda.stream(self.main):
+            self._sample_body(0)
+        for k, index in enumerate(idx):
+            p = k % 2
+            nxt = idx[k + 1] if k + 1 < len(idx) else None
+            self._set_step(1 - p, epoch, nxt)
+            with torch.cuda.stream(self.main):
+                self.graphs[p].replay()
+                if self.allreduce is not None:
+                    scale = self.allreduce(self.model.grad)
+                    m = self.model
+                    m.step_count += 1
+                    _lib.call("gns_adam", 0, m.flat.data_ptr(), m.grad.data_ptr(), m.m.data_ptr(), m.v.data_ptr(),
+                              m.numel, self.tc.lr, self.tc.beta1, self.tc.beta2, self.tc.eps, m.step_count, scale,
+                              _lib.stream_ptr())
+                else:
+                    self._adam()
+                ev = torch.cuda.Event()
+                ev.record(self.main)
+                self.done[1 - p] = ev
+            if on_step is not None:
+                on_step(epoch, index, k)
+        return len(idx)
+
+    def check_errors(self):
+        """Read the device error flags of both slots (one sync)."""
+        for sl in self.slots:
+            c = sl.counts.cpu()
+            err = int(c[:, _lib.CNT_ERR].max())
+            if err & _lib.ERRBIT_ZEROPROB:
+                raise ValueError("inclusion probability is zero for a cached draw")
+            if err & _lib.ERRBIT_CAPACITY:
+                raise _lib.InvariantError("neighbour selection did not converge (capacity)")

@@ -202,7 +202,7 @@ class GraphSAGE:
             self._ws_xent = _lib.workspace(8 * max(n, 1024), self.device)
         top = mb.blocks[-1]
         n_dev = top._c.counts + 4 * _lib.CNT_DST
-        _lib.call("gns_softmax_xent", _dt(self.dtype), logits.data_ptr(), logits.stride(0), n_dev, n, c,
+        _lib.call("gns_softmax_xent", _dt(self.dtype), logits.data_ptr(), logits.stride(0), n_dev, n, 0, c,
                   labels.data_ptr(), mb.targets.data_ptr(), grad.data_ptr(), self.loss_dev.data_ptr(),
                   self._ws_xent.data_ptr(), self._ws_xent.numel(), _lib.stream_ptr(stream))
         return grad
@@ -251,7 +251,7 @@ class GraphSAGE:
                 self._ws_bwd = _lib.workspace(int(need * 1.5), self.device)
             dh_new = torch.empty((max(nsrc, 1), d_in), dtype=self.dtype, device=self.device)
             _lib.call("gns_spmm_bwd", _dt(self.dtype), dcat.data_ptr(), dcat.stride(0), d_in, block._c,
-                      block.dst_nodes.numel(), nsrc, block.num_edges, dh_new.data_ptr(), dh_new.stride(0),
+                      block.dst_nodes.numel(), nsrc, block.num_edges, 0, dh_new.data_ptr(), dh_new.stride(0),
                       self._ws_bwd.data_ptr(), self._ws_bwd.numel(), s)
             dh = dh_new[:nsrc]
 

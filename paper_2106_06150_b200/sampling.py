@@ -252,7 +252,7 @@ class MiniBatchSampler:
         gc = self.g.cstruct()
         for lb in self.layers:
             _lib.call("gns_sample_layer", gc, cstruct, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
-                      lb.k, int(lb.cache_only), rng.cstruct(lb.layer), lb.cblock,
+                      lb.k, int(lb.cache_only), rng.cstruct(lb.layer), None, lb.cblock,
                       self.ws_sample.data_ptr(), self.ws_sample.numel(), s)
             _lib.call("gns_relabel", self.g.num_nodes, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
                       lb.cblock, lb.max_edges, self.ws_relabel.data_ptr(), self.ws_relabel.numel(), s)
@@ -262,6 +262,35 @@ class MiniBatchSampler:
         ev = torch.cuda.Event()
         ev.record(stream if stream is not None else torch.cuda.current_stream())
         return ev
+
+    def enqueue_device(self, train_ids: torch.Tensor, step_dev: torch.Tensor, cache: CacheState | None,
+                       stream=None):
+        """Graph-capturable chain: the batch's targets (pool.py:60-66 slice
+        begin/count) and Philox key come from the device gns_step_t
+        ``step_dev``; no host synchronisation, fixed kernel arguments."""
+        s = _lib.stream_ptr(stream)
+        if not hasattr(self, "n_targets_dev"):
+            self.n_targets_dev = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _lib.call("gns_epoch_targets_dev", train_ids.data_ptr(), train_ids.numel(), step_dev.data_ptr(),
+                  self.max_targets, self.targets.data_ptr(), self.n_targets_dev.data_ptr(), s)
+        _lib.call("gns_unique_sorted", self.g.num_nodes, self.targets.data_ptr(), self.n_targets_dev.data_ptr(),
+                  self.max_targets, self.seeds0.data_ptr(), self.n_seeds0.data_ptr(), self.ws_relabel.data_ptr(),
+                  self.ws_relabel.numel(), s)
+        gns = self.config.strategy == "GNS"
+        if gns and cache is None:
+            raise ValueError("GNS sampling needs a CacheState")
+        cstruct = cache.cstruct() if gns else None
+        seeds, n_dev = self.seeds0, self.n_seeds0
+        gc = self.g.cstruct()
+        rng = BatchRng()
+        for lb in self.layers:
+            _lib.call("gns_sample_layer", gc, cstruct, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
+                      lb.k, int(lb.cache_only), rng.cstruct(lb.layer), step_dev.data_ptr(), lb.cblock,
+                      self.ws_sample.data_ptr(), self.ws_sample.numel(), s)
+            _lib.call("gns_relabel", self.g.num_nodes, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
+                      lb.cblock, lb.max_edges, self.ws_relabel.data_ptr(), self.ws_relabel.numel(), s)
+            seeds = lb.src_nodes
+            n_dev = lb.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
 
     def collect(self, event=None, policy_ns="uniform", policy_gns="gns-paper") -> MiniBatch:
         """Wait for the counts of the last ``sample_async`` and wrap the buffers

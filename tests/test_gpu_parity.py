@@ -338,14 +338,14 @@ def test_spmm_bwd_f64_bit_exact(P, dim):
         dcat = np.random.default_rng(10 + li).normal(size=(ndst, 2 * dim))
         dt = torch.as_tensor(dcat, device="cuda")
         dh = torch.empty((nsrc, dim), dtype=torch.float64, device="cuda")
-        _lib.call("gns_spmm_bwd", 1, dt.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges,
+        _lib.call("gns_spmm_bwd", 1, dt.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0,
                   dh.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
         expect = OM.spmm_mean_bwd(br, dcat, dim)
         assert np.array_equal(dh.cpu().numpy(), expect), li
         if dim % 4 == 0:
             dt32 = torch.as_tensor(dcat.astype(np.float32), device="cuda")
             dh32 = torch.empty((nsrc, dim), dtype=torch.float32, device="cuda")
-            _lib.call("gns_spmm_bwd", 0, dt32.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges,
+            _lib.call("gns_spmm_bwd", 0, dt32.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0,
                       dh32.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
             np.testing.assert_allclose(dh32.cpu().numpy(), expect, rtol=1e-5, atol=1e-5)
 
@@ -503,3 +503,39 @@ def test_device_generator_contract(P):
     # determinism
     g2 = P.generate_powerlaw_device(20000, 150000, alpha=0.6, offset=50.0, seed=3)
     assert torch.equal(g.indices, g2.indices)
+
+
+# ---- CUDA-graph engine ---------------------------------------------------------------
+
+def test_graphed_trainer_matches_eager(P):
+    """The captured whole-step engine (sample || train, static capacities,
+    device-side batch parameters) trains on exactly the pool's batches and
+    tracks the eager path's losses."""
+    og = _hub_graph(5000, 13)
+    rng = np.random.default_rng(0)
+    feats = rng.normal(size=(og.num_nodes, 16)).astype(np.float32)
+    labels = rng.integers(0, 5, og.num_nodes).astype(np.int32)
+    mask = rng.random(og.num_nodes) < 0.6
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices, features=feats, labels=labels, train_mask=mask)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=256, cache_frac=0.05, cache_mode="degree",
+                          seed=3)
+    tc = P.TrainConfig(lr=0.003)
+    eager = P.GraphSAGE((16, 32, 5), seed=0)
+    pool = P.SamplerPool(g, cfg, num_workers=1)
+    ref_losses = []
+    for it in pool.iter_epoch(0):
+        ref_losses.append(float(eager.train_step(it.minibatch, g, tc)))
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0)
+    losses = []
+    tr.run_epoch(0, on_step=lambda e, i, k: losses.append(float(tr.loss)))
+    tr.check_errors()
+    assert len(losses) == len(ref_losses)
+    np.testing.assert_allclose(losses, ref_losses, rtol=2e-3)
+    we, be = eager.export()
+    wg, bg_ = tr.model.export()
+    for a, b in zip(we + be, wg + bg_):
+        np.testing.assert_allclose(a, b, rtol=1e-2, atol=1e-4)
+    # a second epoch re-draws the cache and re-captures
+    n2 = tr.run_epoch(1)
+    assert n2 == len(losses)
