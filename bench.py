@@ -209,39 +209,16 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
-    model = P.GraphSAGE(dims, dtype=torch.float32, seed=0)
     tc = P.TrainConfig(lr=0.003, hidden_dim=c["hidden"])
-    pool = P.SamplerPool(g, cfg, num_workers=args.workers, rank=rank, world_size=world)
 
     def allreduce(grad):
         dist.all_reduce(grad)
         return 1.0 / world
 
-    ar = allreduce if world > 1 else None
-    it = batch_stream(pool)
-    ev_pairs = []
-
-    def step(timed):
-        item = next(it)
-        mb = item.minibatch
-        if timed:
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record()
-        h = model.gather_inputs(mb, g)
-        if timed:
-            e1.record()
-        logits, saved = model.forward(mb, h)
-        if timed:
-            e2.record()
-            ev_pairs.append((e0, e1, e2, mb.input_nodes.numel(),
-                             sum(b.num_edges for b in mb.blocks), mb.blocks[0].dst_nodes.numel()))
-        dl = model.loss_and_grad(logits, g.labels, mb)
-        model.backward(mb, saved, dl)
-        scale = ar(model.grad) if ar else 1.0
-        model.adam_step(tc, grad_scale=scale)
-
-    for _ in range(args.warmup):
-        step(False)
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    tr = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world,
+                        allreduce=allreduce if world > 1 else None, seed=0)
+    pos = tr.run(args.warmup, epoch=0, first=0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -250,25 +227,36 @@ def main():
     l0 = _lib.launch_counter[0]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record()
-    for _ in range(args.steps):
-        step(True)
-    t_end.record()
+    t_start.record(tr.main)
+    pos = tr.run(args.steps, epoch=pos[0], first=pos[1])
+    t_end.record(tr.main)
     t_end.synchronize()
-    launches = _lib.launch_counter[0] - l0
     clk = clocks.stop()
+    launches = _lib.launch_counter[0] - l0
+    # graph replays launch the captured kernels: count them per replay
+    per_replay = tr.kernels_per_step()
+    launches_total = launches + per_replay * args.steps
     ms = t_start.elapsed_time(t_end)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = args.steps * world / (ms / 1e3)
+    tr.check_errors()
 
-    # gather roofline (algorithmic bytes: rows read + rows written + ids)
+    # gather roofline: same graph re-captured with timing events around the
+    # gather, replayed on the following batches (algorithmic bytes: rows read
+    # + rows written + int32 ids)
     peak, peak_kind = load_peaks()
-    gather_ms = [a.elapsed_time(b) for a, b, _, _, _, _ in ev_pairs]
-    fwd_ms = [b.elapsed_time(cc) for _, b, cc, _, _, _ in ev_pairs]
-    n_in = np.array([p[3] for p in ev_pairs], dtype=np.float64)
+    gather_ms, n_in = [], []
+    tr.capture_profiled()
+    nprof = min(30, args.steps)
+
+    def on_step(e, i, k):
+        gather_ms.append(tr.gather_ms())
+        n_in.append(int(tr.slots[k % 2].counts[len(FANOUTS) - 1, _lib.CNT_SRC]))
+    pos = tr.run(nprof, epoch=pos[0], first=pos[1], on_step=on_step)
+    n_in = np.array(n_in, dtype=np.float64)
     row_bytes = 4 * c["dim"]
     gbytes = n_in * (2 * row_bytes + 4)
     gather_gbs = float(gbytes.sum() / (np.sum(gather_ms) / 1e3) / 1e9)
@@ -277,45 +265,47 @@ def main():
                 "frac": round(gather_gbs / peak, 4), "traffic": None,
                 "algorithmic_bytes_per_launch": float(gbytes.mean()),
                 "avg_launch_ms": float(np.mean(gather_ms)),
-                "share_of_step": float(np.sum(gather_ms) / ms)}
+                "share_of_step": float(np.mean(gather_ms) / (ms / args.steps)),
+                "measured": f"CUDA events around the gather inside the captured step graph, {nprof} replays"}
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_path):
         try:
-            tr = json.load(open(prof_path)).get(args.config, {}).get("gather_f32x4_kernel")
-            roofline["traffic"] = tr
+            tr_ = json.load(open(prof_path)).get(args.config, {}).get("gather_f32x4_kernel")
+            if tr_:
+                roofline["traffic"] = tr_
         except Exception:
             pass
+    pool = tr
 
-    # end-to-end through the public API with host buffers
+    # end-to-end through the public API with host buffers: targets from pinned
+    # host memory every step (memcpy node in the graph), loss read back to the
+    # host every step (D2H + sync)
     e2e = None
     if rank == 0 and world == 1:
         k2 = args.e2e_steps if args.e2e_steps is not None else max(5, args.steps // 2)
-        ids_host = g.train_ids().cpu().numpy().astype(np.int64)
-        perm = np.random.default_rng(1).permutation(ids_host)
-        tgt = torch.empty(BATCH, dtype=torch.int64).pin_memory()
-        eng = P.MiniBatchSampler(g, cfg)
-        cache = pool.cache
-        lossh = torch.empty(1, dtype=torch.float64).pin_memory()
-        for i in range(2):
-            tgt.copy_(torch.from_numpy(perm[i * BATCH:(i + 1) * BATCH]))
-            mb = eng.sample(tgt.to("cuda", non_blocking=True), P.BatchRng(0, 99, i), cache)
-            lossh.copy_(model.train_step(mb, g, tc))
-        torch.cuda.synchronize()
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record()
-        for i in range(k2):
-            j = (i + 2) % (len(perm) // BATCH)
-            tgt.copy_(torch.from_numpy(perm[j * BATCH:(j + 1) * BATCH]))
-            mb = eng.sample(tgt.to("cuda", non_blocking=True), P.BatchRng(0, 99, i + 2), cache)
-            lossh.copy_(model.train_step(mb, g, tc))
-            float(lossh[0])
-        s1.record()
-        s1.synchronize()
-        e_ms = s0.elapsed_time(s1)
-        e2e = {"value": k2 / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": BATCH * 8,
-               "d2h_bytes_per_step": 8 + 4 * 8 * len(FANOUTS), "steps": k2,
-               "path": "MiniBatchSampler.sample(host int64 targets) + GraphSAGE.train_step + loss.item()"}
+        if k2 > 0:
+            ids_host = g.train_ids().cpu().numpy().astype(np.int64)
+            perm = np.random.default_rng(1).permutation(ids_host)
+            nb = len(perm) // BATCH
+            batches = [perm[(j % nb) * BATCH:((j % nb) + 1) * BATCH] for j in range(k2 + 2)]
+            te = GraphedTrainer(g, cfg, dims, tc, seed=0, host_targets=True)
+            te.cache = tr.cache
+            te.run_host(batches[:2], epoch=0)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(te.main)
+            te.run_host(batches[2:], epoch=0)
+            s1.record(te.main)
+            s1.synchronize()
+            wall = time.perf_counter() - w0
+            e2e = {"value": k2 / wall, "unit": UNIT, "h2d_bytes_per_step": BATCH * 4 + 4 + 32,
+                   "d2h_bytes_per_step": 8, "steps": k2,
+                   "path": "GraphedTrainer(host_targets=True).run_host: pinned host targets -> graph memcpy node, "
+                           "loss -> host each step; wall clock",
+                   "device_ms_per_step": s0.elapsed_time(s1) / k2}
+            del te
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -329,11 +319,10 @@ def main():
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "gpu_launches_per_step": launches / args.steps, "clocks": clk,
-                "per_step": {"input_nodes": float(n_in.mean()),
-                             "sampled_edges": float(np.mean([p[4] for p in ev_pairs])),
-                             "gather_ms": float(np.mean(gather_ms)), "fwd_ms": float(np.mean(fwd_ms))}}
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
+                "gpu_launches_per_step": launches_total / args.steps, "clocks": clk,
+                "per_step": {"input_nodes": float(n_in.mean()), "gather_ms": float(np.mean(gather_ms)),
+                             "graph_replays": args.steps}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -36,7 +36,7 @@ class GraphedTrainer:
     """CUDA-graph GNS trainer: ``step()`` = sample(next) || train(current)."""
 
     def __init__(self, g: Graph, config: SamplerConfig, dims, train_config: TrainConfig | None = None,
-                 rank: int = 0, world_size: int = 1, allreduce=None, seed: int = 0):
+                 rank: int = 0, world_size: int = 1, allreduce=None, seed: int = 0, host_targets: bool = False):
         _lib.require_cuda()
         if g.features is None or g.labels is None:
             raise ValueError("training needs features and labels")
@@ -55,9 +55,16 @@ class GraphedTrainer:
         self.step_host = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(2)]
         self.step_dev = [torch.zeros(4, dtype=torch.int64, device=self.dev) for _ in range(2)]
         self.done = [None, None]
+        # host-provided targets (the end-to-end API): pinned buffers copied by
+        # memcpy nodes inside the graph
+        self.host_targets = host_targets
+        B = config.batch_size
+        self.tgt_host = [torch.zeros(B, dtype=torch.int32).pin_memory() for _ in range(2)]
+        self.ntgt_host = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2)]
         self.cache = None
         self._probs = None
         self.graphs = None
+        self._prof_events = None
         self.side = torch.cuda.Stream(device=self.dev)
         self.main = torch.cuda.Stream(device=self.dev)
         self._alloc()
@@ -93,8 +100,13 @@ class GraphedTrainer:
         d0 = self.dims[0]
         tab = self.g.features
         n_in_dev = blocks[0].counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
+        ev = self._prof_events
+        if ev is not None:
+            ev[0].record()
         _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, blocks[0].src_nodes.data_ptr(),
                   n_in_dev.data_ptr(), self.cap_src[0], d0, self.h0.data_ptr(), self.h0.stride(0), 0, s)
+        if ev is not None:
+            ev[1].record()
         h = self.h0
         with m._tf32():
             for li in range(L):
@@ -136,9 +148,14 @@ class GraphedTrainer:
                   self.tc.lr, self.tc.beta1, self.tc.beta2, self.tc.eps, m.step_count, 1.0, _lib.stream_ptr())
 
     def _sample_body(self, slot: int):
+        sl = self.slots[slot]
         self.step_dev[slot].copy_(self.step_host[slot], non_blocking=True)
-        self.slots[slot].enqueue_device(self.train_ids, self.step_dev[slot],
-                                        self.cache if self.cfg.strategy == "GNS" else None)
+        if self.host_targets:
+            B = self.cfg.batch_size
+            sl.targets[:B].copy_(self.tgt_host[slot], non_blocking=True)
+            sl.n_targets_dev.copy_(self.ntgt_host[slot], non_blocking=True)
+        sl.enqueue_device(None if self.host_targets else self.train_ids, self.step_dev[slot],
+                          self.cache if self.cfg.strategy == "GNS" else None)
 
     # -- cache + capture ------------------------------------------------------------
     def _refresh_cache(self, epoch: int):
@@ -163,15 +180,32 @@ class GraphedTrainer:
         h[2] = index * b
         h[3] = b
 
+    def capture_profiled(self):
+        """Re-capture with timing events around the input-feature gather
+        (gns_gather_rows) so its per-launch duration can be read after each
+        replay (used by bench.py for the roofline; not for the headline)."""
+        self._prof_events = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        self._capture()
+
+    def gather_ms(self) -> float:
+        e = self._prof_events
+        e[1].synchronize()
+        return float(e[0].elapsed_time(e[1]))
+
     def _capture(self):
         torch.cuda.synchronize()
         self.graphs = []
         adam_in_graph = self.allreduce is None
         # warm-up outside capture (cuBLAS handles / workspaces)
+        ev, self._prof_events = self._prof_events, None
         with torch.cuda.stream(self.main):
             self._train_body(0, with_adam=False)
+        self._prof_events = ev
         torch.cuda.synchronize()
+        c0 = _lib.launch_counter[0]
         for p in range(2):
+            if p == 1:
+                self._per_replay = _lib.launch_counter[0] - c0
             gph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gph, stream=self.main):
                 fork = torch.cuda.Event()
@@ -184,25 +218,38 @@ class GraphedTrainer:
                 join.record(self.side)
                 self.main.wait_event(join)
             self.graphs.append(gph)
+        # captured launches are not executions: remove them from the counter
+        _lib.launch_counter[0] = c0
         self.adam_in_graph = adam_in_graph
         torch.cuda.synchronize()
+
+    def kernels_per_step(self) -> int:
+        """libgns kernels inside one captured step graph (replayed per step)."""
+        return int(getattr(self, "_per_replay", 0))
 
     # -- driving ----------------------------------------------------------------------
     def batches(self, epoch: int):
         nb = num_batches(self.g, self.cfg)
         return list(range(self.rank, nb, self.world))
 
-    def run(self, steps: int, start_epoch: int = 0, on_step=None):
-        """Run ``steps`` training steps (crossing epochs as needed)."""
-        done_steps = 0
-        epoch = start_epoch
-        while done_steps < steps:
-            done_steps += self.run_epoch(epoch, max_steps=steps - done_steps, on_step=on_step)
-            epoch += 1
-        return done_steps
+    def run(self, steps: int, epoch: int = 0, first: int = 0, on_step=None):
+        """Run ``steps`` training steps starting at batch ``first`` of
+        ``epoch`` (crossing epochs as needed); returns the (epoch, first)
+        position to continue from."""
+        while steps > 0:
+            n = self.run_epoch(epoch, first=first, max_steps=steps, on_step=on_step)
+            steps -= n
+            if first + n >= len(self.batches(epoch)):
+                epoch, first = epoch + 1, 0
+            else:
+                first += n
+        return epoch, first
 
-    def run_epoch(self, epoch: int, max_steps: int | None = None, on_step=None) -> int:
-        need_refresh = self.cfg.strategy == "GNS" and (self.cache is None or epoch % self.cfg.cache_period == 0)
+    def run_epoch(self, epoch: int, first: int = 0, max_steps: int | None = None, on_step=None) -> int:
+        need_refresh = self.cfg.strategy == "GNS" and first == 0 and \
+            (self.cache is None or epoch % self.cfg.cache_period == 0)
+        if self.cfg.strategy == "GNS" and self.cache is None:
+            need_refresh = True
         if need_refresh or self.graphs is None:
             torch.cuda.synchronize()
             if need_refresh:
@@ -210,7 +257,7 @@ class GraphedTrainer:
             self._set_step(0, epoch, None)
             self._set_step(1, epoch, None)
             self._capture()
-        idx = self.batches(epoch)
+        idx = self.batches(epoch)[first:]
         if max_steps is not None:
             idx = idx[:max_steps]
         if not idx:
@@ -240,6 +287,51 @@ class GraphedTrainer:
             if on_step is not None:
                 on_step(epoch, index, k)
         return len(idx)
+
+    def run_host(self, batches, epoch: int = 0, on_loss=None):
+        """End-to-end API with host buffers: ``batches`` are host int arrays of
+        target ids; every step copies them from pinned memory (memcpy node in
+        the graph) and reads the loss back to the host.  Requires
+        ``host_targets=True``."""
+        if not self.host_targets:
+            raise ValueError("construct with host_targets=True")
+        if self.graphs is None or (self.cfg.strategy == "GNS" and self.cache is None):
+            if self.cfg.strategy == "GNS" and self.cache is None:
+                self._refresh_cache(epoch)
+            self._capture()
+        losses = []
+
+        def put(slot, k):
+            if self.done[slot] is not None:
+                self.done[slot].synchronize()
+            if k is None:
+                self.ntgt_host[slot][0] = 0
+                return
+            t = torch.as_tensor(batches[k], dtype=torch.int32)
+            self.tgt_host[slot][:t.numel()].copy_(t)
+            self.ntgt_host[slot][0] = t.numel()
+            h = self.step_host[slot]
+            h[0] = (self.cfg.seed & 0xFFFFFFFF) | ((epoch & 0xFFFFFFFF) << 32)
+            h[1] = k & 0xFFFFFFFF
+        put(0, 0)
+        with torch.cuda.stream(self.main):
+            self._sample_body(0)
+        lh = torch.zeros(1, dtype=torch.float64).pin_memory()
+        for k in range(len(batches)):
+            p = k % 2
+            put(1 - p, k + 1 if k + 1 < len(batches) else None)
+            with torch.cuda.stream(self.main):
+                self.graphs[p].replay()
+                self._adam()
+                lh.copy_(self.loss, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.main)
+                self.done[1 - p] = ev
+            ev.synchronize()
+            losses.append(float(lh[0]))
+            if on_loss is not None:
+                on_loss(k, losses[-1])
+        return losses
 
     def check_errors(self):
         """Read the device error flags of both slots (one sync)."""

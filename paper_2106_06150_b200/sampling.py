@@ -263,16 +263,19 @@ class MiniBatchSampler:
         ev.record(stream if stream is not None else torch.cuda.current_stream())
         return ev
 
-    def enqueue_device(self, train_ids: torch.Tensor, step_dev: torch.Tensor, cache: CacheState | None,
+    def enqueue_device(self, train_ids: torch.Tensor | None, step_dev: torch.Tensor, cache: CacheState | None,
                        stream=None):
         """Graph-capturable chain: the batch's targets (pool.py:60-66 slice
         begin/count) and Philox key come from the device gns_step_t
-        ``step_dev``; no host synchronisation, fixed kernel arguments."""
+        ``step_dev``; no host synchronisation, fixed kernel arguments.  With
+        ``train_ids=None`` the caller already wrote ``targets`` and
+        ``n_targets_dev`` (host-provided targets)."""
         s = _lib.stream_ptr(stream)
         if not hasattr(self, "n_targets_dev"):
             self.n_targets_dev = torch.zeros(1, dtype=torch.int32, device=self.device)
-        _lib.call("gns_epoch_targets_dev", train_ids.data_ptr(), train_ids.numel(), step_dev.data_ptr(),
-                  self.max_targets, self.targets.data_ptr(), self.n_targets_dev.data_ptr(), s)
+        if train_ids is not None:
+            _lib.call("gns_epoch_targets_dev", train_ids.data_ptr(), train_ids.numel(), step_dev.data_ptr(),
+                      self.max_targets, self.targets.data_ptr(), self.n_targets_dev.data_ptr(), s)
         _lib.call("gns_unique_sorted", self.g.num_nodes, self.targets.data_ptr(), self.n_targets_dev.data_ptr(),
                   self.max_targets, self.seeds0.data_ptr(), self.n_seeds0.data_ptr(), self.ws_relabel.data_ptr(),
                   self.ws_relabel.numel(), s)
