@@ -120,6 +120,11 @@ typedef struct gns_block {
 GNS_API const char* gns_last_error(void);
 GNS_API int gns_version(void);
 
+/* Record a CUDA event on a stream with cudaEventRecordExternal, so an event
+ * recorded while a stream is being captured into a CUDA graph fires (and can
+ * be timed / waited on) at every replay.  Used for in-graph kernel timing. */
+GNS_API int gns_record_event_external(void* event, void* stream);
+
 /* ---- cache engine (cache.py) ------------------------------------------- */
 
 /* degree_probs (cache.py:53-58): out[i] = deg(i) / E in float64. */

@@ -66,6 +66,7 @@ class GnsBlock(Structure):
 _SIGS = {
     "gns_last_error": (ctypes.c_char_p, []),
     "gns_version": (c_int32, []),
+    "gns_record_event_external": (c_int32, [c_void_p, c_void_p]),
     "gns_degree_probs": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p]),
     "gns_cache_draw_workspace_size": (c_size_t, [c_int64]),
     "gns_cache_draw": (c_int32, [c_void_p, c_int64, c_int64, c_uint32, c_uint32, c_void_p,

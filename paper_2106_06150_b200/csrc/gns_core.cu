@@ -121,6 +121,11 @@ const char* gns_last_error(void) { return g_err; }
 
 int gns_version(void) { return 1; }
 
+int gns_record_event_external(void* event, void* stream) {
+  GNS_CUDA(cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream, cudaEventRecordExternal));
+  return GNS_OK;
+}
+
 int gns_degree_probs(const gns_graph_t* g, double* out_probs, void* stream) {
   if (!g || g->num_edges <= 0) {
     set_error("graph has no edges; degree distribution undefined");

@@ -102,11 +102,11 @@ class GraphedTrainer:
         n_in_dev = blocks[0].counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
         ev = self._prof_events
         if ev is not None:
-            ev[0].record()
+            _lib.call("gns_record_event_external", ev[0].cuda_event, s)
         _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, blocks[0].src_nodes.data_ptr(),
                   n_in_dev.data_ptr(), self.cap_src[0], d0, self.h0.data_ptr(), self.h0.stride(0), 0, s)
         if ev is not None:
-            ev[1].record()
+            _lib.call("gns_record_event_external", ev[1].cuda_event, s)
         h = self.h0
         with m._tf32():
             for li in range(L):
@@ -185,6 +185,9 @@ class GraphedTrainer:
         (gns_gather_rows) so its per-launch duration can be read after each
         replay (used by bench.py for the roofline; not for the headline)."""
         self._prof_events = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        for e in self._prof_events:      # materialise the driver events
+            e.record(self.main)
+        torch.cuda.synchronize()
         self._capture()
 
     def gather_ms(self) -> float:
@@ -222,6 +225,11 @@ class GraphedTrainer:
         _lib.launch_counter[0] = c0
         self.adam_in_graph = adam_in_graph
         torch.cuda.synchronize()
+
+    def loss_value(self) -> float:
+        """Loss of the last replayed step (synchronises the engine stream)."""
+        self.main.synchronize()
+        return float(self.loss[0])
 
     def kernels_per_step(self) -> int:
         """libgns kernels inside one captured step graph (replayed per step)."""

@@ -528,7 +528,7 @@ def test_graphed_trainer_matches_eager(P):
     from paper_2106_06150_b200.engine import GraphedTrainer
     tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0)
     losses = []
-    tr.run_epoch(0, on_step=lambda e, i, k: losses.append(float(tr.loss)))
+    tr.run_epoch(0, on_step=lambda e, i, k: losses.append(tr.loss_value()))
     tr.check_errors()
     assert len(losses) == len(ref_losses)
     np.testing.assert_allclose(losses, ref_losses, rtol=2e-3)
