@@ -249,12 +249,15 @@ GNS_API int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim
  * dh[s,:] = sum_{e: src=s, ascending dst} w_e * (dcat[dst_e, D:2D] / max(deg,1))
  *           (+ dcat[d, 0:D] where self_pos[d] == s).
  * Builds the transposed block CSR in the workspace.  Rows [n_src, pad_rows)
- * of dh are zero-filled. */
-GNS_API size_t gns_spmm_bwd_workspace_size(int64_t max_src, int64_t max_edges);
+ * of dh are zero-filled.  Fused epilogue of the previous layer's backward
+ * (model.py:218,220): with z_mask != NULL the output is relu'(z) * dh (z has
+ * the row stride ld_dh), and with db != NULL the column sums of the output
+ * (the previous layer's bias gradient) are written to db. */
+GNS_API size_t gns_spmm_bwd_workspace_size(int64_t max_src, int64_t max_edges, int32_t dim);
 GNS_API int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim,
                  const gns_block_t* block, int64_t max_dst, int64_t max_src,
-                 int64_t max_edges, int64_t pad_rows, void* dh, int64_t ld_dh, void* ws,
-                 size_t ws_bytes, void* stream);
+                 int64_t max_edges, int64_t pad_rows, const void* z_mask, void* db,
+                 void* dh, int64_t ld_dh, void* ws, size_t ws_bytes, void* stream);
 
 /* relu backward fused with the bias gradient (model.py:218,220):
  * dz = (z > 0) ? dh : 0 (skipped when z == NULL: the output layer), db[c] =

@@ -101,10 +101,10 @@ _SIGS = {
     "gns_bitmap_rank": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
     "gns_spmm_fwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, c_int32, POINTER(GnsBlock),
                                c_int64, c_int64, c_void_p, c_int64, c_void_p]),
-    "gns_spmm_bwd_workspace_size": (c_size_t, [c_int64, c_int64]),
+    "gns_spmm_bwd_workspace_size": (c_size_t, [c_int64, c_int64, c_int32]),
     "gns_spmm_bwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, POINTER(GnsBlock), c_int64,
-                               c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_size_t,
-                               c_void_p]),
+                               c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
+                               c_void_p, c_size_t, c_void_p]),
     "gns_dense_bwd_workspace_size": (c_size_t, [c_int64, c_int32]),
     "gns_dense_bwd_bias": (c_int32, [c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int32,
                                      c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
@@ -171,7 +171,7 @@ KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
     "gns_cached_csr_fill": 1, "gns_sample_layer": 5, "gns_relabel": 5, "gns_unique_sorted": 4,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
-    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 6,
+    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 7,
     "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1,
 }
 launch_counter = [0]

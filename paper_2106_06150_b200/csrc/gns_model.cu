@@ -363,7 +363,9 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
                                                               BlockView bv, const int32_t* __restrict__ tptr,
                                                               const uint64_t* __restrict__ tkeys,
                                                               const int32_t* __restrict__ self_of,
-                                                              T* __restrict__ dh, int64_t ld_dh, int64_t pad_rows) {
+                                                              T* __restrict__ dh, int64_t ld_dh, int64_t pad_rows,
+                                                              const T* __restrict__ zmask,
+                                                              T* __restrict__ colpart) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   constexpr bool EXACT = sizeof(T) == 8;
@@ -372,6 +374,13 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
   const int dv = dim / VW;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // fused epilogue (model.py:218,220): dz = relu'(z) * dh and per-block
+  // column partial sums of dz for the bias gradient (requires dv <= 32*CH)
+  T colacc[CH][VW];
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int q = 0; q < VW; ++q) colacc[j][q] = (T)0;
   for (int64_t s = gw; s < n; s += nw) {
     const int b = tptr[s], e_end = tptr[s + 1];
     const int sd = self_of[s];
@@ -427,8 +436,19 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
         }
         V out;
         T* op = reinterpret_cast<T*>(&out);
+        if (zmask) {
+          V zv = reinterpret_cast<const V*>(zmask + s * ld_dh)[c];
+          const T* zp = reinterpret_cast<const T*>(&zv);
 #pragma unroll
-        for (int q = 0; q < VW; ++q) op[q] = acc[j][q];
+          for (int q = 0; q < VW; ++q) op[q] = zp[q] > (T)0 ? acc[j][q] : (T)0;
+        } else {
+#pragma unroll
+          for (int q = 0; q < VW; ++q) op[q] = acc[j][q];
+        }
+        if (c0 == 0) {
+#pragma unroll
+          for (int q = 0; q < VW; ++q) colacc[j][q] += op[q];
+        }
         reinterpret_cast<V*>(dh + s * ld_dh)[c] = out;
       }
     }
@@ -437,6 +457,21 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
     V zero;
     vzero(zero);
     for (int c = lane; c < dv; c += 32) reinterpret_cast<V*>(dh + s * ld_dh)[c] = zero;
+  }
+  if (colpart) {
+    __shared__ T red[kSpmmBlock / 32][32 * CH * VW];
+    const int wib = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int q = 0; q < VW; ++q) red[wib][(lane + 32 * j) * VW + q] = colacc[j][q];
+    __syncthreads();
+    for (int col = threadIdx.x; col < dim; col += blockDim.x) {
+      T t = 0;
+#pragma unroll
+      for (int w = 0; w < kSpmmBlock / 32; ++w) t += red[w][col];
+      colpart[(int64_t)blockIdx.x * dim + col] = t;
+    }
   }
 }
 
@@ -480,6 +515,7 @@ __global__ void colsum_final_kernel(const T* __restrict__ partial, int nblocks, 
 }
 
 struct BwdWs {
+  void* colpart;
   int32_t* tcount;
   int32_t* tptr;
   int32_t* self_of;
@@ -488,8 +524,9 @@ struct BwdWs {
   long long tiles;
 };
 
-static size_t bwd_ws(int64_t max_src, int64_t max_edges, void* base, size_t cap, BwdWs* w) {
+static size_t bwd_ws(int64_t max_src, int64_t max_edges, int32_t dim, void* base, size_t cap, BwdWs* w) {
   Workspace ws(base, cap);
+  w->colpart = (void*)ws.take<double>((size_t)num_sms() * 8 * (size_t)(dim > 0 ? dim : 1));
   w->tcount = ws.take<int32_t>(max_src + 1);
   w->tptr = ws.take<int32_t>(max_src + 1);
   w->self_of = ws.take<int32_t>(max_src + 1);
@@ -663,17 +700,17 @@ int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_
   return check_launch("spmm_fwd");
 }
 
-size_t gns_spmm_bwd_workspace_size(int64_t max_src, int64_t max_edges) {
+size_t gns_spmm_bwd_workspace_size(int64_t max_src, int64_t max_edges, int32_t dim) {
   BwdWs w;
-  return bwd_ws(max_src, max_edges, nullptr, 0, &w);
+  return bwd_ws(max_src, max_edges, dim, nullptr, 0, &w);
 }
 
 int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, const gns_block_t* block,
-                 int64_t max_dst, int64_t max_src, int64_t max_edges, int64_t pad_rows, void* dh, int64_t ld_dh,
-                 void* ws, size_t ws_bytes, void* stream_) {
+                 int64_t max_dst, int64_t max_src, int64_t max_edges, int64_t pad_rows, const void* z_mask,
+                 void* db, void* dh, int64_t ld_dh, void* ws, size_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   BwdWs w;
-  size_t need = bwd_ws(max_src, max_edges, ws, ws_bytes, &w);
+  size_t need = bwd_ws(max_src, max_edges, dim, ws, ws_bytes, &w);
   if (need > ws_bytes) {
     set_error("spmm_bwd: workspace %zu < %zu", ws_bytes, need);
     return GNS_EINVAL;
@@ -697,9 +734,14 @@ int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, 
   tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys);
   GNS_TRY(check_launch("spmm_bwd transpose"));
   const int dv = dim / VW;
+  if (db && dv > 128) {
+    set_error("spmm_bwd: fused bias gradient needs dim <= %d", 128 * VW);
+    return GNS_EINVAL;
+  }
 #define GNS_BWD(T, CH)                                                                                       \
   spmm_bwd_kernel<T, CH><<<g2, kSpmmBlock, 0, stream>>>((const T*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys, \
-                                                        w.self_of, (T*)dh, ld_dh, pad_rows)
+                                                        w.self_of, (T*)dh, ld_dh, pad_rows, (const T*)z_mask,  \
+                                                        db ? (T*)w.colpart : nullptr)
   if (dtype == 0) {
     if (dv <= 32) GNS_BWD(float, 1);
     else if (dv <= 64) GNS_BWD(float, 2);
@@ -710,7 +752,15 @@ int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim, 
     else GNS_BWD(double, 4);
   }
 #undef GNS_BWD
-  return check_launch("spmm_bwd");
+  GNS_TRY(check_launch("spmm_bwd"));
+  if (db) {
+    if (dtype == 0)
+      colsum_final_kernel<float><<<(dim + 7) / 8, 256, 0, stream>>>((const float*)w.colpart, g2, dim, (float*)db);
+    else
+      colsum_final_kernel<double><<<(dim + 7) / 8, 256, 0, stream>>>((const double*)w.colpart, g2, dim,
+                                                                     (double*)db);
+  }
+  return check_launch("spmm_bwd colsum");
 }
 
 size_t gns_dense_bwd_workspace_size(int64_t max_rows, int32_t ncols) {

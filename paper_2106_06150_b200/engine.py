@@ -82,13 +82,13 @@ class GraphedTrainer:
         self.h0 = torch.empty((max(self.cap_src[0], 1), dims[0]), dtype=f32, device=dev)
         self.cat = [torch.empty((max(self.npad[li], 1), 2 * dims[li]), dtype=f32, device=dev) for li in range(L)]
         self.z = [torch.empty((max(self.cap_dst[li], 1), dims[li + 1]), dtype=f32, device=dev) for li in range(L)]
-        self.dh = [torch.zeros((max(self.npad[li], 1), dims[li + 1]), dtype=f32, device=dev) for li in range(L)]
         self.dz = [torch.zeros((max(self.npad[li], 1), dims[li + 1]), dtype=f32, device=dev) for li in range(L)]
         self.dcat = [torch.empty((max(self.cap_dst[li], 1), 2 * dims[li]), dtype=f32, device=dev) for li in range(L)]
         lib = _lib.lib()
         self.ws_dense = _lib.workspace(max(lib.gns_dense_bwd_workspace_size(max(p, 1), d)
                                            for p, d in zip(self.npad, dims[1:])), dev)
-        self.ws_bwd = _lib.workspace(max(lib.gns_spmm_bwd_workspace_size(self.cap_src[li], self.cap_edges[li])
+        self.ws_bwd = _lib.workspace(max(lib.gns_spmm_bwd_workspace_size(self.cap_src[li], self.cap_edges[li],
+                                                                         dims[li])
                                          for li in range(1, L)) if L > 1 else 256, dev)
         self.ws_xent = _lib.workspace(8 * max(self.cap_dst[L - 1], 1024), dev)
         self.loss = self.model.loss_dev
@@ -117,24 +117,24 @@ class GraphedTrainer:
                 h = self.z[li]
             top = blocks[L - 1]
             logits = self.z[L - 1]
+            # dlogits straight into the output layer's dz (rows >= n zero)
             _lib.call("gns_softmax_xent", 0, logits.data_ptr(), logits.stride(0),
                       top.counts[_lib.CNT_DST:_lib.CNT_DST + 1].data_ptr(), self.cap_dst[L - 1], self.npad[L - 1],
-                      logits.shape[1], self.g.labels.data_ptr(), sl.seeds0.data_ptr(), self.dh[L - 1].data_ptr(),
+                      logits.shape[1], self.g.labels.data_ptr(), sl.seeds0.data_ptr(), self.dz[L - 1].data_ptr(),
                       self.loss.data_ptr(), self.ws_xent.data_ptr(), self.ws_xent.numel(), s)
+            d_last = self.dims[L]
+            _lib.call("gns_dense_bwd_bias", 0, self.dz[L - 1].data_ptr(), None, d_last, None, self.cap_dst[L - 1],
+                      d_last, None, m.gbiases[L - 1].data_ptr(), self.ws_dense.data_ptr(), self.ws_dense.numel(), s)
             for li in range(L - 1, -1, -1):
-                d_out = self.dims[li + 1]
-                zz = self.z[li].data_ptr() if li < L - 1 else None
-                # dh rows >= n are zero (xent / spmm_bwd padding) -> dz rows zero
-                _lib.call("gns_dense_bwd_bias", 0, self.dh[li].data_ptr(), zz, d_out, None, self.cap_dst[li], d_out,
-                          self.dz[li].data_ptr(), m.gbiases[li].data_ptr(), self.ws_dense.data_ptr(),
-                          self.ws_dense.numel(), s)
                 _weight_grad(self.cat[li][:self.npad[li]], self.dz[li][:self.npad[li]], m.gweights[li])
                 if li == 0:
                     break
                 torch.mm(self.dz[li][:self.cap_dst[li]], m.weights[li].t(), out=self.dcat[li])
+                # transpose SpMM fused with the previous layer's relu' and bias grad
                 _lib.call("gns_spmm_bwd", 0, self.dcat[li].data_ptr(), self.dcat[li].stride(0), self.dims[li],
                           blocks[li].cblock, self.cap_dst[li], self.cap_src[li], self.cap_edges[li],
-                          self.npad[li - 1], self.dh[li - 1].data_ptr(), self.dh[li - 1].stride(0),
+                          self.npad[li - 1], self.z[li - 1].data_ptr(), m.gbiases[li - 1].data_ptr(),
+                          self.dz[li - 1].data_ptr(), self.dz[li - 1].stride(0),
                           self.ws_bwd.data_ptr(), self.ws_bwd.numel(), s)
         if with_adam:
             self._adam()

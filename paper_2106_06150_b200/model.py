@@ -216,44 +216,47 @@ class GraphSAGE:
 
     def _backward(self, mb, saved, dlogits, stream):
         s = _lib.stream_ptr(stream)
-        dh = dlogits
         L = self.num_layers
+        # output layer: dz = dlogits; db = column sums (model.py:218-220)
+        n, d_out = dlogits.shape
+        self._ensure_dense_ws(max(n, 1), d_out)
+        _lib.call("gns_dense_bwd_bias", _dt(self.dtype), dlogits.data_ptr(), None, dlogits.stride(0), None, n,
+                  d_out, None, self.gbiases[L - 1].data_ptr(), self._ws_dense.data_ptr(),
+                  self._ws_dense.numel(), s)
+        cat, _ = saved[L - 1]
+        if cat.shape[0] == n:
+            dzp = dlogits
+        else:
+            dzp = torch.zeros((cat.shape[0], d_out), dtype=self.dtype, device=self.device)
+            dzp[:n].copy_(dlogits)
         for li in range(L - 1, -1, -1):
             cat, z = saved[li]
-            n, d_out = dh.shape
-            need = _lib.lib().gns_dense_bwd_workspace_size(max(n, 1), d_out)
-            if self._ws_dense is None or self._ws_dense.numel() < need:
-                self._ws_dense = _lib.workspace(int(need * 1.5), self.device)
-            npad = cat.shape[0]
-            if li == L - 1 and npad == n:
-                dzp = dh
-                _lib.call("gns_dense_bwd_bias", _dt(self.dtype), dh.data_ptr(), None, dh.stride(0), None, n,
-                          d_out, None, self.gbiases[li].data_ptr(), self._ws_dense.data_ptr(),
-                          self._ws_dense.numel(), s)
-            else:
-                dzp = torch.empty((npad, d_out), dtype=self.dtype, device=self.device)
-                if npad > n:
-                    dzp[n:].zero_()
-                zz = z.data_ptr() if li < L - 1 else None
-                _lib.call("gns_dense_bwd_bias", _dt(self.dtype), dh.data_ptr(), zz, dh.stride(0), None,
-                          n, d_out, dzp.data_ptr(), self.gbiases[li].data_ptr(), self._ws_dense.data_ptr(),
-                          self._ws_dense.numel(), s)
-            dz = dzp[:n]
+            n = mb.blocks[li].dst_nodes.numel()
             _weight_grad(cat, dzp, self.gweights[li])
             if li == 0:
                 break
-            dcat = torch.mm(dz, self.weights[li].t())
+            dcat = torch.mm(dzp[:n], self.weights[li].t())
             block = mb.blocks[li]
             nsrc = block.src_nodes.numel()
             d_in = self.dims[li]
-            need = _lib.lib().gns_spmm_bwd_workspace_size(nsrc, block.num_edges)
+            need = _lib.lib().gns_spmm_bwd_workspace_size(nsrc, block.num_edges, d_in)
             if self._ws_bwd is None or self._ws_bwd.numel() < need:
                 self._ws_bwd = _lib.workspace(int(need * 1.5), self.device)
-            dh_new = torch.empty((max(nsrc, 1), d_in), dtype=self.dtype, device=self.device)
+            # A^T (dagg / norm) + self term (model.py:223-225) fused with the
+            # previous layer's relu' mask and bias gradient (model.py:218,220)
+            npad_prev = saved[li - 1][0].shape[0]
+            z_prev = saved[li - 1][1]
+            dzp = torch.empty((max(npad_prev, 1), d_in), dtype=self.dtype, device=self.device)
             _lib.call("gns_spmm_bwd", _dt(self.dtype), dcat.data_ptr(), dcat.stride(0), d_in, block._c,
-                      block.dst_nodes.numel(), nsrc, block.num_edges, 0, dh_new.data_ptr(), dh_new.stride(0),
+                      block.dst_nodes.numel(), nsrc, block.num_edges, npad_prev, z_prev.data_ptr(),
+                      self.gbiases[li - 1].data_ptr(), dzp.data_ptr(), dzp.stride(0),
                       self._ws_bwd.data_ptr(), self._ws_bwd.numel(), s)
-            dh = dh_new[:nsrc]
+            dzp = dzp[:npad_prev]
+
+    def _ensure_dense_ws(self, n, d):
+        need = _lib.lib().gns_dense_bwd_workspace_size(n, d)
+        if self._ws_dense is None or self._ws_dense.numel() < need:
+            self._ws_dense = _lib.workspace(int(need * 1.5), self.device)
 
     def adam_step(self, cfg: TrainConfig, grad_scale: float = 1.0, stream=None):
         """model.py:229-242 (bias-corrected), one launch over the flat buffer."""

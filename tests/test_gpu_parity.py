@@ -338,15 +338,26 @@ def test_spmm_bwd_f64_bit_exact(P, dim):
         dcat = np.random.default_rng(10 + li).normal(size=(ndst, 2 * dim))
         dt = torch.as_tensor(dcat, device="cuda")
         dh = torch.empty((nsrc, dim), dtype=torch.float64, device="cuda")
-        _lib.call("gns_spmm_bwd", 1, dt.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0,
-                  dh.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        dh2 = torch.full((nsrc + 5, dim), 3.0, dtype=torch.float64, device="cuda")
+        _lib.call("gns_spmm_bwd", 1, dt.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0, None,
+                  None, dh.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
         expect = OM.spmm_mean_bwd(br, dcat, dim)
         assert np.array_equal(dh.cpu().numpy(), expect), li
+        # fused epilogue: relu' mask of the previous layer + bias-gradient column sums
+        zprev = np.random.default_rng(20 + li).normal(size=(nsrc, dim))
+        zt = torch.as_tensor(zprev, device="cuda")
+        db = torch.empty(dim, dtype=torch.float64, device="cuda")
+        _lib.call("gns_spmm_bwd", 1, dt.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, nsrc + 5,
+                  zt.data_ptr(), db.data_ptr(), dh2.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        dz = expect * (zprev > 0)
+        assert np.array_equal(dh2.cpu().numpy()[:nsrc], dz)
+        assert np.all(dh2.cpu().numpy()[nsrc:] == 0)
+        np.testing.assert_allclose(db.cpu().numpy(), dz.sum(0), rtol=1e-12, atol=1e-12)
         if dim % 4 == 0:
             dt32 = torch.as_tensor(dcat.astype(np.float32), device="cuda")
             dh32 = torch.empty((nsrc, dim), dtype=torch.float32, device="cuda")
-            _lib.call("gns_spmm_bwd", 0, dt32.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0,
-                      dh32.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+            _lib.call("gns_spmm_bwd", 0, dt32.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0, None,
+                      None, dh32.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
             np.testing.assert_allclose(dh32.cpu().numpy(), expect, rtol=1e-5, atol=1e-5)
 
 

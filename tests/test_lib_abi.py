@@ -50,7 +50,7 @@ def test_workspace_queries_without_gpu(lib):
     assert lib.gns_version() == 1
     assert lib.gns_cache_draw_workspace_size(1000) > 8000
     assert lib.gns_relabel_workspace_size(111_000_000) > 111_000_000 // 8
-    assert lib.gns_spmm_bwd_workspace_size(1000, 10000) > 80000
+    assert lib.gns_spmm_bwd_workspace_size(1000, 10000, 64) > 80000
     assert lib.gns_gen_workspace_size(1000, 5000) > 40000
 
 
