@@ -178,9 +178,10 @@ def main():
     import paper_2106_06150_b200 as P
     from paper_2106_06150_b200 import _lib
 
+    from paper_2106_06150_b200 import dist as gdist
     torch.cuda.set_device(local)
     if world > 1 and args.impl == "ours":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        gdist.init_from_env("nccl")
     g, gen_s = make_graph(P, c, seed=0)
     cfg = P.SamplerConfig(strategy="GNS", fanouts=FANOUTS, batch_size=BATCH, cache_frac=c["cache"],
                           cache_mode="degree", input_layer_cache_only=True, seed=0)
@@ -211,13 +212,9 @@ def main():
 
     tc = P.TrainConfig(lr=0.003, hidden_dim=c["hidden"])
 
-    def allreduce(grad):
-        dist.all_reduce(grad)
-        return 1.0 / world
-
     from paper_2106_06150_b200.engine import GraphedTrainer
     tr = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world,
-                        allreduce=allreduce if world > 1 else None, seed=0)
+                        allreduce=gdist.make_allreduce() if world > 1 else None, seed=0)
     pos = tr.run(args.warmup, epoch=0, first=0)
     torch.cuda.synchronize()
     if world > 1:
@@ -236,11 +233,7 @@ def main():
     # graph replays launch the captured kernels: count them per replay
     per_replay = tr.kernels_per_step()
     launches_total = launches + per_replay * args.steps
-    ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = gdist.max_over_ranks(t_start.elapsed_time(t_end), device="cuda")
     value = args.steps * world / (ms / 1e3)
     tr.check_errors()
 

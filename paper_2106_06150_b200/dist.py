@@ -1,0 +1,59 @@
+"""Data-parallel plumbing.
+
+One process per GPU (torchrun).  Mini-batches shard with no data-path
+collective: rank r takes batch indices r, r+W, r+2W, ... of every epoch —
+the reference's worker striding (pool.py:80) — and every rank draws the same
+cache from the same Philox key (replicated, no collective).  The only
+collective is one all-reduce of the flat gradient buffer per step; Adam then
+scales by 1/W (mean gradient of the W batches).
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def rank_batches(num_batches: int, rank: int, world_size: int) -> list[int]:
+    """Batch indices owned by ``rank`` (pool.py:80 striding)."""
+    if world_size < 1 or not (0 <= rank < world_size):
+        raise ValueError("need 0 <= rank < world_size")
+    return list(range(rank, num_batches, world_size))
+
+
+def make_allreduce(group=None):
+    """Sum-all-reduce of the flat gradient; returns the 1/W scale for Adam."""
+
+    def allreduce(grad: torch.Tensor) -> float:
+        w = dist.get_world_size(group)
+        if w > 1:
+            dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+        return 1.0 / w
+
+    return allreduce
+
+
+def init_from_env(backend: str = "nccl"):
+    """Initialise from torchrun's env (RANK / WORLD_SIZE / LOCAL_RANK / MASTER_*)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        kw = {}
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            kw["device_id"] = torch.device("cuda", local)
+        dist.init_process_group(backend, **kw)
+    return rank, world, local
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """Timing rule: the step time is the max over ranks."""
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

@@ -26,6 +26,7 @@ from . import _lib
 from . import cache as cache_mod
 from .graph import Graph
 from .model import GraphSAGE, TrainConfig, _dt, _split_rows, _weight_grad
+from .dist import rank_batches
 from .pool import cache_probs, num_batches
 from .sampling import MiniBatchSampler, SamplerConfig
 
@@ -237,8 +238,7 @@ class GraphedTrainer:
 
     # -- driving ----------------------------------------------------------------------
     def batches(self, epoch: int):
-        nb = num_batches(self.g, self.cfg)
-        return list(range(self.rank, nb, self.world))
+        return rank_batches(num_batches(self.g, self.cfg), self.rank, self.world)
 
     def run(self, steps: int, epoch: int = 0, first: int = 0, on_step=None):
         """Run ``steps`` training steps starting at batch ``first`` of

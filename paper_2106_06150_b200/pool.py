@@ -121,8 +121,8 @@ class SamplerPool:
                                            rng_seed=[self.config.seed, _CACHE, epoch])
 
     def indices(self, epoch: int):
-        nb = num_batches(self.graph, self.config)
-        return list(range(self.rank, nb, self.world_size))
+        from .dist import rank_batches
+        return rank_batches(num_batches(self.graph, self.config), self.rank, self.world_size)
 
     def _launch(self, slot: int, epoch: int, index: int):
         eng = self.slots[slot]
