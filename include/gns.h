@@ -165,19 +165,24 @@ GNS_API int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits,
  * sample_neighbors_gns (sampling.py:189-266, policy gns-paper) when cache !=
  * NULL, sample_neighbors_uniform (sampling.py:155-170) when cache == NULL.
  * seeds: sorted unique int32 (count in *n_seeds_dev, <= max_dst).  Writes
- * row_scan, dst_degree, edge_node/edge_dst/edge_weight/edge_cached and counts
- * DST/EDGES/CACHED/HUBS/ERR.  Edge capacity must be >= max_dst * k. */
-GNS_API size_t gns_sample_workspace_size(int64_t max_dst);
+ * row_scan, dst_degree, edge_node/edge_dst/edge_weight/edge_cached, and the
+ * assembled block (_assemble, sampling.py:139-152): src_nodes, edge_src,
+ * self_pos, plus counts DST/EDGES/CACHED/SRC/HUBS/ERR.  Edge capacity must be
+ * >= max_dst * k.  The workspace (gns_sample_workspace_size) holds the
+ * two-level dedup bitmap: zero it once before first use; every call leaves it
+ * zero. */
+GNS_API size_t gns_sample_workspace_size(int64_t num_nodes, int64_t max_dst);
 GNS_API int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache,
                      const int32_t* seeds, const int32_t* n_seeds_dev,
                      int64_t max_dst, int32_t k, int32_t cache_only,
                      const gns_rng_t* rng, const gns_step_t* step_dev,
                      gns_block_t* block, void* ws, size_t ws_bytes, void* stream);
 
-/* _assemble (sampling.py:139-152): src_nodes = sorted unique(seeds ∪
- * edge_node), edge_src = rank of edge_node, self_pos = rank of each seed.
- * Bitmap dedup over node ids; the workspace bitmap must be zero on entry
- * and is left zero.  Writes counts[GNS_CNT_SRC]. */
+/* Standalone _assemble (sampling.py:139-152) for an externally produced edge
+ * list: src_nodes = sorted unique(seeds ∪ edge_node), edge_src = rank of
+ * edge_node, self_pos = rank of each seed.  Two-level bitmap dedup over node
+ * ids; the workspace must be zero on first use and is left zero.  Writes
+ * counts[GNS_CNT_SRC].  (gns_sample_layer already does this internally.) */
 GNS_API size_t gns_relabel_workspace_size(int64_t num_nodes);
 GNS_API int gns_relabel(int64_t num_nodes, const int32_t* seeds, const int32_t* n_seeds_dev,
                 int64_t max_dst, gns_block_t* block, int64_t max_edges,

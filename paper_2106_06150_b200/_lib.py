@@ -78,7 +78,7 @@ _SIGS = {
                                        c_void_p, c_size_t, c_void_p]),
     "gns_cached_csr_fill": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p, c_void_p,
                                       c_void_p]),
-    "gns_sample_workspace_size": (c_size_t, [c_int64]),
+    "gns_sample_workspace_size": (c_size_t, [c_int64, c_int64]),
     "gns_sample_layer": (c_int32, [POINTER(GnsGraph), POINTER(GnsCache), c_void_p, c_void_p,
                                    c_int64, c_int32, c_int32, POINTER(GnsRng), c_void_p,
                                    POINTER(GnsBlock), c_void_p, c_size_t, c_void_p]),
@@ -169,7 +169,7 @@ def check(rc: int, what: str = ""):
 # how many of OUR kernels ran inside a timed region
 KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
-    "gns_cached_csr_fill": 1, "gns_sample_layer": 5, "gns_relabel": 5, "gns_unique_sorted": 4,
+    "gns_cached_csr_fill": 1, "gns_sample_layer": 8, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
     "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 7,
     "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1,

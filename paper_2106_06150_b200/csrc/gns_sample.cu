@@ -50,8 +50,19 @@ struct LayerArgs {
   int64_t max_dst;
   uint32_t seed, epoch, batch, layer;
   const gns_step_t* step_dev;
+  uint32_t* dbits;  // dedup bitmap (bit v of word v>>5); NULL = no fused marking
+  uint32_t* dsum;   // summary bitmap (bit w of word w>>5 set iff dbits[w] != 0)
   gns_block_t b;
 };
+
+// mark node v in the two-level dedup bitmap
+__device__ __forceinline__ void mark_node(uint32_t* __restrict__ bits, uint32_t* __restrict__ sum, int32_t v) {
+  const uint32_t m = 1u << (v & 31);
+  const int32_t w = v >> 5;
+  if (__ldg(bits + w) & m) return;  // already set (read-only fast path)
+  const uint32_t old = atomicOr(bits + w, m);
+  if (old == 0u) atomicOr(sum + (w >> 5), 1u << (w & 31));
+}
 
 // per-batch Philox key from device memory (CUDA-graph replay) when given
 __device__ __forceinline__ LayerArgs resolve_rng(const LayerArgs& in) {
@@ -131,6 +142,7 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(LayerArgs 
         RowInfo ri = row_info(a, r);
         a.b.row_scan[r] = ex;
         a.b.dst_degree[r] = ri.deg;
+        if (a.dbits) mark_node(a.dbits, a.dsum, ri.node);
         const int tier = row_tier(ri, a.k);
         if (tier == 1) {  // warp-tier rows fill hub_rows from the front
           int h = atomicAdd(a.b.counts + GNS_CNT_WARPROWS, 1);
@@ -181,6 +193,7 @@ __device__ __forceinline__ void emit_edge(const LayerArgs& a, const RowInfo& ri,
   } else {
     w = DDIV((double)ri.deg, (double)max(ri.fill, 1));
   }
+  if (a.dbits) mark_node(a.dbits, a.dsum, u);
   a.b.edge_node[o] = u;
   a.b.edge_dst[o] = (int32_t)r;
   a.b.edge_weight[o] = w;
@@ -365,33 +378,40 @@ __device__ __forceinline__ void sort16(uint64_t (&a)[16]) {
 // reference's stable lexsort — a 16-wide sorting network orders them and the
 // first `take` are emitted.  Keys are staged per thread in shared memory so
 // the Philox and emit loops stay rolled (small code, no local memory).
-__device__ __noinline__ void thread_select16(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
+__device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
                                              uint64_t* __restrict__ slot) {
   const uint32_t stream = stream_word(32, a.layer, ph.phase);
-  const int npairs = (ph.len + 1) >> 1;
-#pragma unroll 1
-  for (int q = 0; q < 8; ++q) {
-    uint64_t k0 = ~0ull, k1 = ~0ull;
-    if (q < npairs) {
-      key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
-      bool ok0 = true, ok1 = 2 * q + 1 < ph.len;
-      if (ph.filter) {
-        ok0 = !cached_bit(a.mask, __ldg(ph.ids + 2 * q));
-        if (ok1) ok1 = !cached_bit(a.mask, __ldg(ph.ids + 2 * q + 1));
-      }
-      k0 = ok0 ? ((k0 << 11) | (uint64_t)(2 * q)) : ~0ull;
-      k1 = ok1 ? ((k1 << 11) | (uint64_t)(2 * q + 1)) : ~0ull;
-    }
-    slot[(2 * q) * 32] = k0;
-    slot[(2 * q + 1) * 32] = k1;
+  const int len = ph.len;
+  // 1. all neighbour ids and cache-bitmap words of the fill phase in flight
+  //    at once (independent loads: no dependent chain per candidate)
+  int32_t idv[16];
+  uint32_t mw[16];
+  if (ph.filter) {
+#pragma unroll
+    for (int p = 0; p < 16; ++p) idv[p] = p < len ? __ldg(ph.ids + p) : 0;
+#pragma unroll
+    for (int p = 0; p < 16; ++p) mw[p] = p < len ? __ldg(a.mask + (idv[p] >> 5)) : 0u;
   }
+  // 2. Philox keys (ALU) packed with the position: (key53 << 11) | pos
   uint64_t v[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = slot[i * 32];
+  for (int q = 0; q < 8; ++q) {
+    uint64_t k0 = ~0ull, k1 = ~0ull;
+    if (2 * q < len) key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
+    bool ok0 = 2 * q < len, ok1 = 2 * q + 1 < len;
+    if (ph.filter) {
+      ok0 = ok0 && !((mw[2 * q] >> (idv[2 * q] & 31)) & 1u);
+      ok1 = ok1 && !((mw[2 * q + 1] >> (idv[2 * q + 1] & 31)) & 1u);
+    }
+    v[2 * q] = ok0 ? ((k0 << 11) | (uint64_t)(2 * q)) : ~0ull;
+    v[2 * q + 1] = ok1 ? ((k1 << 11) | (uint64_t)(2 * q + 1)) : ~0ull;
+  }
+  // 3. (key, position) order = the reference's stable lexsort
   sort16(v);
 #pragma unroll
   for (int i = 0; i < 16; ++i) slot[i * 32] = v[i];
-#pragma unroll 1
+  // 4. emit the first `take` (loads of several edges in flight)
+#pragma unroll 4
   for (int i = 0; i < ph.take; ++i) emit_edge(a, ri, r, ph, i, (uint32_t)(slot[i * 32] & 2047u));
 }
 
@@ -447,99 +467,125 @@ __global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(LayerArgs a_in) {
 }
 
 // ---- dedup / relabel ----------------------------------------------------------
+// Two-level bitmap: bits (1 per node id, N/8 bytes) + summary (1 per bitmap
+// word).  Enumeration scans only the summary (N/1024 words) and the non-zero
+// bitmap words, emits the sorted unique ids, stores (rank << 32 | word) per
+// non-zero word for the relabel lookups, and clears both levels as it goes —
+// the bitmaps are left zero without a separate clearing pass.
 __global__ void setbits_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ na_dev, int64_t na_host,
                                const int32_t* __restrict__ b, const int32_t* __restrict__ nb_dev,
-                               uint32_t* __restrict__ bits) {
+                               uint32_t* __restrict__ bits, uint32_t* __restrict__ sum) {
   const int64_t na = na_dev ? na_dev[0] : na_host;
   const int64_t nb = (b && nb_dev) ? nb_dev[0] : 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < na + nb;
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t v = i < na ? a[i] : b[i - na];
-    atomicOr(bits + (v >> 5), 1u << (v & 31));
+    mark_node(bits, sum, v);
   }
 }
 
-constexpr int kEnumBlock = 256, kEnumItems = 16;
+constexpr int kEnumBlock = 256, kEnumItems = 4;
 
-__global__ void __launch_bounds__(kEnumBlock) enumerate_reduce_kernel(const uint32_t* __restrict__ bits, int64_t nw,
-                                                                      unsigned long long* tile_sums) {
-  scan2_reduce<kEnumBlock, kEnumItems>(nw, [&](long long w) { return (unsigned long long)__popc(bits[w]); },
-                                       tile_sums);
+__device__ __forceinline__ unsigned long long summary_count(const uint32_t* __restrict__ bits,
+                                                            const uint32_t* __restrict__ sum, long long sw) {
+  uint32_t s = sum[sw];
+  unsigned long long c = 0;
+  while (s) {
+    const int b = __ffs(s) - 1;
+    s &= s - 1;
+    c += __popc(bits[sw * 32 + b]);
+  }
+  return c;
 }
 
-__global__ void __launch_bounds__(kEnumBlock) enumerate_apply_kernel(const uint32_t* __restrict__ bits, int64_t nw,
+__global__ void __launch_bounds__(kEnumBlock) enumerate_reduce_kernel(const uint32_t* __restrict__ bits,
+                                                                      const uint32_t* __restrict__ sum, int64_t nsw,
+                                                                      unsigned long long* tile_sums) {
+  scan2_reduce<kEnumBlock, kEnumItems>(nsw, [&](long long sw) { return summary_count(bits, sum, sw); }, tile_sums);
+}
+
+__global__ void __launch_bounds__(kEnumBlock) enumerate_apply_kernel(uint32_t* __restrict__ bits,
+                                                                     uint32_t* __restrict__ sum, int64_t nsw,
                                                                      const unsigned long long* tile_sums,
-                                                                     int32_t* __restrict__ rank,
+                                                                     unsigned long long* __restrict__ rank2,
                                                                      int32_t* __restrict__ out,
                                                                      int32_t* __restrict__ out_n) {
   scan2_apply<kEnumBlock, kEnumItems>(
-      nw, [&](long long w) { return (unsigned long long)__popc(bits[w]); },
-      [&](long long w, unsigned long long ex, unsigned long long val) {
-        if (!val) return;
-        rank[w] = (int32_t)ex;
-        uint32_t s = bits[w];
-        int32_t pos = (int32_t)ex;
-        while (s) {
-          int bb = __ffs(s) - 1;
-          s &= s - 1;
-          out[pos++] = (int32_t)(w * 32 + bb);
+      nsw, [&](long long sw) { return summary_count(bits, sum, sw); },
+      [&](long long sw, unsigned long long ex, unsigned long long val) {
+        uint32_t sm = sum[sw];
+        if (!sm) return;
+        unsigned long long pos = ex;
+        while (sm) {
+          const int b = __ffs(sm) - 1;
+          sm &= sm - 1;
+          const long long w = sw * 32 + b;
+          uint32_t x = bits[w];
+          rank2[w] = (pos << 32) | (unsigned long long)x;
+          bits[w] = 0u;
+          while (x) {
+            const int bb = __ffs(x) - 1;
+            x &= x - 1;
+            out[pos++] = (int32_t)(w * 32 + bb);
+          }
         }
+        sum[sw] = 0u;
       },
       [&](unsigned long long tot) { out_n[0] = (int32_t)tot; }, tile_sums);
 }
 
-__device__ __forceinline__ int32_t bit_rank(const uint32_t* __restrict__ bits, const int32_t* __restrict__ rank,
-                                            int32_t v) {
-  const uint32_t w = bits[v >> 5];
-  return rank[v >> 5] + __popc(w & ((1u << (v & 31)) - 1u));
+__device__ __forceinline__ int32_t bit_rank(const unsigned long long* __restrict__ rank2, int32_t v) {
+  const unsigned long long rw = rank2[v >> 5];
+  return (int32_t)(rw >> 32) + __popc((uint32_t)rw & ((1u << (v & 31)) - 1u));
 }
 
-__global__ void relabel_kernel(const uint32_t* __restrict__ bits, const int32_t* __restrict__ rank,
-                               const int32_t* __restrict__ seeds, const int32_t* __restrict__ n_seeds_dev,
-                               const int32_t* __restrict__ edge_node, const int32_t* __restrict__ counts,
-                               int32_t* __restrict__ self_pos, int32_t* __restrict__ edge_src) {
+__global__ void relabel_kernel(const unsigned long long* __restrict__ rank2, const int32_t* __restrict__ seeds,
+                               const int32_t* __restrict__ n_seeds_dev, const int32_t* __restrict__ edge_node,
+                               const int32_t* __restrict__ counts, int32_t* __restrict__ self_pos,
+                               int32_t* __restrict__ edge_src) {
   const int64_t ns = n_seeds_dev[0];
   const int64_t ne = counts[GNS_CNT_EDGES];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns + ne;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i < ns)
-      self_pos[i] = bit_rank(bits, rank, seeds[i]);
+      self_pos[i] = bit_rank(rank2, seeds[i]);
     else
-      edge_src[i - ns] = bit_rank(bits, rank, edge_node[i - ns]);
+      edge_src[i - ns] = bit_rank(rank2, edge_node[i - ns]);
   }
 }
 
-__global__ void clearbits_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ n_dev,
-                                 uint32_t* __restrict__ bits) {
-  const int64_t n = n_dev[0];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    bits[ids[i] >> 5] = 0u;
-}
-
-struct RelabelWs {
+struct DedupWs {
   uint32_t* bits;
-  int32_t* rank;
-  void* scan;
-  long long tiles;
+  uint32_t* sum;
+  unsigned long long* rank2;
+  unsigned long long* tiles;
+  int64_t nw, nsw;
 };
 
-static size_t relabel_ws(int64_t num_nodes, void* base, size_t cap, RelabelWs* r) {
-  Workspace w(base, cap);
-  int64_t nw = (num_nodes + 31) / 32;
-  r->bits = w.take<uint32_t>(nw + 1);
-  r->rank = w.take<int32_t>(nw + 1);
-  r->tiles = (nw + 256 * 16 - 1) / (256 * 16) + 1;
-  r->scan = (void*)w.take<char>(scan_status_bytes(r->tiles));
-  return w.off;
+static void dedup_ws(int64_t num_nodes, Workspace& w, DedupWs* d) {
+  d->nw = (num_nodes + 31) / 32;
+  d->nsw = (d->nw + 31) / 32;
+  d->bits = w.take<uint32_t>(d->nw + 1);
+  d->sum = w.take<uint32_t>(d->nsw + 1);
+  d->rank2 = w.take<unsigned long long>(d->nw + 1);
+  d->tiles = w.take<unsigned long long>(d->nsw / (kEnumBlock * kEnumItems) + 2);
 }
 
-static int run_enumerate(const RelabelWs& r, int64_t num_nodes, int32_t* out, int32_t* out_n, cudaStream_t stream) {
-  int64_t nw = (num_nodes + 31) / 32;
-  const unsigned tiles = (unsigned)((nw + kEnumBlock * kEnumItems - 1) / (kEnumBlock * kEnumItems));
-  unsigned long long* tile_sums = (unsigned long long*)r.scan;
-  enumerate_reduce_kernel<<<tiles ? tiles : 1, kEnumBlock, 0, stream>>>(r.bits, nw, tile_sums);
-  enumerate_apply_kernel<<<tiles ? tiles : 1, kEnumBlock, 0, stream>>>(r.bits, nw, tile_sums, r.rank, out, out_n);
+static int run_enumerate(const DedupWs& d, int32_t* out, int32_t* out_n, cudaStream_t stream) {
+  const unsigned tiles = (unsigned)((d.nsw + kEnumBlock * kEnumItems - 1) / (kEnumBlock * kEnumItems));
+  enumerate_reduce_kernel<<<tiles ? tiles : 1, kEnumBlock, 0, stream>>>(d.bits, d.sum, d.nsw, d.tiles);
+  enumerate_apply_kernel<<<tiles ? tiles : 1, kEnumBlock, 0, stream>>>(d.bits, d.sum, d.nsw, d.tiles, d.rank2, out,
+                                                                     out_n);
   return check_launch("enumerate");
+}
+
+static int run_relabel(const DedupWs& d, const int32_t* seeds, const int32_t* n_seeds_dev, int64_t max_dst,
+                       gns_block_t* block, int64_t max_edges, cudaStream_t stream) {
+  GNS_TRY(run_enumerate(d, block->src_nodes, block->counts + GNS_CNT_SRC, stream));
+  int grid = grid_for((max_dst + max_edges + 255) / 256 + 1, (long long)num_sms() * 16);
+  relabel_kernel<<<grid, 256, 0, stream>>>(d.rank2, seeds, n_seeds_dev, block->edge_node, block->counts,
+                                           block->self_pos, block->edge_src);
+  return check_launch("relabel");
 }
 
 }  // namespace gns
@@ -548,9 +594,18 @@ using namespace gns;
 
 extern "C" {
 
-size_t gns_sample_workspace_size(int64_t max_dst) {
-  long long tiles = (max_dst + 256 * 4 - 1) / (256 * 4) + 1;
-  return scan_status_bytes(tiles);
+static size_t sample_ws(int64_t num_nodes, int64_t max_dst, void* base, size_t cap, unsigned long long** tiles,
+                        DedupWs* d) {
+  Workspace w(base, cap);
+  *tiles = w.take<unsigned long long>(max_dst / (kCntBlock * kCntItems) + 2);
+  dedup_ws(num_nodes, w, d);
+  return w.off;
+}
+
+size_t gns_sample_workspace_size(int64_t num_nodes, int64_t max_dst) {
+  unsigned long long* t;
+  DedupWs d;
+  return sample_ws(num_nodes, max_dst, nullptr, 0, &t, &d);
 }
 
 int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32_t* seeds,
@@ -566,7 +621,9 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
     set_error("fanout %d exceeds the supported maximum %d", k, kMaxFanout);
     return GNS_EINVAL;
   }
-  size_t need = gns_sample_workspace_size(max_dst);
+  unsigned long long* ctiles;
+  DedupWs dd;
+  size_t need = sample_ws(g->num_nodes, max_dst, ws, ws_bytes, &ctiles, &dd);
   if (ws_bytes < need) {
     set_error("sample_layer: workspace %zu < %zu", ws_bytes, need);
     return GNS_EINVAL;
@@ -589,11 +646,13 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.batch = rng->batch;
   a.layer = rng->layer;
   a.step_dev = step_dev;
+  a.dbits = dd.bits;
+  a.dsum = dd.sum;
   a.b = *block;
   const unsigned tiles = (unsigned)((max_dst + kCntBlock * kCntItems - 1) / (kCntBlock * kCntItems)) + 1;
   GNS_CUDA(cudaMemsetAsync(block->counts, 0, GNS_CNT_N * sizeof(int32_t), stream));
-  layer_count_reduce_kernel<<<tiles, kCntBlock, 0, stream>>>(a, (unsigned long long*)ws);
-  layer_count_apply_kernel<<<tiles, kCntBlock, 0, stream>>>(a, (unsigned long long*)ws);
+  layer_count_reduce_kernel<<<tiles, kCntBlock, 0, stream>>>(a, ctiles);
+  layer_count_apply_kernel<<<tiles, kCntBlock, 0, stream>>>(a, ctiles);
   GNS_TRY(check_launch("layer_count"));
   const int sms = num_sms();
   int tgrid = grid_for((max_dst + 255) / 256, (long long)sms * 16);
@@ -603,52 +662,50 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   sample_warp_kernel<<<grid, kSampBlock, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_warp"));
   sample_hub_kernel<<<sms, kHubBlock, 0, stream>>>(a);
-  return check_launch("sample_hub");
+  GNS_TRY(check_launch("sample_hub"));
+  // _assemble (sampling.py:139-152): seeds and sampled neighbours were marked
+  // in the dedup bitmap by the count / sample kernels
+  return run_relabel(dd, seeds, n_seeds_dev, max_dst, block, max_dst * (int64_t)k, stream);
 }
 
 size_t gns_relabel_workspace_size(int64_t num_nodes) {
-  RelabelWs r;
-  return relabel_ws(num_nodes, nullptr, 0, &r);
+  Workspace w(nullptr, 0);
+  DedupWs d;
+  dedup_ws(num_nodes, w, &d);
+  return w.off;
 }
 
 int gns_relabel(int64_t num_nodes, const int32_t* seeds, const int32_t* n_seeds_dev, int64_t max_dst,
                 gns_block_t* block, int64_t max_edges, void* ws, size_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
-  RelabelWs r;
-  size_t need = relabel_ws(num_nodes, ws, ws_bytes, &r);
-  if (need > ws_bytes) {
-    set_error("relabel: workspace %zu < %zu", ws_bytes, need);
+  Workspace w(ws, ws_bytes);
+  DedupWs d;
+  dedup_ws(num_nodes, w, &d);
+  if (!w.ok()) {
+    set_error("relabel: workspace %zu < %zu", ws_bytes, w.off);
     return GNS_EINVAL;
   }
-  const int sms = num_sms();
-  int grid = grid_for((max_dst + max_edges + 255) / 256 + 1, (long long)sms * 16);
+  int grid = grid_for((max_dst + max_edges + 255) / 256 + 1, (long long)num_sms() * 16);
   setbits_kernel<<<grid, 256, 0, stream>>>(seeds, n_seeds_dev, 0, block->edge_node, block->counts + GNS_CNT_EDGES,
-                                           r.bits);
+                                           d.bits, d.sum);
   GNS_TRY(check_launch("setbits"));
-  GNS_TRY(run_enumerate(r, num_nodes, block->src_nodes, block->counts + GNS_CNT_SRC, stream));
-  relabel_kernel<<<grid, 256, 0, stream>>>(r.bits, r.rank, seeds, n_seeds_dev, block->edge_node, block->counts,
-                                           block->self_pos, block->edge_src);
-  GNS_TRY(check_launch("relabel"));
-  clearbits_kernel<<<grid, 256, 0, stream>>>(block->src_nodes, block->counts + GNS_CNT_SRC, r.bits);
-  return check_launch("clearbits");
+  return run_relabel(d, seeds, n_seeds_dev, max_dst, block, max_edges, stream);
 }
 
 int gns_unique_sorted(int64_t num_nodes, const int32_t* ids, const int32_t* n_dev, int64_t n_host, int32_t* out,
                       int32_t* out_n_dev, void* ws, size_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
-  RelabelWs r;
-  size_t need = relabel_ws(num_nodes, ws, ws_bytes, &r);
-  if (need > ws_bytes) {
-    set_error("unique_sorted: workspace %zu < %zu", ws_bytes, need);
+  Workspace w(ws, ws_bytes);
+  DedupWs d;
+  dedup_ws(num_nodes, w, &d);
+  if (!w.ok()) {
+    set_error("unique_sorted: workspace %zu < %zu", ws_bytes, w.off);
     return GNS_EINVAL;
   }
-  const int sms = num_sms();
-  int grid = grid_for((n_host + 255) / 256 + 1, (long long)sms * 16);
-  setbits_kernel<<<grid, 256, 0, stream>>>(ids, n_dev, n_host, nullptr, nullptr, r.bits);
+  int grid = grid_for((n_host + 255) / 256 + 1, (long long)num_sms() * 16);
+  setbits_kernel<<<grid, 256, 0, stream>>>(ids, n_dev, n_host, nullptr, nullptr, d.bits, d.sum);
   GNS_TRY(check_launch("setbits"));
-  GNS_TRY(run_enumerate(r, num_nodes, out, out_n_dev, stream));
-  clearbits_kernel<<<grid, 256, 0, stream>>>(out, out_n_dev, r.bits);
-  return check_launch("clearbits");
+  return run_enumerate(d, out, out_n_dev, stream);
 }
 
 }  // extern "C"

@@ -225,8 +225,9 @@ class MiniBatchSampler:
         self.targets = torch.empty(max(self.max_targets, 1), dtype=torch.int32, device=dev)
         self.seeds0 = torch.empty(max(self.max_targets, 1), dtype=torch.int32, device=dev)
         self.n_seeds0 = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.ws_sample = _lib.workspace(lib.gns_sample_workspace_size(max(l.max_dst for l in self.layers)), dev)
-        # bitmap must start zeroed; every relabel leaves it zeroed
+        # dedup bitmaps must start zeroed; every call leaves them zeroed
+        self.ws_sample = _lib.workspace(lib.gns_sample_workspace_size(n, max(l.max_dst for l in self.layers)), dev,
+                                        zero=True)
         self.ws_relabel = _lib.workspace(lib.gns_relabel_workspace_size(n), dev, zero=True)
 
     # -- device-side chain -------------------------------------------------------
@@ -254,8 +255,6 @@ class MiniBatchSampler:
             _lib.call("gns_sample_layer", gc, cstruct, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
                       lb.k, int(lb.cache_only), rng.cstruct(lb.layer), None, lb.cblock,
                       self.ws_sample.data_ptr(), self.ws_sample.numel(), s)
-            _lib.call("gns_relabel", self.g.num_nodes, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
-                      lb.cblock, lb.max_edges, self.ws_relabel.data_ptr(), self.ws_relabel.numel(), s)
             seeds = lb.src_nodes
             n_dev = lb.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
         self.counts_host.copy_(self.counts, non_blocking=True)
@@ -290,8 +289,6 @@ class MiniBatchSampler:
             _lib.call("gns_sample_layer", gc, cstruct, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
                       lb.k, int(lb.cache_only), rng.cstruct(lb.layer), step_dev.data_ptr(), lb.cblock,
                       self.ws_sample.data_ptr(), self.ws_sample.numel(), s)
-            _lib.call("gns_relabel", self.g.num_nodes, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
-                      lb.cblock, lb.max_edges, self.ws_relabel.data_ptr(), self.ws_relabel.numel(), s)
             seeds = lb.src_nodes
             n_dev = lb.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
 
