@@ -484,24 +484,36 @@ __global__ void setbits_kernel(const int32_t* __restrict__ a, const int32_t* __r
   }
 }
 
-constexpr int kEnumBlock = 256, kEnumItems = 4;
+// Tile = 64 summary words (65536 node ids); a warp walks 8 summary words, lane
+// b owning bitmap word sw*32+b (coalesced 128-byte loads; empty summary words
+// are skipped without touching the bitmap).
+constexpr int kEnumBlock = 256;
+constexpr int kEnumWarps = kEnumBlock / 32;
+constexpr int kEnumPerWarp = 8;
+constexpr int kEnumTileSw = kEnumWarps * kEnumPerWarp;
 
-__device__ __forceinline__ unsigned long long summary_count(const uint32_t* __restrict__ bits,
-                                                            const uint32_t* __restrict__ sum, long long sw) {
-  uint32_t s = sum[sw];
-  unsigned long long c = 0;
-  while (s) {
-    const int b = __ffs(s) - 1;
-    s &= s - 1;
-    c += __popc(bits[sw * 32 + b]);
-  }
-  return c;
+__device__ __forceinline__ uint32_t enum_word(const uint32_t* __restrict__ bits, uint32_t smw, long long sw,
+                                              int lane) {
+  return ((smw >> lane) & 1u) ? bits[sw * 32 + lane] : 0u;
 }
 
 __global__ void __launch_bounds__(kEnumBlock) enumerate_reduce_kernel(const uint32_t* __restrict__ bits,
                                                                       const uint32_t* __restrict__ sum, int64_t nsw,
                                                                       unsigned long long* tile_sums) {
-  scan2_reduce<kEnumBlock, kEnumItems>(nsw, [&](long long sw) { return summary_count(bits, sum, sw); }, tile_sums);
+  __shared__ unsigned long long s_w[kEnumWarps + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long sw0 = (long long)blockIdx.x * kEnumTileSw + warp * kEnumPerWarp;
+  unsigned c = 0;
+#pragma unroll
+  for (int i = 0; i < kEnumPerWarp; ++i) {
+    const long long sw = sw0 + i;
+    if (sw < nsw) {
+      const uint32_t smw = sum[sw];
+      if (smw) c += __popc(enum_word(bits, smw, sw, lane));
+    }
+  }
+  unsigned long long t = block_sum<kEnumBlock>((unsigned long long)c, s_w);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = t;
 }
 
 __global__ void __launch_bounds__(kEnumBlock) enumerate_apply_kernel(uint32_t* __restrict__ bits,
@@ -510,28 +522,60 @@ __global__ void __launch_bounds__(kEnumBlock) enumerate_apply_kernel(uint32_t* _
                                                                      unsigned long long* __restrict__ rank2,
                                                                      int32_t* __restrict__ out,
                                                                      int32_t* __restrict__ out_n) {
-  scan2_apply<kEnumBlock, kEnumItems>(
-      nsw, [&](long long sw) { return summary_count(bits, sum, sw); },
-      [&](long long sw, unsigned long long ex, unsigned long long val) {
-        uint32_t sm = sum[sw];
-        if (!sm) return;
-        unsigned long long pos = ex;
-        while (sm) {
-          const int b = __ffs(sm) - 1;
-          sm &= sm - 1;
-          const long long w = sw * 32 + b;
-          uint32_t x = bits[w];
-          rank2[w] = (pos << 32) | (unsigned long long)x;
-          bits[w] = 0u;
-          while (x) {
-            const int bb = __ffs(x) - 1;
-            x &= x - 1;
-            out[pos++] = (int32_t)(w * 32 + bb);
-          }
-        }
-        sum[sw] = 0u;
-      },
-      [&](unsigned long long tot) { out_n[0] = (int32_t)tot; }, tile_sums);
+  __shared__ unsigned long long s_w[kEnumWarps + 1];
+  __shared__ unsigned long long s_wpre[kEnumWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long ntiles = (nsw + kEnumTileSw - 1) / kEnumTileSw;
+  const long long tile = blockIdx.x;
+  if (nsw == 0) {
+    if (tile == 0 && threadIdx.x == 0) out_n[0] = 0;
+    return;
+  }
+  if (tile >= ntiles) return;
+  unsigned long long pre = 0;
+  for (long long j = threadIdx.x; j < tile; j += kEnumBlock) pre += tile_sums[j];
+  pre = block_sum<kEnumBlock>(pre, s_w);
+  // per-warp counts -> exclusive prefix over the 8 warps of the tile
+  const long long sw0 = tile * kEnumTileSw + warp * kEnumPerWarp;
+  uint32_t words[kEnumPerWarp];
+  unsigned c = 0;
+#pragma unroll
+  for (int i = 0; i < kEnumPerWarp; ++i) {
+    const long long sw = sw0 + i;
+    words[i] = 0u;
+    if (sw < nsw) {
+      const uint32_t smw = sum[sw];
+      if (smw) words[i] = enum_word(bits, smw, sw, lane);
+    }
+    c += __popc(words[i]);
+  }
+  c = warp_sum(c);
+  if (lane == 0) s_wpre[warp] = c;
+  __syncthreads();
+  unsigned long long base = pre;
+  for (int w = 0; w < warp; ++w) base += s_wpre[w];
+  if (tile == ntiles - 1 && warp == kEnumWarps - 1 && lane == 0) out_n[0] = (int32_t)(base + c);
+#pragma unroll
+  for (int i = 0; i < kEnumPerWarp; ++i) {
+    const long long sw = sw0 + i;
+    const uint32_t x = words[i];
+    const unsigned pc = __popc(x);
+    const unsigned incl = warp_incl_scan(pc);
+    if (x) {
+      const long long w = sw * 32 + lane;
+      unsigned long long o = base + incl - pc;
+      rank2[w] = (o << 32) | (unsigned long long)x;
+      bits[w] = 0u;
+      uint32_t y = x;
+      while (y) {
+        const int bb = __ffs(y) - 1;
+        y &= y - 1;
+        out[o++] = (int32_t)(w * 32 + bb);
+      }
+    }
+    base += __shfl_sync(GNS_FULL, incl, 31);
+    if (sw < nsw && lane == 0) sum[sw] = 0u;
+  }
 }
 
 __device__ __forceinline__ int32_t bit_rank(const unsigned long long* __restrict__ rank2, int32_t v) {
@@ -568,11 +612,11 @@ static void dedup_ws(int64_t num_nodes, Workspace& w, DedupWs* d) {
   d->bits = w.take<uint32_t>(d->nw + 1);
   d->sum = w.take<uint32_t>(d->nsw + 1);
   d->rank2 = w.take<unsigned long long>(d->nw + 1);
-  d->tiles = w.take<unsigned long long>(d->nsw / (kEnumBlock * kEnumItems) + 2);
+  d->tiles = w.take<unsigned long long>(d->nsw / kEnumTileSw + 2);
 }
 
 static int run_enumerate(const DedupWs& d, int32_t* out, int32_t* out_n, cudaStream_t stream) {
-  const unsigned tiles = (unsigned)((d.nsw + kEnumBlock * kEnumItems - 1) / (kEnumBlock * kEnumItems));
+  const unsigned tiles = (unsigned)((d.nsw + kEnumTileSw - 1) / kEnumTileSw);
   enumerate_reduce_kernel<<<tiles ? tiles : 1, kEnumBlock, 0, stream>>>(d.bits, d.sum, d.nsw, d.tiles);
   enumerate_apply_kernel<<<tiles ? tiles : 1, kEnumBlock, 0, stream>>>(d.bits, d.sum, d.nsw, d.tiles, d.rank2, out,
                                                                      out_n);
