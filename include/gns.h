@@ -58,6 +58,7 @@ extern "C" {
 #define GNS_CNT_HUBS 4     /* rows routed to the CTA-per-row sampler        */
 #define GNS_CNT_ERR 5      /* GNS_ERRBIT_* flags                             */
 #define GNS_CNT_WARPROWS 6 /* rows routed to the warp-per-row sampler        */
+#define GNS_CNT_THREADROWS 7 /* rows routed to the thread-per-row sampler    */
 #define GNS_CNT_N 8
 
 /* CSR graph (graph.py:52-104): indptr int64[N+1], indices int32[E]. */
@@ -104,7 +105,8 @@ typedef struct gns_block {
   uint64_t* row_scan;      /* exclusive scan, packed (cached_prefix<<32 | fill_prefix); [n] = totals */
   int32_t* dst_degree;     /* deg(dst) (sampling.py:149)                              */
   int32_t* self_pos;       /* searchsorted(src_nodes, dst_nodes) (model.py:137)       */
-  int32_t* hub_rows;       /* tier lists: warp-per-row rows from the front, CTA-per-row rows from the back */
+  int32_t* hub_rows;       /* tier lists, capacity 2*max_dst: thread-per-row rows in [0, max_dst),
+                              warp-per-row rows from max_dst up, CTA-per-row rows from 2*max_dst-1 down */
   /* per edge, capacity max_edges; order = cached edges then fill edges, each by (dst row, key) */
   int32_t* edge_node;      /* global id of the sampled neighbour                       */
   int32_t* edge_src;       /* relabelled: index into src_nodes (sampling.py:145)       */

@@ -143,13 +143,20 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(LayerArgs 
         a.b.row_scan[r] = ex;
         a.b.dst_degree[r] = ri.deg;
         if (a.dbits) mark_node(a.dbits, a.dsum, ri.node);
+        // tier lists in hub_rows[2*max_dst]: thread rows [0, max_dst), warp
+        // rows from max_dst upwards, hub rows from 2*max_dst-1 downwards
         const int tier = row_tier(ri, a.k);
-        if (tier == 1) {  // warp-tier rows fill hub_rows from the front
+        if (tier == 0) {
+          if (ri.m > 0 || ri.fill > 0) {
+            int h = atomicAdd(a.b.counts + GNS_CNT_THREADROWS, 1);
+            a.b.hub_rows[h] = (int32_t)r;
+          }
+        } else if (tier == 1) {
           int h = atomicAdd(a.b.counts + GNS_CNT_WARPROWS, 1);
-          a.b.hub_rows[h] = (int32_t)r;
-        } else if (tier == 2) {  // hub rows from the back
+          a.b.hub_rows[a.max_dst + h] = (int32_t)r;
+        } else {
           int h = atomicAdd(a.b.counts + GNS_CNT_HUBS, 1);
-          a.b.hub_rows[a.max_dst - 1 - h] = (int32_t)r;
+          a.b.hub_rows[2 * a.max_dst - 1 - h] = (int32_t)r;
         }
       },
       [&](unsigned long long tot) {
@@ -420,10 +427,10 @@ __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a_in) {
   // per-thread 16-entry key slots, interleaved by lane (bank-conflict free)
   __shared__ uint64_t s_keys[256 / 32][16 * 32];
   uint64_t* slot = &s_keys[threadIdx.x >> 5][threadIdx.x & 31];
-  const int64_t n = a.n_dev[0];
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t nl = a.b.counts[GNS_CNT_THREADROWS];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nl; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = a.b.hub_rows[j];
     RowInfo ri = row_info(a, r);
-    if (row_tier(ri, a.k) != 0) continue;
     PhaseDesc ph[2];
     make_phases(a, ri, r, ph[0], ph[1]);
 #pragma unroll 1
@@ -441,7 +448,7 @@ __global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a_in)
   const int64_t gw = (blockIdx.x * (int64_t)kSampBlock + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSampBlock) >> 5;
   for (int64_t j = gw; j < nl; j += nw) {
-    const int64_t r = a.b.hub_rows[j];
+    const int64_t r = a.b.hub_rows[a.max_dst + j];
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
@@ -457,7 +464,7 @@ __global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(LayerArgs a_in) {
   __shared__ int s_found;
   const int nh = a.b.counts[GNS_CNT_HUBS];
   for (int h = blockIdx.x; h < nh; h += gridDim.x) {
-    const int64_t r = a.b.hub_rows[a.max_dst - 1 - h];
+    const int64_t r = a.b.hub_rows[2 * a.max_dst - 1 - h];
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);

@@ -96,18 +96,26 @@ class GraphedTrainer:
 
     # -- one training step on a slot (captured) ------------------------------------
     def _train_body(self, slot: int, with_adam: bool):
-        m, sl, L, s = self.model, self.slots[slot], self.L, _lib.stream_ptr()
-        blocks = [sl.layers[L - 1 - li] for li in range(L)]
-        d0 = self.dims[0]
+        self._gather(slot)
+        self._train_rest(slot, with_adam)
+
+    def _gather(self, slot: int):
+        """features[input_nodes] -> h0 (model.py:146)."""
+        sl, L, s = self.slots[slot], self.L, _lib.stream_ptr()
+        b0 = sl.layers[L - 1]
         tab = self.g.features
-        n_in_dev = blocks[0].counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
+        n_in_dev = b0.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
         ev = self._prof_events
         if ev is not None:
             _lib.call("gns_record_event_external", ev[0].cuda_event, s)
-        _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, blocks[0].src_nodes.data_ptr(),
-                  n_in_dev.data_ptr(), self.cap_src[0], d0, self.h0.data_ptr(), self.h0.stride(0), 0, s)
+        _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, b0.src_nodes.data_ptr(),
+                  n_in_dev.data_ptr(), self.cap_src[0], self.dims[0], self.h0.data_ptr(), self.h0.stride(0), 0, s)
         if ev is not None:
             _lib.call("gns_record_event_external", ev[1].cuda_event, s)
+
+    def _train_rest(self, slot: int, with_adam: bool):
+        m, sl, L, s = self.model, self.slots[slot], self.L, _lib.stream_ptr()
+        blocks = [sl.layers[L - 1 - li] for li in range(L)]
         h = self.h0
         with m._tf32():
             for li in range(L):
@@ -212,12 +220,15 @@ class GraphedTrainer:
                 self._per_replay = _lib.launch_counter[0] - c0
             gph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gph, stream=self.main):
+                # the HBM-bound gather runs alone first; the (latency-bound)
+                # sampler branch then overlaps the rest of the training step
+                self._gather(p)
                 fork = torch.cuda.Event()
                 fork.record(self.main)
                 self.side.wait_event(fork)
                 with torch.cuda.stream(self.side):
                     self._sample_body(1 - p)
-                self._train_body(p, with_adam=False)
+                self._train_rest(p, with_adam=False)
                 join = torch.cuda.Event()
                 join.record(self.side)
                 self.main.wait_event(join)
