@@ -207,6 +207,19 @@ __device__ __forceinline__ void emit_edge(const LayerArgs& a, const RowInfo& ri,
   a.b.edge_cached[o] = ph.phase == 0 ? 1 : 0;
 }
 
+// Weight of a selected edge (sampling.py:168,252-258).
+__device__ __forceinline__ double edge_weight_of(const LayerArgs& a, const RowInfo& ri, const PhaseDesc& ph,
+                                                 double incl_u) {
+  if (ph.phase == 0) {
+    double q = DDIV((double)a.k, (double)min(a.k, max(ri.nc, 1)));
+    double coeff = DMUL(incl_u, q);
+    if (!(coeff > 0.0)) atomicOr((unsigned*)(a.b.counts + GNS_CNT_ERR), GNS_ERRBIT_ZEROPROB);
+    return DDIV(1.0, coeff);
+  }
+  if (ph.phase == 1) return DDIV((double)(ri.deg - ri.nc), (double)max(ri.fill, 1));
+  return DDIV((double)ri.deg, (double)max(ri.fill, 1));
+}
+
 // warp-cooperative selection of one phase of one row
 __device__ void warp_select(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
                             uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpos) {
@@ -385,8 +398,8 @@ __device__ __forceinline__ void sort16(uint64_t (&a)[16]) {
 // reference's stable lexsort — a 16-wide sorting network orders them and the
 // first `take` are emitted.  Keys are staged per thread in shared memory so
 // the Philox and emit loops stay rolled (small code, no local memory).
-__device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
-                                             uint64_t* __restrict__ slot) {
+__device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInfo& ri, int64_t r,
+                                                const PhaseDesc& ph) {
   const uint32_t stream = stream_word(32, a.layer, ph.phase);
   const int len = ph.len;
   // 1. all neighbour ids and cache-bitmap words of the fill phase in flight
@@ -415,18 +428,40 @@ __device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInf
   }
   // 3. (key, position) order = the reference's stable lexsort
   sort16(v);
+  // 4. emit the first `take`: every load (neighbour id, inclusion, dedup word)
+  //    of all selected edges is issued before any store, so the edges' memory
+  //    latencies overlap instead of serialising behind possibly-aliasing stores
+  const int take = ph.take;
+  int32_t u[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) slot[i * 32] = v[i];
-  // 4. emit the first `take` (loads of several edges in flight)
-#pragma unroll 4
-  for (int i = 0; i < ph.take; ++i) emit_edge(a, ri, r, ph, i, (uint32_t)(slot[i * 32] & 2047u));
+  for (int i = 0; i < 16; ++i) u[i] = i < take ? __ldg(ph.ids + (uint32_t)(v[i] & 2047u)) : 0;
+  double inc[16];
+  uint32_t bw[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    inc[i] = (i < take && ph.phase == 0) ? __ldg(a.incl + u[i]) : 0.0;
+    bw[i] = i < take ? __ldg(a.dbits + (u[i] >> 5)) : 0u;
+  }
+  const int64_t o0 = ph.out_base;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i < take) {
+      const double w = edge_weight_of(a, ri, ph, inc[i]);
+      const uint32_t m = 1u << (u[i] & 31);
+      if (!(bw[i] & m)) {
+        const uint32_t old = atomicOr(a.dbits + (u[i] >> 5), m);
+        if (old == 0u) atomicOr(a.dsum + ((u[i] >> 5) >> 5), 1u << ((u[i] >> 5) & 31));
+      }
+      a.b.edge_node[o0 + i] = u[i];
+      a.b.edge_dst[o0 + i] = (int32_t)r;
+      a.b.edge_weight[o0 + i] = w;
+      a.b.edge_cached[o0 + i] = ph.phase == 0 ? 1 : 0;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a_in) {
   const LayerArgs a = resolve_rng(a_in);
-  // per-thread 16-entry key slots, interleaved by lane (bank-conflict free)
-  __shared__ uint64_t s_keys[256 / 32][16 * 32];
-  uint64_t* slot = &s_keys[threadIdx.x >> 5][threadIdx.x & 31];
   const int64_t nl = a.b.counts[GNS_CNT_THREADROWS];
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nl; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = a.b.hub_rows[j];
@@ -435,7 +470,7 @@ __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a_in) {
     make_phases(a, ri, r, ph[0], ph[1]);
 #pragma unroll 1
     for (int j = 0; j < 2; ++j)
-      if (ph[j].take > 0) thread_select16(a, ri, r, ph[j], slot);
+      if (ph[j].take > 0) thread_select16(a, ri, r, ph[j]);
   }
 }
 
