@@ -99,11 +99,9 @@ __device__ __forceinline__ RowInfo row_info(const LayerArgs& a, int64_t r) {
   return ri;
 }
 
-// 0 = thread per row, 1 = warp per row, 2 = CTA per row (hub)
-__device__ __forceinline__ int row_tier(const RowInfo& ri, int k) {
-  int sc = ri.m > 0 ? ri.nc : 0;
-  int sf = ri.fill > 0 ? ri.deg : 0;
-  int len = max(sc, sf);
+// Work item = (row, phase); tier by the positions the phase scans:
+// 0 = thread per item (<= 16), 1 = warp per item (<= kHubLen), 2 = CTA (hub)
+__device__ __forceinline__ int phase_tier(int len) {
   if (len > kHubLen) return 2;
   if (len > kThreadLen) return 1;
   return 0;
@@ -143,20 +141,27 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(LayerArgs 
         a.b.row_scan[r] = ex;
         a.b.dst_degree[r] = ri.deg;
         if (a.dbits) mark_node(a.dbits, a.dsum, ri.node);
-        // tier lists in hub_rows[2*max_dst]: thread rows [0, max_dst), warp
-        // rows from max_dst upwards, hub rows from 2*max_dst-1 downwards
-        const int tier = row_tier(ri, a.k);
-        if (tier == 0) {
-          if (ri.m > 0 || ri.fill > 0) {
+        // (row, phase) work items in hub_rows[4*max_dst]: thread items in
+        // [0, 2*max_dst), warp items from 2*max_dst up, hub items from
+        // 4*max_dst-1 down.  The two phases of a row are independent (their
+        // output offsets come from the scan), so they run concurrently.
+#pragma unroll
+        for (int ph = 0; ph < 2; ++ph) {
+          const int take = ph == 0 ? ri.m : ri.fill;
+          if (take <= 0) continue;
+          const int len = ph == 0 ? ri.nc : ri.deg;
+          const int32_t item = (int32_t)((r << 1) | ph);
+          const int tier = phase_tier(len);
+          if (tier == 0) {
             int h = atomicAdd(a.b.counts + GNS_CNT_THREADROWS, 1);
-            a.b.hub_rows[h] = (int32_t)r;
+            a.b.hub_rows[h] = item;
+          } else if (tier == 1) {
+            int h = atomicAdd(a.b.counts + GNS_CNT_WARPROWS, 1);
+            a.b.hub_rows[2 * a.max_dst + h] = item;
+          } else {
+            int h = atomicAdd(a.b.counts + GNS_CNT_HUBS, 1);
+            a.b.hub_rows[4 * a.max_dst - 1 - h] = item;
           }
-        } else if (tier == 1) {
-          int h = atomicAdd(a.b.counts + GNS_CNT_WARPROWS, 1);
-          a.b.hub_rows[a.max_dst + h] = (int32_t)r;
-        } else {
-          int h = atomicAdd(a.b.counts + GNS_CNT_HUBS, 1);
-          a.b.hub_rows[2 * a.max_dst - 1 - h] = (int32_t)r;
         }
       },
       [&](unsigned long long tot) {
@@ -464,13 +469,12 @@ __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a_in) {
   const LayerArgs a = resolve_rng(a_in);
   const int64_t nl = a.b.counts[GNS_CNT_THREADROWS];
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nl; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = a.b.hub_rows[j];
+    const int32_t item = a.b.hub_rows[j];
+    const int64_t r = item >> 1;
     RowInfo ri = row_info(a, r);
-    PhaseDesc ph[2];
-    make_phases(a, ri, r, ph[0], ph[1]);
-#pragma unroll 1
-    for (int j = 0; j < 2; ++j)
-      if (ph[j].take > 0) thread_select16(a, ri, r, ph[j]);
+    PhaseDesc pc, pf;
+    make_phases(a, ri, r, pc, pf);
+    thread_select16(a, ri, r, (item & 1) ? pf : pc);
   }
 }
 
@@ -483,12 +487,12 @@ __global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a_in)
   const int64_t gw = (blockIdx.x * (int64_t)kSampBlock + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSampBlock) >> 5;
   for (int64_t j = gw; j < nl; j += nw) {
-    const int64_t r = a.b.hub_rows[a.max_dst + j];
+    const int32_t item = a.b.hub_rows[2 * a.max_dst + j];
+    const int64_t r = item >> 1;
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
-    if (pc.take > 0) warp_select(a, ri, r, pc, s_key[w], s_pos[w]);
-    if (pf.take > 0) warp_select(a, ri, r, pf, s_key[w], s_pos[w]);
+    warp_select(a, ri, r, (item & 1) ? pf : pc, s_key[w], s_pos[w]);
   }
 }
 
@@ -499,12 +503,12 @@ __global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(LayerArgs a_in) {
   __shared__ int s_found;
   const int nh = a.b.counts[GNS_CNT_HUBS];
   for (int h = blockIdx.x; h < nh; h += gridDim.x) {
-    const int64_t r = a.b.hub_rows[2 * a.max_dst - 1 - h];
+    const int32_t item = a.b.hub_rows[4 * a.max_dst - 1 - h];
+    const int64_t r = item >> 1;
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
-    if (pc.take > 0) block_select(a, ri, r, pc, s_key, s_pos, &s_found);
-    if (pf.take > 0) block_select(a, ri, r, pf, s_key, s_pos, &s_found);
+    block_select(a, ri, r, (item & 1) ? pf : pc, s_key, s_pos, &s_found);
   }
 }
 
@@ -741,10 +745,10 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   layer_count_apply_kernel<<<tiles, kCntBlock, 0, stream>>>(a, ctiles);
   GNS_TRY(check_launch("layer_count"));
   const int sms = num_sms();
-  int tgrid = grid_for((max_dst + 255) / 256, (long long)sms * 16);
+  int tgrid = grid_for((2 * max_dst + 255) / 256, (long long)sms * 16);
   sample_thread_kernel<<<tgrid, 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_thread"));
-  int grid = grid_for((max_dst * 32 + kSampBlock - 1) / kSampBlock, (long long)sms * 8);
+  int grid = grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock, (long long)sms * 8);
   sample_warp_kernel<<<grid, kSampBlock, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_warp"));
   sample_hub_kernel<<<sms, kHubBlock, 0, stream>>>(a);
