@@ -245,9 +245,17 @@ def main():
     tr.capture_profiled()
     nprof = min(30, args.steps)
 
+    spmm_ms, spmm_bytes = [], []
+
     def on_step(e, i, k):
         gather_ms.append(tr.gather_ms())
-        n_in.append(int(tr.slots[k % 2].counts[len(FANOUTS) - 1, _lib.CNT_SRC]))
+        spmm_ms.append(tr.spmm0_ms())
+        cnt = tr.slots[k % 2].counts[len(FANOUTS) - 1].tolist()
+        n_in.append(cnt[_lib.CNT_SRC])
+        nd, ne = cnt[_lib.CNT_DST], cnt[_lib.CNT_EDGES]
+        # input-layer SpMM: h rows read (edges + self) + cat rows written (incl.
+        # capacity zero padding) + per-edge index/weight (4 + 8 B) + row scan
+        spmm_bytes.append((ne + nd) * 4 * c["dim"] + tr.npad[0] * 2 * 4 * c["dim"] + 12 * ne + 8 * nd)
     pos = tr.run(nprof, epoch=pos[0], first=pos[1], on_step=on_step)
     n_in = np.array(n_in, dtype=np.float64)
     row_bytes = 4 * c["dim"]
@@ -260,6 +268,14 @@ def main():
                 "avg_launch_ms": float(np.mean(gather_ms)),
                 "share_of_step": float(np.mean(gather_ms) / (ms / args.steps)),
                 "measured": f"CUDA events around the gather inside the captured step graph, {nprof} replays"}
+    spmm_gbs = float(np.sum(spmm_bytes) / (np.sum(spmm_ms) / 1e3) / 1e9)
+    kernels = {
+        "gns_gather_rows": {"achieved_gbs": round(gather_gbs, 1), "frac": round(gather_gbs / peak, 4),
+                            "avg_ms": float(np.mean(gather_ms))},
+        "gns_spmm_fwd (input layer)": {"achieved_gbs": round(spmm_gbs, 1), "frac": round(spmm_gbs / peak, 4),
+                                       "avg_ms": float(np.mean(spmm_ms)),
+                                       "algorithmic_bytes_per_launch": float(np.mean(spmm_bytes))},
+    }
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_path):
         try:
@@ -312,7 +328,7 @@ def main():
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
+                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
                 "gpu_launches_per_step": launches_total / args.steps, "clocks": clk,
                 "per_step": {"input_nodes": float(n_in.mean()), "gather_ms": float(np.mean(gather_ms)),
                              "graph_replays": args.steps}}

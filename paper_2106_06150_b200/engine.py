@@ -120,8 +120,13 @@ class GraphedTrainer:
         with m._tf32():
             for li in range(L):
                 d_in = self.dims[li]
+                ev = self._prof_events if li == 0 else None
+                if ev is not None:
+                    _lib.call("gns_record_event_external", ev[2].cuda_event, s)
                 _lib.call("gns_spmm_fwd", 0, h.data_ptr(), h.stride(0), d_in, 1 if li > 0 else 0, blocks[li].cblock,
                           self.cap_dst[li], self.npad[li], self.cat[li].data_ptr(), self.cat[li].stride(0), s)
+                if ev is not None:
+                    _lib.call("gns_record_event_external", ev[3].cuda_event, s)
                 torch.addmm(m.biases[li], self.cat[li][:self.cap_dst[li]], m.weights[li], out=self.z[li])
                 h = self.z[li]
             top = blocks[L - 1]
@@ -193,7 +198,7 @@ class GraphedTrainer:
         """Re-capture with timing events around the input-feature gather
         (gns_gather_rows) so its per-launch duration can be read after each
         replay (used by bench.py for the roofline; not for the headline)."""
-        self._prof_events = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        self._prof_events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         for e in self._prof_events:      # materialise the driver events
             e.record(self.main)
         torch.cuda.synchronize()
@@ -203,6 +208,12 @@ class GraphedTrainer:
         e = self._prof_events
         e[1].synchronize()
         return float(e[0].elapsed_time(e[1]))
+
+    def spmm0_ms(self) -> float:
+        """Duration of the input-layer aggregation SpMM in the last replay."""
+        e = self._prof_events
+        e[3].synchronize()
+        return float(e[2].elapsed_time(e[3]))
 
     def _capture(self):
         torch.cuda.synchronize()
