@@ -132,6 +132,16 @@ GNS_API int gns_record_event_external(void* event, void* stream);
 /* degree_probs (cache.py:53-58): out[i] = deg(i) / E in float64. */
 GNS_API int gns_degree_probs(const gns_graph_t* g, double* out_probs, void* stream);
 
+/* random_walk_probs (cache.py:61-84): p0 = 1/|train| on train_ids, then for
+ * l < num_layers: p <- d*(A p) + p with d_i = min(fanouts_host[l], deg_i) /
+ * max(deg_i, 1) (A p summed per row in CSR order: bit-identical to scipy),
+ * then p / sum(p) with a fixed-order strided sum.  fanouts_host is a HOST
+ * array of num_layers ints. */
+GNS_API size_t gns_random_walk_workspace_size(int64_t num_nodes);
+GNS_API int gns_random_walk_probs(const gns_graph_t* g, const int32_t* train_ids, int64_t n_train,
+                                  const int32_t* fanouts_host, int32_t num_layers, double* out_probs,
+                                  void* ws, size_t ws_bytes, void* stream);
+
 /* sample_cache (cache.py:87-103) + NodeSet.from_ids (graph.py:118-125):
  * exponential race keys -log(1-U)/p over p>0, smallest min(cache_size,
  * |support|) by (key, id) via radix select, emitted as sorted ids + bitmap.

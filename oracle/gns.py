@@ -162,6 +162,54 @@ def degree_probs(g) -> np.ndarray:
     return w
 
 
+RW_SUM_THREADS = 148 * 256  # fixed strided-sum width of gns_random_walk_probs
+
+
+def random_walk_probs(g, train, fanouts, num_layers: int, device_order: bool = True):
+    """cache.py:61-84.  The iterate uses scipy's CSR matvec (ascending
+    neighbour order, exactly the reference); the final normalising sum is
+    the build's fixed-order strided reduction (``device_order``) or numpy's
+    pairwise ``p.sum()`` (the reference)."""
+    import scipy.sparse as sp
+    g = as_ograph(g)
+    if num_layers < 1:
+        raise ValueError("num_layers must be >= 1")
+    train = np.asarray(train, dtype=np.int64)
+    if len(train) == 0:
+        raise ValueError("training set is empty")
+    adj = sp.csr_matrix((np.ones(g.num_edges), np.asarray(g.indices), np.asarray(g.indptr)),
+                        shape=(g.num_nodes, g.num_nodes))
+    deg = g.degrees.astype(np.float64)
+    safe_deg = np.maximum(deg, 1.0)
+    p = np.zeros(g.num_nodes, dtype=np.float64)
+    p[train] = 1.0 / len(train)
+    for step in range(num_layers):
+        d = np.minimum(float(fanouts[step]), deg) / safe_deg
+        p = d * (adj @ p) + p
+    if not device_order:
+        return p / p.sum()
+    T = RW_SUM_THREADS
+    m = (len(p) + T - 1) // T
+    padded = np.zeros(m * T)
+    padded[:len(p)] = p
+    rows = padded.reshape(m, T)
+    # Neumaier-compensated sums, thread t over x[t], x[t+T], ... then over t
+    s_, c_ = np.zeros(T), np.zeros(T)
+    for i in range(m):
+        x = rows[i]
+        t = s_ + x
+        big = np.abs(s_) >= np.abs(x)
+        c_ = c_ + np.where(big, (s_ - t) + x, (x - t) + s_)
+        s_ = t
+    partial = s_ + c_
+    s1, c1 = 0.0, 0.0
+    for x in partial.tolist():
+        t = s1 + x
+        c1 += ((s1 - t) + x) if abs(s1) >= abs(x) else ((x - t) + s1)
+        s1 = t
+    return p / (s1 + c1)
+
+
 def cache_keys_philox(w: np.ndarray, support: np.ndarray, seed: int, epoch: int):
     """Exponential-race keys Exp(1)/w over the positive support (cache.py:101),
     with Exp(1) = -log(1 - U), U from Philox at (tag 33, pos = node id)."""

@@ -9,7 +9,7 @@ the GraphSAGE aggregation path, all running as hand-written sm_100a kernels in
 
 from ._lib import GraphFormatError, InvariantError
 from .cache import (CacheState, ProbVector, build_cache, degree_probs, inclusion_prob,
-                    sample_cache)
+                    random_walk_probs, sample_cache)
 from .graph import Graph, NodeSet, generate_powerlaw_device
 from .model import GraphSAGE, TrainConfig, init_params_numpy, micro_f1
 from .pool import BatchItem, SamplerPool, epoch_targets

@@ -68,6 +68,9 @@ _SIGS = {
     "gns_version": (c_int32, []),
     "gns_record_event_external": (c_int32, [c_void_p, c_void_p]),
     "gns_degree_probs": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p]),
+    "gns_random_walk_workspace_size": (c_size_t, [c_int64]),
+    "gns_random_walk_probs": (c_int32, [POINTER(GnsGraph), c_void_p, c_int64, c_void_p, c_int32, c_void_p,
+                                        c_void_p, c_size_t, c_void_p]),
     "gns_cache_draw_workspace_size": (c_size_t, [c_int64]),
     "gns_cache_draw": (c_int32, [c_void_p, c_int64, c_int64, c_uint32, c_uint32, c_void_p,
                                  c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
@@ -168,7 +171,7 @@ def check(rc: int, what: str = ""):
 # device kernels each entry point launches (memsets excluded) — used to report
 # how many of OUR kernels ran inside a timed region
 KERNELS_PER_CALL = {
-    "gns_degree_probs": 1, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
+    "gns_degree_probs": 1, "gns_random_walk_probs": 9, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
     "gns_cached_csr_fill": 1, "gns_sample_layer": 8, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
     "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 7,

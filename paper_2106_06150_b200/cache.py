@@ -18,6 +18,7 @@ keys Philox with (seed, epoch); a bare int is (seed, 0).
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -84,6 +85,27 @@ def degree_probs(g: Graph) -> ProbVector:
         raise ValueError("graph has no edges; degree distribution undefined")
     out = torch.empty(g.num_nodes, dtype=torch.float64, device=g.device)
     _lib.call("gns_degree_probs", g.cstruct(), out.data_ptr(), _lib.stream_ptr())
+    return ProbVector(out, normalized=True)
+
+
+def random_walk_probs(g: Graph, train, fanouts, num_layers: int) -> ProbVector:
+    """cache.py:61-84: L-step spread of the training-set indicator
+    (p <- d*(A p) + p, d_i = min(fanout, deg_i)/max(deg_i, 1)), normalised.
+    ``train`` is a NodeSet or an id tensor/array."""
+    _lib.require_cuda()
+    if num_layers < 1:
+        raise ValueError("num_layers must be >= 1")
+    if len(fanouts) < num_layers:
+        raise ValueError("need one fanout per layer")
+    ids = train.ids if isinstance(train, NodeSet) else torch.as_tensor(train, device=g.device)
+    ids = ids.to(device=g.device, dtype=torch.int32).contiguous()
+    if ids.numel() == 0:
+        raise ValueError("training set is empty")
+    out = torch.empty(g.num_nodes, dtype=torch.float64, device=g.device)
+    ws = _lib.workspace(_lib.lib().gns_random_walk_workspace_size(g.num_nodes), g.device)
+    fan = (ctypes.c_int32 * num_layers)(*[int(f) for f in fanouts[:num_layers]])
+    _lib.call("gns_random_walk_probs", g.cstruct(), ids.data_ptr(), ids.numel(), fan, num_layers, out.data_ptr(),
+              ws.data_ptr(), ws.numel(), _lib.stream_ptr())
     return ProbVector(out, normalized=True)
 
 

@@ -345,3 +345,124 @@ int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits, const i
 }
 
 }  // extern "C"
+
+// ---- random-walk cache distribution (cache.py:61-84) -----------
+// p0 = 1/|train| on the train set; L times p <- d * (A p) + p with
+// d_i = min(fanout_l, deg_i) / max(deg_i, 1); then p / sum(p).
+// A p is summed sequentially per row in CSR (ascending neighbour) order with
+// explicitly rounded adds, exactly like scipy's csr_matvec, so the iterate is
+// bit-identical to the reference.  The normalising sum is a fixed-order
+// strided reduction (restated in oracle/gns.py:random_walk_probs).
+namespace gns {
+
+__global__ void rw_init_kernel(double* __restrict__ p, int64_t n, const int32_t* __restrict__ train, int64_t nt,
+                               double val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+
+__global__ void rw_set_kernel(double* __restrict__ p, const int32_t* __restrict__ train, int64_t nt, double val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x)
+    p[train[i]] = val;
+}
+
+__global__ void rw_step_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t n,
+                               double fanout, const double* __restrict__ p, double* __restrict__ q) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = indptr[i], e = indptr[i + 1];
+    double s = 0.0;
+    int64_t j = b;
+    for (; j + 4 <= e; j += 4) {  // loads in flight, adds in order
+      const double x0 = p[__ldg(indices + j)], x1 = p[__ldg(indices + j + 1)];
+      const double x2 = p[__ldg(indices + j + 2)], x3 = p[__ldg(indices + j + 3)];
+      s = DADD(DADD(DADD(DADD(s, x0), x1), x2), x3);
+    }
+    for (; j < e; ++j) s = DADD(s, p[__ldg(indices + j)]);
+    const double deg = (double)(e - b);
+    const double d = DDIV(fmin(fanout, deg), fmax(deg, 1.0));
+    q[i] = DADD(DMUL(d, s), p[i]);
+  }
+}
+
+// Neumaier-compensated running sum (exact op sequence restated in the oracle)
+__device__ __forceinline__ void neumaier_add(double& s, double& c, double x) {
+  const double t = DADD(s, x);
+  if (fabs(s) >= fabs(x))
+    c = DADD(c, DADD(DSUB(s, t), x));
+  else
+    c = DADD(c, DADD(DSUB(x, t), s));
+  s = t;
+}
+
+// partial[t] = compensated sum of x[t], x[t+T], x[t+2T], ... (T = gridDim*blockDim)
+__global__ void strided_sum_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ partial) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  double s = 0.0, c = 0.0;
+  for (int64_t i = t; i < n; i += T) neumaier_add(s, c, x[i]);
+  partial[t] = DADD(s, c);
+}
+
+__global__ void seq_sum_kernel(const double* __restrict__ partial, int64_t T, double* __restrict__ total) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double s = 0.0, c = 0.0;
+    for (int64_t t = 0; t < T; ++t) neumaier_add(s, c, partial[t]);
+    total[0] = DADD(s, c);
+  }
+}
+
+__global__ void scale_kernel(double* __restrict__ p, int64_t n, const double* __restrict__ total) {
+  const double s = total[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = DDIV(p[i], s);
+}
+
+static constexpr int kSumGrid = 148, kSumBlock = 256;  // fixed T: part of the reduction order
+
+}  // namespace gns
+
+extern "C" {
+
+size_t gns_random_walk_workspace_size(int64_t num_nodes) {
+  return ((size_t)num_nodes * 8 + 255) / 256 * 256 + (size_t)kSumGrid * kSumBlock * 8 + 512;
+}
+
+int gns_random_walk_probs(const gns_graph_t* g, const int32_t* train_ids, int64_t n_train,
+                          const int32_t* fanouts_host, int32_t num_layers, double* out_probs, void* ws,
+                          size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int64_t n = g->num_nodes;
+  if (num_layers < 1) {
+    set_error("num_layers must be >= 1");
+    return GNS_EINVAL;
+  }
+  if (n_train <= 0) {
+    set_error("training set is empty");
+    return GNS_EINVAL;
+  }
+  if (ws_bytes < gns_random_walk_workspace_size(n)) {
+    set_error("random_walk_probs: workspace too small");
+    return GNS_EINVAL;
+  }
+  double* tmp = (double*)ws;
+  double* partial = (double*)((char*)ws + ((size_t)n * 8 + 255) / 256 * 256);
+  double* total = partial + kSumGrid * kSumBlock;
+  const int grid = num_sms() * 8;
+  rw_init_kernel<<<grid, 256, 0, stream>>>(out_probs, n, train_ids, n_train, 0.0);
+  rw_set_kernel<<<grid, 256, 0, stream>>>(out_probs, train_ids, n_train, 1.0 / (double)n_train);
+  double* p = out_probs;
+  double* q = tmp;
+  for (int l = 0; l < num_layers; ++l) {
+    rw_step_kernel<<<grid, 256, 0, stream>>>(g->indptr, g->indices, n, (double)fanouts_host[l], p, q);
+    double* t = p;
+    p = q;
+    q = t;
+  }
+  strided_sum_kernel<<<kSumGrid, kSumBlock, 0, stream>>>(p, n, partial);
+  seq_sum_kernel<<<1, 32, 0, stream>>>(partial, (int64_t)kSumGrid * kSumBlock, total);
+  scale_kernel<<<grid, 256, 0, stream>>>(p, n, total);
+  if (p != out_probs) GNS_CUDA(cudaMemcpyAsync(out_probs, p, (size_t)n * 8, cudaMemcpyDeviceToDevice, stream));
+  return check_launch("random_walk_probs");
+}
+
+}  // extern "C"

@@ -48,15 +48,14 @@ class BatchItem:
 
 
 def cache_probs(g: Graph, config: SamplerConfig):
-    """pool.py:44-57 (degree mode; the random-walk mode is SURVEY.md §8(f)1)."""
+    """pool.py:44-57: "auto" -> degree iff >= 50% of nodes train, else walk."""
     mode = config.cache_mode
     if mode == "auto":
-        n_train = g.num_nodes if g.train_mask is None else int(g.train_mask.sum())
+        n_train = g.train_ids().numel()
         mode = "degree" if n_train * 2 >= g.num_nodes else "walk"
     if mode == "degree":
         return cache_mod.degree_probs(g)
-    raise NotImplementedError("random-walk cache probabilities (cache.py:61-84) are SURVEY.md "
-                              "§8(f)1; pin cache_mode='degree'")
+    return cache_mod.random_walk_probs(g, g.train_ids(), config.fanouts, config.num_layers)
 
 
 def num_batches(g: Graph, config: SamplerConfig) -> int:

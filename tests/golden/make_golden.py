@@ -90,6 +90,12 @@ def make_sampler_golden():
                                     O.ReplayRng(rec))
             _block_arrays(f"{name}_e{epoch}_i{index}", mb, out)
             out[f"{name}_e{epoch}_i{index}_nblocks"] = np.array(len(mb.blocks))
+    # random-walk cache distribution (cache.py:61-84) with a 10% train set
+    wmask = np.random.default_rng(11).random(g.num_nodes) < 0.1
+    out["walk_train_ids"] = np.flatnonzero(wmask)
+    ts = gb.NodeSet.from_mask(wmask)
+    out["walk_probs_L3"] = gb.random_walk_probs(g, ts, (15, 10, 5), 3).weights
+    out["walk_probs_L1"] = gb.random_walk_probs(g, ts, (4,), 1).weights
     np.savez_compressed(os.path.join(HERE, "golden_sampler.npz"), **out)
 
 

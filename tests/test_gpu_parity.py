@@ -550,3 +550,26 @@ def test_graphed_trainer_matches_eager(P):
     # a second epoch re-draws the cache and re-captures
     n2 = tr.run_epoch(1)
     assert n2 == len(losses)
+
+
+# ---- random-walk cache distribution -----------------------------
+
+def test_random_walk_probs(P, golden):
+    gold = golden["sampler"]
+    og, g = _golden_graph(P, gold)
+    tid = gold["walk_train_ids"]
+    for L, fan, key in ((3, (15, 10, 5), "walk_probs_L3"), (1, (4,), "walk_probs_L1")):
+        pv = P.random_walk_probs(g, torch.as_tensor(tid, dtype=torch.int32, device="cuda"), fan, L)
+        got = pv.weights.cpu().numpy()
+        assert np.array_equal(got, O.random_walk_probs(og, tid, fan, L))          # bit-exact vs oracle
+        ref = gold[key]
+        nz = np.maximum(np.abs(ref), 1e-300)
+        assert np.max(np.abs(got - ref) / np.spacing(nz)) <= 4                   # vs reference
+    # pool "auto" mode picks the walk distribution when < 50% of nodes train
+    mask = np.zeros(og.num_nodes, dtype=bool)
+    mask[tid] = True
+    g2 = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices, train_mask=mask)
+    from paper_2106_06150_b200.pool import cache_probs
+    cfg = P.SamplerConfig(strategy="GNS", cache_mode="auto")
+    pv = cache_probs(g2, cfg)
+    assert np.array_equal(pv.weights.cpu().numpy(), O.random_walk_probs(og, tid, (15, 10, 5), 3))

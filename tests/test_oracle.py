@@ -208,3 +208,21 @@ def test_oracle_model_equals_reference(gb):
     gr = gb.backward(mb, g.features, p_ref, grad)
     for a, b in zip(dw + db, gr.weights + gr.biases):
         assert np.array_equal(a, b)
+
+
+def test_oracle_random_walk_probs_equals_reference(gb):
+    g = gb.generate_powerlaw(2000, 3, 1)
+    rng = np.random.default_rng(0)
+    mask = rng.random(2000) < 0.1
+    g = g.replace(train_mask=mask)
+    ts = gb.graph.train_set(g)
+    for L, fan in ((1, (3,)), (3, (15, 10, 5))):
+        ref = gb.random_walk_probs(g, ts, fan, L).weights
+        ours_np = O.random_walk_probs(g, ts.ids, fan, L, device_order=False)
+        assert np.array_equal(ref, ours_np)                     # same iterate + same sum
+        ours = O.random_walk_probs(g, ts.ids, fan, L)           # build's fixed-order sum
+        assert _ulps(ours, ref) <= 4
+        assert abs(ours.sum() - 1.0) < 1e-12
+    # SPEC.md:144-146 examples: path 0-1-2, train={0}, fanout 1, L=1 -> [2/3, 1/3, 0]
+    path = O.build_csr([(0, 1), (1, 2)], 3)
+    np.testing.assert_allclose(O.random_walk_probs(path, [0], (1,), 1), [2 / 3, 1 / 3, 0.0], rtol=1e-15)
