@@ -316,6 +316,15 @@ GNS_API int gns_gen_powerlaw_count(int64_t num_nodes, int64_t num_pairs, double 
 GNS_API int gns_gen_powerlaw_fill(int64_t num_nodes, int64_t num_pairs, const int64_t* indptr,
                           int32_t* out_indices, void* ws, size_t ws_bytes, void* stream);
 
+/* build_csr (graph.py:142-169) on the device from caller-given endpoint arrays
+ * (int32 u[m], v[m], all in [0, num_nodes)): symmetrise, drop self loops and
+ * duplicates, sort rows.  Same two phases / workspace as the generator. */
+GNS_API int gns_build_csr_count(int64_t num_nodes, const int32_t* u, const int32_t* v, int64_t num_pairs,
+                                int64_t* out_indptr, int64_t* out_nnz_dev, void* ws, size_t ws_bytes,
+                                void* stream);
+GNS_API int gns_build_csr_fill(int64_t num_nodes, int64_t num_pairs, const int64_t* indptr,
+                               int32_t* out_indices, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,8 @@ the GraphSAGE aggregation path, all running as hand-written sm_100a kernels in
 from ._lib import GraphFormatError, InvariantError
 from .cache import (CacheState, ProbVector, build_cache, degree_probs, inclusion_prob,
                     random_walk_probs, sample_cache)
+from .formats import (build_csr, load_binary, load_edgelist, load_feature_csv, save_binary,
+                      validate_graph)
 from .graph import Graph, NodeSet, generate_powerlaw_device
 from .model import GraphSAGE, TrainConfig, init_params_numpy, micro_f1
 from .pool import BatchItem, SamplerPool, epoch_targets

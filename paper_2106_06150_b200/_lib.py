@@ -117,6 +117,9 @@ _SIGS = {
     "gns_adam": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_double,
                            c_double, c_double, c_double, c_int64, c_double, c_void_p]),
     "gns_gen_workspace_size": (c_size_t, [c_int64, c_int64]),
+    "gns_build_csr_count": (c_int32, [c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                      c_size_t, c_void_p]),
+    "gns_build_csr_fill": (c_int32, [c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "gns_gen_powerlaw_count": (c_int32, [c_int64, c_int64, c_double, c_double, c_uint32,
                                          c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "gns_gen_powerlaw_fill": (c_int32, [c_int64, c_int64, c_void_p, c_void_p, c_void_p,
@@ -175,7 +178,7 @@ KERNELS_PER_CALL = {
     "gns_cached_csr_fill": 1, "gns_sample_layer": 8, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
     "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 7,
-    "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1,
+    "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1, "gns_build_csr_count": 6, "gns_build_csr_fill": 1,
 }
 launch_counter = [0]
 

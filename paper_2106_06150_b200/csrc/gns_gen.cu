@@ -48,10 +48,26 @@ __device__ __forceinline__ void gen_pair(int64_t e, const GenParams& P, int32_t&
   v = gen_rank_to_id(gen_rank(u2, P), P);
 }
 
-__global__ void gen_count_kernel(GenParams P, int32_t* __restrict__ deg) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < P.m; e += (int64_t)gridDim.x * blockDim.x) {
+// Pair sources: Philox power-law pairs, or caller-given (u, v) arrays
+// (build_csr, graph.py:142-169).
+struct GenSource {
+  GenParams P;
+  __device__ __forceinline__ void operator()(int64_t e, int32_t& u, int32_t& v) const { gen_pair(e, P, u, v); }
+};
+struct ArraySource {
+  const int32_t* u;
+  const int32_t* v;
+  __device__ __forceinline__ void operator()(int64_t e, int32_t& a, int32_t& b) const {
+    a = u[e];
+    b = v[e];
+  }
+};
+
+template <typename Src>
+__global__ void gen_count_kernel(Src src, int64_t m, int32_t* __restrict__ deg) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     int32_t u, v;
-    gen_pair(e, P, u, v);
+    src(e, u, v);
     if (u == v) continue;
     atomicAdd(deg + u, 1);
     atomicAdd(deg + v, 1);
@@ -74,11 +90,12 @@ __global__ void __launch_bounds__(BLOCK) gen_scan_kernel(ScanStatus ss, int32_t*
       });
 }
 
-__global__ void gen_scatter_kernel(GenParams P, const int64_t* __restrict__ ptr0, int32_t* __restrict__ cursor,
+template <typename Src>
+__global__ void gen_scatter_kernel(Src src, int64_t m, const int64_t* __restrict__ ptr0, int32_t* __restrict__ cursor,
                                    int32_t* __restrict__ raw) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < P.m; e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     int32_t u, v;
-    gen_pair(e, P, u, v);
+    src(e, u, v);
     if (u == v) continue;
     raw[ptr0[u] + atomicAdd(cursor + u, 1)] = v;
     raw[ptr0[v] + atomicAdd(cursor + v, 1)] = u;
@@ -237,9 +254,34 @@ size_t gns_gen_workspace_size(int64_t num_nodes, int64_t num_pairs) {
   return gen_ws(num_nodes, num_pairs, nullptr, 0, &w);
 }
 
+}  // extern "C"
+
+template <typename Src>
+static int csr_pipeline(Src src, int64_t n, int64_t m, int64_t* out_indptr, int64_t* out_nnz_dev, const GenWs& w,
+                        cudaStream_t stream) {
+  const int sms = num_sms();
+  GNS_CUDA(cudaMemsetAsync(w.cnt, 0, (n + 1) * sizeof(int32_t), stream));
+  GNS_CUDA(cudaMemsetAsync(w.nbig, 0, 64 * sizeof(int32_t), stream));
+  gen_count_kernel<<<sms * 16, 256, 0, stream>>>(src, m, w.cnt);
+  GNS_TRY(check_launch("csr_count"));
+  GNS_CUDA(cudaMemsetAsync(w.scan, 0, scan_status_bytes(w.tiles), stream));
+  gen_scan_kernel<256, 16><<<(unsigned)w.tiles, 256, 0, stream>>>(make_scan_status(w.scan, w.tiles), w.cnt, n, w.ptr0,
+                                                                  nullptr, 1);
+  gen_scatter_kernel<<<sms * 16, 256, 0, stream>>>(src, m, w.ptr0, w.cnt, w.raw);
+  GNS_TRY(check_launch("csr_scatter"));
+  gen_sort_small_kernel<<<sms * 16, 256, 0, stream>>>(w.ptr0, n, w.raw, w.cnt, w.big, w.nbig);
+  gen_sort_big_kernel<<<sms * 2, 1024, 0, stream>>>(w.ptr0, w.raw, w.cnt, w.big, w.nbig);
+  GNS_TRY(check_launch("csr_sort"));
+  GNS_CUDA(cudaMemsetAsync(w.scan, 0, scan_status_bytes(w.tiles), stream));
+  gen_scan_kernel<256, 16><<<(unsigned)w.tiles, 256, 0, stream>>>(make_scan_status(w.scan, w.tiles), w.cnt, n,
+                                                                  out_indptr, out_nnz_dev, 0);
+  return check_launch("csr_scan");
+}
+
+extern "C" {
+
 int gns_gen_powerlaw_count(int64_t n, int64_t m, double alpha, double offset, uint32_t seed, int64_t* out_indptr,
                            int64_t* out_nnz_dev, void* ws, size_t ws_bytes, void* stream_) {
-  cudaStream_t stream = (cudaStream_t)stream_;
   if (n < 2 || m < 0 || !(alpha > 0.0 && alpha < 1.0) || !(offset > 0.0)) {
     set_error("gen_powerlaw: need n >= 2, m >= 0, 0 < alpha < 1, offset > 0");
     return GNS_EINVAL;
@@ -250,24 +292,29 @@ int gns_gen_powerlaw_count(int64_t n, int64_t m, double alpha, double offset, ui
     set_error("gen_powerlaw: workspace %zu < %zu", ws_bytes, need);
     return GNS_EINVAL;
   }
-  GenParams P = make_params(n, m, alpha, offset, seed);
-  const int sms = num_sms();
-  GNS_CUDA(cudaMemsetAsync(w.cnt, 0, (n + 1) * sizeof(int32_t), stream));
-  GNS_CUDA(cudaMemsetAsync(w.nbig, 0, 64 * sizeof(int32_t), stream));
-  gen_count_kernel<<<sms * 16, 256, 0, stream>>>(P, w.cnt);
-  GNS_TRY(check_launch("gen_count"));
-  GNS_CUDA(cudaMemsetAsync(w.scan, 0, scan_status_bytes(w.tiles), stream));
-  gen_scan_kernel<256, 16><<<(unsigned)w.tiles, 256, 0, stream>>>(make_scan_status(w.scan, w.tiles), w.cnt, n, w.ptr0,
-                                                                  nullptr, 1);
-  gen_scatter_kernel<<<sms * 16, 256, 0, stream>>>(P, w.ptr0, w.cnt, w.raw);
-  GNS_TRY(check_launch("gen_scatter"));
-  gen_sort_small_kernel<<<sms * 16, 256, 0, stream>>>(w.ptr0, n, w.raw, w.cnt, w.big, w.nbig);
-  gen_sort_big_kernel<<<sms * 2, 1024, 0, stream>>>(w.ptr0, w.raw, w.cnt, w.big, w.nbig);
-  GNS_TRY(check_launch("gen_sort"));
-  GNS_CUDA(cudaMemsetAsync(w.scan, 0, scan_status_bytes(w.tiles), stream));
-  gen_scan_kernel<256, 16><<<(unsigned)w.tiles, 256, 0, stream>>>(make_scan_status(w.scan, w.tiles), w.cnt, n,
-                                                                  out_indptr, out_nnz_dev, 0);
-  return check_launch("gen_scan");
+  GenSource src{make_params(n, m, alpha, offset, seed)};
+  return csr_pipeline(src, n, m, out_indptr, out_nnz_dev, w, (cudaStream_t)stream_);
+}
+
+int gns_build_csr_count(int64_t n, const int32_t* u, const int32_t* v, int64_t m, int64_t* out_indptr,
+                        int64_t* out_nnz_dev, void* ws, size_t ws_bytes, void* stream_) {
+  if (n < 0 || m < 0) {
+    set_error("build_csr: negative sizes");
+    return GNS_EINVAL;
+  }
+  GenWs w;
+  size_t need = gen_ws(n, m, ws, ws_bytes, &w);
+  if (need > ws_bytes) {
+    set_error("build_csr: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  ArraySource src{u, v};
+  return csr_pipeline(src, n, m, out_indptr, out_nnz_dev, w, (cudaStream_t)stream_);
+}
+
+int gns_build_csr_fill(int64_t n, int64_t m, const int64_t* indptr, int32_t* out_indices, void* ws,
+                       size_t ws_bytes, void* stream_) {
+  return gns_gen_powerlaw_fill(n, m, indptr, out_indices, ws, ws_bytes, stream_);
 }
 
 int gns_gen_powerlaw_fill(int64_t n, int64_t m, const int64_t* indptr, int32_t* out_indices, void* ws,

@@ -158,7 +158,14 @@ def make_model_golden():
     np.savez_compressed(os.path.join(HERE, "golden_model.npz"), **out)
 
 
+def make_format_golden():
+    """A GNSG v1 file written by the reference's save_binary (graph.py:283-299)."""
+    g = gb.generate_sbm(60, 3, 0.3, 0.05, seed=0, feature_dim=5)
+    gb.save_binary(g, os.path.join(HERE, "golden_sbm60.gnsg"))
+
+
 if __name__ == "__main__":
+    make_format_golden()
     make_kat_golden()
     make_sampler_golden()
     make_model_golden()

@@ -573,3 +573,66 @@ def test_random_walk_probs(P, golden):
     cfg = P.SamplerConfig(strategy="GNS", cache_mode="auto")
     pv = cache_probs(g2, cfg)
     assert np.array_equal(pv.weights.cpu().numpy(), O.random_walk_probs(og, tid, (15, 10, 5), 3))
+
+
+# ---- graph formats ----------------------------------------------
+
+def test_build_csr_matches_reference_contract(P):
+    rng = np.random.default_rng(3)
+    edges = rng.integers(0, 500, size=(4000, 2))
+    edges = np.concatenate([edges, edges[:50], [[7, 7], [9, 9]]])      # duplicates + self loops
+    g = P.build_csr(edges, 500)
+    ref = O.build_csr(edges, 500)                                      # graph.py:142-169 restated
+    assert np.array_equal(g.indptr.cpu().numpy(), ref.indptr)
+    assert np.array_equal(g.indices.cpu().numpy(), ref.indices)
+    P.validate_graph(g)
+    g1 = P.build_csr([(0, 1)], 2)
+    assert g1.indptr.tolist() == [0, 1, 2] and g1.indices.tolist() == [1, 0]
+    with pytest.raises(ValueError, match=r"edge \(3, 5\) out of range"):
+        P.build_csr([(0, 1), (3, 5)], 4)
+
+
+def test_gnsg_round_trip(P, tmp_path, golden):
+    gold = golden["model"]
+    n = len(gold["indptr"]) - 1
+    g = P.Graph.from_numpy(n, gold["indptr"], gold["indices"], features=gold["features"], labels=gold["labels"],
+                           train_mask=gold["train_mask"], val_mask=~gold["train_mask"],
+                           test_mask=np.zeros(n, dtype=bool))
+    p = tmp_path / "g.gnsg"
+    P.save_binary(g, p)
+    g2 = P.load_binary(p)
+    assert torch.equal(g.indptr, g2.indptr) and torch.equal(g.indices, g2.indices)
+    assert torch.equal(g.features, g2.features) and torch.equal(g.labels, g2.labels)
+    assert torch.equal(g.train_mask, g2.train_mask) and torch.equal(g.val_mask, g2.val_mask)
+    # byte layout: int64 indptr/indices after the 28-byte header (graph.py:8-28)
+    raw = p.read_bytes()
+    assert raw[:4] == b"GNSG"
+    assert np.array_equal(np.frombuffer(raw, dtype="<i8", count=n + 1, offset=28), gold["indptr"])
+    P.validate_graph(g2)
+
+
+def test_edgelist(P, tmp_path):
+    p = tmp_path / "e.txt"
+    p.write_text("# comment\n0 1\n1 2\n\n2 0\n")
+    g = P.load_edgelist(p)
+    assert g.num_nodes == 3 and g.indices.tolist() == [1, 2, 0, 2, 0, 1]
+    p.write_text("0 x\n")
+    with pytest.raises(P.GraphFormatError, match="non-integer"):
+        P.load_edgelist(p)
+
+
+def test_load_reference_written_gnsg(P):
+    import os
+    from conftest import GOLDEN
+    path = os.path.join(GOLDEN, "golden_sbm60.gnsg")
+    g = P.load_binary(path)
+    raw = open(path, "rb").read()
+    n, e = 60, g.num_edges
+    off = 28
+    ip = np.frombuffer(raw, dtype="<i8", count=n + 1, offset=off); off += 8 * (n + 1)
+    ix = np.frombuffer(raw, dtype="<i8", count=e, offset=off); off += 8 * e
+    f = np.frombuffer(raw, dtype="<f4", count=n * 5, offset=off).reshape(n, 5); off += 20 * n
+    lab = np.frombuffer(raw, dtype="<i4", count=n, offset=off)
+    assert np.array_equal(g.indptr.cpu().numpy(), ip) and np.array_equal(g.indices.cpu().numpy(), ix)
+    assert np.array_equal(g.features[:, :5].cpu().numpy(), f) and np.array_equal(g.labels.cpu().numpy(), lab)
+    P.validate_graph(g)
