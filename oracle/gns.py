@@ -460,6 +460,16 @@ def cache_size_for(g, cache_frac: float) -> int:
     return int(round(cache_frac * g.num_nodes))
 
 
+def isolated_fraction(mb) -> float:
+    """sampling.py:413-425."""
+    block = mb.blocks[0]
+    if len(mb.targets) == 0:
+        return 0.0
+    indeg = np.bincount(block.edge_dst, minlength=len(block.dst_nodes))
+    tpos = np.searchsorted(block.dst_nodes, mb.targets)
+    return float(np.mean(indeg[tpos] == 0))
+
+
 def validate_minibatch(g, mb) -> None:
     """sampling.py:428-470 restated (structural invariants)."""
     g = as_ograph(g)

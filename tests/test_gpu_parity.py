@@ -636,3 +636,32 @@ def test_load_reference_written_gnsg(P):
     assert np.array_equal(g.indptr.cpu().numpy(), ip) and np.array_equal(g.indices.cpu().numpy(), ix)
     assert np.array_equal(g.features[:, :5].cpu().numpy(), f) and np.array_equal(g.labels.cpu().numpy(), lab)
     P.validate_graph(g)
+
+
+# ---- device metrics ------------------------------------------------
+
+def test_metrics_match_reference_definitions(P):
+    """count_input_nodes / copy_cost / isolated_fraction / CSV, vs the oracle's
+    restatement of metrics.py:75-97 and sampling.py:413-425 on the same blocks."""
+    from paper_2106_06150_b200 import metrics as M
+    og = _hub_graph(3000, 21)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    cache = P.build_cache(g, P.degree_probs(g), 60, rng_seed=[0, 33, 0])
+    oc = O.build_cache(og, O.degree_probs(og), 60, seed=0, epoch=0)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(6, 3), batch_size=100, cache_mode="degree")
+    targets = np.arange(0, 3000, 30)
+    mb = P.build_minibatch(g, cache, targets, cfg, P.BatchRng(0, 0, 0))
+    ref_mb = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(0, 0, 0))
+    total, cached = len(ref_mb.input_nodes), int(oc.mask[ref_mb.input_nodes].sum())
+    assert M.count_input_nodes(mb, cache) == (total, cached)
+    assert M.copy_cost(mb, cache, 64) == (total - cached) * 64 * 4
+    assert abs(P.isolated_fraction(mb) - O.isolated_fraction(ref_mb)) < 1e-12
+    s = M.batch_stats(mb, cache, 64, epoch=1, batch=2, sample_ms=1.4, train_ms=2.6)
+    rep = M.MetricsReport(run_id="00_gns", strategy="GNS", config=cfg, seed=0, stats=[s])
+    import tempfile, os
+    with tempfile.TemporaryDirectory() as d:
+        rep.write_csv(os.path.join(d, "a.csv"))
+        lines = open(os.path.join(d, "a.csv")).read().splitlines()
+    assert lines[0].split(",") == ["run_id", "epoch", "batch", "strategy", "num_input", "num_cached", "copy_bytes",
+                                   "isolated_frac", "sample_ms", "train_ms"]
+    assert lines[1].startswith("00_gns,1,2,GNS,%d,%d,%d," % (total, cached, (total - cached) * 256))

@@ -226,3 +226,10 @@ def test_oracle_random_walk_probs_equals_reference(gb):
     # SPEC.md:144-146 examples: path 0-1-2, train={0}, fanout 1, L=1 -> [2/3, 1/3, 0]
     path = O.build_csr([(0, 1), (1, 2)], 3)
     np.testing.assert_allclose(O.random_walk_probs(path, [0], (1,), 1), [2 / 3, 1 / 3, 0.0], rtol=1e-15)
+
+
+def test_oracle_isolated_fraction_equals_reference(gb):
+    g = gb.generate_powerlaw(500, 3, 2)
+    cfg = gb.SamplerConfig(strategy="NS", fanouts=(2, 1), batch_size=50, seed=0)
+    mb = gb.build_minibatch(g, None, np.arange(0, 500, 5), cfg, np.random.default_rng(1))
+    assert O.isolated_fraction(mb) == gb.isolated_fraction(mb)
