@@ -37,7 +37,8 @@ class GraphedTrainer:
     """CUDA-graph GNS trainer: ``step()`` = sample(next) || train(current)."""
 
     def __init__(self, g: Graph, config: SamplerConfig, dims, train_config: TrainConfig | None = None,
-                 rank: int = 0, world_size: int = 1, allreduce=None, seed: int = 0, host_targets: bool = False):
+                 rank: int = 0, world_size: int = 1, allreduce=None, seed: int = 0, host_targets: bool = False,
+                 feature_placement: str = "device", host_features: torch.Tensor | None = None):
         _lib.require_cuda()
         if g.features is None or g.labels is None:
             raise ValueError("training needs features and labels")
@@ -62,6 +63,23 @@ class GraphedTrainer:
         B = config.batch_size
         self.tgt_host = [torch.zeros(B, dtype=torch.int32).pin_memory() for _ in range(2)]
         self.ntgt_host = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2)]
+        # feature placement: "device" (whole table in HBM) or "mixed" (paper
+        # §3.1: table in pinned host memory, the cached rows in an HBM table
+        # refreshed with the cache; uncached rows are read over the host link)
+        if feature_placement not in ("device", "mixed"):
+            raise ValueError(f"unknown feature_placement {feature_placement!r}")
+        self.placement = feature_placement
+        self.host_features = None
+        self.cache_table = None
+        if feature_placement == "mixed":
+            if config.strategy != "GNS":
+                raise ValueError("mixed placement needs the GNS cache")
+            hf = host_features if host_features is not None else g.features.cpu().pin_memory()
+            if not hf.is_pinned():
+                hf = hf.pin_memory()
+            self.host_features = hf
+            cs = int(round(config.cache_frac * g.num_nodes))
+            self.cache_table = torch.empty((max(cs, 1), hf.shape[1]), dtype=torch.float32, device=g.device)
         self.cache = None
         self._probs = None
         self.graphs = None
@@ -103,13 +121,21 @@ class GraphedTrainer:
         """features[input_nodes] -> h0 (model.py:146)."""
         sl, L, s = self.slots[slot], self.L, _lib.stream_ptr()
         b0 = sl.layers[L - 1]
-        tab = self.g.features
         n_in_dev = b0.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
         ev = self._prof_events
         if ev is not None:
             _lib.call("gns_record_event_external", ev[0].cuda_event, s)
-        _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, b0.src_nodes.data_ptr(),
-                  n_in_dev.data_ptr(), self.cap_src[0], self.dims[0], self.h0.data_ptr(), self.h0.stride(0), 0, s)
+        if self.placement == "mixed":
+            hf, c = self.host_features, self.cache
+            _lib.call("gns_gather_rows_mixed", hf.data_ptr(), self.cache_table.data_ptr(),
+                      c.nodes.mask_bits.data_ptr(), c.mask_word_rank().data_ptr(), hf.stride(0),
+                      b0.src_nodes.data_ptr(), n_in_dev.data_ptr(), self.cap_src[0], self.dims[0],
+                      self.h0.data_ptr(), self.h0.stride(0), s)
+        else:
+            tab = self.g.features
+            _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, b0.src_nodes.data_ptr(),
+                      n_in_dev.data_ptr(), self.cap_src[0], self.dims[0], self.h0.data_ptr(), self.h0.stride(0), 0,
+                      s)
         if ev is not None:
             _lib.call("gns_record_event_external", ev[1].cuda_event, s)
 
@@ -180,6 +206,17 @@ class GraphedTrainer:
         cs = int(round(self.cfg.cache_frac * self.g.num_nodes))
         self.cache = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch,
                                            rng_seed=[self.cfg.seed, _CACHE, epoch])
+        if self.placement == "mixed":
+            # feature refresh (paper §3.1): cached rows pinned-host -> HBM on a
+            # side stream, read through UVA by gns_cache_refresh_rows
+            hf, ids = self.host_features, self.cache.nodes.ids
+            n_dev = torch.tensor([ids.numel()], dtype=torch.int64, device=self.dev)
+            with torch.cuda.stream(self.side):
+                self.side.wait_stream(torch.cuda.current_stream())
+                _lib.call("gns_cache_refresh_rows", hf.data_ptr(), hf.stride(0), ids.data_ptr(), n_dev.data_ptr(),
+                          ids.numel(), self.dims[0], self.cache_table.data_ptr(), _lib.stream_ptr(self.side))
+                self.cache.mask_word_rank()
+            self.side.synchronize()
 
     def _set_step(self, slot: int, epoch: int, index: int | None):
         b = self.cfg.batch_size

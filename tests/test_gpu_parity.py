@@ -665,3 +665,43 @@ def test_metrics_match_reference_definitions(P):
     assert lines[0].split(",") == ["run_id", "epoch", "batch", "strategy", "num_input", "num_cached", "copy_bytes",
                                    "isolated_frac", "sample_ms", "train_ms"]
     assert lines[1].startswith("00_gns,1,2,GNS,%d,%d,%d," % (total, cached, (total - cached) * 256))
+
+
+# ---- mixed CPU-GPU feature placement (paper §3.1) ------------------------------------
+
+def test_mixed_placement_gather_and_training(P):
+    from paper_2106_06150_b200 import _lib
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    og = _hub_graph(4000, 31)
+    rng = np.random.default_rng(1)
+    feats = rng.normal(size=(og.num_nodes, 16)).astype(np.float32)
+    labels = rng.integers(0, 4, og.num_nodes).astype(np.int32)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices, features=feats, labels=labels,
+                           train_mask=rng.random(og.num_nodes) < 0.5)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(8, 4), batch_size=200, cache_frac=0.05, cache_mode="degree",
+                          seed=5)
+    # gather: cached rows from the HBM cache table, the rest from pinned host
+    cache = P.build_cache(g, P.degree_probs(g), 200, rng_seed=[5, 33, 0])
+    host = torch.as_tensor(feats).pin_memory()
+    ids = cache.nodes.ids
+    table = torch.empty((ids.numel(), 16), device="cuda")
+    n_dev = torch.tensor([ids.numel()], dtype=torch.int64, device="cuda")
+    _lib.call("gns_cache_refresh_rows", host.data_ptr(), 16, ids.data_ptr(), n_dev.data_ptr(), ids.numel(), 16,
+              table.data_ptr(), _lib.stream_ptr())
+    assert torch.equal(table.cpu(), host[ids.long().cpu()])
+    rows = torch.as_tensor(np.sort(rng.choice(og.num_nodes, 900, replace=False)).astype(np.int32), device="cuda")
+    nr = torch.tensor([900], dtype=torch.int32, device="cuda")
+    out = torch.empty((900, 16), device="cuda")
+    _lib.call("gns_gather_rows_mixed", host.data_ptr(), table.data_ptr(), cache.nodes.mask_bits.data_ptr(),
+              cache.mask_word_rank().data_ptr(), 16, rows.data_ptr(), nr.data_ptr(), 900, 16, out.data_ptr(), 16,
+              _lib.stream_ptr())
+    assert torch.equal(out.cpu(), host[rows.long().cpu()])
+    # the whole engine: identical losses in both placements
+    tc = P.TrainConfig(lr=0.003)
+    res = {}
+    for placement in ("device", "mixed"):
+        tr = GraphedTrainer(g, cfg, (16, 32, 4), tc, seed=0, feature_placement=placement)
+        losses = []
+        tr.run_epoch(0, on_step=lambda e, i, k: losses.append(tr.loss_value()))
+        res[placement] = losses
+    assert res["device"] == res["mixed"]
