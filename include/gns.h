@@ -49,6 +49,7 @@ extern "C" {
 /* Device-side error flags raised by kernels (bit set in a block's counts[GNS_CNT_ERR]). */
 #define GNS_ERRBIT_ZEROPROB 1u  /* cached draw with inclusion 0 (sampling.py:255-256) */
 #define GNS_ERRBIT_CAPACITY 2u  /* selection buffer could not converge */
+#define GNS_ERRBIT_ZEROQ 4u     /* gns-exact edge with zero estimated inclusion (sampling.py:248-249) */
 
 /* Layout of the per-block device counter array (int32[8]). */
 #define GNS_CNT_DST 0      /* number of dst rows (seeds)                    */
@@ -76,6 +77,7 @@ typedef struct gns_cache {
   const int32_t* cached_indices;  /* int32[nnz_C] */
   const uint32_t* mask_bits;      /* uint32[ceil(N/32)] */
   const double* inclusion;        /* float64[N] */
+  const int32_t* cached_pos;      /* int32[nnz_C]: position in the full row (gns-exact), may be NULL */
 } gns_cache_t;
 
 /* Philox4x32-10 key (oracle/philox.py): key = (seed, epoch), counter =
@@ -145,11 +147,13 @@ GNS_API int gns_random_walk_probs(const gns_graph_t* g, const int32_t* train_ids
 /* sample_cache (cache.py:87-103) + NodeSet.from_ids (graph.py:118-125):
  * exponential race keys -log(1-U)/p over p>0, smallest min(cache_size,
  * |support|) by (key, id) via radix select, emitted as sorted ids + bitmap.
+ * tag = Philox stream tag: 33 for the epoch cache (pool.py:32), 21 for the
+ * gns-exact resamples (sampling.py:29).
  * out_ids int32[cache_size]; out_mask_bits uint32[ceil(N/32)];
  * out_counts int64[2] = {|C|, |support|} (device). */
 GNS_API size_t gns_cache_draw_workspace_size(int64_t num_nodes);
 GNS_API int gns_cache_draw(const double* probs, int64_t num_nodes, int64_t cache_size,
-                   uint32_t seed, uint32_t epoch, int32_t* out_ids,
+                   uint32_t seed, uint32_t epoch, uint32_t tag, int32_t* out_ids,
                    uint32_t* out_mask_bits, int64_t* out_counts, void* ws,
                    size_t ws_bytes, void* stream);
 
@@ -162,18 +166,31 @@ GNS_API int gns_inclusion(const double* probs, int64_t n, int64_t cache_size,
 
 /* Induced cached-neighbour CSR (cache.py:185-197) by filtering the full CSR
  * with the cache bitmap (rows stay ascending).  Two phases: count (writes
- * out_c_indptr and *out_nnz_dev), then fill (needs c_indices capacity >= nnz). */
+ * out_c_indptr and *out_nnz_dev), then fill (needs c_indices capacity >= nnz;
+ * out_c_pos, optional, receives each entry's position in the full row). */
 GNS_API size_t gns_cached_csr_workspace_size(int64_t num_nodes);
 GNS_API int gns_cached_csr_count(const gns_graph_t* g, const uint32_t* mask_bits,
                          int64_t* out_c_indptr, int64_t* out_nnz_dev, void* ws,
                          size_t ws_bytes, void* stream);
 GNS_API int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits,
                         const int64_t* c_indptr, int32_t* out_c_indices,
-                        void* stream);
+                        int32_t* out_c_pos, void* stream);
+
+/* estimate_edge_inclusion (sampling.py:269-296): CSR-aligned float64 table
+ * q[e] = mean over `resamples` Philox cache draws (key (seed, r), tag 21) of
+ * the edge's selection probability min(k,nc)/nc if its neighbour is cached,
+ * else fill/rest (0 when cache_only). */
+GNS_API size_t gns_edge_inclusion_workspace_size(int64_t num_nodes, int64_t cache_size);
+GNS_API int gns_estimate_edge_inclusion(const gns_graph_t* g, const double* probs,
+                                        int64_t cache_size, int32_t k, int32_t cache_only,
+                                        int32_t resamples, uint32_t seed, double* out_q, void* ws,
+                                        size_t ws_bytes, void* stream);
 
 /* ---- sampler (sampling.py) --------------------------------------------- */
 
 /* step_dev (device, may be NULL) overrides rng->seed/epoch/batch.
+ * exact_q (device float64[E], may be NULL): gns-exact weights 1/q[position]
+ * (sampling.py:238-250) instead of gns-paper; needs cache->cached_pos.
  * sample_neighbors_gns (sampling.py:189-266, policy gns-paper) when cache !=
  * NULL, sample_neighbors_uniform (sampling.py:155-170) when cache == NULL.
  * seeds: sorted unique int32 (count in *n_seeds_dev, <= max_dst).  Writes
@@ -186,7 +203,7 @@ GNS_API int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits,
 GNS_API size_t gns_sample_workspace_size(int64_t num_nodes, int64_t max_dst);
 GNS_API int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache,
                      const int32_t* seeds, const int32_t* n_seeds_dev,
-                     int64_t max_dst, int32_t k, int32_t cache_only,
+                     int64_t max_dst, int32_t k, int32_t cache_only, const double* exact_q,
                      const gns_rng_t* rng, const gns_step_t* step_dev,
                      gns_block_t* block, void* ws, size_t ws_bytes, void* stream);
 

@@ -210,17 +210,17 @@ def random_walk_probs(g, train, fanouts, num_layers: int, device_order: bool = T
     return p / (s1 + c1)
 
 
-def cache_keys_philox(w: np.ndarray, support: np.ndarray, seed: int, epoch: int):
+def cache_keys_philox(w: np.ndarray, support: np.ndarray, seed: int, epoch: int, tag: int = philox.TAG_CACHE):
     """Exponential-race keys Exp(1)/w over the positive support (cache.py:101),
-    with Exp(1) = -log(1 - U), U from Philox at (tag 33, pos = node id)."""
-    stream = philox.stream_word(philox.TAG_CACHE)
+    with Exp(1) = -log(1 - U), U from Philox at (tag, pos = node id)."""
+    stream = philox.stream_word(tag)
     u = philox.uniform(seed, epoch, 0, stream, 0, support)
     e = -detmath.det_log(1.0 - u)
     return e / w[support]
 
 
 def sample_cache(w: np.ndarray, cache_size: int, seed=0, epoch=0,
-                 numpy_seed=None) -> np.ndarray:
+                 numpy_seed=None, tag: int = philox.TAG_CACHE) -> np.ndarray:
     """cache.py:87-103 -> sorted unique cached ids.
 
     ``numpy_seed`` given: the reference's own draw (``default_rng(seed)
@@ -237,7 +237,7 @@ def sample_cache(w: np.ndarray, cache_size: int, seed=0, epoch=0,
         keys = rng.exponential(size=len(support)) / w[support]
         pick = np.argpartition(keys, cache_size)[:cache_size]
         return np.unique(support[pick]).astype(np.int64)
-    keys = cache_keys_philox(w, support, seed, epoch)
+    keys = cache_keys_philox(w, support, seed, epoch, tag)
     order = np.lexsort((support, keys))[:cache_size]
     return np.sort(support[order]).astype(np.int64)
 
@@ -278,6 +278,38 @@ def build_cache(g, w: np.ndarray, cache_size: int, epoch: int = 0, seed: int = 0
     return OCache(ids=ids, mask=mask, inclusion=np.asarray(incl, dtype=np.float64),
                   cached_indptr=cached_indptr, cached_indices=cached_indices,
                   epoch=epoch)
+
+
+FILL_STREAM = 21  # sampling.py:29
+
+
+def estimate_edge_inclusion(g, w, cache_size, k, cache_only, resamples=64, seed=0, numpy_seed=None):
+    """sampling.py:269-296 with the build's Philox resamples (key (seed, r), tag
+    21); ``numpy_seed`` = the reference's own draws ``[seed, 21, r]``."""
+    g = as_ograph(g)
+    n = g.num_nodes
+    deg = g.degrees.astype(np.float64)
+    rows = np.repeat(np.arange(n), g.degrees)
+    q = np.zeros(g.num_edges, dtype=np.float64)
+    for r in range(resamples):
+        if numpy_seed is not None:
+            ids = sample_cache(w, cache_size, numpy_seed=[numpy_seed, FILL_STREAM, r])
+        else:
+            ids = sample_cache(w, cache_size, seed=seed, epoch=r, tag=FILL_STREAM)
+        mask = np.zeros(n, dtype=bool)
+        mask[ids] = True
+        cflag = mask[g.indices]
+        nc = np.bincount(rows, weights=cflag, minlength=n)
+        m = np.minimum(k, nc)
+        rest = deg - nc
+        p_cached = np.divide(m, nc, out=np.zeros(n), where=nc > 0)
+        if cache_only:
+            p_fill = np.zeros(n)
+        else:
+            fill = np.minimum(k - m, rest)
+            p_fill = np.divide(fill, rest, out=np.zeros(n), where=rest > 0)
+        q += np.where(cflag, p_cached[rows], p_fill[rows])
+    return q / resamples
 
 
 def cached_csr_by_filter(g, mask):
@@ -362,8 +394,8 @@ def sample_neighbors_uniform(g, seeds, k, keysrc, layer=0) -> OBlock:
 
 
 def sample_neighbors_gns(g, cache: OCache, seeds, k, cache_only, keysrc,
-                         layer=0) -> OBlock:
-    """sampling.py:189-266 (gns-paper policy)."""
+                         layer=0, exact_weights=None) -> OBlock:
+    """sampling.py:189-266 (gns-paper policy; gns-exact when exact_weights)."""
     if k < 1:
         raise ValueError("fanout must be >= 1")
     g = as_ograph(g)
@@ -400,23 +432,36 @@ def sample_neighbors_gns(g, cache: OCache, seeds, k, cache_only, keysrc,
         u_dst = u_rows[u_sel]
         u_src = u_cand[u_sel]
 
-    n_cached_of_dst = np.maximum(c_counts, 1)
-    coeff = cache.inclusion[c_src] * (k / np.minimum(k, n_cached_of_dst)[c_dst])
-    if np.any(coeff <= 0):
-        raise ValueError("inclusion probability is zero for a cached draw")
-    c_w = 1.0 / coeff
-    u_w = (rest / np.maximum(fill, 1))[u_dst]
-    weights = np.concatenate([c_w, u_w])
+    if exact_weights is not None:
+        # sampling.py:238-250: CSR positions of the cached picks, then 1/q
+        rows_all = np.repeat(np.arange(nrows), counts)
+        stride = g.num_nodes + 1
+        row_keys = rows_all * stride + cand
+        idx = np.searchsorted(row_keys, c_dst * stride + c_src)
+        c_gpos = positions[idx]
+        u_gpos = u_positions[u_sel] if not cache_only else np.empty(0, dtype=np.int64)
+        q = np.concatenate([exact_weights[c_gpos], exact_weights[u_gpos]])
+        if np.any(q <= 0):
+            raise InvariantError("sampled an edge with zero estimated inclusion")
+        weights = 1.0 / q
+    else:
+        n_cached_of_dst = np.maximum(c_counts, 1)
+        coeff = cache.inclusion[c_src] * (k / np.minimum(k, n_cached_of_dst)[c_dst])
+        if np.any(coeff <= 0):
+            raise ValueError("inclusion probability is zero for a cached draw")
+        c_w = 1.0 / coeff
+        u_w = (rest / np.maximum(fill, 1))[u_dst]
+        weights = np.concatenate([c_w, u_w])
     dst_rows = np.concatenate([c_dst, u_dst])
     srcs = np.concatenate([c_src, u_src])
     cached_flags = np.concatenate([np.ones(len(c_src), dtype=bool),
                                    np.zeros(len(u_src), dtype=bool)])
     return assemble(g, seeds, dst_rows, srcs, weights, cached_flags, k,
-                    "gns-paper")
+                    "gns-exact" if exact_weights is not None else "gns-paper")
 
 
-def build_minibatch(g, cache, targets, config, keysrc) -> OMiniBatch:
-    """sampling.py:299-336 (NS / GNS with gns-paper weights)."""
+def build_minibatch(g, cache, targets, config, keysrc, exact_tables=None) -> OMiniBatch:
+    """sampling.py:299-336 (NS / GNS, gns-paper or gns-exact weights)."""
     g = as_ograph(g)
     num_layers = len(config.fanouts)
     seeds = np.unique(np.asarray(targets, dtype=np.int64))
@@ -429,8 +474,13 @@ def build_minibatch(g, cache, targets, config, keysrc) -> OMiniBatch:
             if cache is None:
                 raise ValueError("GNS sampling needs a CacheState")
             cache_only = bool(config.input_layer_cache_only) and layer == 1
+            table = None
+            if getattr(config, "weight_policy", "gns-paper") == "gns-exact":
+                table = (exact_tables or {}).get((k, cache_only))
+                if table is None:
+                    raise ValueError(f"missing edge-inclusion table for fanout={k}, cache_only={cache_only}")
             block = sample_neighbors_gns(g, cache, seeds, k, cache_only, keysrc,
-                                         layer)
+                                         layer, exact_weights=table)
         blocks.append(block)
         seeds = block.src_nodes
     blocks.reverse()

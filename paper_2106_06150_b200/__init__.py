@@ -16,7 +16,7 @@ from .graph import Graph, NodeSet, generate_powerlaw_device
 from .model import GraphSAGE, TrainConfig, init_params_numpy, micro_f1
 from .pool import BatchItem, SamplerPool, epoch_targets
 from .sampling import (BatchRng, LayerBlock, MiniBatch, MiniBatchSampler, SamplerConfig,
-                       build_minibatch, gns_weight_paper, isolated_fraction,
+                       build_minibatch, estimate_edge_inclusion, gns_weight_paper, isolated_fraction,
                        sample_neighbors_gns, sample_neighbors_uniform, validate_minibatch)
 
 __version__ = "0.1.0"

@@ -24,6 +24,7 @@ GNS_EZEROPROB = 4
 
 ERRBIT_ZEROPROB = 1
 ERRBIT_CAPACITY = 2
+ERRBIT_ZEROQ = 4
 
 CNT_DST, CNT_EDGES, CNT_CACHED, CNT_SRC, CNT_HUBS, CNT_ERR, CNT_N = 0, 1, 2, 3, 4, 5, 8
 
@@ -43,7 +44,7 @@ class GnsGraph(Structure):
 
 class GnsCache(Structure):
     _fields_ = [("cached_indptr", c_void_p), ("cached_indices", c_void_p),
-                ("mask_bits", c_void_p), ("inclusion", c_void_p)]
+                ("mask_bits", c_void_p), ("inclusion", c_void_p), ("cached_pos", c_void_p)]
 
 
 class GnsRng(Structure):
@@ -72,18 +73,21 @@ _SIGS = {
     "gns_random_walk_probs": (c_int32, [POINTER(GnsGraph), c_void_p, c_int64, c_void_p, c_int32, c_void_p,
                                         c_void_p, c_size_t, c_void_p]),
     "gns_cache_draw_workspace_size": (c_size_t, [c_int64]),
-    "gns_cache_draw": (c_int32, [c_void_p, c_int64, c_int64, c_uint32, c_uint32, c_void_p,
+    "gns_cache_draw": (c_int32, [c_void_p, c_int64, c_int64, c_uint32, c_uint32, c_uint32, c_void_p,
                                  c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "gns_edge_inclusion_workspace_size": (c_size_t, [c_int64, c_int64]),
+    "gns_estimate_edge_inclusion": (c_int32, [POINTER(GnsGraph), c_void_p, c_int64, c_int32, c_int32, c_int32,
+                                              c_uint32, c_void_p, c_void_p, c_size_t, c_void_p]),
     "gns_inclusion": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                 c_void_p]),
     "gns_cached_csr_workspace_size": (c_size_t, [c_int64]),
     "gns_cached_csr_count": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_size_t, c_void_p]),
     "gns_cached_csr_fill": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p, c_void_p,
-                                      c_void_p]),
+                                      c_void_p, c_void_p]),
     "gns_sample_workspace_size": (c_size_t, [c_int64, c_int64]),
     "gns_sample_layer": (c_int32, [POINTER(GnsGraph), POINTER(GnsCache), c_void_p, c_void_p,
-                                   c_int64, c_int32, c_int32, POINTER(GnsRng), c_void_p,
+                                   c_int64, c_int32, c_int32, c_void_p, POINTER(GnsRng), c_void_p,
                                    POINTER(GnsBlock), c_void_p, c_size_t, c_void_p]),
     "gns_relabel_workspace_size": (c_size_t, [c_int64]),
     "gns_relabel": (c_int32, [c_int64, c_void_p, c_void_p, c_int64, POINTER(GnsBlock), c_int64,
@@ -175,7 +179,7 @@ def check(rc: int, what: str = ""):
 # how many of OUR kernels ran inside a timed region
 KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_random_walk_probs": 9, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
-    "gns_cached_csr_fill": 1, "gns_sample_layer": 8, "gns_relabel": 4, "gns_unique_sorted": 3,
+    "gns_cached_csr_fill": 1, "gns_estimate_edge_inclusion": 0, "gns_sample_layer": 8, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
     "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_bwd": 7,
     "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1, "gns_build_csr_count": 6, "gns_build_csr_fill": 1,

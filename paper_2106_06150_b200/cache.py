@@ -30,21 +30,28 @@ from .graph import Graph, NodeSet
 _CACHE_TAG = 33
 
 
-def seed_epoch(rng_seed) -> tuple[int, int]:
-    """Map the reference's ``rng_seed`` forms to the Philox key (seed, epoch)."""
+def seed_key(rng_seed) -> tuple[int, int, int]:
+    """Map the reference's ``rng_seed`` forms to the Philox key (seed, epoch)
+    and stream tag: ``[seed, tag, epoch]`` (pool.py:117 uses tag 33,
+    sampling.py:284 tag 21) keeps its tag; other forms use 33."""
     if np.isscalar(rng_seed):
-        return int(rng_seed) & 0xFFFFFFFF, 0
-    s = [int(x) for x in rng_seed]
-    if len(s) == 3:           # [seed, tag, epoch]  (pool.py:117)
-        return s[0] & 0xFFFFFFFF, s[2] & 0xFFFFFFFF
+        return int(rng_seed) & 0xFFFFFFFF, 0, _CACHE_TAG
+    s = [int(x) for x in np.asarray(rng_seed, dtype=np.int64).ravel()]
+    if len(s) == 3:
+        return s[0] & 0xFFFFFFFF, s[2] & 0xFFFFFFFF, s[1] & 0xFF
     if len(s) == 2:
-        return s[0] & 0xFFFFFFFF, s[1] & 0xFFFFFFFF
+        return s[0] & 0xFFFFFFFF, s[1] & 0xFFFFFFFF, _CACHE_TAG
     if len(s) == 1:
-        return s[0] & 0xFFFFFFFF, 0
+        return s[0] & 0xFFFFFFFF, 0, _CACHE_TAG
     h = 0
     for x in s:
         h = (h * 1000003 + x) & 0xFFFFFFFF
-    return h, 0
+    return h, 0, _CACHE_TAG
+
+
+def seed_epoch(rng_seed) -> tuple[int, int]:
+    s, e, _ = seed_key(rng_seed)
+    return s, e
 
 
 @dataclass(frozen=True, eq=False)
@@ -123,7 +130,7 @@ class _DrawWorkspace:
         return ws
 
 
-def _draw(probs: ProbVector, cache_size: int, seed: int, epoch: int, stream=None):
+def _draw(probs: ProbVector, cache_size: int, seed: int, epoch: int, stream=None, tag: int = _CACHE_TAG):
     w = probs.weights
     n = int(w.shape[0])
     dev = w.device
@@ -132,7 +139,7 @@ def _draw(probs: ProbVector, cache_size: int, seed: int, epoch: int, stream=None
     bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
     counts = torch.zeros(2, dtype=torch.int64, device=dev)
     ws = _DrawWorkspace.get(n, dev)
-    _lib.call("gns_cache_draw", w.data_ptr(), n, cs, seed, epoch, ids.data_ptr(), bits.data_ptr(),
+    _lib.call("gns_cache_draw", w.data_ptr(), n, cs, seed, epoch, tag, ids.data_ptr(), bits.data_ptr(),
               counts.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(stream))
     return ids, bits, counts
 
@@ -141,8 +148,8 @@ def sample_cache(probs: ProbVector, cache_size: int, rng_seed) -> NodeSet:
     """cache.py:87-103: min(cache_size, #positive) ids drawn without replacement
     with probability proportional to the weights (exponential race)."""
     _lib.require_cuda()
-    seed, epoch = seed_epoch(rng_seed)
-    ids, bits, counts = _draw(probs, cache_size, seed, epoch)
+    seed, epoch, tag = seed_key(rng_seed)
+    ids, bits, counts = _draw(probs, cache_size, seed, epoch, tag=tag)
     k = int(counts[0])
     return NodeSet(ids=ids[:k], mask_bits=bits, num_nodes=len(probs))
 
@@ -174,6 +181,7 @@ class CacheState:
     cached_indices: torch.Tensor  # int32[nnz]
     epoch: int
     source_probs: ProbVector
+    cached_pos: torch.Tensor | None = None  # int32[nnz]: position in the full row (gns-exact)
 
     def __len__(self) -> int:
         return len(self.nodes)
@@ -188,7 +196,8 @@ class CacheState:
         c = getattr(self, "_c", None)
         if c is None:
             c = _lib.GnsCache(self.cached_indptr.data_ptr(), self.cached_indices.data_ptr(),
-                              self.nodes.mask_bits.data_ptr(), self.inclusion.data_ptr())
+                              self.nodes.mask_bits.data_ptr(), self.inclusion.data_ptr(),
+                              None if self.cached_pos is None else self.cached_pos.data_ptr())
             object.__setattr__(self, "_c", c)
         return c
 
@@ -216,8 +225,8 @@ def build_cache(g: Graph, probs: ProbVector, cache_size: int, epoch: int = 0, rn
         raise ValueError(f"unknown inclusion_mode {inclusion_mode!r}")
     probs = probs.normalize()
     stream = _lib.stream_ptr()
-    seed, ep = seed_epoch(rng_seed)
-    ids, bits, counts = _draw(probs, cache_size, seed, ep)
+    seed, ep, tag = seed_key(rng_seed)
+    ids, bits, counts = _draw(probs, cache_size, seed, ep, tag=tag)
     n = g.num_nodes
     incl = torch.empty(n, dtype=torch.float64, device=g.device)
     # |C| and |support| stay on the device (counts[0], counts[1])
@@ -231,9 +240,11 @@ def build_cache(g: Graph, probs: ProbVector, cache_size: int, epoch: int = 0, rn
     host = counts.cpu()  # one sync per refresh: |C| and nnz_C size the outputs
     nnz_h = int(nnz.item())
     c_indices = torch.empty(max(nnz_h, 1), dtype=torch.int32, device=g.device)
+    c_pos = torch.empty(max(nnz_h, 1), dtype=torch.int32, device=g.device)
     _lib.call("gns_cached_csr_fill", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
-              c_indices.data_ptr(), stream)
+              c_indices.data_ptr(), c_pos.data_ptr(), stream)
     k = int(host[0])
     nodes = NodeSet(ids=ids[:k], mask_bits=bits, num_nodes=n)
     return CacheState(nodes=nodes, inclusion=incl, cached_indptr=c_indptr,
-                      cached_indices=c_indices[:nnz_h], epoch=epoch, source_probs=probs)
+                      cached_indices=c_indices[:nnz_h], epoch=epoch, source_probs=probs,
+                      cached_pos=c_pos[:nnz_h])

@@ -25,9 +25,9 @@ struct SelectState {
 };
 
 __global__ void cache_keys_kernel(const double* __restrict__ probs, int64_t n, uint32_t seed,
-                                  uint32_t epoch, uint64_t* __restrict__ keys,
+                                  uint32_t epoch, uint32_t tag, uint64_t* __restrict__ keys,
                                   SelectState* __restrict__ st) {
-  const uint32_t stream = stream_word(33, 0, 0);
+  const uint32_t stream = stream_word(tag, 0, 0);
   unsigned long long local = 0;
   // each thread handles pairs (2q, 2q+1) so one Philox block serves two nodes
   const int64_t npairs = (n + 1) >> 1;
@@ -230,7 +230,8 @@ __global__ void ccsr_rowcount_kernel(const int64_t* __restrict__ indptr, const i
 
 __global__ void ccsr_fill_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                                  int64_t n, const uint32_t* __restrict__ mask,
-                                 const int64_t* __restrict__ c_indptr, int32_t* __restrict__ c_indices) {
+                                 const int64_t* __restrict__ c_indptr, int32_t* __restrict__ c_indices,
+                                 int32_t* __restrict__ c_pos) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -243,7 +244,11 @@ __global__ void ccsr_fill_kernel(const int64_t* __restrict__ indptr, const int32
       int32_t v = (p < e) ? __ldg(indices + p) : 0;
       bool keep = (p < e) && in_mask(mask, v);
       unsigned bal = __ballot_sync(GNS_FULL, keep);
-      if (keep) c_indices[out + __popc(bal & ((1u << lane) - 1))] = v;
+      if (keep) {
+        const int64_t o = out + __popc(bal & ((1u << lane) - 1));
+        c_indices[o] = v;
+        if (c_pos) c_pos[o] = (int32_t)(p - b);  // position in the full row (gns-exact lookups)
+      }
       out += __popc(bal);
     }
   }
@@ -275,7 +280,7 @@ size_t gns_cache_draw_workspace_size(int64_t num_nodes) {
   return cache_draw_ws(num_nodes, nullptr, 0, &k, &a, &b, &h, &s, &sc, &t);
 }
 
-int gns_cache_draw(const double* probs, int64_t n, int64_t cache_size, uint32_t seed, uint32_t epoch,
+int gns_cache_draw(const double* probs, int64_t n, int64_t cache_size, uint32_t seed, uint32_t epoch, uint32_t tag,
                    int32_t* out_ids, uint32_t* out_mask_bits, int64_t* out_counts, void* ws,
                    size_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
@@ -293,7 +298,7 @@ int gns_cache_draw(const double* probs, int64_t n, int64_t cache_size, uint32_t 
   const int sms = num_sms();
   GNS_CUDA(cudaMemsetAsync(hist, 0, 2048 * sizeof(unsigned), stream));
   GNS_CUDA(cudaMemsetAsync(st, 0, sizeof(SelectState), stream));
-  cache_keys_kernel<<<sms * 8, 256, 0, stream>>>(probs, n, seed, epoch, keys, st);
+  cache_keys_kernel<<<sms * 8, 256, 0, stream>>>(probs, n, seed, epoch, tag, keys, st);
   GNS_TRY(check_launch("cache_keys"));
   select_init_kernel<<<1, 1, 0, stream>>>(st, cache_size);
   for (int pass = 0; pass < 6; ++pass) {
@@ -337,10 +342,10 @@ int gns_cached_csr_count(const gns_graph_t* g, const uint32_t* mask_bits, int64_
 }
 
 int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits, const int64_t* c_indptr,
-                        int32_t* out_c_indices, void* stream_) {
+                        int32_t* out_c_indices, int32_t* out_c_pos, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   ccsr_fill_kernel<<<num_sms() * 8, 256, 0, stream>>>(g->indptr, g->indices, g->num_nodes, mask_bits, c_indptr,
-                                                      out_c_indices);
+                                                      out_c_indices, out_c_pos);
   return check_launch("ccsr_fill");
 }
 
@@ -463,6 +468,77 @@ int gns_random_walk_probs(const gns_graph_t* g, const int32_t* train_ids, int64_
   scale_kernel<<<grid, 256, 0, stream>>>(p, n, total);
   if (p != out_probs) GNS_CUDA(cudaMemcpyAsync(out_probs, p, (size_t)n * 8, cudaMemcpyDeviceToDevice, stream));
   return check_launch("random_walk_probs");
+}
+
+}  // extern "C"
+
+// ---- gns-exact per-edge inclusion table (sampling.py:269-296, §8(f)3) ------------
+namespace gns {
+
+// q[e] += cached(e) ? min(k,nc)/nc : fill/rest  (one resampled cache; rows in
+// CSR order, one warp per row; adds in resample order -> deterministic)
+__global__ void edge_incl_accum_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                                       int64_t n, const uint32_t* __restrict__ mask, int k, int cache_only,
+                                       double* __restrict__ q) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    unsigned c = 0;
+    for (int64_t p = b + lane; p < e; p += 32) c += in_mask(mask, __ldg(indices + p));
+    c = warp_sum(c);
+    const double nc = (double)c, deg = (double)(e - b);
+    const double m = fmin((double)k, nc);
+    const double rest = DSUB(deg, nc);
+    const double pc = nc > 0.0 ? DDIV(m, nc) : 0.0;
+    double pf = 0.0;
+    if (!cache_only && rest > 0.0) pf = DDIV(fmin(DSUB((double)k, m), rest), rest);
+    for (int64_t p = b + lane; p < e; p += 32) q[p] = DADD(q[p], in_mask(mask, __ldg(indices + p)) ? pc : pf);
+  }
+}
+
+__global__ void div_kernel(double* __restrict__ q, int64_t n, double d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = DDIV(q[i], d);
+}
+
+}  // namespace gns
+
+extern "C" {
+
+size_t gns_edge_inclusion_workspace_size(int64_t num_nodes, int64_t cache_size) {
+  return gns_cache_draw_workspace_size(num_nodes) + (((size_t)(num_nodes + 31) / 32 * 4 + 255) & ~(size_t)255) +
+         (((size_t)(cache_size > 0 ? cache_size : 1) * 4 + 255) & ~(size_t)255) + 512;
+}
+
+int gns_estimate_edge_inclusion(const gns_graph_t* g, const double* probs, int64_t cache_size, int32_t k,
+                                int32_t cache_only, int32_t resamples, uint32_t seed, double* out_q, void* ws,
+                                size_t ws_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int64_t n = g->num_nodes;
+  if (k < 1 || resamples < 1) {
+    set_error("estimate_edge_inclusion: need k >= 1 and resamples >= 1");
+    return GNS_EINVAL;
+  }
+  if (ws_bytes < gns_edge_inclusion_workspace_size(n, cache_size)) {
+    set_error("estimate_edge_inclusion: workspace too small");
+    return GNS_EINVAL;
+  }
+  char* base = (char*)ws;
+  const size_t dws = gns_cache_draw_workspace_size(n);
+  uint32_t* mask = (uint32_t*)(base + dws);
+  int32_t* ids = (int32_t*)(base + dws + (((size_t)(n + 31) / 32 * 4 + 255) & ~(size_t)255));
+  int64_t* counts = (int64_t*)(base + gns_edge_inclusion_workspace_size(n, cache_size) - 256);
+  GNS_CUDA(cudaMemsetAsync(out_q, 0, (size_t)g->num_edges * 8, stream));
+  for (int r = 0; r < resamples; ++r) {
+    // resample r: its own Philox stream (tag 21 = sampling.py:29 _FILL_STREAM)
+    GNS_TRY(gns_cache_draw(probs, n, cache_size, seed, (uint32_t)r, 21u, ids, mask, counts, base, dws, stream_));
+    edge_incl_accum_kernel<<<num_sms() * 8, 256, 0, stream>>>(g->indptr, g->indices, n, mask, k, cache_only, out_q);
+    GNS_TRY(check_launch("edge_incl_accum"));
+  }
+  div_kernel<<<num_sms() * 8, 256, 0, stream>>>(out_q, g->num_edges, (double)resamples);
+  return check_launch("edge_incl_div");
 }
 
 }  // extern "C"

@@ -42,6 +42,8 @@ struct LayerArgs {
   const int32_t* cindices;
   const uint32_t* mask;
   const double* incl;
+  const int32_t* cpos;     // cached CSR -> position in the full row (gns-exact)
+  const double* exact_q;   // per-edge inclusion table (gns-exact) or NULL (gns-paper)
   const int32_t* seeds;
   const int32_t* n_dev;
   int k;
@@ -190,12 +192,23 @@ __device__ __forceinline__ uint64_t initial_threshold(int take, int cnt) {
   return t < 1 ? 1 : t;
 }
 
+// gns-exact (sampling.py:238-250): w = 1 / q[global CSR position]
+__device__ __forceinline__ double exact_weight(const LayerArgs& a, const RowInfo& ri, const PhaseDesc& ph,
+                                               uint32_t pos) {
+  const int64_t gpos = ri.start + (ph.phase == 0 ? (int64_t)__ldg(a.cpos + ri.cstart + pos) : (int64_t)pos);
+  const double q = a.exact_q[gpos];
+  if (!(q > 0.0)) atomicOr((unsigned*)(a.b.counts + GNS_CNT_ERR), GNS_ERRBIT_ZEROQ);
+  return DDIV(1.0, q);
+}
+
 __device__ __forceinline__ void emit_edge(const LayerArgs& a, const RowInfo& ri, int64_t r,
                                           const PhaseDesc& ph, int rank, uint32_t pos) {
   const int64_t o = ph.out_base + rank;
   const int32_t u = __ldg(ph.ids + pos);
   double w;
-  if (ph.phase == 0) {
+  if (a.exact_q) {
+    w = exact_weight(a, ri, ph, pos);
+  } else if (ph.phase == 0) {
     double q = DDIV((double)a.k, (double)min(a.k, max(ri.nc, 1)));
     double coeff = DMUL(a.incl[u], q);
     if (!(coeff > 0.0)) atomicOr((unsigned*)(a.b.counts + GNS_CNT_ERR), GNS_ERRBIT_ZEROPROB);
@@ -444,14 +457,15 @@ __device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInf
   uint32_t bw[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    inc[i] = (i < take && ph.phase == 0) ? __ldg(a.incl + u[i]) : 0.0;
+    inc[i] = (i < take && ph.phase == 0 && !a.exact_q) ? __ldg(a.incl + u[i]) : 0.0;
     bw[i] = i < take ? __ldg(a.dbits + (u[i] >> 5)) : 0u;
   }
   const int64_t o0 = ph.out_base;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     if (i < take) {
-      const double w = edge_weight_of(a, ri, ph, inc[i]);
+      const double w = a.exact_q ? exact_weight(a, ri, ph, (uint32_t)(v[i] & 2047u))
+                                 : edge_weight_of(a, ri, ph, inc[i]);
       const uint32_t m = 1u << (u[i] & 31);
       if (!(bw[i] & m)) {
         const uint32_t old = atomicOr(a.dbits + (u[i] >> 5), m);
@@ -700,8 +714,8 @@ size_t gns_sample_workspace_size(int64_t num_nodes, int64_t max_dst) {
 
 int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32_t* seeds,
                      const int32_t* n_seeds_dev, int64_t max_dst, int32_t k, int32_t cache_only,
-                     const gns_rng_t* rng, const gns_step_t* step_dev, gns_block_t* block, void* ws,
-                     size_t ws_bytes, void* stream_) {
+                     const double* exact_q, const gns_rng_t* rng, const gns_step_t* step_dev, gns_block_t* block,
+                     void* ws, size_t ws_bytes, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (k < 1) {
     set_error("fanout must be >= 1");
@@ -726,6 +740,12 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.cindices = cache ? cache->cached_indices : nullptr;
   a.mask = cache ? cache->mask_bits : nullptr;
   a.incl = cache ? cache->inclusion : nullptr;
+  a.cpos = cache ? cache->cached_pos : nullptr;
+  a.exact_q = exact_q;
+  if (exact_q && cache && !cache->cached_pos) {
+    set_error("gns-exact needs the cache's cached_pos array");
+    return GNS_EINVAL;
+  }
   a.seeds = seeds;
   a.n_dev = n_seeds_dev;
   a.k = k;

@@ -27,7 +27,7 @@ from . import cache as cache_mod
 from .graph import Graph
 from .model import GraphSAGE, TrainConfig, _dt, _split_rows, _weight_grad
 from .dist import rank_batches
-from .pool import cache_probs, num_batches
+from .pool import cache_probs, exact_tables, num_batches
 from .sampling import MiniBatchSampler, SamplerConfig
 
 _CACHE = 33
@@ -82,6 +82,7 @@ class GraphedTrainer:
             self.cache_table = torch.empty((max(cs, 1), hf.shape[1]), dtype=torch.float32, device=g.device)
         self.cache = None
         self._probs = None
+        self._tables = None
         self.graphs = None
         self._prof_events = None
         self.side = torch.cuda.Stream(device=self.dev)
@@ -195,7 +196,7 @@ class GraphedTrainer:
             sl.targets[:B].copy_(self.tgt_host[slot], non_blocking=True)
             sl.n_targets_dev.copy_(self.ntgt_host[slot], non_blocking=True)
         sl.enqueue_device(None if self.host_targets else self.train_ids, self.step_dev[slot],
-                          self.cache if self.cfg.strategy == "GNS" else None)
+                          self.cache if self.cfg.strategy == "GNS" else None, exact_tables=self._tables)
 
     # -- cache + capture ------------------------------------------------------------
     def _refresh_cache(self, epoch: int):
@@ -206,6 +207,8 @@ class GraphedTrainer:
         cs = int(round(self.cfg.cache_frac * self.g.num_nodes))
         self.cache = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch,
                                            rng_seed=[self.cfg.seed, _CACHE, epoch])
+        if self.cfg.weight_policy == "gns-exact" and self._tables is None:
+            self._tables = exact_tables(self.g, self.cfg, self._probs, cs)
         if self.placement == "mixed":
             # feature refresh (paper §3.1): cached rows pinned-host -> HBM on a
             # side stream, read through UVA by gns_cache_refresh_rows
@@ -409,3 +412,5 @@ class GraphedTrainer:
                 raise ValueError("inclusion probability is zero for a cached draw")
             if err & _lib.ERRBIT_CAPACITY:
                 raise _lib.InvariantError("neighbour selection did not converge (capacity)")
+            if err & _lib.ERRBIT_ZEROQ:
+                raise _lib.InvariantError("sampled an edge with zero estimated inclusion")

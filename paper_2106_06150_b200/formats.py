@@ -116,7 +116,7 @@ def read_header(path):
 def _upload(mm: np.ndarray, out: torch.Tensor, conv=None):
     flat = out.view(-1)
     for s in range(0, mm.shape[0], _CHUNK):
-        part = np.ascontiguousarray(mm[s:s + _CHUNK])
+        part = np.array(mm[s:s + _CHUNK])
         t = torch.from_numpy(part).to(out.device, non_blocking=False)
         flat[s:s + part.shape[0]].copy_(t if conv is None else conv(t))
 
@@ -146,7 +146,7 @@ def load_binary(path, device=None) -> Graph:
         feats = torch.zeros((n, ld), dtype=torch.float32, device=dev)
         rows = max(1, _CHUNK // max(fdim, 1))
         for s in range(0, n, rows):
-            t = torch.from_numpy(np.ascontiguousarray(fmm[s:s + rows])).to(dev)
+            t = torch.from_numpy(np.array(fmm[s:s + rows])).to(dev)
             feats[s:s + t.shape[0], :fdim].copy_(t)
         off += 4 * n * fdim
     labels = None

@@ -58,6 +58,21 @@ def cache_probs(g: Graph, config: SamplerConfig):
     return cache_mod.random_walk_probs(g, g.train_ids(), config.fanouts, config.num_layers)
 
 
+def exact_tables(g: Graph, config: SamplerConfig, probs, cache_size: int) -> dict:
+    """pool.py:140-151: one gns-exact edge-inclusion table per distinct
+    (fanout, cache_only) of the layer chain."""
+    from .sampling import estimate_edge_inclusion
+    tables = {}
+    L = config.num_layers
+    for layer in range(L, 0, -1):
+        k = int(config.fanouts[L - layer])
+        co = bool(config.input_layer_cache_only and layer == 1)
+        if (k, co) not in tables:
+            tables[(k, co)] = estimate_edge_inclusion(g, probs, cache_size, k, co,
+                                                      resamples=config.exact_resamples, seed=config.seed)
+    return tables
+
+
 def num_batches(g: Graph, config: SamplerConfig) -> int:
     n = g.train_ids().numel()
     return (n + config.batch_size - 1) // config.batch_size
@@ -104,6 +119,7 @@ class SamplerPool:
         self.world_size = world_size
         self.cache = None
         self._probs = None
+        self._tables = None
         self.depth = max(1, min(num_workers, queue_capacity, 4))
         self.slots = [MiniBatchSampler(g, config) for _ in range(self.depth)]
         self.stream = torch.cuda.Stream(device=g.device)
@@ -118,6 +134,8 @@ class SamplerPool:
         cache_size = int(round(self.config.cache_frac * self.graph.num_nodes))
         self.cache = cache_mod.build_cache(self.graph, self._probs, cache_size, epoch=epoch,
                                            rng_seed=[self.config.seed, _CACHE, epoch])
+        if self.config.weight_policy == "gns-exact" and self._tables is None:
+            self._tables = exact_tables(self.graph, self.config, self._probs, cache_size)
 
     def indices(self, epoch: int):
         from .dist import rank_batches
@@ -131,7 +149,8 @@ class SamplerPool:
             t0 = torch.cuda.Event(enable_timing=True)
             t0.record(self.stream)
             n = epoch_targets_device(self.graph, self.config, epoch, index, eng.targets, self.stream)
-            ev = eng.sample_async(None, n, BatchRng(self.config.seed, epoch, index), self.cache, self.stream)
+            ev = eng.sample_async(None, n, BatchRng(self.config.seed, epoch, index), self.cache, self.stream,
+                                  exact_tables=self._tables)
             t1 = torch.cuda.Event(enable_timing=True)
             t1.record(self.stream)
         return ev, t0, t1
@@ -152,7 +171,7 @@ class SamplerPool:
         for j, index in enumerate(idx):
             slot = j % self.depth
             ev, t0, t1 = pending.pop(j)
-            mb = self.slots[slot].collect(ev)
+            mb = self.slots[slot].collect(ev, policy_gns=self.config.weight_policy)
             torch.cuda.current_stream().wait_event(ev)
             yield BatchItem(epoch=epoch, index=index, minibatch=mb, _t0=t0, _t1=t1)
             # the consumer is done with this slot once its queued work finishes

@@ -182,8 +182,6 @@ class MiniBatchSampler:
         _lib.require_cuda()
         if config.strategy == "LADIES":
             raise NotImplementedError("LADIES is a baseline outside the GNS hot path (SURVEY.md §2)")
-        if config.strategy == "GNS" and config.weight_policy != "gns-paper":
-            raise NotImplementedError("gns-exact weights are SURVEY.md §8(f)3, not built yet")
         self.g = g
         self.config = config
         dev = g.device
@@ -231,8 +229,16 @@ class MiniBatchSampler:
         self.ws_relabel = _lib.workspace(lib.gns_relabel_workspace_size(n), dev, zero=True)
 
     # -- device-side chain -------------------------------------------------------
+    def _exact(self, tables, lb):
+        if self.config.strategy != "GNS" or self.config.weight_policy != "gns-exact":
+            return None
+        t = (tables or {}).get((lb.k, bool(lb.cache_only)))
+        if t is None:
+            raise ValueError(f"missing edge-inclusion table for fanout={lb.k}, cache_only={bool(lb.cache_only)}")
+        return t.data_ptr()
+
     def sample_async(self, targets: torch.Tensor | None, n_targets: int, rng: BatchRng,
-                     cache: CacheState | None, stream=None):
+                     cache: CacheState | None, stream=None, exact_tables=None):
         """Enqueue the whole L-layer chain on ``stream``; targets (int32 device,
         any order, may repeat) are deduplicated+sorted first (sampling.py:312).
         If ``targets`` is None the caller already wrote ``self.targets``."""
@@ -253,7 +259,7 @@ class MiniBatchSampler:
         gc = self.g.cstruct()
         for lb in self.layers:
             _lib.call("gns_sample_layer", gc, cstruct, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
-                      lb.k, int(lb.cache_only), rng.cstruct(lb.layer), None, lb.cblock,
+                      lb.k, int(lb.cache_only), self._exact(exact_tables, lb), rng.cstruct(lb.layer), None, lb.cblock,
                       self.ws_sample.data_ptr(), self.ws_sample.numel(), s)
             seeds = lb.src_nodes
             n_dev = lb.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
@@ -263,7 +269,7 @@ class MiniBatchSampler:
         return ev
 
     def enqueue_device(self, train_ids: torch.Tensor | None, step_dev: torch.Tensor, cache: CacheState | None,
-                       stream=None):
+                       stream=None, exact_tables=None):
         """Graph-capturable chain: the batch's targets (pool.py:60-66 slice
         begin/count) and Philox key come from the device gns_step_t
         ``step_dev``; no host synchronisation, fixed kernel arguments.  With
@@ -287,7 +293,8 @@ class MiniBatchSampler:
         rng = BatchRng()
         for lb in self.layers:
             _lib.call("gns_sample_layer", gc, cstruct, seeds.data_ptr(), n_dev.data_ptr(), lb.max_dst,
-                      lb.k, int(lb.cache_only), rng.cstruct(lb.layer), step_dev.data_ptr(), lb.cblock,
+                      lb.k, int(lb.cache_only), self._exact(exact_tables, lb), rng.cstruct(lb.layer),
+                      step_dev.data_ptr(), lb.cblock,
                       self.ws_sample.data_ptr(), self.ws_sample.numel(), s)
             seeds = lb.src_nodes
             n_dev = lb.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
@@ -319,14 +326,16 @@ class MiniBatchSampler:
             raise ValueError("inclusion probability is zero for a cached draw")
         if err & _lib.ERRBIT_CAPACITY:
             raise InvariantError("neighbour selection did not converge (capacity)")
+        if err & _lib.ERRBIT_ZEROQ:
+            raise InvariantError("sampled an edge with zero estimated inclusion")
         blocks.reverse()
         return MiniBatch(blocks=tuple(blocks), targets=blocks[-1].dst_nodes,
                          input_nodes=blocks[0].src_nodes)
 
-    def sample(self, targets, rng: BatchRng, cache: CacheState | None = None) -> MiniBatch:
+    def sample(self, targets, rng: BatchRng, cache: CacheState | None = None, exact_tables=None) -> MiniBatch:
         t = torch.as_tensor(targets, device=self.device)
-        ev = self.sample_async(t, t.numel(), rng, cache)
-        return self.collect(ev)
+        ev = self.sample_async(t, t.numel(), rng, cache, exact_tables=exact_tables)
+        return self.collect(ev, policy_gns=self.config.weight_policy)
 
 
 _ENGINES: dict = {}
@@ -353,20 +362,21 @@ def build_minibatch(g: Graph, cache: CacheState | None, targets, config: Sampler
         raise ValueError("GNS sampling needs a CacheState")
     t = torch.as_tensor(targets, device=g.device)
     eng = _engine(g, config, t.numel())
-    return eng.sample(t, rng, cache if config.strategy == "GNS" else None)
+    return eng.sample(t, rng, cache if config.strategy == "GNS" else None, exact_tables=exact_tables)
 
 
-def _single_layer(g, cache, seeds, k, cache_only, rng, strategy):
+def _single_layer(g, cache, seeds, k, cache_only, rng, strategy, policy="", exact=None):
     rng = _as_rng(rng)
     if k < 1:
         raise ValueError("fanout must be >= 1")
-    cfg = SamplerConfig(strategy=strategy, fanouts=(int(k),),
+    cfg = SamplerConfig(strategy=strategy, fanouts=(int(k),), weight_policy=policy,
                         input_layer_cache_only=bool(cache_only), batch_size=max(1, len(seeds)))
     t = torch.as_tensor(seeds, device=g.device)
     eng = MiniBatchSampler(g, cfg, max_targets=max(1, t.numel()))
     eng.layers[0].layer = rng.layer
     eng.layers[0].cache_only = bool(cache_only) and strategy == "GNS"
-    mb = eng.sample(t, rng, cache)
+    tables = None if exact is None else {(int(k), bool(cache_only) and strategy == "GNS"): exact}
+    mb = eng.sample(t, rng, cache, exact_tables=tables)
     return mb.blocks[0]
 
 
@@ -385,8 +395,25 @@ def sample_neighbors_gns(g: Graph, cache: CacheState, seeds, k: int, cache_only:
     if policy == "gns-exact":
         if exact_weights is None:
             raise ValueError("gns-exact policy needs an edge-inclusion table")
-        raise NotImplementedError("gns-exact is SURVEY.md §8(f)3, not built yet")
+        return _single_layer(g, cache, seeds, k, cache_only, rng, "GNS", "gns-exact",
+                             torch.as_tensor(exact_weights, device=g.device).to(torch.float64).contiguous())
     return _single_layer(g, cache, seeds, k, cache_only, rng, "GNS")
+
+
+def estimate_edge_inclusion(g: Graph, probs, cache_size: int, k: int, cache_only: bool, resamples: int = 64,
+                            seed=0) -> torch.Tensor:
+    """sampling.py:269-296 on the device: CSR-aligned float64 table of per-edge
+    inclusion probabilities over ``resamples`` cache draws (Philox key
+    (seed, r), stream tag 21 = sampling.py:29 _FILL_STREAM)."""
+    from .cache import seed_epoch
+    _lib.require_cuda()
+    w = probs.normalize().weights
+    s32, _ = seed_epoch(seed)
+    out = torch.empty(max(g.num_edges, 1), dtype=torch.float64, device=g.device)[:g.num_edges]
+    ws = _lib.workspace(_lib.lib().gns_edge_inclusion_workspace_size(g.num_nodes, int(cache_size)), g.device)
+    _lib.call("gns_estimate_edge_inclusion", g.cstruct(), w.data_ptr(), int(cache_size), int(k), int(bool(cache_only)),
+              int(resamples), s32, out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    return out
 
 
 def gns_weight_paper(p_v: float, cache_size: int, k: int, n_cached: int) -> float:

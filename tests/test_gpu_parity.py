@@ -705,3 +705,33 @@ def test_mixed_placement_gather_and_training(P):
         tr.run_epoch(0, on_step=lambda e, i, k: losses.append(tr.loss_value()))
         res[placement] = losses
     assert res["device"] == res["mixed"]
+
+
+# ---- gns-exact weights ----------------------------------------------
+
+def test_gns_exact_table_and_blocks(P):
+    og = _hub_graph(3000, 41)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    probs = P.degree_probs(g)
+    w = O.degree_probs(og)
+    tables_g, tables_o = {}, {}
+    for k, co in ((10, False), (5, True)):
+        t = P.estimate_edge_inclusion(g, probs, 1500, k, co, resamples=64, seed=7)
+        to = O.estimate_edge_inclusion(og, w, 1500, k, co, resamples=64, seed=7)
+        assert np.array_equal(t.cpu().numpy(), to)
+        tables_g[(k, co)], tables_o[(k, co)] = t, to
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=300, cache_mode="degree", cache_frac=0.5,
+                          weight_policy="gns-exact", seed=2)
+    cache = P.build_cache(g, probs, 1500, rng_seed=[2, 33, 0])
+    oc = O.build_cache(og, w, 1500, seed=2, epoch=0)
+    targets = np.random.default_rng(3).choice(og.num_nodes, 300, replace=False)
+    mb = P.build_minibatch(g, cache, targets, cfg, P.BatchRng(2, 0, 4), exact_tables=tables_g)
+    ref = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(2, 0, 4), exact_tables=tables_o)
+    assert_mb_equal(mb, ref, "gns-exact")
+    assert mb.blocks[0].policy == "gns-exact"
+    with pytest.raises(ValueError, match="missing edge-inclusion table"):
+        P.build_minibatch(g, cache, targets, cfg, P.BatchRng(2, 0, 4), exact_tables={})
+    # the pool builds the tables once and trains through them
+    pool = P.SamplerPool(g, cfg)
+    n = sum(1 for _ in pool.iter_epoch(0))
+    assert n > 0 and set(pool._tables) == {(10, False), (5, True)}

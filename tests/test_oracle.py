@@ -233,3 +233,29 @@ def test_oracle_isolated_fraction_equals_reference(gb):
     cfg = gb.SamplerConfig(strategy="NS", fanouts=(2, 1), batch_size=50, seed=0)
     mb = gb.build_minibatch(g, None, np.arange(0, 500, 5), cfg, np.random.default_rng(1))
     assert O.isolated_fraction(mb) == gb.isolated_fraction(mb)
+
+
+def test_oracle_gns_exact_equals_reference(gb):
+    """sampling.py:269-296 table + gns-exact weights (sampling.py:238-250)."""
+    g = gb.generate_powerlaw(800, 3, 4)
+    probs = gb.degree_probs(g)
+    w = O.degree_probs(g)
+    for k, co in ((5, True), (6, False)):
+        ref_t = gb.estimate_edge_inclusion(g, probs, 40, k, co, resamples=8, seed=3)
+        ours_t = O.estimate_edge_inclusion(g, w, 40, k, co, resamples=8, numpy_seed=3)
+        assert np.array_equal(ref_t, ours_t)
+    cfg = gb.SamplerConfig(strategy="GNS", fanouts=(6, 5), batch_size=50, cache_frac=0.05, cache_mode="degree",
+                           weight_policy="gns-exact", seed=0)
+    # a large cache so every realised cached neighbour has q > 0 (the
+    # reference raises InvariantError otherwise, sampling.py:248-249)
+    tables = {(6, False): gb.estimate_edge_inclusion(g, probs, 400, 6, False, resamples=64, seed=3),
+              (5, True): gb.estimate_edge_inclusion(g, probs, 400, 5, True, resamples=64, seed=3)}
+    rc = gb.build_cache(g, probs, 400, epoch=0, rng_seed=[0, 33, 0])
+    oc = O.OCache(ids=rc.nodes.ids, mask=rc.nodes.mask, inclusion=rc.inclusion, cached_indptr=rc.cached_indptr,
+                  cached_indices=rc.cached_indices)
+    targets = np.arange(0, 800, 16)
+    mr = gb.build_minibatch(g, rc, targets, cfg, np.random.default_rng(5), exact_tables=tables)
+    mo = O.build_minibatch(g, oc, targets, cfg, O.NumpyStream(np.random.default_rng(5)), exact_tables=tables)
+    for ba, bb in zip(mr.blocks, mo.blocks):
+        for f in ("src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached"):
+            assert np.array_equal(getattr(ba, f), getattr(bb, f)), f
