@@ -1,0 +1,68 @@
+"""Time the two branches of the captured step separately and together.
+
+    python scripts/branch_probe.py [--config papers100m] [--steps 100]
+
+Captures three graph variants on the same engine state: sample-only,
+train-only (gather + layers + backward) and the production step (both,
+overlapped), and reports the per-replay device time of each.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="papers100m")
+    ap.add_argument("--steps", type=int, default=100)
+    args = ap.parse_args()
+    import bench
+    import paper_2106_06150_b200 as P
+    from paper_2106_06150_b200.engine import GraphedTrainer
+
+    c = bench.CONFIGS[args.config]
+    g, _ = bench.make_graph(P, c)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=bench.FANOUTS, batch_size=bench.BATCH, cache_frac=c["cache"],
+                          cache_mode="degree", seed=0)
+    dims = (c["dim"], c["hidden"], c["hidden"], c["classes"])
+    tr = GraphedTrainer(g, cfg, dims, P.TrainConfig(), seed=0)
+    tr.run(5)
+    torch.cuda.synchronize()
+
+    def capture(fn):
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph, stream=tr.main):
+            fn()
+        return gph
+
+    tr._set_step(1, 0, 7)
+    variants = {
+        "sample_only": capture(lambda: tr._sample_body(1)),
+        "train_only": capture(lambda: tr._train_body(0, with_adam=False)),
+        "gather_only": capture(lambda: tr._gather(0)),
+        "step (production graph)": tr.graphs[0],
+    }
+    for name, gph in variants.items():
+        for _ in range(3):
+            gph.replay()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(tr.main)
+        with torch.cuda.stream(tr.main):
+            for _ in range(args.steps):
+                gph.replay()
+        e.record(tr.main)
+        e.synchronize()
+        print(f"{name:26s} {s.elapsed_time(e) / args.steps * 1e3:8.1f} us/replay")
+
+
+if __name__ == "__main__":
+    main()
