@@ -180,8 +180,10 @@ def main():
 
     from paper_2106_06150_b200 import dist as gdist
     torch.cuda.set_device(local)
-    if world > 1 and args.impl == "ours":
+    force_dist = os.environ.get("GNS_FORCE_DIST", "0") == "1"   # captured NCCL path at N=1 (testing)
+    if (world > 1 or force_dist) and args.impl == "ours":
         gdist.init_from_env("nccl")
+    distributed = dist.is_initialized()
     g, gen_s = make_graph(P, c, seed=0)
     cfg = P.SamplerConfig(strategy="GNS", fanouts=FANOUTS, batch_size=BATCH, cache_frac=c["cache"],
                           cache_mode="degree", input_layer_cache_only=True, seed=0)
@@ -213,11 +215,12 @@ def main():
     tc = P.TrainConfig(lr=0.003, hidden_dim=c["hidden"])
 
     from paper_2106_06150_b200.engine import GraphedTrainer
-    tr = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world,
-                        allreduce=gdist.make_allreduce() if world > 1 else None, seed=0)
+    allreduce = gdist.make_allreduce(force=force_dist) if distributed else None
+    tr = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world, allreduce=allreduce, seed=0)
     pos = tr.run(args.warmup, epoch=0, first=0)
+    tr.prepare(args.steps)
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -230,9 +233,9 @@ def main():
     t_end.synchronize()
     clk = clocks.stop()
     launches = _lib.launch_counter[0] - l0
-    # graph replays launch the captured kernels: count them per replay
-    per_replay = tr.kernels_per_step()
-    launches_total = launches + per_replay * args.steps
+    # graph replays launch the captured kernels: count them per step
+    per_step = tr.kernels_per_step()
+    launches_total = int(round(launches + per_step * args.steps))
     ms = gdist.max_over_ranks(t_start.elapsed_time(t_end), device="cuda")
     value = args.steps * world / (ms / 1e3)
     tr.check_errors()
@@ -243,14 +246,16 @@ def main():
     peak, peak_kind = load_peaks()
     gather_ms, n_in = [], []
     tr.capture_profiled()
-    nprof = min(30, args.steps)
+    nprof = min(30, args.steps) * tr.S
 
     spmm_ms, spmm_bytes = [], []
 
     def on_step(e, i, k):
+        if k % tr.S:          # the events time the first step of each replay
+            return
         gather_ms.append(tr.gather_ms())
         spmm_ms.append(tr.spmm0_ms())
-        cnt = tr.slots[k % 2].counts[len(FANOUTS) - 1].tolist()
+        cnt = tr.slots[tr.slot_of(k)].counts[len(FANOUTS) - 1].tolist()
         n_in.append(cnt[_lib.CNT_SRC])
         nd, ne = cnt[_lib.CNT_DST], cnt[_lib.CNT_EDGES]
         # input-layer SpMM: h rows read (edges + self) + cat rows written (incl.
@@ -267,7 +272,7 @@ def main():
                 "algorithmic_bytes_per_launch": float(gbytes.mean()),
                 "avg_launch_ms": float(np.mean(gather_ms)),
                 "share_of_step": float(np.mean(gather_ms) / (ms / args.steps)),
-                "measured": f"CUDA events around the gather inside the captured step graph, {nprof} replays"}
+                "measured": f"CUDA events around the gather inside the captured step graph, {len(gather_ms)} replays"}
     spmm_gbs = float(np.sum(spmm_bytes) / (np.sum(spmm_ms) / 1e3) / 1e9)
     kernels = {
         "gns_gather_rows": {"achieved_gbs": round(gather_gbs, 1), "frac": round(gather_gbs / peak, 4),
@@ -290,31 +295,37 @@ def main():
     # host memory every step (memcpy node in the graph), loss read back to the
     # host every step (D2H + sync)
     e2e = None
-    if rank == 0 and world == 1:
-        k2 = args.e2e_steps if args.e2e_steps is not None else max(5, args.steps // 2)
-        if k2 > 0:
-            ids_host = g.train_ids().cpu().numpy().astype(np.int64)
-            perm = np.random.default_rng(1).permutation(ids_host)
-            nb = len(perm) // BATCH
-            batches = [perm[(j % nb) * BATCH:((j % nb) + 1) * BATCH] for j in range(k2 + 2)]
-            te = GraphedTrainer(g, cfg, dims, tc, seed=0, host_targets=True)
-            te.cache = tr.cache
-            te.run_host(batches[:2], epoch=0)
-            torch.cuda.synchronize()
-            w0 = time.perf_counter()
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
-            s0.record(te.main)
-            te.run_host(batches[2:], epoch=0)
-            s1.record(te.main)
-            s1.synchronize()
-            wall = time.perf_counter() - w0
-            e2e = {"value": k2 / wall, "unit": UNIT, "h2d_bytes_per_step": BATCH * 4 + 4 + 32,
-                   "d2h_bytes_per_step": 8, "steps": k2,
-                   "path": "GraphedTrainer(host_targets=True).run_host: pinned host targets -> graph memcpy node, "
-                           "loss -> host each step; wall clock",
-                   "device_ms_per_step": s0.elapsed_time(s1) / k2}
-            del te
+    k2 = args.e2e_steps if args.e2e_steps is not None else max(5, args.steps // 2)
+    if k2 > 0:
+        ids_host = g.train_ids().cpu().numpy().astype(np.int64)
+        perm = np.random.default_rng(1).permutation(ids_host)
+        nb = len(perm) // BATCH
+        te = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world, allreduce=allreduce, seed=0,
+                            host_targets=True)
+        nw = 4 * te.S          # warm-up captures both graph parities
+        k2 = -(-k2 // te.S) * te.S   # whole replays in the timed region
+        # rank r's host batches: r, r+W, ... of the permutation (pool.py:80)
+        batches = [perm[((j * world + rank) % nb) * BATCH:((j * world + rank) % nb + 1) * BATCH]
+                   for j in range(k2 + nw)]
+        te.cache = tr.cache
+        te.run_host(batches[:nw], epoch=0)
+        torch.cuda.synchronize()
+        if distributed:
+            dist.barrier()
+        w0 = time.perf_counter()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(te.main)
+        te.run_host(batches[nw:], epoch=0)
+        s1.record(te.main)
+        s1.synchronize()
+        wall = gdist.max_over_ranks(time.perf_counter() - w0, device="cuda")
+        e2e = {"value": k2 * world / wall, "unit": UNIT, "h2d_bytes_per_step": BATCH * 4 + 4 + 32,
+               "d2h_bytes_per_step": 8, "steps": k2,
+               "path": "GraphedTrainer(host_targets=True).run_host: pinned host targets -> graph memcpy node, "
+                       "every step's loss -> host after each replay; wall clock, max over ranks",
+               "device_ms_per_step": s0.elapsed_time(s1) / k2}
+        del te
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -331,9 +342,10 @@ def main():
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
                 "gpu_launches_per_step": launches_total / args.steps, "clocks": clk,
                 "per_step": {"input_nodes": float(n_in.mean()), "gather_ms": float(np.mean(gather_ms)),
-                             "graph_replays": args.steps}}
+                             "graph_replays": -(-args.steps // tr.S), "steps_per_graph": tr.S,
+                             "step_priority": tr.prio_mode}}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
 

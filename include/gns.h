@@ -129,6 +129,18 @@ GNS_API int gns_version(void);
  * be timed / waited on) at every replay.  Used for in-graph kernel timing. */
 GNS_API int gns_record_event_external(void* event, void* stream);
 
+/* CUDA-graph plumbing for the whole-step engine (engine.py).  `graph` is a
+ * captured cudaGraph_t (torch.cuda.CUDAGraph(keep_graph=True).raw_cuda_graph()).
+ * gns_graph_instantiate instantiates it, optionally honouring the per-kernel
+ * priorities captured from the streams (cudaGraphInstantiateFlagUseNodePriority)
+ * so the sampling branch of a step is scheduled ahead of the training branch;
+ * gns_graph_launch replays it on `stream`.  gns_graph_kernel_priorities fills
+ * out_hist[|priority|] with the number of kernel nodes at each priority. */
+GNS_API int gns_graph_instantiate(void* graph, int32_t use_node_priority, void** out_exec);
+GNS_API int gns_graph_launch(void* exec, void* stream);
+GNS_API int gns_graph_exec_destroy(void* exec);
+GNS_API int gns_graph_kernel_priorities(void* graph, int32_t* out_hist, int32_t nbins);
+
 /* ---- cache engine (cache.py) ------------------------------------------- */
 
 /* degree_probs (cache.py:53-58): out[i] = deg(i) / E in float64. */
@@ -293,6 +305,18 @@ GNS_API int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32
                  int64_t max_edges, int64_t pad_rows, const void* z_mask, void* db,
                  void* dh, int64_t ld_dh, void* ws, size_t ws_bytes, void* stream);
 
+/* The two halves of gns_spmm_bwd: gns_block_transpose builds the block's
+ * transpose (per src row, its edges sorted by dst — scipy's csc order) in the
+ * workspace; it depends only on the sampled block, so the engine runs it on
+ * the sampling branch.  gns_spmm_bwd_transposed then runs the backward from a
+ * workspace the transpose was built in (same sizes). */
+GNS_API int gns_block_transpose(const gns_block_t* block, int64_t max_dst, int64_t max_src,
+                                int64_t max_edges, int32_t dim, void* ws, size_t ws_bytes, void* stream);
+GNS_API int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim,
+                                    const gns_block_t* block, int64_t max_dst, int64_t max_src,
+                                    int64_t max_edges, int64_t pad_rows, const void* z_mask, void* db,
+                                    void* dh, int64_t ld_dh, void* ws, size_t ws_bytes, void* stream);
+
 /* relu backward fused with the bias gradient (model.py:218,220):
  * dz = (z > 0) ? dh : 0 (skipped when z == NULL: the output layer), db[c] =
  * sum over rows of dz[:, c] in a fixed order (deterministic).  n = *n_dev if
@@ -316,6 +340,12 @@ GNS_API int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, cons
 GNS_API int gns_adam(int32_t dtype, void* params, const void* grads, void* m, void* v,
              int64_t n, double lr, double beta1, double beta2, double eps,
              int64_t step, double grad_scale, void* stream);
+
+/* gns_adam with the step count on the device: uses t = *step_dev + 1 and
+ * then increments *step_dev (graph-replay safe). */
+GNS_API int gns_adam_dev(int32_t dtype, void* params, const void* grads, void* m, void* v,
+                         int64_t n, double lr, double beta1, double beta2, double eps,
+                         int64_t* step_dev, double grad_scale, void* stream);
 
 /* ---- synthetic graphs (graph.py:172-205 analogue, device generator) ---- */
 

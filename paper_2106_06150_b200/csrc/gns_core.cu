@@ -3,6 +3,7 @@
 // (pool.py:60-66), bitmap rank.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "gns_common.cuh"
 
@@ -123,6 +124,47 @@ int gns_version(void) { return 1; }
 
 int gns_record_event_external(void* event, void* stream) {
   GNS_CUDA(cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream, cudaEventRecordExternal));
+  return GNS_OK;
+}
+
+int gns_graph_instantiate(void* graph, int32_t use_node_priority, void** out_exec) {
+  cudaGraphExec_t ex = nullptr;
+  unsigned long long flags = use_node_priority ? cudaGraphInstantiateFlagUseNodePriority : 0;
+  GNS_CUDA(cudaGraphInstantiateWithFlags(&ex, (cudaGraph_t)graph, flags));
+  *out_exec = (void*)ex;
+  return GNS_OK;
+}
+
+int gns_graph_launch(void* exec, void* stream) {
+  GNS_CUDA(cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream));
+  return GNS_OK;
+}
+
+int gns_graph_exec_destroy(void* exec) {
+  if (exec) GNS_CUDA(cudaGraphExecDestroy((cudaGraphExec_t)exec));
+  return GNS_OK;
+}
+
+int gns_graph_kernel_priorities(void* graph, int32_t* out_hist, int32_t nbins) {
+  size_t n = 0;
+  GNS_CUDA(cudaGraphGetNodes((cudaGraph_t)graph, nullptr, &n));
+  cudaGraphNode_t* nodes = (cudaGraphNode_t*)malloc(sizeof(cudaGraphNode_t) * (n ? n : 1));
+  cudaError_t e = cudaGraphGetNodes((cudaGraph_t)graph, nodes, &n);
+  for (int i = 0; i < nbins; ++i) out_hist[i] = 0;
+  for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
+    cudaGraphNodeType t;
+    if ((e = cudaGraphNodeGetType(nodes[i], &t)) != cudaSuccess) break;
+    if (t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeAttrValue v;
+    if ((e = cudaGraphKernelNodeGetAttribute(nodes[i], cudaKernelNodeAttributePriority, &v)) != cudaSuccess) break;
+    int b = v.priority < 0 ? -v.priority : v.priority;  // bin = |priority|
+    out_hist[b < nbins ? b : nbins - 1] += 1;
+  }
+  free(nodes);
+  if (e != cudaSuccess) {
+    set_error("graph_kernel_priorities: %s", cudaGetErrorString(e));
+    return GNS_ECUDA;
+  }
   return GNS_OK;
 }
 

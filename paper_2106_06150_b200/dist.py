@@ -23,12 +23,15 @@ def rank_batches(num_batches: int, rank: int, world_size: int) -> list[int]:
     return list(range(rank, num_batches, world_size))
 
 
-def make_allreduce(group=None):
-    """Sum-all-reduce of the flat gradient; returns the 1/W scale for Adam."""
+def make_allreduce(group=None, force: bool = False):
+    """Sum-all-reduce of the flat gradient; returns the 1/W scale for Adam.
+    Stream-ordered and CUDA-graph capturable with NCCL (the engine captures it
+    between backward and Adam).  ``force`` issues the collective even at
+    W == 1 (exercises the captured-NCCL path on one GPU)."""
 
     def allreduce(grad: torch.Tensor) -> float:
         w = dist.get_world_size(group)
-        if w > 1:
+        if w > 1 or force:
             dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
         return 1.0 / w
 
@@ -40,8 +43,15 @@ def init_from_env(backend: str = "nccl"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and not dist.is_initialized():
+    force = os.environ.get("GNS_FORCE_DIST", "0") == "1"
+    if (world > 1 or force) and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
+        # collectives are captured into the step's CUDA graph (torch CUDA
+        # graphs + DDP notes: no async error-handling watchdog on them)
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "0")
         kw = {}
         if backend == "nccl":
             torch.cuda.set_device(local)

@@ -20,6 +20,9 @@ re-captured after each refresh.
 
 from __future__ import annotations
 
+import ctypes
+import os
+
 import torch
 
 from . import _lib
@@ -34,11 +37,17 @@ _CACHE = 33
 
 
 class GraphedTrainer:
-    """CUDA-graph GNS trainer: ``step()`` = sample(next) || train(current)."""
+    """CUDA-graph GNS trainer.  One replay = S training steps on the main
+    branch (gather -> forward -> backward -> [all-reduce] -> Adam, each on
+    the batch held in its sampler slot) while S side branches sample the next
+    S batches into the other S slots; the sampler is a chain of short,
+    latency-bound kernels, so S independent chains overlap each other and the
+    training kernels.  2S slots alternate roles between the two graphs."""
 
     def __init__(self, g: Graph, config: SamplerConfig, dims, train_config: TrainConfig | None = None,
                  rank: int = 0, world_size: int = 1, allreduce=None, seed: int = 0, host_targets: bool = False,
-                 feature_placement: str = "device", host_features: torch.Tensor | None = None):
+                 feature_placement: str = "device", host_features: torch.Tensor | None = None,
+                 steps_per_graph: int | None = None):
         _lib.require_cuda()
         if g.features is None or g.labels is None:
             raise ValueError("training needs features and labels")
@@ -50,19 +59,28 @@ class GraphedTrainer:
         self.model = GraphSAGE(dims, dtype=torch.float32, device=self.dev, seed=seed)
         self.dims = self.model.dims
         self.L = config.num_layers
-        self.slots = [MiniBatchSampler(g, config), MiniBatchSampler(g, config)]
+        S = steps_per_graph if steps_per_graph is not None else int(os.environ.get("GNS_STEPS_PER_GRAPH", "2"))
+        if S < 1:
+            raise ValueError("steps_per_graph must be >= 1")
+        self.S = S
+        self.slots = [MiniBatchSampler(g, config) for _ in range(2 * S)]
         for sl in self.slots:
             sl.n_targets_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.train_ids = g.train_ids()
-        self.step_host = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(2)]
-        self.step_dev = [torch.zeros(4, dtype=torch.int64, device=self.dev) for _ in range(2)]
-        self.done = [None, None]
+        self.step_host = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(2 * S)]
+        self.step_dev = [torch.zeros(4, dtype=torch.int64, device=self.dev) for _ in range(2 * S)]
+        self.done = [None] * (2 * S)
         # host-provided targets (the end-to-end API): pinned buffers copied by
         # memcpy nodes inside the graph
         self.host_targets = host_targets
         B = config.batch_size
-        self.tgt_host = [torch.zeros(B, dtype=torch.int32).pin_memory() for _ in range(2)]
-        self.ntgt_host = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2)]
+        self.tgt_host = [torch.zeros(B, dtype=torch.int32).pin_memory() for _ in range(2 * S)]
+        self.ntgt_host = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2 * S)]
+        # Adam's step count lives on the device (gns_adam_dev), per-step losses
+        # are kept for the host to read after a replay
+        self.adam_t = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.step_loss = torch.zeros(S, dtype=torch.float64, device=self.dev)
+        self._cur_j = 0
         # feature placement: "device" (whole table in HBM) or "mixed" (paper
         # §3.1: table in pinned host memory, the cached rows in an HBM table
         # refreshed with the cache; uncached rows are read over the host link)
@@ -83,10 +101,20 @@ class GraphedTrainer:
         self.cache = None
         self._probs = None
         self._tables = None
-        self.graphs = None
         self._prof_events = None
-        self.side = torch.cuda.Stream(device=self.dev)
-        self.main = torch.cuda.Stream(device=self.dev)
+        # stream priorities (captured into the kernel nodes and honoured by
+        # gns_graph_instantiate): which branch of a step the block scheduler
+        # serves first when both have CTAs waiting
+        self.prio_mode = os.environ.get("GNS_STEP_PRIORITY", "side")
+        if self.prio_mode not in ("none", "side", "main"):
+            raise ValueError(f"GNS_STEP_PRIORITY must be none|side|main, not {self.prio_mode!r}")
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.sides = [torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "side" else lo)
+                      for _ in range(S)]
+        self.side = self.sides[0]
+        self.main = torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "main" else lo)
+        self._execs = {}
+        self._per_replay = 0
         self._alloc()
 
     # -- static buffers -----------------------------------------------------------
@@ -107,9 +135,12 @@ class GraphedTrainer:
         lib = _lib.lib()
         self.ws_dense = _lib.workspace(max(lib.gns_dense_bwd_workspace_size(max(p, 1), d)
                                            for p, d in zip(self.npad, dims[1:])), dev)
-        self.ws_bwd = _lib.workspace(max(lib.gns_spmm_bwd_workspace_size(self.cap_src[li], self.cap_edges[li],
-                                                                         dims[li])
-                                         for li in range(1, L)) if L > 1 else 256, dev)
+        # per slot and model layer li >= 1: the block transpose for the
+        # backward SpMM, built on the sampling branch (gns_block_transpose);
+        # zeroed so an unsampled slot reads as empty
+        self.tws = [[None] + [_lib.workspace(lib.gns_spmm_bwd_workspace_size(self.cap_src[li], self.cap_edges[li],
+                                                                            dims[li]), dev, zero=True)
+                              for li in range(1, L)] for _ in self.slots]
         self.ws_xent = _lib.workspace(8 * max(self.cap_dst[L - 1], 1024), dev)
         self.loss = self.model.loss_dev
 
@@ -172,21 +203,24 @@ class GraphedTrainer:
                     break
                 torch.mm(self.dz[li][:self.cap_dst[li]], m.weights[li].t(), out=self.dcat[li])
                 # transpose SpMM fused with the previous layer's relu' and bias grad
-                _lib.call("gns_spmm_bwd", 0, self.dcat[li].data_ptr(), self.dcat[li].stride(0), self.dims[li],
-                          blocks[li].cblock, self.cap_dst[li], self.cap_src[li], self.cap_edges[li],
+                ws = self.tws[slot][li]
+                _lib.call("gns_spmm_bwd_transposed", 0, self.dcat[li].data_ptr(), self.dcat[li].stride(0),
+                          self.dims[li], blocks[li].cblock, self.cap_dst[li], self.cap_src[li], self.cap_edges[li],
                           self.npad[li - 1], self.z[li - 1].data_ptr(), m.gbiases[li - 1].data_ptr(),
-                          self.dz[li - 1].data_ptr(), self.dz[li - 1].stride(0),
-                          self.ws_bwd.data_ptr(), self.ws_bwd.numel(), s)
+                          self.dz[li - 1].data_ptr(), self.dz[li - 1].stride(0), ws.data_ptr(), ws.numel(), s)
         if with_adam:
-            self._adam()
+            self._adam_dev()
 
-    def _adam(self):
+    def _adam_dev(self):
+        """[all-reduce of the flat gradient] + Adam with the device step count
+        (captured: t advances on the device at every replay)."""
         m = self.model
-        m.step_count += 1
-        # bias correction uses the host step count; inside a graph the step is
-        # replayed, so Adam's t is passed through a device scalar instead
-        _lib.call("gns_adam", 0, m.flat.data_ptr(), m.grad.data_ptr(), m.m.data_ptr(), m.v.data_ptr(), m.numel,
-                  self.tc.lr, self.tc.beta1, self.tc.beta2, self.tc.eps, m.step_count, 1.0, _lib.stream_ptr())
+        scale = 1.0
+        if self.allreduce is not None:
+            scale = self.allreduce(m.grad)
+        _lib.call("gns_adam_dev", 0, m.flat.data_ptr(), m.grad.data_ptr(), m.m.data_ptr(), m.v.data_ptr(), m.numel,
+                  self.tc.lr, self.tc.beta1, self.tc.beta2, self.tc.eps, self.adam_t.data_ptr(), scale,
+                  _lib.stream_ptr())
 
     def _sample_body(self, slot: int):
         sl = self.slots[slot]
@@ -197,6 +231,11 @@ class GraphedTrainer:
             sl.n_targets_dev.copy_(self.ntgt_host[slot], non_blocking=True)
         sl.enqueue_device(None if self.host_targets else self.train_ids, self.step_dev[slot],
                           self.cache if self.cfg.strategy == "GNS" else None, exact_tables=self._tables)
+        L, s = self.L, _lib.stream_ptr()
+        for li in range(1, L):
+            ws = self.tws[slot][li]
+            _lib.call("gns_block_transpose", sl.layers[L - 1 - li].cblock, self.cap_dst[li], self.cap_src[li],
+                      self.cap_edges[li], self.dims[li], ws.data_ptr(), ws.numel(), s)
 
     # -- cache + capture ------------------------------------------------------------
     def _refresh_cache(self, epoch: int):
@@ -236,13 +275,14 @@ class GraphedTrainer:
 
     def capture_profiled(self):
         """Re-capture with timing events around the input-feature gather
-        (gns_gather_rows) so its per-launch duration can be read after each
-        replay (used by bench.py for the roofline; not for the headline)."""
+        (gns_gather_rows) and the input-layer SpMM of the first step of each
+        replay, so their durations can be read after a replay (bench.py's
+        roofline; not the headline)."""
         self._prof_events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         for e in self._prof_events:      # materialise the driver events
             e.record(self.main)
         torch.cuda.synchronize()
-        self._capture()
+        self._free_execs()
 
     def gather_ms(self) -> float:
         e = self._prof_events
@@ -255,48 +295,119 @@ class GraphedTrainer:
         e[3].synchronize()
         return float(e[2].elapsed_time(e[3]))
 
-    def _capture(self):
-        torch.cuda.synchronize()
-        self.graphs = []
-        adam_in_graph = self.allreduce is None
-        # warm-up outside capture (cuBLAS handles / workspaces)
+    # -- capture / replay ---------------------------------------------------------------
+    def _group(self, p: int):
+        return [p * self.S + j for j in range(self.S)]
+
+    def slot_of(self, k: int) -> int:
+        """Sampler slot holding the k-th batch of a run_epoch call."""
+        return ((k // self.S) % 2) * self.S + k % self.S
+
+    def _warm(self):
+        # outside capture: cuBLAS handles / workspaces, NCCL communicator
         ev, self._prof_events = self._prof_events, None
         with torch.cuda.stream(self.main):
             self._train_body(0, with_adam=False)
+            if self.allreduce is not None:
+                self.allreduce(self.model.grad)
         self._prof_events = ev
         torch.cuda.synchronize()
+
+    def _capture(self, p: int, r: int):
+        """Graph (p, r): train the first r slots of group p (r <= S) and
+        sample the next S batches into group 1-p."""
+        torch.cuda.synchronize()
         c0 = _lib.launch_counter[0]
-        for p in range(2):
-            if p == 1:
-                self._per_replay = _lib.launch_counter[0] - c0
-            gph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gph, stream=self.main):
-                # the HBM-bound gather runs alone first; the (latency-bound)
-                # sampler branch then overlaps the rest of the training step
-                self._gather(p)
-                fork = torch.cuda.Event()
-                fork.record(self.main)
-                self.side.wait_event(fork)
-                with torch.cuda.stream(self.side):
-                    self._sample_body(1 - p)
-                self._train_rest(p, with_adam=False)
-                join = torch.cuda.Event()
-                join.record(self.side)
-                self.main.wait_event(join)
-            self.graphs.append(gph)
+        gph = torch.cuda.CUDAGraph(keep_graph=True)
+        train, nxt = self._group(p)[:r], self._group(1 - p)
+        with torch.cuda.graph(gph, stream=self.main):
+            # the HBM-bound gather of the first step runs alone; the
+            # (latency-bound) sampler branches then overlap the rest
+            self._gather(train[0])
+            fork = torch.cuda.Event()
+            fork.record(self.main)
+            joins = []
+            for j, sl in enumerate(nxt):
+                side = self.sides[j]
+                side.wait_event(fork)
+                with torch.cuda.stream(side):
+                    self._sample_body(sl)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                joins.append(ev)
+            ev_prof, self._prof_events = self._prof_events, None
+            for j, sl in enumerate(train):
+                self._prof_events = ev_prof if j == 0 else None
+                if j > 0:
+                    self._gather(sl)
+                self._train_rest(sl, with_adam=True)
+                self.step_loss[j:j + 1].copy_(self.model.loss_dev)
+            self._prof_events = ev_prof
+            for ev in joins:
+                self.main.wait_event(ev)
+        if p == 0 and r == self.S:
+            self._per_replay = _lib.launch_counter[0] - c0
         # captured launches are not executions: remove them from the counter
         _lib.launch_counter[0] = c0
-        self.adam_in_graph = adam_in_graph
+        ex = ctypes.c_void_p()
+        _lib.call("gns_graph_instantiate", gph.raw_cuda_graph(), 0 if self.prio_mode == "none" else 1,
+                  ctypes.byref(ex))
+        self._execs[(p, r)] = (gph, ex)
         torch.cuda.synchronize()
 
-    def loss_value(self) -> float:
-        """Loss of the last replayed step (synchronises the engine stream)."""
-        self.main.synchronize()
-        return float(self.loss[0])
+    def _free_execs(self):
+        for _, ex in self._execs.values():
+            _lib.call("gns_graph_exec_destroy", ex)
+        self._execs = {}
 
-    def kernels_per_step(self) -> int:
-        """libgns kernels inside one captured step graph (replayed per step)."""
-        return int(getattr(self, "_per_replay", 0))
+    def __del__(self):
+        try:
+            self._free_execs()
+        except Exception:
+            pass
+
+    def _replay(self, p: int, r: int | None = None):
+        r = self.S if r is None else r
+        if (p, r) not in self._execs:
+            if not self._execs:
+                self._warm()
+            self._capture(p, r)
+        _lib.call("gns_graph_launch", self._execs[(p, r)][1], _lib.stream_ptr(self.main))
+
+    def prepare(self, steps: int):
+        """Capture every step graph a run of ``steps`` steps (within one
+        epoch) replays, so no capture happens inside a timed region."""
+        if not self._execs:
+            self._warm()
+        for r in {self.S, steps % self.S} - {0}:
+            for p in (0, 1):
+                if (p, r) not in self._execs:
+                    self._capture(p, r)
+
+    @property
+    def graphs(self):
+        """Captured step graphs of the current cache (torch CUDAGraph objects)."""
+        return [self._execs[k][0] for k in sorted(self._execs)]
+
+    def kernel_priorities(self, p: int = 0):
+        """Histogram of |priority| over the kernel nodes of step graph (p, S)."""
+        if (p, self.S) not in self._execs:
+            self._capture(p, self.S)
+        hist = (ctypes.c_int32 * 8)()
+        _lib.call("gns_graph_kernel_priorities", self._execs[(p, self.S)][0].raw_cuda_graph(), hist, 8)
+        return list(hist)
+
+    def loss_value(self) -> float:
+        """Loss of the step reported by the last on_step/on_loss callback
+        (synchronises the engine stream)."""
+        self.main.synchronize()
+        return float(self.step_loss[self._cur_j])
+
+    def kernels_per_step(self) -> float:
+        """libgns kernels inside the captured step graph, per training step."""
+        if not self._per_replay and (0, self.S) not in self._execs:
+            self._capture(0, self.S)
+        return self._per_replay / self.S
 
     # -- driving ----------------------------------------------------------------------
     def batches(self, epoch: int):
@@ -315,66 +426,68 @@ class GraphedTrainer:
                 first += n
         return epoch, first
 
+    def _begin(self, epoch: int, refresh: bool):
+        torch.cuda.synchronize()
+        if refresh:
+            self._refresh_cache(epoch)
+            self._free_execs()
+        self.adam_t.fill_(self.model.step_count)
+
     def run_epoch(self, epoch: int, first: int = 0, max_steps: int | None = None, on_step=None) -> int:
-        need_refresh = self.cfg.strategy == "GNS" and first == 0 and \
-            (self.cache is None or epoch % self.cfg.cache_period == 0)
-        if self.cfg.strategy == "GNS" and self.cache is None:
-            need_refresh = True
-        if need_refresh or self.graphs is None:
-            torch.cuda.synchronize()
-            if need_refresh:
-                self._refresh_cache(epoch)
-            self._set_step(0, epoch, None)
-            self._set_step(1, epoch, None)
-            self._capture()
+        need_refresh = self.cfg.strategy == "GNS" and (
+            self.cache is None or (first == 0 and epoch % self.cfg.cache_period == 0))
         idx = self.batches(epoch)[first:]
         if max_steps is not None:
             idx = idx[:max_steps]
         if not idx:
             return 0
-        # prologue: sample the first batch into slot 0
-        self._set_step(0, epoch, idx[0])
+        self._begin(epoch, need_refresh)
+        S = self.S
+        groups = [idx[i:i + S] for i in range(0, len(idx), S)]
+        # prologue: sample the first group into group-0 slots
+        for j, sl in enumerate(self._group(0)):
+            self._set_step(sl, epoch, groups[0][j] if j < len(groups[0]) else None)
         with torch.cuda.stream(self.main):
-            self._sample_body(0)
-        for k, index in enumerate(idx):
-            p = k % 2
-            nxt = idx[k + 1] if k + 1 < len(idx) else None
-            self._set_step(1 - p, epoch, nxt)
+            for sl in self._group(0):
+                self._sample_body(sl)
+        k = 0
+        for gi, grp in enumerate(groups):
+            p = gi % 2
+            nxt = groups[gi + 1] if gi + 1 < len(groups) else []
+            for j, sl in enumerate(self._group(1 - p)):
+                self._set_step(sl, epoch, nxt[j] if j < len(nxt) else None)
             with torch.cuda.stream(self.main):
-                self.graphs[p].replay()
-                if self.allreduce is not None:
-                    scale = self.allreduce(self.model.grad)
-                    m = self.model
-                    m.step_count += 1
-                    _lib.call("gns_adam", 0, m.flat.data_ptr(), m.grad.data_ptr(), m.m.data_ptr(), m.v.data_ptr(),
-                              m.numel, self.tc.lr, self.tc.beta1, self.tc.beta2, self.tc.eps, m.step_count, scale,
-                              _lib.stream_ptr())
-                else:
-                    self._adam()
+                self._replay(p, len(grp))
                 ev = torch.cuda.Event()
                 ev.record(self.main)
-                self.done[1 - p] = ev
-            if on_step is not None:
-                on_step(epoch, index, k)
+                for sl in self._group(1 - p):
+                    self.done[sl] = ev
+            self.model.step_count += len(grp)
+            for j, index in enumerate(grp):
+                self._cur_j = j
+                if on_step is not None:
+                    on_step(epoch, index, k)
+                k += 1
         return len(idx)
 
     def run_host(self, batches, epoch: int = 0, on_loss=None):
         """End-to-end API with host buffers: ``batches`` are host int arrays of
-        target ids; every step copies them from pinned memory (memcpy node in
-        the graph) and reads the loss back to the host.  Requires
+        target ids; every step copies them from pinned memory (memcpy nodes in
+        the graph) and every step's loss is read back to the host.  Requires
         ``host_targets=True``."""
         if not self.host_targets:
             raise ValueError("construct with host_targets=True")
-        if self.graphs is None or (self.cfg.strategy == "GNS" and self.cache is None):
-            if self.cfg.strategy == "GNS" and self.cache is None:
-                self._refresh_cache(epoch)
-            self._capture()
+        if not batches:
+            return []
+        self._begin(epoch, self.cfg.strategy == "GNS" and self.cache is None)
+        S = self.S
         losses = []
+        lh = torch.zeros(S, dtype=torch.float64).pin_memory()
 
         def put(slot, k):
             if self.done[slot] is not None:
                 self.done[slot].synchronize()
-            if k is None:
+            if k is None or k >= len(batches):
                 self.ntgt_host[slot][0] = 0
                 return
             t = torch.as_tensor(batches[k], dtype=torch.int32)
@@ -383,24 +496,29 @@ class GraphedTrainer:
             h = self.step_host[slot]
             h[0] = (self.cfg.seed & 0xFFFFFFFF) | ((epoch & 0xFFFFFFFF) << 32)
             h[1] = k & 0xFFFFFFFF
-        put(0, 0)
+        for j, sl in enumerate(self._group(0)):
+            put(sl, j)
         with torch.cuda.stream(self.main):
-            self._sample_body(0)
-        lh = torch.zeros(1, dtype=torch.float64).pin_memory()
-        for k in range(len(batches)):
-            p = k % 2
-            put(1 - p, k + 1 if k + 1 < len(batches) else None)
+            for sl in self._group(0):
+                self._sample_body(sl)
+        for gi, b0 in enumerate(range(0, len(batches), S)):
+            p = gi % 2
+            r = min(S, len(batches) - b0)
+            for j, sl in enumerate(self._group(1 - p)):
+                put(sl, b0 + S + j)
             with torch.cuda.stream(self.main):
-                self.graphs[p].replay()
-                self._adam()
-                lh.copy_(self.loss, non_blocking=True)
+                self._replay(p, r)
+                lh.copy_(self.step_loss, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self.main)
-                self.done[1 - p] = ev
+                for sl in self._group(1 - p):
+                    self.done[sl] = ev
             ev.synchronize()
-            losses.append(float(lh[0]))
-            if on_loss is not None:
-                on_loss(k, losses[-1])
+            self.model.step_count += r
+            for j in range(r):
+                losses.append(float(lh[j]))
+                if on_loss is not None:
+                    on_loss(b0 + j, losses[-1])
         return losses
 
     def check_errors(self):

@@ -43,22 +43,23 @@ def main():
             fn()
         return gph
 
-    tr._set_step(1, 0, 7)
+    tr._set_step(tr.S, 0, 7)
     variants = {
-        "sample_only": capture(lambda: tr._sample_body(1)),
-        "train_only": capture(lambda: tr._train_body(0, with_adam=False)),
-        "gather_only": capture(lambda: tr._gather(0)),
-        "step (production graph)": tr.graphs[0],
+        "sample_only": capture(lambda: tr._sample_body(tr.S)).replay,
+        "train_only": capture(lambda: tr._train_body(0, with_adam=False)).replay,
+        "gather_only": capture(lambda: tr._gather(0)).replay,
+        f"{tr.S} steps (production graph, priority={tr.prio_mode})": lambda: tr._replay(0),
     }
-    for name, gph in variants.items():
+    print("kernel-node |priority| histogram:", tr.kernel_priorities(0))
+    for name, replay in variants.items():
         for _ in range(3):
-            gph.replay()
+            replay()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(tr.main)
         with torch.cuda.stream(tr.main):
             for _ in range(args.steps):
-                gph.replay()
+                replay()
         e.record(tr.main)
         e.synchronize()
         print(f"{name:26s} {s.elapsed_time(e) / args.steps * 1e3:8.1f} us/replay")
