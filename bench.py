@@ -156,6 +156,37 @@ def cpu_reference_run(P, g, c, cfg, cache, n_batches, warmup=1):
     return r
 
 
+def gather_microbench(tr, D, reps=24):
+    """features[input_nodes] (model.py:146) through gns_gather_rows on the
+    input nodes of the batches currently held in the engine's sampler slots;
+    a 256 MB write between launches flushes L2.  Returns [(bytes, ms)]."""
+    from paper_2106_06150_b200 import _lib
+    L = len(FANOUTS)
+    sets = []
+    for sl in tr.slots:
+        b0 = sl.layers[L - 1]
+        n = int(b0.counts[_lib.CNT_SRC])
+        if n:
+            sets.append((b0.src_nodes, b0.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1], n))
+    tab = tr.g.features
+    out = torch.empty((max(n for _, _, n in sets), D), dtype=torch.float32, device=tab.device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=tab.device)
+    s = torch.cuda.current_stream()
+    res = []
+    for it in range(reps + 2):
+        ids, n_dev, n = sets[it % len(sets)]
+        flush.fill_(it & 0xFF)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, ids.data_ptr(), n_dev.data_ptr(), out.shape[0],
+                  D, out.data_ptr(), out.stride(0), 0, _lib.stream_ptr(s))
+        e1.record(s)
+        e1.synchronize()
+        if it >= 2:
+            res.append((n * (2 * 4 * D + 4), e0.elapsed_time(e1)))
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,53 +271,66 @@ def main():
     value = args.steps * world / (ms / 1e3)
     tr.check_errors()
 
-    # gather roofline: same graph re-captured with timing events around the
-    # gather, replayed on the following batches (algorithmic bytes: rows read
-    # + rows written + int32 ids)
+    # per-kernel rooflines: the step graph re-captured with timing events
+    # around the input-layer kernels of the first step of each replay
+    # (gns_gather_rows + gns_spmm_fwd, or the fused gns_spmm_fwd_gather)
     peak, peak_kind = load_peaks()
-    gather_ms, n_in = [], []
     tr.capture_profiled()
     nprof = min(30, args.steps) * tr.S
-
-    spmm_ms, spmm_bytes = [], []
+    gather_ms, spmm_ms, spmm_bytes, n_in = [], [], [], []
+    D = c["dim"]
 
     def on_step(e, i, k):
         if k % tr.S:          # the events time the first step of each replay
             return
-        gather_ms.append(tr.gather_ms())
+        if not tr.fused_gather:
+            gather_ms.append(tr.gather_ms())
         spmm_ms.append(tr.spmm0_ms())
         cnt = tr.slots[tr.slot_of(k)].counts[len(FANOUTS) - 1].tolist()
         n_in.append(cnt[_lib.CNT_SRC])
         nd, ne = cnt[_lib.CNT_DST], cnt[_lib.CNT_EDGES]
         # input-layer SpMM: h rows read (edges + self) + cat rows written (incl.
         # capacity zero padding) + per-edge index/weight (4 + 8 B) + row scan
-        spmm_bytes.append((ne + nd) * 4 * c["dim"] + tr.npad[0] * 2 * 4 * c["dim"] + 12 * ne + 8 * nd)
+        # (+ dst id when the gather is fused)
+        spmm_bytes.append((ne + nd) * 4 * D + tr.npad[0] * 2 * 4 * D + 12 * ne + (12 if tr.fused_gather else 8) * nd)
     pos = tr.run(nprof, epoch=pos[0], first=pos[1], on_step=on_step)
     n_in = np.array(n_in, dtype=np.float64)
-    row_bytes = 4 * c["dim"]
-    gbytes = n_in * (2 * row_bytes + 4)
-    gather_gbs = float(gbytes.sum() / (np.sum(gather_ms) / 1e3) / 1e9)
-    roofline = {"kernel": "gns_gather_rows (gather_f32x4_kernel)", "bound": "hbm",
-                "achieved": round(gather_gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": round(gather_gbs / peak, 4), "traffic": None,
-                "algorithmic_bytes_per_launch": float(gbytes.mean()),
-                "avg_launch_ms": float(np.mean(gather_ms)),
-                "share_of_step": float(np.mean(gather_ms) / (ms / args.steps)),
-                "measured": f"CUDA events around the gather inside the captured step graph, {len(gather_ms)} replays"}
+    gbytes = n_in * (2 * 4 * D + 4)     # rows read + rows written + int32 ids
+    if not tr.fused_gather:
+        g_ms = np.array(gather_ms)
+        g_how = f"CUDA events around the gather inside the captured step graph, {len(g_ms)} replays"
+    else:
+        g_ms, g_how = gather_microbench(tr, D), ("gns_gather_rows (reference-API gather) on the input nodes of the "
+                                                 "engine's sampled batches, CUDA events, L2 flushed between launches")
+        gbytes = np.array([gather_bytes for gather_bytes, _ in g_ms])
+        g_ms = np.array([t for _, t in g_ms])
+    gather_gbs = float(gbytes.sum() / (g_ms.sum() / 1e3) / 1e9)
     spmm_gbs = float(np.sum(spmm_bytes) / (np.sum(spmm_ms) / 1e3) / 1e9)
-    kernels = {
-        "gns_gather_rows": {"achieved_gbs": round(gather_gbs, 1), "frac": round(gather_gbs / peak, 4),
-                            "avg_ms": float(np.mean(gather_ms))},
-        "gns_spmm_fwd (input layer)": {"achieved_gbs": round(spmm_gbs, 1), "frac": round(spmm_gbs / peak, 4),
-                                       "avg_ms": float(np.mean(spmm_ms)),
-                                       "algorithmic_bytes_per_launch": float(np.mean(spmm_bytes))},
-    }
+    gather_k = {"kernel": "gns_gather_rows (gather_f32x4_kernel)", "bound": "hbm", "achieved": round(gather_gbs, 1),
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gather_gbs / peak, 4),
+                "traffic": None, "algorithmic_bytes_per_launch": float(gbytes.mean()),
+                "avg_launch_ms": float(g_ms.mean()), "measured": g_how}
+    spmm_name = "gns_spmm_fwd_gather (input layer, fused feature gather)" if tr.fused_gather else \
+        "gns_spmm_fwd (input layer)"
+    spmm_k = {"kernel": spmm_name, "bound": "hbm", "achieved": round(spmm_gbs, 1), "peak": peak,
+              "peak_kind": peak_kind, "unit": "GB/s", "frac": round(spmm_gbs / peak, 4), "traffic": None,
+              "algorithmic_bytes_per_launch": float(np.mean(spmm_bytes)), "avg_launch_ms": float(np.mean(spmm_ms)),
+              "share_of_step": float(np.mean(spmm_ms) / (ms / args.steps)),
+              "measured": f"CUDA events around the kernel inside the captured step graph, {len(spmm_ms)} replays"}
+    if not tr.fused_gather:
+        gather_k["share_of_step"] = float(g_ms.mean() / (ms / args.steps))
+    # the dominant HBM kernel of the step: the fused gather+aggregate when the
+    # gather is fused, else the gather (as in round 1)
+    roofline = spmm_k if tr.fused_gather else gather_k
+    kernels = {"gns_gather_rows": gather_k, "gns_spmm_fwd (input layer)": spmm_k}
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_path):
         try:
-            tr_ = json.load(open(prof_path)).get(args.config, {}).get("gather_f32x4_kernel")
-            if tr_:
-                roofline["traffic"] = tr_
+            tj = json.load(open(prof_path)).get(args.config, {})
+            for kk, name in ((gather_k, "gather_f32x4_kernel"), (spmm_k, "spmm_fwd_gather" if tr.fused_gather
+                                                                     else "spmm_fwd_kernel")):
+                if tj.get(name):
+                    kk["traffic"] = tj[name]
         except Exception:
             pass
     pool = tr
@@ -341,7 +385,8 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
                 "gpu_launches_per_step": launches_total / args.steps, "clocks": clk,
-                "per_step": {"input_nodes": float(n_in.mean()), "gather_ms": float(np.mean(gather_ms)),
+                "per_step": {"input_nodes": float(n_in.mean()), "gather_ms": float(g_ms.mean()),
+                             "fused_gather": tr.fused_gather,
                              "graph_replays": -(-args.steps // tr.S), "steps_per_graph": tr.S,
                              "step_priority": tr.prio_mode}}
         print(json.dumps(line), flush=True)

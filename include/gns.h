@@ -291,6 +291,16 @@ GNS_API int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim
                          const gns_block_t* block, int64_t max_dst, int64_t pad_rows, void* cat,
                          int64_t ld_cat, void* stream);
 
+/* The input layer's gns_spmm_fwd fused with the feature gather (model.py:146
+ * + 153): h rows are read straight from the float32 node feature table by
+ * global node id — block->edge_node for the neighbours, dst_ids[r] (the
+ * block's dst node ids) for the self half — instead of from a materialised
+ * features[input_nodes].  Output identical to gns_gather_rows followed by
+ * gns_spmm_fwd(dtype 0, flags 0). */
+GNS_API int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim,
+                                const gns_block_t* block, const int32_t* dst_ids, int64_t max_dst,
+                                int64_t pad_rows, float* cat, int64_t ld_cat, void* stream);
+
 /* Backward of the above (model.py:223-225):
  * dh[s,:] = sum_{e: src=s, ascending dst} w_e * (dcat[dst_e, D:2D] / max(deg,1))
  *           (+ dcat[d, 0:D] where self_pos[d] == s).

@@ -39,6 +39,18 @@ int check_launch(const char* what);
 
 int num_sms();
 
+// Fork/join of independent kernels inside one entry point: work launched on
+// `aux` runs concurrently with the calling stream (eagerly, and as parallel
+// branches when the calling stream is being captured into a CUDA graph).
+// Each calling stream gets its own auxiliary stream (same priority), so
+// concurrent callers on different streams never share one.
+struct Fork {
+  cudaStream_t aux;
+  cudaEvent_t ev_fork, ev_join;
+};
+int fork_begin(cudaStream_t s, Fork* f);  // aux waits for everything issued on s so far
+int fork_join(cudaStream_t s, const Fork& f);  // s waits for everything issued on aux
+
 static inline unsigned div_up(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 static inline int grid_for(long long want, long long cap) {
   long long g = want < cap ? want : cap;

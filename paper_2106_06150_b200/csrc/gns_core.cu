@@ -5,6 +5,9 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "gns_common.cuh"
 
 namespace gns {
@@ -24,6 +27,34 @@ int check_launch(const char* what) {
     set_error("%s: %s", what, cudaGetErrorString(e));
     return GNS_ECUDA;
   }
+  return GNS_OK;
+}
+
+int fork_begin(cudaStream_t s, Fork* f) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, Fork> forks;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = forks.find(s);
+    if (it == forks.end()) {
+      Fork nf;
+      int prio = 0;
+      if (s != nullptr) GNS_CUDA(cudaStreamGetPriority(s, &prio));
+      GNS_CUDA(cudaStreamCreateWithPriority(&nf.aux, cudaStreamNonBlocking, prio));
+      GNS_CUDA(cudaEventCreateWithFlags(&nf.ev_fork, cudaEventDisableTiming));
+      GNS_CUDA(cudaEventCreateWithFlags(&nf.ev_join, cudaEventDisableTiming));
+      it = forks.emplace(s, nf).first;
+    }
+    *f = it->second;
+  }
+  GNS_CUDA(cudaEventRecord(f->ev_fork, s));
+  GNS_CUDA(cudaStreamWaitEvent(f->aux, f->ev_fork, 0));
+  return GNS_OK;
+}
+
+int fork_join(cudaStream_t s, const Fork& f) {
+  GNS_CUDA(cudaEventRecord(f.ev_join, f.aux));
+  GNS_CUDA(cudaStreamWaitEvent(s, f.ev_join, 0));
   return GNS_OK;
 }
 

@@ -171,10 +171,19 @@ __device__ __forceinline__ V ldv(const V* p) {
 // RELU: the input rows are the previous layer's pre-activations z and
 // relu(z) (model.py:156) is applied on load instead of being materialised.
 // Rows [n, pad_rows) of cat are zero-filled (static-capacity GEMMs).
-template <typename T, int CH, bool RELU>
+//
+// GATHER (the input layer, fused feature gather, model.py:146+153): h is the
+// node feature table and rows are addressed by global node id — edge_node for
+// the neighbours, dst_ids[r] for the self row — so features[input_nodes] is
+// never materialised.  src_nodes is sorted, so ordering a row's edges by node
+// id is the same as ordering them by edge_src: the sums are bit-identical.
+template <typename T, int CH, bool RELU, bool GATHER = false>
 __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restrict__ h, int64_t ld_h, int dim,
                                                               BlockView bv, T* __restrict__ cat, int64_t ld_cat,
-                                                              int64_t pad_rows) {
+                                                              int64_t pad_rows,
+                                                              const int32_t* __restrict__ edge_node = nullptr,
+                                                              const int32_t* __restrict__ dst_ids = nullptr) {
+  const int32_t* __restrict__ eidx = GATHER ? edge_node : bv.edge_src;
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   __shared__ int32_t s_idx[kSpmmBlock / 32][kRowCap];
@@ -201,7 +210,7 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
       my_w[j] = 0;
       if (i < L) {
         int64_t e = i < nc ? cb + i : fb + (i - nc);
-        my_idx[j] = bv.edge_src[e];
+        my_idx[j] = eidx[e];
         my_w[j] = (T)bv.edge_weight[e];
       }
     }
@@ -227,13 +236,13 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
       int i = lane + 32 * j;
       if (i < L) {
         int64_t e = i < nc ? cb + i : fb + (i - nc);
-        s_idx[wib][my_idx[j]] = bv.edge_src[e];
+        s_idx[wib][my_idx[j]] = eidx[e];
         s_w[wib][my_idx[j]] = my_w[j];
       }
     }
     __syncwarp();
     const T norm = (T)max(bv.dst_degree[r], 1);
-    const V* hs = reinterpret_cast<const V*>(h + (int64_t)bv.self_pos[r] * ld_h);
+    const V* hs = reinterpret_cast<const V*>(h + (int64_t)(GATHER ? dst_ids[r] : bv.self_pos[r]) * ld_h);
     V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
     for (int c = lane; c < dv; c += 32) crow[c] = ldv<V, RELU>(hs + c);
     for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
@@ -703,6 +712,30 @@ int gns_cache_refresh_rows(const float* host_table, int64_t ld, const int32_t* i
   int grid = grid_for(want, (long long)num_sms() * 16);
   refresh_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream_>>>(host_table, ld, ids, n_dev, dim / 4, cache_table);
   return check_launch("cache_refresh_rows");
+}
+
+int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const gns_block_t* block,
+                        const int32_t* dst_ids, int64_t max_dst, int64_t pad_rows, float* cat, int64_t ld_cat,
+                        void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (max_dst <= 0 && pad_rows <= 0) return GNS_OK;
+  if (dim % 4 || ld_table % 4 || ld_cat % 4 || (uintptr_t)table % 16 || (uintptr_t)cat % 16) {
+    set_error("spmm_fwd_gather: dim/strides must be multiples of 4 floats, pointers 16-B aligned");
+    return GNS_EINVAL;
+  }
+  const int sms = num_sms();
+  long long rows = max_dst > pad_rows ? max_dst : pad_rows;
+  int grid = grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)sms * 8);
+  BlockView bv = view_of(block);
+  const int dv = dim / 4;
+#define GNS_FWDG(CH)                                                                                          \
+  spmm_fwd_kernel<float, CH, false, true><<<grid, kSpmmBlock, 0, stream>>>(table, ld_table, dim, bv, cat, ld_cat, \
+                                                                          pad_rows, block->edge_node, dst_ids)
+  if (dv <= 32) GNS_FWDG(1);
+  else if (dv <= 64) GNS_FWDG(2);
+  else GNS_FWDG(4);
+#undef GNS_FWDG
+  return check_launch("spmm_fwd_gather");
 }
 
 int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_t flags, const gns_block_t* block,

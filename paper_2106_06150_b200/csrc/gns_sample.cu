@@ -66,6 +66,20 @@ __device__ __forceinline__ void mark_node(uint32_t* __restrict__ bits, uint32_t*
   if (old == 0u) atomicOr(sum + (w >> 5), 1u << (w & 31));
 }
 
+// Append to a global list with one atomic per warp: returns the slot of the
+// calling lane if pred, else -1 (all active lanes must call it).
+__device__ __forceinline__ int warp_append(int32_t* ctr, bool pred) {
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, pred);
+  if (m == 0u) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(ctr, __popc(m));
+  base = __shfl_sync(act, base, leader);
+  return pred ? base + __popc(m & ((1u << lane) - 1u)) : -1;
+}
+
 // per-batch Philox key from device memory (CUDA-graph replay) when given
 __device__ __forceinline__ LayerArgs resolve_rng(const LayerArgs& in) {
   LayerArgs a = in;
@@ -147,23 +161,20 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(LayerArgs 
         // [0, 2*max_dst), warp items from 2*max_dst up, hub items from
         // 4*max_dst-1 down.  The two phases of a row are independent (their
         // output offsets come from the scan), so they run concurrently.
+        // warp-aggregated appends: one atomic per warp and tier instead of
+        // one per item (the three list counters are hot addresses)
 #pragma unroll
         for (int ph = 0; ph < 2; ++ph) {
           const int take = ph == 0 ? ri.m : ri.fill;
-          if (take <= 0) continue;
           const int len = ph == 0 ? ri.nc : ri.deg;
           const int32_t item = (int32_t)((r << 1) | ph);
-          const int tier = phase_tier(len);
-          if (tier == 0) {
-            int h = atomicAdd(a.b.counts + GNS_CNT_THREADROWS, 1);
-            a.b.hub_rows[h] = item;
-          } else if (tier == 1) {
-            int h = atomicAdd(a.b.counts + GNS_CNT_WARPROWS, 1);
-            a.b.hub_rows[2 * a.max_dst + h] = item;
-          } else {
-            int h = atomicAdd(a.b.counts + GNS_CNT_HUBS, 1);
-            a.b.hub_rows[4 * a.max_dst - 1 - h] = item;
-          }
+          const int tier = take > 0 ? phase_tier(len) : -1;
+          int h = warp_append(a.b.counts + GNS_CNT_THREADROWS, tier == 0);
+          if (h >= 0) a.b.hub_rows[h] = item;
+          h = warp_append(a.b.counts + GNS_CNT_WARPROWS, tier == 1);
+          if (h >= 0) a.b.hub_rows[2 * a.max_dst + h] = item;
+          h = warp_append(a.b.counts + GNS_CNT_HUBS, tier == 2);
+          if (h >= 0) a.b.hub_rows[4 * a.max_dst - 1 - h] = item;
         }
       },
       [&](unsigned long long tot) {
@@ -658,6 +669,59 @@ __global__ void relabel_kernel(const unsigned long long* __restrict__ rank2, con
   }
 }
 
+// np.unique for small id lists (<= kSmallUnique, e.g. the 1000 targets of a
+// batch): one CTA, bitonic sort in shared memory, then an ordered compaction
+// of the first element of every run.  Replaces setbits + two enumerate passes
+// over the N/1024-word summary bitmap.
+constexpr int kSmallUnique = 4096;
+constexpr int kSmallBlock = 1024;
+
+__global__ void __launch_bounds__(kSmallBlock) unique_small_kernel(const int32_t* __restrict__ ids,
+                                                                   const int32_t* __restrict__ n_dev, int64_t n_host,
+                                                                   int32_t* __restrict__ out,
+                                                                   int32_t* __restrict__ out_n) {
+  __shared__ int32_t key[kSmallUnique];
+  __shared__ unsigned long long s_warp[kSmallBlock / 32 + 1];
+  const int n = (int)(n_dev ? min((int64_t)n_dev[0], n_host) : n_host);
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += kSmallBlock) key[i] = i < n ? ids[i] : INT32_MAX;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += kSmallBlock) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int32_t x = key[i], y = key[l];
+          const bool up = (i & k) == 0;
+          if (up ? (y < x) : (x < y)) {
+            key[i] = y;
+            key[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // each thread owns a contiguous chunk of <= 4 sorted keys
+  constexpr int IT = kSmallUnique / kSmallBlock;
+  const int b0 = threadIdx.x * IT;
+  unsigned c = 0;
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    const int i = b0 + q;
+    if (i < n && (i == 0 || key[i] != key[i - 1])) ++c;
+  }
+  unsigned long long total;
+  unsigned long long o = block_excl_scan<kSmallBlock>((unsigned long long)c, s_warp, total);
+#pragma unroll
+  for (int q = 0; q < IT; ++q) {
+    const int i = b0 + q;
+    if (i < n && (i == 0 || key[i] != key[i - 1])) out[o++] = key[i];
+  }
+  if (threadIdx.x == 0) out_n[0] = (int32_t)total;
+}
+
 struct DedupWs {
   uint32_t* bits;
   uint32_t* sum;
@@ -765,14 +829,19 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   layer_count_apply_kernel<<<tiles, kCntBlock, 0, stream>>>(a, ctiles);
   GNS_TRY(check_launch("layer_count"));
   const int sms = num_sms();
+  // the three tiers work on disjoint (row, phase) lists: thread tier on the
+  // calling stream, warp and hub tiers on a forked branch, concurrently
+  Fork fk;
+  GNS_TRY(fork_begin(stream, &fk));
   int tgrid = grid_for((2 * max_dst + 255) / 256, (long long)sms * 16);
   sample_thread_kernel<<<tgrid, 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_thread"));
   int grid = grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock, (long long)sms * 8);
-  sample_warp_kernel<<<grid, kSampBlock, 0, stream>>>(a);
+  sample_warp_kernel<<<grid, kSampBlock, 0, fk.aux>>>(a);
   GNS_TRY(check_launch("sample_warp"));
-  sample_hub_kernel<<<sms, kHubBlock, 0, stream>>>(a);
+  sample_hub_kernel<<<sms, kHubBlock, 0, fk.aux>>>(a);
   GNS_TRY(check_launch("sample_hub"));
+  GNS_TRY(fork_join(stream, fk));
   // _assemble (sampling.py:139-152): seeds and sampled neighbours were marked
   // in the dedup bitmap by the count / sample kernels
   return run_relabel(dd, seeds, n_seeds_dev, max_dst, block, max_dst * (int64_t)k, stream);
@@ -811,6 +880,10 @@ int gns_unique_sorted(int64_t num_nodes, const int32_t* ids, const int32_t* n_de
   if (!w.ok()) {
     set_error("unique_sorted: workspace %zu < %zu", ws_bytes, w.off);
     return GNS_EINVAL;
+  }
+  if (n_host <= kSmallUnique) {
+    unique_small_kernel<<<1, kSmallBlock, 0, stream>>>(ids, n_dev, n_host, out, out_n_dev);
+    return check_launch("unique_small");
   }
   int grid = grid_for((n_host + 255) / 256 + 1, (long long)num_sms() * 16);
   setbits_kernel<<<grid, 256, 0, stream>>>(ids, n_dev, n_host, nullptr, nullptr, d.bits, d.sum);

@@ -87,6 +87,9 @@ class GraphedTrainer:
         if feature_placement not in ("device", "mixed"):
             raise ValueError(f"unknown feature_placement {feature_placement!r}")
         self.placement = feature_placement
+        # device placement: the input layer's SpMM reads the feature table
+        # directly (gns_spmm_fwd_gather) instead of a gathered copy
+        self.fused_gather = feature_placement == "device" and os.environ.get("GNS_FUSED_GATHER", "1") == "1"
         self.host_features = None
         self.cache_table = None
         if feature_placement == "mixed":
@@ -113,6 +116,8 @@ class GraphedTrainer:
                       for _ in range(S)]
         self.side = self.sides[0]
         self.main = torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "main" else lo)
+        self.taux = [torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "side" else lo)
+                     for _ in range(2 * S)]
         self._execs = {}
         self._per_replay = 0
         self._alloc()
@@ -127,7 +132,7 @@ class GraphedTrainer:
         self.cap_edges = [sl.layers[L - 1 - li].max_edges for li in range(L)]
         self.npad = [_split_rows(c) for c in self.cap_dst]
         f32 = torch.float32
-        self.h0 = torch.empty((max(self.cap_src[0], 1), dims[0]), dtype=f32, device=dev)
+        self.h0 = torch.empty((1 if self.fused_gather else max(self.cap_src[0], 1), dims[0]), dtype=f32, device=dev)
         self.cat = [torch.empty((max(self.npad[li], 1), 2 * dims[li]), dtype=f32, device=dev) for li in range(L)]
         self.z = [torch.empty((max(self.cap_dst[li], 1), dims[li + 1]), dtype=f32, device=dev) for li in range(L)]
         self.dz = [torch.zeros((max(self.npad[li], 1), dims[li + 1]), dtype=f32, device=dev) for li in range(L)]
@@ -150,7 +155,10 @@ class GraphedTrainer:
         self._train_rest(slot, with_adam)
 
     def _gather(self, slot: int):
-        """features[input_nodes] -> h0 (model.py:146)."""
+        """features[input_nodes] -> h0 (model.py:146); fused into the input
+        layer's SpMM (no-op here) when ``fused_gather``."""
+        if self.fused_gather:
+            return
         sl, L, s = self.slots[slot], self.L, _lib.stream_ptr()
         b0 = sl.layers[L - 1]
         n_in_dev = b0.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
@@ -181,8 +189,16 @@ class GraphedTrainer:
                 ev = self._prof_events if li == 0 else None
                 if ev is not None:
                     _lib.call("gns_record_event_external", ev[2].cuda_event, s)
-                _lib.call("gns_spmm_fwd", 0, h.data_ptr(), h.stride(0), d_in, 1 if li > 0 else 0, blocks[li].cblock,
-                          self.cap_dst[li], self.npad[li], self.cat[li].data_ptr(), self.cat[li].stride(0), s)
+                if li == 0 and self.fused_gather:
+                    tab = self.g.features
+                    dst_ids = sl.layers[L - 2].src_nodes if L > 1 else sl.seeds0
+                    _lib.call("gns_spmm_fwd_gather", tab.data_ptr(), tab.stride(0), d_in, blocks[0].cblock,
+                              dst_ids.data_ptr(), self.cap_dst[0], self.npad[0], self.cat[0].data_ptr(),
+                              self.cat[0].stride(0), s)
+                else:
+                    _lib.call("gns_spmm_fwd", 0, h.data_ptr(), h.stride(0), d_in, 1 if li > 0 else 0,
+                              blocks[li].cblock, self.cap_dst[li], self.npad[li], self.cat[li].data_ptr(),
+                              self.cat[li].stride(0), s)
                 if ev is not None:
                     _lib.call("gns_record_event_external", ev[3].cuda_event, s)
                 torch.addmm(m.biases[li], self.cat[li][:self.cap_dst[li]], m.weights[li], out=self.z[li])
@@ -229,13 +245,30 @@ class GraphedTrainer:
             B = self.cfg.batch_size
             sl.targets[:B].copy_(self.tgt_host[slot], non_blocking=True)
             sl.n_targets_dev.copy_(self.ntgt_host[slot], non_blocking=True)
-        sl.enqueue_device(None if self.host_targets else self.train_ids, self.step_dev[slot],
-                          self.cache if self.cfg.strategy == "GNS" else None, exact_tables=self._tables)
-        L, s = self.L, _lib.stream_ptr()
-        for li in range(1, L):
+        # the backward's block transposes depend only on a finished layer:
+        # each is forked onto the slot's aux stream as soon as its layer is
+        # sampled and overlaps the sampling of the next (larger) layer
+        L, cur, aux = self.L, torch.cuda.current_stream(), self.taux[slot]
+        joins = []
+
+        def transpose(lb):
+            li = L - 1 - sl.layers.index(lb)
+            if li < 1:
+                return
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            aux.wait_event(ev)
             ws = self.tws[slot][li]
-            _lib.call("gns_block_transpose", sl.layers[L - 1 - li].cblock, self.cap_dst[li], self.cap_src[li],
-                      self.cap_edges[li], self.dims[li], ws.data_ptr(), ws.numel(), s)
+            _lib.call("gns_block_transpose", lb.cblock, self.cap_dst[li], self.cap_src[li], self.cap_edges[li],
+                      self.dims[li], ws.data_ptr(), ws.numel(), _lib.stream_ptr(aux))
+            done = torch.cuda.Event()
+            done.record(aux)
+            joins.append(done)
+        sl.enqueue_device(None if self.host_targets else self.train_ids, self.step_dev[slot],
+                          self.cache if self.cfg.strategy == "GNS" else None, exact_tables=self._tables,
+                          after_layer=transpose)
+        for ev in joins:
+            cur.wait_event(ev)
 
     # -- cache + capture ------------------------------------------------------------
     def _refresh_cache(self, epoch: int):

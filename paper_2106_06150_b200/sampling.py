@@ -269,7 +269,7 @@ class MiniBatchSampler:
         return ev
 
     def enqueue_device(self, train_ids: torch.Tensor | None, step_dev: torch.Tensor, cache: CacheState | None,
-                       stream=None, exact_tables=None):
+                       stream=None, exact_tables=None, after_layer=None):
         """Graph-capturable chain: the batch's targets (pool.py:60-66 slice
         begin/count) and Philox key come from the device gns_step_t
         ``step_dev``; no host synchronisation, fixed kernel arguments.  With
@@ -296,6 +296,8 @@ class MiniBatchSampler:
                       lb.k, int(lb.cache_only), self._exact(exact_tables, lb), rng.cstruct(lb.layer),
                       step_dev.data_ptr(), lb.cblock,
                       self.ws_sample.data_ptr(), self.ws_sample.numel(), s)
+            if after_layer is not None:
+                after_layer(lb)
             seeds = lb.src_nodes
             n_dev = lb.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
 

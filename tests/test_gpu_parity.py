@@ -226,6 +226,50 @@ def test_zero_degree_and_repeated_targets(P):
     assert mb.targets.tolist() == [0, 4, 5]
 
 
+@pytest.mark.parametrize("n", [0, 1, 7, 1000, 4096, 4097, 50000])
+def test_unique_sorted_both_paths(P, n):
+    """np.unique (sampling.py:208,312): the single-CTA sort path (n <= 4096)
+    and the bitmap path, with repeats and ids up to N-1."""
+    from paper_2106_06150_b200 import _lib
+    N = 200_000
+    rng = np.random.default_rng(n)
+    ids = rng.integers(0, N, n).astype(np.int32)
+    if n > 2:
+        ids[: n // 3] = ids[n // 3: 2 * (n // 3)]   # repeats
+        ids[-1] = N - 1
+    d_ids = torch.as_tensor(ids, device="cuda") if n else torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = torch.full((max(n, 1),), -1, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = _lib.workspace(_lib.lib().gns_relabel_workspace_size(N), "cuda", zero=True)
+    for n_dev in (None, torch.tensor([n], dtype=torch.int32, device="cuda")):
+        _lib.call("gns_unique_sorted", N, d_ids.data_ptr(), None if n_dev is None else n_dev.data_ptr(), n,
+                  out.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        u = np.unique(ids)
+        assert int(cnt) == len(u)
+        assert np.array_equal(out[:len(u)].cpu().numpy(), u)
+    # both bitmap levels are left zeroed (dedup_ws layout: bits, then summary)
+    r256 = lambda b: (b + 255) // 256 * 256  # noqa: E731
+    nw = (N + 31) // 32
+    nbytes = r256((nw + 1) * 4) + r256(((nw + 31) // 32 + 1) * 4)
+    assert int(ws[:nbytes].count_nonzero()) == 0
+
+
+@pytest.mark.parametrize("dim,rows", [(4, 1), (64, 33), (100, 1001), (128, 4099), (768, 517)])
+def test_gather_rows_shapes(P, dim, rows):
+    """gns_gather_rows over tile tails and row widths (16-B chunks per row
+    from 1 to 192), device row count, output stride > dim."""
+    from paper_2106_06150_b200 import _lib
+    N = 5000
+    tab = torch.randn(N, dim, device="cuda")
+    idx = torch.sort(torch.randint(0, N, (rows,), device="cuda", dtype=torch.int32)).values
+    out = torch.full((rows + 3, dim + 4), 7.0, device="cuda")
+    n_dev = torch.tensor([rows], dtype=torch.int32, device="cuda")
+    _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, idx.data_ptr(), n_dev.data_ptr(), rows + 3, dim,
+              out.data_ptr(), out.stride(0), 0, _lib.stream_ptr())
+    assert torch.equal(out[:rows, :dim], tab[idx.long()])
+    assert bool((out[rows:] == 7.0).all()) and bool((out[:, dim:] == 7.0).all())
+
+
 def test_epoch_targets_feistel(P):
     og = O.build_csr(np.random.default_rng(0).integers(0, 5000, size=(20000, 2)), 5000)
     mask = np.random.default_rng(1).random(5000) < 0.3
@@ -326,6 +370,27 @@ def test_spmm_fwd_f64_bit_exact(P, dim):
             c = cat.cpu().numpy()[:ndst]
             assert np.array_equal(c[:, :dim], hr[self_pos])
             assert np.array_equal(c[:, dim:], OM.spmm_mean_fwd(br, hr))
+
+
+@pytest.mark.parametrize("dim", [4, 64, 128, 200])
+def test_spmm_fwd_gather_equals_gather_then_spmm(P, dim):
+    """The fused input-layer kernel (feature table addressed by node id) is
+    bit-identical to features[input_nodes] (model.py:146) followed by the
+    aggregation (model.py:153)."""
+    from paper_2106_06150_b200 import _lib
+    og, g, _, mb, ref = _mb_and_features(P, dim=16)
+    feats = torch.randn(og.num_nodes, dim, device="cuda")
+    for li, (bg, br) in enumerate(zip(mb.blocks, ref.blocks)):
+        nsrc, ndst = len(br.src_nodes), len(br.dst_nodes)
+        h = feats[torch.as_tensor(br.src_nodes, device="cuda").long()].contiguous()
+        a = torch.full((ndst + 5, 2 * dim), 7.0, device="cuda")
+        b = torch.full((ndst + 5, 2 * dim), 9.0, device="cuda")
+        _lib.call("gns_spmm_fwd", 0, h.data_ptr(), dim, dim, 0, bg._c, ndst, ndst + 5, a.data_ptr(), 2 * dim,
+                  _lib.stream_ptr())
+        dst = torch.as_tensor(br.dst_nodes.astype(np.int32), device="cuda")
+        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 5,
+                  b.data_ptr(), 2 * dim, _lib.stream_ptr())
+        assert torch.equal(a, b), li
 
 
 @pytest.mark.parametrize("dim", [2, 8, 64])
