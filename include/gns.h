@@ -141,6 +141,12 @@ GNS_API int gns_graph_launch(void* exec, void* stream);
 GNS_API int gns_graph_exec_destroy(void* exec);
 GNS_API int gns_graph_kernel_priorities(void* graph, int32_t* out_hist, int32_t nbins);
 
+/* Developer knob for A/B measurements of kernel variants ("spmm_narrow":
+ * 1 = row-per-warp shuffle-sorted SpMM for float32 rows of <= 128 floats
+ * (default), 0 = the generic shared-memory kernel).  Not used on the product
+ * path. */
+GNS_API int gns_tune(const char* name, int32_t value);
+
 /* ---- cache engine (cache.py) ------------------------------------------- */
 
 /* degree_probs (cache.py:53-58): out[i] = deg(i) / E in float64. */

@@ -68,6 +68,7 @@ _SIGS = {
     "gns_last_error": (ctypes.c_char_p, []),
     "gns_version": (c_int32, []),
     "gns_record_event_external": (c_int32, [c_void_p, c_void_p]),
+    "gns_tune": (c_int32, [ctypes.c_char_p, c_int32]),
     "gns_graph_instantiate": (c_int32, [c_void_p, c_int32, c_void_p]),
     "gns_graph_launch": (c_int32, [c_void_p, c_void_p]),
     "gns_graph_exec_destroy": (c_int32, [c_void_p]),
@@ -164,6 +165,11 @@ def load(path: str = LIB_PATH):
         fn.argtypes = args
     if path == LIB_PATH:
         _lib = lib
+    # developer A/B knobs: GNS_TUNE="spmm_bwd=0,spmm_narrow=1" (gns_tune)
+    for kv in filter(None, os.environ.get("GNS_TUNE", "").split(",")):
+        k, v = kv.split("=")
+        if lib.gns_tune(k.strip().encode(), int(v)) != GNS_OK:
+            raise ValueError(f"GNS_TUNE: {lib.gns_last_error().decode()}")
     return lib
 
 

@@ -3,6 +3,8 @@
 // (model.py:223-225), softmax cross-entropy (model.py:189-200) and Adam
 // (model.py:229-242).  All HBM-bound; no tensor cores (the GraphSAGE linear
 // layers are cuBLAS GEMMs issued by the Python side).
+#include <string.h>
+
 #include <algorithm>
 
 #include "gns_common.cuh"
@@ -18,51 +20,66 @@ __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
   return r;
 }
 
-// out[i, :] = table[rows[i], :] with 16-byte vectors.  The (row, 16-B chunk)
-// space is flattened and cut into warp tiles of 32*U consecutive chunks: a warp
-// issues all U loads of its tile (U adjacent rows at D=128: the ids are sorted,
-// so the rows are near each other in the table) before any store.  Measured
-// on B200 against grid-strided chunks (scripts/gather_probe2.cu, 285K random
-// rows of 512 B): 48 us vs 58 us; U=2 and 8 resident CTAs/SM is the optimum.
-template <int U>
-__global__ void __launch_bounds__(256) gather_f32x4_kernel(const float* __restrict__ table, int64_t ld_in,
+// out[i, :] = table[rows[i], :] with 16-byte vectors.  A warp owns G
+// consecutive rows per iteration (the ids are sorted, so they are near each
+// other in the table); one coalesced load fetches the G row ids, lane l
+// moves 16-byte chunks l, l+32, ... of each row, and all G*C loads of the
+// iteration are issued before any store.  C column blocks of 32 chunks cover
+// rows up to C*512 bytes (wider rows loop over column blocks).  Measured on
+// B200 (scripts/gather_probe2.cu, 285K random 512-B rows, L2 full of dirty
+// lines): G=2 at 8 resident CTAs/SM = 55 us, a grid-strided flat chunk loop
+// = 60-68 us, cudaMemcpy of the same bytes = 56 us.
+// (register cap: 8 resident CTAs/SM = full occupancy for <= 2 loads in
+// flight per lane; the wider variants trade occupancy for loads in flight)
+template <int G, int C>
+__global__ void __launch_bounds__(256, (G == 2 && C == 1) ? 8 : 4) gather_f32x4_kernel(const float* __restrict__ table, int64_t ld_in,
                                                            const int32_t* __restrict__ rows,
                                                            const int32_t* __restrict__ n_dev, int64_t n_host,
                                                            int dim4, float* __restrict__ out, int64_t ld_out) {
   const int64_t n = n_dev ? n_dev[0] : n_host;
-  const int64_t total = n * dim4;
-  const bool small = total < (int64_t(1) << 32);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t tile_stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * (32 * U);
-  for (int64_t base = warp * (32 * U); base < total; base += tile_stride) {
-    float4 v[U];
-    int64_t orow[U];
-    int oc[U];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (G == 2 && C == 1 && dim4 == 32) {
+    // 512-byte rows (D = 128, the papers100M shape): one chunk per lane
+    for (int64_t r0 = warp * G; r0 < n; r0 += nw * G) {
+      const int32_t myrow = (lane < G && r0 + lane < n) ? __ldg(rows + r0 + lane) : 0;
+      float4 v[G];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t ii = base + u * 32 + lane;
-      orow[u] = -1;
-      if (ii < total) {
-        int64_t r;
-        int c;
-        if (small) {  // 32-bit division (uniform branch)
-          const uint32_t q = (uint32_t)ii / (uint32_t)dim4;
-          r = q;
-          c = (int)((uint32_t)ii - q * (uint32_t)dim4);
-        } else {
-          r = ii / dim4;
-          c = (int)(ii - r * dim4);
+      for (int g = 0; g < G; ++g) {
+        const int32_t src = __shfl_sync(GNS_FULL, myrow, g);
+        if (r0 + g < n) v[g] = ld_stream_f4(reinterpret_cast<const float4*>(table + (int64_t)src * ld_in) + lane);
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (r0 + g < n) reinterpret_cast<float4*>(out + (r0 + g) * ld_out)[lane] = v[g];
+    }
+    return;
+  }
+  for (int64_t r0 = warp * G; r0 < n; r0 += nw * G) {
+    const int32_t myrow = (lane < G && r0 + lane < n) ? __ldg(rows + r0 + lane) : 0;
+    for (int c0 = 0; c0 < dim4; c0 += 32 * C) {
+      float4 v[G][C];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int32_t src = __shfl_sync(GNS_FULL, myrow, g);
+        const float4* rp = reinterpret_cast<const float4*>(table + (int64_t)src * ld_in);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const int ch = c0 + c * 32 + lane;
+          if (r0 + g < n && ch < dim4) v[g][c] = ld_stream_f4(rp + ch);
         }
-        const int32_t src = __ldg(rows + r);
-        v[u] = ld_stream_f4(reinterpret_cast<const float4*>(table + (int64_t)src * ld_in) + c);
-        orow[u] = r;
-        oc[u] = c;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float4* op = reinterpret_cast<float4*>(out + (r0 + g) * ld_out);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const int ch = c0 + c * 32 + lane;
+          if (r0 + g < n && ch < dim4) op[ch] = v[g][c];
+        }
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (orow[u] >= 0) reinterpret_cast<float4*>(out + orow[u] * ld_out)[oc[u]] = v[u];
   }
 }
 
@@ -291,6 +308,113 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
   }
 }
 
+// Narrow rows (float32, D <= 128: one 16-byte chunk per lane) with <= 32
+// edges per dst row — the input layer.  Per warp and dst row: lane i loads
+// edge i, the ranks by source index come from a shuffle count (no shared
+// memory), the self row and up to kNarrowGroup neighbour rows are all in
+// flight at once, then the weighted sum runs in ascending source order (the
+// scipy CSR order, same FMA sequence as spmm_fwd_kernel: bit-identical).
+// Rows with more than 32 edges take the generic per-row path.
+template <bool RELU, bool GATHER, int kNarrowGroup = 4, int kMinBlocks = 4>
+__global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel(const float* __restrict__ h, int64_t ld_h,
+                                                                         int dim, BlockView bv,
+                                                                         float* __restrict__ cat, int64_t ld_cat,
+                                                                         int64_t pad_rows,
+                                                                         const int32_t* __restrict__ edge_node,
+                                                                         const int32_t* __restrict__ dst_ids) {
+  const int32_t* __restrict__ eidx = GATHER ? edge_node : bv.edge_src;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = bv.counts[GNS_CNT_DST];
+  const int64_t tm = (int64_t)(bv.row_scan[n] >> 32);
+  const int dv = dim >> 2;
+  const bool on = lane < dv;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < n; r += nw) {
+    const uint64_t s0 = bv.row_scan[r], s1 = bv.row_scan[r + 1];
+    const int64_t self = GATHER ? (int64_t)dst_ids[r] : (int64_t)bv.self_pos[r];
+    const float norm = (float)max(bv.dst_degree[r], 1);
+    const int64_t cb = (int64_t)(s0 >> 32), ce = (int64_t)(s1 >> 32);
+    const int64_t fb = tm + (int64_t)(s0 & 0xffffffffull), fe = tm + (int64_t)(s1 & 0xffffffffull);
+    const int nc = (int)(ce - cb), L = nc + (int)(fe - fb);
+    float4 xs = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (on) xs = ldv<float4, RELU>(reinterpret_cast<const float4*>(h + self * ld_h) + lane);
+    float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (L <= 32) {
+      int32_t idx = INT32_MAX;
+      float w = 0.f;
+      if (lane < L) {
+        const int64_t e = lane < nc ? cb + lane : fb + (lane - nc);
+        idx = eidx[e];
+        w = (float)bv.edge_weight[e];
+      }
+      // rank among the row's edges by source index (distinct within a row)
+      int rank = 0;
+      for (int j = 0; j < L; ++j) rank += __shfl_sync(GNS_FULL, idx, j) < idx;
+      // lane u fetches the edge of rank u
+      int src = 0;
+      for (int u = 0; u < L; ++u) {
+        const unsigned m = __ballot_sync(GNS_FULL, lane < L && rank == u);
+        if (lane == u) src = __ffs(m) - 1;
+      }
+      const int32_t sidx = __shfl_sync(GNS_FULL, idx, src);
+      const float sw = __shfl_sync(GNS_FULL, w, src);
+      for (int t = 0; t < L; t += kNarrowGroup) {
+        float4 x[kNarrowGroup];
+#pragma unroll
+        for (int u = 0; u < kNarrowGroup; ++u) {
+          const int32_t iu = __shfl_sync(GNS_FULL, sidx, (t + u) & 31);
+          if (on && t + u < L) x[u] = ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)iu * ld_h) + lane);
+        }
+#pragma unroll
+        for (int u = 0; u < kNarrowGroup; ++u) {
+          const float wu = __shfl_sync(GNS_FULL, sw, (t + u) & 31);
+          if (on && t + u < L) vfma<true>(acc, wu, x[u]);
+        }
+      }
+    } else {
+      // > 32 edges: sort through shared memory in 32-edge rounds is not
+      // worth a second path — rank each edge against all others directly
+      for (int t = 0; t < L; ++t) {
+        // the t-th smallest source index among the row's edges
+        int32_t best = INT32_MAX;
+        float bw = 0.f;
+        for (int i = lane; i < L; i += 32) {
+          const int64_t e = i < nc ? cb + i : fb + (i - nc);
+          const int32_t v = eidx[e];
+          int rk = 0;
+          for (int j = 0; j < L; ++j) {
+            const int64_t ej = j < nc ? cb + j : fb + (j - nc);
+            rk += eidx[ej] < v;
+          }
+          if (rk == t) {
+            best = v;
+            bw = (float)bv.edge_weight[e];
+          }
+        }
+        const unsigned m = __ballot_sync(GNS_FULL, best != INT32_MAX);
+        const int sl = __ffs(m) - 1;
+        const int32_t iu = __shfl_sync(GNS_FULL, best, sl);
+        const float wu = __shfl_sync(GNS_FULL, bw, sl);
+        if (on) vfma<true>(acc, wu, ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)iu * ld_h) + lane));
+      }
+    }
+    if (on) {
+      crow[lane] = xs;
+      crow[dv + lane] = vdiv(acc, norm);
+    }
+  }
+  for (int64_t r = n + gw; r < pad_rows; r += nw) {
+    float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
+    for (int c = lane; c < 2 * dv; c += 32) crow[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// experiment knobs (gns_tune)
+static int g_tune_narrow = 1;  // narrow-row forward SpMM variant (0 = generic)
+static int g_tune_bwd = 1;     // short-chain float32 backward (0 = generic)
+
 // ---- SpMM backward -------------------------------------------------------------
 __global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of) {
   const int64_t ne = bv.counts[GNS_CNT_EDGES], nd = bv.counts[GNS_CNT_DST];
@@ -497,6 +621,125 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
   }
 }
 
+// float32 backward with short dependency chains (same rows per warp, same
+// accumulation order and the same block partials as spmm_bwd_kernel, so the
+// results are bit-identical).  Per src row: the transposed row bounds and the
+// self index are loaded first; the self row of dcat and the relu mask row are
+// issued right away (they do not depend on the edges); the row's edge keys,
+// weights and dst degrees are fetched lane-parallel (32 at a time) and the
+// dcat rows of G edges are in flight together.  Requires dim <= 128 * CH.
+template <int CH, int G, int MINB>
+__global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_f32_kernel(
+    const float* __restrict__ dcat, int64_t ld_dcat, int dim, BlockView bv, const int32_t* __restrict__ tptr,
+    const uint64_t* __restrict__ tkeys, const int32_t* __restrict__ self_of, float* __restrict__ dh, int64_t ld_dh,
+    int64_t pad_rows, const float* __restrict__ zmask, float* __restrict__ colpart) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = bv.counts[GNS_CNT_SRC];
+  const int dv = dim >> 2;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  float colacc[CH][4];
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) colacc[j][q] = 0.f;
+  for (int64_t s = gw; s < n; s += nw) {
+    const int b = tptr[s], e_end = tptr[s + 1];
+    const int sd = self_of[s];
+    float4 sv[CH], zv[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int c = lane + 32 * j;
+      sv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      zv[j] = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (c < dv) {
+        if (sd >= 0) sv[j] = reinterpret_cast<const float4*>(dcat + (int64_t)sd * ld_dcat)[c];
+        if (zmask) zv[j] = reinterpret_cast<const float4*>(zmask + s * ld_dh)[c];
+      }
+    }
+    float acc[CH][4];
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
+    for (int t0 = b; t0 < e_end; t0 += 32) {
+      const int m = min(32, e_end - t0);
+      int32_t d = 0;
+      float wn = 0.f;
+      if (lane < m) {
+        const uint64_t key = tkeys[t0 + lane];
+        d = (int32_t)(key >> 32);
+        const int32_t e = (int32_t)(key & 0xffffffffu);
+        wn = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
+      }
+      for (int u0 = 0; u0 < m; u0 += G) {
+        float4 g[G][CH];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const int32_t du = __shfl_sync(GNS_FULL, d, (u0 + u) & 31);
+          const float4* grow = reinterpret_cast<const float4*>(dcat + (int64_t)du * ld_dcat + dim);
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int c = lane + 32 * j;
+            if (u0 + u < m && c < dv) g[u][j] = grow[c];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const float wu = __shfl_sync(GNS_FULL, wn, (u0 + u) & 31);
+          if (u0 + u < m) {
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+              acc[j][0] = fmaf(wu, g[u][j].x, acc[j][0]);
+              acc[j][1] = fmaf(wu, g[u][j].y, acc[j][1]);
+              acc[j][2] = fmaf(wu, g[u][j].z, acc[j][2]);
+              acc[j][3] = fmaf(wu, g[u][j].w, acc[j][3]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int c = lane + 32 * j;
+      if (c >= dv) continue;
+      float4 out;
+      if (sd >= 0) {
+        acc[j][0] = acc[j][0] + sv[j].x;
+        acc[j][1] = acc[j][1] + sv[j].y;
+        acc[j][2] = acc[j][2] + sv[j].z;
+        acc[j][3] = acc[j][3] + sv[j].w;
+      }
+      out.x = zv[j].x > 0.f ? acc[j][0] : 0.f;
+      out.y = zv[j].y > 0.f ? acc[j][1] : 0.f;
+      out.z = zv[j].z > 0.f ? acc[j][2] : 0.f;
+      out.w = zv[j].w > 0.f ? acc[j][3] : 0.f;
+      colacc[j][0] += out.x;
+      colacc[j][1] += out.y;
+      colacc[j][2] += out.z;
+      colacc[j][3] += out.w;
+      reinterpret_cast<float4*>(dh + s * ld_dh)[c] = out;
+    }
+  }
+  for (int64_t s = n + gw; s < pad_rows; s += nw)
+    for (int c = lane; c < dv; c += 32) reinterpret_cast<float4*>(dh + s * ld_dh)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (colpart) {
+    __shared__ float red[kSpmmBlock / 32][32 * CH * 4];
+    const int wib = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[wib][(lane + 32 * j) * 4 + q] = colacc[j][q];
+    __syncthreads();
+    for (int col = threadIdx.x; col < dim; col += blockDim.x) {
+      float t = 0;
+#pragma unroll
+      for (int w = 0; w < kSpmmBlock / 32; ++w) t += red[w][col];
+      colpart[(int64_t)blockIdx.x * dim + col] = t;
+    }
+  }
+}
+
 // dz = relu'(z) * dh (model.py:218) fused with the bias gradient db = sum_r dz
 // (model.py:220): per-block column partials, then a fixed-order reduction.
 template <typename T>
@@ -661,11 +904,21 @@ int gns_gather_rows(const void* table, int64_t ld_in, int32_t dtype_in, const in
     bool vec = (dim % 4 == 0) && (ld_in % 4 == 0) && (ld_out % 4 == 0) && ((uintptr_t)table % 16 == 0) &&
                ((uintptr_t)out % 16 == 0);
     if (vec) {
-      // 8 resident 256-thread CTAs per SM; tiles of 64 chunks per warp
-      long long want = (max_rows * (dim / 4) + 256 * 2 - 1) / (256 * 2);
-      int grid = grid_for(want, (long long)sms * 8);
-      gather_f32x4_kernel<2><<<grid, 256, 0, stream>>>((const float*)table, ld_in, rows, n_rows_dev, max_rows,
-                                                       dim / 4, (float*)out, ld_out);
+      // 8 resident 256-thread CTAs per SM; G rows x C column blocks per warp
+      const int dim4 = dim / 4;
+      const int G = dim4 <= 8 ? 8 : dim4 <= 16 ? 4 : dim4 <= 32 ? 2 : 1;
+      const long long want = ((max_rows + G - 1) / G * 32 + 255) / 256;
+      const int grid = grid_for(want, (long long)sms * 8);
+#define GNS_GATHER(G_, C_)                                                                                     \
+  gather_f32x4_kernel<G_, C_><<<grid, 256, 0, stream>>>((const float*)table, ld_in, rows, n_rows_dev, max_rows, \
+                                                        dim4, (float*)out, ld_out)
+      if (dim4 <= 8) GNS_GATHER(8, 1);
+      else if (dim4 <= 16) GNS_GATHER(4, 1);
+      else if (dim4 <= 32) GNS_GATHER(2, 1);
+      else if (dim4 <= 64) GNS_GATHER(1, 2);
+      else if (dim4 <= 128) GNS_GATHER(1, 4);
+      else GNS_GATHER(1, 8);
+#undef GNS_GATHER
       return check_launch("gather_f32x4");
     }
     gather_scalar_kernel<float, float><<<sms * 16, 256, 0, stream>>>((const float*)table, ld_in, rows, n_rows_dev,
@@ -714,6 +967,19 @@ int gns_cache_refresh_rows(const float* host_table, int64_t ld, const int32_t* i
   return check_launch("cache_refresh_rows");
 }
 
+int gns_tune(const char* name, int32_t value) {
+  if (!strcmp(name, "spmm_narrow")) {
+    g_tune_narrow = value;
+    return GNS_OK;
+  }
+  if (!strcmp(name, "spmm_bwd")) {
+    g_tune_bwd = value;
+    return GNS_OK;
+  }
+  set_error("unknown tuning knob %s", name);
+  return GNS_EINVAL;
+}
+
 int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const gns_block_t* block,
                         const int32_t* dst_ids, int64_t max_dst, int64_t pad_rows, float* cat, int64_t ld_cat,
                         void* stream_) {
@@ -728,6 +994,16 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
   int grid = grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)sms * 8);
   BlockView bv = view_of(block);
   const int dv = dim / 4;
+  if (dv <= 32 && g_tune_narrow == 1) {
+    spmm_fwd_narrow_kernel<false, true><<<grid, kSpmmBlock, 0, stream>>>(table, ld_table, dim, bv, cat, ld_cat,
+                                                                        pad_rows, block->edge_node, dst_ids);
+    return check_launch("spmm_fwd_gather");
+  }
+  if (dv <= 32 && g_tune_narrow == 2) {
+    spmm_fwd_narrow_kernel<false, true, 8, 3><<<grid, kSpmmBlock, 0, stream>>>(
+        table, ld_table, dim, bv, cat, ld_cat, pad_rows, block->edge_node, dst_ids);
+    return check_launch("spmm_fwd_gather");
+  }
 #define GNS_FWDG(CH)                                                                                          \
   spmm_fwd_kernel<float, CH, false, true><<<grid, kSpmmBlock, 0, stream>>>(table, ld_table, dim, bv, cat, ld_cat, \
                                                                           pad_rows, block->edge_node, dst_ids)
@@ -755,7 +1031,16 @@ int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_
       return GNS_EINVAL;
     }
     const int dv = dim / 4;
-    if (dv <= 32) { if (relu) GNS_FWD(float, 1, true); else GNS_FWD(float, 1, false); }
+    if (dv <= 32 && g_tune_narrow) {
+      if (relu)
+        spmm_fwd_narrow_kernel<true, false><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv,
+                                                                            (float*)cat, ld_cat, pad_rows, nullptr,
+                                                                            nullptr);
+      else
+        spmm_fwd_narrow_kernel<false, false><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv,
+                                                                             (float*)cat, ld_cat, pad_rows, nullptr,
+                                                                             nullptr);
+    } else if (dv <= 32) { if (relu) GNS_FWD(float, 1, true); else GNS_FWD(float, 1, false); }
     else if (dv <= 64) { if (relu) GNS_FWD(float, 2, true); else GNS_FWD(float, 2, false); }
     else { if (relu) GNS_FWD(float, 4, true); else GNS_FWD(float, 4, false); }
   } else {
@@ -837,7 +1122,15 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
   spmm_bwd_kernel<T, CH><<<g2, kSpmmBlock, 0, stream>>>((const T*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys, \
                                                         w.self_of, (T*)dh, ld_dh, pad_rows, (const T*)z_mask,  \
                                                         db ? (T*)w.colpart : nullptr)
-  if (dtype == 0) {
+#define GNS_BWDF(CH, G, MINB)                                                                                    \
+  spmm_bwd_f32_kernel<CH, G, MINB><<<g2, kSpmmBlock, 0, stream>>>((const float*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys, \
+                                                            w.self_of, (float*)dh, ld_dh, pad_rows,                 \
+                                                            (const float*)z_mask, db ? (float*)w.colpart : nullptr)
+  if (dtype == 0 && g_tune_bwd) {
+    if (dv <= 32) GNS_BWDF(1, 4, 4);
+    else if (dv <= 64) GNS_BWDF(2, 2, 3);
+    else GNS_BWDF(4, 1, 2);
+  } else if (dtype == 0) {
     if (dv <= 32) GNS_BWD(float, 1);
     else if (dv <= 64) GNS_BWD(float, 2);
     else GNS_BWD(float, 4);
@@ -847,6 +1140,7 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
     else GNS_BWD(double, 4);
   }
 #undef GNS_BWD
+#undef GNS_BWDF
   GNS_TRY(check_launch("spmm_bwd"));
   if (db) {
     if (dtype == 0)

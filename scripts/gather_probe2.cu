@@ -1,13 +1,22 @@
 // Gather-kernel variants, round 2: load cache hints, unroll depth, grid size,
 // and a warp-per-row-group layout, on a papers100M-sized table (111M x 128
 // fp32), 285K sorted random rows (the bench's per-step input-node count).
-//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o /tmp/gp2 scripts/gather_probe2.cu && /tmp/gp2
+// argv[2] = "dirty": flush L2 with a 256 MB memset (L2 full of dirty lines
+// when the gather starts, as inside a training step); default: read-only flush.
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o /tmp/gp2 scripts/gather_probe2.cu && /tmp/gp2 [n] [dirty]
+// (add -DWITH_LIBGNS -Lpaper_2106_06150_b200 -lgns -Xlinker -rpath=$PWD/paper_2106_06150_b200 to also time
+// the library's gns_gather_rows on the same buffers)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
+
+#ifdef WITH_LIBGNS
+#include "../include/gns.h"
+#endif
 #include <random>
 #include <vector>
 
@@ -72,10 +81,11 @@ __global__ void g_flat(const float* __restrict__ t, const int* __restrict__ rows
 
 // warp-contiguous: each warp owns G consecutive rows per iteration (dim4 == 32:
 // one lane per 16-B chunk), loads all G rows, then stores them.
-template <int G, int LM>
+template <int G, int LM, int SMODE = 0>
 __global__ void g_warp(const float* __restrict__ t, const int* __restrict__ rows, int64_t n, float* __restrict__ out) {
-  uint64_t pf = 0;
+  uint64_t pf = 0, pl = 0;
   if (LM == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  if (SMODE == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -89,12 +99,13 @@ __global__ void g_warp(const float* __restrict__ t, const int* __restrict__ rows
     }
 #pragma unroll
     for (int g = 0; g < G; ++g)
-      if (r0 + g < n) reinterpret_cast<float4*>(out + (r0 + g) * 128)[lane] = v[g];
+      if (r0 + g < n) st<SMODE>(reinterpret_cast<float4*>(out + (r0 + g) * 128) + lane, v[g], pl);
   }
 }
 
 int main(int argc, char** argv) {
   const int64_t N = 111000000, D = 128, n = argc > 1 ? atol(argv[1]) : 285000;
+  const bool dirty = argc > 2 && !strcmp(argv[2], "dirty");
   const int dim4 = D / 4;
   float* t;
   CK(cudaMalloc(&t, N * D * 4));
@@ -123,9 +134,13 @@ int main(int argc, char** argv) {
   auto run = [&](const char* name, auto launch) {
     float best = 1e9, tot = 0;
     for (int it = 0; it < 22; ++it) {
-      // evict the table/output from L2 without leaving dirty lines: read-only flush
-      CK(cudaMemcpyAsync(scratch, flush, 256 << 20, cudaMemcpyDeviceToDevice));
-      CK(cudaMemcpyAsync(flush, scratch, 8 << 20, cudaMemcpyDeviceToDevice));
+      if (dirty) {
+        CK(cudaMemsetAsync(flush, it, 256 << 20));
+      } else {
+        // evict the table/output from L2 without leaving dirty lines: read-only flush
+        CK(cudaMemcpyAsync(scratch, flush, 256 << 20, cudaMemcpyDeviceToDevice));
+        CK(cudaMemcpyAsync(flush, scratch, 8 << 20, cudaMemcpyDeviceToDevice));
+      }
       cudaEventRecord(a);
       launch();
       cudaEventRecord(b);
@@ -144,33 +159,28 @@ int main(int argc, char** argv) {
   snprintf(nm, 96, "flat U%d ld%d st%d grid=%dxSM blk%d", U, LM, SMODE, GM, BS);            \
   run(nm, [&] { g_flat<U, LM, SMODE><<<sms * GM, BS>>>(t, rows, m, dim4, out); });
   FLAT(4, 0, 0, 16, 256)
-  FLAT(4, 0, 0, 8, 256)
-  FLAT(2, 0, 0, 16, 256)
   FLAT(2, 0, 0, 8, 256)
-  FLAT(3, 0, 0, 16, 256)
-  FLAT(1, 0, 0, 16, 256)
-  FLAT(1, 0, 0, 8, 256)
-  FLAT(4, 1, 0, 16, 256)
-  FLAT(2, 1, 0, 16, 256)
-  FLAT(4, 2, 0, 16, 256)
   FLAT(4, 0, 1, 16, 256)
-  FLAT(4, 0, 2, 16, 256)
   FLAT(4, 2, 1, 16, 256)
-  FLAT(4, 0, 0, 4, 512)
   FLAT(4, 0, 0, 6, 256)
-  FLAT(4, 0, 0, 12, 256)
-  FLAT(4, 0, 0, 24, 256)
   FLAT(2, 0, 0, 32, 128)
-#define WARP(G, LM, GM)                                                             \
-  snprintf(nm, 96, "warp G%d ld%d grid=%dxSM", G, LM, GM);                         \
-  run(nm, [&] { g_warp<G, LM><<<sms * GM, 256>>>(t, rows, m, out); });
-  WARP(2, 0, 8)
-  WARP(4, 0, 8)
-  WARP(4, 0, 4)
-  WARP(8, 0, 4)
-  WARP(8, 0, 2)
-  WARP(4, 1, 8)
-  WARP(4, 2, 8)
+#define WARP(G, LM, GM, SMODE)                                                      \
+  snprintf(nm, 96, "warp G%d ld%d st%d grid=%dxSM", G, LM, SMODE, GM);             \
+  run(nm, [&] { g_warp<G, LM, SMODE><<<sms * GM, 256>>>(t, rows, m, out); });
+  WARP(1, 0, 8, 0)
+  WARP(2, 0, 8, 0)
+  WARP(2, 0, 4, 0)
+  WARP(2, 0, 16, 0)
+  WARP(4, 0, 8, 0)
+  WARP(2, 0, 8, 1)
+  WARP(2, 2, 8, 1)
+  WARP(2, 1, 8, 0)
+  WARP(2, 2, 8, 0)
+  WARP(2, 0, 8, 2)
+  WARP(4, 0, 4, 1)
+#ifdef WITH_LIBGNS
+  run("libgns gns_gather_rows", [&] { gns_gather_rows(t, D, 0, rows, nullptr, m, (int)D, out, D, 0, nullptr); });
+#endif
   run("cudaMemcpyAsync D2D (ref)", [&] { cudaMemcpyAsync(out, t, m * D * 4, cudaMemcpyDeviceToDevice); });
   return 0;
 }

@@ -393,6 +393,44 @@ def test_spmm_fwd_gather_equals_gather_then_spmm(P, dim):
         assert torch.equal(a, b), li
 
 
+@pytest.mark.parametrize("dim", [16, 64, 128])
+def test_spmm_fwd_narrow_equals_generic(P, dim):
+    """The narrow-row kernel (shuffle sort, <= 32 edges per row; > 32 edges
+    take its fallback) is bit-identical to the generic SpMM, with and without
+    relu-on-load, fused gather or not."""
+    from paper_2106_06150_b200 import _lib
+    og = _hub_graph(4000, 21)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy="NS", fanouts=(40, 3), batch_size=200, seed=5)
+    targets = np.random.default_rng(5).choice(og.num_nodes, 200, replace=False)
+    mb = P.build_minibatch(g, None, targets, cfg, P.BatchRng(5, 0, 0))
+    feats = torch.randn(og.num_nodes, dim, device="cuda")
+    try:
+        for bg in mb.blocks:
+            ns, nd = bg.src_nodes.numel(), bg.dst_nodes.numel()
+            h = torch.randn(ns, dim, device="cuda")
+            dst = bg.dst_nodes.to(torch.int32).contiguous()
+            outs = {}
+            for v in (0, 1):
+                _lib.call("gns_tune", b"spmm_narrow", v)
+                for relu in (0, 1):
+                    o = torch.full((nd + 3, 2 * dim), 5.0, device="cuda")
+                    _lib.call("gns_spmm_fwd", 0, h.data_ptr(), dim, dim, relu, bg._c, nd, nd + 3, o.data_ptr(),
+                              2 * dim, _lib.stream_ptr())
+                    outs[(v, relu)] = o
+                o = torch.full((nd + 3, 2 * dim), 5.0, device="cuda")
+                _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), nd, nd + 3,
+                          o.data_ptr(), 2 * dim, _lib.stream_ptr())
+                outs[(v, "g")] = o
+            for key in ((0, 1), "g"):
+                k0 = (0, key) if key == "g" else (0, key[1])
+                k1 = (1, key) if key == "g" else (1, key[1])
+                assert torch.equal(outs[k0], outs[k1]), key
+            assert torch.equal(outs[(0, 0)], outs[(1, 0)])
+    finally:
+        _lib.call("gns_tune", b"spmm_narrow", 1)
+
+
 @pytest.mark.parametrize("dim", [2, 8, 64])
 def test_spmm_bwd_f64_bit_exact(P, dim):
     from paper_2106_06150_b200 import _lib
@@ -424,6 +462,34 @@ def test_spmm_bwd_f64_bit_exact(P, dim):
             _lib.call("gns_spmm_bwd", 0, dt32.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0, None,
                       None, dh32.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
             np.testing.assert_allclose(dh32.cpu().numpy(), expect, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("dim", [16, 64, 256, 512])
+def test_spmm_bwd_f32_variants_identical(P, dim):
+    """The short-chain float32 backward (default) equals the generic kernel
+    bit for bit: dh, relu' mask, zero padding and the bias gradient."""
+    from paper_2106_06150_b200 import _lib
+    og, g, feats, mb, ref = _mb_and_features(P, dim=16)
+    ws = _lib.workspace(1 << 24, "cuda")
+    try:
+        for li, (bg, br) in enumerate(zip(mb.blocks, ref.blocks)):
+            nsrc, ndst = len(br.src_nodes), len(br.dst_nodes)
+            gen = torch.Generator(device="cuda").manual_seed(li)
+            dt = torch.randn((ndst, 2 * dim), device="cuda", generator=gen)
+            zt = torch.randn((nsrc, dim), device="cuda", generator=gen)
+            res = []
+            for v in (0, 1):
+                _lib.call("gns_tune", b"spmm_bwd", v)
+                dh = torch.full((nsrc + 5, dim), 3.0, device="cuda")
+                db = torch.empty(dim, device="cuda")
+                _lib.call("gns_spmm_bwd", 0, dt.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, nsrc + 5,
+                          zt.data_ptr(), db.data_ptr(), dh.data_ptr(), dim, ws.data_ptr(), ws.numel(),
+                          _lib.stream_ptr())
+                res.append((dh, db))
+            assert torch.equal(res[0][0], res[1][0]), li
+            assert torch.equal(res[0][1], res[1][1]), li
+    finally:
+        _lib.call("gns_tune", b"spmm_bwd", 1)
 
 
 def test_full_batch_equivalence(P):
