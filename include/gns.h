@@ -59,8 +59,9 @@ extern "C" {
 #define GNS_CNT_HUBS 4     /* (row, phase) items for the CTA-per-item sampler */
 #define GNS_CNT_ERR 5      /* GNS_ERRBIT_* flags                             */
 #define GNS_CNT_WARPROWS 6 /* (row, phase) items for the warp-per-item sampler  */
-#define GNS_CNT_THREADROWS 7 /* (row, phase) items for the thread-per-item sampler */
-#define GNS_CNT_N 8
+#define GNS_CNT_THREADROWS 7 /* (row, phase) items for the thread-per-item sorting-network sampler */
+#define GNS_CNT_STREAMROWS 8 /* (row, phase) items for the thread-per-item streaming top-k sampler */
+#define GNS_CNT_N 16
 
 /* CSR graph (graph.py:52-104): indptr int64[N+1], indices int32[E]. */
 typedef struct gns_graph {
@@ -107,8 +108,9 @@ typedef struct gns_block {
   uint64_t* row_scan;      /* exclusive scan, packed (cached_prefix<<32 | fill_prefix); [n] = totals */
   int32_t* dst_degree;     /* deg(dst) (sampling.py:149)                              */
   int32_t* self_pos;       /* searchsorted(src_nodes, dst_nodes) (model.py:137)       */
-  int32_t* hub_rows;       /* (row<<1|phase) work lists, capacity 4*max_dst: thread tier in
-                              [0, 2*max_dst), warp tier from 2*max_dst up, CTA tier from 4*max_dst-1 down */
+  int32_t* hub_rows;       /* (row<<1|phase) work lists, capacity 6*max_dst: sorting-network
+                              thread tier in [0, 2*max_dst), streaming thread tier in [2*max_dst,
+                              4*max_dst), warp tier from 4*max_dst up, CTA tier from 6*max_dst-1 down */
   /* per edge, capacity max_edges; order = cached edges then fill edges, each by (dst row, key) */
   int32_t* edge_node;      /* global id of the sampled neighbour                       */
   int32_t* edge_src;       /* relabelled: index into src_nodes (sampling.py:145)       */

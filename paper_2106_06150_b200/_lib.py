@@ -26,7 +26,8 @@ ERRBIT_ZEROPROB = 1
 ERRBIT_CAPACITY = 2
 ERRBIT_ZEROQ = 4
 
-CNT_DST, CNT_EDGES, CNT_CACHED, CNT_SRC, CNT_HUBS, CNT_ERR, CNT_N = 0, 1, 2, 3, 4, 5, 8
+CNT_DST, CNT_EDGES, CNT_CACHED, CNT_SRC, CNT_HUBS, CNT_ERR, CNT_N = 0, 1, 2, 3, 4, 5, 16
+CNT_WARPROWS, CNT_THREADROWS, CNT_STREAMROWS = 6, 7, 8
 
 
 class GraphFormatError(ValueError):
@@ -198,7 +199,7 @@ def check(rc: int, what: str = ""):
 # how many of OUR kernels ran inside a timed region
 KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_random_walk_probs": 9, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
-    "gns_cached_csr_fill": 1, "gns_estimate_edge_inclusion": 0, "gns_sample_layer": 8, "gns_relabel": 4, "gns_unique_sorted": 3,
+    "gns_cached_csr_fill": 1, "gns_estimate_edge_inclusion": 0, "gns_sample_layer": 9, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
     "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2,
     "gns_adam_dev": 2,

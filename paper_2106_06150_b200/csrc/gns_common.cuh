@@ -49,6 +49,9 @@ struct Fork {
   cudaEvent_t ev_fork, ev_join;
 };
 int fork_begin(cudaStream_t s, Fork* f);  // aux waits for everything issued on s so far
+}  // namespace gns
+extern "C" int gns_sample_tune(const char* name, int32_t value);  // gns_tune's sampler knobs (internal)
+namespace gns {
 int fork_join(cudaStream_t s, const Fork& f);  // s waits for everything issued on aux
 
 static inline unsigned div_up(long long a, long long b) { return (unsigned)((a + b - 1) / b); }

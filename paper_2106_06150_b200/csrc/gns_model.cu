@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel
 
 // experiment knobs (gns_tune)
 static int g_tune_narrow = 1;  // narrow-row forward SpMM variant (0 = generic)
-static int g_tune_bwd = 1;     // short-chain float32 backward (0 = generic)
+static int g_tune_bwd = 0;     // 1 = short-chain float32 backward (slower on B200: occupancy), 0 = generic
 
 // ---- SpMM backward -------------------------------------------------------------
 __global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of) {
@@ -976,7 +976,8 @@ int gns_tune(const char* name, int32_t value) {
     g_tune_bwd = value;
     return GNS_OK;
   }
-  set_error("unknown tuning knob %s", name);
+  if (gns_sample_tune(name, value) == GNS_OK) return GNS_OK;
+  set_error("unknown tuning knob %s (or value %d out of range)", name, value);
   return GNS_EINVAL;
 }
 

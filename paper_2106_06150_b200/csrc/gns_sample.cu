@@ -20,6 +20,8 @@
 // seeds and sampled neighbours, a single-pass scan over the bitmap words emits
 // the sorted unique src set and per-word ranks, and edge_src = word rank +
 // popc(prefix bits).  The bits are cleared by walking src_nodes.
+#include <string.h>
+
 #include <algorithm>
 
 #include "gns_common.cuh"
@@ -30,6 +32,8 @@ constexpr int kSampBlock = 256;
 constexpr int kWarpCap = 256;
 constexpr int kHubLen = 2048;
 constexpr int kThreadLen = 16;    // rows scanning <= 16 positions: one thread per row, register sort
+constexpr int kStreamK = 8;       // streaming top-k tier: take <= 8 and <= stream_len positions
+static int g_stream_len = 32;     // (gns_tune "stream_len", <= 2047)
 constexpr int kHubBlock = 512;
 constexpr int kHubCap = 512;
 constexpr int kMaxFanout = 128;
@@ -54,6 +58,7 @@ struct LayerArgs {
   const gns_step_t* step_dev;
   uint32_t* dbits;  // dedup bitmap (bit v of word v>>5); NULL = no fused marking
   uint32_t* dsum;   // summary bitmap (bit w of word w>>5 set iff dbits[w] != 0)
+  int stream_len;   // rows up to this many positions with take <= kStreamK: streaming tier
   gns_block_t b;
 };
 
@@ -66,29 +71,61 @@ __device__ __forceinline__ void mark_node(uint32_t* __restrict__ bits, uint32_t*
   if (old == 0u) atomicOr(sum + (w >> 5), 1u << (w & 31));
 }
 
-// Append to a global list with one atomic per warp: returns the slot of the
-// calling lane if pred, else -1 (all active lanes must call it).
-__device__ __forceinline__ int warp_append(int32_t* ctr, bool pred) {
-  const unsigned act = __activemask();
-  const unsigned m = __ballot_sync(act, pred);
-  if (m == 0u) return -1;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(m) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(ctr, __popc(m));
-  base = __shfl_sync(act, base, leader);
-  return pred ? base + __popc(m & ((1u << lane) - 1u)) : -1;
+// Lists of (row, phase) work items per tier, packed in hub_rows[4*max_dst]:
+// thread items from 0 up, warp items from 2*max_dst up, hub items from
+// 4*max_dst-1 down; the counters are counts[GNS_CNT_THREADROWS/WARPROWS/HUBS].
+// Tiers: 0 = thread + sorting network, 1 = warp, 2 = CTA (hub), 3 = thread +
+// streaming top-k.
+constexpr int kTiers = 4;
+__device__ __forceinline__ int32_t* tier_counter(int32_t* counts, int tier) {
+  return counts + (tier == 0 ? GNS_CNT_THREADROWS : tier == 1 ? GNS_CNT_WARPROWS
+                   : tier == 2 ? GNS_CNT_HUBS : GNS_CNT_STREAMROWS);
+}
+__device__ __forceinline__ int64_t tier_slot(int64_t max_dst, int tier, int h) {
+  return tier == 0 ? h : tier == 3 ? 2 * max_dst + h : tier == 1 ? 4 * max_dst + h : 6 * max_dst - 1 - h;
 }
 
-// per-batch Philox key from device memory (CUDA-graph replay) when given
-__device__ __forceinline__ LayerArgs resolve_rng(const LayerArgs& in) {
-  LayerArgs a = in;
-  if (a.step_dev) {
-    a.seed = a.step_dev->seed;
-    a.epoch = a.step_dev->epoch;
-    a.batch = a.step_dev->batch;
+// Append each active lane's phase-0 item (tier t0, -1 = none) and phase-1
+// item (tier t1) to its tier list; returns the list positions.  One atomic
+// per tier and warp, issued by lanes 0..kTiers-1 together.
+__device__ __forceinline__ void warp_append_tiers(int32_t* counts, int t0, int t1, int& h0, int& h1) {
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned m0[kTiers], m1[kTiers];
+#pragma unroll
+  for (int t = 0; t < kTiers; ++t) {
+    m0[t] = __ballot_sync(act, t0 == t);
+    m1[t] = __ballot_sync(act, t1 == t);
   }
-  return a;
+  // lane t (if active) reserves the slots of tier t; otherwise the lowest
+  // active lane does it
+  const int first = __ffs(act) - 1;
+  int base[kTiers] = {0, 0, 0, 0};
+#pragma unroll
+  for (int t = 0; t < kTiers; ++t) {   // the atomics are independent: all in flight
+    const int cnt = __popc(m0[t]) + __popc(m1[t]);
+    const int owner = ((act >> t) & 1u) ? t : first;
+    if (lane == owner && cnt) base[t] = atomicAdd(tier_counter(counts, t), cnt);
+  }
+#pragma unroll
+  for (int t = 0; t < kTiers; ++t) {
+    const int owner = ((act >> t) & 1u) ? t : first;
+    const int bt = __shfl_sync(act, base[t], owner);
+    if (t0 == t) h0 = bt + __popc(m0[t] & lt);
+    if (t1 == t) h1 = bt + __popc(m0[t]) + __popc(m1[t] & lt);
+  }
+}
+
+// Per-batch Philox key words: from the device gns_step_t when given (CUDA
+// graph replay), else the launch arguments.  Kernels take LayerArgs as a
+// __grid_constant__ parameter and keep only these three words per thread.
+struct Rng3 {
+  uint32_t seed, epoch, batch;
+};
+__device__ __forceinline__ Rng3 batch_rng(const LayerArgs& a) {
+  if (a.step_dev) return {a.step_dev->seed, a.step_dev->epoch, a.step_dev->batch};
+  return {a.seed, a.epoch, a.batch};
 }
 
 struct RowInfo {
@@ -115,9 +152,12 @@ __device__ __forceinline__ RowInfo row_info(const LayerArgs& a, int64_t r) {
   return ri;
 }
 
-// Work item = (row, phase); tier by the positions the phase scans:
-// 0 = thread per item (<= 16), 1 = warp per item (<= kHubLen), 2 = CTA (hub)
-__device__ __forceinline__ int phase_tier(int len) {
+// Work item = (row, phase); tier by the positions the phase scans and the
+// selections it makes: 3 = thread per item, streaming top-k (take <= 8,
+// <= 64 positions), 0 = thread per item, sorting network (<= 16 positions),
+// 1 = warp per item (<= kHubLen), 2 = CTA per item (hub)
+__device__ __forceinline__ int phase_tier(int len, int take, int stream_len) {
+  if (take <= kStreamK && len <= stream_len) return 3;
   if (len > kHubLen) return 2;
   if (len > kThreadLen) return 1;
   return 0;
@@ -135,7 +175,8 @@ __device__ __forceinline__ unsigned long long row_counts(const LayerArgs& a, lon
 
 constexpr int kCntBlock = 256, kCntItems = 4;
 
-__global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(LayerArgs a, unsigned long long* tile_sums) {
+__global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __grid_constant__ LayerArgs a,
+                                                                       unsigned long long* tile_sums) {
   const long long n = a.n_dev[0];
   // the per-row value is stashed in row_scan[r] for the apply pass
   scan2_reduce<kCntBlock, kCntItems>(
@@ -148,7 +189,8 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(LayerArgs
       tile_sums);
 }
 
-__global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(LayerArgs a, const unsigned long long* tile_sums) {
+__global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(const __grid_constant__ LayerArgs a,
+                                                                      const unsigned long long* tile_sums) {
   const long long n = a.n_dev[0];
   scan2_apply<kCntBlock, kCntItems>(
       n, [&](long long r) { return (unsigned long long)a.b.row_scan[r]; },
@@ -157,25 +199,16 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(LayerArgs 
         a.b.row_scan[r] = ex;
         a.b.dst_degree[r] = ri.deg;
         if (a.dbits) mark_node(a.dbits, a.dsum, ri.node);
-        // (row, phase) work items in hub_rows[4*max_dst]: thread items in
-        // [0, 2*max_dst), warp items from 2*max_dst up, hub items from
-        // 4*max_dst-1 down.  The two phases of a row are independent (their
-        // output offsets come from the scan), so they run concurrently.
-        // warp-aggregated appends: one atomic per warp and tier instead of
-        // one per item (the three list counters are hot addresses)
-#pragma unroll
-        for (int ph = 0; ph < 2; ++ph) {
-          const int take = ph == 0 ? ri.m : ri.fill;
-          const int len = ph == 0 ? ri.nc : ri.deg;
-          const int32_t item = (int32_t)((r << 1) | ph);
-          const int tier = take > 0 ? phase_tier(len) : -1;
-          int h = warp_append(a.b.counts + GNS_CNT_THREADROWS, tier == 0);
-          if (h >= 0) a.b.hub_rows[h] = item;
-          h = warp_append(a.b.counts + GNS_CNT_WARPROWS, tier == 1);
-          if (h >= 0) a.b.hub_rows[2 * a.max_dst + h] = item;
-          h = warp_append(a.b.counts + GNS_CNT_HUBS, tier == 2);
-          if (h >= 0) a.b.hub_rows[4 * a.max_dst - 1 - h] = item;
-        }
+        // (row, phase) work items go to the tier lists in hub_rows (see
+        // tier_slot).  The two phases of a row are independent (their output
+        // offsets come from the scan), so they run concurrently.
+        // Warp-aggregated appends: one atomic per warp and tier.
+        const int t0 = ri.m > 0 ? phase_tier(ri.nc, ri.m, a.stream_len) : -1;
+        const int t1 = ri.fill > 0 ? phase_tier(ri.deg, ri.fill, a.stream_len) : -1;
+        int h0, h1;
+        warp_append_tiers(a.b.counts, t0, t1, h0, h1);
+        if (t0 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t0, h0)] = (int32_t)(r << 1);
+        if (t1 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t1, h1)] = (int32_t)((r << 1) | 1);
       },
       [&](unsigned long long tot) {
         a.b.row_scan[n] = tot;
@@ -250,7 +283,7 @@ __device__ __forceinline__ double edge_weight_of(const LayerArgs& a, const RowIn
 }
 
 // warp-cooperative selection of one phase of one row
-__device__ void warp_select(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
+__device__ void warp_select(const LayerArgs& a, const Rng3& rk, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
                             uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpos) {
   const int lane = lane_id();
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -264,7 +297,7 @@ __device__ void warp_select(const LayerArgs& a, const RowInfo& ri, int64_t r, co
     for (int64_t qb = 0; qb < npairs; qb += 32) {
       const int64_t q = qb + lane;
       uint64_t k0 = kTwo53, k1 = kTwo53;
-      if (q < npairs) key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
+      if (q < npairs) key53_pair(rk.seed, rk.epoch, (uint32_t)ri.node, stream, rk.batch, (uint32_t)q, k0, k1);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int64_t p = 2 * q + j;
@@ -315,7 +348,7 @@ __device__ void warp_select(const LayerArgs& a, const RowInfo& ri, int64_t r, co
 }
 
 // CTA-cooperative selection for hub rows
-__device__ void block_select(const LayerArgs& a, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
+__device__ void block_select(const LayerArgs& a, const Rng3& rk, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
                              uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpos, int* s_found) {
   const uint32_t stream = stream_word(32, a.layer, ph.phase);
   uint64_t T = initial_threshold(ph.take, ph.cnt);
@@ -327,7 +360,7 @@ __device__ void block_select(const LayerArgs& a, const RowInfo& ri, int64_t r, c
     __syncthreads();
     for (int64_t q = threadIdx.x; q < npairs; q += kHubBlock) {
       uint64_t k0, k1;
-      key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
+      key53_pair(rk.seed, rk.epoch, (uint32_t)ri.node, stream, rk.batch, (uint32_t)q, k0, k1);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int64_t p = 2 * q + j;
@@ -427,7 +460,7 @@ __device__ __forceinline__ void sort16(uint64_t (&a)[16]) {
 // reference's stable lexsort — a 16-wide sorting network orders them and the
 // first `take` are emitted.  Keys are staged per thread in shared memory so
 // the Philox and emit loops stay rolled (small code, no local memory).
-__device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInfo& ri, int64_t r,
+__device__ __forceinline__ void thread_select16(const LayerArgs& a, const Rng3& rk, const RowInfo& ri, int64_t r,
                                                 const PhaseDesc& ph) {
   const uint32_t stream = stream_word(32, a.layer, ph.phase);
   const int len = ph.len;
@@ -446,7 +479,7 @@ __device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInf
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     uint64_t k0 = ~0ull, k1 = ~0ull;
-    if (2 * q < len) key53_pair(a.seed, a.epoch, (uint32_t)ri.node, stream, a.batch, (uint32_t)q, k0, k1);
+    if (2 * q < len) key53_pair(rk.seed, rk.epoch, (uint32_t)ri.node, stream, rk.batch, (uint32_t)q, k0, k1);
     bool ok0 = 2 * q < len, ok1 = 2 * q + 1 < len;
     if (ph.filter) {
       ok0 = ok0 && !((mw[2 * q] >> (idv[2 * q] & 31)) & 1u);
@@ -490,8 +523,103 @@ __device__ __forceinline__ void thread_select16(const LayerArgs& a, const RowInf
   }
 }
 
-__global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a_in) {
-  const LayerArgs a = resolve_rng(a_in);
+// One thread per item, take <= kStreamK, <= kStreamLen positions: keys are
+// generated 8 positions at a time and inserted into a sorted register array
+// of the kStreamK smallest packed (key53 << 11 | position) values — the
+// reference's (key, position) lexsort order — so only ~kStreamK live keys
+// are held (the sorting-network tier holds 16 plus the candidates' ids).
+__device__ __forceinline__ void insert_sorted(uint64_t (&best)[kStreamK], uint64_t v) {
+#pragma unroll
+  for (int i = kStreamK - 1; i >= 1; --i) {
+    const uint64_t lo = best[i - 1];
+    best[i] = v < lo ? lo : (v < best[i] ? v : best[i]);
+  }
+  best[0] = v < best[0] ? v : best[0];
+}
+
+__device__ __forceinline__ void thread_select_stream(const LayerArgs& a, const Rng3& rk, const RowInfo& ri,
+                                                     int64_t r, const PhaseDesc& ph) {
+  const uint32_t stream = stream_word(32, a.layer, ph.phase);
+  const int len = ph.len;
+  uint64_t best[kStreamK];
+#pragma unroll
+  for (int i = 0; i < kStreamK; ++i) best[i] = ~0ull;
+  for (int p0 = 0; p0 < len; p0 += 8) {
+    // fill phase: the 8 neighbour ids and cache-bitmap words in flight at once
+    int32_t idv[8];
+    uint32_t mw[8];
+    if (ph.filter) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) idv[j] = p0 + j < len ? __ldg(ph.ids + p0 + j) : 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mw[j] = p0 + j < len ? __ldg(a.mask + (idv[j] >> 5)) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = p0 + 2 * q;
+      if (p >= len) break;
+      uint64_t k0, k1;
+      key53_pair(rk.seed, rk.epoch, (uint32_t)ri.node, stream, rk.batch, (uint32_t)(p >> 1), k0, k1);
+      bool ok0 = true, ok1 = p + 1 < len;
+      if (ph.filter) {
+        ok0 = !((mw[2 * q] >> (idv[2 * q] & 31)) & 1u);
+        ok1 = ok1 && !((mw[2 * q + 1] >> (idv[2 * q + 1] & 31)) & 1u);
+      }
+      if (ok0) insert_sorted(best, (k0 << 11) | (uint64_t)p);
+      if (ok1) insert_sorted(best, (k1 << 11) | (uint64_t)(p + 1));
+    }
+  }
+  // emit the first `take`, 4 at a time: every load of a chunk's edges
+  // (neighbour id, inclusion, dedup word) before any of its stores
+  const int take = ph.take;
+  const int64_t o0 = ph.out_base;
+#pragma unroll
+  for (int c0 = 0; c0 < kStreamK; c0 += 4) {
+    if (c0 >= take) break;
+    int32_t u[4];
+    double inc[4];
+    uint32_t bw[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u[i] = c0 + i < take ? __ldg(ph.ids + (uint32_t)(best[c0 + i] & 2047u)) : 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      inc[i] = (c0 + i < take && ph.phase == 0 && !a.exact_q) ? __ldg(a.incl + u[i]) : 0.0;
+      bw[i] = c0 + i < take ? __ldg(a.dbits + (u[i] >> 5)) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (c0 + i < take) {
+        const double w = a.exact_q ? exact_weight(a, ri, ph, (uint32_t)(best[c0 + i] & 2047u))
+                                   : edge_weight_of(a, ri, ph, inc[i]);
+        const uint32_t m = 1u << (u[i] & 31);
+        if (!(bw[i] & m)) {
+          const uint32_t old = atomicOr(a.dbits + (u[i] >> 5), m);
+          if (old == 0u) atomicOr(a.dsum + ((u[i] >> 5) >> 5), 1u << ((u[i] >> 5) & 31));
+        }
+        a.b.edge_node[o0 + c0 + i] = u[i];
+        a.b.edge_dst[o0 + c0 + i] = (int32_t)r;
+        a.b.edge_weight[o0 + c0 + i] = w;
+        a.b.edge_cached[o0 + c0 + i] = ph.phase == 0 ? 1 : 0;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) sample_stream_kernel(const __grid_constant__ LayerArgs a) {
+  const Rng3 rk = batch_rng(a);
+  const int64_t nl = a.b.counts[GNS_CNT_STREAMROWS];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nl; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t item = a.b.hub_rows[2 * a.max_dst + j];
+    const int64_t r = item >> 1;
+    RowInfo ri = row_info(a, r);
+    PhaseDesc pc, pf;
+    make_phases(a, ri, r, pc, pf);
+    thread_select_stream(a, rk, ri, r, (item & 1) ? pf : pc);
+  }
+}
+
+__global__ void __launch_bounds__(256) sample_thread_kernel(const __grid_constant__ LayerArgs a) {
+  const Rng3 rk = batch_rng(a);
   const int64_t nl = a.b.counts[GNS_CNT_THREADROWS];
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nl; j += (int64_t)gridDim.x * blockDim.x) {
     const int32_t item = a.b.hub_rows[j];
@@ -499,12 +627,12 @@ __global__ void __launch_bounds__(256) sample_thread_kernel(LayerArgs a_in) {
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
-    thread_select16(a, ri, r, (item & 1) ? pf : pc);
+    thread_select16(a, rk, ri, r, (item & 1) ? pf : pc);
   }
 }
 
-__global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a_in) {
-  const LayerArgs a = resolve_rng(a_in);
+__global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(const __grid_constant__ LayerArgs a) {
+  const Rng3 rk = batch_rng(a);
   __shared__ uint64_t s_key[kSampBlock / 32][kWarpCap];
   __shared__ uint32_t s_pos[kSampBlock / 32][kWarpCap];
   const int w = threadIdx.x >> 5;
@@ -512,28 +640,28 @@ __global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(LayerArgs a_in)
   const int64_t gw = (blockIdx.x * (int64_t)kSampBlock + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kSampBlock) >> 5;
   for (int64_t j = gw; j < nl; j += nw) {
-    const int32_t item = a.b.hub_rows[2 * a.max_dst + j];
+    const int32_t item = a.b.hub_rows[4 * a.max_dst + j];
     const int64_t r = item >> 1;
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
-    warp_select(a, ri, r, (item & 1) ? pf : pc, s_key[w], s_pos[w]);
+    warp_select(a, rk, ri, r, (item & 1) ? pf : pc, s_key[w], s_pos[w]);
   }
 }
 
-__global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(LayerArgs a_in) {
-  const LayerArgs a = resolve_rng(a_in);
+__global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(const __grid_constant__ LayerArgs a) {
+  const Rng3 rk = batch_rng(a);
   __shared__ uint64_t s_key[kHubCap];
   __shared__ uint32_t s_pos[kHubCap];
   __shared__ int s_found;
   const int nh = a.b.counts[GNS_CNT_HUBS];
   for (int h = blockIdx.x; h < nh; h += gridDim.x) {
-    const int32_t item = a.b.hub_rows[4 * a.max_dst - 1 - h];
+    const int32_t item = a.b.hub_rows[6 * a.max_dst - 1 - h];
     const int64_t r = item >> 1;
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
-    block_select(a, ri, r, (item & 1) ? pf : pc, s_key, s_pos, &s_found);
+    block_select(a, rk, ri, r, (item & 1) ? pf : pc, s_key, s_pos, &s_found);
   }
 }
 
@@ -574,14 +702,13 @@ __global__ void __launch_bounds__(kEnumBlock) enumerate_reduce_kernel(const uint
   __shared__ unsigned long long s_w[kEnumWarps + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long sw0 = (long long)blockIdx.x * kEnumTileSw + warp * kEnumPerWarp;
+  // the warp's 8 summary words in one load, then all bitmap loads in flight
+  const uint32_t my_sum = (lane < kEnumPerWarp && sw0 + lane < nsw) ? sum[sw0 + lane] : 0u;
   unsigned c = 0;
 #pragma unroll
   for (int i = 0; i < kEnumPerWarp; ++i) {
-    const long long sw = sw0 + i;
-    if (sw < nsw) {
-      const uint32_t smw = sum[sw];
-      if (smw) c += __popc(enum_word(bits, smw, sw, lane));
-    }
+    const uint32_t smw = __shfl_sync(GNS_FULL, my_sum, i);
+    c += __popc(enum_word(bits, smw, sw0 + i, lane));
   }
   unsigned long long t = block_sum<kEnumBlock>((unsigned long long)c, s_w);
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = t;
@@ -608,16 +735,13 @@ __global__ void __launch_bounds__(kEnumBlock) enumerate_apply_kernel(uint32_t* _
   pre = block_sum<kEnumBlock>(pre, s_w);
   // per-warp counts -> exclusive prefix over the 8 warps of the tile
   const long long sw0 = tile * kEnumTileSw + warp * kEnumPerWarp;
+  const uint32_t my_sum = (lane < kEnumPerWarp && sw0 + lane < nsw) ? sum[sw0 + lane] : 0u;
   uint32_t words[kEnumPerWarp];
   unsigned c = 0;
 #pragma unroll
   for (int i = 0; i < kEnumPerWarp; ++i) {
-    const long long sw = sw0 + i;
-    words[i] = 0u;
-    if (sw < nsw) {
-      const uint32_t smw = sum[sw];
-      if (smw) words[i] = enum_word(bits, smw, sw, lane);
-    }
+    const uint32_t smw = __shfl_sync(GNS_FULL, my_sum, i);
+    words[i] = enum_word(bits, smw, sw0 + i, lane);
     c += __popc(words[i]);
   }
   c = warp_sum(c);
@@ -822,6 +946,7 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.step_dev = step_dev;
   a.dbits = dd.bits;
   a.dsum = dd.sum;
+  a.stream_len = g_stream_len;
   a.b = *block;
   const unsigned tiles = (unsigned)((max_dst + kCntBlock * kCntItems - 1) / (kCntBlock * kCntItems)) + 1;
   GNS_CUDA(cudaMemsetAsync(block->counts, 0, GNS_CNT_N * sizeof(int32_t), stream));
@@ -834,6 +959,8 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   Fork fk;
   GNS_TRY(fork_begin(stream, &fk));
   int tgrid = grid_for((2 * max_dst + 255) / 256, (long long)sms * 16);
+  sample_stream_kernel<<<tgrid, 256, 0, stream>>>(a);
+  GNS_TRY(check_launch("sample_stream"));
   sample_thread_kernel<<<tgrid, 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_thread"));
   int grid = grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock, (long long)sms * 8);
@@ -845,6 +972,14 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   // _assemble (sampling.py:139-152): seeds and sampled neighbours were marked
   // in the dedup bitmap by the count / sample kernels
   return run_relabel(dd, seeds, n_seeds_dev, max_dst, block, max_dst * (int64_t)k, stream);
+}
+
+int gns_sample_tune(const char* name, int32_t value) {
+  if (!strcmp(name, "stream_len") && value >= 0 && value < 2048) {
+    g_stream_len = value;
+    return GNS_OK;
+  }
+  return GNS_EINVAL;
 }
 
 size_t gns_relabel_workspace_size(int64_t num_nodes) {

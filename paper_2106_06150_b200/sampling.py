@@ -205,7 +205,7 @@ class MiniBatchSampler:
                 row_scan=torch.empty(dst_cap + 1, dtype=torch.int64, device=dev),
                 dst_degree=torch.empty(dst_cap, dtype=torch.int32, device=dev),
                 self_pos=torch.empty(dst_cap, dtype=torch.int32, device=dev),
-                hub_rows=torch.empty(4 * dst_cap, dtype=torch.int32, device=dev),
+                hub_rows=torch.empty(6 * max(dst_cap, 1), dtype=torch.int32, device=dev),
                 edge_node=torch.empty(max(edge_cap, 1), dtype=torch.int32, device=dev),
                 edge_src=torch.empty(max(edge_cap, 1), dtype=torch.int32, device=dev),
                 edge_dst=torch.empty(max(edge_cap, 1), dtype=torch.int32, device=dev),

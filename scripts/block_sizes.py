@@ -48,6 +48,9 @@ def main():
         print(f" layer {l}: dst {d.mean():9.0f} (cap {lb.max_dst:8d})  src {s.mean():9.0f} (cap {lb.max_src:8d})  "
               f"edges {e.mean():9.0f} (cap {lb.max_edges:8d})  cached-edges {cc.mean():9.0f}  "
               f"max dst/src/edges {d.max():.0f}/{s.max():.0f}/{e.max():.0f}")
+        th, wa, hu = a[:, l, 7], a[:, l, 6], a[:, l, _lib.CNT_HUBS]
+        print(f"          (row, phase) items: thread tier {th.mean():9.0f}  warp tier {wa.mean():8.0f}  "
+              f"hub tier {hu.mean():6.0f}")
 
 
 if __name__ == "__main__":

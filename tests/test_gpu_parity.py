@@ -489,7 +489,7 @@ def test_spmm_bwd_f32_variants_identical(P, dim):
             assert torch.equal(res[0][0], res[1][0]), li
             assert torch.equal(res[0][1], res[1][1]), li
     finally:
-        _lib.call("gns_tune", b"spmm_bwd", 1)
+        _lib.call("gns_tune", b"spmm_bwd", 0)
 
 
 def test_full_batch_equivalence(P):
