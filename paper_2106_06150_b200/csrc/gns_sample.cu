@@ -168,25 +168,74 @@ __device__ __forceinline__ bool cached_bit(const uint32_t* __restrict__ mask, in
 }
 
 // ---- pass 1: per-row counts + exclusive scan (two kernels) ----------------------
-__device__ __forceinline__ unsigned long long row_counts(const LayerArgs& a, long long r) {
-  RowInfo ri = row_info(a, r);
-  return ((unsigned long long)ri.m << 32) | (unsigned long long)ri.fill;
-}
-
+// Reduce kernel: all per-row work — row bounds, dst degree, dedup mark of the
+// seed, (row, phase) work items into the tier lists, the packed (m, fill)
+// count in row_scan[r] and the tile sums.  A thread's kCntItems rows issue
+// their loads together (seed ids, then the four CSR offsets) instead of one
+// row's dependent chain after another.  Apply kernel: the exclusive scan of
+// row_scan only.
 constexpr int kCntBlock = 256, kCntItems = 4;
 
 __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __grid_constant__ LayerArgs a,
                                                                        unsigned long long* tile_sums) {
+  __shared__ unsigned long long s_warp[kCntBlock / 32 + 1];
   const long long n = a.n_dev[0];
-  // the per-row value is stashed in row_scan[r] for the apply pass
-  scan2_reduce<kCntBlock, kCntItems>(
-      n,
-      [&](long long r) {
-        unsigned long long v = row_counts(a, r);
+  const long long base = (long long)blockIdx.x * (kCntBlock * kCntItems);
+  unsigned long long tsum = 0;
+  if (base < n) {
+    int32_t node[kCntItems];
+#pragma unroll
+    for (int j = 0; j < kCntItems; ++j) {
+      const long long r = base + j * kCntBlock + threadIdx.x;
+      node[j] = r < n ? __ldg(a.seeds + r) : 0;
+    }
+    int64_t s0[kCntItems], s1[kCntItems], c0[kCntItems], c1[kCntItems];
+#pragma unroll
+    for (int j = 0; j < kCntItems; ++j) {
+      const long long r = base + j * kCntBlock + threadIdx.x;
+      s0[j] = s1[j] = c0[j] = c1[j] = 0;
+      if (r < n) {
+        s0[j] = __ldg(a.indptr + node[j]);
+        s1[j] = __ldg(a.indptr + node[j] + 1);
+        if (a.gns) {
+          c0[j] = __ldg(a.cindptr + node[j]);
+          c1[j] = __ldg(a.cindptr + node[j] + 1);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kCntItems; ++j) {
+      const long long r = base + j * kCntBlock + threadIdx.x;
+      const bool on = r < n;
+      const int32_t deg = (int32_t)(s1[j] - s0[j]);
+      int32_t m = 0, fill = 0, nc = 0;
+      if (a.gns) {
+        nc = (int32_t)(c1[j] - c0[j]);
+        m = min(a.k, nc);
+        fill = a.cache_only ? 0 : min(a.k - m, deg - nc);
+      } else {
+        fill = min(a.k, deg);
+      }
+      if (on) {
+        const unsigned long long v = ((unsigned long long)m << 32) | (unsigned long long)fill;
         a.b.row_scan[r] = v;
-        return v;
-      },
-      tile_sums);
+        a.b.dst_degree[r] = deg;
+        if (a.dbits) mark_node(a.dbits, a.dsum, node[j]);
+        tsum += v;
+      }
+      // (row, phase) work items into the tier lists (tier_slot); the two
+      // phases of a row are independent (their output offsets come from
+      // the scan), so they run concurrently.  One atomic per warp and tier.
+      const int t0 = on && m > 0 ? phase_tier(nc, m, a.stream_len) : -1;
+      const int t1 = on && fill > 0 ? phase_tier(deg, fill, a.stream_len) : -1;
+      int h0 = 0, h1 = 0;
+      warp_append_tiers(a.b.counts, t0, t1, h0, h1);
+      if (t0 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t0, h0)] = (int32_t)(r << 1);
+      if (t1 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t1, h1)] = (int32_t)((r << 1) | 1);
+    }
+  }
+  tsum = block_sum<kCntBlock>(tsum, s_warp);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tsum;
 }
 
 __global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(const __grid_constant__ LayerArgs a,
@@ -194,22 +243,7 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(const __gr
   const long long n = a.n_dev[0];
   scan2_apply<kCntBlock, kCntItems>(
       n, [&](long long r) { return (unsigned long long)a.b.row_scan[r]; },
-      [&](long long r, unsigned long long ex, unsigned long long) {
-        RowInfo ri = row_info(a, r);
-        a.b.row_scan[r] = ex;
-        a.b.dst_degree[r] = ri.deg;
-        if (a.dbits) mark_node(a.dbits, a.dsum, ri.node);
-        // (row, phase) work items go to the tier lists in hub_rows (see
-        // tier_slot).  The two phases of a row are independent (their output
-        // offsets come from the scan), so they run concurrently.
-        // Warp-aggregated appends: one atomic per warp and tier.
-        const int t0 = ri.m > 0 ? phase_tier(ri.nc, ri.m, a.stream_len) : -1;
-        const int t1 = ri.fill > 0 ? phase_tier(ri.deg, ri.fill, a.stream_len) : -1;
-        int h0, h1;
-        warp_append_tiers(a.b.counts, t0, t1, h0, h1);
-        if (t0 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t0, h0)] = (int32_t)(r << 1);
-        if (t1 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t1, h1)] = (int32_t)((r << 1) | 1);
-      },
+      [&](long long r, unsigned long long ex, unsigned long long) { a.b.row_scan[r] = ex; },
       [&](unsigned long long tot) {
         a.b.row_scan[n] = tot;
         a.b.counts[GNS_CNT_DST] = (int32_t)n;

@@ -59,7 +59,7 @@ class GraphedTrainer:
         self.model = GraphSAGE(dims, dtype=torch.float32, device=self.dev, seed=seed)
         self.dims = self.model.dims
         self.L = config.num_layers
-        S = steps_per_graph if steps_per_graph is not None else int(os.environ.get("GNS_STEPS_PER_GRAPH", "2"))
+        S = steps_per_graph if steps_per_graph is not None else int(os.environ.get("GNS_STEPS_PER_GRAPH", "1"))
         if S < 1:
             raise ValueError("steps_per_graph must be >= 1")
         self.S = S
