@@ -920,11 +920,15 @@ using namespace gns;
 
 extern "C" {
 
+// The dedup bitmaps come first so their offsets depend on num_nodes only:
+// every layer of a batch (different max_dst) sees the same, zeroed bitmaps.
+// (With the count tile sums first, a larger layer's tile sums were written
+// over the bitmap words of the smaller layers' layout.)
 static size_t sample_ws(int64_t num_nodes, int64_t max_dst, void* base, size_t cap, unsigned long long** tiles,
                         DedupWs* d) {
   Workspace w(base, cap);
-  *tiles = w.take<unsigned long long>(max_dst / (kCntBlock * kCntItems) + 2);
   dedup_ws(num_nodes, w, d);
+  *tiles = w.take<unsigned long long>(max_dst / (kCntBlock * kCntItems) + 2);
   return w.off;
 }
 

@@ -194,6 +194,30 @@ def test_minibatch_bit_exact_vs_oracle_hubs(P, strategy, cache_only, frac):
         assert_mb_equal(mb, ref, f"{strategy}-{cache_only}-{index}")
 
 
+def test_minibatch_layers_with_large_capacities(P):
+    """Layers whose capacities differ by > 32K rows share one sampler
+    workspace: consecutive batches through the same MiniBatchSampler stay
+    bit-exact (regression: the count pass's tile sums once overlapped the
+    dedup bitmap of a smaller layer's layout)."""
+    n = 60_000
+    rng = np.random.default_rng(11)
+    og = O.build_csr(rng.integers(0, n, size=(600_000, 2)), n)
+    g = P.Graph.from_numpy(n, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=1000, cache_mode="degree",
+                          cache_frac=0.01, seed=6)
+    cs = O.cache_size_for(og, cfg.cache_frac)
+    cache = P.build_cache(g, P.degree_probs(g), cs, rng_seed=[6, 33, 0])
+    oc = O.build_cache(og, O.degree_probs(og), cs, seed=6, epoch=0)
+    from paper_2106_06150_b200.sampling import MiniBatchSampler
+    eng = MiniBatchSampler(g, cfg)
+    assert eng.layers[-1].max_dst > 32 * 1024
+    for b in range(3):
+        targets = rng.choice(n, 1000, replace=False)
+        mb = eng.sample(targets, P.BatchRng(6, 0, b), cache)
+        ref = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(6, 0, b))
+        assert_mb_equal(mb, ref, f"batch {b}")
+
+
 def test_single_layer_entry_points(P):
     og = _hub_graph(2000, 3)
     g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
