@@ -142,18 +142,40 @@ def host_cache(cache, n):
                     cached_indices=cache.cached_indices.cpu().numpy())
 
 
-def cpu_reference_run(P, g, c, cfg, cache, n_batches, warmup=1):
+def cpu_reference_run(P, g, c, cfg, cache, n_batches, warmup=1, host=None):
     """The reference's CPU algorithm (oracle port: pool.py fork workers + the
     float64 trainer loop body) on this host's cores."""
     from oracle import cpu_pipeline, gns as O
-    og = host_graph(g)
-    oc = host_cache(cache, g.num_nodes) if cache is not None else None
+    og, oc = host if host is not None else host_inputs(g, cache)
     batches = O.epoch_targets(og, cfg.batch_size, cfg.seed, 0, numpy_mode=True)
     batches = batches[:n_batches + warmup]
     dims = (c["dim"], c["hidden"], c["hidden"], c["classes"])
     r = cpu_pipeline.run(og, oc, cfg, dims, batches, epoch=0, warmup=warmup)
     r["cores"] = r["workers"] + 1
     return r
+
+
+def host_inputs(g, cache):
+    return host_graph(g), (host_cache(cache, g.num_nodes) if cache is not None else None)
+
+
+def full_size_parity(P, g, cfg, cache, og, oc, n_batches=1):
+    """One mini-batch of the bench workload sampled on the device (libgns)
+    and by the oracle restatement of the reference (Philox keys): every block
+    field must be bit-identical."""
+    from oracle import gns as O
+    fields = ("dst_nodes", "src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached", "dst_degree")
+    train = np.flatnonzero(og.train_mask)
+    ok = True
+    for b in range(n_batches):
+        targets = np.random.default_rng(1000 + b).choice(train, cfg.batch_size, replace=False)
+        mb = P.build_minibatch(g, cache, targets, cfg, P.BatchRng(cfg.seed, 0, b))
+        ref = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(cfg.seed, 0, b))
+        for bg, br in zip(mb.blocks, ref.blocks):
+            h = bg.to_numpy()
+            ok &= all(np.array_equal(getattr(h, f), np.asarray(getattr(br, f))) for f in fields)
+    return {"batches": n_batches, "bit_exact": bool(ok), "fields": list(fields),
+            "vs": "oracle restatement of sampling.py:189-336 with the same Philox keys, full-size graph"}
 
 
 def gather_microbench(tr, D, reps=24):
@@ -372,8 +394,11 @@ def main():
         del te
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference_run(P, g, c, cfg, pool.cache, c["cpu_batches"])
+        host = host_inputs(g, pool.cache)
+        parity = full_size_parity(P, g, cfg, pool.cache, *host)
+        r = cpu_reference_run(P, g, c, cfg, pool.cache, c["cpu_batches"], host=host)
         cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
                "sample": f"{r['steps']} mini-batches of this workload (epoch 0, after 1 warm-up), oracle port "
                          f"of pool.py fork workers ({r['workers']}) + float64 trainer loop body; sample "
@@ -383,7 +408,8 @@ def main():
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
-                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_total,
+                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+                "gpu_launches": launches_total,
                 "gpu_launches_per_step": launches_total / args.steps, "clocks": clk,
                 "per_step": {"input_nodes": float(n_in.mean()), "gather_ms": float(g_ms.mean()),
                              "fused_gather": tr.fused_gather,
