@@ -130,14 +130,18 @@ class _DrawWorkspace:
         return ws
 
 
-def _draw(probs: ProbVector, cache_size: int, seed: int, epoch: int, stream=None, tag: int = _CACHE_TAG):
+def _draw(probs: ProbVector, cache_size: int, seed: int, epoch: int, stream=None, tag: int = _CACHE_TAG,
+          out=None):
     w = probs.weights
     n = int(w.shape[0])
     dev = w.device
     cs = max(int(cache_size), 0)
-    ids = torch.empty(max(cs, 1), dtype=torch.int32, device=dev)
-    bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
-    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    if out is not None:
+        ids, bits, counts = out
+    else:
+        ids = torch.empty(max(cs, 1), dtype=torch.int32, device=dev)
+        bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+        counts = torch.zeros(2, dtype=torch.int64, device=dev)
     ws = _DrawWorkspace.get(n, dev)
     _lib.call("gns_cache_draw", w.data_ptr(), n, cs, seed, epoch, tag, ids.data_ptr(), bits.data_ptr(),
               counts.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(stream))
@@ -223,28 +227,61 @@ def build_cache(g: Graph, probs: ProbVector, cache_size: int, epoch: int = 0, rn
                                   "hot path (SURVEY.md §8(f)3)")
     if inclusion_mode != "analytic":
         raise ValueError(f"unknown inclusion_mode {inclusion_mode!r}")
+    return _build_cache_into(None, g, probs, cache_size, epoch, rng_seed)
+
+
+def refresh_cache(state: CacheState, g: Graph, probs: ProbVector, cache_size: int, epoch: int, rng_seed) -> bool:
+    """build_cache into the buffers of an existing CacheState of the same
+    graph and cache size (the per-epoch refresh of pool.py:133-135).  Device
+    addresses stay the same unless the new cached CSR outgrows its buffer, so
+    CUDA graphs that captured the cache stay valid; returns True when every
+    address was kept."""
+    new = _build_cache_into(state, g, probs, cache_size, epoch, rng_seed)
+    return new is state
+
+
+def _build_cache_into(state, g, probs, cache_size, epoch, rng_seed):
     probs = probs.normalize()
     stream = _lib.stream_ptr()
     seed, ep, tag = seed_key(rng_seed)
-    ids, bits, counts = _draw(probs, cache_size, seed, ep, tag=tag)
     n = g.num_nodes
-    incl = torch.empty(n, dtype=torch.float64, device=g.device)
+    if state is not None:
+        bufs = (state._buf_ids, state.nodes.mask_bits, state._buf_counts)
+        incl, c_indptr = state.inclusion, state.cached_indptr
+    else:
+        bufs = None
+        incl = torch.empty(n, dtype=torch.float64, device=g.device)
+        c_indptr = torch.empty(n + 1, dtype=torch.int64, device=g.device)
+    ids, bits, counts = _draw(probs, cache_size, seed, ep, tag=tag, out=bufs)
     # |C| and |support| stay on the device (counts[0], counts[1])
     _lib.call("gns_inclusion", probs.weights.data_ptr(), n, 0, counts.data_ptr(),
               counts[1:].data_ptr(), incl.data_ptr(), stream)
-    c_indptr = torch.empty(n + 1, dtype=torch.int64, device=g.device)
     nnz = torch.zeros(1, dtype=torch.int64, device=g.device)
     ws = _lib.workspace(_lib.lib().gns_cached_csr_workspace_size(n), g.device)
     _lib.call("gns_cached_csr_count", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
               nnz.data_ptr(), ws.data_ptr(), ws.numel(), stream)
     host = counts.cpu()  # one sync per refresh: |C| and nnz_C size the outputs
     nnz_h = int(nnz.item())
-    c_indices = torch.empty(max(nnz_h, 1), dtype=torch.int32, device=g.device)
-    c_pos = torch.empty(max(nnz_h, 1), dtype=torch.int32, device=g.device)
+    k = int(host[0])
+    keep = state is not None and state._buf_cidx.numel() >= nnz_h and k == len(state.nodes)
+    if keep:
+        c_indices, c_pos = state._buf_cidx, state._buf_cpos
+    else:
+        cap = max(nnz_h + nnz_h // 4, 1)      # headroom: later draws rarely reallocate
+        c_indices = torch.empty(cap, dtype=torch.int32, device=g.device)
+        c_pos = torch.empty(cap, dtype=torch.int32, device=g.device)
     _lib.call("gns_cached_csr_fill", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
               c_indices.data_ptr(), c_pos.data_ptr(), stream)
-    k = int(host[0])
+    if keep:   # frozen dataclass: refresh the views in place (same addresses)
+        for name, val in (("cached_indices", c_indices[:nnz_h]), ("cached_pos", c_pos[:nnz_h]),
+                          ("epoch", epoch), ("source_probs", probs)):
+            object.__setattr__(state, name, val)
+        state.__dict__.pop("_rank", None)      # bitmap content changed
+        return state
     nodes = NodeSet(ids=ids[:k], mask_bits=bits, num_nodes=n)
-    return CacheState(nodes=nodes, inclusion=incl, cached_indptr=c_indptr,
-                      cached_indices=c_indices[:nnz_h], epoch=epoch, source_probs=probs,
-                      cached_pos=c_pos[:nnz_h])
+    st = CacheState(nodes=nodes, inclusion=incl, cached_indptr=c_indptr,
+                    cached_indices=c_indices[:nnz_h], epoch=epoch, source_probs=probs,
+                    cached_pos=c_pos[:nnz_h])
+    for name, val in (("_buf_ids", ids), ("_buf_counts", counts), ("_buf_cidx", c_indices), ("_buf_cpos", c_pos)):
+        object.__setattr__(st, name, val)
+    return st

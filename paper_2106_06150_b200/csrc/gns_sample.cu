@@ -59,6 +59,7 @@ struct LayerArgs {
   uint32_t* dbits;  // dedup bitmap (bit v of word v>>5); NULL = no fused marking
   uint32_t* dsum;   // summary bitmap (bit w of word w>>5 set iff dbits[w] != 0)
   int stream_len;   // rows up to this many positions with take <= kStreamK: streaming tier
+  struct RowDesc* desc;  // per-row descriptors (count pass -> selection kernels)
   gns_block_t b;
 };
 
@@ -133,19 +134,27 @@ struct RowInfo {
   int32_t node, deg, nc, m, fill;
 };
 
+// Per-row descriptor written by the count pass (32 B, two 16-B loads): the
+// selection kernels read one descriptor per item instead of the chain
+// seeds[r] -> indptr/cindptr[node].
+struct __align__(16) RowDesc {
+  int64_t start, cstart;
+  int32_t node, deg, nc, pad;
+};
+
 __device__ __forceinline__ RowInfo row_info(const LayerArgs& a, int64_t r) {
+  const int4* d = reinterpret_cast<const int4*>(a.desc + r);
+  const int4 lo = d[0], hi = d[1];
   RowInfo ri;
-  ri.node = a.seeds[r];
-  ri.start = a.indptr[ri.node];
-  ri.deg = (int32_t)(a.indptr[ri.node + 1] - ri.start);
+  ri.start = ((int64_t)(uint32_t)lo.y << 32) | (uint32_t)lo.x;
+  ri.cstart = ((int64_t)(uint32_t)lo.w << 32) | (uint32_t)lo.z;
+  ri.node = hi.x;
+  ri.deg = hi.y;
+  ri.nc = hi.z;
   if (a.gns) {
-    ri.cstart = a.cindptr[ri.node];
-    ri.nc = (int32_t)(a.cindptr[ri.node + 1] - ri.cstart);
     ri.m = min(a.k, ri.nc);
     ri.fill = a.cache_only ? 0 : min(a.k - ri.m, ri.deg - ri.nc);
   } else {
-    ri.cstart = 0;
-    ri.nc = 0;
     ri.m = 0;
     ri.fill = min(a.k, ri.deg);
   }
@@ -220,6 +229,10 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __g
         const unsigned long long v = ((unsigned long long)m << 32) | (unsigned long long)fill;
         a.b.row_scan[r] = v;
         a.b.dst_degree[r] = deg;
+        int4* d = reinterpret_cast<int4*>(a.desc + r);
+        d[0] = make_int4((int32_t)(uint64_t)s0[j], (int32_t)((uint64_t)s0[j] >> 32), (int32_t)(uint64_t)c0[j],
+                         (int32_t)((uint64_t)c0[j] >> 32));
+        d[1] = make_int4(node[j], deg, nc, 0);
         if (a.dbits) mark_node(a.dbits, a.dsum, node[j]);
         tsum += v;
       }
@@ -326,6 +339,12 @@ __device__ void warp_select(const LayerArgs& a, const Rng3& rk, const RowInfo& r
   uint64_t lo = 0, hi = kTwo53 + 1;
   const int64_t npairs = ((int64_t)ph.len + 1) >> 1;
   int found = 0;
+  // Fill phase: collect every position under T first (Philox ALU only) and
+  // probe the cache bitmap for the collected ones afterwards, all lanes'
+  // loads in flight together, instead of a dependent id + bitmap load inside
+  // every scan iteration that has a hit.  Falls back to the inline probe if
+  // the unfiltered candidates overflow the buffer (densely cached rows).
+  bool deferred = ph.filter;
   for (int iter = 0; iter < 64; ++iter) {
     found = 0;
     for (int64_t qb = 0; qb < npairs; qb += 32) {
@@ -337,7 +356,7 @@ __device__ void warp_select(const LayerArgs& a, const Rng3& rk, const RowInfo& r
         const int64_t p = 2 * q + j;
         const uint64_t key = j ? k1 : k0;
         bool pred = (q < npairs) && (p < ph.len) && (key < T);
-        if (pred && ph.filter) pred = !cached_bit(a.mask, __ldg(ph.ids + p));
+        if (pred && ph.filter && !deferred) pred = !cached_bit(a.mask, __ldg(ph.ids + p));
         unsigned bal = __ballot_sync(GNS_FULL, pred);
         if (pred) {
           int o = found + __popc(bal & lt_mask);
@@ -348,6 +367,51 @@ __device__ void warp_select(const LayerArgs& a, const Rng3& rk, const RowInfo& r
         }
         found += __popc(bal);
       }
+    }
+    if (deferred) {
+      if (found > kWarpCap) {   // too many cached candidates under T: probe inline
+        deferred = false;
+        --iter;
+        continue;
+      }
+      __syncwarp();
+      // probe the collected candidates: every lane's id loads, then bitmap loads
+      constexpr int PER = kWarpCap / 32;
+      int32_t idv[PER];
+#pragma unroll
+      for (int t = 0; t < PER; ++t) {
+        const int i = t * 32 + lane;
+        idv[t] = i < found ? __ldg(ph.ids + bpos[i]) : 0;
+      }
+      bool keep[PER];
+#pragma unroll
+      for (int t = 0; t < PER; ++t) {
+        const int i = t * 32 + lane;
+        keep[t] = i < found && !cached_bit(a.mask, idv[t]);
+      }
+      // in-place ordered compaction of the survivors
+      int kept = 0;
+#pragma unroll
+      for (int t = 0; t < PER; ++t) {
+        if (t * 32 >= found) break;
+        const int i = t * 32 + lane;
+        uint64_t kv = 0;
+        uint32_t pv = 0;
+        if (keep[t]) {
+          kv = bkey[i];
+          pv = bpos[i];
+        }
+        const unsigned bal = __ballot_sync(GNS_FULL, keep[t]);
+        __syncwarp();
+        if (keep[t]) {
+          const int o = kept + __popc(bal & lt_mask);
+          bkey[o] = kv;
+          bpos[o] = pv;
+        }
+        kept += __popc(bal);
+        __syncwarp();
+      }
+      found = kept;
     }
     if (found > kWarpCap) {
       hi = T;
@@ -665,7 +729,7 @@ __global__ void __launch_bounds__(256) sample_thread_kernel(const __grid_constan
   }
 }
 
-__global__ void __launch_bounds__(kSampBlock) sample_warp_kernel(const __grid_constant__ LayerArgs a) {
+__global__ void __launch_bounds__(kSampBlock, 4) sample_warp_kernel(const __grid_constant__ LayerArgs a) {
   const Rng3 rk = batch_rng(a);
   __shared__ uint64_t s_key[kSampBlock / 32][kWarpCap];
   __shared__ uint32_t s_pos[kSampBlock / 32][kWarpCap];
@@ -925,17 +989,19 @@ extern "C" {
 // (With the count tile sums first, a larger layer's tile sums were written
 // over the bitmap words of the smaller layers' layout.)
 static size_t sample_ws(int64_t num_nodes, int64_t max_dst, void* base, size_t cap, unsigned long long** tiles,
-                        DedupWs* d) {
+                        DedupWs* d, RowDesc** desc) {
   Workspace w(base, cap);
   dedup_ws(num_nodes, w, d);
   *tiles = w.take<unsigned long long>(max_dst / (kCntBlock * kCntItems) + 2);
+  *desc = w.take<RowDesc>(max_dst + 1);
   return w.off;
 }
 
 size_t gns_sample_workspace_size(int64_t num_nodes, int64_t max_dst) {
   unsigned long long* t;
   DedupWs d;
-  return sample_ws(num_nodes, max_dst, nullptr, 0, &t, &d);
+  RowDesc* desc;
+  return sample_ws(num_nodes, max_dst, nullptr, 0, &t, &d, &desc);
 }
 
 int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32_t* seeds,
@@ -953,7 +1019,8 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   }
   unsigned long long* ctiles;
   DedupWs dd;
-  size_t need = sample_ws(g->num_nodes, max_dst, ws, ws_bytes, &ctiles, &dd);
+  RowDesc* desc;
+  size_t need = sample_ws(g->num_nodes, max_dst, ws, ws_bytes, &ctiles, &dd, &desc);
   if (ws_bytes < need) {
     set_error("sample_layer: workspace %zu < %zu", ws_bytes, need);
     return GNS_EINVAL;
@@ -985,6 +1052,7 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.dbits = dd.bits;
   a.dsum = dd.sum;
   a.stream_len = g_stream_len;
+  a.desc = desc;
   a.b = *block;
   const unsigned tiles = (unsigned)((max_dst + kCntBlock * kCntItems - 1) / (kCntBlock * kCntItems)) + 1;
   GNS_CUDA(cudaMemsetAsync(block->counts, 0, GNS_CNT_N * sizeof(int32_t), stream));

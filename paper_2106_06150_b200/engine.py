@@ -271,14 +271,21 @@ class GraphedTrainer:
             cur.wait_event(ev)
 
     # -- cache + capture ------------------------------------------------------------
-    def _refresh_cache(self, epoch: int):
+    def _refresh_cache(self, epoch: int) -> bool:
+        """pool.py:109-135; returns True when device addresses the captured
+        graphs use changed (they must be re-captured)."""
         if self.cfg.strategy != "GNS":
-            return
+            return False
         if self._probs is None:
             self._probs = cache_probs(self.g, self.cfg)
         cs = int(round(self.cfg.cache_frac * self.g.num_nodes))
-        self.cache = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch,
-                                           rng_seed=[self.cfg.seed, _CACHE, epoch])
+        seed = [self.cfg.seed, _CACHE, epoch]
+        moved = True
+        if self.cache is not None and self.placement == "device":
+            # in place: same buffers, so the step graphs stay valid
+            moved = not cache_mod.refresh_cache(self.cache, self.g, self._probs, cs, epoch, seed)
+        else:
+            self.cache = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch, rng_seed=seed)
         if self.cfg.weight_policy == "gns-exact" and self._tables is None:
             self._tables = exact_tables(self.g, self.cfg, self._probs, cs)
         if self.placement == "mixed":
@@ -292,6 +299,7 @@ class GraphedTrainer:
                           ids.numel(), self.dims[0], self.cache_table.data_ptr(), _lib.stream_ptr(self.side))
                 self.cache.mask_word_rank()
             self.side.synchronize()
+        return moved
 
     def _set_step(self, slot: int, epoch: int, index: int | None):
         b = self.cfg.batch_size
@@ -461,8 +469,7 @@ class GraphedTrainer:
 
     def _begin(self, epoch: int, refresh: bool):
         torch.cuda.synchronize()
-        if refresh:
-            self._refresh_cache(epoch)
+        if refresh and self._refresh_cache(epoch):
             self._free_execs()
         self.adam_t.fill_(self.model.step_count)
 

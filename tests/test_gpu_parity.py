@@ -702,9 +702,18 @@ def test_graphed_trainer_matches_eager(P):
     wg, bg_ = tr.model.export()
     for a, b in zip(we + be, wg + bg_):
         np.testing.assert_allclose(a, b, rtol=1e-2, atol=1e-4)
-    # a second epoch re-draws the cache and re-captures
-    n2 = tr.run_epoch(1)
+    # a second epoch re-draws the cache in place (the captured graphs stay
+    # valid) and keeps tracking the eager pool (which builds a new cache)
+    ref2 = [float(eager.train_step(it.minibatch, g, tc)) for it in pool.iter_epoch(1)]
+    execs = dict(tr._execs)
+    losses2 = []
+    n2 = tr.run_epoch(1, on_step=lambda e, i, k: losses2.append(tr.loss_value()))
     assert n2 == len(losses)
+    assert tr._execs.keys() == execs.keys() and all(tr._execs[k][1].value == execs[k][1].value for k in execs)
+    assert tr.cache.epoch == 1 and pool.cache.epoch == 1
+    assert torch.equal(tr.cache.nodes.ids, pool.cache.nodes.ids)
+    assert torch.equal(tr.cache.cached_indices, pool.cache.cached_indices)
+    np.testing.assert_allclose(losses2, ref2, rtol=2e-3)
 
 
 # ---- random-walk cache distribution -----------------------------
