@@ -335,6 +335,24 @@ GNS_API int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_
                                     int64_t max_edges, int64_t pad_rows, const void* z_mask, void* db,
                                     void* dh, int64_t ld_dh, void* ws, size_t ws_bytes, void* stream);
 
+/* The hidden-layer pair with a compact relu' mask: gns_spmm_fwd_bits is
+ * gns_spmm_fwd(dtype 0, GNS_SPMM_RELU_INPUT) that also writes, for every h
+ * row it reads, the row's relu' bits (word blk*4+q, bit l <-> element
+ * 4*(blk*32+l)+q; gns_relu_bits_size(rows, dim) bytes); every src row of a
+ * block is read (as a dst self row or an edge source).
+ * gns_spmm_bwd_transposed_bits is gns_spmm_bwd_transposed(dtype 0) with the
+ * mask taken from those bits instead of the pre-activation rows z (32 bytes
+ * instead of dim*4 per row); results are identical. */
+GNS_API size_t gns_relu_bits_size(int64_t rows, int32_t dim);
+GNS_API int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block_t* block,
+                              int64_t max_dst, int64_t pad_rows, float* cat, int64_t ld_cat,
+                              uint32_t* relu_bits, void* stream);
+GNS_API int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim,
+                                         const gns_block_t* block, int64_t max_dst, int64_t max_src,
+                                         int64_t max_edges, int64_t pad_rows, const uint32_t* relu_bits,
+                                         float* db, float* dh, int64_t ld_dh, void* ws, size_t ws_bytes,
+                                         void* stream);
+
 /* relu backward fused with the bias gradient (model.py:218,220):
  * dz = (z > 0) ? dh : 0 (skipped when z == NULL: the output layer), db[c] =
  * sum over rows of dz[:, c] in a fixed order (deterministic).  n = *n_dev if

@@ -185,6 +185,18 @@ __device__ __forceinline__ V ldv(const V* p) {
   return v;
 }
 
+// relu' bits of a float32 row as the forward reads it (MASK variants): word
+// blk*4+q, bit l <-> element 4*(blk*32+l)+q, so lane l of a backward warp
+// finds its chunk's four bits at the same bit position of four words.
+// Written by lanes 0..3 after four ballots; every lane must call it.
+__device__ __forceinline__ void put_relu_bits(uint32_t* __restrict__ mrow, int blk, const float4& v, bool valid) {
+  const unsigned b0 = __ballot_sync(GNS_FULL, valid && v.x > 0.f), b1 = __ballot_sync(GNS_FULL, valid && v.y > 0.f);
+  const unsigned b2 = __ballot_sync(GNS_FULL, valid && v.z > 0.f), b3 = __ballot_sync(GNS_FULL, valid && v.w > 0.f);
+  const int lane = threadIdx.x & 31;
+  if (lane < 4) mrow[blk * 4 + lane] = lane == 0 ? b0 : lane == 1 ? b1 : lane == 2 ? b2 : b3;
+}
+__device__ __forceinline__ void put_relu_bits(uint32_t*, int, const double2&, bool) {}
+
 // RELU: the input rows are the previous layer's pre-activations z and
 // relu(z) (model.py:156) is applied on load instead of being materialised.
 // Rows [n, pad_rows) of cat are zero-filled (static-capacity GEMMs).
@@ -194,12 +206,19 @@ __device__ __forceinline__ V ldv(const V* p) {
 // the neighbours, dst_ids[r] for the self row — so features[input_nodes] is
 // never materialised.  src_nodes is sorted, so ordering a row's edges by node
 // id is the same as ordering them by edge_src: the sums are bit-identical.
-template <typename T, int CH, bool RELU, bool GATHER = false>
+//
+// MASK (float32 with RELU): also writes the relu' bits of every h row it
+// reads (put_relu_bits, (dv+31)/32*4 words per row) for the backward, which
+// then reads 32 bytes per row instead of the whole pre-activation row.  Every
+// src row of a block is a dst (self) row or an edge source, so every row the
+// backward needs gets its bits.
+template <typename T, int CH, bool RELU, bool GATHER = false, bool MASK = false>
 __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restrict__ h, int64_t ld_h, int dim,
                                                               BlockView bv, T* __restrict__ cat, int64_t ld_cat,
                                                               int64_t pad_rows,
                                                               const int32_t* __restrict__ edge_node = nullptr,
-                                                              const int32_t* __restrict__ dst_ids = nullptr) {
+                                                              const int32_t* __restrict__ dst_ids = nullptr,
+                                                              uint32_t* __restrict__ relu_bits = nullptr) {
   const int32_t* __restrict__ eidx = GATHER ? edge_node : bv.edge_src;
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
@@ -261,7 +280,22 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
     const T norm = (T)max(bv.dst_degree[r], 1);
     const V* hs = reinterpret_cast<const V*>(h + (int64_t)(GATHER ? dst_ids[r] : bv.self_pos[r]) * ld_h);
     V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
-    for (int c = lane; c < dv; c += 32) crow[c] = ldv<V, RELU>(hs + c);
+    const int mw = ((dv + 31) >> 5) * 4;
+    if constexpr (MASK) {
+      uint32_t* mrow = relu_bits + (int64_t)bv.self_pos[r] * mw;
+      for (int c0 = 0; c0 < dv; c0 += 32) {
+        const int c = c0 + lane;
+        V v;
+        vzero(v);
+        if (c < dv) {
+          v = ldv<V, RELU>(hs + c);
+          crow[c] = v;
+        }
+        put_relu_bits(mrow, c0 >> 5, v, c < dv);
+      }
+    } else {
+      for (int c = lane; c < dv; c += 32) crow[c] = ldv<V, RELU>(hs + c);
+    }
     for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
       V acc[CH];
 #pragma unroll
@@ -282,6 +316,14 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
           vfma<true>(acc[j], w0, x0[j]);
           vfma<true>(acc[j], w1, x1[j]);
         }
+        if constexpr (MASK) {
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int c = c0 + lane + 32 * j;
+            put_relu_bits(relu_bits + (int64_t)s_idx[wib][t] * mw, (c0 >> 5) + j, x0[j], c < dv);
+            put_relu_bits(relu_bits + (int64_t)s_idx[wib][t + 1] * mw, (c0 >> 5) + j, x1[j], c < dv);
+          }
+        }
       }
       if (t < L) {
         const V* r0 = reinterpret_cast<const V*>(h + (int64_t)s_idx[wib][t] * ld_h);
@@ -289,7 +331,13 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int c = c0 + lane + 32 * j;
-          if (c < dv) vfma<true>(acc[j], w0, ldv<V, RELU>(r0 + c));
+          V x;
+          vzero(x);
+          if (c < dv) {
+            x = ldv<V, RELU>(r0 + c);
+            vfma<true>(acc[j], w0, x);
+          }
+          if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)s_idx[wib][t] * mw, (c0 >> 5) + j, x, c < dv);
         }
       }
 #pragma unroll
@@ -504,14 +552,17 @@ __device__ __forceinline__ T div_norm(T x, T d);
 template <> __device__ __forceinline__ float div_norm<float, false>(float x, float d) { return __fdiv_rn(x, d); }
 template <> __device__ __forceinline__ double div_norm<double, true>(double x, double d) { return DDIV(x, d); }
 
-template <typename T, int CH>
+// BITS: the relu' mask comes from the forward's put_relu_bits words
+// (relu_bits, 32 B per row at D = 256) instead of the pre-activation rows.
+template <typename T, int CH, bool BITS = false>
 __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restrict__ dcat, int64_t ld_dcat, int dim,
                                                               BlockView bv, const int32_t* __restrict__ tptr,
                                                               const uint64_t* __restrict__ tkeys,
                                                               const int32_t* __restrict__ self_of,
                                                               T* __restrict__ dh, int64_t ld_dh, int64_t pad_rows,
                                                               const T* __restrict__ zmask,
-                                                              T* __restrict__ colpart) {
+                                                              T* __restrict__ colpart,
+                                                              const uint32_t* __restrict__ relu_bits = nullptr) {
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   constexpr bool EXACT = sizeof(T) == 8;
@@ -527,9 +578,12 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
   for (int j = 0; j < CH; ++j)
 #pragma unroll
     for (int q = 0; q < VW; ++q) colacc[j][q] = (T)0;
+  const int mw = ((dv + 31) >> 5) * 4;
   for (int64_t s = gw; s < n; s += nw) {
     const int b = tptr[s], e_end = tptr[s + 1];
     const int sd = self_of[s];
+    uint32_t my_bits = 0;   // lane i < mw holds relu-bit word i of row s
+    if constexpr (BITS) my_bits = lane < mw ? relu_bits[s * mw + lane] : 0u;
     for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
       T acc[CH][VW];
 #pragma unroll
@@ -570,6 +624,11 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
 #pragma unroll
       for (int j = 0; j < CH; ++j) {
         const int c = c0 + lane + 32 * j;
+        uint32_t wq[VW];
+        if constexpr (BITS) {   // every lane takes part in the shuffles
+#pragma unroll
+          for (int q = 0; q < VW; ++q) wq[q] = __shfl_sync(GNS_FULL, my_bits, ((c0 >> 5) + j) * 4 + q);
+        }
         if (c >= dv) continue;
         if (srow) {
           V g = srow[c];
@@ -582,7 +641,10 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
         }
         V out;
         T* op = reinterpret_cast<T*>(&out);
-        if (zmask) {
+        if constexpr (BITS) {
+#pragma unroll
+          for (int q = 0; q < VW; ++q) op[q] = ((wq[q] >> lane) & 1u) ? acc[j][q] : (T)0;
+        } else if (zmask) {
           V zv = reinterpret_cast<const V*>(zmask + s * ld_dh)[c];
           const T* zp = reinterpret_cast<const T*>(&zv);
 #pragma unroll
@@ -1013,6 +1075,65 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
   else GNS_FWDG(4);
 #undef GNS_FWDG
   return check_launch("spmm_fwd_gather");
+}
+
+size_t gns_relu_bits_size(int64_t rows, int32_t dim) {
+  return (size_t)(rows > 0 ? rows : 1) * (size_t)(((dim / 4 + 31) / 32) * 4) * sizeof(uint32_t);
+}
+
+int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block_t* block, int64_t max_dst,
+                      int64_t pad_rows, float* cat, int64_t ld_cat, uint32_t* relu_bits, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (max_dst <= 0 && pad_rows <= 0) return GNS_OK;
+  if (dim % 4 || ld_h % 4 || ld_cat % 4) {
+    set_error("spmm_fwd_bits: dim/strides must be multiples of 4");
+    return GNS_EINVAL;
+  }
+  long long rows = max_dst > pad_rows ? max_dst : pad_rows;
+  int grid = grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)num_sms() * 8);
+  BlockView bv = view_of(block);
+  const int dv = dim / 4;
+#define GNS_FWDB(CH)                                                                                             \
+  spmm_fwd_kernel<float, CH, true, false, true><<<grid, kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat, \
+                                                                                pad_rows, nullptr, nullptr,   \
+                                                                                relu_bits)
+  if (dv <= 32) GNS_FWDB(1);
+  else if (dv <= 64) GNS_FWDB(2);
+  else GNS_FWDB(4);
+#undef GNS_FWDB
+  return check_launch("spmm_fwd_bits");
+}
+
+int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim, const gns_block_t* block,
+                                 int64_t max_dst, int64_t max_src, int64_t max_edges, int64_t pad_rows,
+                                 const uint32_t* relu_bits, float* db, float* dh, int64_t ld_dh, void* ws,
+                                 size_t ws_bytes, void* stream_) {
+  (void)max_dst;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  BwdWs w;
+  size_t need = bwd_ws(max_src, max_edges, dim, ws, ws_bytes, &w);
+  if (need > ws_bytes) {
+    set_error("spmm_bwd_bits: workspace %zu < %zu", ws_bytes, need);
+    return GNS_EINVAL;
+  }
+  if (dim % 4 || ld_dcat % 4 || ld_dh % 4 || dim > 512) {
+    set_error("spmm_bwd_bits: dim/strides must be multiples of 4 and dim <= 512");
+    return GNS_EINVAL;
+  }
+  BlockView bv = view_of(block);
+  int g2 = grid_for(((max_src > pad_rows ? max_src : pad_rows) * 32 + 255) / 256, (long long)num_sms() * 8);
+  const int dv = dim / 4;
+#define GNS_BWDB(CH)                                                                                             \
+  spmm_bwd_kernel<float, CH, true><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,       \
+                                                                  w.self_of, dh, ld_dh, pad_rows, nullptr,       \
+                                                                  db ? (float*)w.colpart : nullptr, relu_bits)
+  if (dv <= 32) GNS_BWDB(1);
+  else if (dv <= 64) GNS_BWDB(2);
+  else GNS_BWDB(4);
+#undef GNS_BWDB
+  GNS_TRY(check_launch("spmm_bwd_bits"));
+  if (db) colsum_final_kernel<float><<<(dim + 7) / 8, 256, 0, stream>>>((const float*)w.colpart, g2, dim, db);
+  return check_launch("spmm_bwd_bits colsum");
 }
 
 int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_t flags, const gns_block_t* block,

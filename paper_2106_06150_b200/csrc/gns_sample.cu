@@ -34,6 +34,8 @@ constexpr int kHubLen = 2048;
 constexpr int kThreadLen = 16;    // rows scanning <= 16 positions: one thread per row, register sort
 constexpr int kStreamK = 8;       // streaming top-k tier: take <= 8 and <= stream_len positions
 static int g_stream_len = 32;     // (gns_tune "stream_len", <= 2047)
+static int g_sampler_ctas = 0;    // (gns_tune "sampler_ctas") cap grid-stride sampler grids at this many CTAs
+                                  // per SM (0 = no cap): leaves SM room to the concurrent training branch
 constexpr int kHubBlock = 512;
 constexpr int kHubCap = 512;
 constexpr int kMaxFanout = 128;
@@ -972,7 +974,8 @@ static int run_enumerate(const DedupWs& d, int32_t* out, int32_t* out_n, cudaStr
 static int run_relabel(const DedupWs& d, const int32_t* seeds, const int32_t* n_seeds_dev, int64_t max_dst,
                        gns_block_t* block, int64_t max_edges, cudaStream_t stream) {
   GNS_TRY(run_enumerate(d, block->src_nodes, block->counts + GNS_CNT_SRC, stream));
-  int grid = grid_for((max_dst + max_edges + 255) / 256 + 1, (long long)num_sms() * 16);
+  int grid = grid_for((max_dst + max_edges + 255) / 256 + 1,
+                      (long long)num_sms() * (g_sampler_ctas ? g_sampler_ctas : 16));
   relabel_kernel<<<grid, 256, 0, stream>>>(d.rank2, seeds, n_seeds_dev, block->edge_node, block->counts,
                                            block->self_pos, block->edge_src);
   return check_launch("relabel");
@@ -1064,12 +1067,14 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   // calling stream, warp and hub tiers on a forked branch, concurrently
   Fork fk;
   GNS_TRY(fork_begin(stream, &fk));
-  int tgrid = grid_for((2 * max_dst + 255) / 256, (long long)sms * 16);
+  const long long cap16 = (long long)sms * (g_sampler_ctas ? g_sampler_ctas : 16);
+  const long long cap8 = (long long)sms * (g_sampler_ctas ? g_sampler_ctas : 8);
+  int tgrid = grid_for((2 * max_dst + 255) / 256, cap16);
   sample_stream_kernel<<<tgrid, 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_stream"));
   sample_thread_kernel<<<tgrid, 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_thread"));
-  int grid = grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock, (long long)sms * 8);
+  int grid = grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock, cap8);
   sample_warp_kernel<<<grid, kSampBlock, 0, fk.aux>>>(a);
   GNS_TRY(check_launch("sample_warp"));
   sample_hub_kernel<<<sms, kHubBlock, 0, fk.aux>>>(a);
@@ -1083,6 +1088,10 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
 int gns_sample_tune(const char* name, int32_t value) {
   if (!strcmp(name, "stream_len") && value >= 0 && value < 2048) {
     g_stream_len = value;
+    return GNS_OK;
+  }
+  if (!strcmp(name, "sampler_ctas") && value >= 0) {
+    g_sampler_ctas = value;
     return GNS_OK;
   }
   return GNS_EINVAL;

@@ -147,6 +147,11 @@ class GraphedTrainer:
                                                                             dims[li]), dev, zero=True)
                               for li in range(1, L)] for _ in self.slots]
         self.ws_xent = _lib.workspace(8 * max(self.cap_dst[L - 1], 1024), dev)
+        # relu' bits of z[li-1] written by layer li's forward, read by its
+        # backward (gns_spmm_fwd_bits / gns_spmm_bwd_transposed_bits)
+        self.relu_bits = [None] + [
+            _lib.workspace(lib.gns_relu_bits_size(max(self.cap_src[li], self.npad[li - 1]), dims[li]), dev)
+            for li in range(1, L)]
         self.loss = self.model.loss_dev
 
     # -- one training step on a slot (captured) ------------------------------------
@@ -195,10 +200,13 @@ class GraphedTrainer:
                     _lib.call("gns_spmm_fwd_gather", tab.data_ptr(), tab.stride(0), d_in, blocks[0].cblock,
                               dst_ids.data_ptr(), self.cap_dst[0], self.npad[0], self.cat[0].data_ptr(),
                               self.cat[0].stride(0), s)
+                elif li > 0:
+                    _lib.call("gns_spmm_fwd_bits", h.data_ptr(), h.stride(0), d_in, blocks[li].cblock,
+                              self.cap_dst[li], self.npad[li], self.cat[li].data_ptr(), self.cat[li].stride(0),
+                              self.relu_bits[li].data_ptr(), s)
                 else:
-                    _lib.call("gns_spmm_fwd", 0, h.data_ptr(), h.stride(0), d_in, 1 if li > 0 else 0,
-                              blocks[li].cblock, self.cap_dst[li], self.npad[li], self.cat[li].data_ptr(),
-                              self.cat[li].stride(0), s)
+                    _lib.call("gns_spmm_fwd", 0, h.data_ptr(), h.stride(0), d_in, 0, blocks[li].cblock,
+                              self.cap_dst[li], self.npad[li], self.cat[li].data_ptr(), self.cat[li].stride(0), s)
                 if ev is not None:
                     _lib.call("gns_record_event_external", ev[3].cuda_event, s)
                 torch.addmm(m.biases[li], self.cat[li][:self.cap_dst[li]], m.weights[li], out=self.z[li])
@@ -219,10 +227,13 @@ class GraphedTrainer:
                     break
                 torch.mm(self.dz[li][:self.cap_dst[li]], m.weights[li].t(), out=self.dcat[li])
                 # transpose SpMM fused with the previous layer's relu' and bias grad
+                # transpose SpMM fused with the previous layer's relu' (from the
+                # forward's bits) and bias grad.  dz rows past the count are not
+                # zeroed: the weight gradient multiplies them by cat's zero rows
                 ws = self.tws[slot][li]
-                _lib.call("gns_spmm_bwd_transposed", 0, self.dcat[li].data_ptr(), self.dcat[li].stride(0),
+                _lib.call("gns_spmm_bwd_transposed_bits", self.dcat[li].data_ptr(), self.dcat[li].stride(0),
                           self.dims[li], blocks[li].cblock, self.cap_dst[li], self.cap_src[li], self.cap_edges[li],
-                          self.npad[li - 1], self.z[li - 1].data_ptr(), m.gbiases[li - 1].data_ptr(),
+                          0, self.relu_bits[li].data_ptr(), m.gbiases[li - 1].data_ptr(),
                           self.dz[li - 1].data_ptr(), self.dz[li - 1].stride(0), ws.data_ptr(), ws.numel(), s)
         if with_adam:
             self._adam_dev()

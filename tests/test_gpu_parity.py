@@ -516,6 +516,40 @@ def test_spmm_bwd_f32_variants_identical(P, dim):
         _lib.call("gns_tune", b"spmm_bwd", 0)
 
 
+@pytest.mark.parametrize("dim", [16, 100, 256])
+def test_relu_bits_pair_equals_zmask_path(P, dim):
+    """gns_spmm_fwd_bits == gns_spmm_fwd(relu) and gns_spmm_bwd_transposed_bits
+    (mask from the forward's bits) == gns_spmm_bwd (mask from z), bit for bit."""
+    from paper_2106_06150_b200 import _lib
+    og, g, feats, mb, ref = _mb_and_features(P, dim=16)
+    lib = _lib.lib()
+    ws = _lib.workspace(1 << 24, "cuda")
+    for li, (bg, br) in enumerate(zip(mb.blocks, ref.blocks)):
+        nsrc, ndst = len(br.src_nodes), len(br.dst_nodes)
+        gen = torch.Generator(device="cuda").manual_seed(30 + li)
+        z = torch.randn((nsrc, dim), device="cuda", generator=gen)
+        a = torch.empty((ndst + 2, 2 * dim), device="cuda")
+        b = torch.empty((ndst + 2, 2 * dim), device="cuda")
+        bits = torch.zeros(lib.gns_relu_bits_size(nsrc, dim) // 4, dtype=torch.int32, device="cuda")
+        _lib.call("gns_spmm_fwd", 0, z.data_ptr(), dim, dim, 1, bg._c, ndst, ndst + 2, a.data_ptr(), 2 * dim,
+                  _lib.stream_ptr())
+        _lib.call("gns_spmm_fwd_bits", z.data_ptr(), dim, dim, bg._c, ndst, ndst + 2, b.data_ptr(), 2 * dim,
+                  bits.data_ptr(), _lib.stream_ptr())
+        assert torch.equal(a, b), li
+        dcat = torch.randn((ndst, 2 * dim), device="cuda", generator=gen)
+        d1 = torch.empty((nsrc, dim), device="cuda")
+        d2 = torch.empty((nsrc, dim), device="cuda")
+        db1 = torch.empty(dim, device="cuda")
+        db2 = torch.empty(dim, device="cuda")
+        _lib.call("gns_spmm_bwd", 0, dcat.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0,
+                  z.data_ptr(), db1.data_ptr(), d1.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        _lib.call("gns_spmm_bwd_transposed_bits", dcat.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges,
+                  0, bits.data_ptr(), db2.data_ptr(), d2.data_ptr(), dim, ws.data_ptr(), ws.numel(),
+                  _lib.stream_ptr())
+        assert torch.equal(d1, d2), li
+        assert torch.equal(db1, db2), li
+
+
 def test_full_batch_equivalence(P):
     """with k >= max degree the sampled forward equals the
     full-neighbourhood forward (NS keeps every neighbour, weight 1)."""
