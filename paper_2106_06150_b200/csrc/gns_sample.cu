@@ -34,6 +34,7 @@ constexpr int kHubLen = 2048;
 constexpr int kThreadLen = 16;    // rows scanning <= 16 positions: one thread per row, register sort
 constexpr int kStreamK = 8;       // streaming top-k tier: take <= 8 and <= stream_len positions
 static int g_stream_len = 32;     // (gns_tune "stream_len", <= 2047)
+static int g_thread_len = 0;      // (gns_tune "thread_len", <= 16; 0 = no sorting-network tier: measured best)
 static int g_sampler_ctas = 0;    // (gns_tune "sampler_ctas") cap grid-stride sampler grids at this many CTAs
                                   // per SM (0 = no cap): leaves SM room to the concurrent training branch
 constexpr int kHubBlock = 512;
@@ -61,6 +62,7 @@ struct LayerArgs {
   uint32_t* dbits;  // dedup bitmap (bit v of word v>>5); NULL = no fused marking
   uint32_t* dsum;   // summary bitmap (bit w of word w>>5 set iff dbits[w] != 0)
   int stream_len;   // rows up to this many positions with take <= kStreamK: streaming tier
+  int thread_len;   // other rows up to this many positions (<= kThreadLen): sorting-network tier
   struct RowDesc* desc;  // per-row descriptors (count pass -> selection kernels)
   gns_block_t b;
 };
@@ -167,10 +169,10 @@ __device__ __forceinline__ RowInfo row_info(const LayerArgs& a, int64_t r) {
 // selections it makes: 3 = thread per item, streaming top-k (take <= 8,
 // <= 64 positions), 0 = thread per item, sorting network (<= 16 positions),
 // 1 = warp per item (<= kHubLen), 2 = CTA per item (hub)
-__device__ __forceinline__ int phase_tier(int len, int take, int stream_len) {
+__device__ __forceinline__ int phase_tier(int len, int take, int stream_len, int thread_len) {
   if (take <= kStreamK && len <= stream_len) return 3;
   if (len > kHubLen) return 2;
-  if (len > kThreadLen) return 1;
+  if (len > thread_len) return 1;
   return 0;
 }
 
@@ -241,8 +243,8 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __g
       // (row, phase) work items into the tier lists (tier_slot); the two
       // phases of a row are independent (their output offsets come from
       // the scan), so they run concurrently.  One atomic per warp and tier.
-      const int t0 = on && m > 0 ? phase_tier(nc, m, a.stream_len) : -1;
-      const int t1 = on && fill > 0 ? phase_tier(deg, fill, a.stream_len) : -1;
+      const int t0 = on && m > 0 ? phase_tier(nc, m, a.stream_len, a.thread_len) : -1;
+      const int t1 = on && fill > 0 ? phase_tier(deg, fill, a.stream_len, a.thread_len) : -1;
       int h0 = 0, h1 = 0;
       warp_append_tiers(a.b.counts, t0, t1, h0, h1);
       if (t0 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t0, h0)] = (int32_t)(r << 1);
@@ -1055,6 +1057,7 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.dbits = dd.bits;
   a.dsum = dd.sum;
   a.stream_len = g_stream_len;
+  a.thread_len = g_thread_len;
   a.desc = desc;
   a.b = *block;
   const unsigned tiles = (unsigned)((max_dst + kCntBlock * kCntItems - 1) / (kCntBlock * kCntItems)) + 1;
@@ -1088,6 +1091,10 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
 int gns_sample_tune(const char* name, int32_t value) {
   if (!strcmp(name, "stream_len") && value >= 0 && value < 2048) {
     g_stream_len = value;
+    return GNS_OK;
+  }
+  if (!strcmp(name, "thread_len") && value >= 0 && value <= kThreadLen) {
+    g_thread_len = value;
     return GNS_OK;
   }
   if (!strcmp(name, "sampler_ctas") && value >= 0) {

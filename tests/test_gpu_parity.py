@@ -194,6 +194,33 @@ def test_minibatch_bit_exact_vs_oracle_hubs(P, strategy, cache_only, frac):
         assert_mb_equal(mb, ref, f"{strategy}-{cache_only}-{index}")
 
 
+@pytest.mark.parametrize("tune", [{"thread_len": 16, "stream_len": 0}, {"thread_len": 16, "stream_len": 32},
+                                  {"thread_len": 0, "stream_len": 64}, {"sampler_ctas": 1}])
+def test_minibatch_selection_tiers_all_exact(P, tune):
+    """Every routing of (row, phase) items over the selection tiers (sorting
+    network, streaming top-k, warp, CTA) gives the reference's blocks."""
+    from paper_2106_06150_b200 import _lib
+    og = _hub_graph(5000, 17)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=400, input_layer_cache_only=False,
+                          cache_mode="degree", cache_frac=0.05, seed=3)
+    cs = O.cache_size_for(og, cfg.cache_frac)
+    cache = P.build_cache(g, P.degree_probs(g), cs, rng_seed=[3, 33, 0])
+    oc = O.build_cache(og, O.degree_probs(og), cs, seed=3, epoch=0)
+    targets = np.random.default_rng(2).choice(og.num_nodes, 400, replace=False)
+    defaults = {"thread_len": 0, "stream_len": 32, "sampler_ctas": 0}
+    try:
+        for k, v in tune.items():
+            _lib.call("gns_tune", k.encode(), v)
+        for index in range(2):
+            mb = P.build_minibatch(g, cache, targets, cfg, P.BatchRng(3, 0, index))
+            ref = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(3, 0, index))
+            assert_mb_equal(mb, ref, f"{tune}-{index}")
+    finally:
+        for k, v in defaults.items():
+            _lib.call("gns_tune", k.encode(), v)
+
+
 def test_minibatch_layers_with_large_capacities(P):
     """Layers whose capacities differ by > 32K rows share one sampler
     workspace: consecutive batches through the same MiniBatchSampler stay
