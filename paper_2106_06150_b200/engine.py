@@ -533,7 +533,18 @@ class GraphedTrainer:
         self._begin(epoch, self.cfg.strategy == "GNS" and self.cache is None)
         S = self.S
         losses = []
-        lh = torch.zeros(S, dtype=torch.float64).pin_memory()
+        # double-buffered loss read-back: replay g+1 is queued before the host
+        # waits for replay g's losses, so the GPU never idles on the host
+        lh = [torch.zeros(S, dtype=torch.float64).pin_memory() for _ in range(2)]
+        pending = []
+
+        def drain():
+            ev, buf, first, r = pending.pop(0)
+            ev.synchronize()
+            for j in range(r):
+                losses.append(float(buf[j]))
+                if on_loss is not None:
+                    on_loss(first + j, losses[-1])
 
         def put(slot, k):
             if self.done[slot] is not None:
@@ -559,17 +570,17 @@ class GraphedTrainer:
                 put(sl, b0 + S + j)
             with torch.cuda.stream(self.main):
                 self._replay(p, r)
-                lh.copy_(self.step_loss, non_blocking=True)
+                lh[p].copy_(self.step_loss, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self.main)
                 for sl in self._group(1 - p):
                     self.done[sl] = ev
-            ev.synchronize()
             self.model.step_count += r
-            for j in range(r):
-                losses.append(float(lh[j]))
-                if on_loss is not None:
-                    on_loss(b0 + j, losses[-1])
+            pending.append((ev, lh[p], b0, r))
+            if len(pending) > 1:
+                drain()
+        while pending:
+            drain()
         return losses
 
     def check_errors(self):

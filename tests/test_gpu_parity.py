@@ -777,6 +777,29 @@ def test_graphed_trainer_matches_eager(P):
     np.testing.assert_allclose(losses2, ref2, rtol=2e-3)
 
 
+def test_graphed_trainer_run_host_matches_eager(P):
+    """The end-to-end API (host target arrays copied into the step graph,
+    every step's loss read back, one replay kept in flight) trains exactly
+    the given batches: losses track the eager model on the same batches."""
+    og = _hub_graph(4000, 23)
+    rng = np.random.default_rng(1)
+    feats = rng.normal(size=(og.num_nodes, 16)).astype(np.float32)
+    labels = rng.integers(0, 5, og.num_nodes).astype(np.int32)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices, features=feats, labels=labels)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=200, cache_frac=0.05, cache_mode="degree",
+                          seed=4)
+    tc = P.TrainConfig(lr=0.003)
+    batches = [rng.choice(og.num_nodes, 200, replace=False) for _ in range(7)]
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0, host_targets=True)
+    got = tr.run_host(batches, epoch=0)
+    eager = P.GraphSAGE((16, 32, 5), seed=0)
+    ref = [float(eager.train_step(P.build_minibatch(g, tr.cache, b, cfg, P.BatchRng(4, 0, k)), g, tc))
+           for k, b in enumerate(batches)]
+    assert len(got) == len(batches)
+    np.testing.assert_allclose(got, ref, rtol=2e-3)
+
+
 # ---- random-walk cache distribution (SURVEY.md §8(f)1) -----------------------------
 
 def test_random_walk_probs(P, golden):
