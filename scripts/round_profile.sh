@@ -16,8 +16,10 @@ for c in products oag cfg1; do
 done
 ncu --metrics gpu__time_duration.sum --clock-control none -s 1500 -c 300 --csv --log-file $O/launches_papers100m.csv \
     python bench.py --steps 20 --warmup 10 --no-cpu-baseline --e2e-steps 0 > $O/ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"spmm_fwd_narrow|spmm_bwd_kernel|sample_warp|sample_stream" \
-    -s 40 -c 8 -o $O/ncu_full_step python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $O/ncu_full_step.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"spmm_fwd_narrow|spmm_bwd_kernel|spmm_fwd_kernel" \
+    -s 6 -c 5 -o $O/ncu_full_step python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $O/ncu_full_step.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"sample_warp|sample_stream|layer_count_reduce|enumerate_apply" \
+    -s 24 -c 8 -o $O/ncu_full_sampler python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $O/ncu_full_sampler.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"gather_f32x4" -s 2 -c 2 -o $O/ncu_full_gather \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $O/ncu_full_gather.log 2>&1
 ls -la $O
