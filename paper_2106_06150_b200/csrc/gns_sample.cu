@@ -90,35 +90,41 @@ __device__ __forceinline__ int64_t tier_slot(int64_t max_dst, int tier, int h) {
   return tier == 0 ? h : tier == 3 ? 2 * max_dst + h : tier == 1 ? 4 * max_dst + h : 6 * max_dst - 1 - h;
 }
 
-// Append each active lane's phase-0 item (tier t0, -1 = none) and phase-1
-// item (tier t1) to its tier list; returns the list positions.  One atomic
-// per tier and warp, issued by lanes 0..kTiers-1 together.
-__device__ __forceinline__ void warp_append_tiers(int32_t* counts, int t0, int t1, int& h0, int& h1) {
+// Append each active lane's NI (row, phase) items (tier[i] = -1: none) to
+// their tier lists; returns the list positions.  One atomic per tier and
+// warp for all of them, the kTiers atomics issued together; item i of lane l
+// lands after the items i' < i of every lane and item i of lanes l' < l.
+template <int NI>
+__device__ __forceinline__ void warp_append_tiers(int32_t* counts, const int (&tier)[NI], int (&h)[NI]) {
   const unsigned act = __activemask();
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  unsigned m0[kTiers], m1[kTiers];
-#pragma unroll
-  for (int t = 0; t < kTiers; ++t) {
-    m0[t] = __ballot_sync(act, t0 == t);
-    m1[t] = __ballot_sync(act, t1 == t);
-  }
-  // lane t (if active) reserves the slots of tier t; otherwise the lowest
-  // active lane does it
   const int first = __ffs(act) - 1;
+  int cnt[kTiers] = {0, 0, 0, 0};
+  int pre[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    pre[i] = 0;
+#pragma unroll
+    for (int t = 0; t < kTiers; ++t) {
+      const unsigned m = __ballot_sync(act, tier[i] == t);
+      if (tier[i] == t) pre[i] = cnt[t] + __popc(m & lt);
+      cnt[t] += __popc(m);
+    }
+  }
   int base[kTiers] = {0, 0, 0, 0};
 #pragma unroll
-  for (int t = 0; t < kTiers; ++t) {   // the atomics are independent: all in flight
-    const int cnt = __popc(m0[t]) + __popc(m1[t]);
+  for (int t = 0; t < kTiers; ++t) {   // independent atomics: all in flight
     const int owner = ((act >> t) & 1u) ? t : first;
-    if (lane == owner && cnt) base[t] = atomicAdd(tier_counter(counts, t), cnt);
+    if (lane == owner && cnt[t]) base[t] = atomicAdd(tier_counter(counts, t), cnt[t]);
   }
 #pragma unroll
   for (int t = 0; t < kTiers; ++t) {
     const int owner = ((act >> t) & 1u) ? t : first;
     const int bt = __shfl_sync(act, base[t], owner);
-    if (t0 == t) h0 = bt + __popc(m0[t] & lt);
-    if (t1 == t) h1 = bt + __popc(m0[t]) + __popc(m1[t] & lt);
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (tier[i] == t) h[i] = bt + pre[i];
   }
 }
 
@@ -216,6 +222,8 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __g
         }
       }
     }
+    // per-row values and plain stores (no memory dependence between rows)
+    int tier[2 * kCntItems];
 #pragma unroll
     for (int j = 0; j < kCntItems; ++j) {
       const long long r = base + j * kCntBlock + threadIdx.x;
@@ -237,18 +245,47 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __g
         d[0] = make_int4((int32_t)(uint64_t)s0[j], (int32_t)((uint64_t)s0[j] >> 32), (int32_t)(uint64_t)c0[j],
                          (int32_t)((uint64_t)c0[j] >> 32));
         d[1] = make_int4(node[j], deg, nc, 0);
-        if (a.dbits) mark_node(a.dbits, a.dsum, node[j]);
         tsum += v;
       }
       // (row, phase) work items into the tier lists (tier_slot); the two
       // phases of a row are independent (their output offsets come from
-      // the scan), so they run concurrently.  One atomic per warp and tier.
-      const int t0 = on && m > 0 ? phase_tier(nc, m, a.stream_len, a.thread_len) : -1;
-      const int t1 = on && fill > 0 ? phase_tier(deg, fill, a.stream_len, a.thread_len) : -1;
-      int h0 = 0, h1 = 0;
-      warp_append_tiers(a.b.counts, t0, t1, h0, h1);
-      if (t0 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t0, h0)] = (int32_t)(r << 1);
-      if (t1 >= 0) a.b.hub_rows[tier_slot(a.max_dst, t1, h1)] = (int32_t)((r << 1) | 1);
+      // the scan), so they run concurrently
+      tier[2 * j] = on && m > 0 ? phase_tier(nc, m, a.stream_len, a.thread_len) : -1;
+      tier[2 * j + 1] = on && fill > 0 ? phase_tier(deg, fill, a.stream_len, a.thread_len) : -1;
+    }
+    // dedup marks of the seeds: every row's bitmap probe, then every row's
+    // atomics, in flight together (mark_node's steps, batched)
+    if (a.dbits) {
+      uint32_t bw[kCntItems];
+#pragma unroll
+      for (int j = 0; j < kCntItems; ++j) {
+        const long long r = base + j * kCntBlock + threadIdx.x;
+        bw[j] = r < n ? __ldg(a.dbits + (node[j] >> 5)) : ~0u;
+      }
+      uint32_t old[kCntItems];
+#pragma unroll
+      for (int j = 0; j < kCntItems; ++j) {
+        const uint32_t mb = 1u << (node[j] & 31);
+        old[j] = ~0u;
+        if (!(bw[j] & mb)) old[j] = atomicOr(a.dbits + (node[j] >> 5), mb);
+      }
+#pragma unroll
+      for (int j = 0; j < kCntItems; ++j) {
+        const int32_t w = node[j] >> 5;
+        if (old[j] == 0u) atomicOr(a.dsum + (w >> 5), 1u << (w & 31));
+      }
+    }
+    // all 2*kCntItems (row, phase) items of the warp in one aggregated append
+    int h[2 * kCntItems];
+    warp_append_tiers<2 * kCntItems>(a.b.counts, tier, h);
+#pragma unroll
+    for (int j = 0; j < kCntItems; ++j) {
+      const long long r = base + j * kCntBlock + threadIdx.x;
+#pragma unroll
+      for (int ph = 0; ph < 2; ++ph) {
+        const int t = tier[2 * j + ph];
+        if (t >= 0) a.b.hub_rows[tier_slot(a.max_dst, t, h[2 * j + ph])] = (int32_t)((r << 1) | ph);
+      }
     }
   }
   tsum = block_sum<kCntBlock>(tsum, s_warp);
