@@ -459,9 +459,127 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel
   }
 }
 
+// Rows of 32 < dim/4 <= 32*CH float4 chunks (the hidden layers, D = 256:
+// CH = 2), float32, RELU on load: the narrow kernel's structure — lane-held
+// edges, shuffle ranks, G neighbour rows in flight — with CH chunks per lane,
+// and (MASK) the relu' bits of every row read (put_relu_bits) for the
+// backward.  Same ascending-source FMA order as spmm_fwd_kernel.
+template <int CH, int G, bool MASK>
+__global__ void __launch_bounds__(kSpmmBlock, 3) spmm_fwd_wide_kernel(const float* __restrict__ h, int64_t ld_h,
+                                                                       int dim, BlockView bv,
+                                                                       float* __restrict__ cat, int64_t ld_cat,
+                                                                       int64_t pad_rows,
+                                                                       uint32_t* __restrict__ relu_bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = bv.counts[GNS_CNT_DST];
+  const int64_t tm = (int64_t)(bv.row_scan[n] >> 32);
+  const int dv = dim >> 2;
+  const int mw = ((dv + 31) >> 5) * 4;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < n; r += nw) {
+    const uint64_t s0 = bv.row_scan[r], s1 = bv.row_scan[r + 1];
+    const int64_t self = (int64_t)bv.self_pos[r];
+    const float norm = (float)max(bv.dst_degree[r], 1);
+    const int64_t cb = (int64_t)(s0 >> 32), ce = (int64_t)(s1 >> 32);
+    const int64_t fb = tm + (int64_t)(s0 & 0xffffffffull), fe = tm + (int64_t)(s1 & 0xffffffffull);
+    const int nc = (int)(ce - cb), L = nc + (int)(fe - fb);
+    float4 xs[CH], acc[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int c = lane + 32 * j;
+      xs[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < dv) xs[j] = vrelu(reinterpret_cast<const float4*>(h + self * ld_h)[c]);
+    }
+    if constexpr (MASK) {
+#pragma unroll
+      for (int j = 0; j < CH; ++j) put_relu_bits(relu_bits + self * mw, j, xs[j], lane + 32 * j < dv);
+    }
+    float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
+    for (int t0 = 0; t0 < L; t0 += 32) {
+      // edges t0..t0+31 of the row in ascending source order: with L <= 32
+      // one round; longer rows rank each 32-edge window against all edges
+      const int m = min(32, L - t0);
+      int32_t idx = INT32_MAX;
+      float w = 0.f;
+      if (L <= 32) {
+        if (lane < L) {
+          const int64_t e = lane < nc ? cb + lane : fb + (lane - nc);
+          idx = bv.edge_src[e];
+          w = (float)bv.edge_weight[e];
+        }
+        int rank = 0;
+        for (int j = 0; j < L; ++j) rank += __shfl_sync(GNS_FULL, idx, j) < idx;
+        int src = 0;
+        for (int u = 0; u < L; ++u) {
+          const unsigned mm = __ballot_sync(GNS_FULL, lane < L && rank == u);
+          if (lane == u) src = __ffs(mm) - 1;
+        }
+        idx = __shfl_sync(GNS_FULL, idx, src);
+        w = __shfl_sync(GNS_FULL, w, src);
+      } else {
+        // lane u < m finds the edge of rank t0 + u (distinct sources)
+        for (int i = 0; i < L; ++i) {
+          const int64_t e = i < nc ? cb + i : fb + (i - nc);
+          const int32_t v = bv.edge_src[e];
+          int rk = 0;
+          for (int j = lane; j < L; j += 32) {
+            const int64_t ej = j < nc ? cb + j : fb + (j - nc);
+            rk += bv.edge_src[ej] < v;
+          }
+          rk = warp_sum((unsigned)rk);
+          if (lane < m && rk == t0 + lane) {
+            idx = v;
+            w = (float)bv.edge_weight[e];
+          }
+        }
+      }
+      for (int t = 0; t < m; t += G) {
+        float4 x[G][CH];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const int32_t iu = __shfl_sync(GNS_FULL, idx, (t + u) & 31);
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int c = lane + 32 * j;
+            x[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t + u < m && c < dv) x[u][j] = vrelu(reinterpret_cast<const float4*>(h + (int64_t)iu * ld_h)[c]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const float wu = __shfl_sync(GNS_FULL, w, (t + u) & 31);
+          const int32_t iu = __shfl_sync(GNS_FULL, idx, (t + u) & 31);
+          if (t + u < m) {
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+              if (lane + 32 * j < dv) vfma<true>(acc[j], wu, x[u][j]);
+              if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)iu * mw, j, x[u][j], lane + 32 * j < dv);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int c = lane + 32 * j;
+      if (c < dv) {
+        crow[c] = xs[j];
+        crow[dv + c] = vdiv(acc[j], norm);
+      }
+    }
+  }
+  for (int64_t r = n + gw; r < pad_rows; r += nw) {
+    float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
+    for (int c = lane; c < 2 * dv; c += 32) crow[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // experiment knobs (gns_tune)
 static int g_tune_narrow = 1;  // narrow-row forward SpMM variant (0 = generic)
 static int g_tune_bwd = 0;     // 1 = short-chain float32 backward (slower on B200: occupancy), 0 = generic
+static int g_tune_wide = 1;    // hidden-layer forward: 1 = spmm_fwd_wide_kernel, 0 = generic
 
 // ---- SpMM backward -------------------------------------------------------------
 __global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of) {
@@ -507,21 +625,38 @@ __global__ void tscatter_kernel(BlockView bv, int32_t* __restrict__ cursor, cons
 
 // sort each transposed row by dst (ascending): registers for <= 32 entries,
 // an all-ascending bitonic network in place otherwise
-__global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uint64_t* __restrict__ tkeys) {
+// Also writes twn[t] = w_e / max(deg(dst_e), 1) in float32 for every sorted
+// entry — the float32 backward's per-edge coefficient, computed exactly as
+// that kernel would (IEEE division), so it reads one value instead of the
+// dependent weight + dst-degree loads.
+__device__ __forceinline__ void put_twn(BlockView bv, const uint64_t* a, int L, float* twn, int lane) {
+  for (int t = lane; t < L; t += 32) {
+    const uint64_t key = a[t];
+    const int32_t d = (int32_t)(key >> 32), e = (int32_t)(key & 0xffffffffu);
+    twn[t] = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
+  }
+}
+
+__global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uint64_t* __restrict__ tkeys,
+                             float* __restrict__ twn) {
   const int lane = threadIdx.x & 31;
   const int64_t n = bv.counts[GNS_CNT_SRC];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = gw; s < n; s += nw) {
     const int b = tptr[s], L = tptr[s + 1] - b;
-    if (L <= 1) continue;
+    if (L <= 0) continue;
     uint64_t* a = tkeys + b;
     if (L <= 32) {
       uint64_t x = lane < L ? a[lane] : ~0ull;
       int rank = 0;
       for (int j = 0; j < L; ++j) rank += __shfl_sync(GNS_FULL, x, j) < x;
       __syncwarp();
-      if (lane < L) a[rank] = x;
+      if (lane < L) {
+        a[rank] = x;
+        const int32_t d = (int32_t)(x >> 32), e = (int32_t)(x & 0xffffffffu);
+        twn[b + rank] = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
+      }
       __syncwarp();
       continue;
     }
@@ -544,6 +679,8 @@ __global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uin
         __syncwarp();
       }
     }
+    put_twn(bv, a, L, twn + b, lane);
+    __syncwarp();
   }
 }
 
@@ -562,7 +699,11 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
                                                               T* __restrict__ dh, int64_t ld_dh, int64_t pad_rows,
                                                               const T* __restrict__ zmask,
                                                               T* __restrict__ colpart,
-                                                              const uint32_t* __restrict__ relu_bits = nullptr) {
+                                                              const uint32_t* __restrict__ relu_bits = nullptr,
+                                                              const float* __restrict__ twn = nullptr) {
+  // BITS (float32): the per-edge coefficient comes from the transpose's twn
+  // and the self row of dcat is requested before the edge loop, so a row's
+  // chain is bounds -> (keys, coefficients, self row) -> dcat rows
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
   constexpr bool EXACT = sizeof(T) == 8;
@@ -590,12 +731,24 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
       for (int j = 0; j < CH; ++j)
 #pragma unroll
         for (int q = 0; q < VW; ++q) acc[j][q] = (T)0;
+      V sv[CH];   // BITS: the self row, requested early
+      if constexpr (BITS) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int c = c0 + lane + 32 * j;
+          vzero(sv[j]);
+          if (sd >= 0 && c < dv) sv[j] = reinterpret_cast<const V*>(dcat + (int64_t)sd * ld_dcat)[c];
+        }
+      }
       // transposed row in ascending dst order (csc_matvecs order, model.py:224)
       for (int t = b; t < e_end; ++t) {
         const uint64_t key = tkeys[t];
         const int32_t d = (int32_t)(key >> 32), e = (int32_t)(key & 0xffffffffu);
-        const T w = (T)bv.edge_weight[e];
-        const T nrm = (T)max(bv.dst_degree[d], 1);
+        T w = (T)0, nrm = (T)1;
+        if constexpr (!BITS) {
+          w = (T)bv.edge_weight[e];
+          nrm = (T)max(bv.dst_degree[d], 1);
+        }
         const V* grow = reinterpret_cast<const V*>(dcat + (int64_t)d * ld_dcat + dim);
         V g[CH];
 #pragma unroll
@@ -611,7 +764,9 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
             for (int q = 0; q < VW; ++q) acc[j][q] = DADD(acc[j][q], DMUL(w, DDIV(gp[q], nrm)));
           }
         } else {
-          const T wn = w / nrm;
+          T wn;
+          if constexpr (BITS) wn = (T)twn[t];
+          else wn = w / nrm;
 #pragma unroll
           for (int j = 0; j < CH; ++j) {
             const T* gp = reinterpret_cast<const T*>(&g[j]);
@@ -631,7 +786,9 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
         }
         if (c >= dv) continue;
         if (srow) {
-          V g = srow[c];
+          V g;
+          if constexpr (BITS) g = sv[j];
+          else g = srow[c];
           const T* gp = reinterpret_cast<const T*>(&g);
 #pragma unroll
           for (int q = 0; q < VW; ++q) {
@@ -830,16 +987,29 @@ __global__ void dense_bwd_partial_kernel(const T* __restrict__ dh, const T* __re
 }
 
 // one warp per column: fixed lane-strided partial sums + shuffle tree (deterministic)
+// db[c] = sum over blocks of partial[b][c] in a fixed order: CTA per 32
+// columns, warp w sums rows w, w+8, ... (coalesced 128-byte row reads), then
+// the 8 warp sums are added in warp order.  Launch with colsum_grid(ncols).
+constexpr int kColsumWarps = 8;
 template <typename T>
-__global__ void colsum_final_kernel(const T* __restrict__ partial, int nblocks, int ncols, T* __restrict__ db) {
-  const int lane = threadIdx.x & 31;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= ncols) return;
+__global__ void __launch_bounds__(kColsumWarps * 32) colsum_final_kernel(const T* __restrict__ partial, int nblocks,
+                                                                         int ncols, T* __restrict__ db) {
+  __shared__ T red[kColsumWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   T s = 0;
-  for (int b = lane; b < nblocks; b += 32) s += partial[(int64_t)b * ncols + c];
-  s = warp_sum(s);
-  if (lane == 0) db[c] = s;
+  if (c < ncols)
+    for (int b = w; b < nblocks; b += kColsumWarps) s += partial[(int64_t)b * ncols + c];
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < ncols) {
+    T t = red[0][lane];
+#pragma unroll
+    for (int i = 1; i < kColsumWarps; ++i) t += red[i][lane];
+    db[c] = t;
+  }
 }
+static inline unsigned colsum_grid(int ncols) { return (unsigned)((ncols + 31) / 32); }
 
 struct BwdWs {
   void* colpart;
@@ -847,6 +1017,7 @@ struct BwdWs {
   int32_t* tptr;
   int32_t* self_of;
   uint64_t* tkeys;
+  float* twn;
   void* scan;
   long long tiles;
 };
@@ -858,6 +1029,7 @@ static size_t bwd_ws(int64_t max_src, int64_t max_edges, int32_t dim, void* base
   w->tptr = ws.take<int32_t>(max_src + 1);
   w->self_of = ws.take<int32_t>(max_src + 1);
   w->tkeys = ws.take<uint64_t>(max_edges + 1);
+  w->twn = ws.take<float>(max_edges + 1);
   w->tiles = (max_src + 256 * 8 - 1) / (256 * 8) + 1;
   w->scan = (void*)ws.take<char>(scan_status_bytes(w->tiles));
   return ws.off;
@@ -1038,6 +1210,10 @@ int gns_tune(const char* name, int32_t value) {
     g_tune_bwd = value;
     return GNS_OK;
   }
+  if (!strcmp(name, "spmm_wide")) {
+    g_tune_wide = value;
+    return GNS_OK;
+  }
   if (gns_sample_tune(name, value) == GNS_OK) return GNS_OK;
   set_error("unknown tuning knob %s (or value %d out of range)", name, value);
   return GNS_EINVAL;
@@ -1093,6 +1269,16 @@ int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block
   int grid = grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)num_sms() * 8);
   BlockView bv = view_of(block);
   const int dv = dim / 4;
+  if (g_tune_wide && dv > 32 && dv <= 64) {
+    spmm_fwd_wide_kernel<2, 4, true><<<grid, kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows,
+                                                                     relu_bits);
+    return check_launch("spmm_fwd_bits");
+  }
+  if (g_tune_wide && dv > 64 && dv <= 128) {
+    spmm_fwd_wide_kernel<4, 2, true><<<grid, kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows,
+                                                                     relu_bits);
+    return check_launch("spmm_fwd_bits");
+  }
 #define GNS_FWDB(CH)                                                                                             \
   spmm_fwd_kernel<float, CH, true, false, true><<<grid, kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat, \
                                                                                 pad_rows, nullptr, nullptr,   \
@@ -1126,13 +1312,14 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
 #define GNS_BWDB(CH)                                                                                             \
   spmm_bwd_kernel<float, CH, true><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,       \
                                                                   w.self_of, dh, ld_dh, pad_rows, nullptr,       \
-                                                                  db ? (float*)w.colpart : nullptr, relu_bits)
+                                                                  db ? (float*)w.colpart : nullptr, relu_bits,   \
+                                                                  w.twn)
   if (dv <= 32) GNS_BWDB(1);
   else if (dv <= 64) GNS_BWDB(2);
   else GNS_BWDB(4);
 #undef GNS_BWDB
   GNS_TRY(check_launch("spmm_bwd_bits"));
-  if (db) colsum_final_kernel<float><<<(dim + 7) / 8, 256, 0, stream>>>((const float*)w.colpart, g2, dim, db);
+  if (db) colsum_final_kernel<float><<<colsum_grid(dim), kColsumWarps * 32, 0, stream>>>((const float*)w.colpart, g2, dim, db);
   return check_launch("spmm_bwd_bits colsum");
 }
 
@@ -1203,7 +1390,7 @@ int gns_block_transpose(const gns_block_t* block, int64_t max_dst, int64_t max_s
   tscan_apply_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, w.tptr, (unsigned long long*)w.scan);
   tscatter_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.tptr, w.tkeys);
   int g2 = grid_for((max_src * 32 + 255) / 256, (long long)sms * 8);
-  tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys);
+  tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys, w.twn);
   return check_launch("block_transpose");
 }
 
@@ -1266,9 +1453,9 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
   GNS_TRY(check_launch("spmm_bwd"));
   if (db) {
     if (dtype == 0)
-      colsum_final_kernel<float><<<(dim + 7) / 8, 256, 0, stream>>>((const float*)w.colpart, g2, dim, (float*)db);
+      colsum_final_kernel<float><<<colsum_grid(dim), kColsumWarps * 32, 0, stream>>>((const float*)w.colpart, g2, dim, (float*)db);
     else
-      colsum_final_kernel<double><<<(dim + 7) / 8, 256, 0, stream>>>((const double*)w.colpart, g2, dim,
+      colsum_final_kernel<double><<<colsum_grid(dim), kColsumWarps * 32, 0, stream>>>((const double*)w.colpart, g2, dim,
                                                                      (double*)db);
   }
   return check_launch("spmm_bwd colsum");
@@ -1296,11 +1483,11 @@ int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int64_t ld,
   if (dtype == 0) {
     dense_bwd_partial_kernel<float><<<grid, 256, 0, stream>>>((const float*)dh, (const float*)z, ld, n_dev, n_rows,
                                                               ncols, (float*)dz, (float*)ws, rpb);
-    colsum_final_kernel<float><<<(ncols + 7) / 8, 256, 0, stream>>>((const float*)ws, nblocks, ncols, (float*)db);
+    colsum_final_kernel<float><<<colsum_grid(ncols), kColsumWarps * 32, 0, stream>>>((const float*)ws, nblocks, ncols, (float*)db);
   } else {
     dense_bwd_partial_kernel<double><<<grid, 256, 0, stream>>>((const double*)dh, (const double*)z, ld, n_dev,
                                                                n_rows, ncols, (double*)dz, (double*)ws, rpb);
-    colsum_final_kernel<double><<<(ncols + 7) / 8, 256, 0, stream>>>((const double*)ws, nblocks, ncols,
+    colsum_final_kernel<double><<<colsum_grid(ncols), kColsumWarps * 32, 0, stream>>>((const double*)ws, nblocks, ncols,
                                                                      (double*)db);
   }
   return check_launch("dense_bwd_bias");

@@ -444,6 +444,36 @@ def test_spmm_fwd_gather_equals_gather_then_spmm(P, dim):
         assert torch.equal(a, b), li
 
 
+@pytest.mark.parametrize("dim", [132, 256, 512])
+def test_spmm_fwd_wide_equals_generic(P, dim):
+    """Hidden-layer forward with relu' bits: the wide kernel (lane-held edges,
+    shuffle ranks; rows with > 32 edges ranked window by window) equals the
+    generic kernel bit for bit, cat and bits."""
+    from paper_2106_06150_b200 import _lib
+    og = _hub_graph(4000, 29)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy="NS", fanouts=(70, 3), batch_size=200, seed=8)
+    targets = np.random.default_rng(8).choice(og.num_nodes, 200, replace=False)
+    mb = P.build_minibatch(g, None, targets, cfg, P.BatchRng(8, 0, 0))
+    lib = _lib.lib()
+    try:
+        for bg in mb.blocks:
+            ns, nd = bg.src_nodes.numel(), bg.dst_nodes.numel()
+            h = torch.randn(ns, dim, device="cuda")
+            res = []
+            for v in (0, 1):
+                _lib.call("gns_tune", b"spmm_wide", v)
+                o = torch.full((nd + 3, 2 * dim), 5.0, device="cuda")
+                bits = torch.zeros(lib.gns_relu_bits_size(ns, dim) // 4, dtype=torch.int32, device="cuda")
+                _lib.call("gns_spmm_fwd_bits", h.data_ptr(), dim, dim, bg._c, nd, nd + 3, o.data_ptr(), 2 * dim,
+                          bits.data_ptr(), _lib.stream_ptr())
+                res.append((o, bits))
+            assert torch.equal(res[0][0], res[1][0])
+            assert torch.equal(res[0][1], res[1][1])
+    finally:
+        _lib.call("gns_tune", b"spmm_wide", 1)
+
+
 @pytest.mark.parametrize("dim", [16, 64, 128])
 def test_spmm_fwd_narrow_equals_generic(P, dim):
     """The narrow-row kernel (shuffle sort, <= 32 edges per row; > 32 edges
