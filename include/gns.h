@@ -143,6 +143,20 @@ GNS_API int gns_graph_launch(void* exec, void* stream);
 GNS_API int gns_graph_exec_destroy(void* exec);
 GNS_API int gns_graph_kernel_priorities(void* graph, int32_t* out_hist, int32_t nbins);
 
+/* Size-switched graph regions: called while `stream` is being captured,
+ * gns_graph_switch_begin appends a kernel that reads the device row count
+ * *n_dev and a SWITCH conditional node with `nbodies` empty body graphs
+ * (out_bodies[k]); at every replay body k = min(ceil(n / chunk), nbodies-1)
+ * runs.  The caller records body k — typically the dense op over the first
+ * k*chunk rows — by capturing onto another stream between
+ * gns_graph_body_capture_begin(aux, out_bodies[k]) and
+ * gns_graph_body_capture_end(aux).  Lets capacity-sized GEMMs run on the
+ * rows the batch actually has. */
+GNS_API int gns_graph_switch_begin(void* stream, const int32_t* n_dev, int64_t chunk, int32_t nbodies,
+                                   void** out_bodies);
+GNS_API int gns_graph_body_capture_begin(void* stream, void* body);
+GNS_API int gns_graph_body_capture_end(void* stream);
+
 /* Developer knob for A/B measurements of kernel variants ("spmm_narrow":
  * 1 = row-per-warp shuffle-sorted SpMM for float32 rows of <= 128 floats
  * (default), 0 = the generic shared-memory kernel).  Not used on the product
@@ -304,10 +318,18 @@ GNS_API int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim
  * global node id — block->edge_node for the neighbours, dst_ids[r] (the
  * block's dst node ids) for the self half — instead of from a materialised
  * features[input_nodes].  Output identical to gns_gather_rows followed by
- * gns_spmm_fwd(dtype 0, flags 0). */
+ * gns_spmm_fwd(dtype 0, flags 0).  pad_chunk > 0 zero-fills rows [n, pad_rows)
+ * only up to the next multiple of pad_chunk (what a size-switched GEMM over
+ * the first ceil(n / pad_chunk) * pad_chunk rows reads). */
 GNS_API int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim,
                                 const gns_block_t* block, const int32_t* dst_ids, int64_t max_dst,
-                                int64_t pad_rows, float* cat, int64_t ld_cat, void* stream);
+                                int64_t pad_rows, int64_t pad_chunk, float* cat, int64_t ld_cat,
+                                void* stream);
+
+/* out[c] = sum over r < nrows of part[r * ncols + c], fixed order (the
+ * reduction of split-K partial products).  dtype 0 = float32, 1 = float64. */
+GNS_API int gns_sum_rows(int32_t dtype, const void* part, int64_t nrows, int64_t ncols, void* out,
+                         void* stream);
 
 /* Backward of the above (model.py:223-225):
  * dh[s,:] = sum_{e: src=s, ascending dst} w_e * (dcat[dst_e, D:2D] / max(deg,1))

@@ -74,6 +74,9 @@ _SIGS = {
     "gns_graph_launch": (c_int32, [c_void_p, c_void_p]),
     "gns_graph_exec_destroy": (c_int32, [c_void_p]),
     "gns_graph_kernel_priorities": (c_int32, [c_void_p, c_void_p, c_int32]),
+    "gns_graph_switch_begin": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
+    "gns_graph_body_capture_begin": (c_int32, [c_void_p, c_void_p]),
+    "gns_graph_body_capture_end": (c_int32, [c_void_p]),
     "gns_degree_probs": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p]),
     "gns_random_walk_workspace_size": (c_size_t, [c_int64]),
     "gns_random_walk_probs": (c_int32, [POINTER(GnsGraph), c_void_p, c_int64, c_void_p, c_int32, c_void_p,
@@ -115,7 +118,8 @@ _SIGS = {
     "gns_spmm_fwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, c_int32, POINTER(GnsBlock),
                                c_int64, c_int64, c_void_p, c_int64, c_void_p]),
     "gns_spmm_fwd_gather": (c_int32, [c_void_p, c_int64, c_int32, POINTER(GnsBlock), c_void_p, c_int64, c_int64,
-                                      c_void_p, c_int64, c_void_p]),
+                                      c_int64, c_void_p, c_int64, c_void_p]),
+    "gns_sum_rows": (c_int32, [c_int32, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "gns_spmm_bwd_workspace_size": (c_size_t, [c_int64, c_int64, c_int32]),
     "gns_spmm_bwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, POINTER(GnsBlock), c_int64,
                                c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
@@ -207,7 +211,7 @@ KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_random_walk_probs": 9, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
     "gns_cached_csr_fill": 1, "gns_estimate_edge_inclusion": 0, "gns_sample_layer": 9, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
-    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2, "gns_spmm_fwd_bits": 1, "gns_spmm_bwd_transposed_bits": 2,
+    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_sum_rows": 1, "gns_graph_switch_begin": 1, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2, "gns_spmm_fwd_bits": 1, "gns_spmm_bwd_transposed_bits": 2,
     "gns_adam_dev": 2,
     "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1, "gns_build_csr_count": 6, "gns_build_csr_fill": 1,
 }

@@ -69,6 +69,16 @@ int num_sms() {
   return sms;
 }
 
+// SWITCH conditional node selector: body k covers the first k*chunk rows;
+// the selected body is the smallest one covering the device row count.
+__global__ void switch_set_kernel(cudaGraphConditionalHandle h, const int32_t* __restrict__ n_dev, int64_t chunk,
+                                  int32_t nbodies) {
+  const int64_t n = n_dev[0];
+  int64_t k = (n + chunk - 1) / chunk;
+  if (k > nbodies - 1) k = nbodies - 1;
+  cudaGraphSetConditional(h, (unsigned)k);
+}
+
 // ---------------------------------------------------------------------------
 __global__ void degree_probs_kernel(const int64_t* __restrict__ indptr, int64_t n, double total,
                                     double* __restrict__ out) {
@@ -176,6 +186,51 @@ int gns_graph_exec_destroy(void* exec) {
   return GNS_OK;
 }
 
+int gns_graph_switch_begin(void* stream_, const int32_t* n_dev, int64_t chunk, int32_t nbodies, void** out_bodies) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (chunk <= 0 || nbodies < 1) {
+    set_error("graph_switch_begin: chunk and nbodies must be positive");
+    return GNS_EINVAL;
+  }
+  cudaStreamCaptureStatus st;
+  unsigned long long id = 0;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  GNS_CUDA(cudaStreamGetCaptureInfo(stream, &st, &id, &graph, &deps, &ndeps));
+  if (st != cudaStreamCaptureStatusActive) {
+    set_error("graph_switch_begin: the stream is not being captured");
+    return GNS_EINVAL;
+  }
+  cudaGraphConditionalHandle h;
+  GNS_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
+  switch_set_kernel<<<1, 1, 0, stream>>>(h, n_dev, chunk, nbodies);
+  GNS_TRY(check_launch("switch_set"));
+  GNS_CUDA(cudaStreamGetCaptureInfo(stream, &st, &id, &graph, &deps, &ndeps));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeSwitch;
+  p.conditional.size = (unsigned)nbodies;
+  cudaGraphNode_t node;
+  GNS_CUDA(cudaGraphAddNode(&node, graph, deps, ndeps, &p));
+  GNS_CUDA(cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies));
+  for (int i = 0; i < nbodies; ++i) out_bodies[i] = (void*)p.conditional.phGraph_out[i];
+  return GNS_OK;
+}
+
+int gns_graph_body_capture_begin(void* stream, void* body) {
+  GNS_CUDA(cudaStreamBeginCaptureToGraph((cudaStream_t)stream, (cudaGraph_t)body, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+  return GNS_OK;
+}
+
+int gns_graph_body_capture_end(void* stream) {
+  cudaGraph_t g = nullptr;
+  GNS_CUDA(cudaStreamEndCapture((cudaStream_t)stream, &g));
+  return GNS_OK;
+}
+
 int gns_graph_kernel_priorities(void* graph, int32_t* out_hist, int32_t nbins) {
   size_t n = 0;
   GNS_CUDA(cudaGraphGetNodes((cudaGraph_t)graph, nullptr, &n));
@@ -184,10 +239,17 @@ int gns_graph_kernel_priorities(void* graph, int32_t* out_hist, int32_t nbins) {
   for (int i = 0; i < nbins; ++i) out_hist[i] = 0;
   for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
     cudaGraphNodeType t;
-    if ((e = cudaGraphNodeGetType(nodes[i], &t)) != cudaSuccess) break;
+    if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess) {   // e.g. conditional nodes: not kernels
+      cudaGetLastError();
+      continue;
+    }
     if (t != cudaGraphNodeTypeKernel) continue;
     cudaKernelNodeAttrValue v;
-    if ((e = cudaGraphKernelNodeGetAttribute(nodes[i], cudaKernelNodeAttributePriority, &v)) != cudaSuccess) break;
+    // (kernel nodes of other libraries may not expose the attribute: skip)
+    if (cudaGraphKernelNodeGetAttribute(nodes[i], cudaKernelNodeAttributePriority, &v) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
     int b = v.priority < 0 ? -v.priority : v.priority;  // bin = |priority|
     out_hist[b < nbins ? b : nbins - 1] += 1;
   }

@@ -369,7 +369,8 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel
                                                                          float* __restrict__ cat, int64_t ld_cat,
                                                                          int64_t pad_rows,
                                                                          const int32_t* __restrict__ edge_node,
-                                                                         const int32_t* __restrict__ dst_ids) {
+                                                                         const int32_t* __restrict__ dst_ids,
+                                                                         int64_t pad_chunk = 0) {
   const int32_t* __restrict__ eidx = GATHER ? edge_node : bv.edge_src;
   const int lane = threadIdx.x & 31;
   const int64_t n = bv.counts[GNS_CNT_DST];
@@ -453,7 +454,10 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel
       crow[dv + lane] = vdiv(acc, norm);
     }
   }
-  for (int64_t r = n + gw; r < pad_rows; r += nw) {
+  // zero padding up to pad_rows, or (pad_chunk > 0) only up to the next
+  // multiple of pad_chunk: the rows a size-switched GEMM body reads
+  const int64_t pad_end = pad_chunk > 0 ? min(pad_rows, (n + pad_chunk - 1) / pad_chunk * pad_chunk) : pad_rows;
+  for (int64_t r = n + gw; r < pad_end; r += nw) {
     float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
     for (int c = lane; c < 2 * dv; c += 32) crow[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -1219,9 +1223,21 @@ int gns_tune(const char* name, int32_t value) {
   return GNS_EINVAL;
 }
 
+int gns_sum_rows(int32_t dtype, const void* part, int64_t nrows, int64_t ncols, void* out, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (ncols <= 0) return GNS_OK;
+  if (dtype == 0)
+    colsum_final_kernel<float><<<colsum_grid((int)ncols), kColsumWarps * 32, 0, stream>>>(
+        (const float*)part, (int)nrows, (int)ncols, (float*)out);
+  else
+    colsum_final_kernel<double><<<colsum_grid((int)ncols), kColsumWarps * 32, 0, stream>>>(
+        (const double*)part, (int)nrows, (int)ncols, (double*)out);
+  return check_launch("sum_rows");
+}
+
 int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const gns_block_t* block,
-                        const int32_t* dst_ids, int64_t max_dst, int64_t pad_rows, float* cat, int64_t ld_cat,
-                        void* stream_) {
+                        const int32_t* dst_ids, int64_t max_dst, int64_t pad_rows, int64_t pad_chunk, float* cat,
+                        int64_t ld_cat, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (max_dst <= 0 && pad_rows <= 0) return GNS_OK;
   if (dim % 4 || ld_table % 4 || ld_cat % 4 || (uintptr_t)table % 16 || (uintptr_t)cat % 16) {
@@ -1235,8 +1251,13 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
   const int dv = dim / 4;
   if (dv <= 32 && g_tune_narrow == 1) {
     spmm_fwd_narrow_kernel<false, true><<<grid, kSpmmBlock, 0, stream>>>(table, ld_table, dim, bv, cat, ld_cat,
-                                                                        pad_rows, block->edge_node, dst_ids);
+                                                                        pad_rows, block->edge_node, dst_ids,
+                                                                        pad_chunk);
     return check_launch("spmm_fwd_gather");
+  }
+  if (pad_chunk > 0) {
+    set_error("spmm_fwd_gather: pad_chunk needs the narrow kernel (dim <= 128)");
+    return GNS_EINVAL;
   }
   if (dv <= 32 && g_tune_narrow == 2) {
     spmm_fwd_narrow_kernel<false, true, 8, 3><<<grid, kSpmmBlock, 0, stream>>>(

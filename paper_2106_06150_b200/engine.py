@@ -47,7 +47,7 @@ class GraphedTrainer:
     def __init__(self, g: Graph, config: SamplerConfig, dims, train_config: TrainConfig | None = None,
                  rank: int = 0, world_size: int = 1, allreduce=None, seed: int = 0, host_targets: bool = False,
                  feature_placement: str = "device", host_features: torch.Tensor | None = None,
-                 steps_per_graph: int | None = None):
+                 steps_per_graph: int | None = None, switch_chunk: int | None = None):
         _lib.require_cuda()
         if g.features is None or g.labels is None:
             raise ValueError("training needs features and labels")
@@ -118,6 +118,12 @@ class GraphedTrainer:
         self.main = torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "main" else lo)
         self.taux = [torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "side" else lo)
                      for _ in range(2 * S)]
+        # size-switched input-layer dense ops: the capacity-sized GEMMs run
+        # over the first ceil(n / chunk) * chunk rows (SWITCH graph node on
+        # the device row count); bodies are recorded on aux_dense
+        self.switch_chunk = switch_chunk if switch_chunk is not None else \
+            int(os.environ.get("GNS_SWITCH_CHUNK", "8192"))
+        self.aux_dense = torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "main" else lo)
         self._execs = {}
         self._per_replay = 0
         self._alloc()
@@ -147,6 +153,10 @@ class GraphedTrainer:
                                                                             dims[li]), dev, zero=True)
                               for li in range(1, L)] for _ in self.slots]
         self.ws_xent = _lib.workspace(8 * max(self.cap_dst[L - 1], 1024), dev)
+        self.use_switch = self.switch_chunk > 0 and self.switch_chunk % 2048 == 0 and \
+            self.cap_dst[0] >= 2 * self.switch_chunk
+        # split-K partial products of the input layer's weight gradient
+        self.part0 = torch.empty((max(self.npad[0] // 2048, 1), 2 * dims[0], dims[1]), dtype=f32, device=dev)
         # relu' bits of z[li-1] written by layer li's forward, read by its
         # backward (gns_spmm_fwd_bits / gns_spmm_bwd_transposed_bits)
         self.relu_bits = [None] + [
@@ -198,7 +208,8 @@ class GraphedTrainer:
                     tab = self.g.features
                     dst_ids = sl.layers[L - 2].src_nodes if L > 1 else sl.seeds0
                     _lib.call("gns_spmm_fwd_gather", tab.data_ptr(), tab.stride(0), d_in, blocks[0].cblock,
-                              dst_ids.data_ptr(), self.cap_dst[0], self.npad[0], self.cat[0].data_ptr(),
+                              dst_ids.data_ptr(), self.cap_dst[0], self.npad[0],
+                              self.switch_chunk if self.use_switch else 0, self.cat[0].data_ptr(),
                               self.cat[0].stride(0), s)
                 elif li > 0:
                     _lib.call("gns_spmm_fwd_bits", h.data_ptr(), h.stride(0), d_in, blocks[li].cblock,
@@ -209,7 +220,12 @@ class GraphedTrainer:
                               self.cap_dst[li], self.npad[li], self.cat[li].data_ptr(), self.cat[li].stride(0), s)
                 if ev is not None:
                     _lib.call("gns_record_event_external", ev[3].cuda_event, s)
-                torch.addmm(m.biases[li], self.cat[li][:self.cap_dst[li]], m.weights[li], out=self.z[li])
+                if li == 0 and self.use_switch:
+                    self._switched(blocks[0].counts[_lib.CNT_DST:_lib.CNT_DST + 1], self.cap_dst[0],
+                                   lambda R: torch.addmm(m.biases[0], self.cat[0][:R], m.weights[0],
+                                                         out=self.z[0][:R]))
+                else:
+                    torch.addmm(m.biases[li], self.cat[li][:self.cap_dst[li]], m.weights[li], out=self.z[li])
                 h = self.z[li]
             top = blocks[L - 1]
             logits = self.z[L - 1]
@@ -222,7 +238,12 @@ class GraphedTrainer:
             _lib.call("gns_dense_bwd_bias", 0, self.dz[L - 1].data_ptr(), None, d_last, None, self.cap_dst[L - 1],
                       d_last, None, m.gbiases[L - 1].data_ptr(), self.ws_dense.data_ptr(), self.ws_dense.numel(), s)
             for li in range(L - 1, -1, -1):
-                _weight_grad(self.cat[li][:self.npad[li]], self.dz[li][:self.npad[li]], m.gweights[li])
+                if li == 0 and self.use_switch:
+                    self._switched(blocks[0].counts[_lib.CNT_DST:_lib.CNT_DST + 1], self.npad[0],
+                                   lambda R: _weight_grad(self.cat[0][:R], self.dz[0][:R], m.gweights[0], self.part0),
+                                   empty=lambda: m.gweights[0].zero_())
+                else:
+                    _weight_grad(self.cat[li][:self.npad[li]], self.dz[li][:self.npad[li]], m.gweights[li])
                 if li == 0:
                     break
                 torch.mm(self.dz[li][:self.cap_dst[li]], m.weights[li].t(), out=self.dcat[li])
@@ -237,6 +258,29 @@ class GraphedTrainer:
                           self.dz[li - 1].data_ptr(), self.dz[li - 1].stride(0), ws.data_ptr(), ws.numel(), s)
         if with_adam:
             self._adam_dev()
+
+    def _switched(self, n_dev: torch.Tensor, limit: int, fn, empty=None):
+        """fn(R) over the first R = min(k * chunk, limit) rows, k = ceil(n /
+        chunk) from the device count: a SWITCH graph node with one recorded
+        body per k when capturing (gns_graph_switch_begin), fn(limit) eagerly.
+        Bodies must not allocate (they are recorded outside torch's graph
+        memory pool): out= ops and preallocated buffers only."""
+        if not torch.cuda.is_current_stream_capturing():
+            fn(limit)
+            return
+        C = self.switch_chunk
+        K = -(-limit // C) + 1
+        bodies = (ctypes.c_void_p * K)()
+        _lib.call("gns_graph_switch_begin", _lib.stream_ptr(), n_dev.data_ptr(), C, K, bodies)
+        aux = self.aux_dense
+        for k in range(K):
+            _lib.call("gns_graph_body_capture_begin", _lib.stream_ptr(aux), bodies[k])
+            with torch.cuda.stream(aux):
+                if k:
+                    fn(min(k * C, limit))
+                elif empty is not None:
+                    empty()
+            _lib.call("gns_graph_body_capture_end", _lib.stream_ptr(aux))
 
     def _adam_dev(self):
         """[all-reduce of the flat gradient] + Adam with the device step count
@@ -362,6 +406,12 @@ class GraphedTrainer:
             self._train_body(0, with_adam=False)
             if self.allreduce is not None:
                 self.allreduce(self.model.grad)
+        if self.use_switch:   # cuBLAS / cuBLASLt handles and workspaces of aux_dense
+            m, C = self.model, self.switch_chunk
+            with torch.cuda.stream(self.aux_dense), m._tf32():
+                torch.addmm(m.biases[0], self.cat[0][:C], m.weights[0], out=self.z[0][:C])
+                _weight_grad(self.cat[0][:C], self.dz[0][:C], m.gweights[0], self.part0)
+                m.gweights[0].zero_()
         self._prof_events = ev
         torch.cuda.synchronize()
 

@@ -74,17 +74,23 @@ def _split_rows(n: int) -> int:
     return (n + _SPLIT_CHUNK - 1) // _SPLIT_CHUNK * _SPLIT_CHUNK
 
 
-def _weight_grad(cat: torch.Tensor, dz: torch.Tensor, out: torch.Tensor):
+def _weight_grad(cat: torch.Tensor, dz: torch.Tensor, out: torch.Tensor, part: torch.Tensor | None = None):
     """dW = cat^T dz (model.py:219).  K = rows is ~10^5 while the output is
     only (2 d_in) x d_out, so a single GEMM has too few output tiles to fill
-    148 SMs: split K into 2048-row chunks (batched GEMM) and reduce."""
+    148 SMs: split K into 2048-row chunks (batched GEMM into ``part``,
+    allocated here unless given) and reduce them in a fixed order
+    (gns_sum_rows)."""
     n = cat.shape[0]
     if n < _SPLIT_MIN or n % _SPLIT_CHUNK:
         torch.mm(cat.t(), dz, out=out)
         return
     s = n // _SPLIT_CHUNK
-    part = torch.bmm(cat.view(s, _SPLIT_CHUNK, -1).transpose(1, 2), dz.view(s, _SPLIT_CHUNK, -1))
-    torch.sum(part, dim=0, out=out)
+    if part is None:
+        part = torch.empty((s,) + tuple(out.shape), dtype=out.dtype, device=out.device)
+    p = part[:s]
+    torch.bmm(cat.view(s, _SPLIT_CHUNK, -1).transpose(1, 2), dz.view(s, _SPLIT_CHUNK, -1), out=p)
+    _lib.call("gns_sum_rows", 0 if out.dtype == torch.float32 else 1, p.data_ptr(), s, out.numel(), out.data_ptr(),
+              _lib.stream_ptr())
 
 
 class _TF32:

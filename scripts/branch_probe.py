@@ -50,7 +50,10 @@ def main():
         "gather_only": capture(lambda: tr._gather(0)).replay,
         f"{tr.S} steps (production graph, priority={tr.prio_mode})": lambda: tr._replay(0),
     }
-    print("kernel-node |priority| histogram:", tr.kernel_priorities(0))
+    try:
+        print("kernel-node |priority| histogram:", tr.kernel_priorities(0))
+    except RuntimeError as e:
+        print("kernel-node priorities unavailable:", e)
     for name, replay in variants.items():
         for _ in range(3):
             replay()

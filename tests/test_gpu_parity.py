@@ -439,7 +439,7 @@ def test_spmm_fwd_gather_equals_gather_then_spmm(P, dim):
         _lib.call("gns_spmm_fwd", 0, h.data_ptr(), dim, dim, 0, bg._c, ndst, ndst + 5, a.data_ptr(), 2 * dim,
                   _lib.stream_ptr())
         dst = torch.as_tensor(br.dst_nodes.astype(np.int32), device="cuda")
-        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 5,
+        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 5, 0,
                   b.data_ptr(), 2 * dim, _lib.stream_ptr())
         assert torch.equal(a, b), li
 
@@ -500,7 +500,7 @@ def test_spmm_fwd_narrow_equals_generic(P, dim):
                               2 * dim, _lib.stream_ptr())
                     outs[(v, relu)] = o
                 o = torch.full((nd + 3, 2 * dim), 5.0, device="cuda")
-                _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), nd, nd + 3,
+                _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), nd, nd + 3, 0,
                           o.data_ptr(), 2 * dim, _lib.stream_ptr())
                 outs[(v, "g")] = o
             for key in ((0, 1), "g"):
@@ -805,6 +805,36 @@ def test_graphed_trainer_matches_eager(P):
     assert torch.equal(tr.cache.nodes.ids, pool.cache.nodes.ids)
     assert torch.equal(tr.cache.cached_indices, pool.cache.cached_indices)
     np.testing.assert_allclose(losses2, ref2, rtol=2e-3)
+
+
+@pytest.mark.parametrize("chunk", [0, 4096])
+def test_graphed_trainer_size_switched_dense_ops(P, chunk):
+    """Input-layer GEMMs as SWITCH graph nodes over the device row count
+    (bodies over ceil(n / chunk) * chunk rows) train exactly like the
+    capacity-sized ones and the eager model."""
+    n = 30_000
+    rng = np.random.default_rng(5)
+    og = O.build_csr(rng.integers(0, n, size=(150_000, 2)), n)
+    feats = rng.normal(size=(n, 16)).astype(np.float32)
+    labels = rng.integers(0, 5, n).astype(np.int32)
+    mask = rng.random(n) < 0.3
+    g = P.Graph.from_numpy(n, og.indptr, og.indices, features=feats, labels=labels, train_mask=mask)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=1500, cache_frac=0.02, cache_mode="degree",
+                          seed=9)
+    tc = P.TrainConfig(lr=0.003)
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0, switch_chunk=chunk)
+    assert tr.use_switch == (chunk > 0) and tr.cap_dst[0] >= 2 * 4096
+    losses = []
+    tr.run_epoch(0, max_steps=5, on_step=lambda e, i, k: losses.append(tr.loss_value()))
+    eager = P.GraphSAGE((16, 32, 5), seed=0)
+    pool = P.SamplerPool(g, cfg, num_workers=1)
+    ref = [float(eager.train_step(it.minibatch, g, tc)) for _, it in zip(range(5), pool.iter_epoch(0))]
+    np.testing.assert_allclose(losses, ref, rtol=2e-3)
+    we, be = eager.export()
+    wg, bg_ = tr.model.export()
+    for a, b in zip(we + be, wg + bg_):
+        np.testing.assert_allclose(a, b, rtol=1e-2, atol=1e-4)
 
 
 def test_graphed_trainer_run_host_matches_eager(P):
