@@ -157,10 +157,19 @@ GNS_API int gns_graph_switch_begin(void* stream, const int32_t* n_dev, int64_t c
 GNS_API int gns_graph_body_capture_begin(void* stream, void* body);
 GNS_API int gns_graph_body_capture_end(void* stream);
 
-/* Developer knob for A/B measurements of kernel variants ("spmm_narrow":
- * 1 = row-per-warp shuffle-sorted SpMM for float32 rows of <= 128 floats
- * (default), 0 = the generic shared-memory kernel).  Not used on the product
- * path. */
+/* Developer knobs for A/B measurements of kernel variants (defaults = the
+ * measured best; every setting gives identical results):
+ *   "spmm_narrow"  1: shuffle-ranked forward SpMM for float32 rows of <= 128
+ *                  floats, 0: the generic shared-memory kernel;
+ *   "spmm_wide"    1: shuffle-ranked hidden-layer forward (rows of <= 512
+ *                  floats), 0: generic;
+ *   "stream_len"   selection tier routing: items with take <= 8 scanning <=
+ *                  this many positions go to the streaming thread tier (32);
+ *   "thread_len"   other items scanning <= this many positions go to the
+ *                  sorting-network thread tier (0 = off);
+ *   "sampler_ctas" cap grid-stride sampler grids at this many CTAs per SM
+ *                  (0 = no cap).
+ * Not used on the product path. */
 GNS_API int gns_tune(const char* name, int32_t value);
 
 /* ---- cache engine (cache.py) ------------------------------------------- */

@@ -176,7 +176,7 @@ def load(path: str = LIB_PATH):
         fn.argtypes = args
     if path == LIB_PATH:
         _lib = lib
-    # developer A/B knobs: GNS_TUNE="spmm_bwd=0,spmm_narrow=1" (gns_tune)
+    # developer A/B knobs: GNS_TUNE="spmm_narrow=0,stream_len=16" (gns_tune)
     for kv in filter(None, os.environ.get("GNS_TUNE", "").split(",")):
         k, v = kv.split("=")
         if lib.gns_tune(k.strip().encode(), int(v)) != GNS_OK:

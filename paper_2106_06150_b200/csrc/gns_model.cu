@@ -582,8 +582,14 @@ __global__ void __launch_bounds__(kSpmmBlock, 3) spmm_fwd_wide_kernel(const floa
 
 // experiment knobs (gns_tune)
 static int g_tune_narrow = 1;  // narrow-row forward SpMM variant (0 = generic)
-static int g_tune_bwd = 0;     // 1 = short-chain float32 backward (slower on B200: occupancy), 0 = generic
 static int g_tune_wide = 1;    // hidden-layer forward: 1 = spmm_fwd_wide_kernel, 0 = generic
+
+// Forward SpMM grids: one wave of persistent CTAs (grid-stride rows).  Short
+// CTAs (k rows per warp, many waves) were measured slower both alone and
+// next to the sampling branch on B200.
+static inline int spmm_grid(long long rows) {
+  return grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)num_sms() * 8);
+}
 
 // ---- SpMM backward -------------------------------------------------------------
 __global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of) {
@@ -844,125 +850,6 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
   }
 }
 
-// float32 backward with short dependency chains (same rows per warp, same
-// accumulation order and the same block partials as spmm_bwd_kernel, so the
-// results are bit-identical).  Per src row: the transposed row bounds and the
-// self index are loaded first; the self row of dcat and the relu mask row are
-// issued right away (they do not depend on the edges); the row's edge keys,
-// weights and dst degrees are fetched lane-parallel (32 at a time) and the
-// dcat rows of G edges are in flight together.  Requires dim <= 128 * CH.
-template <int CH, int G, int MINB>
-__global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_f32_kernel(
-    const float* __restrict__ dcat, int64_t ld_dcat, int dim, BlockView bv, const int32_t* __restrict__ tptr,
-    const uint64_t* __restrict__ tkeys, const int32_t* __restrict__ self_of, float* __restrict__ dh, int64_t ld_dh,
-    int64_t pad_rows, const float* __restrict__ zmask, float* __restrict__ colpart) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n = bv.counts[GNS_CNT_SRC];
-  const int dv = dim >> 2;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  float colacc[CH][4];
-#pragma unroll
-  for (int j = 0; j < CH; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) colacc[j][q] = 0.f;
-  for (int64_t s = gw; s < n; s += nw) {
-    const int b = tptr[s], e_end = tptr[s + 1];
-    const int sd = self_of[s];
-    float4 sv[CH], zv[CH];
-#pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      const int c = lane + 32 * j;
-      sv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      zv[j] = make_float4(1.f, 1.f, 1.f, 1.f);
-      if (c < dv) {
-        if (sd >= 0) sv[j] = reinterpret_cast<const float4*>(dcat + (int64_t)sd * ld_dcat)[c];
-        if (zmask) zv[j] = reinterpret_cast<const float4*>(zmask + s * ld_dh)[c];
-      }
-    }
-    float acc[CH][4];
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[j][q] = 0.f;
-    for (int t0 = b; t0 < e_end; t0 += 32) {
-      const int m = min(32, e_end - t0);
-      int32_t d = 0;
-      float wn = 0.f;
-      if (lane < m) {
-        const uint64_t key = tkeys[t0 + lane];
-        d = (int32_t)(key >> 32);
-        const int32_t e = (int32_t)(key & 0xffffffffu);
-        wn = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
-      }
-      for (int u0 = 0; u0 < m; u0 += G) {
-        float4 g[G][CH];
-#pragma unroll
-        for (int u = 0; u < G; ++u) {
-          const int32_t du = __shfl_sync(GNS_FULL, d, (u0 + u) & 31);
-          const float4* grow = reinterpret_cast<const float4*>(dcat + (int64_t)du * ld_dcat + dim);
-#pragma unroll
-          for (int j = 0; j < CH; ++j) {
-            const int c = lane + 32 * j;
-            if (u0 + u < m && c < dv) g[u][j] = grow[c];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < G; ++u) {
-          const float wu = __shfl_sync(GNS_FULL, wn, (u0 + u) & 31);
-          if (u0 + u < m) {
-#pragma unroll
-            for (int j = 0; j < CH; ++j) {
-              acc[j][0] = fmaf(wu, g[u][j].x, acc[j][0]);
-              acc[j][1] = fmaf(wu, g[u][j].y, acc[j][1]);
-              acc[j][2] = fmaf(wu, g[u][j].z, acc[j][2]);
-              acc[j][3] = fmaf(wu, g[u][j].w, acc[j][3]);
-            }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      const int c = lane + 32 * j;
-      if (c >= dv) continue;
-      float4 out;
-      if (sd >= 0) {
-        acc[j][0] = acc[j][0] + sv[j].x;
-        acc[j][1] = acc[j][1] + sv[j].y;
-        acc[j][2] = acc[j][2] + sv[j].z;
-        acc[j][3] = acc[j][3] + sv[j].w;
-      }
-      out.x = zv[j].x > 0.f ? acc[j][0] : 0.f;
-      out.y = zv[j].y > 0.f ? acc[j][1] : 0.f;
-      out.z = zv[j].z > 0.f ? acc[j][2] : 0.f;
-      out.w = zv[j].w > 0.f ? acc[j][3] : 0.f;
-      colacc[j][0] += out.x;
-      colacc[j][1] += out.y;
-      colacc[j][2] += out.z;
-      colacc[j][3] += out.w;
-      reinterpret_cast<float4*>(dh + s * ld_dh)[c] = out;
-    }
-  }
-  for (int64_t s = n + gw; s < pad_rows; s += nw)
-    for (int c = lane; c < dv; c += 32) reinterpret_cast<float4*>(dh + s * ld_dh)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (colpart) {
-    __shared__ float red[kSpmmBlock / 32][32 * CH * 4];
-    const int wib = threadIdx.x >> 5;
-#pragma unroll
-    for (int j = 0; j < CH; ++j)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) red[wib][(lane + 32 * j) * 4 + q] = colacc[j][q];
-    __syncthreads();
-    for (int col = threadIdx.x; col < dim; col += blockDim.x) {
-      float t = 0;
-#pragma unroll
-      for (int w = 0; w < kSpmmBlock / 32; ++w) t += red[w][col];
-      colpart[(int64_t)blockIdx.x * dim + col] = t;
-    }
-  }
-}
-
 // dz = relu'(z) * dh (model.py:218) fused with the bias gradient db = sum_r dz
 // (model.py:220): per-block column partials, then a fixed-order reduction.
 template <typename T>
@@ -1210,10 +1097,6 @@ int gns_tune(const char* name, int32_t value) {
     g_tune_narrow = value;
     return GNS_OK;
   }
-  if (!strcmp(name, "spmm_bwd")) {
-    g_tune_bwd = value;
-    return GNS_OK;
-  }
   if (!strcmp(name, "spmm_wide")) {
     g_tune_wide = value;
     return GNS_OK;
@@ -1246,7 +1129,7 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
   }
   const int sms = num_sms();
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
-  int grid = grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)sms * 8);
+  int grid = spmm_grid(rows);
   BlockView bv = view_of(block);
   const int dv = dim / 4;
   if (dv <= 32 && g_tune_narrow == 1) {
@@ -1287,7 +1170,7 @@ int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block
     return GNS_EINVAL;
   }
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
-  int grid = grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)num_sms() * 8);
+  int grid = spmm_grid(rows);
   BlockView bv = view_of(block);
   const int dv = dim / 4;
   if (g_tune_wide && dv > 32 && dv <= 64) {
@@ -1350,7 +1233,7 @@ int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_
   if (max_dst <= 0 && pad_rows <= 0) return GNS_OK;
   const int sms = num_sms();
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
-  int grid = grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)sms * 8);
+  int grid = spmm_grid(rows);
   BlockView bv = view_of(block);
   const bool relu = flags & GNS_SPMM_RELU_INPUT;
 #define GNS_FWD(T, CH, R)                                                                                      \
@@ -1452,15 +1335,7 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
   spmm_bwd_kernel<T, CH><<<g2, kSpmmBlock, 0, stream>>>((const T*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys, \
                                                         w.self_of, (T*)dh, ld_dh, pad_rows, (const T*)z_mask,  \
                                                         db ? (T*)w.colpart : nullptr)
-#define GNS_BWDF(CH, G, MINB)                                                                                    \
-  spmm_bwd_f32_kernel<CH, G, MINB><<<g2, kSpmmBlock, 0, stream>>>((const float*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys, \
-                                                            w.self_of, (float*)dh, ld_dh, pad_rows,                 \
-                                                            (const float*)z_mask, db ? (float*)w.colpart : nullptr)
-  if (dtype == 0 && g_tune_bwd) {
-    if (dv <= 32) GNS_BWDF(1, 4, 4);
-    else if (dv <= 64) GNS_BWDF(2, 2, 3);
-    else GNS_BWDF(4, 1, 2);
-  } else if (dtype == 0) {
+  if (dtype == 0) {
     if (dv <= 32) GNS_BWD(float, 1);
     else if (dv <= 64) GNS_BWD(float, 2);
     else GNS_BWD(float, 4);
@@ -1470,7 +1345,6 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
     else GNS_BWD(double, 4);
   }
 #undef GNS_BWD
-#undef GNS_BWDF
   GNS_TRY(check_launch("spmm_bwd"));
   if (db) {
     if (dtype == 0)

@@ -545,34 +545,6 @@ def test_spmm_bwd_f64_bit_exact(P, dim):
             np.testing.assert_allclose(dh32.cpu().numpy(), expect, rtol=1e-5, atol=1e-5)
 
 
-@pytest.mark.parametrize("dim", [16, 64, 256, 512])
-def test_spmm_bwd_f32_variants_identical(P, dim):
-    """The short-chain float32 backward (default) equals the generic kernel
-    bit for bit: dh, relu' mask, zero padding and the bias gradient."""
-    from paper_2106_06150_b200 import _lib
-    og, g, feats, mb, ref = _mb_and_features(P, dim=16)
-    ws = _lib.workspace(1 << 24, "cuda")
-    try:
-        for li, (bg, br) in enumerate(zip(mb.blocks, ref.blocks)):
-            nsrc, ndst = len(br.src_nodes), len(br.dst_nodes)
-            gen = torch.Generator(device="cuda").manual_seed(li)
-            dt = torch.randn((ndst, 2 * dim), device="cuda", generator=gen)
-            zt = torch.randn((nsrc, dim), device="cuda", generator=gen)
-            res = []
-            for v in (0, 1):
-                _lib.call("gns_tune", b"spmm_bwd", v)
-                dh = torch.full((nsrc + 5, dim), 3.0, device="cuda")
-                db = torch.empty(dim, device="cuda")
-                _lib.call("gns_spmm_bwd", 0, dt.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, nsrc + 5,
-                          zt.data_ptr(), db.data_ptr(), dh.data_ptr(), dim, ws.data_ptr(), ws.numel(),
-                          _lib.stream_ptr())
-                res.append((dh, db))
-            assert torch.equal(res[0][0], res[1][0]), li
-            assert torch.equal(res[0][1], res[1][1]), li
-    finally:
-        _lib.call("gns_tune", b"spmm_bwd", 0)
-
-
 @pytest.mark.parametrize("dim", [16, 100, 256])
 def test_relu_bits_pair_equals_zmask_path(P, dim):
     """gns_spmm_fwd_bits == gns_spmm_fwd(relu) and gns_spmm_bwd_transposed_bits
