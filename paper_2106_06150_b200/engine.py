@@ -273,14 +273,20 @@ class GraphedTrainer:
         bodies = (ctypes.c_void_p * K)()
         _lib.call("gns_graph_switch_begin", _lib.stream_ptr(), n_dev.data_ptr(), C, K, bodies)
         aux = self.aux_dense
+        c0 = _lib.launch_counter[0]
+        per_body = 0
         for k in range(K):
             _lib.call("gns_graph_body_capture_begin", _lib.stream_ptr(aux), bodies[k])
+            before = _lib.launch_counter[0]
             with torch.cuda.stream(aux):
                 if k:
                     fn(min(k * C, limit))
                 elif empty is not None:
                     empty()
+            per_body = max(per_body, _lib.launch_counter[0] - before)
             _lib.call("gns_graph_body_capture_end", _lib.stream_ptr(aux))
+        # one body runs per replay: count its launches once
+        _lib.launch_counter[0] = c0 + per_body
 
     def _adam_dev(self):
         """[all-reduce of the flat gradient] + Adam with the device step count
