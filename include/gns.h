@@ -280,6 +280,13 @@ GNS_API int gns_epoch_targets_dev(const int32_t* train_ids, int64_t n_train,
                                   const gns_step_t* step_dev, int64_t max_count, int32_t* out,
                                   int32_t* out_n_dev, void* stream);
 
+/* gns_epoch_targets_dev followed by np.unique (sampling.py:312) in one
+ * single-CTA kernel, for batches of <= 1024 targets: out_sorted receives the
+ * sorted distinct targets, *out_n_dev their number. */
+GNS_API int gns_batch_targets_sorted(const int32_t* train_ids, int64_t n_train,
+                                     const gns_step_t* step_dev, int64_t max_count, int32_t* out_sorted,
+                                     int32_t* out_n_dev, void* stream);
+
 /* ---- model side (model.py) --------------------------------------------- */
 
 /* features[input_nodes] (model.py:146): out[i,:] = table[rows[i],:], D

@@ -144,6 +144,65 @@ __global__ void epoch_targets_dev_kernel(const int32_t* __restrict__ train_ids, 
   }
 }
 
+// The batch's targets (epoch_targets_dev_kernel's Feistel slice) sorted and
+// deduplicated in one CTA (np.unique, sampling.py:312): thread t owns target
+// t; a 1024-wide bitonic network runs its strides < 32 as register shuffles
+// and only the 15 wider ones through shared memory; ordered compaction of the
+// first element of every run.  Replaces epoch_targets_dev + unique_small.
+constexpr int kTargetsBlock = 1024;
+
+__global__ void __launch_bounds__(kTargetsBlock) batch_targets_sorted_kernel(
+    const int32_t* __restrict__ train_ids, int64_t n_train, int h, const gns_step_t* __restrict__ step,
+    int64_t max_count, int32_t* __restrict__ out, int32_t* __restrict__ out_n) {
+  __shared__ int32_t sk[kTargetsBlock];
+  __shared__ int s_warp[kTargetsBlock / 32];
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  const int64_t begin = step->begin;
+  int64_t count = step->count;
+  if (count > n_train - begin) count = n_train - begin;
+  if (count > max_count) count = max_count;
+  if (count < 0) count = 0;
+  int32_t v = INT32_MAX;
+  if (i < count) {
+    uint64_t y = (uint64_t)(begin + i);
+    if (n_train > 1) {
+      y = feistel_once(y, h, step->seed, step->epoch);
+      while (y >= (uint64_t)n_train) y = feistel_once(y, h, step->seed, step->epoch);
+    }
+    v = train_ids[y];
+  }
+  for (int k = 2; k <= kTargetsBlock; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      int32_t partner;
+      if (j >= 32) {
+        sk[i] = v;
+        __syncthreads();
+        partner = sk[i ^ j];
+        __syncthreads();
+      } else {
+        partner = __shfl_xor_sync(GNS_FULL, v, j);
+      }
+      const bool up = (i & k) == 0, lower = (i & j) == 0;
+      v = (lower == up) ? min(v, partner) : max(v, partner);
+    }
+  }
+  // first element of every run of equal ids (padding INT32_MAX excluded)
+  sk[i] = v;
+  __syncthreads();
+  const bool head = i < count && (i == 0 || sk[i - 1] != v);
+  const unsigned bal = __ballot_sync(GNS_FULL, head);
+  if (lane == 0) s_warp[warp] = __popc(bal);
+  __syncthreads();
+  int base = 0, total = 0;
+  for (int w = 0; w < kTargetsBlock / 32; ++w) {
+    const int c = s_warp[w];
+    base += w < warp ? c : 0;
+    total += c;
+  }
+  if (head) out[base + __popc(bal & ((1u << lane) - 1u))] = v;
+  if (i == 0) out_n[0] = total;
+}
+
 template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) bitmap_rank_kernel(ScanStatus st, const uint32_t* __restrict__ bits,
                                                             int64_t nwords, int32_t* __restrict__ rank) {
@@ -308,6 +367,20 @@ int gns_epoch_targets_dev(const int32_t* train_ids, int64_t n_train, const gns_s
   epoch_targets_dev_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(train_ids, n_train, bits / 2, step_dev,
                                                                    max_count, out, out_n_dev);
   return check_launch("epoch_targets_dev");
+}
+
+int gns_batch_targets_sorted(const int32_t* train_ids, int64_t n_train, const gns_step_t* step_dev,
+                             int64_t max_count, int32_t* out_sorted, int32_t* out_n_dev, void* stream) {
+  if (max_count > kTargetsBlock) {
+    set_error("batch_targets_sorted: batch of %lld exceeds %d", (long long)max_count, kTargetsBlock);
+    return GNS_EINVAL;
+  }
+  int bits = 2;
+  while ((1ll << bits) < n_train) ++bits;
+  bits += bits & 1;
+  batch_targets_sorted_kernel<<<1, kTargetsBlock, 0, (cudaStream_t)stream>>>(train_ids, n_train, bits / 2, step_dev,
+                                                                            max_count, out_sorted, out_n_dev);
+  return check_launch("batch_targets_sorted");
 }
 
 int gns_bitmap_rank(const uint32_t* bits, int64_t nwords, int32_t* out_rank, void* ws,

@@ -278,12 +278,17 @@ class MiniBatchSampler:
         s = _lib.stream_ptr(stream)
         if not hasattr(self, "n_targets_dev"):
             self.n_targets_dev = torch.zeros(1, dtype=torch.int32, device=self.device)
-        if train_ids is not None:
-            _lib.call("gns_epoch_targets_dev", train_ids.data_ptr(), train_ids.numel(), step_dev.data_ptr(),
-                      self.max_targets, self.targets.data_ptr(), self.n_targets_dev.data_ptr(), s)
-        _lib.call("gns_unique_sorted", self.g.num_nodes, self.targets.data_ptr(), self.n_targets_dev.data_ptr(),
-                  self.max_targets, self.seeds0.data_ptr(), self.n_seeds0.data_ptr(), self.ws_relabel.data_ptr(),
-                  self.ws_relabel.numel(), s)
+        if train_ids is not None and self.max_targets <= 1024:
+            # epoch slice + np.unique in one single-CTA kernel
+            _lib.call("gns_batch_targets_sorted", train_ids.data_ptr(), train_ids.numel(), step_dev.data_ptr(),
+                      self.max_targets, self.seeds0.data_ptr(), self.n_seeds0.data_ptr(), s)
+        else:
+            if train_ids is not None:
+                _lib.call("gns_epoch_targets_dev", train_ids.data_ptr(), train_ids.numel(), step_dev.data_ptr(),
+                          self.max_targets, self.targets.data_ptr(), self.n_targets_dev.data_ptr(), s)
+            _lib.call("gns_unique_sorted", self.g.num_nodes, self.targets.data_ptr(), self.n_targets_dev.data_ptr(),
+                      self.max_targets, self.seeds0.data_ptr(), self.n_seeds0.data_ptr(),
+                      self.ws_relabel.data_ptr(), self.ws_relabel.numel(), s)
         gns = self.config.strategy == "GNS"
         if gns and cache is None:
             raise ValueError("GNS sampling needs a CacheState")

@@ -336,6 +336,31 @@ def test_epoch_targets_feistel(P):
     assert np.array_equal(np.sort(allv), np.flatnonzero(mask))
 
 
+@pytest.mark.parametrize("batch", [97, 1000, 1024])
+def test_batch_targets_sorted_matches_epoch_slice(P, batch):
+    """gns_batch_targets_sorted (Feistel epoch slice + np.unique in one CTA)
+    = np.unique of the reference's epoch batch (pool.py:60-66), every batch of
+    an epoch including the short last one."""
+    from paper_2106_06150_b200 import _lib
+    n = 7000
+    og = O.build_csr(np.random.default_rng(0).integers(0, n, size=(20000, 2)), n)
+    mask = np.random.default_rng(2).random(n) < 0.4
+    og.train_mask = mask
+    g = P.Graph.from_numpy(n, og.indptr, og.indices, train_mask=mask)
+    seed, epoch = 6, 2
+    ref = O.epoch_targets(og, batch, seed, epoch)
+    tid = g.train_ids()
+    out = torch.empty(batch, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for k, r in enumerate(ref):
+        step = torch.tensor([(seed & 0xFFFFFFFF) | (epoch << 32), k, k * batch, batch], dtype=torch.int64,
+                            device="cuda")
+        _lib.call("gns_batch_targets_sorted", tid.data_ptr(), tid.numel(), step.data_ptr(), batch, out.data_ptr(),
+                  cnt.data_ptr(), _lib.stream_ptr())
+        m = int(cnt)
+        assert np.array_equal(out[:m].cpu().numpy(), np.unique(r)), k
+
+
 def test_pool_deterministic_and_complete(P):
     og = _hub_graph(3000, 5)
     mask = np.random.default_rng(2).random(3000) < 0.5
