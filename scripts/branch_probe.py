@@ -54,7 +54,14 @@ def main():
         print("kernel-node |priority| histogram:", tr.kernel_priorities(0))
     except RuntimeError as e:
         print("kernel-node priorities unavailable:", e)
+    def production_empty():
+        tr._replay(0)
+
+    variants["production, sampling an empty batch"] = production_empty
     for name, replay in variants.items():
+        if name.startswith("production, sampling an empty"):
+            torch.cuda.synchronize()
+            tr._set_step(tr.S, 0, None)
         for _ in range(3):
             replay()
         torch.cuda.synchronize()
