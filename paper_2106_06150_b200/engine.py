@@ -1,21 +1,25 @@
 """Whole-step CUDA-graph training engine (the B200 answer to pool.py + model.py:257-307).
 
-One replay of a captured graph = one training step: on a side branch it
-samples the NEXT mini-batch into one sampler slot (epoch-permutation slice,
-L x (sample, relabel) — all device-count driven), while the main branch runs
-gather -> L x (SpMM + GEMM) -> softmax-CE -> backward -> Adam on the CURRENT
-batch held in the other slot.  Two graphs alternate the slot roles, so the
-host issues one graph launch per step and the sampler overlaps training.
+One replay of a captured graph = one training step (``steps_per_graph`` > 1:
+several): on a high-priority side branch it samples the NEXT mini-batch into
+one sampler slot (epoch-permutation slice, L x (sample, dedup, relabel), the
+backward's block transposes — all device-count driven), while the main branch
+runs the fused feature gather + aggregation -> L x (SpMM + GEMM) -> softmax-CE
+-> backward -> [NCCL all-reduce] -> Adam on the CURRENT batch held in the
+other slot.  Two graphs alternate the slot roles, so the host issues one
+graph launch per step.
 
 Per-batch values (Philox key, the batch's slice of the epoch permutation)
 live in a device ``gns_step_t`` refreshed from pinned host memory by a
 memcpy node inside the graph.  Dense tensors are allocated at the static
 capacity bounds; kernels zero-fill rows past the device counts, so GEMMs
-over padded rows contribute exact zeros to the gradients.
+over padded rows contribute exact zeros, and the input layer's two
+capacity-sized GEMMs are SWITCH conditional nodes that run over
+ceil(n / chunk) * chunk rows of the batch's device count.
 
-The cache (cache.py) is rebuilt at epoch boundaries every ``cache_period``
-epochs (pool.py:133-135); the graphs capture the cache pointers, so they are
-re-captured after each refresh.
+The cache (cache.py) is redrawn at epoch boundaries every ``cache_period``
+epochs (pool.py:133-135) into the same device buffers, so the graphs stay
+valid (re-captured only if a buffer has to grow, or for the mixed placement).
 """
 
 from __future__ import annotations
