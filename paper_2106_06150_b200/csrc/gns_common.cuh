@@ -9,6 +9,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "../../include/gns.h"
 
 #define GNS_WARP 32
@@ -58,6 +61,27 @@ static inline unsigned div_up(long long a, long long b) { return (unsigned)((a +
 static inline int grid_for(long long want, long long cap) {
   long long g = want < cap ? want : cap;
   return (int)(g < 1 ? 1 : g);
+}
+
+// Grid for a grid-stride kernel: at most one wave of resident CTAs
+// (cudaOccupancyMaxActiveBlocksPerMultiprocessor, cached per kernel), so no
+// CTA waits for a second wave and no empty CTAs are launched past it.
+template <typename Kernel>
+static inline int resident_grid(Kernel kernel, int block, size_t smem, long long want) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> per_sm_cache;
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_sm_cache.find((const void*)kernel);
+    if (it != per_sm_cache.end()) {
+      per_sm = it->second;
+    } else {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess) per_sm = 1;
+      per_sm_cache[(const void*)kernel] = per_sm;
+    }
+  }
+  return grid_for(want, (long long)num_sms() * (per_sm > 0 ? per_sm : 1));
 }
 
 // Bump allocator over a caller-given workspace (256-byte aligned slices).

@@ -587,8 +587,9 @@ static int g_tune_wide = 1;    // hidden-layer forward: 1 = spmm_fwd_wide_kernel
 // Forward SpMM grids: one wave of persistent CTAs (grid-stride rows).  Short
 // CTAs (k rows per warp, many waves) were measured slower both alone and
 // next to the sampling branch on B200.
-static inline int spmm_grid(long long rows) {
-  return grid_for((rows * 32 + kSpmmBlock - 1) / kSpmmBlock, (long long)num_sms() * 8);
+template <typename Kernel>
+static inline int spmm_grid(Kernel k, long long rows) {
+  return resident_grid(k, kSpmmBlock, 0, (rows * 32 + kSpmmBlock - 1) / kSpmmBlock);
 }
 
 // ---- SpMM backward -------------------------------------------------------------
@@ -1129,11 +1130,11 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
   }
   const int sms = num_sms();
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
-  int grid = spmm_grid(rows);
   BlockView bv = view_of(block);
   const int dv = dim / 4;
   if (dv <= 32 && g_tune_narrow == 1) {
-    spmm_fwd_narrow_kernel<false, true><<<grid, kSpmmBlock, 0, stream>>>(table, ld_table, dim, bv, cat, ld_cat,
+    spmm_fwd_narrow_kernel<false, true><<<spmm_grid(spmm_fwd_narrow_kernel<false, true>, rows), kSpmmBlock, 0,
+                                          stream>>>(table, ld_table, dim, bv, cat, ld_cat,
                                                                         pad_rows, block->edge_node, dst_ids,
                                                                         pad_chunk);
     return check_launch("spmm_fwd_gather");
@@ -1142,13 +1143,9 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
     set_error("spmm_fwd_gather: pad_chunk needs the narrow kernel (dim <= 128)");
     return GNS_EINVAL;
   }
-  if (dv <= 32 && g_tune_narrow == 2) {
-    spmm_fwd_narrow_kernel<false, true, 8, 3><<<grid, kSpmmBlock, 0, stream>>>(
-        table, ld_table, dim, bv, cat, ld_cat, pad_rows, block->edge_node, dst_ids);
-    return check_launch("spmm_fwd_gather");
-  }
 #define GNS_FWDG(CH)                                                                                          \
-  spmm_fwd_kernel<float, CH, false, true><<<grid, kSpmmBlock, 0, stream>>>(table, ld_table, dim, bv, cat, ld_cat, \
+  spmm_fwd_kernel<float, CH, false, true><<<spmm_grid(spmm_fwd_kernel<float, CH, false, true>, rows), kSpmmBlock, \
+                                            0, stream>>>(table, ld_table, dim, bv, cat, ld_cat,             \
                                                                           pad_rows, block->edge_node, dst_ids)
   if (dv <= 32) GNS_FWDG(1);
   else if (dv <= 64) GNS_FWDG(2);
@@ -1170,21 +1167,23 @@ int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block
     return GNS_EINVAL;
   }
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
-  int grid = spmm_grid(rows);
   BlockView bv = view_of(block);
   const int dv = dim / 4;
   if (g_tune_wide && dv > 32 && dv <= 64) {
-    spmm_fwd_wide_kernel<2, 4, true><<<grid, kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows,
+    spmm_fwd_wide_kernel<2, 4, true><<<spmm_grid(spmm_fwd_wide_kernel<2, 4, true>, rows), kSpmmBlock, 0,
+                                       stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows,
                                                                      relu_bits);
     return check_launch("spmm_fwd_bits");
   }
   if (g_tune_wide && dv > 64 && dv <= 128) {
-    spmm_fwd_wide_kernel<4, 2, true><<<grid, kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows,
+    spmm_fwd_wide_kernel<4, 2, true><<<spmm_grid(spmm_fwd_wide_kernel<4, 2, true>, rows), kSpmmBlock, 0,
+                                       stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows,
                                                                      relu_bits);
     return check_launch("spmm_fwd_bits");
   }
 #define GNS_FWDB(CH)                                                                                             \
-  spmm_fwd_kernel<float, CH, true, false, true><<<grid, kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat, \
+  spmm_fwd_kernel<float, CH, true, false, true><<<spmm_grid(spmm_fwd_kernel<float, CH, true, false, true>, rows), \
+                                                  kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat,       \
                                                                                 pad_rows, nullptr, nullptr,   \
                                                                                 relu_bits)
   if (dv <= 32) GNS_FWDB(1);
@@ -1211,16 +1210,23 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
     return GNS_EINVAL;
   }
   BlockView bv = view_of(block);
-  int g2 = grid_for(((max_src > pad_rows ? max_src : pad_rows) * 32 + 255) / 256, (long long)num_sms() * 8);
+  const long long want = ((max_src > pad_rows ? max_src : pad_rows) * 32 + 255) / 256;
+  int g2 = 1;
   const int dv = dim / 4;
+  // one wave of resident CTAs (<= 8 per SM: the colpart workspace bound)
 #define GNS_BWDB(CH)                                                                                             \
+  g2 = resident_grid(spmm_bwd_kernel<float, CH, true>, kSpmmBlock, 0, want < num_sms() * 8LL ? want : num_sms() * 8LL); \
   spmm_bwd_kernel<float, CH, true><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,       \
                                                                   w.self_of, dh, ld_dh, pad_rows, nullptr,       \
                                                                   db ? (float*)w.colpart : nullptr, relu_bits,   \
                                                                   w.twn)
-  if (dv <= 32) GNS_BWDB(1);
-  else if (dv <= 64) GNS_BWDB(2);
-  else GNS_BWDB(4);
+  if (dv <= 32) {
+    GNS_BWDB(1);
+  } else if (dv <= 64) {
+    GNS_BWDB(2);
+  } else {
+    GNS_BWDB(4);
+  }
 #undef GNS_BWDB
   GNS_TRY(check_launch("spmm_bwd_bits"));
   if (db) colsum_final_kernel<float><<<colsum_grid(dim), kColsumWarps * 32, 0, stream>>>((const float*)w.colpart, g2, dim, db);
@@ -1233,11 +1239,11 @@ int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_
   if (max_dst <= 0 && pad_rows <= 0) return GNS_OK;
   const int sms = num_sms();
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
-  int grid = spmm_grid(rows);
   BlockView bv = view_of(block);
   const bool relu = flags & GNS_SPMM_RELU_INPUT;
 #define GNS_FWD(T, CH, R)                                                                                      \
-  spmm_fwd_kernel<T, CH, R><<<grid, kSpmmBlock, 0, stream>>>((const T*)h, ld_h, dim, bv, (T*)cat, ld_cat, pad_rows)
+  spmm_fwd_kernel<T, CH, R><<<spmm_grid(spmm_fwd_kernel<T, CH, R>, rows), kSpmmBlock, 0, stream>>>(                \
+      (const T*)h, ld_h, dim, bv, (T*)cat, ld_cat, pad_rows)
   if (dtype == 0) {
     if (dim % 4 || ld_h % 4 || ld_cat % 4) {
       set_error("spmm_fwd(f32): dim/strides must be multiples of 4");
@@ -1246,11 +1252,13 @@ int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_
     const int dv = dim / 4;
     if (dv <= 32 && g_tune_narrow) {
       if (relu)
-        spmm_fwd_narrow_kernel<true, false><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv,
+        spmm_fwd_narrow_kernel<true, false><<<spmm_grid(spmm_fwd_narrow_kernel<true, false>, rows), kSpmmBlock, 0,
+                                              stream>>>((const float*)h, ld_h, dim, bv,
                                                                             (float*)cat, ld_cat, pad_rows, nullptr,
                                                                             nullptr);
       else
-        spmm_fwd_narrow_kernel<false, false><<<grid, kSpmmBlock, 0, stream>>>((const float*)h, ld_h, dim, bv,
+        spmm_fwd_narrow_kernel<false, false><<<spmm_grid(spmm_fwd_narrow_kernel<false, false>, rows), kSpmmBlock, 0,
+                                               stream>>>((const float*)h, ld_h, dim, bv,
                                                                              (float*)cat, ld_cat, pad_rows, nullptr,
                                                                              nullptr);
     } else if (dv <= 32) { if (relu) GNS_FWD(float, 1, true); else GNS_FWD(float, 1, false); }

@@ -1013,8 +1013,9 @@ static int run_enumerate(const DedupWs& d, int32_t* out, int32_t* out_n, cudaStr
 static int run_relabel(const DedupWs& d, const int32_t* seeds, const int32_t* n_seeds_dev, int64_t max_dst,
                        gns_block_t* block, int64_t max_edges, cudaStream_t stream) {
   GNS_TRY(run_enumerate(d, block->src_nodes, block->counts + GNS_CNT_SRC, stream));
-  int grid = grid_for((max_dst + max_edges + 255) / 256 + 1,
-                      (long long)num_sms() * (g_sampler_ctas ? g_sampler_ctas : 16));
+  const int grid = resident_grid(relabel_kernel, 256, 0,
+                                 grid_for((max_dst + max_edges + 255) / 256 + 1,
+                                          g_sampler_ctas ? (long long)num_sms() * g_sampler_ctas : (1LL << 30)));
   relabel_kernel<<<grid, 256, 0, stream>>>(d.rank2, seeds, n_seeds_dev, block->edge_node, block->counts,
                                            block->self_pos, block->edge_src);
   return check_launch("relabel");
@@ -1107,14 +1108,15 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   // calling stream, warp and hub tiers on a forked branch, concurrently
   Fork fk;
   GNS_TRY(fork_begin(stream, &fk));
-  const long long cap16 = (long long)sms * (g_sampler_ctas ? g_sampler_ctas : 16);
-  const long long cap8 = (long long)sms * (g_sampler_ctas ? g_sampler_ctas : 8);
-  int tgrid = grid_for((2 * max_dst + 255) / 256, cap16);
-  sample_stream_kernel<<<tgrid, 256, 0, stream>>>(a);
+  // one wave of resident CTAs at most (grid-stride loops over the item lists)
+  const long long cap = g_sampler_ctas ? (long long)sms * g_sampler_ctas : (1LL << 30);
+  const long long titems = grid_for((2 * max_dst + 255) / 256, cap);
+  sample_stream_kernel<<<resident_grid(sample_stream_kernel, 256, 0, titems), 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_stream"));
-  sample_thread_kernel<<<tgrid, 256, 0, stream>>>(a);
+  sample_thread_kernel<<<resident_grid(sample_thread_kernel, 256, 0, titems), 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_thread"));
-  int grid = grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock, cap8);
+  const int grid = resident_grid(sample_warp_kernel, kSampBlock, 0,
+                                 grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock, cap));
   sample_warp_kernel<<<grid, kSampBlock, 0, fk.aux>>>(a);
   GNS_TRY(check_launch("sample_warp"));
   sample_hub_kernel<<<sms, kHubBlock, 0, fk.aux>>>(a);
