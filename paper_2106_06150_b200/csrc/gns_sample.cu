@@ -67,13 +67,13 @@ struct LayerArgs {
   gns_block_t b;
 };
 
-// mark node v in the two-level dedup bitmap
+// mark node v in the two-level dedup bitmap: two fire-and-forget reductions
+// (RED, no returned value to wait for).  The summary bit is set by every mark
+// (idempotent), so every non-zero bitmap word has its summary bit.
 __device__ __forceinline__ void mark_node(uint32_t* __restrict__ bits, uint32_t* __restrict__ sum, int32_t v) {
-  const uint32_t m = 1u << (v & 31);
   const int32_t w = v >> 5;
-  if (__ldg(bits + w) & m) return;  // already set (read-only fast path)
-  const uint32_t old = atomicOr(bits + w, m);
-  if (old == 0u) atomicOr(sum + (w >> 5), 1u << (w & 31));
+  atomicOr(bits + w, 1u << (v & 31));
+  atomicOr(sum + (w >> 5), 1u << (w & 31));
 }
 
 // Lists of (row, phase) work items per tier, packed in hub_rows[4*max_dst]:
@@ -253,27 +253,11 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __g
       tier[2 * j] = on && m > 0 ? phase_tier(nc, m, a.stream_len, a.thread_len) : -1;
       tier[2 * j + 1] = on && fill > 0 ? phase_tier(deg, fill, a.stream_len, a.thread_len) : -1;
     }
-    // dedup marks of the seeds: every row's bitmap probe, then every row's
-    // atomics, in flight together (mark_node's steps, batched)
+    // dedup marks of the seeds (fire-and-forget reductions)
     if (a.dbits) {
-      uint32_t bw[kCntItems];
 #pragma unroll
-      for (int j = 0; j < kCntItems; ++j) {
-        const long long r = base + j * kCntBlock + threadIdx.x;
-        bw[j] = r < n ? __ldg(a.dbits + (node[j] >> 5)) : ~0u;
-      }
-      uint32_t old[kCntItems];
-#pragma unroll
-      for (int j = 0; j < kCntItems; ++j) {
-        const uint32_t mb = 1u << (node[j] & 31);
-        old[j] = ~0u;
-        if (!(bw[j] & mb)) old[j] = atomicOr(a.dbits + (node[j] >> 5), mb);
-      }
-#pragma unroll
-      for (int j = 0; j < kCntItems; ++j) {
-        const int32_t w = node[j] >> 5;
-        if (old[j] == 0u) atomicOr(a.dsum + (w >> 5), 1u << (w & 31));
-      }
+      for (int j = 0; j < kCntItems; ++j)
+        if (base + j * kCntBlock + threadIdx.x < n) mark_node(a.dbits, a.dsum, node[j]);
     }
     // all 2*kCntItems (row, phase) items of the warp in one aggregated append
     int h[2 * kCntItems];
@@ -629,7 +613,7 @@ __device__ __forceinline__ void thread_select16(const LayerArgs& a, const Rng3& 
   }
   // 3. (key, position) order = the reference's stable lexsort
   sort16(v);
-  // 4. emit the first `take`: every load (neighbour id, inclusion, dedup word)
+  // 4. emit the first `take`: every load (neighbour id, inclusion)
   //    of all selected edges is issued before any store, so the edges' memory
   //    latencies overlap instead of serialising behind possibly-aliasing stores
   const int take = ph.take;
@@ -637,23 +621,15 @@ __device__ __forceinline__ void thread_select16(const LayerArgs& a, const Rng3& 
 #pragma unroll
   for (int i = 0; i < 16; ++i) u[i] = i < take ? __ldg(ph.ids + (uint32_t)(v[i] & 2047u)) : 0;
   double inc[16];
-  uint32_t bw[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    inc[i] = (i < take && ph.phase == 0 && !a.exact_q) ? __ldg(a.incl + u[i]) : 0.0;
-    bw[i] = i < take ? __ldg(a.dbits + (u[i] >> 5)) : 0u;
-  }
+  for (int i = 0; i < 16; ++i) inc[i] = (i < take && ph.phase == 0 && !a.exact_q) ? __ldg(a.incl + u[i]) : 0.0;
   const int64_t o0 = ph.out_base;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     if (i < take) {
       const double w = a.exact_q ? exact_weight(a, ri, ph, (uint32_t)(v[i] & 2047u))
                                  : edge_weight_of(a, ri, ph, inc[i]);
-      const uint32_t m = 1u << (u[i] & 31);
-      if (!(bw[i] & m)) {
-        const uint32_t old = atomicOr(a.dbits + (u[i] >> 5), m);
-        if (old == 0u) atomicOr(a.dsum + ((u[i] >> 5) >> 5), 1u << ((u[i] >> 5) & 31));
-      }
+      mark_node(a.dbits, a.dsum, u[i]);
       a.b.edge_node[o0 + i] = u[i];
       a.b.edge_dst[o0 + i] = (int32_t)r;
       a.b.edge_weight[o0 + i] = w;
@@ -717,24 +693,17 @@ __device__ __forceinline__ void thread_select_stream(const LayerArgs& a, const R
     if (c0 >= take) break;
     int32_t u[4];
     double inc[4];
-    uint32_t bw[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) u[i] = c0 + i < take ? __ldg(ph.ids + (uint32_t)(best[c0 + i] & 2047u)) : 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 4; ++i)
       inc[i] = (c0 + i < take && ph.phase == 0 && !a.exact_q) ? __ldg(a.incl + u[i]) : 0.0;
-      bw[i] = c0 + i < take ? __ldg(a.dbits + (u[i] >> 5)) : 0u;
-    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (c0 + i < take) {
         const double w = a.exact_q ? exact_weight(a, ri, ph, (uint32_t)(best[c0 + i] & 2047u))
                                    : edge_weight_of(a, ri, ph, inc[i]);
-        const uint32_t m = 1u << (u[i] & 31);
-        if (!(bw[i] & m)) {
-          const uint32_t old = atomicOr(a.dbits + (u[i] >> 5), m);
-          if (old == 0u) atomicOr(a.dsum + ((u[i] >> 5) >> 5), 1u << ((u[i] >> 5) & 31));
-        }
+        mark_node(a.dbits, a.dsum, u[i]);
         a.b.edge_node[o0 + c0 + i] = u[i];
         a.b.edge_dst[o0 + c0 + i] = (int32_t)r;
         a.b.edge_weight[o0 + c0 + i] = w;

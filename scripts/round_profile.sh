@@ -14,6 +14,9 @@ timeout 600 python bench.py --impl reference > $O/bench_papers100m_reference.log
 for c in products oag cfg1; do
   timeout 600 python bench.py --config $c > $O/bench_$c.log 2>&1
 done
+# ncu cannot profile kernel nodes of graphs with conditional nodes: profile with the
+# size-switched GEMMs off (GNS_SWITCH_CHUNK=0; every other kernel is identical)
+export GNS_SWITCH_CHUNK=0
 ncu --metrics gpu__time_duration.sum --clock-control none -s 1500 -c 300 --csv --log-file $O/launches_papers100m.csv \
     python bench.py --steps 20 --warmup 10 --no-cpu-baseline --e2e-steps 0 > $O/ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"spmm_fwd_narrow|spmm_bwd_kernel|spmm_fwd_kernel" \
