@@ -311,10 +311,15 @@ def main():
         cnt = tr.slots[tr.slot_of(k)].counts[len(FANOUTS) - 1].tolist()
         n_in.append(cnt[_lib.CNT_SRC])
         nd, ne = cnt[_lib.CNT_DST], cnt[_lib.CNT_EDGES]
-        # input-layer SpMM: h rows read (edges + self) + cat rows written (incl.
-        # capacity zero padding) + per-edge index/weight (4 + 8 B) + row scan
-        # (+ dst id when the gather is fused)
-        spmm_bytes.append((ne + nd) * 4 * D + tr.npad[0] * 2 * 4 * D + 12 * ne + (12 if tr.fused_gather else 8) * nd)
+        # input-layer SpMM, algorithmic bytes: every
+        # distinct input row read once (n_src; a batch's repeated rows are L2
+        # hits, ncu DRAM traffic ~ this) + the cat rows written, incl. the zero
+        # padding the GEMM reads (up to the size-switched row count) +
+        # per-edge index/weight (4 + 8 B) + row scan (+ dst id, fused gather)
+        C = tr.switch_chunk
+        rows_w = min(tr.npad[0], -(-nd // C) * C) if tr.use_switch else tr.npad[0]
+        spmm_bytes.append(cnt[_lib.CNT_SRC] * 4 * D + rows_w * 2 * 4 * D + 12 * ne
+                          + (12 if tr.fused_gather else 8) * nd)
     pos = tr.run(nprof, epoch=pos[0], first=pos[1], on_step=on_step)
     n_in = np.array(n_in, dtype=np.float64)
     gbytes = n_in * (2 * 4 * D + 4)     # rows read + rows written + int32 ids

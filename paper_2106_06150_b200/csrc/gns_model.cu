@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
                                                               int64_t pad_rows,
                                                               const int32_t* __restrict__ edge_node = nullptr,
                                                               const int32_t* __restrict__ dst_ids = nullptr,
-                                                              uint32_t* __restrict__ relu_bits = nullptr) {
+                                                              uint32_t* __restrict__ relu_bits = nullptr,
+                                                              int64_t pad_chunk = 0) {
   const int32_t* __restrict__ eidx = GATHER ? edge_node : bv.edge_src;
   using V = typename Vec<T>::type;
   constexpr int VW = Vec<T>::W;
@@ -348,7 +349,8 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
     }
     __syncwarp();
   }
-  for (int64_t r = n + gw; r < pad_rows; r += nw) {
+  const int64_t pad_end = pad_chunk > 0 ? min(pad_rows, (n + pad_chunk - 1) / pad_chunk * pad_chunk) : pad_rows;
+  for (int64_t r = n + gw; r < pad_end; r += nw) {
     V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
     V zero;
     vzero(zero);
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
 // flight at once, then the weighted sum runs in ascending source order (the
 // scipy CSR order, same FMA sequence as spmm_fwd_kernel: bit-identical).
 // Rows with more than 32 edges take the generic per-row path.
-template <bool RELU, bool GATHER, int kNarrowGroup = 4, int kMinBlocks = 4>
+template <bool RELU, bool GATHER, int kNarrowGroup = 3, int kMinBlocks = 4>
 __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel(const float* __restrict__ h, int64_t ld_h,
                                                                          int dim, BlockView bv,
                                                                          float* __restrict__ cat, int64_t ld_cat,
@@ -379,10 +381,22 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel
   const bool on = lane < dv;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // the next row's scan bounds are requested while the current row's feature
+  // rows are in flight, so its edge loads issue at once (one round trip less
+  // per row; the self id and degree load alongside them)
+  uint64_t n_s0 = 0, n_s1 = 0;
+  if (gw < n) {
+    n_s0 = bv.row_scan[gw];
+    n_s1 = bv.row_scan[gw + 1];
+  }
   for (int64_t r = gw; r < n; r += nw) {
-    const uint64_t s0 = bv.row_scan[r], s1 = bv.row_scan[r + 1];
+    const uint64_t s0 = n_s0, s1 = n_s1;
     const int64_t self = GATHER ? (int64_t)dst_ids[r] : (int64_t)bv.self_pos[r];
     const float norm = (float)max(bv.dst_degree[r], 1);
+    if (r + nw < n) {
+      n_s0 = bv.row_scan[r + nw];
+      n_s1 = bv.row_scan[r + nw + 1];
+    }
     const int64_t cb = (int64_t)(s0 >> 32), ce = (int64_t)(s1 >> 32);
     const int64_t fb = tm + (int64_t)(s0 & 0xffffffffull), fe = tm + (int64_t)(s1 & 0xffffffffull);
     const int nc = (int)(ce - cb), L = nc + (int)(fe - fb);
@@ -1139,14 +1153,10 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
                                                                         pad_chunk);
     return check_launch("spmm_fwd_gather");
   }
-  if (pad_chunk > 0) {
-    set_error("spmm_fwd_gather: pad_chunk needs the narrow kernel (dim <= 128)");
-    return GNS_EINVAL;
-  }
 #define GNS_FWDG(CH)                                                                                          \
   spmm_fwd_kernel<float, CH, false, true><<<spmm_grid(spmm_fwd_kernel<float, CH, false, true>, rows), kSpmmBlock, \
                                             0, stream>>>(table, ld_table, dim, bv, cat, ld_cat,             \
-                                                                          pad_rows, block->edge_node, dst_ids)
+                                                         pad_rows, block->edge_node, dst_ids, nullptr, pad_chunk)
   if (dv <= 32) GNS_FWDG(1);
   else if (dv <= 64) GNS_FWDG(2);
   else GNS_FWDG(4);

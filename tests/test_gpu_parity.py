@@ -467,6 +467,13 @@ def test_spmm_fwd_gather_equals_gather_then_spmm(P, dim):
         _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 5, 0,
                   b.data_ptr(), 2 * dim, _lib.stream_ptr())
         assert torch.equal(a, b), li
+        # chunk-bounded zero padding: rows [n, ceil(n/8)*8) zeroed, the rest untouched
+        c = torch.full((ndst + 40, 2 * dim), 9.0, device="cuda")
+        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 40, 8,
+                  c.data_ptr(), 2 * dim, _lib.stream_ptr())
+        end = min(-(-ndst // 8) * 8, ndst + 40)
+        assert torch.equal(c[:ndst], a[:ndst])
+        assert bool((c[ndst:end] == 0).all()) and bool((c[end:] == 9.0).all())
 
 
 @pytest.mark.parametrize("dim", [132, 256, 512])
