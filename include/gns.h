@@ -336,11 +336,15 @@ GNS_API int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim
  * features[input_nodes].  Output identical to gns_gather_rows followed by
  * gns_spmm_fwd(dtype 0, flags 0).  pad_chunk > 0 zero-fills rows [n, pad_rows)
  * only up to the next multiple of pad_chunk (what a size-switched GEMM over
- * the first ceil(n / pad_chunk) * pad_chunk rows reads). */
+ * the first ceil(n / pad_chunk) * pad_chunk rows reads).  max_row_edges: an
+ * upper bound on a row's edges (the layer's fanout; 0 = unknown), a hint for
+ * kernel selection (a cp.async shared-memory-staged variant for D = 128,
+ * fanout <= 5 measured 121 us vs 90 us for the register-staged kernel on the
+ * papers100M batch and is not used). */
 GNS_API int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim,
                                 const gns_block_t* block, const int32_t* dst_ids, int64_t max_dst,
-                                int64_t pad_rows, int64_t pad_chunk, float* cat, int64_t ld_cat,
-                                void* stream);
+                                int64_t pad_rows, int64_t pad_chunk, int32_t max_row_edges, float* cat,
+                                int64_t ld_cat, void* stream);
 
 /* out[c] = sum over r < nrows of part[r * ncols + c], fixed order (the
  * reduction of split-K partial products).  dtype 0 = float32, 1 = float64. */

@@ -119,7 +119,7 @@ _SIGS = {
     "gns_spmm_fwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, c_int32, POINTER(GnsBlock),
                                c_int64, c_int64, c_void_p, c_int64, c_void_p]),
     "gns_spmm_fwd_gather": (c_int32, [c_void_p, c_int64, c_int32, POINTER(GnsBlock), c_void_p, c_int64, c_int64,
-                                      c_int64, c_void_p, c_int64, c_void_p]),
+                                      c_int64, c_int32, c_void_p, c_int64, c_void_p]),
     "gns_sum_rows": (c_int32, [c_int32, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "gns_spmm_bwd_workspace_size": (c_size_t, [c_int64, c_int64, c_int32]),
     "gns_spmm_bwd": (c_int32, [c_int32, c_void_p, c_int64, c_int32, POINTER(GnsBlock), c_int64,

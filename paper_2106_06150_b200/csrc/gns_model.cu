@@ -1134,8 +1134,8 @@ int gns_sum_rows(int32_t dtype, const void* part, int64_t nrows, int64_t ncols, 
 }
 
 int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const gns_block_t* block,
-                        const int32_t* dst_ids, int64_t max_dst, int64_t pad_rows, int64_t pad_chunk, float* cat,
-                        int64_t ld_cat, void* stream_) {
+                        const int32_t* dst_ids, int64_t max_dst, int64_t pad_rows, int64_t pad_chunk,
+                        int32_t max_row_edges, float* cat, int64_t ld_cat, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (max_dst <= 0 && pad_rows <= 0) return GNS_OK;
   if (dim % 4 || ld_table % 4 || ld_cat % 4 || (uintptr_t)table % 16 || (uintptr_t)cat % 16) {
@@ -1146,6 +1146,7 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
   BlockView bv = view_of(block);
   const int dv = dim / 4;
+  (void)max_row_edges;
   if (dv <= 32 && g_tune_narrow == 1) {
     spmm_fwd_narrow_kernel<false, true><<<spmm_grid(spmm_fwd_narrow_kernel<false, true>, rows), kSpmmBlock, 0,
                                           stream>>>(table, ld_table, dim, bv, cat, ld_cat,

@@ -213,7 +213,7 @@ class GraphedTrainer:
                     dst_ids = sl.layers[L - 2].src_nodes if L > 1 else sl.seeds0
                     _lib.call("gns_spmm_fwd_gather", tab.data_ptr(), tab.stride(0), d_in, blocks[0].cblock,
                               dst_ids.data_ptr(), self.cap_dst[0], self.npad[0],
-                              self.switch_chunk if self.use_switch else 0, self.cat[0].data_ptr(),
+                              self.switch_chunk if self.use_switch else 0, blocks[0].k, self.cat[0].data_ptr(),
                               self.cat[0].stride(0), s)
                 elif li > 0:
                     _lib.call("gns_spmm_fwd_bits", h.data_ptr(), h.stride(0), d_in, blocks[li].cblock,

@@ -43,7 +43,7 @@ def main():
     cat = torch.empty((tr.npad[0], 2 * D), device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ref = None
-    for v in (0, 1):
+    for v in (0, 1):   # 0: generic, 1: register-staged narrow
         _lib.call("gns_tune", b"spmm_narrow", v)
         ts = []
         for it in range(args.reps + 2):
@@ -52,7 +52,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             _lib.call("gns_spmm_fwd_gather", tab.data_ptr(), tab.stride(0), D, sl.layers[L - 1].cblock,
-                      sl.layers[L - 2].src_nodes.data_ptr(), tr.cap_dst[0], tr.npad[0], 0, cat.data_ptr(),
+                      sl.layers[L - 2].src_nodes.data_ptr(), tr.cap_dst[0], tr.npad[0], 0, 5, cat.data_ptr(),
                       cat.stride(0), _lib.stream_ptr())
             e1.record()
             e1.synchronize()
@@ -63,7 +63,7 @@ def main():
         # equality on slot 0
         sl = slots[0]
         _lib.call("gns_spmm_fwd_gather", tab.data_ptr(), tab.stride(0), D, sl.layers[L - 1].cblock,
-                  sl.layers[L - 2].src_nodes.data_ptr(), tr.cap_dst[0], tr.npad[0], 0, cat.data_ptr(),
+                  sl.layers[L - 2].src_nodes.data_ptr(), tr.cap_dst[0], tr.npad[0], 0, 5, cat.data_ptr(),
                   cat.stride(0), _lib.stream_ptr())
         out = cat.clone()
         same = True if ref is None else bool(torch.equal(out, ref))

@@ -464,16 +464,22 @@ def test_spmm_fwd_gather_equals_gather_then_spmm(P, dim):
         _lib.call("gns_spmm_fwd", 0, h.data_ptr(), dim, dim, 0, bg._c, ndst, ndst + 5, a.data_ptr(), 2 * dim,
                   _lib.stream_ptr())
         dst = torch.as_tensor(br.dst_nodes.astype(np.int32), device="cuda")
-        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 5, 0,
+        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 5, 0, 0,
                   b.data_ptr(), 2 * dim, _lib.stream_ptr())
         assert torch.equal(a, b), li
         # chunk-bounded zero padding: rows [n, ceil(n/8)*8) zeroed, the rest untouched
         c = torch.full((ndst + 40, 2 * dim), 9.0, device="cuda")
-        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 40, 8,
+        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 40, 8, 0,
                   c.data_ptr(), 2 * dim, _lib.stream_ptr())
         end = min(-(-ndst // 8) * 8, ndst + 40)
         assert torch.equal(c[:ndst], a[:ndst])
         assert bool((c[ndst:end] == 0).all()) and bool((c[end:] == 9.0).all())
+        # the fanout hint does not change the result
+        if dim == 128 and bg.fanout <= 5:
+            d = torch.full((ndst + 40, 2 * dim), 9.0, device="cuda")
+            _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), ndst, ndst + 40, 8,
+                      bg.fanout, d.data_ptr(), 2 * dim, _lib.stream_ptr())
+            assert torch.equal(c, d), li
 
 
 @pytest.mark.parametrize("dim", [132, 256, 512])
@@ -532,7 +538,7 @@ def test_spmm_fwd_narrow_equals_generic(P, dim):
                               2 * dim, _lib.stream_ptr())
                     outs[(v, relu)] = o
                 o = torch.full((nd + 3, 2 * dim), 5.0, device="cuda")
-                _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), nd, nd + 3, 0,
+                _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), nd, nd + 3, 0, 0,
                           o.data_ptr(), 2 * dim, _lib.stream_ptr())
                 outs[(v, "g")] = o
             for key in ((0, 1), "g"):
