@@ -151,6 +151,9 @@ __global__ void epoch_targets_dev_kernel(const int32_t* __restrict__ train_ids, 
 // first element of every run.  Replaces epoch_targets_dev + unique_small.
 constexpr int kTargetsBlock = 1024;
 
+// PERM: train_ids already holds the epoch's permutation (gns_epoch_targets
+// over the whole epoch), so target t is a plain coalesced load.
+template <bool PERM>
 __global__ void __launch_bounds__(kTargetsBlock) batch_targets_sorted_kernel(
     const int32_t* __restrict__ train_ids, int64_t n_train, int h, const gns_step_t* __restrict__ step,
     int64_t max_count, int32_t* __restrict__ out, int32_t* __restrict__ out_n) {
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(kTargetsBlock) batch_targets_sorted_kernel(
   int32_t v = INT32_MAX;
   if (i < count) {
     uint64_t y = (uint64_t)(begin + i);
-    if (n_train > 1) {
+    if (!PERM && n_train > 1) {
       y = feistel_once(y, h, step->seed, step->epoch);
       while (y >= (uint64_t)n_train) y = feistel_once(y, h, step->seed, step->epoch);
     }
@@ -378,9 +381,20 @@ int gns_batch_targets_sorted(const int32_t* train_ids, int64_t n_train, const gn
   int bits = 2;
   while ((1ll << bits) < n_train) ++bits;
   bits += bits & 1;
-  batch_targets_sorted_kernel<<<1, kTargetsBlock, 0, (cudaStream_t)stream>>>(train_ids, n_train, bits / 2, step_dev,
-                                                                            max_count, out_sorted, out_n_dev);
+  batch_targets_sorted_kernel<false><<<1, kTargetsBlock, 0, (cudaStream_t)stream>>>(
+      train_ids, n_train, bits / 2, step_dev, max_count, out_sorted, out_n_dev);
   return check_launch("batch_targets_sorted");
+}
+
+int gns_batch_slice_sorted(const int32_t* epoch_perm, int64_t n_train, const gns_step_t* step_dev, int64_t max_count,
+                           int32_t* out_sorted, int32_t* out_n_dev, void* stream) {
+  if (max_count > kTargetsBlock) {
+    set_error("batch_slice_sorted: batch of %lld exceeds %d", (long long)max_count, kTargetsBlock);
+    return GNS_EINVAL;
+  }
+  batch_targets_sorted_kernel<true><<<1, kTargetsBlock, 0, (cudaStream_t)stream>>>(
+      epoch_perm, n_train, 0, step_dev, max_count, out_sorted, out_n_dev);
+  return check_launch("batch_slice_sorted");
 }
 
 int gns_bitmap_rank(const uint32_t* bits, int64_t nwords, int32_t* out_rank, void* ws,

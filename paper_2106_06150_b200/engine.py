@@ -71,6 +71,11 @@ class GraphedTrainer:
         for sl in self.slots:
             sl.n_targets_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.train_ids = g.train_ids()
+        # the epoch's whole target permutation, computed once per epoch
+        # (gns_epoch_targets) so a step's first sampler kernel only slices it
+        self.epoch_perm = (torch.empty_like(self.train_ids)
+                           if os.environ.get("GNS_EPOCH_PERM", "1") == "1" and self.train_ids.numel() else None)
+        self._perm_epoch = None
         self.step_host = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(2 * S)]
         self.step_dev = [torch.zeros(4, dtype=torch.int64, device=self.dev) for _ in range(2 * S)]
         self.done = [None] * (2 * S)
@@ -331,7 +336,7 @@ class GraphedTrainer:
             joins.append(done)
         sl.enqueue_device(None if self.host_targets else self.train_ids, self.step_dev[slot],
                           self.cache if self.cfg.strategy == "GNS" else None, exact_tables=self._tables,
-                          after_layer=transpose)
+                          after_layer=transpose, epoch_perm=None if self.host_targets else self.epoch_perm)
         for ev in joins:
             cur.wait_event(ev)
 
@@ -543,6 +548,12 @@ class GraphedTrainer:
         if refresh and self._refresh_cache(epoch):
             self._free_execs()
         self.adam_t.fill_(self.model.step_count)
+        if self.epoch_perm is not None and self._perm_epoch != epoch:
+            n = self.train_ids.numel()
+            _lib.call("gns_epoch_targets", self.train_ids.data_ptr(), n, self.cfg.seed & 0xFFFFFFFF,
+                      epoch & 0xFFFFFFFF, 0, n, self.epoch_perm.data_ptr(), _lib.stream_ptr())
+            torch.cuda.synchronize()
+            self._perm_epoch = epoch
 
     def run_epoch(self, epoch: int, first: int = 0, max_steps: int | None = None, on_step=None) -> int:
         need_refresh = self.cfg.strategy == "GNS" and (

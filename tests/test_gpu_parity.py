@@ -359,6 +359,18 @@ def test_batch_targets_sorted_matches_epoch_slice(P, batch):
                   cnt.data_ptr(), _lib.stream_ptr())
         m = int(cnt)
         assert np.array_equal(out[:m].cpu().numpy(), np.unique(r)), k
+    # the engine's variant: slice of the epoch permutation computed up front
+    perm = torch.empty_like(tid)
+    _lib.call("gns_epoch_targets", tid.data_ptr(), tid.numel(), seed, epoch, 0, tid.numel(), perm.data_ptr(),
+              _lib.stream_ptr())
+    for k, r in enumerate(ref):
+        step = torch.tensor([(seed & 0xFFFFFFFF) | (epoch << 32), k, k * batch, batch], dtype=torch.int64,
+                            device="cuda")
+        out.fill_(-1)
+        _lib.call("gns_batch_slice_sorted", perm.data_ptr(), perm.numel(), step.data_ptr(), batch, out.data_ptr(),
+                  cnt.data_ptr(), _lib.stream_ptr())
+        m = int(cnt)
+        assert np.array_equal(out[:m].cpu().numpy(), np.unique(r)), k
 
 
 def test_pool_deterministic_and_complete(P):
