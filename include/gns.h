@@ -290,9 +290,13 @@ GNS_API int gns_batch_targets_sorted(const int32_t* train_ids, int64_t n_train,
 /* Same from a precomputed epoch permutation (epoch_perm[j] = the j-th target
  * of the epoch, gns_epoch_targets over the whole epoch): the batch is the
  * slice [begin, begin + count), sorted and deduplicated — no per-batch
- * Feistel evaluation inside the step. */
-GNS_API int gns_batch_slice_sorted(const int32_t* epoch_perm, int64_t n_train, const gns_step_t* step_dev,
-                                   int64_t max_count, int32_t* out_sorted, int32_t* out_n_dev, void* stream);
+ * Feistel evaluation inside the step.  step_src may be pinned (mapped) host
+ * memory written between graph replays; when step_dev_out is non-NULL the
+ * kernel reads step_src once, uncached, and stores it there for the step's
+ * later kernels (no separate host->device copy). */
+GNS_API int gns_batch_slice_sorted(const int32_t* epoch_perm, int64_t n_train, const gns_step_t* step_src,
+                                   gns_step_t* step_dev_out, int64_t max_count, int32_t* out_sorted,
+                                   int32_t* out_n_dev, void* stream);
 
 /* ---- model side (model.py) --------------------------------------------- */
 

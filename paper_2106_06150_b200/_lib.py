@@ -108,7 +108,8 @@ _SIGS = {
     "gns_epoch_targets_dev": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                                         c_void_p]),
     "gns_batch_targets_sorted": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
-    "gns_batch_slice_sorted": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "gns_batch_slice_sorted": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                                         c_void_p]),
     "gns_gather_rows": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_int64,
                                   c_int32, c_void_p, c_int64, c_int32, c_void_p]),
     "gns_gather_rows_mixed": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64,

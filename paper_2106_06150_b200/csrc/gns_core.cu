@@ -156,10 +156,23 @@ constexpr int kTargetsBlock = 1024;
 template <bool PERM>
 __global__ void __launch_bounds__(kTargetsBlock) batch_targets_sorted_kernel(
     const int32_t* __restrict__ train_ids, int64_t n_train, int h, const gns_step_t* __restrict__ step,
-    int64_t max_count, int32_t* __restrict__ out, int32_t* __restrict__ out_n) {
+    int64_t max_count, int32_t* __restrict__ out, int32_t* __restrict__ out_n, gns_step_t* __restrict__ step_out) {
   __shared__ int32_t sk[kTargetsBlock];
   __shared__ int s_warp[kTargetsBlock / 32];
+  __shared__ gns_step_t s_step;
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  if (step_out != nullptr) {
+    // step may live in pinned host memory written between graph replays:
+    // fetch it once, uncached, and publish the device copy for the rest of
+    // the step (replaces a host->device memcpy node)
+    if (i < 4) {
+      const unsigned long long w = *(reinterpret_cast<const volatile unsigned long long*>(step) + i);
+      reinterpret_cast<unsigned long long*>(&s_step)[i] = w;
+      reinterpret_cast<unsigned long long*>(step_out)[i] = w;
+    }
+    __syncthreads();
+    step = &s_step;
+  }
   const int64_t begin = step->begin;
   int64_t count = step->count;
   if (count > n_train - begin) count = n_train - begin;
@@ -382,18 +395,19 @@ int gns_batch_targets_sorted(const int32_t* train_ids, int64_t n_train, const gn
   while ((1ll << bits) < n_train) ++bits;
   bits += bits & 1;
   batch_targets_sorted_kernel<false><<<1, kTargetsBlock, 0, (cudaStream_t)stream>>>(
-      train_ids, n_train, bits / 2, step_dev, max_count, out_sorted, out_n_dev);
+      train_ids, n_train, bits / 2, step_dev, max_count, out_sorted, out_n_dev, nullptr);
   return check_launch("batch_targets_sorted");
 }
 
-int gns_batch_slice_sorted(const int32_t* epoch_perm, int64_t n_train, const gns_step_t* step_dev, int64_t max_count,
-                           int32_t* out_sorted, int32_t* out_n_dev, void* stream) {
+int gns_batch_slice_sorted(const int32_t* epoch_perm, int64_t n_train, const gns_step_t* step_src,
+                           gns_step_t* step_dev_out, int64_t max_count, int32_t* out_sorted, int32_t* out_n_dev,
+                           void* stream) {
   if (max_count > kTargetsBlock) {
     set_error("batch_slice_sorted: batch of %lld exceeds %d", (long long)max_count, kTargetsBlock);
     return GNS_EINVAL;
   }
   batch_targets_sorted_kernel<true><<<1, kTargetsBlock, 0, (cudaStream_t)stream>>>(
-      epoch_perm, n_train, 0, step_dev, max_count, out_sorted, out_n_dev);
+      epoch_perm, n_train, 0, step_src, max_count, out_sorted, out_n_dev, step_dev_out);
   return check_launch("batch_slice_sorted");
 }
 

@@ -310,7 +310,11 @@ class GraphedTrainer:
 
     def _sample_body(self, slot: int):
         sl = self.slots[slot]
-        self.step_dev[slot].copy_(self.step_host[slot], non_blocking=True)
+        # with the epoch permutation the first sampler kernel fetches the
+        # step struct from pinned host memory itself
+        fetch = self.epoch_perm is not None and not self.host_targets
+        if not fetch:
+            self.step_dev[slot].copy_(self.step_host[slot], non_blocking=True)
         if self.host_targets:
             B = self.cfg.batch_size
             sl.targets[:B].copy_(self.tgt_host[slot], non_blocking=True)
@@ -336,7 +340,8 @@ class GraphedTrainer:
             joins.append(done)
         sl.enqueue_device(None if self.host_targets else self.train_ids, self.step_dev[slot],
                           self.cache if self.cfg.strategy == "GNS" else None, exact_tables=self._tables,
-                          after_layer=transpose, epoch_perm=None if self.host_targets else self.epoch_perm)
+                          after_layer=transpose, epoch_perm=self.epoch_perm if fetch else None,
+                          step_src=self.step_host[slot] if fetch else None)
         for ev in joins:
             cur.wait_event(ev)
 

@@ -269,7 +269,8 @@ class MiniBatchSampler:
         return ev
 
     def enqueue_device(self, train_ids: torch.Tensor | None, step_dev: torch.Tensor, cache: CacheState | None,
-                       stream=None, exact_tables=None, after_layer=None, epoch_perm: torch.Tensor | None = None):
+                       stream=None, exact_tables=None, after_layer=None, epoch_perm: torch.Tensor | None = None,
+                       step_src: torch.Tensor | None = None):
         """Graph-capturable chain: the batch's targets (pool.py:60-66 slice
         begin/count) and Philox key come from the device gns_step_t
         ``step_dev``; no host synchronisation, fixed kernel arguments.  With
@@ -278,10 +279,17 @@ class MiniBatchSampler:
         s = _lib.stream_ptr(stream)
         if not hasattr(self, "n_targets_dev"):
             self.n_targets_dev = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if step_src is not None and (epoch_perm is None or self.max_targets > 1024):
+            with torch.cuda.stream(stream or torch.cuda.current_stream()):
+                step_dev.copy_(step_src, non_blocking=True)
+            step_src = None
         if epoch_perm is not None and self.max_targets <= 1024:
             # slice of the precomputed epoch permutation + np.unique, one CTA
-            _lib.call("gns_batch_slice_sorted", epoch_perm.data_ptr(), epoch_perm.numel(), step_dev.data_ptr(),
-                      self.max_targets, self.seeds0.data_ptr(), self.n_seeds0.data_ptr(), s)
+            # step_src (pinned host) -> step_dev inside the kernel when given
+            src = step_src if step_src is not None else step_dev
+            _lib.call("gns_batch_slice_sorted", epoch_perm.data_ptr(), epoch_perm.numel(), src.data_ptr(),
+                      step_dev.data_ptr() if step_src is not None else None, self.max_targets,
+                      self.seeds0.data_ptr(), self.n_seeds0.data_ptr(), s)
         elif train_ids is not None and self.max_targets <= 1024:
             # epoch slice + np.unique in one single-CTA kernel
             _lib.call("gns_batch_targets_sorted", train_ids.data_ptr(), train_ids.numel(), step_dev.data_ptr(),

@@ -367,10 +367,17 @@ def test_batch_targets_sorted_matches_epoch_slice(P, batch):
         step = torch.tensor([(seed & 0xFFFFFFFF) | (epoch << 32), k, k * batch, batch], dtype=torch.int64,
                             device="cuda")
         out.fill_(-1)
-        _lib.call("gns_batch_slice_sorted", perm.data_ptr(), perm.numel(), step.data_ptr(), batch, out.data_ptr(),
-                  cnt.data_ptr(), _lib.stream_ptr())
+        _lib.call("gns_batch_slice_sorted", perm.data_ptr(), perm.numel(), step.data_ptr(), None, batch,
+                  out.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
         m = int(cnt)
         assert np.array_equal(out[:m].cpu().numpy(), np.unique(r)), k
+        # step struct fetched from pinned host memory and published on the device
+        hstep, dstep = step.cpu().pin_memory(), torch.zeros_like(step)
+        out.fill_(-1)
+        _lib.call("gns_batch_slice_sorted", perm.data_ptr(), perm.numel(), hstep.data_ptr(), dstep.data_ptr(),
+                  batch, out.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
+        assert torch.equal(dstep, step)
+        assert np.array_equal(out[:int(cnt)].cpu().numpy(), np.unique(r)), k
 
 
 def test_pool_deterministic_and_complete(P):
