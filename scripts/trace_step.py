@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="papers100m")
     ap.add_argument("--replays", type=int, default=5)
     ap.add_argument("--dump", action="store_true")
+    ap.add_argument("--sampler-only", action="store_true")
     args = ap.parse_args()
     import bench
     import paper_2106_06150_b200 as P
@@ -39,7 +40,15 @@ def main():
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        tr.run(args.replays, epoch=pos[0], first=pos[1])
+        if args.sampler_only:
+            # the sampling body alone, eagerly (per-kernel device durations
+            # without the training branch's contention)
+            with torch.cuda.stream(tr.main):
+                for i in range(args.replays):
+                    tr._set_step(1, pos[0], 10 + i)
+                    tr._sample_body(1)
+        else:
+            tr.run(args.replays, epoch=pos[0], first=pos[1])
         torch.cuda.synchronize()
     path = os.path.join(tempfile.mkdtemp(), "trace.json")
     prof.export_chrome_trace(path)

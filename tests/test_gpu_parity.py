@@ -194,13 +194,23 @@ def test_minibatch_bit_exact_vs_oracle_hubs(P, strategy, cache_only, frac):
         assert_mb_equal(mb, ref, f"{strategy}-{cache_only}-{index}")
 
 
+def _mid_hub_graph(n=5000, seed=17):
+    """_hub_graph plus 150 rows of degree ~130-1900 (long warp-tier rows)."""
+    rng = np.random.default_rng(seed)
+    base = _hub_graph(n, seed)
+    src = np.repeat(np.arange(8, 8 + 150), rng.integers(65, 950, 150))
+    e3 = np.stack([src, rng.integers(0, n, src.size)], 1)
+    rows = np.repeat(np.arange(n), np.diff(base.indptr))
+    return O.build_csr(np.concatenate([np.stack([rows, base.indices], 1), e3]), n)
+
+
 @pytest.mark.parametrize("tune", [{"thread_len": 16, "stream_len": 0}, {"thread_len": 16, "stream_len": 32},
                                   {"thread_len": 0, "stream_len": 64}, {"sampler_ctas": 1}])
 def test_minibatch_selection_tiers_all_exact(P, tune):
     """Every routing of (row, phase) items over the selection tiers (sorting
     network, streaming top-k, warp, CTA) gives the reference's blocks."""
     from paper_2106_06150_b200 import _lib
-    og = _hub_graph(5000, 17)
+    og = _mid_hub_graph(5000, 17)
     g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
     cfg = P.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=400, input_layer_cache_only=False,
                           cache_mode="degree", cache_frac=0.05, seed=3)
