@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="papers100m")
     ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--trace", default=None, help="CUPTI per-kernel durations of one variant (e.g. train_only)")
     args = ap.parse_args()
     import bench
     import paper_2106_06150_b200 as P
@@ -58,6 +59,29 @@ def main():
         tr._replay(0)
 
     variants["production, sampling an empty batch"] = production_empty
+    if args.trace:
+        import collections
+        from torch.profiler import ProfilerActivity, profile
+        replay = variants[args.trace]
+        for _ in range(3):
+            replay()
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            with torch.cuda.stream(tr.main):
+                for _ in range(10):
+                    replay()
+            torch.cuda.synchronize()
+        tot = collections.defaultdict(float)
+        cnt = collections.Counter()
+        for e in prof.events():
+            if e.device_type == torch.autograd.DeviceType.CUDA:
+                k = e.name.split("(")[0].replace("void ", "")[:70]
+                tot[k] += e.device_time / 10
+                cnt[k] += 1
+        print(f"--- {args.trace}: per-kernel device time per replay (sum {sum(tot.values()):.1f} us)")
+        for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+            print(f"  {v:7.1f} us  x{cnt[k] / 10:4.1f}  {k}")
+        return
     for name, replay in variants.items():
         if name.startswith("production, sampling an empty"):
             torch.cuda.synchronize()

@@ -108,6 +108,21 @@ def main():
     print("idle gaps (> 1 us) per step, by the kernel that ends the gap:")
     for nm, d in gaps.most_common(15):
         print(f"  {d:6.1f} us before {nm}")
+    # per replay (split at the first sampler kernel of each replay): when the
+    # training kernels and the sampling kernels end, relative to replay start
+    samp = ("sample_", "layer_count", "enumerate_", "relabel", "batch_targets", "batch_slice", "tsort", "tscan",
+            "tscatter", "tcount", "unique_small")
+    starts = [i for i, e in enumerate(ev) if "batch_targets" in e["name"] or "batch_slice" in e["name"]]
+    rows = []
+    for a, b in zip(starts, starts[1:] + [len(ev)]):
+        seg = ev[a:b]
+        t0_ = min(e["ts"] for e in seg)
+        tr_end = max((e["ts"] + e["dur"] for e in seg if not any(k in e["name"] for k in samp)), default=t0_)
+        sa_end = max((e["ts"] + e["dur"] for e in seg if any(k in e["name"] for k in samp)), default=t0_)
+        rows.append((tr_end - t0_, sa_end - t0_))
+    if rows:
+        print("per replay (us from its first kernel): train ends / sampler ends: " +
+              ", ".join(f"{x:.0f}/{y:.0f}" for x, y in rows))
     mi = [(e["ts"], e["ts"] + e["dur"]) for e in ev if e["args"].get("stream") == main_stream]
     si = [(e["ts"], e["ts"] + e["dur"]) for e in ev if e["args"].get("stream") != main_stream]
     um, us_, ua = union(mi), union(si), union(mi + si)
