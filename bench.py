@@ -393,8 +393,9 @@ def main():
         wall = gdist.max_over_ranks(time.perf_counter() - w0, device="cuda")
         e2e = {"value": k2 * world / wall, "unit": UNIT, "h2d_bytes_per_step": BATCH * 4 + 4 + 32,
                "d2h_bytes_per_step": 8, "steps": k2,
-               "path": "GraphedTrainer(host_targets=True).run_host: pinned host targets -> graph memcpy node, "
-                       "every step's loss -> host after each replay; wall clock, max over ranks",
+               "path": "GraphedTrainer(host_targets=True).run_host: pinned host targets read by a copy kernel in "
+                       "the step graph, every step's loss written to pinned host memory by the graph and read "
+                       "by the host one replay late; wall clock, max over ranks",
                "device_ms_per_step": s0.elapsed_time(s1) / k2}
         del te
 

@@ -131,6 +131,12 @@ GNS_API int gns_version(void);
  * be timed / waited on) at every replay.  Used for in-graph kernel timing. */
 GNS_API int gns_record_event_external(void* event, void* stream);
 
+/* Kernel copy of `bytes` between device-addressable buffers, either of which
+ * may be mapped pinned host memory (UVA): used inside captured step graphs
+ * for the per-step host inputs / outputs instead of memcpy nodes.  Source
+ * loads are volatile (fresh on every replay).  4-byte aligned pointers. */
+GNS_API int gns_copy_mapped(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* CUDA-graph plumbing for the whole-step engine (engine.py).  `graph` is a
  * captured cudaGraph_t (torch.cuda.CUDAGraph(keep_graph=True).raw_cuda_graph()).
  * gns_graph_instantiate instantiates it, optionally honouring the per-kernel

@@ -219,6 +219,20 @@ __global__ void __launch_bounds__(kTargetsBlock) batch_targets_sorted_kernel(
   if (i == 0) out_n[0] = total;
 }
 
+// byte copy between two device-addressable buffers, one of which may be
+// mapped pinned host memory written / read by the host between graph
+// replays (volatile loads: fetched fresh every launch)
+__global__ void __launch_bounds__(256) copy_mapped_kernel(unsigned char* __restrict__ dst,
+                                                          const unsigned char* __restrict__ src, int64_t bytes) {
+  const int64_t words = bytes >> 2;
+  const volatile uint32_t* s4 = reinterpret_cast<const volatile uint32_t*>(src);
+  uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+  for (int64_t i = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+    d4[i] = s4[i];
+  const int64_t tail = bytes & 3;
+  if (blockIdx.x == 0 && threadIdx.x < tail) dst[words * 4 + threadIdx.x] = ((const volatile unsigned char*)src)[words * 4 + threadIdx.x];
+}
+
 template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) bitmap_rank_kernel(ScanStatus st, const uint32_t* __restrict__ bits,
                                                             int64_t nwords, int32_t* __restrict__ rank) {
@@ -237,6 +251,18 @@ extern "C" {
 const char* gns_last_error(void) { return g_err; }
 
 int gns_version(void) { return 1; }
+
+int gns_copy_mapped(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes <= 0) return GNS_OK;
+  if ((uintptr_t)dst % 4 || (uintptr_t)src % 4) {
+    set_error("copy_mapped: pointers must be 4-byte aligned");
+    return GNS_EINVAL;
+  }
+  const long long words = (bytes + 3) / 4;
+  const int grid = (int)(words < 256 * 8 ? (words + 255) / 256 : 8);
+  copy_mapped_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((unsigned char*)dst, (const unsigned char*)src, bytes);
+  return check_launch("copy_mapped");
+}
 
 int gns_record_event_external(void* event, void* stream) {
   GNS_CUDA(cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream, cudaEventRecordExternal));

@@ -10,8 +10,8 @@ other slot.  Two graphs alternate the slot roles, so the host issues one
 graph launch per step.
 
 Per-batch values (Philox key, the batch's slice of the epoch permutation)
-live in a device ``gns_step_t`` refreshed from pinned host memory by a
-memcpy node inside the graph.  Dense tensors are allocated at the static
+live in a device ``gns_step_t`` that the step's first sampler kernel reads
+from pinned host memory (written by the host before the launch).  Dense tensors are allocated at the static
 capacity bounds; kernels zero-fill rows past the device counts, so GEMMs
 over padded rows contribute exact zeros, and the input layer's two
 capacity-sized GEMMs are SWITCH conditional nodes that run over
@@ -79,12 +79,15 @@ class GraphedTrainer:
         self.step_host = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(2 * S)]
         self.step_dev = [torch.zeros(4, dtype=torch.int64, device=self.dev) for _ in range(2 * S)]
         self.done = [None] * (2 * S)
-        # host-provided targets (the end-to-end API): pinned buffers copied by
-        # memcpy nodes inside the graph
+        # host-provided targets (the end-to-end API): pinned buffers read by a
+        # copy kernel inside the graph (gns_copy_mapped)
         self.host_targets = host_targets
         B = config.batch_size
         self.tgt_host = [torch.zeros(B, dtype=torch.int32).pin_memory() for _ in range(2 * S)]
         self.ntgt_host = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(2 * S)]
+        # per-step losses of the replays of graph p (host_targets: written by
+        # the graph itself, read by run_host after the replay's event)
+        self.loss_host = [torch.zeros(S, dtype=torch.float64).pin_memory() for _ in range(2)]
         # Adam's step count lives on the device (gns_adam_dev), per-step losses
         # are kept for the host to read after a replay
         self.adam_t = torch.zeros(1, dtype=torch.int64, device=self.dev)
@@ -316,12 +319,14 @@ class GraphedTrainer:
         # with the epoch permutation the first sampler kernel fetches the
         # step struct from pinned host memory itself
         fetch = self.epoch_perm is not None and not self.host_targets
+        s = _lib.stream_ptr()
         if not fetch:
-            self.step_dev[slot].copy_(self.step_host[slot], non_blocking=True)
+            _lib.call("gns_copy_mapped", self.step_dev[slot].data_ptr(), self.step_host[slot].data_ptr(), 32, s)
         if self.host_targets:
+            # the host's target ids, read from pinned memory by a kernel
             B = self.cfg.batch_size
-            sl.targets[:B].copy_(self.tgt_host[slot], non_blocking=True)
-            sl.n_targets_dev.copy_(self.ntgt_host[slot], non_blocking=True)
+            _lib.call("gns_copy_mapped", sl.n_targets_dev.data_ptr(), self.ntgt_host[slot].data_ptr(), 4, s)
+            _lib.call("gns_copy_mapped", sl.targets.data_ptr(), self.tgt_host[slot].data_ptr(), 4 * B, s)
         # the backward's block transposes depend only on a finished layer:
         # each is forked onto the slot's aux stream as soon as its layer is
         # sampled and overlaps the sampling of the next (larger) layer
@@ -466,7 +471,12 @@ class GraphedTrainer:
                 if j > 0:
                     self._gather(sl)
                 self._train_rest(sl, with_adam=True)
-                self.step_loss[j:j + 1].copy_(self.model.loss_dev)
+                # kernel copies (no copy-engine memcpy nodes on the critical path)
+                _lib.call("gns_copy_mapped", self.step_loss[j:j + 1].data_ptr(), self.model.loss_dev.data_ptr(),
+                          8, _lib.stream_ptr())
+            if self.host_targets:   # every step's loss straight into pinned host memory
+                _lib.call("gns_copy_mapped", self.loss_host[p].data_ptr(), self.step_loss.data_ptr(), 8 * r,
+                          _lib.stream_ptr())
             self._prof_events = ev_prof
             for ev in joins:
                 self.main.wait_event(ev)
@@ -602,8 +612,10 @@ class GraphedTrainer:
 
     def run_host(self, batches, epoch: int = 0, on_loss=None):
         """End-to-end API with host buffers: ``batches`` are host int arrays of
-        target ids; every step copies them from pinned memory (memcpy nodes in
-        the graph) and every step's loss is read back to the host.  Requires
+        target ids; every step reads them from pinned memory (a copy kernel in
+        the graph) and writes every step's loss into pinned memory (another
+        copy kernel at the end of the replay), read by the host one replay
+        late.  Requires
         ``host_targets=True``."""
         if not self.host_targets:
             raise ValueError("construct with host_targets=True")
@@ -614,7 +626,7 @@ class GraphedTrainer:
         losses = []
         # double-buffered loss read-back: replay g+1 is queued before the host
         # waits for replay g's losses, so the GPU never idles on the host
-        lh = [torch.zeros(S, dtype=torch.float64).pin_memory() for _ in range(2)]
+        lh = self.loss_host   # written by graph p at the end of its replay
         pending = []
 
         def drain():
@@ -649,7 +661,6 @@ class GraphedTrainer:
                 put(sl, b0 + S + j)
             with torch.cuda.stream(self.main):
                 self._replay(p, r)
-                lh[p].copy_(self.step_loss, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self.main)
                 for sl in self._group(1 - p):
