@@ -181,9 +181,12 @@ def full_size_parity(P, g, cfg, cache, og, oc, n_batches=1):
 def gather_microbench(tr, D, reps=24):
     """features[input_nodes] (model.py:146) through gns_gather_rows on the
     input nodes of the batches currently held in the engine's sampler slots;
-    a 256 MB write between launches flushes L2.  Returns [(bytes, ms)]."""
+    a 256 MB copy between launches flushes L2.  Returns [(bytes, ms)]."""
     from paper_2106_06150_b200 import _lib
     L = len(FANOUTS)
+    # the engine's last replay may still be sampling into a slot on its side
+    # stream: settle every stream before reading the slots' device counts
+    torch.cuda.synchronize()
     sets = []
     for sl in tr.slots:
         b0 = sl.layers[L - 1]
@@ -192,12 +195,15 @@ def gather_microbench(tr, D, reps=24):
             sets.append((b0.src_nodes, b0.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1], n))
     tab = tr.g.features
     out = torch.empty((max(n for _, _, n in sets), D), dtype=torch.float32, device=tab.device)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=tab.device)
+    # L2 flush: copy 256 MB of random bytes (a constant memset can be
+    # absorbed without displacing L2 lines; a real read+write stream cannot)
+    flush = torch.randint(0, 256, (256 << 20,), dtype=torch.uint8, device=tab.device)
+    scratch = torch.empty_like(flush)
     s = torch.cuda.current_stream()
     res = []
     for it in range(reps + 2):
         ids, n_dev, n = sets[it % len(sets)]
-        flush.fill_(it & 0xFF)
+        scratch.copy_(flush)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, ids.data_ptr(), n_dev.data_ptr(), out.shape[0],

@@ -346,6 +346,25 @@ def test_epoch_targets_feistel(P):
     assert np.array_equal(np.sort(allv), np.flatnonzero(mask))
 
 
+@pytest.mark.parametrize("nbytes", [4, 32, 4000, 4 * 1000 + 3, 1 << 20])
+def test_copy_mapped_host_device(P, nbytes):
+    """gns_copy_mapped moves bytes pinned host -> device and device -> pinned
+    host (UVA), including a ragged tail and multi-CTA sizes, and re-reads
+    the host source on every launch (the step graph's per-replay inputs)."""
+    from paper_2106_06150_b200 import _lib
+    src = torch.randint(0, 256, (nbytes,), dtype=torch.uint8).pin_memory()
+    dev = torch.zeros(nbytes + 4, dtype=torch.uint8, device="cuda")
+    _lib.call("gns_copy_mapped", dev.data_ptr(), src.data_ptr(), nbytes, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(dev[:nbytes].cpu(), src) and int(dev[nbytes:].sum()) == 0
+    src.fill_(7)   # host rewrites between launches
+    _lib.call("gns_copy_mapped", dev.data_ptr(), src.data_ptr(), nbytes, _lib.stream_ptr())
+    back = torch.zeros(nbytes, dtype=torch.uint8).pin_memory()
+    _lib.call("gns_copy_mapped", back.data_ptr(), dev.data_ptr(), nbytes, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert bool((back == 7).all())
+
+
 @pytest.mark.parametrize("batch", [97, 1000, 1024])
 def test_batch_targets_sorted_matches_epoch_slice(P, batch):
     """gns_batch_targets_sorted (Feistel epoch slice + np.unique in one CTA)
