@@ -594,9 +594,108 @@ __global__ void __launch_bounds__(kSpmmBlock, 3) spmm_fwd_wide_kernel(const floa
   }
 }
 
+// Column-split hidden-layer forward: warp task = (row, 128-float column
+// chunk), so a row's chunks run on different warps (twice the independent
+// chains of spmm_fwd_wide_kernel at D = 256, one float4 per lane per
+// neighbour row, G rows in flight).  Each warp ranks the row's edges itself;
+// per-element FMA order is unchanged (bit-identical).
+template <int G, bool MASK>
+__global__ void __launch_bounds__(kSpmmBlock, 4) spmm_fwd_wide_split_kernel(const float* __restrict__ h,
+                                                                             int64_t ld_h, int dim, BlockView bv,
+                                                                             float* __restrict__ cat, int64_t ld_cat,
+                                                                             int64_t pad_rows,
+                                                                             uint32_t* __restrict__ relu_bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = bv.counts[GNS_CNT_DST];
+  const int64_t tm = (int64_t)(bv.row_scan[n] >> 32);
+  const int dv = dim >> 2;
+  const int nch = (dv + 31) >> 5;
+  const int mw = nch * 4;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t task = gw; task < n * nch; task += nw) {
+    const int64_t r = task / nch;
+    const int j = (int)(task - r * nch);
+    const int c = lane + 32 * j;
+    const bool on = c < dv;
+    const uint64_t s0 = bv.row_scan[r], s1 = bv.row_scan[r + 1];
+    const int64_t self = (int64_t)bv.self_pos[r];
+    const float norm = (float)max(bv.dst_degree[r], 1);
+    const int64_t cb = (int64_t)(s0 >> 32), ce = (int64_t)(s1 >> 32);
+    const int64_t fb = tm + (int64_t)(s0 & 0xffffffffull), fe = tm + (int64_t)(s1 & 0xffffffffull);
+    const int nc = (int)(ce - cb), L = nc + (int)(fe - fb);
+    float4 xs = make_float4(0.f, 0.f, 0.f, 0.f), acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (on) xs = vrelu(reinterpret_cast<const float4*>(h + self * ld_h)[c]);
+    if constexpr (MASK) put_relu_bits(relu_bits + self * mw, j, xs, on);
+    for (int t0 = 0; t0 < L; t0 += 32) {
+      const int m = min(32, L - t0);
+      int32_t idx = INT32_MAX;
+      float w = 0.f;
+      if (L <= 32) {
+        if (lane < L) {
+          const int64_t e = lane < nc ? cb + lane : fb + (lane - nc);
+          idx = bv.edge_src[e];
+          w = (float)bv.edge_weight[e];
+        }
+        int rank = 0;
+        for (int q = 0; q < L; ++q) rank += __shfl_sync(GNS_FULL, idx, q) < idx;
+        int src = 0;
+        for (int u = 0; u < L; ++u) {
+          const unsigned mm = __ballot_sync(GNS_FULL, lane < L && rank == u);
+          if (lane == u) src = __ffs(mm) - 1;
+        }
+        idx = __shfl_sync(GNS_FULL, idx, src);
+        w = __shfl_sync(GNS_FULL, w, src);
+      } else {
+        for (int i = 0; i < L; ++i) {
+          const int64_t e = i < nc ? cb + i : fb + (i - nc);
+          const int32_t v = bv.edge_src[e];
+          int rk = 0;
+          for (int q = lane; q < L; q += 32) {
+            const int64_t eq = q < nc ? cb + q : fb + (q - nc);
+            rk += bv.edge_src[eq] < v;
+          }
+          rk = warp_sum((unsigned)rk);
+          if (lane < m && rk == t0 + lane) {
+            idx = v;
+            w = (float)bv.edge_weight[e];
+          }
+        }
+      }
+      for (int t = 0; t < m; t += G) {
+        float4 x[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const int32_t iu = __shfl_sync(GNS_FULL, idx, (t + u) & 31);
+          x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (t + u < m && on) x[u] = vrelu(reinterpret_cast<const float4*>(h + (int64_t)iu * ld_h)[c]);
+        }
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const float wu = __shfl_sync(GNS_FULL, w, (t + u) & 31);
+          const int32_t iu = __shfl_sync(GNS_FULL, idx, (t + u) & 31);
+          if (t + u < m) {
+            if (on) vfma<true>(acc, wu, x[u]);
+            if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)iu * mw, j, x[u], on);
+          }
+        }
+      }
+    }
+    if (on) {
+      float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
+      crow[c] = xs;
+      crow[dv + c] = vdiv(acc, norm);
+    }
+  }
+  for (int64_t r = n + gw; r < pad_rows; r += nw) {
+    float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
+    for (int cc = lane; cc < 2 * dv; cc += 32) crow[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // experiment knobs (gns_tune)
 static int g_tune_narrow = 1;  // narrow-row forward SpMM variant (0 = generic)
-static int g_tune_wide = 1;    // hidden-layer forward: 1 = spmm_fwd_wide_kernel, 0 = generic
+static int g_tune_wide = 2;    // hidden-layer forward: 2 = column-split, 1 = spmm_fwd_wide_kernel, 0 = generic
 
 // Forward SpMM grids: one wave of persistent CTAs (grid-stride rows).  Short
 // CTAs (k rows per warp, many waves) were measured slower both alone and
@@ -1180,6 +1279,12 @@ int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
   BlockView bv = view_of(block);
   const int dv = dim / 4;
+  if (g_tune_wide == 2 && dv > 32 && dv <= 128) {
+    const long long tasks = rows * ((dv + 31) / 32);
+    spmm_fwd_wide_split_kernel<4, true><<<spmm_grid(spmm_fwd_wide_split_kernel<4, true>, tasks), kSpmmBlock, 0,
+                                           stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows, relu_bits);
+    return check_launch("spmm_fwd_bits");
+  }
   if (g_tune_wide && dv > 32 && dv <= 64) {
     spmm_fwd_wide_kernel<2, 4, true><<<spmm_grid(spmm_fwd_wide_kernel<2, 4, true>, rows), kSpmmBlock, 0,
                                        stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows,

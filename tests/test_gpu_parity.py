@@ -547,17 +547,18 @@ def test_spmm_fwd_wide_equals_generic(P, dim):
             ns, nd = bg.src_nodes.numel(), bg.dst_nodes.numel()
             h = torch.randn(ns, dim, device="cuda")
             res = []
-            for v in (0, 1):
+            for v in (0, 1, 2):
                 _lib.call("gns_tune", b"spmm_wide", v)
                 o = torch.full((nd + 3, 2 * dim), 5.0, device="cuda")
                 bits = torch.zeros(lib.gns_relu_bits_size(ns, dim) // 4, dtype=torch.int32, device="cuda")
                 _lib.call("gns_spmm_fwd_bits", h.data_ptr(), dim, dim, bg._c, nd, nd + 3, o.data_ptr(), 2 * dim,
                           bits.data_ptr(), _lib.stream_ptr())
                 res.append((o, bits))
-            assert torch.equal(res[0][0], res[1][0])
-            assert torch.equal(res[0][1], res[1][1])
+            for v in range(1, len(res)):
+                assert torch.equal(res[0][0], res[v][0]), v
+                assert torch.equal(res[0][1], res[v][1]), v
     finally:
-        _lib.call("gns_tune", b"spmm_wide", 1)
+        _lib.call("gns_tune", b"spmm_wide", 2)
 
 
 @pytest.mark.parametrize("dim", [16, 64, 128])
