@@ -308,7 +308,9 @@ GNS_API int gns_batch_slice_sorted(const int32_t* epoch_perm, int64_t n_train, c
 
 /* features[input_nodes] (model.py:146): out[i,:] = table[rows[i],:], D
  * columns.  dtype_in/out: 0 = float32, 1 = float64 (float32 -> float64 for
- * the reference-parity mode).  ld_* are row strides in elements. */
+ * the reference-parity mode).  ld_* are row strides in elements.  float32
+ * rows of D <= 64 go through the TMA (tile::gather4 loads + bulk stores);
+ * wider rows through the register-staged kernel (gns_tune "gather_tma"). */
 GNS_API int gns_gather_rows(const void* table, int64_t ld_in, int32_t dtype_in,
                     const int32_t* rows, const int32_t* n_rows_dev, int64_t max_rows,
                     int32_t dim, void* out, int64_t ld_out, int32_t dtype_out,

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 
+#include <cuda.h>   // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
+
 #include "gns_common.cuh"
 
 namespace gns {
@@ -1133,6 +1135,198 @@ using namespace gns;
 
 extern "C" {
 
+// ---- TMA gather (features[input_nodes], float32, D <= 256) --------------------
+// The Tensor Memory Accelerator fetches rows by index: one elected thread per
+// warp issues cp.async.bulk.tensor.2d ... tile::gather4 (4 table rows of D
+// floats into shared memory, completion on the slot's mbarrier), then a bulk
+// shared->global store of the 4 rows to their contiguous place in `out`.
+// kTmaSlots groups per warp are in flight; no feature bytes pass through
+// registers.
+constexpr int kTmaWarps = 8;
+constexpr int kTmaSlots = 6;
+constexpr int kTmaLag = 3;   // gathers in flight per warp; the other slots drain their stores
+constexpr int kTmaBarBytes = 512;   // kTmaWarps * kTmaSlots mbarriers, padded
+
+__device__ __forceinline__ uint32_t tma_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(kTmaWarps * 32) gather_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                    const int32_t* __restrict__ rows,
+                                                                    const int32_t* __restrict__ n_rows_dev,
+                                                                    int64_t max_rows, int dim, float* __restrict__ out,
+                                                                    int64_t ld_out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t row_bytes = (uint32_t)dim * 4u;
+  // slots are 128-byte aligned (TMA shared-memory destinations)
+  const uint32_t slot_bytes = (4u * row_bytes + 127u) & ~127u;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + wib * kTmaSlots;
+  unsigned char* slots = smem + kTmaBarBytes + (size_t)wib * kTmaSlots * slot_bytes;
+  int64_t n = n_rows_dev ? (int64_t)n_rows_dev[0] : max_rows;
+  if (n > max_rows) n = max_rows;
+  const int64_t ngroups = (n + 3) >> 2;
+  const int64_t gw = (int64_t)blockIdx.x * kTmaWarps + wib, nw = (int64_t)gridDim.x * kTmaWarps;
+  const bool leader = lane == 0;   // one thread per warp drives the TMA unit
+  if (leader) {
+    for (int i = 0; i < kTmaSlots; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tma_smem_u32(&bars[i])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto store_group = [&](int64_t g, int slot, uint32_t parity) {
+    // wait for the gather, then write the group's valid rows
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "DONE:\n\t}" ::"r"(tma_smem_u32(&bars[slot])),
+        "r"(parity)
+        : "memory");
+    const int valid = (int)(n - 4 * g < 4 ? n - 4 * g : 4);
+    unsigned char* src = slots + (size_t)slot * slot_bytes;
+    if (ld_out == dim) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + 4 * g * ld_out),
+                   "r"(tma_smem_u32(src)), "r"(row_bytes * (uint32_t)valid)
+                   : "memory");
+    } else {
+      for (int i = 0; i < valid; ++i)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + (4 * g + i) * ld_out),
+                     "r"(tma_smem_u32(src + i * row_bytes)), "r"(row_bytes)
+                     : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  };
+  // group k of this warp (global group gw + k*nw) lives in slot k % kTmaSlots;
+  // at step k group k-lag is stored and the gather of group k is issued once
+  // the store of group k-S (same slot, issued S-lag steps earlier) has
+  // finished reading shared memory.  The warp's lanes load the row ids of
+  // 32 groups at a time (one int4 each); the leader takes them by shuffle.
+  const int64_t my_groups = gw < ngroups ? (ngroups - gw + nw - 1) / nw : 0;
+  for (int64_t k0 = 0; k0 < my_groups; k0 += 32) {
+    int4 ids = make_int4(0, 0, 0, 0);
+    {
+      const int64_t k = k0 + lane;
+      if (k < my_groups) {
+        const int64_t b = 4 * (gw + k * nw);
+        if (b + 3 < n) {
+          ids = *reinterpret_cast<const int4*>(rows + b);
+        } else {
+          ids.x = rows[b];
+          ids.y = b + 1 < n ? rows[b + 1] : ids.x;
+          ids.z = b + 2 < n ? rows[b + 2] : ids.x;
+          ids.w = ids.x;
+        }
+      }
+    }
+    const int cnt = (int)(my_groups - k0 < 32 ? my_groups - k0 : 32);
+    for (int u = 0; u < cnt; ++u) {
+      const int r0 = __shfl_sync(GNS_FULL, ids.x, u), r1 = __shfl_sync(GNS_FULL, ids.y, u);
+      const int r2 = __shfl_sync(GNS_FULL, ids.z, u), r3 = __shfl_sync(GNS_FULL, ids.w, u);
+      if (leader) {
+        const int64_t k = k0 + u;
+        const int slot = (int)(k % kTmaSlots);
+        if (k >= kTmaLag) {
+          const int64_t q = k - kTmaLag;
+          store_group(gw + q * nw, (int)(q % kTmaSlots), (uint32_t)((q / kTmaSlots) & 1));
+        }
+        // the store of group k-S (this slot's previous group) has read its
+        // shared memory; the S-lag stores issued after it may still pend
+        if (k >= kTmaSlots) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaSlots - kTmaLag) : "memory");
+        const uint32_t bar = tma_smem_u32(&bars[slot]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(4u * row_bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(tma_smem_u32(slots + (size_t)slot * slot_bytes)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(bar), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+            : "memory");
+      }
+    }
+  }
+  if (leader) {
+    // drain: the groups not stored yet
+    const int64_t first = my_groups > kTmaLag ? my_groups - kTmaLag : 0;
+    for (int64_t k = first; k < my_groups; ++k)
+      store_group(gw + k * nw, (int)(k % kTmaSlots), (uint32_t)((k / kTmaSlots) & 1));
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
+// (gns_tune "gather_tma") TMA gather4 path for float32 rows: 1 = for D <= 64
+// (cfg1, D = 64: 0.33 vs 0.28 of HBM peak), 2 = for D <= 256 (papers100M,
+// D = 128: 0.81 vs 0.84 for the register kernel, so not the default), 0 = off
+static int g_gather_tma = 1;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  });
+  return fn;
+}
+
+// 2-D float32 map over the table (rows x dim, row pitch ld floats), box = one
+// full row: what tile::gather4 fetches per row index
+static bool table_map(CUtensorMap* m, const float* table, int64_t ld, int dim) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)0x7fffffff};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)dim, 1};
+  const cuuint32_t estride[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)table, gdim, gstride, box, estride,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool gather_tma(const float* table, int64_t ld_in, const int32_t* rows, const int32_t* n_rows_dev,
+                       int64_t max_rows, int dim, float* out, int64_t ld_out, cudaStream_t stream, int* err) {
+  *err = GNS_OK;
+  if (!g_gather_tma || dim % 4 || dim > (g_gather_tma == 2 ? 256 : 64) || ld_in % 4 || ld_out % 4 ||
+      (uintptr_t)table % 16 ||
+      (uintptr_t)out % 16 || (uintptr_t)rows % 4)
+    return false;
+  CUtensorMap m;
+  if (!table_map(&m, table, ld_in, dim)) return false;
+  const size_t slot_bytes = ((size_t)16 * dim + 127) & ~(size_t)127;
+  const size_t smem = kTmaBarBytes + (size_t)kTmaWarps * kTmaSlots * slot_bytes;
+  const size_t smem_max = kTmaBarBytes + (size_t)kTmaWarps * kTmaSlots * 16 * 256;
+  static std::once_flag attr;
+  std::call_once(attr, [smem_max] {
+    cudaFuncSetAttribute(gather_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  });
+  const long long want = ((max_rows + 3) / 4 + kTmaWarps - 1) / kTmaWarps;
+  static std::mutex mu;
+  static std::unordered_map<int, int> per_sm_by_dim;
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_sm_by_dim.find(dim);
+    if (it != per_sm_by_dim.end()) {
+      per_sm = it->second;
+    } else {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_tma_kernel, kTmaWarps * 32, smem) !=
+          cudaSuccess)
+        per_sm = 1;
+      per_sm_by_dim[dim] = per_sm;
+    }
+  }
+  const int grid = grid_for(want, (long long)num_sms() * (per_sm > 0 ? per_sm : 1));
+  gather_tma_kernel<<<grid, kTmaWarps * 32, smem, stream>>>(m, rows, n_rows_dev, max_rows, dim, out, ld_out);
+  *err = check_launch("gather_tma");
+  return true;
+}
+
 int gns_gather_rows(const void* table, int64_t ld_in, int32_t dtype_in, const int32_t* rows,
                     const int32_t* n_rows_dev, int64_t max_rows, int32_t dim, void* out, int64_t ld_out,
                     int32_t dtype_out, void* stream_) {
@@ -1142,6 +1336,10 @@ int gns_gather_rows(const void* table, int64_t ld_in, int32_t dtype_in, const in
   if (dtype_in == 0 && dtype_out == 0) {
     bool vec = (dim % 4 == 0) && (ld_in % 4 == 0) && (ld_out % 4 == 0) && ((uintptr_t)table % 16 == 0) &&
                ((uintptr_t)out % 16 == 0);
+    int terr;
+    if (vec && gather_tma((const float*)table, ld_in, rows, n_rows_dev, max_rows, dim, (float*)out, ld_out, stream,
+                          &terr))
+      return terr;
     if (vec) {
       // 8 resident 256-thread CTAs per SM; G rows x C column blocks per warp
       const int dim4 = dim / 4;
@@ -1209,6 +1407,10 @@ int gns_cache_refresh_rows(const float* host_table, int64_t ld, const int32_t* i
 int gns_tune(const char* name, int32_t value) {
   if (!strcmp(name, "spmm_narrow")) {
     g_tune_narrow = value;
+    return GNS_OK;
+  }
+  if (!strcmp(name, "gather_tma") && value >= 0 && value <= 2) {
+    g_gather_tma = value;
     return GNS_OK;
   }
   if (!strcmp(name, "spmm_wide")) {

@@ -315,20 +315,34 @@ def test_unique_sorted_both_paths(P, n):
     assert int(ws[:nbytes].count_nonzero()) == 0
 
 
-@pytest.mark.parametrize("dim,rows", [(4, 1), (64, 33), (100, 1001), (128, 4099), (768, 517)])
-def test_gather_rows_shapes(P, dim, rows):
+@pytest.mark.parametrize("tma", [2, 0])
+@pytest.mark.parametrize("dim,rows", [(4, 1), (64, 33), (100, 1001), (128, 4099), (256, 4098), (768, 517)])
+def test_gather_rows_shapes(P, dim, rows, tma):
     """gns_gather_rows over tile tails and row widths (16-B chunks per row
-    from 1 to 192), device row count, output stride > dim."""
+    from 1 to 192), device row count, output stride > dim and == dim; tma=2
+    takes the TMA gather4 path for every float32 D <= 256, tma=0 the register
+    kernel."""
     from paper_2106_06150_b200 import _lib
     N = 5000
     tab = torch.randn(N, dim, device="cuda")
     idx = torch.sort(torch.randint(0, N, (rows,), device="cuda", dtype=torch.int32)).values
-    out = torch.full((rows + 3, dim + 4), 7.0, device="cuda")
     n_dev = torch.tensor([rows], dtype=torch.int32, device="cuda")
-    _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, idx.data_ptr(), n_dev.data_ptr(), rows + 3, dim,
-              out.data_ptr(), out.stride(0), 0, _lib.stream_ptr())
-    assert torch.equal(out[:rows, :dim], tab[idx.long()])
-    assert bool((out[rows:] == 7.0).all()) and bool((out[:, dim:] == 7.0).all())
+    try:
+        _lib.call("gns_tune", b"gather_tma", tma)
+        for pad in (4, 0):
+            out = torch.full((rows + 3, dim + pad), 7.0, device="cuda")
+            _lib.call("gns_gather_rows", tab.data_ptr(), tab.stride(0), 0, idx.data_ptr(), n_dev.data_ptr(),
+                      rows + 3, dim, out.data_ptr(), out.stride(0), 0, _lib.stream_ptr())
+            assert torch.equal(out[:rows, :dim], tab[idx.long()]), pad
+            assert bool((out[rows:] == 7.0).all()) and bool((out[:, dim:] == 7.0).all()), pad
+        # rows read from a strided table view (row pitch > dim)
+        wide = torch.randn(N, dim + 8, device="cuda")
+        out = torch.full((rows, dim), 7.0, device="cuda")
+        _lib.call("gns_gather_rows", wide.data_ptr(), wide.stride(0), 0, idx.data_ptr(), n_dev.data_ptr(), rows,
+                  dim, out.data_ptr(), out.stride(0), 0, _lib.stream_ptr())
+        assert torch.equal(out, wide[idx.long(), :dim])
+    finally:
+        _lib.call("gns_tune", b"gather_tma", 1)
 
 
 def test_epoch_targets_feistel(P):
