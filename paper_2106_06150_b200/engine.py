@@ -32,7 +32,7 @@ import torch
 from . import _lib
 from . import cache as cache_mod
 from .graph import Graph
-from .model import GraphSAGE, TrainConfig, _dt, _split_rows, _weight_grad
+from .model import GraphSAGE, TrainConfig, _split_rows, _weight_grad
 from .dist import rank_batches
 from .pool import cache_probs, exact_tables, num_batches
 from .sampling import MiniBatchSampler, SamplerConfig

@@ -20,7 +20,7 @@ host reads all counts once per batch (``DeviceMiniBatch.sync``).
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import torch
 
