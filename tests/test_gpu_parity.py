@@ -837,10 +837,11 @@ def test_device_generator_contract(P):
 
 # ---- CUDA-graph engine ---------------------------------------------------------------
 
-def test_graphed_trainer_matches_eager(P):
+@pytest.mark.parametrize("S", [1, 2])
+def test_graphed_trainer_matches_eager(P, S):
     """The captured whole-step engine (sample || train, static capacities,
-    device-side batch parameters) trains on exactly the pool's batches and
-    tracks the eager path's losses."""
+    device-side batch parameters; S steps per graph replay) trains on exactly
+    the pool's batches and tracks the eager path's losses."""
     og = _hub_graph(5000, 13)
     rng = np.random.default_rng(0)
     feats = rng.normal(size=(og.num_nodes, 16)).astype(np.float32)
@@ -856,7 +857,7 @@ def test_graphed_trainer_matches_eager(P):
     for it in pool.iter_epoch(0):
         ref_losses.append(float(eager.train_step(it.minibatch, g, tc)))
     from paper_2106_06150_b200.engine import GraphedTrainer
-    tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0)
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0, steps_per_graph=S)
     losses = []
     tr.run_epoch(0, on_step=lambda e, i, k: losses.append(tr.loss_value()))
     tr.check_errors()
@@ -910,7 +911,8 @@ def test_graphed_trainer_size_switched_dense_ops(P, chunk):
         np.testing.assert_allclose(a, b, rtol=1e-2, atol=1e-4)
 
 
-def test_graphed_trainer_run_host_matches_eager(P):
+@pytest.mark.parametrize("S", [1, 2])
+def test_graphed_trainer_run_host_matches_eager(P, S):
     """The end-to-end API (host target arrays copied into the step graph,
     every step's loss read back, one replay kept in flight) trains exactly
     the given batches: losses track the eager model on the same batches."""
@@ -924,7 +926,7 @@ def test_graphed_trainer_run_host_matches_eager(P):
     tc = P.TrainConfig(lr=0.003)
     batches = [rng.choice(og.num_nodes, 200, replace=False) for _ in range(7)]
     from paper_2106_06150_b200.engine import GraphedTrainer
-    tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0, host_targets=True)
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0, host_targets=True, steps_per_graph=S)
     got = tr.run_host(batches, epoch=0)
     eager = P.GraphSAGE((16, 32, 5), seed=0)
     ref = [float(eager.train_step(P.build_minibatch(g, tr.cache, b, cfg, P.BatchRng(4, 0, k)), g, tc))
