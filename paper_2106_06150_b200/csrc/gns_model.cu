@@ -998,25 +998,35 @@ __global__ void dense_bwd_partial_kernel(const T* __restrict__ dh, const T* __re
 // columns, warp w sums rows w, w+8, ... (coalesced 128-byte row reads), then
 // the 8 warp sums are added in warp order.  Launch with colsum_grid(ncols).
 constexpr int kColsumWarps = 8;
-template <typename T>
-__global__ void __launch_bounds__(kColsumWarps * 32) colsum_final_kernel(const T* __restrict__ partial, int nblocks,
-                                                                         int ncols, T* __restrict__ db) {
-  __shared__ T red[kColsumWarps][32];
+template <typename T, int W = kColsumWarps>
+__global__ void __launch_bounds__(W * 32) colsum_final_kernel(const T* __restrict__ partial, int nblocks, int ncols,
+                                                              T* __restrict__ db) {
+  __shared__ T red[W][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   T s = 0;
   if (c < ncols)
-    for (int b = w; b < nblocks; b += kColsumWarps) s += partial[(int64_t)b * ncols + c];
+    for (int b = w; b < nblocks; b += W) s += partial[(int64_t)b * ncols + c];
   red[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < ncols) {
     T t = red[0][lane];
 #pragma unroll
-    for (int i = 1; i < kColsumWarps; ++i) t += red[i][lane];
+    for (int i = 1; i < W; ++i) t += red[i][lane];
     db[c] = t;
   }
 }
 static inline unsigned colsum_grid(int ncols) { return (unsigned)((ncols + 31) / 32); }
+// Few columns over many partial rows (a bias gradient: <= 1024 columns,
+// hundreds of per-CTA partials) get 32 warps per column block, so each warp's
+// dependent add chain is 4x shorter; wide reductions keep 8 warps.
+template <typename T>
+static inline void colsum_launch(const T* part, int nrows, int ncols, T* out, cudaStream_t stream) {
+  if (ncols <= 1024 && nrows >= 128)
+    colsum_final_kernel<T, 32><<<colsum_grid(ncols), 32 * 32, 0, stream>>>(part, nrows, ncols, out);
+  else
+    colsum_final_kernel<T><<<colsum_grid(ncols), kColsumWarps * 32, 0, stream>>>(part, nrows, ncols, out);
+}
 
 struct BwdWs {
   void* colpart;
@@ -1426,8 +1436,7 @@ int gns_sum_rows(int32_t dtype, const void* part, int64_t nrows, int64_t ncols, 
   cudaStream_t stream = (cudaStream_t)stream_;
   if (ncols <= 0) return GNS_OK;
   if (dtype == 0)
-    colsum_final_kernel<float><<<colsum_grid((int)ncols), kColsumWarps * 32, 0, stream>>>(
-        (const float*)part, (int)nrows, (int)ncols, (float*)out);
+    colsum_launch<float>((const float*)part, (int)nrows, (int)ncols, (float*)out, stream);
   else
     colsum_final_kernel<double><<<colsum_grid((int)ncols), kColsumWarps * 32, 0, stream>>>(
         (const double*)part, (int)nrows, (int)ncols, (double*)out);
@@ -1547,7 +1556,7 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
   }
 #undef GNS_BWDB
   GNS_TRY(check_launch("spmm_bwd_bits"));
-  if (db) colsum_final_kernel<float><<<colsum_grid(dim), kColsumWarps * 32, 0, stream>>>((const float*)w.colpart, g2, dim, db);
+  if (db) colsum_launch<float>((const float*)w.colpart, g2, dim, db, stream);
   return check_launch("spmm_bwd_bits colsum");
 }
 
@@ -1674,7 +1683,7 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
   GNS_TRY(check_launch("spmm_bwd"));
   if (db) {
     if (dtype == 0)
-      colsum_final_kernel<float><<<colsum_grid(dim), kColsumWarps * 32, 0, stream>>>((const float*)w.colpart, g2, dim, (float*)db);
+      colsum_launch<float>((const float*)w.colpart, g2, dim, (float*)db, stream);
     else
       colsum_final_kernel<double><<<colsum_grid(dim), kColsumWarps * 32, 0, stream>>>((const double*)w.colpart, g2, dim,
                                                                      (double*)db);
@@ -1704,7 +1713,7 @@ int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int64_t ld,
   if (dtype == 0) {
     dense_bwd_partial_kernel<float><<<grid, 256, 0, stream>>>((const float*)dh, (const float*)z, ld, n_dev, n_rows,
                                                               ncols, (float*)dz, (float*)ws, rpb);
-    colsum_final_kernel<float><<<colsum_grid(ncols), kColsumWarps * 32, 0, stream>>>((const float*)ws, nblocks, ncols, (float*)db);
+    colsum_launch<float>((const float*)ws, nblocks, ncols, (float*)db, stream);
   } else {
     dense_bwd_partial_kernel<double><<<grid, 256, 0, stream>>>((const double*)dh, (const double*)z, ld, n_dev,
                                                                n_rows, ncols, (double*)dz, (double*)ws, rpb);
