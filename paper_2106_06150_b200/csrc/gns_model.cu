@@ -1691,15 +1691,19 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
   return check_launch("spmm_bwd colsum");
 }
 
+// rows per partial block: 64 for float32 (more CTAs, short per-thread add
+// chains), 512 for the float64 parity mode
+constexpr int kDenseRpbF32 = 64, kDenseRpbF64 = 512;
+
 size_t gns_dense_bwd_workspace_size(int64_t max_rows, int32_t ncols) {
-  return (size_t)((max_rows + 511) / 512 + 1) * (size_t)ncols * 8 + 256;
+  return (size_t)((max_rows + kDenseRpbF32 - 1) / kDenseRpbF32 + 1) * (size_t)ncols * 8 + 256;
 }
 
 int gns_dense_bwd_bias(int32_t dtype, const void* dh, const void* z, int64_t ld, const int32_t* n_dev,
                        int64_t n_rows, int32_t ncols, void* dz, void* db, void* ws, size_t ws_bytes,
                        void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
-  const int rpb = 512;
+  const int rpb = dtype == 0 ? kDenseRpbF32 : kDenseRpbF64;
   const int nblocks = (int)((n_rows + rpb - 1) / rpb);
   if (ws_bytes < gns_dense_bwd_workspace_size(n_rows, ncols)) {
     set_error("dense_bwd_bias: workspace too small");
