@@ -160,6 +160,15 @@ GNS_API int gns_graph_kernel_priorities(void* graph, int32_t* out_hist, int32_t 
  * rows the batch actually has. */
 GNS_API int gns_graph_switch_begin(void* stream, const int32_t* n_dev, int64_t chunk, int32_t nbodies,
                                    void** out_bodies);
+/* Several SWITCH nodes over the same device count with one selector kernel:
+ * gns_graph_switch_handles creates `count` (<= 4) conditional handles in the
+ * graph being captured on `stream` and appends ONE kernel setting handle i to
+ * min(ceil(n / chunk), nbodies[i] - 1); gns_graph_switch_node then appends
+ * the SWITCH node of a handle (no selector kernel of its own) wherever the
+ * capture has reached. */
+GNS_API int gns_graph_switch_handles(void* stream, const int32_t* n_dev, int64_t chunk, int32_t count,
+                                     const int32_t* nbodies, uint64_t* handles);
+GNS_API int gns_graph_switch_node(void* stream, uint64_t handle, int32_t nbodies, void** out_bodies);
 GNS_API int gns_graph_body_capture_begin(void* stream, void* body);
 GNS_API int gns_graph_body_capture_end(void* stream);
 

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, Structure, c_double, c_int32, c_int64, c_size_t, c_uint32, c_void_p
+from ctypes import POINTER, Structure, c_double, c_int32, c_int64, c_size_t, c_uint32, c_uint64, c_void_p
 
 import torch
 
@@ -76,6 +76,8 @@ _SIGS = {
     "gns_graph_exec_destroy": (c_int32, [c_void_p]),
     "gns_graph_kernel_priorities": (c_int32, [c_void_p, c_void_p, c_int32]),
     "gns_graph_switch_begin": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
+    "gns_graph_switch_handles": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    "gns_graph_switch_node": (c_int32, [c_void_p, c_uint64, c_int32, c_void_p]),
     "gns_graph_body_capture_begin": (c_int32, [c_void_p, c_void_p]),
     "gns_graph_body_capture_end": (c_int32, [c_void_p]),
     "gns_degree_probs": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p]),
@@ -215,7 +217,7 @@ KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_random_walk_probs": 9, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
     "gns_cached_csr_fill": 1, "gns_estimate_edge_inclusion": 0, "gns_sample_layer": 9, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_batch_targets_sorted": 1, "gns_batch_slice_sorted": 1, "gns_copy_mapped": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
-    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_sum_rows": 1, "gns_graph_switch_begin": 1, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2, "gns_spmm_fwd_bits": 1, "gns_spmm_bwd_transposed_bits": 2,
+    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_sum_rows": 1, "gns_graph_switch_begin": 1, "gns_graph_switch_handles": 1, "gns_graph_switch_node": 0, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2, "gns_spmm_fwd_bits": 1, "gns_spmm_bwd_transposed_bits": 2,
     "gns_adam_dev": 2,
     "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1, "gns_build_csr_count": 6, "gns_build_csr_fill": 1,
 }

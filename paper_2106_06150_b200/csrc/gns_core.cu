@@ -79,6 +79,19 @@ __global__ void switch_set_kernel(cudaGraphConditionalHandle h, const int32_t* _
   cudaGraphSetConditional(h, (unsigned)k);
 }
 
+struct SwitchSet {
+  cudaGraphConditionalHandle h[4];
+  int32_t nbodies[4];
+  int32_t count;
+};
+__global__ void switch_set_multi_kernel(const __grid_constant__ SwitchSet ss, const int32_t* __restrict__ n_dev,
+                                        int64_t chunk) {
+  const int64_t n = n_dev[0];
+  const int64_t k = (n + chunk - 1) / chunk;
+  for (int i = 0; i < ss.count; ++i)
+    cudaGraphSetConditional(ss.h[i], (unsigned)(k > ss.nbodies[i] - 1 ? ss.nbodies[i] - 1 : k));
+}
+
 // ---------------------------------------------------------------------------
 __global__ void degree_probs_kernel(const int64_t* __restrict__ indptr, int64_t n, double total,
                                     double* __restrict__ out) {
@@ -311,6 +324,62 @@ int gns_graph_switch_begin(void* stream_, const int32_t* n_dev, int64_t chunk, i
   cudaGraphNodeParams p = {};
   p.type = cudaGraphNodeTypeConditional;
   p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeSwitch;
+  p.conditional.size = (unsigned)nbodies;
+  cudaGraphNode_t node;
+  GNS_CUDA(cudaGraphAddNode(&node, graph, deps, ndeps, &p));
+  GNS_CUDA(cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies));
+  for (int i = 0; i < nbodies; ++i) out_bodies[i] = (void*)p.conditional.phGraph_out[i];
+  return GNS_OK;
+}
+
+int gns_graph_switch_handles(void* stream_, const int32_t* n_dev, int64_t chunk, int32_t count,
+                             const int32_t* nbodies, uint64_t* handles) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (chunk <= 0 || count < 1 || count > 4) {
+    set_error("graph_switch_handles: chunk must be positive and 1 <= count <= 4");
+    return GNS_EINVAL;
+  }
+  cudaStreamCaptureStatus st;
+  unsigned long long id = 0;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  GNS_CUDA(cudaStreamGetCaptureInfo(stream, &st, &id, &graph, &deps, &ndeps));
+  if (st != cudaStreamCaptureStatusActive) {
+    set_error("graph_switch_handles: the stream is not being captured");
+    return GNS_EINVAL;
+  }
+  SwitchSet ss = {};
+  ss.count = count;
+  for (int i = 0; i < count; ++i) {
+    if (nbodies[i] < 1) {
+      set_error("graph_switch_handles: nbodies must be positive");
+      return GNS_EINVAL;
+    }
+    GNS_CUDA(cudaGraphConditionalHandleCreate(&ss.h[i], graph, 0, cudaGraphCondAssignDefault));
+    ss.nbodies[i] = nbodies[i];
+    handles[i] = (uint64_t)ss.h[i];
+  }
+  switch_set_multi_kernel<<<1, 1, 0, stream>>>(ss, n_dev, chunk);
+  return check_launch("switch_set_multi");
+}
+
+int gns_graph_switch_node(void* stream_, uint64_t handle, int32_t nbodies, void** out_bodies) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  cudaStreamCaptureStatus st;
+  unsigned long long id = 0;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  GNS_CUDA(cudaStreamGetCaptureInfo(stream, &st, &id, &graph, &deps, &ndeps));
+  if (st != cudaStreamCaptureStatusActive) {
+    set_error("graph_switch_node: the stream is not being captured");
+    return GNS_EINVAL;
+  }
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = (cudaGraphConditionalHandle)handle;
   p.conditional.type = cudaGraphCondTypeSwitch;
   p.conditional.size = (unsigned)nbodies;
   cudaGraphNode_t node;

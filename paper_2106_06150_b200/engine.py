@@ -217,6 +217,11 @@ class GraphedTrainer:
         blocks = [sl.layers[L - 1 - li] for li in range(L)]
         h = self.h0
         with m._tf32():
+            # the input layer's two size-switched dense ops (forward GEMM,
+            # weight gradient) share one selector kernel
+            n0 = blocks[0].counts[_lib.CNT_DST:_lib.CNT_DST + 1]
+            hs = self._switch_handles(n0, [self.cap_dst[0], self.npad[0]]) if self.use_switch else None
+            h_fwd, h_wg = (hs if hs is not None else (None, None))
             for li in range(L):
                 d_in = self.dims[li]
                 ev = self._prof_events if li == 0 else None
@@ -239,9 +244,9 @@ class GraphedTrainer:
                 if ev is not None:
                     _lib.call("gns_record_event_external", ev[3].cuda_event, s)
                 if li == 0 and self.use_switch:
-                    self._switched(blocks[0].counts[_lib.CNT_DST:_lib.CNT_DST + 1], self.cap_dst[0],
+                    self._switched(n0, self.cap_dst[0],
                                    lambda R: torch.addmm(m.biases[0], self.cat[0][:R], m.weights[0],
-                                                         out=self.z[0][:R]))
+                                                         out=self.z[0][:R]), handle=h_fwd)
                 else:
                     torch.addmm(m.biases[li], self.cat[li][:self.cap_dst[li]], m.weights[li], out=self.z[li])
                 h = self.z[li]
@@ -257,9 +262,9 @@ class GraphedTrainer:
                       d_last, None, m.gbiases[L - 1].data_ptr(), self.ws_dense.data_ptr(), self.ws_dense.numel(), s)
             for li in range(L - 1, -1, -1):
                 if li == 0 and self.use_switch:
-                    self._switched(blocks[0].counts[_lib.CNT_DST:_lib.CNT_DST + 1], self.npad[0],
+                    self._switched(n0, self.npad[0],
                                    lambda R: _weight_grad(self.cat[0][:R], self.dz[0][:R], m.gweights[0], self.part0),
-                                   empty=lambda: m.gweights[0].zero_())
+                                   empty=lambda: m.gweights[0].zero_(), handle=h_wg)
                 else:
                     _weight_grad(self.cat[li][:self.npad[li]], self.dz[li][:self.npad[li]], m.gweights[li])
                 if li == 0:
@@ -277,7 +282,19 @@ class GraphedTrainer:
         if with_adam:
             self._adam_dev()
 
-    def _switched(self, n_dev: torch.Tensor, limit: int, fn, empty=None):
+    def _switch_handles(self, n_dev: torch.Tensor, limits):
+        """One selector kernel for all SWITCH nodes over the same device row
+        count (gns_graph_switch_handles); returns the handles, or None when
+        not capturing."""
+        if not torch.cuda.is_current_stream_capturing():
+            return None
+        C = self.switch_chunk
+        nb = (ctypes.c_int32 * len(limits))(*[-(-lim // C) + 1 for lim in limits])
+        hs = (ctypes.c_uint64 * len(limits))()
+        _lib.call("gns_graph_switch_handles", _lib.stream_ptr(), n_dev.data_ptr(), C, len(limits), nb, hs)
+        return list(hs)
+
+    def _switched(self, n_dev: torch.Tensor, limit: int, fn, empty=None, handle=None):
         """fn(R) over the first R = min(k * chunk, limit) rows, k = ceil(n /
         chunk) from the device count: a SWITCH graph node with one recorded
         body per k when capturing (gns_graph_switch_begin), fn(limit) eagerly.
@@ -289,7 +306,10 @@ class GraphedTrainer:
         C = self.switch_chunk
         K = -(-limit // C) + 1
         bodies = (ctypes.c_void_p * K)()
-        _lib.call("gns_graph_switch_begin", _lib.stream_ptr(), n_dev.data_ptr(), C, K, bodies)
+        if handle is not None:   # selector already appended (_switch_handles)
+            _lib.call("gns_graph_switch_node", _lib.stream_ptr(), handle, K, bodies)
+        else:
+            _lib.call("gns_graph_switch_begin", _lib.stream_ptr(), n_dev.data_ptr(), C, K, bodies)
         aux = self.aux_dense
         c0 = _lib.launch_counter[0]
         per_body = 0
