@@ -137,6 +137,15 @@ GNS_API int gns_record_event_external(void* event, void* stream);
  * loads are volatile (fresh on every replay).  4-byte aligned pointers. */
 GNS_API int gns_copy_mapped(void* dst, const void* src, int64_t bytes, void* stream);
 
+/* Sticky device error word: ORs counts[l * stride + GNS_CNT_ERR] of `layers`
+ * per-layer counter rows into *sticky (one thread, graph-capturable).  The
+ * per-batch counters are reset by every gns_sample_layer call, so an engine
+ * that reuses sampler slots accumulates each batch's error bits here and
+ * reads the word once per epoch (the reference raises at the failing call,
+ * sampling.py:248-249,255-256; the façade raises the same exceptions). */
+GNS_API int gns_errors_accumulate(const int32_t* counts, int32_t layers, int32_t stride, int32_t* sticky,
+                                  void* stream);
+
 /* CUDA-graph plumbing for the whole-step engine (engine.py).  `graph` is a
  * captured cudaGraph_t (torch.cuda.CUDAGraph(keep_graph=True).raw_cuda_graph()).
  * gns_graph_instantiate instantiates it, optionally honouring the per-kernel

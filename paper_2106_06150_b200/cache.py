@@ -205,16 +205,23 @@ class CacheState:
             object.__setattr__(self, "_c", c)
         return c
 
-    def mask_word_rank(self) -> torch.Tensor:
-        """Per-word popcount rank of the cache bitmap (cache-slot lookup)."""
+    def mask_word_rank(self, stream=None) -> torch.Tensor:
+        """Per-word popcount rank of the cache bitmap (cache-slot lookup).
+        Recomputed into the same buffer after a refresh (captured graphs
+        that read it stay valid)."""
         r = getattr(self, "_rank", None)
-        if r is None:
+        if r is None or self.__dict__.get("_rank_stale", False):
             bits = self.nodes.mask_bits
-            r = torch.empty_like(bits)
-            ws = _lib.workspace(1 << 20, bits.device)
+            if r is None:
+                r = torch.empty_like(bits)
+            ws = getattr(self, "_rank_ws", None)
+            if ws is None:
+                ws = _lib.workspace(1 << 20, bits.device)
+                object.__setattr__(self, "_rank_ws", ws)
             _lib.call("gns_bitmap_rank", bits.data_ptr(), bits.numel(), r.data_ptr(), ws.data_ptr(),
-                      ws.numel(), _lib.stream_ptr())
+                      ws.numel(), _lib.stream_ptr(stream))
             object.__setattr__(self, "_rank", r)
+            object.__setattr__(self, "_rank_stale", False)
         return r
 
 
@@ -231,57 +238,139 @@ def build_cache(g: Graph, probs: ProbVector, cache_size: int, epoch: int = 0, rn
 
 
 def refresh_cache(state: CacheState, g: Graph, probs: ProbVector, cache_size: int, epoch: int, rng_seed) -> bool:
-    """build_cache into the buffers of an existing CacheState of the same
-    graph and cache size (the per-epoch refresh of pool.py:133-135).  Device
-    addresses stay the same unless the new cached CSR outgrows its buffer, so
-    CUDA graphs that captured the cache stay valid; returns True when every
-    address was kept."""
-    new = _build_cache_into(state, g, probs, cache_size, epoch, rng_seed)
-    return new is state
+    """build_cache into an existing CacheState of the same graph and cache
+    size (the per-epoch refresh of pool.py:133-135), in place: ``state`` is
+    the new cache afterwards.  Device addresses stay the same unless the new
+    cached CSR outgrows its buffer — then ``state`` gets larger buffers (still
+    the same object) and CUDA graphs that captured the old addresses must be
+    re-captured.  Returns True when every address was kept."""
+    return refresh_finish(refresh_begin(state, g, probs, cache_size, epoch, rng_seed))
 
 
-def _build_cache_into(state, g, probs, cache_size, epoch, rng_seed):
+def empty_like(state: CacheState, g: Graph) -> CacheState:
+    """A second CacheState with buffers of the same sizes (double-buffered
+    refresh: the next epoch's cache is drawn into it while this one is in
+    use).  Contents are undefined until refresh_begin/refresh_finish."""
+    n = g.num_nodes
+    dev = state.inclusion.device
+    ids = torch.empty_like(state._buf_ids)
+    bits = torch.empty_like(state.nodes.mask_bits)
+    counts = torch.zeros_like(state._buf_counts)
+    k = len(state.nodes)
+    st = CacheState(nodes=NodeSet(ids=ids[:k], mask_bits=bits, num_nodes=n),
+                    inclusion=torch.empty(n, dtype=torch.float64, device=dev),
+                    cached_indptr=torch.empty(n + 1, dtype=torch.int64, device=dev),
+                    cached_indices=state._buf_cidx[:0], epoch=-1, source_probs=state.source_probs,
+                    cached_pos=state._buf_cpos[:0])
+    for name, val in (("_buf_ids", ids), ("_buf_counts", counts),
+                      ("_buf_cidx", torch.empty_like(state._buf_cidx)),
+                      ("_buf_cpos", torch.empty_like(state._buf_cpos))):
+        object.__setattr__(st, name, val)
+    object.__setattr__(st, "cached_indices", st._buf_cidx[:0])
+    object.__setattr__(st, "cached_pos", st._buf_cpos[:0])
+    return st
+
+
+class PendingRefresh:
+    """First half of a cache (re)build: the draw (cache.py:87-103), the
+    inclusion vector (cache.py:171-183) and the cached-CSR row counts
+    (cache.py:185-197) are enqueued on ``stream`` and (|C|, nnz_C) are copied
+    to pinned host memory; nothing waits on the host.  ``ready()`` polls;
+    ``refresh_finish`` sizes the cached CSR and enqueues its fill."""
+
+    def __init__(self, state, g, probs, epoch, stream, counts, nnz, host, ev, ws):
+        self.state, self.g, self.probs, self.epoch, self.stream = state, g, probs, epoch, stream
+        self.counts, self.nnz, self.host, self.ev, self._ws = counts, nnz, host, ev, ws
+        self.done = None      # event after the fill (refresh_finish)
+
+    def ready(self) -> bool:
+        return self.ev.query()
+
+
+def refresh_begin(state, g: Graph, probs: ProbVector, cache_size: int, epoch: int, rng_seed,
+                  stream=None) -> PendingRefresh:
+    """Enqueue draw + inclusion + cached-CSR count into ``state``'s buffers
+    (``state=None``: fresh buffers) on ``stream`` (default: current)."""
     probs = probs.normalize()
-    stream = _lib.stream_ptr()
+    stream = stream if stream is not None else torch.cuda.current_stream()
+    sp = _lib.stream_ptr(stream)
     seed, ep, tag = seed_key(rng_seed)
     n = g.num_nodes
+    with torch.cuda.stream(stream):
+        if state is not None:
+            bufs = (state._buf_ids, state.nodes.mask_bits, state._buf_counts)
+            incl, c_indptr = state.inclusion, state.cached_indptr
+        else:
+            bufs = None
+            incl = torch.empty(n, dtype=torch.float64, device=g.device)
+            c_indptr = torch.empty(n + 1, dtype=torch.int64, device=g.device)
+        ids, bits, counts = _draw(probs, cache_size, seed, ep, stream=stream, tag=tag, out=bufs)
+        # |C| and |support| stay on the device (counts[0], counts[1])
+        _lib.call("gns_inclusion", probs.weights.data_ptr(), n, 0, counts.data_ptr(),
+                  counts[1:].data_ptr(), incl.data_ptr(), sp)
+        nnz = torch.zeros(1, dtype=torch.int64, device=g.device)
+        ws = _lib.workspace(_lib.lib().gns_cached_csr_workspace_size(n), g.device)
+        _lib.call("gns_cached_csr_count", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
+                  nnz.data_ptr(), ws.data_ptr(), ws.numel(), sp)
+        host = torch.empty(2, dtype=torch.int64).pin_memory()
+        host[:1].copy_(counts[:1], non_blocking=True)
+        host[1:].copy_(nnz, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+    if state is None:
+        state = (ids, bits, counts, incl, c_indptr)
+    return PendingRefresh(state, g, probs, epoch, stream, counts, nnz, host, ev, ws)
+
+
+def refresh_finish(p: PendingRefresh):
+    """Second half: read (|C|, nnz_C) (waits for the first half), grow the
+    cached-CSR buffers if needed and enqueue the fill on the same stream.
+    For a refresh into an existing state returns True when every device
+    address was kept (False: captured graphs must be re-captured); for a
+    fresh build returns the new CacheState."""
+    p.ev.synchronize()
+    k, nnz_h = int(p.host[0]), int(p.host[1])
+    g, stream = p.g, p.stream
+    state = p.state if isinstance(p.state, CacheState) else None
+    if state is not None and k != len(state.nodes):
+        raise ValueError(f"refresh_cache: cache size changed ({len(state.nodes)} -> {k}); use build_cache")
+    with torch.cuda.stream(stream):
+        keep = state is not None and state._buf_cidx.numel() >= nnz_h
+        if keep:
+            c_indices, c_pos = state._buf_cidx, state._buf_cpos
+        else:
+            cap = max(nnz_h + nnz_h // 4, 1)      # headroom: later draws rarely reallocate
+            c_indices = torch.empty(cap, dtype=torch.int32, device=g.device)
+            c_pos = torch.empty(cap, dtype=torch.int32, device=g.device)
+        if state is not None:
+            bits, c_indptr = state.nodes.mask_bits, state.cached_indptr
+        else:
+            ids, bits, counts, incl, c_indptr = p.state
+        _lib.call("gns_cached_csr_fill", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
+                  c_indices.data_ptr(), c_pos.data_ptr(), _lib.stream_ptr(stream))
+        p.done = torch.cuda.Event()
+        p.done.record(stream)
     if state is not None:
-        bufs = (state._buf_ids, state.nodes.mask_bits, state._buf_counts)
-        incl, c_indptr = state.inclusion, state.cached_indptr
-    else:
-        bufs = None
-        incl = torch.empty(n, dtype=torch.float64, device=g.device)
-        c_indptr = torch.empty(n + 1, dtype=torch.int64, device=g.device)
-    ids, bits, counts = _draw(probs, cache_size, seed, ep, tag=tag, out=bufs)
-    # |C| and |support| stay on the device (counts[0], counts[1])
-    _lib.call("gns_inclusion", probs.weights.data_ptr(), n, 0, counts.data_ptr(),
-              counts[1:].data_ptr(), incl.data_ptr(), stream)
-    nnz = torch.zeros(1, dtype=torch.int64, device=g.device)
-    ws = _lib.workspace(_lib.lib().gns_cached_csr_workspace_size(n), g.device)
-    _lib.call("gns_cached_csr_count", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
-              nnz.data_ptr(), ws.data_ptr(), ws.numel(), stream)
-    host = counts.cpu()  # one sync per refresh: |C| and nnz_C size the outputs
-    nnz_h = int(nnz.item())
-    k = int(host[0])
-    keep = state is not None and state._buf_cidx.numel() >= nnz_h and k == len(state.nodes)
-    if keep:
-        c_indices, c_pos = state._buf_cidx, state._buf_cpos
-    else:
-        cap = max(nnz_h + nnz_h // 4, 1)      # headroom: later draws rarely reallocate
-        c_indices = torch.empty(cap, dtype=torch.int32, device=g.device)
-        c_pos = torch.empty(cap, dtype=torch.int32, device=g.device)
-    _lib.call("gns_cached_csr_fill", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
-              c_indices.data_ptr(), c_pos.data_ptr(), stream)
-    if keep:   # frozen dataclass: refresh the views in place (same addresses)
+        # frozen dataclass: refresh the fields in place.  The draw, inclusion
+        # and cached_indptr were written into the state's own buffers; the
+        # cached CSR buffers are the old ones or (grown) new ones
         for name, val in (("cached_indices", c_indices[:nnz_h]), ("cached_pos", c_pos[:nnz_h]),
-                          ("epoch", epoch), ("source_probs", probs)):
+                          ("epoch", p.epoch), ("source_probs", p.probs), ("_buf_cidx", c_indices),
+                          ("_buf_cpos", c_pos)):
             object.__setattr__(state, name, val)
-        state.__dict__.pop("_rank", None)      # bitmap content changed
-        return state
+        object.__setattr__(state, "_rank_stale", True)   # bitmap content changed
+        state.__dict__.pop("_c", None)         # cstruct: cached_indices may have moved
+        return keep
+    n = g.num_nodes
     nodes = NodeSet(ids=ids[:k], mask_bits=bits, num_nodes=n)
     st = CacheState(nodes=nodes, inclusion=incl, cached_indptr=c_indptr,
-                    cached_indices=c_indices[:nnz_h], epoch=epoch, source_probs=probs,
+                    cached_indices=c_indices[:nnz_h], epoch=p.epoch, source_probs=p.probs,
                     cached_pos=c_pos[:nnz_h])
     for name, val in (("_buf_ids", ids), ("_buf_counts", counts), ("_buf_cidx", c_indices), ("_buf_cpos", c_pos)):
         object.__setattr__(st, name, val)
     return st
+
+
+def _build_cache_into(state, g, probs, cache_size, epoch, rng_seed):
+    r = refresh_finish(refresh_begin(state, g, probs, cache_size, epoch, rng_seed))
+    return state if state is not None else r

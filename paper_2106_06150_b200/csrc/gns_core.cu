@@ -246,6 +246,13 @@ __global__ void __launch_bounds__(256) copy_mapped_kernel(unsigned char* __restr
   if (blockIdx.x == 0 && threadIdx.x < tail) dst[words * 4 + threadIdx.x] = ((const volatile unsigned char*)src)[words * 4 + threadIdx.x];
 }
 
+__global__ void errors_accumulate_kernel(const int32_t* __restrict__ counts, int layers, int stride,
+                                        int32_t* __restrict__ sticky) {
+  int32_t e = 0;
+  for (int l = 0; l < layers; ++l) e |= counts[(int64_t)l * stride + GNS_CNT_ERR];
+  if (e) sticky[0] |= e;
+}
+
 template <int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK) bitmap_rank_kernel(ScanStatus st, const uint32_t* __restrict__ bits,
                                                             int64_t nwords, int32_t* __restrict__ rank) {
@@ -275,6 +282,16 @@ int gns_copy_mapped(void* dst, const void* src, int64_t bytes, void* stream) {
   const int grid = (int)(words < 256 * 8 ? (words + 255) / 256 : 8);
   copy_mapped_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((unsigned char*)dst, (const unsigned char*)src, bytes);
   return check_launch("copy_mapped");
+}
+
+int gns_errors_accumulate(const int32_t* counts, int32_t layers, int32_t stride, int32_t* sticky, void* stream) {
+  if (layers <= 0) return GNS_OK;
+  if (!counts || !sticky || stride <= GNS_CNT_ERR) {
+    set_error("errors_accumulate: null pointer or stride <= GNS_CNT_ERR");
+    return GNS_EINVAL;
+  }
+  errors_accumulate_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(counts, layers, stride, sticky);
+  return check_launch("errors_accumulate");
 }
 
 int gns_record_event_external(void* event, void* stream) {

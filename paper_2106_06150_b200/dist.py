@@ -16,11 +16,44 @@ import torch
 import torch.distributed as dist
 
 
-def rank_batches(num_batches: int, rank: int, world_size: int) -> list[int]:
-    """Batch indices owned by ``rank`` (pool.py:80 striding)."""
+def rank_batches(num_batches: int, rank: int, world_size: int, pad: bool = False) -> list:
+    """Batch indices owned by ``rank`` (pool.py:80 striding).
+
+    ``pad=True`` is the data-parallel schedule: every rank gets the same
+    number of steps per epoch, ceil(num_batches / W); a rank whose stripe is
+    one batch short gets ``None`` for its last step and trains on an empty
+    batch there, i.e. contributes a zero gradient to that step's all-reduce
+    ("a rank that is one batch short contributes a zero
+    gradient").  Every batch of the epoch is still trained exactly once and
+    every rank issues the same number of collectives."""
     if world_size < 1 or not (0 <= rank < world_size):
         raise ValueError("need 0 <= rank < world_size")
-    return list(range(rank, num_batches, world_size))
+    own = list(range(rank, num_batches, world_size))
+    if pad:
+        steps = -(-num_batches // world_size)
+        own += [None] * (steps - len(own))
+    return own
+
+
+def steps_per_epoch(num_batches: int, world_size: int) -> int:
+    """Training steps (= gradient all-reduces) per epoch on every rank."""
+    return -(-num_batches // world_size)
+
+
+def epoch_schedule(num_batches: int, rank: int, world_size: int, epochs: int, cache_period: int = 1,
+                   start_epoch: int = 0):
+    """The rank's whole step schedule over ``epochs`` epochs: a list of
+    ``(epoch, index_or_None, refresh_cache_before)`` in issue order.  This is
+    what ``GraphedTrainer.run_epoch`` executes; the cache is redrawn at the
+    first step of every epoch with ``epoch % cache_period == 0``
+    (pool.py:133-135) with the key ``[seed, 33, epoch]`` — the same points on
+    every rank, so the replicated caches stay identical."""
+    out = []
+    for e in range(start_epoch, start_epoch + epochs):
+        idx = rank_batches(num_batches, rank, world_size, pad=world_size > 1)
+        for j, i in enumerate(idx):
+            out.append((e, i, j == 0 and (e == start_epoch or e % cache_period == 0)))
+    return out
 
 
 def make_allreduce(group=None, force: bool = False):

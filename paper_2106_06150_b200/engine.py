@@ -18,8 +18,22 @@ capacity-sized GEMMs are SWITCH conditional nodes that run over
 ceil(n / chunk) * chunk rows of the batch's device count.
 
 The cache (cache.py) is redrawn at epoch boundaries every ``cache_period``
-epochs (pool.py:133-135) into the same device buffers, so the graphs stay
-valid (re-captured only if a buffer has to grow, or for the mixed placement).
+epochs (pool.py:133-135) with the key ``[seed, 33, epoch]``.  It is
+double-buffered: two cache buffer sets (plus, for the mixed placement, two
+HBM feature tables) with step graphs captured once per set.  While epoch e
+trains on one set, the cache of the next refresh epoch is drawn into the
+other on a low-priority stream (draw + inclusion + cached-CSR count, then —
+polled from the host loop without blocking — the cached-CSR fill and the
+pinned-host -> HBM feature-row refresh), and the epoch boundary only flips
+the active set.  Graphs are re-captured only if a cached-CSR buffer grows.
+
+Data parallel: every rank runs ceil(num_batches / W) steps per epoch
+(dist.rank_batches(pad=True)); a rank whose stripe is short trains its last
+step on an empty batch (zero gradient), so all ranks issue the same
+collectives and refresh their (identical, replicated) caches at the same
+steps.  Device error flags of every sampled batch are OR-ed into a sticky
+word (gns_errors_accumulate) that ``run_epoch`` / ``run_host`` check once per
+call and raise as the reference does (sampling.py:248-249,255-256).
 """
 
 from __future__ import annotations
@@ -33,7 +47,7 @@ from . import _lib
 from . import cache as cache_mod
 from .graph import Graph
 from .model import GraphSAGE, TrainConfig, _split_rows, _weight_grad
-from .dist import rank_batches
+from .dist import rank_batches, steps_per_epoch
 from .pool import cache_probs, exact_tables, num_batches
 from .sampling import MiniBatchSampler, SamplerConfig
 
@@ -62,6 +76,10 @@ class GraphedTrainer:
         self.dev = g.device
         self.model = GraphSAGE(dims, dtype=torch.float32, device=self.dev, seed=seed)
         self.dims = self.model.dims
+        lab = g.labels
+        if lab.numel() and (int(lab.min()) < 0 or int(lab.max()) >= self.dims[-1]):
+            # model.py:192-193 (checked once here: the labels are fixed)
+            raise ValueError(f"label out of range for {self.dims[-1]} classes")
         self.L = config.num_layers
         # two steps per replay by default: half the graph launches and host
         # round trips (papers100M e2e 1645 vs 1614 mb/s, OAG/products/cfg1
@@ -106,7 +124,7 @@ class GraphedTrainer:
         # directly (gns_spmm_fwd_gather) instead of a gathered copy
         self.fused_gather = feature_placement == "device" and os.environ.get("GNS_FUSED_GATHER", "1") == "1"
         self.host_features = None
-        self.cache_table = None
+        self.tables = [None, None]
         if feature_placement == "mixed":
             if config.strategy != "GNS":
                 raise ValueError("mixed placement needs the GNS cache")
@@ -115,8 +133,16 @@ class GraphedTrainer:
                 hf = hf.pin_memory()
             self.host_features = hf
             cs = int(round(config.cache_frac * g.num_nodes))
-            self.cache_table = torch.empty((max(cs, 1), hf.shape[1]), dtype=torch.float32, device=g.device)
-        self.cache = None
+            self.tables[0] = torch.empty((max(cs, 1), hf.shape[1]), dtype=torch.float32, device=g.device)
+        # double-buffered cache: csets[cur] is the active CacheState; the
+        # other set receives the next refresh epoch's cache (prefetch)
+        self.csets = [None, None]
+        self.cur = 0
+        self._pf = None
+        self.prefetch = os.environ.get("GNS_CACHE_PREFETCH", "1") == "1"
+        self.refresh_log = []      # (epoch, how) of every cache refresh, for tests / bench
+        # sticky device error word (gns_errors_accumulate after every sampled batch)
+        self.err_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self._probs = None
         self._tables = None
         self._prof_events = None
@@ -134,6 +160,7 @@ class GraphedTrainer:
                       for _ in range(S)]
         self.side = self.sides[0]
         self.main = torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "main" else lo)
+        self.refresh_stream = torch.cuda.Stream(device=self.dev, priority=lo)
         self.taux = [torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "side" else lo)
                      for _ in range(2 * S)]
         # size-switched input-layer dense ops: the capacity-sized GEMMs run
@@ -143,8 +170,26 @@ class GraphedTrainer:
             int(os.environ.get("GNS_SWITCH_CHUNK", "8192"))
         self.aux_dense = torch.cuda.Stream(device=self.dev, priority=hi if self.prio_mode == "main" else lo)
         self._execs = {}
+        self._warmed = False
         self._per_replay = 0
         self._alloc()
+
+    @property
+    def cache(self):
+        """The active CacheState (the one the current epoch samples with)."""
+        return self.csets[self.cur]
+
+    @cache.setter
+    def cache(self, state):
+        """Adopt an externally built cache as the active set."""
+        self.csets[self.cur] = state
+        self._free_execs(self.cur)
+        if self.placement == "mixed" and state is not None:
+            self._fill_table(self.cur, torch.cuda.current_stream())
+
+    @property
+    def cache_table(self):
+        return self.tables[self.cur]
 
     # -- static buffers -----------------------------------------------------------
     def _alloc(self):
@@ -200,7 +245,7 @@ class GraphedTrainer:
             _lib.call("gns_record_event_external", ev[0].cuda_event, s)
         if self.placement == "mixed":
             hf, c = self.host_features, self.cache
-            _lib.call("gns_gather_rows_mixed", hf.data_ptr(), self.cache_table.data_ptr(),
+            _lib.call("gns_gather_rows_mixed", hf.data_ptr(), self.tables[self.cur].data_ptr(),
                       c.nodes.mask_bits.data_ptr(), c.mask_word_rank().data_ptr(), hf.stride(0),
                       b0.src_nodes.data_ptr(), n_in_dev.data_ptr(), self.cap_src[0], self.dims[0],
                       self.h0.data_ptr(), self.h0.stride(0), s)
@@ -373,39 +418,104 @@ class GraphedTrainer:
                           self.cache if self.cfg.strategy == "GNS" else None, exact_tables=self._tables,
                           after_layer=transpose, epoch_perm=self.epoch_perm if fetch else None,
                           step_src=self.step_host[slot] if fetch else None)
+        _lib.call("gns_errors_accumulate", sl.counts.data_ptr(), self.L, _lib.CNT_N, self.err_dev.data_ptr(), s)
         for ev in joins:
             cur.wait_event(ev)
 
     # -- cache + capture ------------------------------------------------------------
-    def _refresh_cache(self, epoch: int) -> bool:
-        """pool.py:109-135; returns True when device addresses the captured
-        graphs use changed (they must be re-captured)."""
+    def _cache_size(self) -> int:
+        return int(round(self.cfg.cache_frac * self.g.num_nodes))     # pool.py:114
+
+    def _needs_refresh(self, epoch: int) -> bool:
+        """pool.py:133-135: redraw when there is no cache or epoch % P == 0."""
         if self.cfg.strategy != "GNS":
             return False
+        c = self.cache
+        return c is None or (epoch % self.cfg.cache_period == 0 and c.epoch != epoch)
+
+    def _fill_table(self, cs: int, stream):
+        """Mixed placement, feature refresh (paper §3.1): the cached rows of
+        cache set ``cs``, pinned host -> its HBM table, read through UVA by
+        gns_cache_refresh_rows on ``stream``; plus the bitmap word ranks the
+        mixed gather uses to find a row's slot."""
+        st = self.csets[cs]
+        hf, ids = self.host_features, st.nodes.ids
+        if self.tables[cs] is None:
+            self.tables[cs] = torch.empty_like(self.tables[1 - cs])
+        with torch.cuda.stream(stream):
+            _lib.call("gns_cache_refresh_rows", hf.data_ptr(), hf.stride(0), ids.data_ptr(),
+                      st._buf_counts.data_ptr(), ids.numel(), self.dims[0], self.tables[cs].data_ptr(),
+                      _lib.stream_ptr(stream))
+            st.mask_word_rank(stream)
+
+    def _refresh_cache(self, epoch: int):
+        """pool.py:109-135 at an epoch boundary: activate the prefetched
+        cache of this epoch if there is one, else draw it now (stop-the-world,
+        into the idle set).  Re-captures only the graphs of a set whose
+        buffers moved."""
+        if self.cfg.strategy != "GNS":
+            return
         if self._probs is None:
             self._probs = cache_probs(self.g, self.cfg)
-        cs = int(round(self.cfg.cache_frac * self.g.num_nodes))
+        cs = self._cache_size()
         seed = [self.cfg.seed, _CACHE, epoch]
-        moved = True
-        if self.cache is not None and self.placement == "device":
-            # in place: same buffers, so the step graphs stay valid
-            moved = not cache_mod.refresh_cache(self.cache, self.g, self._probs, cs, epoch, seed)
+        pf = self._pf
+        if pf is not None and pf[1].epoch == epoch:
+            t, p, stage = pf
+            if stage == 1:
+                self._prefetch_finish()
+            self._pf = None
+            torch.cuda.synchronize()
+            self.cur = t
+            self.refresh_log.append((epoch, "prefetched"))
         else:
-            self.cache = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch, rng_seed=seed)
+            self._pf = None
+            t = self.cur if self.cache is None else 1 - self.cur
+            if self.csets[t] is None:
+                if self.csets[1 - t] is None:
+                    self.csets[t] = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch, rng_seed=seed)
+                else:
+                    self.csets[t] = cache_mod.empty_like(self.csets[1 - t], self.g)
+                    cache_mod.refresh_cache(self.csets[t], self.g, self._probs, cs, epoch, seed)
+                self._free_execs(t)
+            elif not cache_mod.refresh_cache(self.csets[t], self.g, self._probs, cs, epoch, seed):
+                self._free_execs(t)
+            if self.placement == "mixed":
+                self._fill_table(t, torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            self.cur = t
+            self.refresh_log.append((epoch, "sync"))
         if self.cfg.weight_policy == "gns-exact" and self._tables is None:
             self._tables = exact_tables(self.g, self.cfg, self._probs, cs)
+
+    def _prefetch_begin(self, epoch: int):
+        """Start drawing the cache of ``epoch`` into the idle set on the
+        low-priority refresh stream (no host wait)."""
+        if self.cfg.strategy != "GNS" or self.cache is None:
+            return
+        if self._pf is not None and self._pf[1].epoch == epoch:
+            return
+        t = 1 - self.cur
+        if self.csets[t] is None:
+            self.csets[t] = cache_mod.empty_like(self.cache, self.g)
+            self._free_execs(t)
+        rs = self.refresh_stream
+        rs.wait_stream(torch.cuda.current_stream())
+        p = cache_mod.refresh_begin(self.csets[t], self.g, self._probs, self._cache_size(), epoch,
+                                    [self.cfg.seed, _CACHE, epoch], stream=rs)
+        self._pf = (t, p, 1)
+
+    def _prefetch_poll(self, block: bool = False):
+        if self._pf is not None and self._pf[2] == 1 and (block or self._pf[1].ready()):
+            self._prefetch_finish()
+
+    def _prefetch_finish(self):
+        t, p, _ = self._pf
+        if not cache_mod.refresh_finish(p):
+            self._free_execs(t)
         if self.placement == "mixed":
-            # feature refresh (paper §3.1): cached rows pinned-host -> HBM on a
-            # side stream, read through UVA by gns_cache_refresh_rows
-            hf, ids = self.host_features, self.cache.nodes.ids
-            n_dev = torch.tensor([ids.numel()], dtype=torch.int64, device=self.dev)
-            with torch.cuda.stream(self.side):
-                self.side.wait_stream(torch.cuda.current_stream())
-                _lib.call("gns_cache_refresh_rows", hf.data_ptr(), hf.stride(0), ids.data_ptr(), n_dev.data_ptr(),
-                          ids.numel(), self.dims[0], self.cache_table.data_ptr(), _lib.stream_ptr(self.side))
-                self.cache.mask_word_rank()
-            self.side.synchronize()
-        return moved
+            self._fill_table(t, self.refresh_stream)
+        self._pf = (t, p, 2)
 
     def _set_step(self, slot: int, epoch: int, index: int | None):
         b = self.cfg.batch_size
@@ -464,6 +574,7 @@ class GraphedTrainer:
                 _weight_grad(self.cat[0][:C], self.dz[0][:C], m.gweights[0], self.part0)
                 m.gweights[0].zero_()
         self._prof_events = ev
+        self._warmed = True
         torch.cuda.synchronize()
 
     def _capture(self, p: int, r: int):
@@ -510,13 +621,13 @@ class GraphedTrainer:
         ex = ctypes.c_void_p()
         _lib.call("gns_graph_instantiate", gph.raw_cuda_graph(), 0 if self.prio_mode == "none" else 1,
                   ctypes.byref(ex))
-        self._execs[(p, r)] = (gph, ex)
+        self._execs[(p, r, self.cur)] = (gph, ex)
         torch.cuda.synchronize()
 
-    def _free_execs(self):
-        for _, ex in self._execs.values():
-            _lib.call("gns_graph_exec_destroy", ex)
-        self._execs = {}
+    def _free_execs(self, cset: int | None = None):
+        """Destroy the step graphs (of one cache set, or all)."""
+        for key in [k for k in self._execs if cset is None or k[2] == cset]:
+            _lib.call("gns_graph_exec_destroy", self._execs.pop(key)[1])
 
     def __del__(self):
         try:
@@ -526,20 +637,20 @@ class GraphedTrainer:
 
     def _replay(self, p: int, r: int | None = None):
         r = self.S if r is None else r
-        if (p, r) not in self._execs:
-            if not self._execs:
+        if (p, r, self.cur) not in self._execs:
+            if not self._warmed:
                 self._warm()
             self._capture(p, r)
-        _lib.call("gns_graph_launch", self._execs[(p, r)][1], _lib.stream_ptr(self.main))
+        _lib.call("gns_graph_launch", self._execs[(p, r, self.cur)][1], _lib.stream_ptr(self.main))
 
     def prepare(self, steps: int):
         """Capture every step graph a run of ``steps`` steps (within one
         epoch) replays, so no capture happens inside a timed region."""
-        if not self._execs:
+        if not self._warmed:
             self._warm()
         for r in {self.S, steps % self.S} - {0}:
             for p in (0, 1):
-                if (p, r) not in self._execs:
+                if (p, r, self.cur) not in self._execs:
                     self._capture(p, r)
 
     @property
@@ -549,10 +660,10 @@ class GraphedTrainer:
 
     def kernel_priorities(self, p: int = 0):
         """Histogram of |priority| over the kernel nodes of step graph (p, S)."""
-        if (p, self.S) not in self._execs:
+        if (p, self.S, self.cur) not in self._execs:
             self._capture(p, self.S)
         hist = (ctypes.c_int32 * 8)()
-        _lib.call("gns_graph_kernel_priorities", self._execs[(p, self.S)][0].raw_cuda_graph(), hist, 8)
+        _lib.call("gns_graph_kernel_priorities", self._execs[(p, self.S, self.cur)][0].raw_cuda_graph(), hist, 8)
         return list(hist)
 
     def loss_value(self) -> float:
@@ -563,13 +674,16 @@ class GraphedTrainer:
 
     def kernels_per_step(self) -> float:
         """libgns kernels inside the captured step graph, per training step."""
-        if not self._per_replay and (0, self.S) not in self._execs:
+        if not self._per_replay and (0, self.S, self.cur) not in self._execs:
             self._capture(0, self.S)
         return self._per_replay / self.S
 
     # -- driving ----------------------------------------------------------------------
     def batches(self, epoch: int):
-        return rank_batches(num_batches(self.g, self.cfg), self.rank, self.world)
+        """This rank's step schedule of ``epoch``: batch indices (pool.py:80
+        striding); data parallel (W > 1): padded to ceil(nb / W) steps with
+        None = an empty batch (zero gradient), the same count on every rank."""
+        return rank_batches(num_batches(self.g, self.cfg), self.rank, self.world, pad=self.world > 1)
 
     def run(self, steps: int, epoch: int = 0, first: int = 0, on_step=None):
         """Run ``steps`` training steps starting at batch ``first`` of
@@ -584,10 +698,10 @@ class GraphedTrainer:
                 first += n
         return epoch, first
 
-    def _begin(self, epoch: int, refresh: bool):
+    def _begin(self, epoch: int):
         torch.cuda.synchronize()
-        if refresh and self._refresh_cache(epoch):
-            self._free_execs()
+        if self._needs_refresh(epoch):
+            self._refresh_cache(epoch)
         self.adam_t.fill_(self.model.step_count)
         if self.epoch_perm is not None and self._perm_epoch != epoch:
             n = self.train_ids.numel()
@@ -596,15 +710,23 @@ class GraphedTrainer:
             torch.cuda.synchronize()
             self._perm_epoch = epoch
 
+    def _next_refresh_epoch(self, epoch: int):
+        """The epoch after ``epoch`` if it redraws the cache (pool.py:133-135)."""
+        e = epoch + 1
+        return e if self.cfg.strategy == "GNS" and e % self.cfg.cache_period == 0 else None
+
     def run_epoch(self, epoch: int, first: int = 0, max_steps: int | None = None, on_step=None) -> int:
-        need_refresh = self.cfg.strategy == "GNS" and (
-            self.cache is None or (first == 0 and epoch % self.cfg.cache_period == 0))
+        """Steps ``first``, ``first+1``, ... of this rank's schedule of
+        ``epoch`` (at most ``max_steps``); returns the number of steps run.
+        ``on_step(epoch, index, k)`` (index None = padded empty step) runs
+        after each step is enqueued."""
         idx = self.batches(epoch)[first:]
         if max_steps is not None:
             idx = idx[:max_steps]
         if not idx:
             return 0
-        self._begin(epoch, need_refresh)
+        self._begin(epoch)
+        nre = self._next_refresh_epoch(epoch) if self.prefetch else None
         S = self.S
         groups = [idx[i:i + S] for i in range(0, len(idx), S)]
         # prologue: sample the first group into group-0 slots
@@ -625,12 +747,20 @@ class GraphedTrainer:
                 ev.record(self.main)
                 for sl in self._group(1 - p):
                     self.done[sl] = ev
+            if nre is not None:
+                # the next refresh epoch's cache is drawn into the idle set on
+                # the low-priority refresh stream, behind the first replay
+                if gi == 0:
+                    self._prefetch_begin(nre)
+                else:
+                    self._prefetch_poll()
             self.model.step_count += len(grp)
             for j, index in enumerate(grp):
                 self._cur_j = j
                 if on_step is not None:
                     on_step(epoch, index, k)
                 k += 1
+        self.check_errors()
         return len(idx)
 
     def run_host(self, batches, epoch: int = 0, on_loss=None):
@@ -644,7 +774,7 @@ class GraphedTrainer:
             raise ValueError("construct with host_targets=True")
         if not batches:
             return []
-        self._begin(epoch, self.cfg.strategy == "GNS" and self.cache is None)
+        self._begin(epoch)
         S = self.S
         losses = []
         # double-buffered loss read-back: replay g+1 is queued before the host
@@ -694,16 +824,20 @@ class GraphedTrainer:
                 drain()
         while pending:
             drain()
+        self.check_errors()
         return losses
 
     def check_errors(self):
-        """Read the device error flags of both slots (one sync)."""
-        for sl in self.slots:
-            c = sl.counts.cpu()
-            err = int(c[:, _lib.CNT_ERR].max())
-            if err & _lib.ERRBIT_ZEROPROB:
-                raise ValueError("inclusion probability is zero for a cached draw")
-            if err & _lib.ERRBIT_CAPACITY:
-                raise _lib.InvariantError("neighbour selection did not converge (capacity)")
-            if err & _lib.ERRBIT_ZEROQ:
-                raise _lib.InvariantError("sampled an edge with zero estimated inclusion")
+        """Raise the reference's exception for any device error flag of a
+        batch sampled since the last check (sticky word; one sync)."""
+        torch.cuda.synchronize()
+        err = int(self.err_dev.item())
+        if not err:
+            return
+        self.err_dev.zero_()
+        if err & _lib.ERRBIT_ZEROPROB:
+            raise ValueError("inclusion probability is zero for a cached draw")   # sampling.py:255-256
+        if err & _lib.ERRBIT_CAPACITY:
+            raise _lib.InvariantError("neighbour selection did not converge (capacity)")
+        if err & _lib.ERRBIT_ZEROQ:
+            raise _lib.InvariantError("sampled an edge with zero estimated inclusion")   # sampling.py:248-249

@@ -145,6 +145,7 @@ class GraphSAGE:
         self._ws_xent = None
         self._ws_dense = None
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._labels_checked = None
 
     @property
     def num_layers(self) -> int:
@@ -203,6 +204,13 @@ class GraphSAGE:
     def loss_and_grad(self, logits: torch.Tensor, labels: torch.Tensor, mb: MiniBatch, stream=None):
         """model.py:189-200 fused: returns dlogits; mean loss lands in loss_dev."""
         n, c = logits.shape
+        key = (labels.data_ptr(), labels.numel(), c)
+        if self._labels_checked != key:
+            # model.py:192-193 (once per labels tensor: the kernel indexes
+            # labels[targets[r]] and would silently use a wrong row otherwise)
+            if labels.numel() and (int(labels.min()) < 0 or int(labels.max()) >= c):
+                raise ValueError(f"label out of range for {c} classes")
+            self._labels_checked = key
         grad = torch.empty_like(logits)
         if self._ws_xent is None or self._ws_xent.numel() < 8 * max(n, 1):
             self._ws_xent = _lib.workspace(8 * max(n, 1024), self.device)

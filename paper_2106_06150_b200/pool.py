@@ -11,6 +11,13 @@ dedicated CUDA stream, so batch i+1 is sampled while the consumer trains on
 batch i.  ``num_workers`` slots (capped at ``queue_capacity``) are kept in
 flight.  Rank striding for data parallelism is ``index ≡ rank (mod world)``
 exactly like the reference's worker striding (pool.py:80).
+
+Batch lifetime: a yielded ``BatchItem.minibatch`` is a view of its slot's
+buffers and stays valid until the consumer advances the iterator ``depth``
+more times (the slot is then re-sampled).  ``copy=True`` yields independent
+clones instead — the reference's semantics (every batch its own arrays), at
+the cost of one device copy per batch; use it when batches are kept (e.g.
+``list(pool.iter_epoch(e))``).
 """
 
 from __future__ import annotations
@@ -105,7 +112,7 @@ class SamplerPool:
     """Produces one epoch of mini-batches at a time (pool.py:88-198)."""
 
     def __init__(self, g: Graph, config: SamplerConfig, num_workers: int = 1, queue_capacity: int = 8,
-                 rank: int = 0, world_size: int = 1):
+                 rank: int = 0, world_size: int = 1, copy: bool = False):
         if num_workers < 1:
             raise ValueError("num_workers must be >= 1")
         if queue_capacity < 1:
@@ -117,6 +124,7 @@ class SamplerPool:
         self.queue_capacity = queue_capacity
         self.rank = rank
         self.world_size = world_size
+        self.copy = bool(copy)
         self.cache = None
         self._probs = None
         self._tables = None
@@ -173,6 +181,8 @@ class SamplerPool:
             ev, t0, t1 = pending.pop(j)
             mb = self.slots[slot].collect(ev, policy_gns=self.config.weight_policy)
             torch.cuda.current_stream().wait_event(ev)
+            if self.copy:
+                mb = mb.clone()
             yield BatchItem(epoch=epoch, index=index, minibatch=mb, _t0=t0, _t1=t1)
             # the consumer is done with this slot once its queued work finishes
             rel = torch.cuda.Event()

@@ -114,10 +114,27 @@ class LayerBlock:
     edge_node: torch.Tensor | None = None
     row_scan: torch.Tensor | None = None
     _c: object = None  # gns_block_t of the engine buffers
+    counts: torch.Tensor | None = None  # int32[GNS_CNT_N] device counters of this block
 
     @property
     def num_edges(self) -> int:
         return int(self.edge_src.shape[0])
+
+    def clone(self) -> "LayerBlock":
+        """Independent copy (own device buffers and gns_block_t), no longer
+        tied to the sampler slot that produced it."""
+        def c(t):
+            return None if t is None else t.clone()
+        b = LayerBlock(dst_nodes=c(self.dst_nodes), src_nodes=c(self.src_nodes), edge_src=c(self.edge_src),
+                       edge_dst=c(self.edge_dst), edge_weight=c(self.edge_weight), edge_cached=c(self.edge_cached),
+                       dst_degree=c(self.dst_degree), fanout=self.fanout, policy=self.policy,
+                       self_pos=c(self.self_pos), edge_node=c(self.edge_node), row_scan=c(self.row_scan),
+                       counts=c(self.counts))
+        if self.counts is not None:
+            b._c = _lib.GnsBlock(*(0 if t is None else t.data_ptr() for t in (
+                b.row_scan, b.dst_degree, b.self_pos, None, b.edge_node, b.edge_src, b.edge_dst,
+                b.edge_weight, b.edge_cached, b.src_nodes, b.counts)))
+        return b
 
     def to_numpy(self):
         """Reference dtypes (int64 / float64 / bool) on the host."""
@@ -141,6 +158,12 @@ class MiniBatch:
     @property
     def num_layers(self) -> int:
         return len(self.blocks)
+
+    def clone(self) -> "MiniBatch":
+        """Independent copy of a batch (the façade's batches are views of a
+        sampler slot's buffers that the slot's next batch overwrites)."""
+        blocks = tuple(b.clone() for b in self.blocks)
+        return MiniBatch(blocks=blocks, targets=blocks[-1].dst_nodes, input_nodes=blocks[0].src_nodes)
 
 
 # ---------------------------------------------------------------------------
@@ -325,7 +348,16 @@ class MiniBatchSampler:
             event.synchronize()
         else:
             torch.cuda.current_stream().synchronize()
-        c = self.counts_host.tolist()
+        return self._wrap(self.counts_host.tolist(), policy_ns, policy_gns)
+
+    def snapshot(self, policy_ns="uniform", policy_gns="gns-paper") -> MiniBatch:
+        """The batch currently held in this slot's buffers, whoever sampled it
+        (e.g. a captured engine step): synchronises the device, reads the
+        device counts and wraps the buffers (views; raises on error flags)."""
+        torch.cuda.synchronize()
+        return self._wrap(self.counts.cpu().tolist(), policy_ns, policy_gns)
+
+    def _wrap(self, c, policy_ns, policy_gns) -> MiniBatch:
         err = 0
         blocks = []
         seeds_n = None
@@ -339,7 +371,7 @@ class MiniBatchSampler:
                 edge_cached=lb.edge_cached[:ne], dst_degree=lb.dst_degree[:nd], fanout=lb.k,
                 policy=policy_gns if self.config.strategy == "GNS" else policy_ns,
                 self_pos=lb.self_pos[:nd], edge_node=lb.edge_node[:ne], row_scan=lb.row_scan[:nd + 1],
-                _c=lb.cblock))
+                _c=lb.cblock, counts=lb.counts))
             seeds_n = nsrc
         if err & _lib.ERRBIT_ZEROPROB:
             raise ValueError("inclusion probability is zero for a cached draw")

@@ -867,18 +867,190 @@ def test_graphed_trainer_matches_eager(P, S):
     wg, bg_ = tr.model.export()
     for a, b in zip(we + be, wg + bg_):
         np.testing.assert_allclose(a, b, rtol=1e-2, atol=1e-4)
-    # a second epoch re-draws the cache in place (the captured graphs stay
-    # valid) and keeps tracking the eager pool (which builds a new cache)
-    ref2 = [float(eager.train_step(it.minibatch, g, tc)) for it in pool.iter_epoch(1)]
-    execs = dict(tr._execs)
-    losses2 = []
-    n2 = tr.run_epoch(1, on_step=lambda e, i, k: losses2.append(tr.loss_value()))
-    assert n2 == len(losses)
-    assert tr._execs.keys() == execs.keys() and all(tr._execs[k][1].value == execs[k][1].value for k in execs)
-    assert tr.cache.epoch == 1 and pool.cache.epoch == 1
-    assert torch.equal(tr.cache.nodes.ids, pool.cache.nodes.ids)
-    assert torch.equal(tr.cache.cached_indices, pool.cache.cached_indices)
-    np.testing.assert_allclose(losses2, ref2, rtol=2e-3)
+    # epochs 1 and 2 re-draw the cache (double-buffered: epoch 1's cache is
+    # prefetched into the second set during epoch 0, epoch 2's back into the
+    # first) and keep tracking the eager pool (which builds a new cache);
+    # epoch 2 replays the first set's graphs without re-capturing
+    for epoch in (1, 2):
+        ref2 = [float(eager.train_step(it.minibatch, g, tc)) for it in pool.iter_epoch(epoch)]
+        execs = {k: v[1].value for k, v in tr._execs.items()}
+        losses2 = []
+        n2 = tr.run_epoch(epoch, on_step=lambda e, i, k: losses2.append(tr.loss_value()))
+        assert n2 == len(losses)
+        assert tr.refresh_log[-1] == (epoch, "prefetched")
+        if epoch == 2:
+            assert {k: v[1].value for k, v in tr._execs.items()} == execs
+        assert tr.cache.epoch == epoch and pool.cache.epoch == epoch
+        assert torch.equal(tr.cache.nodes.ids, pool.cache.nodes.ids)
+        assert torch.equal(tr.cache.cached_indices, pool.cache.cached_indices)
+        np.testing.assert_allclose(losses2, ref2, rtol=2e-3)
+
+
+def _engine_graph(P, og, dim=16, classes=5, train=0.6, seed=0):
+    rng = np.random.default_rng(seed)
+    feats = rng.normal(size=(og.num_nodes, dim)).astype(np.float32)
+    labels = rng.integers(0, classes, og.num_nodes).astype(np.int32)
+    mask = rng.random(og.num_nodes) < train
+    og2 = O.OGraph(num_nodes=og.num_nodes, indptr=og.indptr, indices=og.indices, features=feats, labels=labels,
+                   train_mask=mask)
+    return og2, P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices, features=feats, labels=labels,
+                                   train_mask=mask)
+
+
+@pytest.mark.parametrize("S,period", [(1, 1), (2, 1), (2, 2)])
+def test_engine_epoch_slots_bit_exact_vs_oracle(P, S, period):
+    """Every batch the captured engine trains on — read back from its sampler
+    slot buffers — is bit-identical to the oracle restatement of
+    sampling.py:299-336 on the same (seed, epoch, index) Philox key, the
+    Feistel epoch partition (pool.py:60-66) and the epoch's cache
+    (pool.py:133-135, double-buffered / prefetched), over 3 epochs."""
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    og, g = _engine_graph(P, _hub_graph(5000, 29), train=0.5)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=400, cache_frac=0.03,
+                          cache_mode="degree", cache_period=period, seed=5)
+    tr = GraphedTrainer(g, cfg, (16, 32, 32, 5), P.TrainConfig(), seed=0, steps_per_graph=S)
+    cs = O.cache_size_for(og, cfg.cache_frac)
+    w = O.degree_probs(og)
+    seen = []
+    for epoch in range(3):
+        ce = epoch - epoch % period
+        oc = O.build_cache(og, w, cs, seed=cfg.seed, epoch=ce)
+        batches = O.epoch_targets(og, cfg.batch_size, cfg.seed, epoch)
+
+        def check(e, index, k):
+            mb = tr.slots[tr.slot_of(k)].snapshot()
+            ref = O.build_minibatch(og, oc, batches[index], cfg, O.PhiloxKeys(cfg.seed, e, index))
+            assert_mb_equal(mb, ref, f"S{S} e{e} i{index}")
+            seen.append((e, index))
+        n = tr.run_epoch(epoch, on_step=check)
+        assert n == len(batches)
+        assert tr.cache.epoch == ce
+        assert np.array_equal(tr.cache.nodes.ids.cpu().numpy(), oc.ids)
+    assert seen == [(e, i) for e in range(3) for i in range(len(batches))]
+
+
+def test_refresh_cache_grows_cached_csr_in_place(P):
+    """a refresh whose cached CSR outgrows the buffer gets larger
+    buffers on the SAME CacheState (no stale pointers) and reports it."""
+    og = _hub_graph(4000, 31)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    probs = P.degree_probs(g)
+    st = P.build_cache(g, probs, 60, rng_seed=[0, 33, 0])
+    object.__setattr__(st, "_buf_cidx", st._buf_cidx[:3])     # force growth
+    object.__setattr__(st, "_buf_cpos", st._buf_cpos[:3])
+    from paper_2106_06150_b200 import cache as C
+    kept = C.refresh_cache(st, g, probs, 60, 1, [0, 33, 1])
+    assert kept is False and st.epoch == 1
+    fresh = P.build_cache(g, probs, 60, rng_seed=[0, 33, 1])
+    for f in ("cached_indptr", "cached_indices", "inclusion"):
+        assert torch.equal(getattr(st, f), getattr(fresh, f)), f
+    assert torch.equal(st.nodes.ids, fresh.nodes.ids)
+    c = st.cstruct()
+    assert c.cached_indices == st.cached_indices.data_ptr()
+    # and in place when it fits
+    before = st.cached_indices.data_ptr()
+    assert C.refresh_cache(st, g, probs, 60, 2, [0, 33, 2]) in (True, False)
+    fresh2 = P.build_cache(g, probs, 60, rng_seed=[0, 33, 2])
+    assert torch.equal(st.cached_indices, fresh2.cached_indices)
+    if st.cached_indices.data_ptr() == before:
+        assert st.cstruct().cached_indices == before
+
+
+def test_engine_device_errors_are_sticky(P):
+    """A zero-inclusion cached draw in an engine step raises the reference's
+    ValueError (sampling.py:255-256) at the end of the run, even though the
+    failing batch's slot has been re-sampled since."""
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    og, g = _engine_graph(P, _hub_graph(3000, 37))
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=200, cache_frac=0.05, cache_mode="degree",
+                          seed=1)
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), P.TrainConfig(), seed=0)
+    tr.run_epoch(0, max_steps=2)
+    tr.cache.inclusion.zero_()        # same buffer the captured steps read
+    with pytest.raises(ValueError, match="inclusion probability is zero"):
+        tr.run_epoch(0, first=2, max_steps=4)
+    tr.check_errors()                 # cleared once raised
+
+
+def test_engine_rejects_out_of_range_labels(P):
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    og, g = _engine_graph(P, _hub_graph(2000, 3), classes=7)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(5,), batch_size=100, cache_mode="degree")
+    with pytest.raises(ValueError, match="label out of range"):
+        GraphedTrainer(g, cfg, (16, 5), P.TrainConfig())
+    m = P.GraphSAGE((16, 5))
+    mb = P.build_minibatch(g, P.build_cache(g, P.degree_probs(g), 20), np.arange(50), cfg, P.BatchRng())
+    with pytest.raises(ValueError, match="label out of range"):
+        m.train_step(mb, g, P.TrainConfig())
+
+
+def test_engine_padded_data_parallel_schedule(P):
+    """World size 2, rank 1 with an odd batch count: ceil(nb/2) steps, the
+    last one on an empty batch (zero loss, zero gradient)."""
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    og, g = _engine_graph(P, _hub_graph(3000, 41), train=0.5)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=300, cache_frac=0.05, cache_mode="degree",
+                          seed=2)
+    nb = -(-int(og.train_mask.sum()) // 300)
+    assert nb % 2 == 1
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), P.TrainConfig(), rank=1, world_size=2, seed=0, steps_per_graph=1)
+    sched = tr.batches(0)
+    assert len(sched) == (nb + 1) // 2 and sched[-1] is None and sched[:-1] == list(range(1, nb, 2))
+    got = []
+
+    def on(e, i, k):
+        got.append((i, tr.loss_value(), float(tr.model.grad.abs().sum())))
+    assert tr.run_epoch(0, on_step=on) == len(sched)
+    assert [i for i, _, _ in got] == sched
+    assert got[-1][1] == 0.0 and got[-1][2] == 0.0
+    assert all(l > 0 and gs > 0 for _, l, gs in got[:-1])
+
+
+def test_pool_copy_batches_are_independent(P):
+    og, g = _engine_graph(P, _hub_graph(3000, 43))
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=200, cache_frac=0.05, cache_mode="degree")
+    kept = [it.minibatch for it in P.SamplerPool(g, cfg, num_workers=2, copy=True).iter_epoch(0)]
+    views = [it.minibatch.clone() for it in P.SamplerPool(g, cfg, num_workers=2).iter_epoch(0)]
+    assert len(kept) == len(views) > 2
+    for a, b in zip(kept, views):
+        for ba, bb in zip(a.blocks, b.blocks):
+            assert torch.equal(ba.edge_src, bb.edge_src) and torch.equal(ba.src_nodes, bb.src_nodes)
+    # a cloned batch trains like the slot view it was copied from
+    m1, m2 = P.GraphSAGE((16, 32, 5), seed=0), P.GraphSAGE((16, 32, 5), seed=0)
+    l1 = float(m1.train_step(kept[0], g, P.TrainConfig()))
+    l2 = float(m2.train_step(views[0], g, P.TrainConfig()))
+    assert l1 == l2
+
+
+def test_engine_captured_nccl_allreduce_world1(P, tmp_path):
+    """GNS_FORCE_DIST path: the NCCL all-reduce captured in the step graph
+    at world size 1 trains exactly like the engine without it."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2106_06150_b200 import dist as gdist
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    og, g = _engine_graph(P, _hub_graph(3000, 47))
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=200, cache_frac=0.05, cache_mode="degree",
+                          seed=6)
+    tc = P.TrainConfig()
+    base = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0)
+    ref = []
+    base.run(12, on_step=lambda e, i, k: ref.append(base.loss_value()))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0, allreduce=gdist.make_allreduce(force=True))
+        got = []
+        tr.run(12, on_step=lambda e, i, k: got.append(tr.loss_value()))
+        assert got == ref
+        assert torch.equal(tr.model.flat, base.model.flat)
+    finally:
+        dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("chunk", [0, 4096])
