@@ -1,14 +1,23 @@
 """GNS mini-batch training throughput on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config papers100m]
-                    [--impl ours|reference] [--no-cpu-baseline]
+                    [--impl ours|reference] [--precision tf32|fp32]
+                    [--no-cpu-baseline] [--no-extras]
 
 One step = sample one mini-batch (3-layer GNS, fanouts 15,10,5, batch 1000,
 input layer cache-only) + gather its input features + one GraphSAGE training
 step (forward, loss, backward, Adam), on a synthetic power-law graph of the
-named shape generated on the device.  N>1: one process per GPU (torchrun),
-rank r takes batches r, r+W, ... (pool.py:80 striding), NCCL gradient
-all-reduce; time = max over ranks.  Prints ONE JSON line on rank 0.
+named shape (device generator; oracle/gen.cc rebuilds the same graph bit for
+bit on the host for the CPU arm).  N>1: one process per GPU (torchrun; spawned
+by this script when WORLD_SIZE is unset), rank r takes batches r, r+W, ...
+(pool.py:80 striding, padded to equal step counts), NCCL gradient all-reduce
+captured in the step graph; time = max over ranks.  Prints ONE JSON line on
+rank 0.
+
+``--impl reference`` is the CPU arm: the reference's algorithm (oracle port
+of pool.py fork workers + the float64 trainer loop body, numpy PCG64 streams)
+on this host's cores, on the same graph (built on the host by oracle/gen.cc:
+this process never loads libgns.so or touches the GPU).
 """
 
 from __future__ import annotations
@@ -16,20 +25,20 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
 import time
 
 import numpy as np
-import torch
-import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GNS mini-batches/sec (sample+gather+train) at 1/2/4/8 B200; gather HBM GB/s"
 UNIT = "mini-batches/s"
+L2_BYTES = 126 << 20
 
 CONFIGS = {
     # name: nodes, undirected pairs drawn, feature dim, classes, train fraction, hidden, cache frac, alpha, offset
@@ -48,6 +57,7 @@ CONFIGS = {
 }
 FANOUTS = (15, 10, 5)
 BATCH = 1000
+BLOCK_FIELDS = ("dst_nodes", "src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached", "dst_degree")
 
 
 def load_peaks():
@@ -104,24 +114,103 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def workload_config(name, c, nodes, edges, world):
+    """The ``config`` object of both arms (identical for the same workload)."""
+    ld = (c["dim"] + 3) // 4 * 4
+    resident = nodes * ld * 4 + edges * 4 + (nodes + 1) * 8
+    l2 = ("inputs larger than L2 (feature table + CSR >> 126 MB); no flush" if resident > 4 * L2_BYTES else
+          "inputs fit in L2 (feature table + CSR < 4x 126 MB): L2-resident numbers, no flush")
+    return {"workload": c["label"], "config": name, "nodes": int(nodes), "edges": int(edges),
+            "feature_dim": c["dim"], "fanouts": list(FANOUTS), "global_batch": BATCH * world,
+            "cache_frac": c["cache"], "cache_mode": "degree", "hidden": c["hidden"], "classes": c["classes"],
+            "parallelism": f"dp{world}", "l2": l2}
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+# ---------------------------------------------------------------------------
+# CPU arm (the reference algorithm on the host; no libgns, no GPU)
+# ---------------------------------------------------------------------------
+
+class RefConfig:
+    """The fields of the reference's SamplerConfig (sampling.py:80-126) the
+    oracle sampler reads."""
+
+    def __init__(self, cache_frac, seed=0):
+        self.strategy, self.fanouts, self.batch_size = "GNS", FANOUTS, BATCH
+        self.cache_frac, self.cache_period, self.cache_mode = cache_frac, 1, "degree"
+        self.input_layer_cache_only, self.seed, self.weight_policy = True, seed, "gns-paper"
+
+
+def host_reference_inputs(c, seed=0, threads=None):
+    """The bench graph rebuilt on the host (oracle/gen.cc, bit-identical to
+    the device generator) and the epoch-0 cache drawn the reference's way
+    (cache.py:87-103: numpy exponential race + argpartition, seed
+    [seed, 33, 0]; inclusion Eq. 9 on the cached ids, the only entries the
+    sampler reads, sampling.py:253; cached CSR = the full CSR filtered by the
+    cache mask, cache.py:185-197)."""
+    from oracle import detmath, gen, gns as O
+    t0 = time.perf_counter()
+    og = gen.powerlaw_graph(c["nodes"], c["pairs"], c["alpha"], c["offset"], seed, feature_dim=c["dim"],
+                            num_classes=c["classes"], train_frac=c["train"], threads=threads)
+    t1 = time.perf_counter()
+    w = O.degree_probs(og)
+    cs = O.cache_size_for(og, c["cache"])
+    ids = O.sample_cache(w, cs, numpy_seed=[seed, 33, 0])
+    mask = np.zeros(og.num_nodes, dtype=bool)
+    mask[ids] = True
+    incl = np.zeros(og.num_nodes, dtype=np.float64)
+    incl[ids] = detmath.inclusion_prob(w[ids], len(ids))
+    c_indptr, c_indices = gen.cached_csr(og.indptr, og.indices, mask, threads=threads)
+    oc = O.OCache(ids=ids, mask=mask, inclusion=incl, cached_indptr=c_indptr, cached_indices=c_indices, epoch=0)
+    return og, oc, {"graph_s": round(t1 - t0, 1), "cache_s": round(time.perf_counter() - t1, 1)}
+
+
+def reference_arm(args, name, c, world, rank):
+    """``--impl reference``: rank 0 alone, the host's cores, K timed steps
+    after W warm-up steps (the same K and W as our arm)."""
+    if rank != 0:
+        return
+    from oracle import cpu_pipeline, gns as O
+    og, oc, setup = host_reference_inputs(c)
+    cfg = RefConfig(c["cache"])
+    batches = O.epoch_targets(og, BATCH, cfg.seed, 0, numpy_mode=True)      # pool.py:60-66
+    need = args.steps + args.warmup
+    batches = (batches * (-(-need // len(batches))))[:need]
+    dims = (c["dim"], c["hidden"], c["hidden"], c["classes"])
+    r = cpu_pipeline.run(og, oc, cfg, dims, batches, epoch=0, warmup=args.warmup)
+    cores = r["workers"] + 1
+    sample = (f"{r['steps']} mini-batches of this workload after {args.warmup} warm-up (epoch 0): oracle port of "
+              f"pool.py fork workers ({r['workers']}, numpy PCG64 streams) + the float64 trainer loop body "
+              f"(model.py:279-285); sample {r['sample_ms']:.0f} ms/batch/worker, train {r['train_ms']:.0f} "
+              f"ms/batch; graph rebuilt on the host by oracle/gen.cc")
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / r["value"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(name, c, og.num_nodes, og.num_edges, world),
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup": setup, "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
 def make_graph(P, c, seed=0):
+    import torch
     t0 = time.perf_counter()
     g = P.generate_powerlaw_device(c["nodes"], c["pairs"], alpha=c["alpha"], offset=c["offset"], seed=seed,
                                    feature_dim=c["dim"], num_classes=c["classes"], train_frac=c["train"])
     torch.cuda.synchronize()
     return g, time.perf_counter() - t0
-
-
-def batch_stream(pool, start_epoch=0):
-    epoch = start_epoch
-    while True:
-        n = 0
-        for item in pool.iter_epoch(epoch):
-            n += 1
-            yield item
-        if n == 0:
-            raise RuntimeError("empty epoch")
-        epoch += 1
 
 
 def host_graph(g):
@@ -142,50 +231,50 @@ def host_cache(cache, n):
                     cached_indices=cache.cached_indices.cpu().numpy())
 
 
-def cpu_reference_run(P, g, c, cfg, cache, n_batches, warmup=1, host=None):
-    """The reference's CPU algorithm (oracle port: pool.py fork workers + the
-    float64 trainer loop body) on this host's cores."""
-    from oracle import cpu_pipeline, gns as O
-    og, oc = host if host is not None else host_inputs(g, cache)
-    batches = O.epoch_targets(og, cfg.batch_size, cfg.seed, 0, numpy_mode=True)
-    batches = batches[:n_batches + warmup]
-    dims = (c["dim"], c["hidden"], c["hidden"], c["classes"])
-    r = cpu_pipeline.run(og, oc, cfg, dims, batches, epoch=0, warmup=warmup)
-    r["cores"] = r["workers"] + 1
-    return r
+def slot_blocks(tr, slot):
+    """Host copy of the batch held in an engine sampler slot (the exact
+    buffers the captured training step read)."""
+    mb = tr.slots[slot].snapshot()
+    out = []
+    for b in mb.blocks:
+        h = b.to_numpy()
+        out.append({f: getattr(h, f) for f in BLOCK_FIELDS} | {"self_pos": b.self_pos.long().cpu().numpy()})
+    return out
 
 
-def host_inputs(g, cache):
-    return host_graph(g), (host_cache(cache, g.num_nodes) if cache is not None else None)
-
-
-def full_size_parity(P, g, cfg, cache, og, oc, n_batches=1):
-    """One mini-batch of the bench workload sampled on the device (libgns)
-    and by the oracle restatement of the reference (Philox keys): every block
-    field must be bit-identical."""
+def engine_parity(og, oc, cfg, kept):
+    """``kept``: [(epoch, index, targets or None, blocks)] read from the
+    engine's slots after the timed runs.  Each must equal the oracle's
+    build_minibatch (sampling.py:299-336 restated) on the same Philox key
+    (seed, epoch, index) and the same targets (the Feistel epoch slice,
+    pool.py:60-66, or the host's target array) — every block field and the
+    relabel map self_pos, bit for bit."""
     from oracle import gns as O
-    fields = ("dst_nodes", "src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached", "dst_degree")
-    train = np.flatnonzero(og.train_mask)
-    ok = True
-    for b in range(n_batches):
-        targets = np.random.default_rng(1000 + b).choice(train, cfg.batch_size, replace=False)
-        mb = P.build_minibatch(g, cache, targets, cfg, P.BatchRng(cfg.seed, 0, b))
-        ref = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(cfg.seed, 0, b))
-        for bg, br in zip(mb.blocks, ref.blocks):
-            h = bg.to_numpy()
-            ok &= all(np.array_equal(getattr(h, f), np.asarray(getattr(br, f))) for f in fields)
-    return {"batches": n_batches, "bit_exact": bool(ok), "fields": list(fields),
-            "vs": "oracle restatement of sampling.py:189-336 with the same Philox keys, full-size graph"}
+    perms = {}
+    ok, checked = True, []
+    for epoch, index, targets, blocks in kept:
+        if targets is None:
+            if epoch not in perms:
+                perms[epoch] = O.epoch_targets(og, cfg.batch_size, cfg.seed, epoch)
+            targets = perms[epoch][index]
+        ref = O.build_minibatch(og, oc, targets, cfg, O.PhiloxKeys(cfg.seed, epoch, index))
+        same = len(ref.blocks) == len(blocks)
+        for b, r in zip(blocks, ref.blocks):
+            same &= all(np.array_equal(b[f], np.asarray(getattr(r, f))) for f in BLOCK_FIELDS)
+            same &= np.array_equal(b["self_pos"], np.searchsorted(np.asarray(r.src_nodes), np.asarray(r.dst_nodes)))
+        ok &= bool(same)
+        checked.append({"epoch": epoch, "index": index, "bit_exact": bool(same),
+                        "edges": int(sum(len(b["edge_src"]) for b in blocks))})
+    return ok, checked
 
 
 def gather_microbench(tr, D, reps=24):
     """features[input_nodes] (model.py:146) through gns_gather_rows on the
     input nodes of the batches currently held in the engine's sampler slots;
     a 256 MB copy between launches flushes L2.  Returns [(bytes, ms)]."""
+    import torch
     from paper_2106_06150_b200 import _lib
     L = len(FANOUTS)
-    # the engine's last replay may still be sampling into a slot on its side
-    # stream: settle every stream before reading the slots' device counts
     torch.cuda.synchronize()
     sets = []
     for sl in tr.slots:
@@ -195,8 +284,6 @@ def gather_microbench(tr, D, reps=24):
             sets.append((b0.src_nodes, b0.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1], n))
     tab = tr.g.features
     out = torch.empty((max(n for _, _, n in sets), D), dtype=torch.float32, device=tab.device)
-    # L2 flush: copy 256 MB of random bytes (a constant memset can be
-    # absorbed without displacing L2 lines; a real read+write stream cannot)
     flush = torch.randint(0, 256, (256 << 20,), dtype=torch.uint8, device=tab.device)
     scratch = torch.empty_like(flush)
     s = torch.cuda.current_stream()
@@ -215,6 +302,99 @@ def gather_microbench(tr, D, reps=24):
     return res
 
 
+def kernel_line(name, nbytes, ms, peak, peak_kind, how, step_ms=None):
+    gbs = float(np.sum(nbytes) / (np.sum(ms) / 1e3) / 1e9)
+    d = {"kernel": name, "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "peak_kind": peak_kind,
+         "unit": "GB/s", "frac": round(gbs / peak, 4), "traffic": None,
+         "algorithmic_bytes_per_launch": float(np.mean(nbytes)), "avg_launch_ms": float(np.mean(ms)),
+         "measured": how}
+    if step_ms:
+        d["share_of_step"] = float(np.mean(ms) / step_ms)
+    return d
+
+
+def sampler_throughput(P, tr, g, cfg, n_batches=24):
+    """The sampling branch alone (K5 sampler + K6 dedup/relabel, all layers of
+    one mini-batch) on one stream, batch after batch: mini-batches/s and
+    sampled edges/s (north star), plus the bytes lower bound of SURVEY.md
+    §8(d) (seed offsets, the sampled edges' output, relabel reads/writes)."""
+    import torch
+    from paper_2106_06150_b200 import _lib
+    from paper_2106_06150_b200.sampling import MiniBatchSampler
+    sl = MiniBatchSampler(g, cfg)
+    perm = tr.epoch_perm
+    nb = perm.numel() // cfg.batch_size
+    # one gns_step_t per batch, on the device before the timed chain starts
+    steps = torch.zeros((n_batches + 2, 4), dtype=torch.int64)
+    for it in range(n_batches + 2):
+        idx = (it * 7) % nb
+        steps[it, 0] = (cfg.seed & 0xFFFFFFFF) | ((tr._perm_epoch & 0xFFFFFFFF) << 32)
+        steps[it, 1], steps[it, 2], steps[it, 3] = idx, idx * cfg.batch_size, cfg.batch_size
+    steps = steps.to(g.device)
+    s = torch.cuda.Stream(device=g.device)
+    cache = tr.cache
+    edges = seeds = srcs = 0
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        for it in range(n_batches + 2):
+            if it == 2:
+                t0.record(s)
+            sl.enqueue_device(None, steps[it], cache, epoch_perm=perm)
+        t1.record(s)
+    t1.synchronize()
+    ms = t0.elapsed_time(t1) / n_batches
+    # counts of the last batch (representative; every batch is ~the same size)
+    c = sl.counts.cpu().numpy()
+    for layer in range(len(cfg.fanouts)):
+        edges += int(c[layer][_lib.CNT_EDGES])
+        seeds += int(c[layer][_lib.CNT_DST])
+        srcs += int(c[layer][_lib.CNT_SRC])
+    # lower bound (SURVEY §8(d) K5 + K6): indptr + cached_indptr per seed,
+    # per-edge output (src id, row, fp64 weight, flag = 17 B), relabel:
+    # 4 (E + seeds) read + 4 src + 4 E written
+    nbytes = 16 * seeds + 17 * edges + 4 * (edges + seeds) + 4 * srcs + 4 * edges
+    return {"ms_per_batch": round(ms, 4), "mini_batches_per_s": round(1e3 / ms, 1),
+            "sampled_edges_per_batch": edges, "sampled_edges_per_s": round(edges / (ms / 1e3), 1),
+            "bytes_lower_bound_per_batch": nbytes, "achieved_gbs_lower_bound": round(nbytes / (ms / 1e3) / 1e9, 1),
+            "how": f"one sampler chain (gns_batch_slice_sorted + 3 x gns_sample_layer), {n_batches} batches back to "
+                   "back on one stream, CUDA events; the engine runs it concurrently with training on a "
+                   "low-priority branch"}
+
+
+def refresh_timing(P, tr, g, reps=3):
+    """Per-epoch cache refresh at full size (K1-K3: exponential-race draw over
+    N nodes, Eq. 9 inclusion, cached CSR by filtering all E entries) into a
+    spare cache set, CUDA events.  Algorithmic bytes per SURVEY.md §8(d):
+    4N (deg) + 8N (keys) + 4E (scan indices) + 8N (cached indptr) + 4 nnz_C."""
+    import torch
+    from paper_2106_06150_b200 import cache as C
+    st = C.empty_like(tr.cache, g)
+    probs = tr._probs
+    cs = tr._cache_size()
+    res = []
+    for r in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        C.refresh_cache(st, g, probs, cs, 100 + r, [tr.cfg.seed, 33, 100 + r])
+        e1.record()
+        e1.synchronize()
+        if r:
+            res.append(e0.elapsed_time(e1))
+    n, E = g.num_nodes, g.num_edges
+    nnz = int(st.cached_indices.numel())
+    nbytes = 4 * n + 8 * n + 4 * E + 8 * n + 4 * nnz
+    ms = float(np.mean(res))
+    del st
+    return {"ms": round(ms, 3), "algorithmic_bytes": nbytes, "gbs": round(nbytes / (ms / 1e3) / 1e9, 1),
+            "cache_size": cs, "cached_csr_nnz": nnz,
+            "how": "cache.refresh_cache (gns_cache_draw + gns_inclusion + gns_cached_csr_count/fill) into a spare "
+                   "set, host-synchronised (the engine prefetches it on a low-priority stream during the "
+                   "previous epoch instead)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -222,60 +402,62 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default=os.environ.get("GNS_BENCH_CONFIG", "papers100m"), choices=list(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
+                    help="GEMM precision of the headline engine (the sampler, gather, SpMMs, loss and Adam are "
+                         "fp32/int either way); fp32 and fp64 lines are added at N=1 unless --no-extras")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the precision / epoch / mixed / sampler extras")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--workers", type=int, default=2, help="sampling slots in flight (SamplerPool num_workers)")
     args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: re-launch under torchrun (127.0.0.1 rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    c = CONFIGS[args.config]
-
-    if args.impl == "reference" and rank != 0:
+    name = args.config
+    c = CONFIGS[name]
+    if args.impl == "reference":
+        reference_arm(args, name, c, world, rank)
         return
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: refusing to report n_gpus != N")
+    ours_arm(args, name, c, world, rank, local)
+
+
+def ours_arm(args, name, c, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
     import paper_2106_06150_b200 as P
     from paper_2106_06150_b200 import _lib
-
     from paper_2106_06150_b200 import dist as gdist
+    from paper_2106_06150_b200.engine import GraphedTrainer
+
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"rank {rank}: no CUDA device {local}")
     torch.cuda.set_device(local)
     force_dist = os.environ.get("GNS_FORCE_DIST", "0") == "1"   # captured NCCL path at N=1 (testing)
-    if (world > 1 or force_dist) and args.impl == "ours":
+    if world > 1 or force_dist:
         gdist.init_from_env("nccl")
     distributed = dist.is_initialized()
     g, gen_s = make_graph(P, c, seed=0)
     cfg = P.SamplerConfig(strategy="GNS", fanouts=FANOUTS, batch_size=BATCH, cache_frac=c["cache"],
                           cache_mode="degree", input_layer_cache_only=True, seed=0)
     dims = (c["dim"], c["hidden"], c["hidden"], c["classes"])
-    config = {"workload": c["label"], "config": args.config, "nodes": g.num_nodes, "edges": g.num_edges,
-              "feature_dim": c["dim"], "fanouts": list(FANOUTS), "global_batch": BATCH * world,
-              "cache_frac": c["cache"], "cache_mode": "degree", "hidden": c["hidden"],
-              "classes": c["classes"], "parallelism": f"dp{world}",
-              "l2": "inputs larger than L2 (feature table + CSR >> 126 MB); no flush",
-              "graph_gen_s": round(gen_s, 2)}
-
-    if args.impl == "reference":
-        pool = P.SamplerPool(g, cfg)
-        pool._refresh_cache(0)
-        n = max(1, min(args.steps, c["cpu_batches"] * 2))
-        r = cpu_reference_run(P, g, c, cfg, pool.cache, n, warmup=min(args.warmup, 1))
-        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
-               "sample": f"{r['steps']} mini-batches of the same workload (epoch 0), oracle port of pool.py "
-                         f"fork workers ({r['workers']}) + float64 trainer loop body; "
-                         f"sample {r['sample_ms']:.0f} ms/batch/worker, train {r['train_ms']:.0f} ms/batch"}
-        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
-                "steps": r["steps"], "warmup": 1, "ms_per_step": 1e3 / r["value"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-                "cpu_baseline": cpu,
-                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return
-
+    config = workload_config(name, c, g.num_nodes, g.num_edges, world)
     tc = P.TrainConfig(lr=0.003, hidden_dim=c["hidden"])
-
-    from paper_2106_06150_b200.engine import GraphedTrainer
     allreduce = gdist.make_allreduce(force=force_dist) if distributed else None
-    tr = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world, allreduce=allreduce, seed=0)
+    solo = rank == 0 and world == 1
+    extras = solo and not args.no_extras
+
+    tr = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world, allreduce=allreduce, seed=0,
+                        tf32=args.precision == "tf32")
     pos = tr.run(args.warmup, epoch=0, first=0)
     tr.prepare(args.steps)
     torch.cuda.synchronize()
@@ -284,156 +466,299 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     l0 = _lib.launch_counter[0]
+    trained = []
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(tr.main)
-    pos = tr.run(args.steps, epoch=pos[0], first=pos[1])
+    pos = tr.run(args.steps, epoch=pos[0], first=pos[1], on_step=lambda e, i, k: trained.append((e, i, k)))
     t_end.record(tr.main)
     t_end.synchronize()
     clk = clocks.stop()
     launches = _lib.launch_counter[0] - l0
-    # graph replays launch the captured kernels: count them per step
-    per_step = tr.kernels_per_step()
+    per_step = tr.kernels_per_step()     # graph replays launch the captured kernels
     launches_total = int(round(launches + per_step * args.steps))
     ms = gdist.max_over_ranks(t_start.elapsed_time(t_end), device="cuda")
     value = args.steps * world / (ms / 1e3)
+    step_ms = ms / args.steps
     tr.check_errors()
+    # the last replay's training slots still hold the batches it trained on
+    kept = []
+    if solo:
+        for e, i, k in trained[-tr.S:]:
+            if i is not None and e == 0:
+                kept.append((e, i, None, slot_blocks(tr, tr.slot_of(k))))
 
-    # per-kernel rooflines: the step graph re-captured with timing events
-    # around the input-layer kernels of the first step of each replay
-    # (gns_gather_rows + gns_spmm_fwd, or the fused gns_spmm_fwd_gather)
+    # ---- per-kernel rooflines: the step graph re-captured with CUDA events
     peak, peak_kind = load_peaks()
     tr.capture_profiled()
     nprof = min(30, args.steps) * tr.S
-    gather_ms, spmm_ms, spmm_bytes, n_in = [], [], [], []
-    D = c["dim"]
+    spmm_ms, spmm_bytes, n_in, bwd_ms, bwd_bytes = [], [], [], [], []
+    D, H = c["dim"], c["hidden"]
 
     def on_step(e, i, k):
         if k % tr.S:          # the events time the first step of each replay
             return
-        if not tr.fused_gather:
-            gather_ms.append(tr.gather_ms())
         spmm_ms.append(tr.spmm0_ms())
-        cnt = tr.slots[tr.slot_of(k)].counts[len(FANOUTS) - 1].tolist()
+        bwd_ms.append(tr.bwd1_ms())
+        sl = tr.slots[tr.slot_of(k)]
+        cnt = sl.counts[len(FANOUTS) - 1].tolist()
         n_in.append(cnt[_lib.CNT_SRC])
         nd, ne = cnt[_lib.CNT_DST], cnt[_lib.CNT_EDGES]
         # input-layer SpMM, algorithmic bytes: every
-        # distinct input row read once (n_src; a batch's repeated rows are L2
-        # hits, ncu DRAM traffic ~ this) + the cat rows written, incl. the zero
-        # padding the GEMM reads (up to the size-switched row count) +
-        # per-edge index/weight (4 + 8 B) + row scan (+ dst id, fused gather)
+        # distinct input row read once (a batch's repeated rows are L2 hits) +
+        # the cat rows written incl. the zero padding the size-switched GEMM
+        # reads + per-edge index/weight (4 + 8 B) + row scan + dst id
         C = tr.switch_chunk
         rows_w = min(tr.npad[0], -(-nd // C) * C) if tr.use_switch else tr.npad[0]
-        spmm_bytes.append(cnt[_lib.CNT_SRC] * 4 * D + rows_w * 2 * 4 * D + 12 * ne
-                          + (12 if tr.fused_gather else 8) * nd)
+        spmm_bytes.append(cnt[_lib.CNT_SRC] * 4 * D + rows_w * 2 * 4 * D + 12 * ne + 12 * nd)
+        # layer 1's transposed SpMM (K8 bwd): dcat rows (self + neighbour
+        # halves) of its dst rows, dz rows written for its src rows, 12 B/edge
+        c1 = sl.counts[len(FANOUTS) - 2].tolist()
+        bwd_bytes.append(4 * 2 * H * c1[_lib.CNT_DST] + 4 * H * c1[_lib.CNT_SRC] + 12 * c1[_lib.CNT_EDGES])
     pos = tr.run(nprof, epoch=pos[0], first=pos[1], on_step=on_step)
     n_in = np.array(n_in, dtype=np.float64)
-    gbytes = n_in * (2 * 4 * D + 4)     # rows read + rows written + int32 ids
-    if not tr.fused_gather:
-        g_ms = np.array(gather_ms)
-        g_how = f"CUDA events around the gather inside the captured step graph, {len(g_ms)} replays"
-    else:
-        g_ms, g_how = gather_microbench(tr, D), ("gns_gather_rows (reference-API gather) on the input nodes of the "
-                                                 "engine's sampled batches, CUDA events, L2 flushed between launches")
-        gbytes = np.array([gather_bytes for gather_bytes, _ in g_ms])
-        g_ms = np.array([t for _, t in g_ms])
-    gather_gbs = float(gbytes.sum() / (g_ms.sum() / 1e3) / 1e9)
-    spmm_gbs = float(np.sum(spmm_bytes) / (np.sum(spmm_ms) / 1e3) / 1e9)
-    gather_k = {"kernel": "gns_gather_rows (gather_f32x4_kernel)", "bound": "hbm", "achieved": round(gather_gbs, 1),
-                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gather_gbs / peak, 4),
-                "traffic": None, "algorithmic_bytes_per_launch": float(gbytes.mean()),
-                "avg_launch_ms": float(g_ms.mean()), "measured": g_how}
-    spmm_name = "gns_spmm_fwd_gather (input layer, fused feature gather)" if tr.fused_gather else \
-        "gns_spmm_fwd (input layer)"
-    spmm_k = {"kernel": spmm_name, "bound": "hbm", "achieved": round(spmm_gbs, 1), "peak": peak,
-              "peak_kind": peak_kind, "unit": "GB/s", "frac": round(spmm_gbs / peak, 4), "traffic": None,
-              "algorithmic_bytes_per_launch": float(np.mean(spmm_bytes)), "avg_launch_ms": float(np.mean(spmm_ms)),
-              "share_of_step": float(np.mean(spmm_ms) / (ms / args.steps)),
-              "measured": f"CUDA events around the kernel inside the captured step graph, {len(spmm_ms)} replays"}
-    if not tr.fused_gather:
-        gather_k["share_of_step"] = float(g_ms.mean() / (ms / args.steps))
-    # the dominant HBM kernel of the step: the fused gather+aggregate when the
-    # gather is fused, else the gather (as in round 1)
-    roofline = spmm_k if tr.fused_gather else gather_k
-    kernels = {"gns_gather_rows": gather_k, "gns_spmm_fwd (input layer)": spmm_k}
+    g_res = gather_microbench(tr, D)
+    spmm_k = kernel_line("gns_spmm_fwd_gather (input layer: feature gather fused with the mean aggregation)",
+                         spmm_bytes, spmm_ms, peak, peak_kind,
+                         f"CUDA events around the kernel inside the captured step graph, {len(spmm_ms)} replays",
+                         step_ms)
+    bwd_k = kernel_line("gns_spmm_bwd_transposed_bits (model layer 1 backward, hidden 256)", bwd_bytes, bwd_ms,
+                        peak, peak_kind, f"CUDA events inside the captured step graph, {len(bwd_ms)} replays",
+                        step_ms)
+    gather_k = kernel_line("gns_gather_rows (reference-API gather features[input_nodes], gather_f32x4_kernel)",
+                           [b for b, _ in g_res], [t for _, t in g_res], peak, peak_kind,
+                           "standalone on the input nodes of the engine's sampled batches, CUDA events, L2 flushed "
+                           "(256 MB copy) between launches")
+    kernels = {"spmm_fwd_gather": spmm_k, "spmm_bwd_transposed": bwd_k, "gather_rows": gather_k}
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_path):
         try:
-            tj = json.load(open(prof_path)).get(args.config, {})
-            for kk, name in ((gather_k, "gather_f32x4_kernel"), (spmm_k, "spmm_fwd_gather" if tr.fused_gather
-                                                                     else "spmm_fwd_kernel")):
-                if tj.get(name):
-                    kk["traffic"] = tj[name]
+            tj = json.load(open(prof_path)).get(name, {})
+            for kk, key in ((gather_k, "gather_f32x4_kernel"), (spmm_k, "spmm_fwd_gather"),
+                            (bwd_k, "spmm_bwd_transposed")):
+                if tj.get(key):
+                    kk["traffic"] = tj[key]
         except Exception:
             pass
-    pool = tr
+    roofline = spmm_k
 
-    # end-to-end through the public API with host buffers: targets from pinned
-    # host memory every step (read by a copy kernel in the graph), every
-    # step's loss back in pinned host memory and read by the host; the timed
-    # run_host call includes its eager prologue (sampling the first batch)
+    extra = {}
+    if extras:
+        extra["sampler"] = sampler_throughput(P, tr, g, cfg)
+        extra["cache_refresh"] = refresh_timing(P, tr, g)
+        # a window of whole epochs including their boundaries: the epoch
+        # permutation (gns_epoch_targets) and the cache refresh of every
+        # epoch (pool.py:133-135; prefetched into the idle set during the
+        # previous epoch) are inside the timed region
+        tr._free_execs()          # the profiled graphs carry events
+        tr._prof_events = None
+        # two untimed epochs capture the step graphs of both cache sets (the
+        # double buffer alternates sets at every refresh)
+        e0 = pos[0] + 1
+        nsteps = 2 * len(tr.batches(e0))
+        tr.run(nsteps, epoch=e0, first=0)
+        e0 += 2
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(tr.main)
+        tr.run(nsteps, epoch=e0, first=0)
+        a1.record(tr.main)
+        a1.synchronize()
+        wall = time.perf_counter() - w0
+        extra["epochs"] = {"epochs": [e0, e0 + 1], "steps": nsteps, "wall_s": round(wall, 4),
+                           "mini_batches_per_s": round(nsteps / wall, 1),
+                           "device_ms_per_step": round(a0.elapsed_time(a1) / nsteps, 4),
+                           "refreshes": [x for x in tr.refresh_log if x[0] >= e0],
+                           "how": "GraphedTrainer.run over two whole epochs from the first batch: every step, the "
+                                  "epoch permutations and both epoch-start cache refreshes inside the window "
+                                  "(host wall clock, incl. graph re-captures when a refreshed cached CSR outgrew "
+                                  "its buffer)"}
+    S, prio = tr.S, tr.prio_mode
+    del tr
+    torch.cuda.empty_cache()
+
+    # ---- end to end through the public API with host buffers: targets from
+    # pinned host memory every step (read by a copy kernel in the graph), every
+    # step's loss back in pinned host memory and read by the host
     e2e = None
     k2 = args.e2e_steps if args.e2e_steps is not None else max(5, args.steps)
-    if k2 > 0:
-        ids_host = g.train_ids().cpu().numpy().astype(np.int64)
-        perm = np.random.default_rng(1).permutation(ids_host)
-        nb = len(perm) // BATCH
-        te = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world, allreduce=allreduce, seed=0,
-                            host_targets=True)
-        # warm-up: captures both graph parities and brings the clocks back up
-        # after the host-only parity check (a cold start skews a short run)
+    ids_host = g.train_ids().cpu().numpy().astype(np.int64)
+    perm = np.random.default_rng(1).permutation(ids_host)
+    nbh = len(perm) // BATCH
+
+    def run_e2e(te, k2, tag):
         nw = 4 * te.S * max(1, 48 // (4 * te.S))
         k2 = -(-k2 // te.S) * te.S   # whole replays in the timed region
         # rank r's host batches: r, r+W, ... of the permutation (pool.py:80)
-        batches = [perm[((j * world + rank) % nb) * BATCH:((j * world + rank) % nb + 1) * BATCH]
+        batches = [perm[((j * world + rank) % nbh) * BATCH:((j * world + rank) % nbh + 1) * BATCH]
                    for j in range(k2 + nw)]
-        te.cache = tr.cache
         te.run_host(batches[:nw], epoch=0)
         torch.cuda.synchronize()
         if distributed:
             dist.barrier()
         w0 = time.perf_counter()
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(te.main)
         te.run_host(batches[nw:], epoch=0)
         s1.record(te.main)
         s1.synchronize()
         wall = gdist.max_over_ranks(time.perf_counter() - w0, device="cuda")
-        e2e = {"value": k2 * world / wall, "unit": UNIT, "h2d_bytes_per_step": BATCH * 4 + 4 + 32,
-               "d2h_bytes_per_step": 8, "steps": k2,
-               "path": "GraphedTrainer(host_targets=True).run_host: pinned host targets read by a copy kernel in "
-                       "the step graph, every step's loss written to pinned host memory by the graph and read "
-                       "by the host one replay late; wall clock, max over ranks",
-               "device_ms_per_step": s0.elapsed_time(s1) / k2}
+        got = []
+        if solo:   # the last replay's slots: its batches k2-S .. k2-1 (Philox batch = position)
+            for k in range(k2 - te.S, k2):
+                got.append((0, k, batches[nw + k], slot_blocks(te, te.slot_of(k))))
+        return {"value": k2 * world / wall, "unit": UNIT, "h2d_bytes_per_step": BATCH * 4 + 4 + 32,
+                "d2h_bytes_per_step": 8, "steps": k2, "device_ms_per_step": s0.elapsed_time(s1) / k2,
+                "path": f"GraphedTrainer(host_targets=True{tag}).run_host: pinned host targets read by a copy kernel "
+                        "in the step graph, every step's loss written to pinned host memory by the graph and read "
+                        "by the host one replay late; wall clock, max over ranks"}, got
+
+    cache0 = None
+    if k2 > 0:
+        te = GraphedTrainer(g, cfg, dims, tc, rank=rank, world_size=world, allreduce=allreduce, seed=0,
+                            host_targets=True, tf32=args.precision == "tf32")
+        te._begin(0)
+        cache0 = te.cache
+        e2e, got = run_e2e(te, k2, "")
+        kept += got
         del te
+    torch.cuda.empty_cache()
+
+    precisions = None
+    if extras and k2 > 0:
+        precisions = {args.precision: {"value": round(value, 3), "ms_per_step": round(step_ms, 4),
+                                       "e2e": round(e2e["value"], 3)}}
+        other = "fp32" if args.precision == "tf32" else "tf32"
+        t2 = GraphedTrainer(g, cfg, dims, tc, seed=0, host_targets=True, tf32=other == "tf32")
+        t2.cache = cache0
+        e2b, _ = run_e2e(t2, k2, f", tf32={other == 'tf32'}")
+        precisions[other] = {"e2e": round(e2b["value"], 3), "device_ms_per_step": round(e2b["device_ms_per_step"], 4),
+                             "how": "same engine, GEMMs " + ("TF32 tensor cores" if other == "tf32" else
+                                                            "full fp32 (no TF32)")}
+        del t2
+        torch.cuda.empty_cache()
+        precisions["fp64"] = fp64_e2e(P, g, cfg, dims, tc, cache0, perm, min(k2, 40))
+
+    mixed = None
+    if extras and os.environ.get("GNS_BENCH_MIXED", "1") == "1":
+        mixed = mixed_placement(P, g, cfg, dims, tc, cache0, min(args.steps, 200), args.warmup)
 
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        host = host_inputs(g, pool.cache)
-        parity = full_size_parity(P, g, cfg, pool.cache, *host)
-        r = cpu_reference_run(P, g, c, cfg, pool.cache, c["cpu_batches"], host=host)
-        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+    if solo and not args.no_cpu_baseline:
+        og, oc = host_graph(g), host_cache(cache0, g.num_nodes)
+        ok, checked = engine_parity(og, oc, cfg, kept)
+        parity = {"batches": len(checked), "bit_exact": bool(ok), "fields": list(BLOCK_FIELDS) + ["self_pos"],
+                  "checked": checked,
+                  "vs": "the engine's sampler-slot buffers of the last trained batches (device-timed run: Feistel "
+                        "epoch slices; end-to-end run: host target arrays) vs the oracle restatement of "
+                        "sampling.py:299-336 on the same (seed, epoch, batch) Philox keys, full-size graph"}
+        from oracle import cpu_pipeline, gns as O
+        batches = O.epoch_targets(og, BATCH, 0, 0, numpy_mode=True)[:c["cpu_batches"] + 1]
+        r = cpu_pipeline.run(og, oc, cfg, dims, batches, epoch=0, warmup=1)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["workers"] + 1, "kind": "port",
                "sample": f"{r['steps']} mini-batches of this workload (epoch 0, after 1 warm-up), oracle port "
                          f"of pool.py fork workers ({r['workers']}) + float64 trainer loop body; sample "
                          f"{r['sample_ms']:.0f} ms/batch/worker, train {r['train_ms']:.0f} ms/batch"}
 
     if rank == 0:
+        dtype = {"tf32": "tf32", "fp32": "f32"}[args.precision]
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
-                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
-                "gpu_launches": launches_total,
+                "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+                "precision_detail": "sampler ids int32, weights/inclusion f64 (bit-exact to the reference); gather, "
+                                    "SpMMs, loss, Adam f32; linear-layer GEMMs " +
+                                    ("TF32 tensor cores (fp32 accumulate)" if args.precision == "tf32" else "fp32"),
+                "data": "synthetic", "config": config, "roofline": roofline, "kernels": kernels,
+                "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "precisions": precisions,
+                "mixed_placement": mixed, "gpu_launches": launches_total,
                 "gpu_launches_per_step": launches_total / args.steps, "clocks": clk,
-                "per_step": {"input_nodes": float(n_in.mean()), "gather_ms": float(g_ms.mean()),
-                             "fused_gather": tr.fused_gather,
-                             "graph_replays": -(-args.steps // tr.S), "steps_per_graph": tr.S,
-                             "step_priority": tr.prio_mode}}
+                "setup": {"graph_gen_s": round(gen_s, 2)},
+                "per_step": {"input_nodes": float(n_in.mean()), "fused_gather": True,
+                             "graph_replays": -(-args.steps // S), "steps_per_graph": S,
+                             "step_priority": prio}} | extra
         print(json.dumps(line), flush=True)
     if distributed:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def fp64_e2e(P, g, cfg, dims, tc, cache, perm, steps):
+    """The reference-parity precision end to end through the reference-API
+    façade: build_minibatch(host targets) + GraphSAGE(float64).train_step
+    (fp64 gather, the bit-exact fp64 SpMM, fp64 GEMMs, fp64 loss and Adam) +
+    the loss read back, per step (model.py:279-285 loop body)."""
+    import torch
+    model = P.GraphSAGE(dims, dtype=torch.float64, seed=0)
+    nb = len(perm) // BATCH
+    batches = [perm[(j % nb) * BATCH:(j % nb + 1) * BATCH] for j in range(steps + 3)]
+    for j in range(3):
+        float(model.train_step(P.build_minibatch(g, cache, batches[j], cfg, P.BatchRng(0, 0, j)), g, tc))
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    for j in range(3, steps + 3):
+        mb = P.build_minibatch(g, cache, batches[j], cfg, P.BatchRng(0, 0, j))
+        float(model.train_step(mb, g, tc))
+    wall = time.perf_counter() - w0
+    return {"e2e": round(steps / wall, 3), "steps": steps, "dtype": "f64",
+            "how": "eager reference-API path: P.build_minibatch(g, cache, host targets, cfg, BatchRng) + "
+                   "GraphSAGE(dtype=float64).train_step + float(loss) per step (fp64 GEMMs, bit-exact fp64 SpMM); "
+                   "wall clock — the like-for-like precision of the float64 reference"}
+
+
+def mixed_placement(P, g, cfg, dims, tc, cache, steps, warmup):
+    """North-star subsystem 1 / paper §3.1: the feature table in pinned host
+    memory; the cached rows refreshed into an HBM table (gns_cache_refresh_rows
+    over the host link) and read from HBM, uncached input rows read over the
+    host link by the mixed gather (gns_gather_rows_mixed)."""
+    import torch
+    from paper_2106_06150_b200 import _lib
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    t0 = time.perf_counter()
+    hf = torch.empty(tuple(g.features.shape), dtype=torch.float32, pin_memory=True)
+    hf.copy_(g.features)
+    pin_s = time.perf_counter() - t0
+    tm = GraphedTrainer(g, cfg, dims, tc, seed=0, feature_placement="mixed", host_features=hf)
+    # feature refresh over the host link, timed alone
+    tm.cache = cache
+    torch.cuda.synchronize()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record()
+    tm._fill_table(tm.cur, torch.cuda.current_stream())
+    r1.record()
+    r1.synchronize()
+    refresh_ms = r0.elapsed_time(r1)
+    ld = g.features.shape[1]
+    refresh_bytes = cache.nodes.ids.numel() * ld * 4
+    pos = tm.run(warmup, epoch=0)
+    tm.prepare(steps)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(tm.main)
+    host_rows = []
+    tm.run(steps, epoch=pos[0], first=pos[1])
+    s1.record(tm.main)
+    s1.synchronize()
+    ms = s0.elapsed_time(s1) / steps
+    # input rows read over the host link per step (the uncached ones), from the
+    # slots of the last replay
+    for sl in tm._group(0) + tm._group(1):
+        mb = tm.slots[sl].snapshot()
+        ids = mb.input_nodes
+        if ids.numel():
+            host_rows.append(int((~cache.nodes.contains(ids)).sum()))
+    rows = float(np.mean(host_rows)) if host_rows else 0.0
+    del tm, hf
+    torch.cuda.empty_cache()
+    return {"mini_batches_per_s": round(1e3 / ms, 1), "ms_per_step": round(ms, 4), "steps": steps,
+            "host_rows_per_step": rows, "host_link_gbs": round(rows * ld * 4 / (ms / 1e3) / 1e9, 2),
+            "feature_refresh": {"ms": round(refresh_ms, 3), "bytes": refresh_bytes,
+                                "gbs": round(refresh_bytes / (refresh_ms / 1e3) / 1e9, 2)},
+            "pin_s": round(pin_s, 1),
+            "how": "GraphedTrainer(feature_placement='mixed'): 57 GB feature table in pinned host memory; cached "
+                   "rows in an HBM table refreshed from host at each cache refresh; uncached input rows read over "
+                   "the host link by the gather inside the step graph; device-timed"}
 
 
 if __name__ == "__main__":

@@ -478,6 +478,17 @@ GNS_API int gns_gen_powerlaw_count(int64_t num_nodes, int64_t num_pairs, double 
 GNS_API int gns_gen_powerlaw_fill(int64_t num_nodes, int64_t num_pairs, const int64_t* indptr,
                           int32_t* out_indices, void* ws, size_t ws_bytes, void* stream);
 
+/* Node attributes of the synthetic graphs (graph.py:249-253 scheme), pure
+ * functions of (seed, node) so oracle/gen.c rebuilds them bit for bit:
+ * labels in [0, num_classes), train/val/test masks (uniform r < train_frac,
+ * then halves of the rest), and class-mean + noise float32 features
+ * [n, ld] (columns >= dim zero; class_means = caller scratch [classes, ld]). */
+GNS_API int gns_gen_node_attrs(int64_t n, int32_t num_classes, double train_frac, uint32_t seed,
+                               int32_t* labels, uint8_t* train, uint8_t* val, uint8_t* test, void* stream);
+GNS_API int gns_gen_features(int64_t n, int32_t dim, int32_t ld, int32_t num_classes, float noise,
+                             uint32_t seed, const int32_t* labels, float* class_means, float* out,
+                             void* stream);
+
 /* build_csr (graph.py:142-169) on the device from caller-given endpoint arrays
  * (int32 u[m], v[m], all in [0, num_nodes)): symmetrise, drop self loops and
  * duplicates, sort rows.  Same two phases / workspace as the generator. */

@@ -17,6 +17,6 @@ node, position).  The oracle restates the reference with the build's Philox
 keys injected through the reference's own duck-typed ``rng.random(n)`` hook
 (``sampling.py:166,214,233``).  It is pinned against the reference itself by
 replaying the oracle's key arrays into ``gnsbench.build_minibatch``
-(``tests/test_oracle_pin.py``) and by golden fixtures generated from the
+(``tests/test_oracle.py::test_oracle_numpy_stream_equals_reference``) and by golden fixtures generated from the
 reference (``tests/golden/make_golden.py``).
 """

@@ -6,10 +6,10 @@ The reference evaluates ``np.log`` (inside numpy's exponential draw,
 ``cache.py:101``) and ``np.log1p``/``np.expm1`` (Eq. 9, ``cache.py:115``) with
 the platform libm.  libm and CUDA's libdevice may disagree in the last ulp, so
 the build defines these three functions as fixed sequences of correctly
-rounded IEEE operations (no FMA).  ``paper_2106_06150_b200/csrc/gns_detmath.cuh``
+rounded IEEE operations (no FMA).  ``paper_2106_06150_b200/csrc/gns_common.cuh``
 evaluates the *same* sequence with ``__dadd_rn``/``__dmul_rn``/``__ddiv_rn``,
 which makes GPU and oracle bit-identical by construction; the functions are
-checked against numpy's libm to a few ulp in ``tests/test_oracle_detmath.py``.
+checked against numpy's libm to a few ulp in ``tests/test_oracle.py::test_detmath_close_to_libm``.
 """
 
 from __future__ import annotations
@@ -96,3 +96,17 @@ def inclusion_prob(p, cache_size: int):
     out = -det_expm1(float(cache_size) * det_log1p(-np.minimum(p, ONE_MINUS_1EM15)))
     out = np.where(p >= 1.0, 1.0 if cache_size >= 1 else 0.0, out)
     return float(out) if out.ndim == 0 else out
+
+
+def det_exp(y):
+    """exp(y) for |y| < 700: k = rint(y/ln2), r = y - k ln2 (two-part),
+    (expm1_taylor(r) + 1) * 2^k — gns_common.cuh det_exp / oracle/gen.cc."""
+    y = np.asarray(y, dtype=np.float64)
+    k = np.rint(y * INV_LN2)
+    r = (y - k * LN2_HI) - k * LN2_LO
+    return np.ldexp(_expm1_taylor(r) + 1.0, k.astype(np.int64))
+
+
+def det_pow(a, b):
+    """a**b = det_exp(b * det_log(a)) for a > 0 (the generator's inverse CDF)."""
+    return det_exp(b * det_log(a))

@@ -7,7 +7,7 @@ Every function cites the reference lines it restates (paths relative to
   (one call per phase per layer, ``sampling.py:166,214,233``).  With
   ``np.random.default_rng([seed, 32, epoch, index])`` (``pool.py:70``) the
   oracle reproduces ``gnsbench.build_minibatch`` bit for bit — this is how
-  the restatement itself is pinned (``tests/test_oracle_pin.py``) and how the
+  the restatement itself is pinned (``tests/test_oracle.py``) and how the
   CPU baseline is timed (the reference's own RNG cost).
 * ``PhiloxKeys(seed, epoch, batch)`` — the build's counter-based keys
   (``oracle/philox.py``).  The B200 kernels must match this mode bit for bit.

@@ -3,9 +3,9 @@
 TEST INFRASTRUCTURE ONLY (see ``oracle/__init__.py``).
 
 This is the RNG contract shared bit-for-bit with ``paper_2106_06150_b200/csrc/
-gns_rng.cuh``.  Philox4x32-10 is the Salmon et al. (SC'11) generator; its
+gns_common.cuh``.  Philox4x32-10 is the Salmon et al. (SC'11) generator; its
 known-answer vectors (Random123 ``kat_vectors``) are checked in
-``tests/test_oracle_rng.py``.
+``tests/test_oracle.py::test_philox_kat``.
 
 Key layout (restates the SPEC intent "deterministic per (seed, epoch,
 batch_index, layer, dst node id)", ``SPEC.md:292``; the reference's

@@ -160,6 +160,10 @@ _SIGS = {
                                          c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "gns_gen_powerlaw_fill": (c_int32, [c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                         c_size_t, c_void_p]),
+    "gns_gen_node_attrs": (c_int32, [c_int64, c_int32, c_double, c_uint32, c_void_p, c_void_p, c_void_p,
+                                     c_void_p, c_void_p]),
+    "gns_gen_features": (c_int32, [c_int64, c_int32, c_int32, c_int32, ctypes.c_float, c_uint32, c_void_p,
+                                   c_void_p, c_void_p, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -221,6 +225,7 @@ KERNELS_PER_CALL = {
     "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_sum_rows": 1, "gns_graph_switch_begin": 1, "gns_graph_switch_handles": 1, "gns_graph_switch_node": 0, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2, "gns_spmm_fwd_bits": 1, "gns_spmm_bwd_transposed_bits": 2,
     "gns_adam_dev": 2,
     "gns_softmax_xent": 2, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1, "gns_build_csr_count": 6, "gns_build_csr_fill": 1,
+    "gns_gen_node_attrs": 1, "gns_gen_features": 2,
 }
 launch_counter = [0]
 

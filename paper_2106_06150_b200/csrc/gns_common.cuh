@@ -225,6 +225,16 @@ __device__ __forceinline__ double det_expm1(double y) {  // y <= 0
   return DSUB(ldexp(er, (int)k), 1.0);
 }
 
+// exp(y) for |y| < 700 and pow(a, b) = exp(b * log(a)) for a > 0, same IEEE
+// op sequence as oracle/gen.c (the synthetic-graph generator's inverse CDF).
+__device__ __forceinline__ double det_exp(double y) {
+  double k = rint(DMUL(y, GNS_INV_LN2));
+  double r = DSUB(DSUB(y, DMUL(k, GNS_LN2_HI)), DMUL(k, GNS_LN2_LO));
+  return ldexp(DADD(expm1_taylor(r), 1.0), (int)k);
+}
+
+__device__ __forceinline__ double det_pow(double a, double b) { return det_exp(DMUL(b, det_log(a))); }
+
 // ---------------------------------------------------------------------------
 // warp helpers
 // ---------------------------------------------------------------------------

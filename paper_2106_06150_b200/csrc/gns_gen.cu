@@ -32,8 +32,11 @@ __device__ __forceinline__ int32_t gen_rank_to_id(uint64_t x, const GenParams& P
 }
 
 __device__ __forceinline__ int64_t gen_rank(double u, const GenParams& P) {
-  const double oma = 1.0 - P.alpha;
-  double x = pow(P.a0 + u * P.span, 1.0 / oma) - P.offset;
+  // inverse CDF with the deterministic pow (gns_common.cuh det_pow): the same
+  // IEEE op sequence as oracle/gen.c, so the host restatement rebuilds this
+  // graph bit for bit (the CPU reference arm of bench.py uses it)
+  const double oma = DSUB(1.0, P.alpha);
+  double x = DSUB(det_pow(DADD(P.a0, DMUL(u, P.span)), DDIV(1.0, oma)), P.offset);
   int64_t r = (int64_t)x;
   if (r < 0) r = 0;
   if (r >= P.n) r = P.n - 1;
@@ -205,6 +208,66 @@ __global__ void gen_compact_kernel(const int64_t* __restrict__ ptr0, const int32
   }
 }
 
+// ---------------------------------------------------------------------------
+// Node attributes: labels, train/val/test masks and class-mean + noise
+// features (the graph.py:249-253 scheme), each a pure function of
+// (seed, node[, column]) through Philox, so oracle/gen.c reproduces them bit
+// for bit on the host.  The noise is an Irwin-Hall(4) normal: four 16-bit
+// uniforms summed as an integer (exact), scaled by 2^-16, centred, times
+// sqrt(3) -- float ops only, each explicitly rounded (no FMA contraction).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kAttrKey = 0x4e4f4445u;  // "NODE"
+constexpr float kSqrt3f = 0x1.bb67aep+0f;
+
+__device__ __forceinline__ float ih4_normal(uint32_t a, uint32_t b) {
+  uint32_t s = (a & 0xffffu) + (a >> 16) + (b & 0xffffu) + (b >> 16);
+  return __fmul_rn(__fsub_rn(__fmul_rn((float)s, 0x1p-16f), 2.0f), kSqrt3f);
+}
+
+__global__ void gen_attrs_kernel(int64_t n, uint32_t classes, float t1, float t2, uint32_t seed,
+                                 int32_t* __restrict__ labels, uint8_t* __restrict__ train,
+                                 uint8_t* __restrict__ val, uint8_t* __restrict__ test) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    u32x4 w = philox4x32_10((uint32_t)v, (uint32_t)(v >> 32), stream_word(41, 0, 0), 0u, seed, kAttrKey);
+    labels[v] = (int32_t)(((uint64_t)w.x * classes) >> 32);
+    float r = __fmul_rn((float)(w.y >> 8), 0x1p-24f);
+    train[v] = r < t1;
+    val[v] = r >= t1 && r < t2;
+    test[v] = r >= t2;
+  }
+}
+
+// class means: one thread per (class, column pair)
+__global__ void gen_means_kernel(int32_t classes, int32_t ld, uint32_t seed, float* __restrict__ means) {
+  const int pairs = ld >> 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < classes * pairs; i += gridDim.x * blockDim.x) {
+    const int c = i / pairs, q = i % pairs;
+    u32x4 w = philox4x32_10((uint32_t)q, (uint32_t)c, stream_word(42, 0, 0), 0u, seed, kAttrKey);
+    means[(int64_t)c * ld + 2 * q] = ih4_normal(w.x, w.y);
+    means[(int64_t)c * ld + 2 * q + 1] = ih4_normal(w.z, w.w);
+  }
+}
+
+__global__ void gen_feats_kernel(int64_t n, int32_t dim, int32_t ld, float noise, uint32_t seed,
+                                 const int32_t* __restrict__ labels, const float* __restrict__ means,
+                                 float* __restrict__ out) {
+  const int pairs = ld >> 1;
+  const int64_t total = n * pairs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / pairs;
+    const int q = (int)(i - v * pairs);
+    const int j = 2 * q;
+    float2 o = make_float2(0.f, 0.f);
+    if (j < dim) {
+      u32x4 w = philox4x32_10((uint32_t)q, (uint32_t)v, stream_word(43, 0, 0), (uint32_t)(v >> 32), seed, kAttrKey);
+      const float* m = means + (int64_t)labels[v] * ld;
+      o.x = __fadd_rn(m[j], __fmul_rn(noise, ih4_normal(w.x, w.y)));
+      if (j + 1 < dim) o.y = __fadd_rn(m[j + 1], __fmul_rn(noise, ih4_normal(w.z, w.w)));
+    }
+    reinterpret_cast<float2*>(out)[i] = o;
+  }
+}
+
 struct GenWs {
   int32_t* cnt;
   int64_t* ptr0;
@@ -227,14 +290,17 @@ static size_t gen_ws(int64_t n, int64_t m, void* base, size_t cap, GenWs* w) {
   return ws.off;
 }
 
+// host-side parameters: libm pow, the same call oracle/gen.c makes
+static double gen_host_pow(double a, double b) { return pow(a, b); }
+
 static GenParams make_params(int64_t n, int64_t m, double alpha, double offset, uint32_t seed) {
   GenParams P;
   P.n = n;
   P.m = m;
   P.alpha = alpha;
   P.offset = offset;
-  P.a0 = pow(offset, 1.0 - alpha);
-  P.span = pow((double)n + offset, 1.0 - alpha) - P.a0;
+  P.a0 = gen_host_pow(offset, 1.0 - alpha);
+  P.span = gen_host_pow((double)n + offset, 1.0 - alpha) - P.a0;
   int bits = 2;
   while ((1ll << bits) < n) ++bits;
   bits += bits & 1;
@@ -330,3 +396,31 @@ int gns_gen_powerlaw_fill(int64_t n, int64_t m, const int64_t* indptr, int32_t* 
 }
 
 }  // extern "C"
+
+extern "C" int gns_gen_node_attrs(int64_t n, int32_t num_classes, double train_frac, uint32_t seed, int32_t* labels,
+                                  uint8_t* train, uint8_t* val, uint8_t* test, void* stream_) {
+  if (n < 0 || num_classes < 1 || !(train_frac >= 0.0 && train_frac <= 1.0)) {
+    set_error("gen_node_attrs: need n >= 0, num_classes >= 1, 0 <= train_frac <= 1");
+    return GNS_EINVAL;
+  }
+  if (n == 0) return GNS_OK;
+  const float t1 = (float)train_frac;
+  const float t2 = (float)(train_frac + (1.0 - train_frac) / 2);
+  gen_attrs_kernel<<<num_sms() * 8, 256, 0, (cudaStream_t)stream_>>>(n, (uint32_t)num_classes, t1, t2, seed, labels,
+                                                                     train, val, test);
+  return check_launch("gen_attrs");
+}
+
+extern "C" int gns_gen_features(int64_t n, int32_t dim, int32_t ld, int32_t num_classes, float noise, uint32_t seed,
+                                const int32_t* labels, float* class_means, float* out, void* stream_) {
+  if (n < 0 || dim < 1 || ld < dim || (ld & 1) || num_classes < 1) {
+    set_error("gen_features: need dim >= 1, even ld >= dim, num_classes >= 1");
+    return GNS_EINVAL;
+  }
+  if (n == 0) return GNS_OK;
+  cudaStream_t s = (cudaStream_t)stream_;
+  gen_means_kernel<<<div_up((long long)num_classes * (ld / 2), 256), 256, 0, s>>>(num_classes, ld, seed, class_means);
+  GNS_TRY(check_launch("gen_means"));
+  gen_feats_kernel<<<num_sms() * 16, 256, 0, s>>>(n, dim, ld, noise, seed, labels, class_means, out);
+  return check_launch("gen_feats");
+}

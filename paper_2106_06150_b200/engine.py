@@ -65,7 +65,7 @@ class GraphedTrainer:
     def __init__(self, g: Graph, config: SamplerConfig, dims, train_config: TrainConfig | None = None,
                  rank: int = 0, world_size: int = 1, allreduce=None, seed: int = 0, host_targets: bool = False,
                  feature_placement: str = "device", host_features: torch.Tensor | None = None,
-                 steps_per_graph: int | None = None, switch_chunk: int | None = None):
+                 steps_per_graph: int | None = None, switch_chunk: int | None = None, tf32: bool = True):
         _lib.require_cuda()
         if g.features is None or g.labels is None:
             raise ValueError("training needs features and labels")
@@ -74,7 +74,11 @@ class GraphedTrainer:
         self.rank, self.world = rank, world_size
         self.allreduce = allreduce
         self.dev = g.device
-        self.model = GraphSAGE(dims, dtype=torch.float32, device=self.dev, seed=seed)
+        # float32 storage; tf32=True runs the linear layers' GEMMs on the
+        # tensor cores in TF32 (10-bit mantissa inputs, fp32 accumulate),
+        # tf32=False in full fp32 (the SpMMs, gather, loss and Adam are fp32
+        # either way)
+        self.model = GraphSAGE(dims, dtype=torch.float32, device=self.dev, seed=seed, tf32=tf32)
         self.dims = self.model.dims
         lab = g.labels
         if lab.numel() and (int(lab.min()) < 0 or int(lab.max()) >= self.dims[-1]):
@@ -320,10 +324,15 @@ class GraphedTrainer:
                 # forward's bits) and bias grad.  dz rows past the count are not
                 # zeroed: the weight gradient multiplies them by cat's zero rows
                 ws = self.tws[slot][li]
+                evb = self._prof_events if li == 1 else None
+                if evb is not None:
+                    _lib.call("gns_record_event_external", evb[4].cuda_event, s)
                 _lib.call("gns_spmm_bwd_transposed_bits", self.dcat[li].data_ptr(), self.dcat[li].stride(0),
                           self.dims[li], blocks[li].cblock, self.cap_dst[li], self.cap_src[li], self.cap_edges[li],
                           0, self.relu_bits[li].data_ptr(), m.gbiases[li - 1].data_ptr(),
                           self.dz[li - 1].data_ptr(), self.dz[li - 1].stride(0), ws.data_ptr(), ws.numel(), s)
+                if evb is not None:
+                    _lib.call("gns_record_event_external", evb[5].cuda_event, s)
         if with_adam:
             self._adam_dev()
 
@@ -495,6 +504,8 @@ class GraphedTrainer:
             return
         if self._pf is not None and self._pf[1].epoch == epoch:
             return
+        if self._probs is None:       # the active cache was adopted (cache setter)
+            self._probs = cache_probs(self.g, self.cfg)
         t = 1 - self.cur
         if self.csets[t] is None:
             self.csets[t] = cache_mod.empty_like(self.cache, self.g)
@@ -532,10 +543,10 @@ class GraphedTrainer:
 
     def capture_profiled(self):
         """Re-capture with timing events around the input-feature gather
-        (gns_gather_rows) and the input-layer SpMM of the first step of each
-        replay, so their durations can be read after a replay (bench.py's
-        roofline; not the headline)."""
-        self._prof_events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        (gns_gather_rows), the input-layer SpMM and layer 1's transposed
+        SpMM of the first step of each replay, so their durations can be read
+        after a replay (bench.py's rooflines; not the headline)."""
+        self._prof_events = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         for e in self._prof_events:      # materialise the driver events
             e.record(self.main)
         torch.cuda.synchronize()
@@ -551,6 +562,15 @@ class GraphedTrainer:
         e = self._prof_events
         e[3].synchronize()
         return float(e[2].elapsed_time(e[3]))
+
+    def bwd1_ms(self) -> float:
+        """Duration of model layer 1's transposed SpMM (backward) in the last
+        replay (0 for a one-layer model)."""
+        e = self._prof_events
+        if self.L < 2:
+            return 0.0
+        e[5].synchronize()
+        return float(e[4].elapsed_time(e[5]))
 
     # -- capture / replay ---------------------------------------------------------------
     def _group(self, p: int):

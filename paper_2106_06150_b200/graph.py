@@ -181,25 +181,19 @@ def generate_powerlaw_device(num_nodes: int, num_pairs: int, alpha: float = 0.6,
     _lib.call("gns_gen_powerlaw_fill", num_nodes, num_pairs, indptr.data_ptr(), indices.data_ptr(),
               ws.data_ptr(), ws.numel(), stream)
     del ws
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(seed)
-    labels = torch.randint(0, num_classes, (num_nodes,), generator=gen, device=dev, dtype=torch.int32)
+    # labels, masks and features: pure functions of (seed, node) on the device
+    # (gns_gen_node_attrs / gns_gen_features), reproducible bit for bit by the
+    # host restatement oracle/gen.c
+    labels = torch.empty(num_nodes, dtype=torch.int32, device=dev)
+    train, val, test = (torch.empty(num_nodes, dtype=torch.bool, device=dev) for _ in range(3))
+    _lib.call("gns_gen_node_attrs", num_nodes, num_classes, float(train_frac), seed & 0xFFFFFFFF,
+              labels.data_ptr(), train.data_ptr(), val.data_ptr(), test.data_ptr(), stream)
     feats = None
     if feature_dim > 0:
         ld = (feature_dim + 3) // 4 * 4
-        means = torch.randn((num_classes, ld), generator=gen, device=dev)
+        means = torch.empty((num_classes, ld), dtype=torch.float32, device=dev)
         feats = torch.empty((num_nodes, ld), dtype=torch.float32, device=dev)
-        chunk = 1 << 22
-        for s in range(0, num_nodes, chunk):
-            t = min(num_nodes, s + chunk)
-            feats[s:t] = means[labels[s:t].long()]
-            feats[s:t].add_(torch.randn((t - s, ld), generator=gen, device=dev), alpha=feature_noise)
-        if ld != feature_dim:
-            feats[:, feature_dim:] = 0
-    r = torch.rand(num_nodes, generator=gen, device=dev)
-    train = r < train_frac
-    rest = (1.0 - train_frac) / 2
-    val = (r >= train_frac) & (r < train_frac + rest)
-    test = r >= train_frac + rest
+        _lib.call("gns_gen_features", num_nodes, feature_dim, ld, num_classes, float(feature_noise),
+                  seed & 0xFFFFFFFF, labels.data_ptr(), means.data_ptr(), feats.data_ptr(), stream)
     return Graph(num_nodes, indptr, indices, feats, labels, train, val, test,
                  feature_dim=feature_dim if feature_dim else None)

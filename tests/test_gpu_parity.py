@@ -835,6 +835,27 @@ def test_device_generator_contract(P):
     assert torch.equal(g.indices, g2.indices)
 
 
+@pytest.mark.parametrize("n,m,alpha,offset,seed", [(20000, 150000, 0.6, 50.0, 3), (100000, 1000000, 0.6, 10.0, 0),
+                                                    (5000, 60000, 0.3, 2.0, 11)])
+def test_device_generator_equals_host_restatement(P, n, m, alpha, offset, seed):
+    """The device generator (gns_gen_powerlaw_*, gns_gen_node_attrs,
+    gns_gen_features) and its host restatement oracle/gen.cc build the same
+    graph bit for bit: CSR, labels, masks, features (the CPU reference arm of
+    bench.py builds its graph on the host with the latter)."""
+    from oracle import gen
+    g = P.generate_powerlaw_device(n, m, alpha=alpha, offset=offset, seed=seed, feature_dim=30, num_classes=7,
+                                   train_frac=0.2)
+    og = gen.powerlaw_graph(n, m, alpha, offset, seed, feature_dim=30, num_classes=7, train_frac=0.2)
+    assert np.array_equal(g.indptr.cpu().numpy(), og.indptr)
+    assert np.array_equal(g.indices.cpu().numpy(), og.indices)
+    assert np.array_equal(g.labels.cpu().numpy(), og.labels)
+    for a, b in ((g.train_mask, og.train_mask), (g.val_mask, og.val_mask), (g.test_mask, og.test_mask)):
+        assert np.array_equal(a.cpu().numpy(), b)
+    f = g.features.cpu().numpy()          # row stride padded to 16 B, zero columns
+    assert f.shape == (n, 32) and g.feature_dim == 30
+    assert np.array_equal(f.view(np.uint32), og.features.view(np.uint32))
+
+
 # ---- CUDA-graph engine ---------------------------------------------------------------
 
 @pytest.mark.parametrize("S", [1, 2])

@@ -259,3 +259,58 @@ def test_oracle_gns_exact_equals_reference(gb):
     for ba, bb in zip(mr.blocks, mo.blocks):
         for f in ("src_nodes", "edge_src", "edge_dst", "edge_weight", "edge_cached"):
             assert np.array_equal(getattr(ba, f), getattr(bb, f)), f
+
+
+# ---- host restatement of the synthetic-graph generator (oracle/gen.cc) -------------
+
+@pytest.mark.parametrize("n,m,alpha,offset,seed", [(5000, 20000, 0.6, 10.0, 7), (300000, 400000, 0.6, 300.0, 0),
+                                                    (1000, 8000, 0.3, 2.0, 5)])
+def test_host_generator_pairs_and_csr(n, m, alpha, offset, seed):
+    """oracle/gen.cc pair draw == its numpy restatement (Philox + the
+    deterministic pow + Feistel), and its CSR pipeline == the restatement of
+    the reference's build_csr (graph.py:142-169) on those pairs."""
+    from oracle import gen
+    u, v = gen.gen_pairs(n, alpha, offset, seed, 0, m)
+    un, vn = gen.gen_pairs_np(n, alpha, offset, seed, 0, m)
+    assert np.array_equal(u, un) and np.array_equal(v, vn)
+    ip, ix = gen.powerlaw_csr(n, m, alpha, offset, seed, threads=3)
+    og = O.build_csr(np.stack([u, v], 1), n)
+    assert np.array_equal(ip, og.indptr) and np.array_equal(ix, og.indices)
+    ip2, ix2 = gen.build_csr_pairs(n, u, v, threads=2)
+    assert np.array_equal(ip2, og.indptr) and np.array_equal(ix2, og.indices)
+
+
+def test_host_generator_attributes():
+    from oracle import gen
+    n = 20000
+    lab, tr, va, te = gen.node_attrs(n, 13, 0.1, 3)
+    ref = gen.node_attrs_np(n, 13, 0.1, 3)
+    for a, b in zip((lab, tr, va, te), ref):
+        assert np.array_equal(a, b)
+    assert lab.min() >= 0 and lab.max() < 13 and not (tr & va).any() and (tr | va | te).all()
+    assert abs(tr.mean() - 0.1) < 0.01
+    f = gen.features(n, 30, 13, lab, 3.0, 3, threads=4)
+    fn = gen.features_np(n, 30, 13, lab, 3.0, 3)
+    assert np.array_equal(f.view(np.uint32), fn.view(np.uint32))
+    assert f.shape == (n, 32) and not f[:, 30:].any()
+    # class-mean + noise: per-class means separate, noise sd ~ 3
+    assert 2.5 < f[:, :30].std() < 3.6
+
+
+def test_detmath_exp_pow_close_to_libm():
+    y = np.random.default_rng(0).uniform(-40, 40, 20000)
+    np.testing.assert_allclose(detmath.det_exp(y), np.exp(y), rtol=4e-16 * 8)
+    a = np.random.default_rng(1).uniform(1.0, 2000.0, 20000)
+    np.testing.assert_allclose(detmath.det_pow(a, 2.5), np.power(a, 2.5), rtol=1e-14)
+
+
+def test_host_cached_csr_equals_build_cache():
+    """cache.py:185-197 by filtering (oracle/gen.cc og_cached_csr) equals
+    build_cache's gather_rows + lexsort construction."""
+    from oracle import gen
+    g = gen.powerlaw_graph(20000, 100000, 0.6, 10.0, 3)
+    w = O.degree_probs(g)
+    c = O.build_cache(g, w, 300, numpy_seed=[0, 33, 0])
+    ip, ix = gen.cached_csr(g.indptr, g.indices, c.mask, threads=3)
+    assert np.array_equal(ip, c.cached_indptr) and np.array_equal(ix, c.cached_indices)
+
