@@ -15,6 +15,8 @@ from .formats import (build_csr, load_binary, load_edgelist, load_feature_csv, s
 from .graph import Graph, NodeSet, generate_powerlaw_device
 from .model import GraphSAGE, TrainConfig, init_params_numpy, micro_f1
 from .pool import BatchItem, SamplerPool, epoch_targets
+from .train import (AdamState, EpochStats, ModelParams, ParamGrads, TrainReport, adam_step, backward, evaluate,
+                    forward, full_batch_forward, init_params, loss_and_grad, train)
 from .sampling import (BatchRng, LayerBlock, MiniBatch, MiniBatchSampler, SamplerConfig,
                        build_minibatch, estimate_edge_inclusion, gns_weight_paper, isolated_fraction,
                        sample_neighbors_gns, sample_neighbors_uniform, validate_minibatch)

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -91,10 +92,20 @@ class BatchRng:
 
 
 def _as_rng(rng) -> BatchRng:
+    """The reference injects a duck-typed numpy ``rng`` (sampling.py:166,214,
+    233).  The device sampler draws counter-based Philox keys, so a numpy
+    ``Generator`` (or anything with ``.integers``) seeds one: three 32-bit
+    draws become the (seed, epoch, batch) Philox key.  Deterministic in the
+    generator's state and it advances the generator, but the keys are not the
+    ones numpy's ``random()`` would have produced (PCG64 is not restated on
+    the device); pass ``BatchRng`` to name the key directly."""
     if isinstance(rng, BatchRng):
         return rng
+    if hasattr(rng, "integers"):
+        s, e, b = (int(x) for x in rng.integers(0, 1 << 32, size=3, dtype=np.uint64))
+        return BatchRng(s, e, b)
     raise TypeError("the B200 sampler draws counter-based Philox keys: pass "
-                    "paper_2106_06150_b200.BatchRng(seed, epoch, batch) as rng")
+                    "paper_2106_06150_b200.BatchRng(seed, epoch, batch) or a numpy Generator as rng")
 
 
 @dataclass(eq=False)

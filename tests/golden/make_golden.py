@@ -158,6 +158,85 @@ def make_model_golden():
     np.savez_compressed(os.path.join(HERE, "golden_model.npz"), **out)
 
 
+def _philox_cache(g, probs, w, cs, epoch):
+    """The build's Philox cache of ``epoch`` (key [0, 33, epoch]) injected into
+    the reference's build_cache (cache replay), deterministic inclusion."""
+    ids = O.sample_cache(w, cs, seed=0, epoch=epoch)
+    orig = gb.cache.sample_cache
+    gb.cache.sample_cache = lambda probs_, size_, seed_: gb.NodeSet.from_ids(ids, g.num_nodes)
+    try:
+        cache = gb.build_cache(g, probs, cs, epoch=epoch, rng_seed=[0, 33, epoch])
+    finally:
+        gb.cache.sample_cache = orig
+    cache = _with_det_inclusion(gb, cache, w)
+    oc = O.OCache(ids=cache.nodes.ids, mask=cache.nodes.mask, inclusion=cache.inclusion,
+                  cached_indptr=cache.cached_indptr, cached_indices=cache.cached_indices)
+    return cache, oc
+
+
+def make_train_golden():
+    """SPEC.md:371-373,519 convergence task: SBM(2000, 4 blocks, 0.02, 0.002),
+    16-d features, GNS cache 10% P=1, fanouts (15,10,5), batch 100, hidden 64,
+    10 epochs (model.py:257-307).  (a) the reference's fp64 trainer on the
+    build's Philox keys (cache, epoch permutation and per-batch keys replayed):
+    every step's loss, per-epoch mean loss and micro-F1; (b) the reference
+    free-running on its own PCG64 streams (gnsbench.train), GNS and NS: final
+    F1 (the SPEC's 2-point tolerance is against these)."""
+    out = {}
+    g = gb.generate_sbm(2000, 4, 0.02, 0.002, seed=0, feature_dim=16)
+    for f in ("indptr", "indices", "features", "labels", "train_mask", "val_mask", "test_mask"):
+        out[f] = np.asarray(getattr(g, f))
+    cfg = gb.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=100, cache_frac=0.1,
+                           cache_period=1, cache_mode="degree", seed=0)
+    tc = gb.TrainConfig(epochs=10, seed=0, hidden_dim=64, lr=0.003)
+    dims = (16, 64, 64, 4)
+    params = gb.init_params(dims, seed=0)
+    state = gb.AdamState.zeros_like(params)
+    probs = gb.degree_probs(g)
+    w = O.degree_probs(g)
+    cs = int(round(cfg.cache_frac * g.num_nodes))
+    losses, epoch_loss, f1s = [], [], []
+    for epoch in range(tc.epochs):
+        cache, oc = _philox_cache(g, probs, w, cs, epoch)
+        el = []
+        for index, targets in enumerate(O.epoch_targets(g, cfg.batch_size, cfg.seed, epoch)):
+            rec = []
+            O.build_minibatch(g, oc, targets, cfg, O.PhiloxKeys(cfg.seed, epoch, index, record=rec))
+            mb = gb.build_minibatch(g, cache, targets, cfg, O.ReplayRng(rec))
+            logits = gb.forward(mb, g.features, params)
+            loss, grad = gb.loss_and_grad(logits, g.labels[mb.targets])
+            grads = gb.backward(mb, g.features, params, grad)
+            gb.adam_step(params, grads, state, tc)
+            el.append(loss)
+        losses += el
+        epoch_loss.append(np.mean(el))
+        f = gb.model.evaluate(g, params)
+        f1s.append([f["train"], f["val"], f["test"]])
+    out["losses"] = np.array(losses)
+    out["epoch_loss"] = np.array(epoch_loss)
+    out["f1"] = np.array(f1s)
+    for strat, kw in (("gns", dict(cache_frac=0.1, cache_period=1, cache_mode="degree")), ("ns", {})):
+        c2 = gb.SamplerConfig(strategy=strat.upper(), fanouts=(15, 10, 5), batch_size=100, seed=0, **kw)
+        rep = gb.train(g, c2, tc)
+        out[f"free_{strat}_test_f1"] = np.array(rep.final_test_f1)
+        out[f"free_{strat}_epoch_loss"] = np.array([r.loss for r in rep.rows])
+    np.savez_compressed(os.path.join(HERE, "golden_train.npz"), **out)
+
+
+def make_stat_golden():
+    """The reference's own cache draw (cache.py:87-103, numpy exponential race
+    with seeds [1, 33, e]) repeated R times on a small power-law graph: per-node
+    inclusion counts for the two-sample |C| > 1 test of the device draw."""
+    g = gb.generate_powerlaw(60, 2, 3)
+    probs = gb.degree_probs(g)
+    R, cs = 20000, 8
+    counts = np.zeros(g.num_nodes, dtype=np.int64)
+    for e in range(R):
+        counts[gb.sample_cache(probs, cs, [1, 33, e]).ids] += 1
+    np.savez_compressed(os.path.join(HERE, "golden_stat.npz"), indptr=g.indptr, indices=g.indices,
+                        cache_size=np.array(cs), draws=np.array(R), ref_counts=counts)
+
+
 def make_format_golden():
     """A GNSG v1 file written by the reference's save_binary (graph.py:283-299)."""
     g = gb.generate_sbm(60, 3, 0.3, 0.05, seed=0, feature_dim=5)
@@ -169,6 +248,8 @@ if __name__ == "__main__":
     make_kat_golden()
     make_sampler_golden()
     make_model_golden()
+    make_train_golden()
+    make_stat_golden()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

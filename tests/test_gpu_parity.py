@@ -1311,3 +1311,242 @@ def test_gns_exact_table_and_blocks(P):
     pool = P.SamplerPool(g, cfg)
     n = sum(1 for _ in pool.iter_epoch(0))
     assert n > 0 and set(pool._tables) == {(10, False), (5, True)}
+
+
+# ---- training parity on the SPEC convergence task (golden_train.npz) --------------
+# SBM(2000, 4 blocks, 0.02, 0.002), 16-d, GNS cache 10% P=1, fanouts (15,10,5),
+# batch 100, hidden 64, 10 epochs (model.py:257-307)
+
+@pytest.fixture(scope="module")
+def sbm(P):
+    import os
+    from conftest import GOLDEN
+    z = dict(np.load(os.path.join(GOLDEN, "golden_train.npz")))
+    n = len(z["indptr"]) - 1
+    g = P.Graph.from_numpy(n, z["indptr"], z["indices"], features=z["features"].astype(np.float32),
+                           labels=z["labels"], train_mask=z["train_mask"], val_mask=z["val_mask"],
+                           test_mask=z["test_mask"])
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=100, cache_frac=0.1, cache_period=1,
+                          cache_mode="degree", seed=0)
+    return z, g, cfg
+
+
+def test_train_api_fp64_matches_reference_on_replayed_keys(P, sbm):
+    """The reference's loop body (model.py:279-285) through the drop-in
+    module API — init_params / forward / loss_and_grad / backward / adam_step
+    in float64 — on the same Philox batches the golden reference run used
+    (cache, epoch permutation and per-batch keys replayed): the first 20 step
+    losses within 1e-9 relative, every epoch's mean loss within 1e-7, and the
+    micro-F1 of every epoch (full-neighbourhood evaluate) within 1 point."""
+    z, g, cfg = sbm
+    tc = P.TrainConfig(epochs=10, seed=0, hidden_dim=64, lr=0.003)
+    params = P.init_params((16, 64, 64, 4), seed=0)
+    state = P.AdamState.zeros_like(params)
+    pool = P.SamplerPool(g, cfg, num_workers=2)
+    losses, epoch_loss, f1 = [], [], []
+    for epoch in range(10):
+        el = []
+        for it in pool.iter_epoch(epoch):
+            mb = it.minibatch
+            logits = P.forward(mb, g, params)
+            loss, grad = P.loss_and_grad(logits, g.labels[mb.targets.long()])
+            grads = P.backward(mb, g, params, grad)
+            P.adam_step(params, grads, state, tc)
+            el.append(loss)
+        losses += el
+        epoch_loss.append(np.mean(el))
+        f = P.evaluate(g, params)
+        f1.append([f["train"], f["val"], f["test"]])
+    assert len(losses) == len(z["losses"])
+    np.testing.assert_allclose(losses[:20], z["losses"][:20], rtol=1e-9)
+    np.testing.assert_allclose(epoch_loss, z["epoch_loss"], rtol=1e-7)
+    np.testing.assert_allclose(np.array(f1), z["f1"], atol=0.01)
+
+
+@pytest.mark.parametrize("tf32", [True, False])
+def test_engine_fp32_tf32_training_tracks_reference(P, sbm, tf32):
+    """The production engine (CUDA-graph steps, float32 storage, GEMMs in TF32
+    or full fp32) on the same replayed batches: per-epoch mean loss within the
+    stated tolerance of the fp64 reference (fp32 1e-3 relative; TF32 — 10-bit
+    mantissa GEMM inputs — 2e-2 relative) and final test micro-F1 within 1
+    point."""
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    z, g, cfg = sbm
+    tc = P.TrainConfig(epochs=10, seed=0, hidden_dim=64, lr=0.003)
+    tr = GraphedTrainer(g, cfg, (16, 64, 64, 4), tc, seed=0, tf32=tf32)
+    epoch_loss = []
+    for epoch in range(10):
+        el = []
+        tr.run_epoch(epoch, on_step=lambda e, i, k: el.append(tr.loss_value()))
+        epoch_loss.append(np.mean(el))
+    f = P.evaluate(g, P.ModelParams(tr.model))
+    np.testing.assert_allclose(epoch_loss, z["epoch_loss"], rtol=2e-2 if tf32 else 1e-3)
+    assert abs(f["test"] - z["f1"][-1][2]) <= 0.01, (f, z["f1"][-1])
+
+
+@pytest.mark.parametrize("strategy", ["GNS", "NS"])
+def test_train_free_running_f1_within_two_points(P, sbm, strategy):
+    """free-running Philox training (P.train, the
+    reference's train() loop, float32 production precision) reaches a test
+    micro-F1 within 2 points of the reference's own PCG64 run, and >= 0.90."""
+    z, g, cfg = sbm
+    if strategy == "NS":
+        cfg = P.SamplerConfig(strategy="NS", fanouts=(15, 10, 5), batch_size=100, seed=0)
+    rep = P.train(g, cfg, P.TrainConfig(epochs=10, seed=0, hidden_dim=64, lr=0.003), dtype=torch.float32)
+    ref = float(z[f"free_{strategy.lower()}_test_f1"])
+    assert len(rep.rows) == 10 and rep.rows[-1].mean_input_nodes > 0
+    assert abs(rep.final_test_f1 - ref) <= 0.02, (rep.final_test_f1, ref)
+    assert rep.final_test_f1 >= 0.90
+
+
+def test_engine_precisions_at_bench_dims(P):
+    """Bench dims (128, 256, 256, 172): the engine in TF32 and fp32 against the
+    float64 façade on the same Philox batches of one epoch — per-step loss
+    within 1e-3 relative (fp32) / 5e-3 (TF32), epoch mean within 1e-3."""
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    g = P.generate_powerlaw_device(60_000, 600_000, alpha=0.6, offset=10.0, seed=5, feature_dim=128,
+                                   num_classes=172, train_frac=0.2)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(15, 10, 5), batch_size=1000, cache_frac=0.01,
+                          cache_mode="degree", seed=0)
+    dims = (128, 256, 256, 172)
+    tc = P.TrainConfig(lr=0.003, hidden_dim=256)
+    params = P.init_params(dims, seed=0)
+    state = P.AdamState.zeros_like(params)
+    ref = []
+    for it in P.SamplerPool(g, cfg).iter_epoch(0):
+        mb = it.minibatch
+        loss, grad = P.loss_and_grad(P.forward(mb, g, params), g.labels[mb.targets.long()])
+        P.adam_step(params, P.backward(mb, g, params, grad), state, tc)
+        ref.append(loss)
+    for tf32, tol in ((False, 1e-3), (True, 5e-3)):
+        tr = GraphedTrainer(g, cfg, dims, tc, seed=0, tf32=tf32)
+        got = []
+        tr.run_epoch(0, on_step=lambda e, i, k: got.append(tr.loss_value()))
+        assert len(got) == len(ref) >= 10
+        np.testing.assert_allclose(got, ref, rtol=tol)
+        assert abs(np.mean(got) / np.mean(ref) - 1) < 1e-3
+
+
+# ---- SPEC statistical properties ------------------------------------------------------
+
+def test_cache_draw_two_sample_vs_reference(P):
+    """|C| > 1: per-node inclusion frequencies of the device
+    draw (Philox exponential race) vs the reference's own numpy draw
+    (golden_stat.npz, 2e4 draws each): two-sample z per node, Bonferroni
+    |z| < 4.5."""
+    import os
+    from conftest import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "golden_stat.npz"))
+    n = len(z["indptr"]) - 1
+    g = P.Graph.from_numpy(n, z["indptr"], z["indices"])
+    probs = P.degree_probs(g)
+    R, cs = int(z["draws"]), int(z["cache_size"])
+    hits = torch.zeros(n, dtype=torch.int64, device="cuda")
+    for e in range(R):
+        hits[P.sample_cache(probs, cs, [1, 33, e]).ids.long()] += 1
+    a, b = hits.cpu().numpy() / R, z["ref_counts"] / R
+    pooled = (a + b) / 2
+    se = np.sqrt(np.maximum(pooled * (1 - pooled), 1e-12) * 2 / R)
+    zs = np.abs(a - b) / se
+    assert zs.max() < 4.5, (zs.max(), int(zs.argmax()))
+
+
+def test_gns_full_cache_marginals_equal_ns(P):
+    """GNS with C = V and cache_only = false draws each seed's
+    neighbours with NS's marginals (uniform without replacement: min(k,d)/d
+    per edge); chi-square over T Philox batches, p > 0.01, on a 30-node
+    graph."""
+    from scipy.stats import chi2
+    og = O.build_csr(np.random.default_rng(11).integers(0, 30, size=(120, 2)), 30)
+    g = P.Graph.from_numpy(30, og.indptr, og.indices)
+    cache = P.build_cache(g, P.degree_probs(g), 30, rng_seed=[0, 33, 0])
+    assert int(cache.nodes.mask.sum()) == int((np.diff(og.indptr) > 0).sum())
+    k, T = 3, 4000
+    seeds = np.arange(30)
+    out = {}
+    for strat in ("GNS", "NS"):
+        cfg = P.SamplerConfig(strategy=strat, fanouts=(k,), batch_size=30, input_layer_cache_only=False,
+                              cache_mode="degree", cache_frac=1.0)
+        cnt = np.zeros((30, 30))
+        for t in range(T):
+            mb = P.build_minibatch(g, cache if strat == "GNS" else None, seeds, cfg, P.BatchRng(0, 0, t))
+            b = mb.blocks[0]
+            np.add.at(cnt, (b.dst_nodes.cpu().numpy()[b.edge_dst.cpu().numpy()], b.edge_node.cpu().numpy()), 1)
+        out[strat] = cnt
+    deg = np.diff(og.indptr)
+    for strat, cnt in out.items():
+        stat, dof = 0.0, 0
+        for v in range(30):
+            d = deg[v]
+            if d <= k:       # every neighbour, every time
+                nb = og.indices[og.indptr[v]:og.indptr[v + 1]]
+                assert np.all(cnt[v, nb] == T), (strat, v)
+                continue
+            nb = og.indices[og.indptr[v]:og.indptr[v + 1]]
+            e = T * k / d
+            stat += float(((cnt[v, nb] - e) ** 2 / e).sum())
+            dof += d - 1
+        assert chi2.sf(stat, max(dof, 1)) > 0.01, (strat, stat, dof)
+
+
+def test_ns_weighted_sum_unbiased(P):
+    """E[sum over sampled u of w_u h_u] = sum over N(v) of h_u
+    for NS weights deg/min(k,deg) (50-node graph; 100 disjoint copies per
+    batch x 1000 batches = 1e5 trials per node), relative error < 2%."""
+    rng = np.random.default_rng(3)
+    base = rng.integers(0, 50, size=(200, 2))
+    copies = 100
+    edges = np.concatenate([base + 50 * c for c in range(copies)])
+    n = 50 * copies
+    og = O.build_csr(edges, n)
+    g = P.Graph.from_numpy(n, og.indptr, og.indices)
+    h = rng.uniform(0.5, 1.5, size=50)
+    hh = np.tile(h, copies)
+    k = 3
+    cfg = P.SamplerConfig(strategy="NS", fanouts=(k,), batch_size=n)
+    est = np.zeros(50)
+    B = 1000
+    for t in range(B):
+        b = P.build_minibatch(g, None, np.arange(n), cfg, P.BatchRng(7, 0, t)).blocks[0]
+        dst = b.dst_nodes.cpu().numpy()[b.edge_dst.cpu().numpy()]
+        contrib = np.zeros(n)
+        np.add.at(contrib, dst, b.edge_weight.cpu().numpy() * hh[b.edge_node.cpu().numpy()])
+        est += contrib.reshape(copies, 50).sum(0)
+    est /= B * copies
+    full = np.array([hh[og.indices[og.indptr[v]:og.indptr[v + 1]]].sum() for v in range(50)])
+    live = full > 0
+    assert np.all(np.abs(est[live] / full[live] - 1) < 0.02), np.abs(est[live] / full[live] - 1).max()
+
+
+def test_gns_input_node_reduction(P):
+    """SPEC.md:287 (Table 3 analog): on a power-law graph (100K nodes, batch
+    1000) GNS with cache 1%, fanouts (15, 10) and a cache-only input layer
+    needs < 0.5x the input nodes of NS with fanouts (15, 10, 5)."""
+    g = P.generate_powerlaw_device(100_000, 250_000, alpha=0.6, offset=10.0, seed=1)
+    gns = P.SamplerConfig(strategy="GNS", fanouts=(15, 10), batch_size=1000, cache_frac=0.01, cache_mode="degree",
+                          input_layer_cache_only=True)
+    ns = P.SamplerConfig(strategy="NS", fanouts=(15, 10, 5), batch_size=1000)
+    cache = P.build_cache(g, P.degree_probs(g), 1000, rng_seed=[0, 33, 0])
+    rng = np.random.default_rng(0)
+    n_g, n_n = [], []
+    for t in range(10):
+        targets = rng.choice(100_000, 1000, replace=False)
+        n_g.append(P.build_minibatch(g, cache, targets, gns, P.BatchRng(0, 0, t)).input_nodes.numel())
+        n_n.append(P.build_minibatch(g, None, targets, ns, P.BatchRng(0, 0, t)).input_nodes.numel())
+    assert np.mean(n_g) < 0.5 * np.mean(n_n), (np.mean(n_g), np.mean(n_n))
+
+
+def test_numpy_generator_as_rng(P):
+    """A numpy Generator passed as rng (the reference's duck-typed hook,
+    sampling.py:93-97) seeds the Philox key: deterministic in its state,
+    different for a different state."""
+    og = _hub_graph(2000, 5)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy="NS", fanouts=(5, 3), batch_size=100)
+
+    def draw(seed):
+        mb = P.build_minibatch(g, None, np.arange(100), cfg, np.random.default_rng(seed))
+        return [{f: getattr(b.to_numpy(), f) for f in FIELDS} for b in mb.blocks]
+    a, b, c = draw(5), draw(5), draw(6)
+    assert all(np.array_equal(x[f], y[f]) for x, y in zip(a, b) for f in FIELDS)
+    assert not all(np.array_equal(x[f], y[f]) for x, y in zip(a, c) for f in ("src_nodes", "edge_src"))
