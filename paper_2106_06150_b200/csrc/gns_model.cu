@@ -479,6 +479,235 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel
   }
 }
 
+// Narrow rows (float32, D <= 128), rows staged 32 at a time (the input
+// layer: fused feature gather + mean aggregation).  A warp owns a chunk of 32
+// consecutive dst rows; their metadata (row scan, self id, degree) and all of
+// their edges (contiguous in the block's cached and fill regions) are read
+// with coalesced loads into shared memory, each lane sorts ITS row's <= MAXL
+// edges by source index in registers (a sorting network), and the warp then
+// walks the rows with nothing but feature-row loads on the critical path:
+// ROWS rows' self + neighbour rows are all issued before the first FMA.
+// Sum order = ascending source index, the same FMA sequence as
+// spmm_fwd_kernel / spmm_fwd_narrow_kernel: bit-identical.  Rows with more
+// than MAXL edges (and chunks whose edges overflow the staging buffer) take
+// the per-row path of spmm_fwd_narrow_kernel.
+constexpr int kChunkRows = 32;
+
+// x / d correctly rounded (== __fdiv_rn(x, d)) for an integer 1 <= d < 2^26,
+// without the division subroutine: rd = RN64(1/d), RN32(RN64(x * rd)).  The
+// exact quotient x/d is never a float rounding midpoint (a 25-bit odd
+// significand cannot divide a 24-bit one) and stays >= 2^-25 / d relative
+// away from one, while the two fp64 roundings add < 2^-51: the float
+// rounding is the same as for the exact quotient.
+__device__ __forceinline__ float div_by_count(float x, double rd) {
+  return __double2float_rn(__dmul_rn((double)x, rd));
+}
+__device__ __forceinline__ float4 vdiv_count(const float4& a, double rd) {
+  return make_float4(div_by_count(a.x, rd), div_by_count(a.y, rd), div_by_count(a.z, rd), div_by_count(a.w, rd));
+}
+
+template <int MAXL>
+__device__ __forceinline__ void sort_pairs(int32_t (&k)[MAXL], float (&v)[MAXL]) {
+  // odd-even transposition network: MAXL rounds, registers only
+#pragma unroll
+  for (int rnd = 0; rnd < MAXL; ++rnd) {
+#pragma unroll
+    for (int i = rnd & 1; i + 1 < MAXL; i += 2) {
+      const bool sw = k[i + 1] < k[i];
+      const int32_t a = sw ? k[i + 1] : k[i], b = sw ? k[i] : k[i + 1];
+      const float x = sw ? v[i + 1] : v[i], y = sw ? v[i] : v[i + 1];
+      k[i] = a; k[i + 1] = b; v[i] = x; v[i + 1] = y;
+    }
+  }
+}
+
+// one dst row through the per-row (rank-by-count) path; every lane calls it
+template <bool RELU>
+__device__ __noinline__ void narrow_row_slow(const float* __restrict__ h, int64_t ld_h, const int32_t* __restrict__ eidx,
+                                                const double* __restrict__ ew, int64_t cb, int nc, int64_t fb, int L,
+                                                int lane, bool on, float4& acc) {
+  for (int t = 0; t < L; ++t) {
+    int32_t best = INT32_MAX;
+    float bw = 0.f;
+    for (int i = lane; i < L; i += 32) {
+      const int64_t e = i < nc ? cb + i : fb + (i - nc);
+      const int32_t v = eidx[e];
+      int rk = 0;
+      for (int j = 0; j < L; ++j) {
+        const int64_t ej = j < nc ? cb + j : fb + (j - nc);
+        rk += eidx[ej] < v;
+      }
+      if (rk == t) {
+        best = v;
+        bw = (float)ew[e];
+      }
+    }
+    const unsigned m = __ballot_sync(GNS_FULL, best != INT32_MAX);
+    const int sl = __ffs(m) - 1;
+    const int32_t iu = __shfl_sync(GNS_FULL, best, sl);
+    const float wu = __shfl_sync(GNS_FULL, bw, sl);
+    if (on) vfma<true>(acc, wu, ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)iu * ld_h) + lane));
+  }
+}
+
+template <bool RELU, bool GATHER, int MAXL, int ROWS, int kMinBlocks>
+__global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_chunk_kernel(const float* __restrict__ h, int64_t ld_h,
+                                                                        int dim, BlockView bv,
+                                                                        float* __restrict__ cat, int64_t ld_cat,
+                                                                        int64_t pad_rows,
+                                                                        const int32_t* __restrict__ edge_node,
+                                                                        const int32_t* __restrict__ dst_ids,
+                                                                        int64_t pad_chunk = 0) {
+  constexpr int CAP = kChunkRows * MAXL;  // staged edges per warp
+  constexpr int W = kSpmmBlock / 32;
+  __shared__ int32_t s_raw[W][CAP];       // chunk edges in position order (cached, then fill)
+  __shared__ float s_rw[W][CAP];
+  __shared__ int32_t s_idx[W][CAP];       // per row, sorted by source index
+  __shared__ float s_w[W][CAP];
+  __shared__ int32_t s_self[W][kChunkRows], s_base[W][kChunkRows], s_len[W][kChunkRows];
+  __shared__ double s_rnorm[W][kChunkRows];   // 1 / max(deg, 1), fp64
+  const int32_t* __restrict__ eidx = GATHER ? edge_node : bv.edge_src;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t n = bv.counts[GNS_CNT_DST];
+  const int64_t tm = (int64_t)(bv.row_scan[n] >> 32);
+  const int dv = dim >> 2;
+  const bool on = lane < dv;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  for (int64_t ch = gw; ch < nchunks; ch += nw) {
+    const int64_t r0 = ch * kChunkRows;
+    const int rows = (int)min((int64_t)kChunkRows, n - r0);
+    unsigned fast;
+    {
+      // ---- stage the chunk: per-lane row metadata, then its edges
+      uint64_t s0 = 0, s1 = 0;
+      int32_t self = 0;
+      int deg = 1;
+      if (lane < rows) {
+        s0 = bv.row_scan[r0 + lane];
+        s1 = bv.row_scan[r0 + lane + 1];
+        self = GATHER ? dst_ids[r0 + lane] : bv.self_pos[r0 + lane];
+        deg = max(bv.dst_degree[r0 + lane], 1);
+      }
+      const uint64_t last0 = __shfl_sync(GNS_FULL, s0, 0), last1 = __shfl_sync(GNS_FULL, s1, rows - 1);
+      const int64_t c_begin = (int64_t)(last0 >> 32), f_begin = tm + (int64_t)(last0 & 0xffffffffull);
+      const int nC = (int)((int64_t)(last1 >> 32) - c_begin);
+      const int nF = (int)(tm + (int64_t)(last1 & 0xffffffffull) - f_begin);
+      // chunk-relative positions of my row's cached / fill edges
+      const int cpos = (int)((int64_t)(s0 >> 32) - c_begin);
+      const int fpos = nC + (int)(tm + (int64_t)(s0 & 0xffffffffull) - f_begin);
+      const int nc = lane < rows ? (int)((s1 >> 32) - (s0 >> 32)) : 0;
+      const int L = lane < rows ? nc + (int)((s1 & 0xffffffffull) - (s0 & 0xffffffffull)) : 0;
+      const bool staged = nC + nF <= CAP;
+      // exclusive prefix of the rows' edge counts = each row's slot base
+      int base = L;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(GNS_FULL, base, o);
+        if (lane >= o) base += y;
+      }
+      base -= L;
+      s_self[wib][lane] = self;
+      s_rnorm[wib][lane] = __drcp_rn((double)deg);
+      s_base[wib][lane] = base;
+      s_len[wib][lane] = L;
+      if (staged) {
+        for (int i = lane; i < nC; i += 32) {
+          s_raw[wib][i] = eidx[c_begin + i];
+          s_rw[wib][i] = (float)bv.edge_weight[c_begin + i];
+        }
+        for (int i = lane; i < nF; i += 32) {
+          s_raw[wib][nC + i] = eidx[f_begin + i];
+          s_rw[wib][nC + i] = (float)bv.edge_weight[f_begin + i];
+        }
+        __syncwarp();
+        if (L <= MAXL) {
+          int32_t k[MAXL];
+          float v[MAXL];
+#pragma unroll
+          for (int t = 0; t < MAXL; ++t) {
+            k[t] = INT32_MAX;
+            v[t] = 0.f;
+            if (t < L) {
+              const int p = t < nc ? cpos + t : fpos + (t - nc);
+              k[t] = s_raw[wib][p];
+              v[t] = s_rw[wib][p];
+            }
+          }
+          sort_pairs<MAXL>(k, v);
+#pragma unroll
+          for (int t = 0; t < MAXL; ++t)
+            if (t < L) {
+              s_idx[wib][base + t] = k[t];
+              s_w[wib][base + t] = v[t];
+            }
+        }
+      }
+      fast = __ballot_sync(GNS_FULL, staged && lane < rows && L <= MAXL);
+      __syncwarp();
+    }
+    // ---- the rows: ROWS at a time, every feature row in flight before any FMA
+    for (int j0 = 0; j0 < rows; j0 += ROWS) {
+      float4 xs[ROWS], x[ROWS][MAXL];
+#pragma unroll
+      for (int q = 0; q < ROWS; ++q) {
+        const int j = j0 + q;
+        const int Lj = (j < rows && ((fast >> j) & 1)) ? s_len[wib][j] : 0;
+        const int bj = s_base[wib][j & 31];
+        xs[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (on && j < rows && ((fast >> j) & 1))
+          xs[q] = ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)s_self[wib][j] * ld_h) + lane);
+#pragma unroll
+        for (int t = 0; t < MAXL; ++t) {
+          // defined on every path: a conditionally kept old value would pin
+          // the array in local memory across iterations
+          x[q][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (on && t < Lj)
+            x[q][t] = ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)s_idx[wib][bj + t] * ld_h) + lane);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < ROWS; ++q) {
+        const int j = j0 + q;
+        if (j >= rows || !((fast >> j) & 1)) continue;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int Lj = s_len[wib][j], bj = s_base[wib][j];
+#pragma unroll
+        for (int t = 0; t < MAXL; ++t)
+          if (on && t < Lj) vfma<true>(acc, s_w[wib][bj + t], x[q][t]);
+        float4* crow = reinterpret_cast<float4*>(cat + (r0 + j) * ld_cat);
+        if (on) {
+          crow[lane] = xs[q];
+          crow[dv + lane] = vdiv_count(acc, s_rnorm[wib][j]);
+        }
+      }
+    }
+    // wide rows / an overflowing chunk: the per-row path (rare; kept out of
+    // the loop above so no feature registers are live across it)
+    const unsigned slow = ~fast & (rows == 32 ? GNS_FULL : ((1u << rows) - 1u));
+    for (unsigned m = slow; m; m &= m - 1) {
+      const int j = __ffs(m) - 1;
+      const uint64_t a0 = bv.row_scan[r0 + j], a1 = bv.row_scan[r0 + j + 1];
+      const int64_t cbs = (int64_t)(a0 >> 32), fbs = tm + (int64_t)(a0 & 0xffffffffull);
+      const int ncs = (int)((a1 >> 32) - (a0 >> 32));
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      narrow_row_slow<RELU>(h, ld_h, eidx, bv.edge_weight, cbs, ncs, fbs, s_len[wib][j], lane, on, acc);
+      float4* crow = reinterpret_cast<float4*>(cat + (r0 + j) * ld_cat);
+      if (on) {
+        crow[lane] = ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)s_self[wib][j] * ld_h) + lane);
+        crow[dv + lane] = vdiv_count(acc, s_rnorm[wib][j]);
+      }
+    }
+    __syncwarp();
+  }
+  const int64_t pad_end = pad_chunk > 0 ? min(pad_rows, (n + pad_chunk - 1) / pad_chunk * pad_chunk) : pad_rows;
+  for (int64_t r = n + gw; r < pad_end; r += nw) {
+    float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
+    for (int c = lane; c < 2 * dv; c += 32) crow[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // Rows of 32 < dim/4 <= 32*CH float4 chunks (the hidden layers, D = 256:
 // CH = 2), float32, RELU on load: the narrow kernel's structure — lane-held
 // edges, shuffle ranks, G neighbour rows in flight — with CH chunks per lane,
@@ -696,7 +925,7 @@ __global__ void __launch_bounds__(kSpmmBlock, 4) spmm_fwd_wide_split_kernel(cons
 }
 
 // experiment knobs (gns_tune)
-static int g_tune_narrow = 1;  // narrow-row forward SpMM variant (0 = generic)
+static int g_tune_narrow = 2;  // narrow-row forward SpMM: 0 generic, 1 per-row narrow, 2+ chunk-staged
 static int g_tune_wide = 2;    // hidden-layer forward: 2 = column-split, 1 = spmm_fwd_wide_kernel, 0 = generic
 
 // Forward SpMM grids: one wave of persistent CTAs (grid-stride rows).  Short
@@ -1456,8 +1685,20 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
   BlockView bv = view_of(block);
   const int dv = dim / 4;
-  (void)max_row_edges;
-  if (dv <= 32 && g_tune_narrow == 1) {
+#define GNS_CHUNK(R, MB)                                                                                       \
+  spmm_fwd_chunk_kernel<false, true, 6, R, MB><<<spmm_grid(spmm_fwd_chunk_kernel<false, true, 6, R, MB>, rows),      \
+                                                 kSpmmBlock, 0, stream>>>(table, ld_table, dim, bv, cat, ld_cat,      \
+                                                                          pad_rows, block->edge_node, dst_ids,        \
+                                                                          pad_chunk)
+  if (dv <= 32 && max_row_edges <= 6 && g_tune_narrow >= 2) {
+    if (g_tune_narrow == 2) GNS_CHUNK(1, 4);
+    else if (g_tune_narrow == 3) GNS_CHUNK(2, 4);
+    else if (g_tune_narrow == 4) GNS_CHUNK(1, 5);
+    else GNS_CHUNK(1, 6);
+    return check_launch("spmm_fwd_gather");
+  }
+#undef GNS_CHUNK
+  if (dv <= 32 && g_tune_narrow >= 1) {
     spmm_fwd_narrow_kernel<false, true><<<spmm_grid(spmm_fwd_narrow_kernel<false, true>, rows), kSpmmBlock, 0,
                                           stream>>>(table, ld_table, dim, bv, cat, ld_cat,
                                                                         pad_rows, block->edge_node, dst_ids,

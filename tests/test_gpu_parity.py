@@ -544,6 +544,39 @@ def test_spmm_fwd_gather_equals_gather_then_spmm(P, dim):
             assert torch.equal(c, d), li
 
 
+@pytest.mark.parametrize("dim", [16, 64, 128])
+@pytest.mark.parametrize("fanouts", [(5, 3), (40, 3)])
+def test_spmm_fwd_gather_chunk_kernel_variants(P, dim, fanouts):
+    """The chunk-staged input-layer kernel (32 rows' metadata and edges staged
+    in shared memory, per-row register sort, all feature rows in flight; its
+    per-row fallback for rows with > 6 edges and overflowing chunks, forced
+    here by a fanout hint of 5 on blocks with up to 40 edges per row) is
+    bit-identical to the per-row narrow kernel and the generic kernel, every
+    variant, padding included."""
+    from paper_2106_06150_b200 import _lib
+    og = _hub_graph(4000, 19)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy="NS", fanouts=fanouts, batch_size=300, seed=2)
+    targets = np.random.default_rng(2).choice(og.num_nodes, 300, replace=False)
+    mb = P.build_minibatch(g, None, targets, cfg, P.BatchRng(2, 0, 0))
+    feats = torch.randn(og.num_nodes, dim, device="cuda")
+    try:
+        for bg in mb.blocks:
+            nd = bg.dst_nodes.numel()
+            dst = bg.dst_nodes.to(torch.int32).contiguous()
+            outs = []
+            for v in (0, 1, 2, 3, 4, 5):
+                _lib.call("gns_tune", b"spmm_narrow", v)
+                o = torch.full((nd + 37, 2 * dim), 5.0, device="cuda")
+                _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), nd, nd + 37, 8, 5,
+                          o.data_ptr(), 2 * dim, _lib.stream_ptr())
+                outs.append(o)
+            for v in range(1, len(outs)):
+                assert torch.equal(outs[0], outs[v]), v
+    finally:
+        _lib.call("gns_tune", b"spmm_narrow", 2)
+
+
 @pytest.mark.parametrize("dim", [132, 256, 512])
 def test_spmm_fwd_wide_equals_generic(P, dim):
     """Hidden-layer forward with relu' bits: the wide kernel (lane-held edges,
@@ -610,7 +643,7 @@ def test_spmm_fwd_narrow_equals_generic(P, dim):
                 assert torch.equal(outs[k0], outs[k1]), key
             assert torch.equal(outs[(0, 0)], outs[(1, 0)])
     finally:
-        _lib.call("gns_tune", b"spmm_narrow", 1)
+        _lib.call("gns_tune", b"spmm_narrow", 2)
 
 
 @pytest.mark.parametrize("dim", [2, 8, 64])
