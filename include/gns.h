@@ -232,16 +232,18 @@ GNS_API int gns_inclusion(const double* probs, int64_t n, int64_t cache_size,
                   double* out, void* stream);
 
 /* Induced cached-neighbour CSR (cache.py:185-197) by filtering the full CSR
- * with the cache bitmap (rows stay ascending).  Two phases: count (writes
+ * with the cache bitmap (rows stay ascending).  Two phases sharing one
+ * workspace (it holds one keep bit per CSR entry between them): count (writes
  * out_c_indptr and *out_nnz_dev), then fill (needs c_indices capacity >= nnz;
- * out_c_pos, optional, receives each entry's position in the full row). */
-GNS_API size_t gns_cached_csr_workspace_size(int64_t num_nodes);
+ * out_c_pos, optional — gns-exact only — receives each entry's position in
+ * the full row). */
+GNS_API size_t gns_cached_csr_workspace_size(int64_t num_nodes, int64_t num_edges);
 GNS_API int gns_cached_csr_count(const gns_graph_t* g, const uint32_t* mask_bits,
                          int64_t* out_c_indptr, int64_t* out_nnz_dev, void* ws,
                          size_t ws_bytes, void* stream);
 GNS_API int gns_cached_csr_fill(const gns_graph_t* g, const uint32_t* mask_bits,
                         const int64_t* c_indptr, int32_t* out_c_indices,
-                        int32_t* out_c_pos, void* stream);
+                        int32_t* out_c_pos, void* ws, size_t ws_bytes, void* stream);
 
 /* estimate_edge_inclusion (sampling.py:269-296): CSR-aligned float64 table
  * q[e] = mean over `resamples` Philox cache draws (key (seed, r), tag 21) of

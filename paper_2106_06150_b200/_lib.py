@@ -93,11 +93,11 @@ _SIGS = {
                                               c_uint32, c_void_p, c_void_p, c_size_t, c_void_p]),
     "gns_inclusion": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                 c_void_p]),
-    "gns_cached_csr_workspace_size": (c_size_t, [c_int64]),
+    "gns_cached_csr_workspace_size": (c_size_t, [c_int64, c_int64]),
     "gns_cached_csr_count": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_size_t, c_void_p]),
     "gns_cached_csr_fill": (c_int32, [POINTER(GnsGraph), c_void_p, c_void_p, c_void_p,
-                                      c_void_p, c_void_p]),
+                                      c_void_p, c_void_p, c_size_t, c_void_p]),
     "gns_sample_workspace_size": (c_size_t, [c_int64, c_int64]),
     "gns_sample_layer": (c_int32, [POINTER(GnsGraph), POINTER(GnsCache), c_void_p, c_void_p,
                                    c_int64, c_int32, c_int32, c_void_p, POINTER(GnsRng), c_void_p,
@@ -219,7 +219,7 @@ def check(rc: int, what: str = ""):
 # device kernels each entry point launches (memsets excluded) — used to report
 # how many of OUR kernels ran inside a timed region
 KERNELS_PER_CALL = {
-    "gns_degree_probs": 1, "gns_random_walk_probs": 9, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 2,
+    "gns_degree_probs": 1, "gns_random_walk_probs": 9, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 3,
     "gns_cached_csr_fill": 1, "gns_estimate_edge_inclusion": 0, "gns_sample_layer": 9, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_batch_targets_sorted": 1, "gns_batch_slice_sorted": 1, "gns_copy_mapped": 1, "gns_errors_accumulate": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
     "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_sum_rows": 1, "gns_graph_switch_begin": 1, "gns_graph_switch_handles": 1, "gns_graph_switch_node": 0, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2, "gns_spmm_fwd_bits": 1, "gns_spmm_bwd_transposed_bits": 2,

@@ -226,25 +226,28 @@ class CacheState:
 
 
 def build_cache(g: Graph, probs: ProbVector, cache_size: int, epoch: int = 0, rng_seed=0,
-                inclusion_mode: str = "analytic", resamples: int = 64) -> CacheState:
-    """cache.py:160-197 (analytic inclusion)."""
+                inclusion_mode: str = "analytic", resamples: int = 64, positions: bool = True) -> CacheState:
+    """cache.py:160-197 (analytic inclusion).  ``positions``: also record each
+    cached-CSR entry's position in its full row (``cached_pos``, read only by
+    the gns-exact policy); False skips that per-row pass."""
     _lib.require_cuda()
     if inclusion_mode == "empirical":
         raise NotImplementedError("empirical inclusion (cache.py:178-181) is outside the B200 "
                                   "hot path (SURVEY.md §8(f)3)")
     if inclusion_mode != "analytic":
         raise ValueError(f"unknown inclusion_mode {inclusion_mode!r}")
-    return _build_cache_into(None, g, probs, cache_size, epoch, rng_seed)
+    return _build_cache_into(None, g, probs, cache_size, epoch, rng_seed, positions)
 
 
-def refresh_cache(state: CacheState, g: Graph, probs: ProbVector, cache_size: int, epoch: int, rng_seed) -> bool:
+def refresh_cache(state: CacheState, g: Graph, probs: ProbVector, cache_size: int, epoch: int, rng_seed,
+                  positions: bool = True) -> bool:
     """build_cache into an existing CacheState of the same graph and cache
     size (the per-epoch refresh of pool.py:133-135), in place: ``state`` is
     the new cache afterwards.  Device addresses stay the same unless the new
     cached CSR outgrows its buffer — then ``state`` gets larger buffers (still
     the same object) and CUDA graphs that captured the old addresses must be
     re-captured.  Returns True when every address was kept."""
-    return refresh_finish(refresh_begin(state, g, probs, cache_size, epoch, rng_seed))
+    return refresh_finish(refresh_begin(state, g, probs, cache_size, epoch, rng_seed, positions=positions))
 
 
 def empty_like(state: CacheState, g: Graph) -> CacheState:
@@ -278,9 +281,10 @@ class PendingRefresh:
     to pinned host memory; nothing waits on the host.  ``ready()`` polls;
     ``refresh_finish`` sizes the cached CSR and enqueues its fill."""
 
-    def __init__(self, state, g, probs, epoch, stream, counts, nnz, host, ev, ws):
+    def __init__(self, state, g, probs, epoch, stream, counts, nnz, host, ev, ws, positions):
         self.state, self.g, self.probs, self.epoch, self.stream = state, g, probs, epoch, stream
         self.counts, self.nnz, self.host, self.ev, self._ws = counts, nnz, host, ev, ws
+        self.positions = positions
         self.done = None      # event after the fill (refresh_finish)
 
     def ready(self) -> bool:
@@ -288,7 +292,7 @@ class PendingRefresh:
 
 
 def refresh_begin(state, g: Graph, probs: ProbVector, cache_size: int, epoch: int, rng_seed,
-                  stream=None) -> PendingRefresh:
+                  stream=None, positions: bool = True) -> PendingRefresh:
     """Enqueue draw + inclusion + cached-CSR count into ``state``'s buffers
     (``state=None``: fresh buffers) on ``stream`` (default: current)."""
     probs = probs.normalize()
@@ -309,7 +313,8 @@ def refresh_begin(state, g: Graph, probs: ProbVector, cache_size: int, epoch: in
         _lib.call("gns_inclusion", probs.weights.data_ptr(), n, 0, counts.data_ptr(),
                   counts[1:].data_ptr(), incl.data_ptr(), sp)
         nnz = torch.zeros(1, dtype=torch.int64, device=g.device)
-        ws = _lib.workspace(_lib.lib().gns_cached_csr_workspace_size(n), g.device)
+        # the keep bits of every CSR entry live in the workspace until the fill
+        ws = _lib.workspace(_lib.lib().gns_cached_csr_workspace_size(n, g.num_edges), g.device)
         _lib.call("gns_cached_csr_count", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
                   nnz.data_ptr(), ws.data_ptr(), ws.numel(), sp)
         host = torch.empty(2, dtype=torch.int64).pin_memory()
@@ -319,7 +324,7 @@ def refresh_begin(state, g: Graph, probs: ProbVector, cache_size: int, epoch: in
         ev.record(stream)
     if state is None:
         state = (ids, bits, counts, incl, c_indptr)
-    return PendingRefresh(state, g, probs, epoch, stream, counts, nnz, host, ev, ws)
+    return PendingRefresh(state, g, probs, epoch, stream, counts, nnz, host, ev, ws, positions)
 
 
 def refresh_finish(p: PendingRefresh):
@@ -347,7 +352,8 @@ def refresh_finish(p: PendingRefresh):
         else:
             ids, bits, counts, incl, c_indptr = p.state
         _lib.call("gns_cached_csr_fill", g.cstruct(), bits.data_ptr(), c_indptr.data_ptr(),
-                  c_indices.data_ptr(), c_pos.data_ptr(), _lib.stream_ptr(stream))
+                  c_indices.data_ptr(), c_pos.data_ptr() if p.positions else None, p._ws.data_ptr(),
+                  p._ws.numel(), _lib.stream_ptr(stream))
         p.done = torch.cuda.Event()
         p.done.record(stream)
     if state is not None:
@@ -371,6 +377,6 @@ def refresh_finish(p: PendingRefresh):
     return st
 
 
-def _build_cache_into(state, g, probs, cache_size, epoch, rng_seed):
-    r = refresh_finish(refresh_begin(state, g, probs, cache_size, epoch, rng_seed))
+def _build_cache_into(state, g, probs, cache_size, epoch, rng_seed, positions=True):
+    r = refresh_finish(refresh_begin(state, g, probs, cache_size, epoch, rng_seed, positions=positions))
     return state if state is not None else r

@@ -432,6 +432,11 @@ class GraphedTrainer:
             cur.wait_event(ev)
 
     # -- cache + capture ------------------------------------------------------------
+    @property
+    def _positions(self) -> bool:
+        """Cached-CSR row positions are read only by the gns-exact policy."""
+        return self.cfg.weight_policy == "gns-exact"
+
     def _cache_size(self) -> int:
         return int(round(self.cfg.cache_frac * self.g.num_nodes))     # pool.py:114
 
@@ -482,12 +487,15 @@ class GraphedTrainer:
             t = self.cur if self.cache is None else 1 - self.cur
             if self.csets[t] is None:
                 if self.csets[1 - t] is None:
-                    self.csets[t] = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch, rng_seed=seed)
+                    self.csets[t] = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch, rng_seed=seed,
+                                                          positions=self._positions)
                 else:
                     self.csets[t] = cache_mod.empty_like(self.csets[1 - t], self.g)
-                    cache_mod.refresh_cache(self.csets[t], self.g, self._probs, cs, epoch, seed)
+                    cache_mod.refresh_cache(self.csets[t], self.g, self._probs, cs, epoch, seed,
+                                            positions=self._positions)
                 self._free_execs(t)
-            elif not cache_mod.refresh_cache(self.csets[t], self.g, self._probs, cs, epoch, seed):
+            elif not cache_mod.refresh_cache(self.csets[t], self.g, self._probs, cs, epoch, seed,
+                                             positions=self._positions):
                 self._free_execs(t)
             if self.placement == "mixed":
                 self._fill_table(t, torch.cuda.current_stream())
@@ -513,7 +521,7 @@ class GraphedTrainer:
         rs = self.refresh_stream
         rs.wait_stream(torch.cuda.current_stream())
         p = cache_mod.refresh_begin(self.csets[t], self.g, self._probs, self._cache_size(), epoch,
-                                    [self.cfg.seed, _CACHE, epoch], stream=rs)
+                                    [self.cfg.seed, _CACHE, epoch], stream=rs, positions=self._positions)
         self._pf = (t, p, 1)
 
     def _prefetch_poll(self, block: bool = False):

@@ -141,7 +141,8 @@ class SamplerPool:
             self._probs = cache_probs(self.graph, self.config)
         cache_size = int(round(self.config.cache_frac * self.graph.num_nodes))
         self.cache = cache_mod.build_cache(self.graph, self._probs, cache_size, epoch=epoch,
-                                           rng_seed=[self.config.seed, _CACHE, epoch])
+                                           rng_seed=[self.config.seed, _CACHE, epoch],
+                                           positions=self.config.weight_policy == "gns-exact")
         if self.config.weight_policy == "gns-exact" and self._tables is None:
             self._tables = exact_tables(self.graph, self.config, self._probs, cache_size)
 

@@ -983,6 +983,30 @@ def test_engine_epoch_slots_bit_exact_vs_oracle(P, S, period):
     assert seen == [(e, i) for e in range(3) for i in range(len(batches))]
 
 
+@pytest.mark.parametrize("n,pairs", [(4000, 0), (3000, 1024 * 7), (20000, 100000)])
+def test_cached_csr_flat_passes_equal_per_row(P, n, pairs):
+    """The cached CSR from the flat (entry-parallel) passes — keep bits per
+    CSR entry, tile counts, scanned tile offsets, c_indptr from popcounts,
+    flat compaction — equals the per-row path (positions=True) and the oracle's
+    filter of the full CSR (cache.py:185-197), for edge counts on and off the
+    1024-entry tile boundary."""
+    rng = np.random.default_rng(n + pairs)
+    if pairs == 0:
+        og = _hub_graph(n, 3)
+    else:
+        og = O.build_csr(rng.integers(0, n, size=(pairs, 2)), n)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    probs = P.degree_probs(g)
+    cs = max(1, og.num_nodes // 20)
+    a = P.build_cache(g, probs, cs, rng_seed=[0, 33, 4], positions=True)
+    b = P.build_cache(g, probs, cs, rng_seed=[0, 33, 4], positions=False)
+    assert torch.equal(a.cached_indptr, b.cached_indptr)
+    assert torch.equal(a.cached_indices, b.cached_indices)
+    ci, cx = O.cached_csr_by_filter(og, a.nodes.mask.cpu().numpy())
+    assert np.array_equal(b.cached_indptr.cpu().numpy(), ci)
+    assert np.array_equal(b.cached_indices.cpu().numpy(), cx)
+
+
 def test_refresh_cache_grows_cached_csr_in_place(P):
     """a refresh whose cached CSR outgrows the buffer gets larger
     buffers on the SAME CacheState (no stale pointers) and reports it."""
