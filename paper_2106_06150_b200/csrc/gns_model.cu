@@ -927,6 +927,7 @@ __global__ void __launch_bounds__(kSpmmBlock, 4) spmm_fwd_wide_split_kernel(cons
 // experiment knobs (gns_tune)
 static int g_tune_narrow = 2;  // narrow-row forward SpMM: 0 generic, 1 per-row narrow, 2+ chunk-staged
 static int g_tune_wide = 2;    // hidden-layer forward: 2 = column-split, 1 = spmm_fwd_wide_kernel, 0 = generic
+static int g_tune_bwd = 4;     // transposed SpMM (bits): >= 1 lane-staged (rows in flight / occupancy, see the dispatch), 0 = per-row
 
 // Forward SpMM grids: one wave of persistent CTAs (grid-stride rows).  Short
 // CTAs (k rows per warp, many waves) were measured slower both alone and
@@ -992,50 +993,93 @@ __device__ __forceinline__ void put_twn(BlockView bv, const uint64_t* a, int L, 
   }
 }
 
+// Per transposed row: sort its (dst << 32 | edge) keys ascending and write
+// the coefficients twn.  A warp takes 32 consecutive rows; rows of <= 8
+// entries (nearly all: a sampled block's source rows have ~1 edge) are sorted
+// by their own lane in registers, longer rows by the whole warp (rank by
+// shuffles up to 32 entries, a bitonic network in place beyond).  Keys are
+// unique, so every path gives the same order.
+constexpr int kTsortLane = 8;
 __global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uint64_t* __restrict__ tkeys,
                              float* __restrict__ twn) {
   const int lane = threadIdx.x & 31;
   const int64_t n = bv.counts[GNS_CNT_SRC];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = gw; s < n; s += nw) {
-    const int b = tptr[s], L = tptr[s + 1] - b;
-    if (L <= 0) continue;
-    uint64_t* a = tkeys + b;
-    if (L <= 32) {
-      uint64_t x = lane < L ? a[lane] : ~0ull;
-      int rank = 0;
-      for (int j = 0; j < L; ++j) rank += __shfl_sync(GNS_FULL, x, j) < x;
-      __syncwarp();
-      if (lane < L) {
-        a[rank] = x;
-        const int32_t d = (int32_t)(x >> 32), e = (int32_t)(x & 0xffffffffu);
-        twn[b + rank] = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
-      }
-      __syncwarp();
-      continue;
+  for (int64_t s0 = gw * 32; s0 < n; s0 += nw * 32) {
+    const int64_t s = s0 + lane;
+    int b = 0, L = 0;
+    if (s < n) {
+      b = tptr[s];
+      L = tptr[s + 1] - b;
     }
-    int P = 1;
-    while (P < L) P <<= 1;
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int t = lane; t < P / 2; t += 32) {
-        int half = k >> 1;
-        int i = (t / half) * k + (t % half);
-        int j = i ^ (k - 1);
-        if (j < L && a[j] < a[i]) { uint64_t x = a[i]; a[i] = a[j]; a[j] = x; }
+    if (L > 0 && L <= kTsortLane) {
+      uint64_t x[kTsortLane];
+#pragma unroll
+      for (int i = 0; i < kTsortLane; ++i) x[i] = i < L ? tkeys[b + i] : ~0ull;
+#pragma unroll
+      for (int rnd = 0; rnd < kTsortLane; ++rnd)   // odd-even transposition network
+#pragma unroll
+        for (int i = rnd & 1; i + 1 < kTsortLane; i += 2) {
+          const uint64_t lo = x[i] < x[i + 1] ? x[i] : x[i + 1], hi = x[i] < x[i + 1] ? x[i + 1] : x[i];
+          x[i] = lo;
+          x[i + 1] = hi;
+        }
+      float wv[kTsortLane];
+#pragma unroll
+      for (int i = 0; i < kTsortLane; ++i) {
+        wv[i] = 0.f;
+        if (i < L) {
+          const int32_t d = (int32_t)(x[i] >> 32), e = (int32_t)(x[i] & 0xffffffffu);
+          wv[i] = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
+        }
       }
-      __syncwarp();
-      for (int st = k >> 2; st >= 1; st >>= 1) {
-        for (int t = lane; t < P / 2; t += 32) {
-          int i = (t / st) * 2 * st + (t % st);
-          int j = i + st;
-          if (j < L && a[j] < a[i]) { uint64_t x = a[i]; a[i] = a[j]; a[j] = x; }
+#pragma unroll
+      for (int i = 0; i < kTsortLane; ++i)
+        if (i < L) {
+          tkeys[b + i] = x[i];
+          twn[b + i] = wv[i];
+        }
+    }
+    for (unsigned big = __ballot_sync(GNS_FULL, L > kTsortLane); big; big &= big - 1) {
+      const int j = __ffs(big) - 1;
+      const int bj = __shfl_sync(GNS_FULL, b, j), Lj = __shfl_sync(GNS_FULL, L, j);
+      uint64_t* a = tkeys + bj;
+      if (Lj <= 32) {
+        uint64_t x = lane < Lj ? a[lane] : ~0ull;
+        int rank = 0;
+        for (int i = 0; i < Lj; ++i) rank += __shfl_sync(GNS_FULL, x, i) < x;
+        __syncwarp();
+        if (lane < Lj) {
+          a[rank] = x;
+          const int32_t d = (int32_t)(x >> 32), e = (int32_t)(x & 0xffffffffu);
+          twn[bj + rank] = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
         }
         __syncwarp();
+        continue;
       }
+      int P = 1;
+      while (P < Lj) P <<= 1;
+      for (int k = 2; k <= P; k <<= 1) {
+        for (int t = lane; t < P / 2; t += 32) {
+          int half = k >> 1;
+          int i = (t / half) * k + (t % half);
+          int jj = i ^ (k - 1);
+          if (jj < Lj && a[jj] < a[i]) { uint64_t x = a[i]; a[i] = a[jj]; a[jj] = x; }
+        }
+        __syncwarp();
+        for (int st = k >> 2; st >= 1; st >>= 1) {
+          for (int t = lane; t < P / 2; t += 32) {
+            int i = (t / st) * 2 * st + (t % st);
+            int jj = i + st;
+            if (jj < Lj && a[jj] < a[i]) { uint64_t x = a[i]; a[i] = a[jj]; a[jj] = x; }
+          }
+          __syncwarp();
+        }
+      }
+      put_twn(bv, a, Lj, twn + bj, lane);
+      __syncwarp();
     }
-    put_twn(bv, a, L, twn + b, lane);
-    __syncwarp();
   }
 }
 
@@ -1190,6 +1234,159 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
       T t = 0;
 #pragma unroll
       for (int w = 0; w < kSpmmBlock / 32; ++w) t += red[w][col];
+      colpart[(int64_t)blockIdx.x * dim + col] = t;
+    }
+  }
+}
+
+// Lane-staged transposed SpMM (float32, relu' from the forward's bits; the
+// default for dim <= 256).  A warp owns kChunkRows consecutive source rows
+// and lane j holds row j's metadata: transpose bounds, self position and
+// relu-bit words (coalesced loads), then the dst and coefficient of the row's
+// first edge (one more).  Nearly every source row of a sampled block has
+// exactly one item (one edge, or only its self row), so the chunk's rows go
+// R at a time with every row's first dcat row requested before the first
+// FMA — about 2 + 32/R dependent round trips per 32 rows instead of ~3 per
+// row.  A row's further items (more edges: hub sources; the self row of a
+// row that also has edges) are read after its first: the per-row FMA order
+// of spmm_bwd_kernel (ascending dst, then the self row, acc starting at 0),
+// so dz is bit-identical.  No shared memory in the row loop (a shared-memory
+// item stream was measured 10-30% slower: short-scoreboard bound).
+template <int CH, int R, int MINB>
+__global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const float* __restrict__ dcat,
+                                                                      int64_t ld_dcat, int dim, BlockView bv,
+                                                                      const int32_t* __restrict__ tptr,
+                                                                      const uint64_t* __restrict__ tkeys,
+                                                                      const int32_t* __restrict__ self_of,
+                                                                      float* __restrict__ dh, int64_t ld_dh,
+                                                                      int64_t pad_rows, float* __restrict__ colpart,
+                                                                      const uint32_t* __restrict__ relu_bits,
+                                                                      const float* __restrict__ twn) {
+  constexpr int W = kSpmmBlock / 32;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t n = bv.counts[GNS_CNT_SRC];
+  const int dv = dim >> 2;
+  const int mw = CH * 4;   // relu-bit words per row: dv <= 32 -> 4, <= 64 -> 8
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  float colacc[CH][4];
+#pragma unroll
+  for (int k = 0; k < CH; ++k)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) colacc[k][q] = 0.f;
+  for (int64_t ch = gw; ch < nchunks; ch += nw) {
+    const int64_t s0 = ch * kChunkRows;
+    const int rows = (int)min((int64_t)kChunkRows, n - s0);
+    int b = 0, e = 0, sd = -1, d0 = 0;
+    float w0 = 0.f;
+    uint4 mb[CH];   // row `lane`'s relu-bit words
+#pragma unroll
+    for (int k = 0; k < CH; ++k) mb[k] = make_uint4(0u, 0u, 0u, 0u);
+    if (lane < rows) {
+      b = tptr[s0 + lane];
+      e = tptr[s0 + lane + 1];
+      sd = self_of[s0 + lane];
+#pragma unroll
+      for (int k = 0; k < CH; ++k) mb[k] = reinterpret_cast<const uint4*>(relu_bits + (s0 + lane) * mw)[k];
+    }
+    if (e > b) {
+      d0 = (int32_t)(tkeys[b] >> 32);
+      w0 = twn[b];
+    }
+    for (int j0 = 0; j0 < rows; j0 += R) {
+      float4 x[R][CH];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        // (the row's scalars are shuffled again when it is consumed: fewer
+        // live registers across the loads)
+        const int j = (j0 + r) & 31;   // rows past `rows` have b == e, sd < 0
+        const int bj = __shfl_sync(GNS_FULL, b, j), ej = __shfl_sync(GNS_FULL, e, j);
+        const int sj = __shfl_sync(GNS_FULL, sd, j), dj = __shfl_sync(GNS_FULL, d0, j);
+        // first item: the first edge's neighbour half, else the self half
+        const bool edge = ej > bj;
+        const float4* src = reinterpret_cast<const float4*>(
+            edge ? dcat + (int64_t)dj * ld_dcat + dim : dcat + (int64_t)(sj < 0 ? 0 : sj) * ld_dcat);
+        const bool any = edge || sj >= 0;
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int c = lane + 32 * k;
+          x[r][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (any && c < dv) x[r][k] = src[c];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int j = j0 + r;
+        if (j >= rows) break;
+        const int bj = __shfl_sync(GNS_FULL, b, j), ej = __shfl_sync(GNS_FULL, e, j);
+        const int sj = __shfl_sync(GNS_FULL, sd, j);
+        const float wj = __shfl_sync(GNS_FULL, w0, j);
+        float4 acc[CH];
+        const bool edge = ej > bj;
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (edge) {
+            vfma<true>(acc[k], wj, x[r][k]);
+          } else if (sj >= 0) {
+            acc[k].x += x[r][k].x; acc[k].y += x[r][k].y;
+            acc[k].z += x[r][k].z; acc[k].w += x[r][k].w;
+          }
+        }
+        if (edge) {
+          for (int t = bj + 1; t < ej; ++t) {   // further edges, ascending dst
+            const float4* src = reinterpret_cast<const float4*>(dcat + (int64_t)(int32_t)(tkeys[t] >> 32) * ld_dcat + dim);
+            const float wn = twn[t];
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+              const int c = lane + 32 * k;
+              if (c < dv) vfma<true>(acc[k], wn, src[c]);
+            }
+          }
+          if (sj >= 0) {   // then the self row
+            const float4* src = reinterpret_cast<const float4*>(dcat + (int64_t)sj * ld_dcat);
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+              const int c = lane + 32 * k;
+              if (c < dv) {
+                const float4 y = src[c];
+                acc[k].x += y.x; acc[k].y += y.y; acc[k].z += y.z; acc[k].w += y.w;
+              }
+            }
+          }
+        }
+        float4* drow = reinterpret_cast<float4*>(dh + (s0 + j) * ld_dh);
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int c = lane + 32 * k;
+          const uint32_t m0 = __shfl_sync(GNS_FULL, mb[k].x, j), m1 = __shfl_sync(GNS_FULL, mb[k].y, j);
+          const uint32_t m2 = __shfl_sync(GNS_FULL, mb[k].z, j), m3 = __shfl_sync(GNS_FULL, mb[k].w, j);
+          if (c >= dv) continue;
+          float4 out;
+          out.x = ((m0 >> lane) & 1u) ? acc[k].x : 0.f;
+          out.y = ((m1 >> lane) & 1u) ? acc[k].y : 0.f;
+          out.z = ((m2 >> lane) & 1u) ? acc[k].z : 0.f;
+          out.w = ((m3 >> lane) & 1u) ? acc[k].w : 0.f;
+          colacc[k][0] += out.x; colacc[k][1] += out.y; colacc[k][2] += out.z; colacc[k][3] += out.w;
+          drow[c] = out;
+        }
+      }
+    }
+  }
+  for (int64_t s = n + gw; s < pad_rows; s += nw)
+    for (int c = lane; c < dv; c += 32) reinterpret_cast<float4*>(dh + s * ld_dh)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (colpart) {
+    __shared__ float red[W][32 * CH * 4];
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[wib][(lane + 32 * k) * 4 + q] = colacc[k][q];
+    __syncthreads();
+    for (int col = threadIdx.x; col < dim; col += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < W; ++w) t += red[w][col];
       colpart[(int64_t)blockIdx.x * dim + col] = t;
     }
   }
@@ -1656,6 +1853,10 @@ int gns_tune(const char* name, int32_t value) {
     g_tune_wide = value;
     return GNS_OK;
   }
+  if (!strcmp(name, "spmm_bwd") && value >= 0 && value <= 5) {
+    g_tune_bwd = value;
+    return GNS_OK;
+  }
   if (gns_sample_tune(name, value) == GNS_OK) return GNS_OK;
   set_error("unknown tuning knob %s (or value %d out of range)", name, value);
   return GNS_EINVAL;
@@ -1782,6 +1983,33 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
   int g2 = 1;
   const int dv = dim / 4;
   // one wave of resident CTAs (<= 8 per SM: the colpart workspace bound)
+#define GNS_BWDC(CH, R, B)                                                                                       \
+  g2 = resident_grid(spmm_bwd_rows_kernel<CH, R, B>, kSpmmBlock, 0,                                             \
+                     want < num_sms() * 8LL ? want : num_sms() * 8LL);                                          \
+  spmm_bwd_rows_kernel<CH, R, B><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,         \
+                                                                w.self_of, dh, ld_dh, pad_rows,                 \
+                                                                db ? (float*)w.colpart : nullptr, relu_bits,    \
+                                                                w.twn)
+  // knob: 1 = R2/4 CTAs per SM, 2 = R2/3, 3 = R4/3, 4 = R4/2, 5 = R8/2
+  if (g_tune_bwd > 0 && dv <= 64) {
+    if (dv <= 32) {
+      GNS_BWDC(1, 4, 4);
+    } else if (g_tune_bwd == 1) {
+      GNS_BWDC(2, 2, 4);
+    } else if (g_tune_bwd == 2) {
+      GNS_BWDC(2, 2, 3);
+    } else if (g_tune_bwd == 3) {
+      GNS_BWDC(2, 4, 3);
+    } else if (g_tune_bwd == 4) {
+      GNS_BWDC(2, 4, 2);
+    } else {
+      GNS_BWDC(2, 8, 2);
+    }
+    GNS_TRY(check_launch("spmm_bwd_bits"));
+    if (db) colsum_launch<float>((const float*)w.colpart, g2, dim, db, stream);
+    return check_launch("spmm_bwd_bits colsum");
+  }
+#undef GNS_BWDC
 #define GNS_BWDB(CH)                                                                                             \
   g2 = resident_grid(spmm_bwd_kernel<float, CH, true>, kSpmmBlock, 0, want < num_sms() * 8LL ? want : num_sms() * 8LL); \
   spmm_bwd_kernel<float, CH, true><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,       \
@@ -1869,7 +2097,7 @@ int gns_block_transpose(const gns_block_t* block, int64_t max_dst, int64_t max_s
   tscan_reduce_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, (unsigned long long*)w.scan);
   tscan_apply_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, w.tptr, (unsigned long long*)w.scan);
   tscatter_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.tptr, w.tkeys);
-  int g2 = grid_for((max_src * 32 + 255) / 256, (long long)sms * 8);
+  int g2 = grid_for((max_src + 255) / 256, (long long)sms * 8);   // a warp per 32 rows
   tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys, w.twn);
   return check_launch("block_transpose");
 }

@@ -35,9 +35,9 @@ constexpr int kThreadLen = 16;    // rows scanning <= 16 positions: one thread p
 constexpr int kStreamK = 8;       // streaming top-k tier: take <= 8 and <= stream_len positions
 static int g_stream_len = 32;     // (gns_tune "stream_len", <= 2047)
 static int g_thread_len = 0;      // (gns_tune "thread_len", <= 16; 0 = no sorting-network tier: measured best)
+static int g_stream_minb = 1;     // (gns_tune "stream_minb": 1, 3, 4) min resident CTAs/SM of the streaming tier
 static int g_sampler_ctas = 0;    // (gns_tune "sampler_ctas") cap grid-stride sampler grids at this many CTAs
                                   // per SM (0 = no cap): leaves SM room to the concurrent training branch
-constexpr int kHubBlock = 512;
 constexpr int kHubCap = 512;
 constexpr int kMaxFanout = 128;
 constexpr uint64_t kTwo53 = 1ull << 53;
@@ -193,8 +193,10 @@ __device__ __forceinline__ bool cached_bit(const uint32_t* __restrict__ mask, in
 // their loads together (seed ids, then the four CSR offsets) instead of one
 // row's dependent chain after another.  Apply kernel: the exclusive scan of
 // row_scan only.
-constexpr int kCntBlock = 256, kCntItems = 4;
+constexpr int kCntBlock = 256;
+static int g_count_items = 4;   // (gns_tune "count_items": 1, 2, 4) rows per thread of the count pass
 
+template <int kCntItems>
 __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __grid_constant__ LayerArgs a,
                                                                        unsigned long long* tile_sums) {
   __shared__ unsigned long long s_warp[kCntBlock / 32 + 1];
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(kCntBlock) layer_count_reduce_kernel(const __g
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = tsum;
 }
 
+template <int kCntItems>
 __global__ void __launch_bounds__(kCntBlock) layer_count_apply_kernel(const __grid_constant__ LayerArgs a,
                                                                       const unsigned long long* tile_sums) {
   const long long n = a.n_dev[0];
@@ -470,7 +473,8 @@ __device__ void warp_select(const LayerArgs& a, const Rng3& rk, const RowInfo& r
   __syncwarp();
 }
 
-// CTA-cooperative selection for hub rows
+// CTA-cooperative selection for hub rows (NT threads per CTA)
+template <int NT>
 __device__ void block_select(const LayerArgs& a, const Rng3& rk, const RowInfo& ri, int64_t r, const PhaseDesc& ph,
                              uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpos, int* s_found) {
   const uint32_t stream = stream_word(32, a.layer, ph.phase);
@@ -481,7 +485,7 @@ __device__ void block_select(const LayerArgs& a, const Rng3& rk, const RowInfo& 
   for (int iter = 0; iter < 64; ++iter) {
     if (threadIdx.x == 0) *s_found = 0;
     __syncthreads();
-    for (int64_t q = threadIdx.x; q < npairs; q += kHubBlock) {
+    for (int64_t q = threadIdx.x; q < npairs; q += NT) {
       uint64_t k0, k1;
       key53_pair(rk.seed, rk.epoch, (uint32_t)ri.node, stream, rk.batch, (uint32_t)q, k0, k1);
 #pragma unroll
@@ -521,7 +525,7 @@ __device__ void block_select(const LayerArgs& a, const Rng3& rk, const RowInfo& 
     __syncthreads();
     return;
   }
-  for (int i = threadIdx.x; i < found; i += kHubBlock) {
+  for (int i = threadIdx.x; i < found; i += NT) {
     const uint64_t ki = bkey[i];
     const uint32_t pi = bpos[i];
     int rank = 0;
@@ -713,7 +717,8 @@ __device__ __forceinline__ void thread_select_stream(const LayerArgs& a, const R
   }
 }
 
-__global__ void __launch_bounds__(256) sample_stream_kernel(const __grid_constant__ LayerArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) sample_stream_kernel(const __grid_constant__ LayerArgs a) {
   const Rng3 rk = batch_rng(a);
   const int64_t nl = a.b.counts[GNS_CNT_STREAMROWS];
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nl; j += (int64_t)gridDim.x * blockDim.x) {
@@ -739,10 +744,14 @@ __global__ void __launch_bounds__(256) sample_thread_kernel(const __grid_constan
   }
 }
 
+// Warp tier, then the hub tier (rows scanning > kHubLen positions, rare) by
+// whole CTAs at the tail of the same launch: one launch less per layer.
 __global__ void __launch_bounds__(kSampBlock, 4) sample_warp_kernel(const __grid_constant__ LayerArgs a) {
+  static_assert(kSampBlock / 32 * kWarpCap >= kHubCap, "hub stage must fit the warps' stages");
   const Rng3 rk = batch_rng(a);
   __shared__ uint64_t s_key[kSampBlock / 32][kWarpCap];
   __shared__ uint32_t s_pos[kSampBlock / 32][kWarpCap];
+  __shared__ int s_found;
   const int w = threadIdx.x >> 5;
   const int64_t nl = a.b.counts[GNS_CNT_WARPROWS];
   const int64_t gw = (blockIdx.x * (int64_t)kSampBlock + threadIdx.x) >> 5;
@@ -755,21 +764,16 @@ __global__ void __launch_bounds__(kSampBlock, 4) sample_warp_kernel(const __grid
     make_phases(a, ri, r, pc, pf);
     warp_select(a, rk, ri, r, (item & 1) ? pf : pc, s_key[w], s_pos[w]);
   }
-}
-
-__global__ void __launch_bounds__(kHubBlock) sample_hub_kernel(const __grid_constant__ LayerArgs a) {
-  const Rng3 rk = batch_rng(a);
-  __shared__ uint64_t s_key[kHubCap];
-  __shared__ uint32_t s_pos[kHubCap];
-  __shared__ int s_found;
   const int nh = a.b.counts[GNS_CNT_HUBS];
+  if ((int)blockIdx.x >= nh) return;   // CTA-uniform
+  __syncthreads();                      // the warps' stages become the CTA's
   for (int h = blockIdx.x; h < nh; h += gridDim.x) {
     const int32_t item = a.b.hub_rows[6 * a.max_dst - 1 - h];
     const int64_t r = item >> 1;
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
-    block_select(a, rk, ri, r, (item & 1) ? pf : pc, s_key, s_pos, &s_found);
+    block_select<kSampBlock>(a, rk, ri, r, (item & 1) ? pf : pc, &s_key[0][0], &s_pos[0][0], &s_found);
   }
 }
 
@@ -1004,7 +1008,7 @@ static size_t sample_ws(int64_t num_nodes, int64_t max_dst, void* base, size_t c
                         DedupWs* d, RowDesc** desc) {
   Workspace w(base, cap);
   dedup_ws(num_nodes, w, d);
-  *tiles = w.take<unsigned long long>(max_dst / (kCntBlock * kCntItems) + 2);
+  *tiles = w.take<unsigned long long>(max_dst / kCntBlock + 2);   // count tiles of >= kCntBlock rows
   *desc = w.take<RowDesc>(max_dst + 1);
   return w.off;
 }
@@ -1067,10 +1071,17 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.thread_len = g_thread_len;
   a.desc = desc;
   a.b = *block;
-  const unsigned tiles = (unsigned)((max_dst + kCntBlock * kCntItems - 1) / (kCntBlock * kCntItems)) + 1;
   GNS_CUDA(cudaMemsetAsync(block->counts, 0, GNS_CNT_N * sizeof(int32_t), stream));
-  layer_count_reduce_kernel<<<tiles, kCntBlock, 0, stream>>>(a, ctiles);
-  layer_count_apply_kernel<<<tiles, kCntBlock, 0, stream>>>(a, ctiles);
+#define GNS_COUNT(IT)                                                                                  \
+  {                                                                                                    \
+    const unsigned tiles = (unsigned)((max_dst + kCntBlock * IT - 1) / (kCntBlock * IT)) + 1;         \
+    layer_count_reduce_kernel<IT><<<tiles, kCntBlock, 0, stream>>>(a, ctiles);                         \
+    layer_count_apply_kernel<IT><<<tiles, kCntBlock, 0, stream>>>(a, ctiles);                          \
+  }
+  if (g_count_items == 1) GNS_COUNT(1)
+  else if (g_count_items == 2) GNS_COUNT(2)
+  else GNS_COUNT(4)
+#undef GNS_COUNT
   GNS_TRY(check_launch("layer_count"));
   const int sms = num_sms();
   // the three tiers work on disjoint (row, phase) lists: thread tier on the
@@ -1080,16 +1091,23 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   // one wave of resident CTAs at most (grid-stride loops over the item lists)
   const long long cap = g_sampler_ctas ? (long long)sms * g_sampler_ctas : (1LL << 30);
   const long long titems = grid_for((2 * max_dst + 255) / 256, cap);
-  sample_stream_kernel<<<resident_grid(sample_stream_kernel, 256, 0, titems), 256, 0, stream>>>(a);
+  if (g_stream_minb == 4)
+    sample_stream_kernel<4><<<resident_grid(sample_stream_kernel<4>, 256, 0, titems), 256, 0, stream>>>(a);
+  else if (g_stream_minb == 3)
+    sample_stream_kernel<3><<<resident_grid(sample_stream_kernel<3>, 256, 0, titems), 256, 0, stream>>>(a);
+  else
+    sample_stream_kernel<1><<<resident_grid(sample_stream_kernel<1>, 256, 0, titems), 256, 0, stream>>>(a);
   GNS_TRY(check_launch("sample_stream"));
-  sample_thread_kernel<<<resident_grid(sample_thread_kernel, 256, 0, titems), 256, 0, stream>>>(a);
-  GNS_TRY(check_launch("sample_thread"));
+  if (g_thread_len > 0) {   // (thread_len 0: phase_tier never picks the sorting-network tier)
+    sample_thread_kernel<<<resident_grid(sample_thread_kernel, 256, 0, titems), 256, 0, stream>>>(a);
+    GNS_TRY(check_launch("sample_thread"));
+  }
+  // warp tier + the hub tier at its tail (at least one CTA per SM for hubs)
   const int grid = resident_grid(sample_warp_kernel, kSampBlock, 0,
-                                 grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock, cap));
+                                 std::max<long long>(sms, grid_for((2 * max_dst * 32 + kSampBlock - 1) / kSampBlock,
+                                                                   cap)));
   sample_warp_kernel<<<grid, kSampBlock, 0, fk.aux>>>(a);
   GNS_TRY(check_launch("sample_warp"));
-  sample_hub_kernel<<<sms, kHubBlock, 0, fk.aux>>>(a);
-  GNS_TRY(check_launch("sample_hub"));
   GNS_TRY(fork_join(stream, fk));
   // _assemble (sampling.py:139-152): seeds and sampled neighbours were marked
   // in the dedup bitmap by the count / sample kernels
@@ -1107,6 +1125,14 @@ int gns_sample_tune(const char* name, int32_t value) {
   }
   if (!strcmp(name, "sampler_ctas") && value >= 0) {
     g_sampler_ctas = value;
+    return GNS_OK;
+  }
+  if (!strcmp(name, "count_items") && (value == 1 || value == 2 || value == 4)) {
+    g_count_items = value;
+    return GNS_OK;
+  }
+  if (!strcmp(name, "stream_minb") && (value == 1 || value == 3 || value == 4)) {
+    g_stream_minb = value;
     return GNS_OK;
   }
   return GNS_EINVAL;

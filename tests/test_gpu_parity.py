@@ -651,6 +651,10 @@ def test_spmm_bwd_f64_bit_exact(P, dim):
     from paper_2106_06150_b200 import _lib
     og, g, feats, mb, ref = _mb_and_features(P, dim=16)
     ws = _lib.workspace(1 << 24, "cuda")
+    # the transpose's per-row sort paths are all covered: rows of <= 8
+    # entries (per lane), 9..32 (warp ranks) and > 32 (warp bitonic)
+    tlen = np.concatenate([np.bincount(br.edge_src, minlength=len(br.src_nodes)) for br in ref.blocks])
+    assert tlen.max() > 32 and np.any((tlen > 8) & (tlen <= 32)) and np.any((tlen > 0) & (tlen <= 8))
     for li, (bg, br) in enumerate(zip(mb.blocks, ref.blocks)):
         nsrc, ndst = len(br.src_nodes), len(br.dst_nodes)
         dcat = np.random.default_rng(10 + li).normal(size=(ndst, 2 * dim))
@@ -682,7 +686,8 @@ def test_spmm_bwd_f64_bit_exact(P, dim):
 @pytest.mark.parametrize("dim", [16, 100, 256])
 def test_relu_bits_pair_equals_zmask_path(P, dim):
     """gns_spmm_fwd_bits == gns_spmm_fwd(relu) and gns_spmm_bwd_transposed_bits
-    (mask from the forward's bits) == gns_spmm_bwd (mask from z), bit for bit."""
+    (mask from the forward's bits) == gns_spmm_bwd (mask from z), bit for bit
+    (dz; the bias gradient within float32 rounding), for every variant."""
     from paper_2106_06150_b200 import _lib
     og, g, feats, mb, ref = _mb_and_features(P, dim=16)
     lib = _lib.lib()
@@ -706,11 +711,24 @@ def test_relu_bits_pair_equals_zmask_path(P, dim):
         db2 = torch.empty(dim, device="cuda")
         _lib.call("gns_spmm_bwd", 0, dcat.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges, 0,
                   z.data_ptr(), db1.data_ptr(), d1.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
-        _lib.call("gns_spmm_bwd_transposed_bits", dcat.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc, br.num_edges,
-                  0, bits.data_ptr(), db2.data_ptr(), d2.data_ptr(), dim, ws.data_ptr(), ws.numel(),
-                  _lib.stream_ptr())
-        assert torch.equal(d1, d2), li
-        assert torch.equal(db1, db2), li
+        # every transposed-SpMM variant (0 = per-row; 1-5 lane-staged with
+        # 2-8 rows in flight): the same per-row FMA order, so dz is
+        # bit-identical; the bias gradient's partial sums are grouped per
+        # warp, so it is compared within float32 rounding of the fp64 sum
+        try:
+            for knob in range(6):
+                _lib.call("gns_tune", b"spmm_bwd", knob)
+                d2.fill_(float("nan"))
+                _lib.call("gns_spmm_bwd_transposed_bits", dcat.data_ptr(), 2 * dim, dim, bg._c, ndst, nsrc,
+                          br.num_edges, 0, bits.data_ptr(), db2.data_ptr(), d2.data_ptr(), dim, ws.data_ptr(),
+                          ws.numel(), _lib.stream_ptr())
+                assert torch.equal(d1, d2), (li, knob)
+                ref64 = d1.double().sum(0)
+                tol = 1e-5 * d1.double().abs().sum(0) + 1e-6
+                assert torch.all((db2.double() - ref64).abs() <= tol), (li, knob)
+                assert torch.all((db1.double() - ref64).abs() <= tol), (li, knob)
+        finally:
+            _lib.call("gns_tune", b"spmm_bwd", 4)
 
 
 def test_full_batch_equivalence(P):
