@@ -30,12 +30,13 @@ namespace gns {
 
 constexpr int kSampBlock = 256;
 constexpr int kWarpCap = 256;
-constexpr int kHubLen = 2048;
+constexpr int kHubLen = 2048;   // <= 2^11: the warp tier packs positions in 11 bits
 constexpr int kThreadLen = 16;    // rows scanning <= 16 positions: one thread per row, register sort
 constexpr int kStreamK = 8;       // streaming top-k tier: take <= 8 and <= stream_len positions
 static int g_stream_len = 32;     // (gns_tune "stream_len", <= 2047)
 static int g_thread_len = 0;      // (gns_tune "thread_len", <= 16; 0 = no sorting-network tier: measured best)
 static int g_stream_minb = 1;     // (gns_tune "stream_minb": 1, 3, 4) min resident CTAs/SM of the streaming tier
+static int g_warp_sort = 1;       // (gns_tune "warp_sort": 0/1) see LayerArgs::warp_sort
 static int g_sampler_ctas = 0;    // (gns_tune "sampler_ctas") cap grid-stride sampler grids at this many CTAs
                                   // per SM (0 = no cap): leaves SM room to the concurrent training branch
 constexpr int kHubCap = 512;
@@ -63,6 +64,7 @@ struct LayerArgs {
   uint32_t* dsum;   // summary bitmap (bit w of word w>>5 set iff dbits[w] != 0)
   int stream_len;   // rows up to this many positions with take <= kStreamK: streaming tier
   int thread_len;   // other rows up to this many positions (<= kThreadLen): sorting-network tier
+  int warp_sort;    // warp tier: rank <= 32 candidates by a shuffle bitonic sort (else the shared rank loop)
   struct RowDesc* desc;  // per-row descriptors (count pass -> selection kernels)
   gns_block_t b;
 };
@@ -460,6 +462,25 @@ __device__ void warp_select(const LayerArgs& a, const Rng3& rk, const RowInfo& r
     if (lane == 0) atomicOr((unsigned*)(a.b.counts + GNS_CNT_ERR), GNS_ERRBIT_CAPACITY);
     return;
   }
+  if (found <= 32 && a.warp_sort) {
+    // (the usual case: E[found] = take + 4 sqrt(take) + 8) one candidate per
+    // lane, packed (key53 << 11 | pos) — pos < kHubLen = 2^11, so the packed
+    // order is the (key, position) order — and a 32-lane bitonic sort by
+    // shuffles; lane i then holds rank i
+    uint64_t v = lane < found ? (bkey[lane] << 11) | (uint64_t)bpos[lane] : ~0ull;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const uint64_t o = __shfl_xor_sync(GNS_FULL, v, j);
+        const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+        v = keep_min ? (o < v ? o : v) : (o < v ? v : o);
+      }
+    }
+    if (lane < ph.take) emit_edge(a, ri, r, ph, lane, (uint32_t)(v & 2047u));
+    __syncwarp();
+    return;
+  }
   for (int i = lane; i < found; i += 32) {
     const uint64_t ki = bkey[i];
     const uint32_t pi = bpos[i];
@@ -795,17 +816,30 @@ __global__ void setbits_kernel(const int32_t* __restrict__ a, const int32_t* __r
   }
 }
 
-// Tile = 64 summary words (65536 node ids); a warp walks 8 summary words, lane
-// b owning bitmap word sw*32+b (coalesced 128-byte loads; empty summary words
-// are skipped without touching the bitmap).
+// Tile = 64 summary words (65536 node ids) per CTA, 8 per warp: the warp's
+// 256 bitmap words are read as 8 consecutive words per lane (two 16-B loads,
+// skipped when the lane's 8 summary bits are zero), so the output order —
+// ascending word — is lane-major and one warp scan of the lanes' popcounts
+// ranks every word (instead of one scan per summary word).
 constexpr int kEnumBlock = 256;
 constexpr int kEnumWarps = kEnumBlock / 32;
 constexpr int kEnumPerWarp = 8;
 constexpr int kEnumTileSw = kEnumWarps * kEnumPerWarp;
 
-__device__ __forceinline__ uint32_t enum_word(const uint32_t* __restrict__ bits, uint32_t smw, long long sw,
-                                              int lane) {
-  return ((smw >> lane) & 1u) ? bits[sw * 32 + lane] : 0u;
+// lane's 8 bitmap words (bitmap words (sw0 * 32 + 8 * lane) ...) and their popcount
+__device__ __forceinline__ unsigned enum_lane_words(const uint32_t* __restrict__ bits,
+                                                    const uint32_t* __restrict__ sum, int64_t nsw, long long sw0,
+                                                    int lane, uint4& w0, uint4& w1) {
+  const long long sw = sw0 + (lane >> 2);
+  const uint32_t smw = sw < nsw ? sum[sw] : 0u;
+  const uint32_t sb = (smw >> (8 * (lane & 3))) & 0xffu;
+  w0 = make_uint4(0u, 0u, 0u, 0u);
+  w1 = make_uint4(0u, 0u, 0u, 0u);
+  const uint4* p = reinterpret_cast<const uint4*>(bits + sw0 * 32 + 8 * lane);
+  if (sb & 0x0fu) w0 = p[0];
+  if (sb & 0xf0u) w1 = p[1];
+  return __popc(w0.x) + __popc(w0.y) + __popc(w0.z) + __popc(w0.w) + __popc(w1.x) + __popc(w1.y) + __popc(w1.z) +
+         __popc(w1.w);
 }
 
 __global__ void __launch_bounds__(kEnumBlock) enumerate_reduce_kernel(const uint32_t* __restrict__ bits,
@@ -814,14 +848,8 @@ __global__ void __launch_bounds__(kEnumBlock) enumerate_reduce_kernel(const uint
   __shared__ unsigned long long s_w[kEnumWarps + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long sw0 = (long long)blockIdx.x * kEnumTileSw + warp * kEnumPerWarp;
-  // the warp's 8 summary words in one load, then all bitmap loads in flight
-  const uint32_t my_sum = (lane < kEnumPerWarp && sw0 + lane < nsw) ? sum[sw0 + lane] : 0u;
-  unsigned c = 0;
-#pragma unroll
-  for (int i = 0; i < kEnumPerWarp; ++i) {
-    const uint32_t smw = __shfl_sync(GNS_FULL, my_sum, i);
-    c += __popc(enum_word(bits, smw, sw0 + i, lane));
-  }
+  uint4 w0, w1;
+  const unsigned c = enum_lane_words(bits, sum, nsw, sw0, lane, w0, w1);
   unsigned long long t = block_sum<kEnumBlock>((unsigned long long)c, s_w);
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = t;
 }
@@ -845,44 +873,35 @@ __global__ void __launch_bounds__(kEnumBlock) enumerate_apply_kernel(uint32_t* _
   unsigned long long pre = 0;
   for (long long j = threadIdx.x; j < tile; j += kEnumBlock) pre += tile_sums[j];
   pre = block_sum<kEnumBlock>(pre, s_w);
-  // per-warp counts -> exclusive prefix over the 8 warps of the tile
   const long long sw0 = tile * kEnumTileSw + warp * kEnumPerWarp;
-  const uint32_t my_sum = (lane < kEnumPerWarp && sw0 + lane < nsw) ? sum[sw0 + lane] : 0u;
-  uint32_t words[kEnumPerWarp];
-  unsigned c = 0;
-#pragma unroll
-  for (int i = 0; i < kEnumPerWarp; ++i) {
-    const uint32_t smw = __shfl_sync(GNS_FULL, my_sum, i);
-    words[i] = enum_word(bits, smw, sw0 + i, lane);
-    c += __popc(words[i]);
-  }
-  c = warp_sum(c);
-  if (lane == 0) s_wpre[warp] = c;
+  uint4 w0, w1;
+  const unsigned c = enum_lane_words(bits, sum, nsw, sw0, lane, w0, w1);
+  const unsigned incl = warp_incl_scan(c);
+  if (lane == 31) s_wpre[warp] = incl;
   __syncthreads();
-  unsigned long long base = pre;
-  for (int w = 0; w < warp; ++w) base += s_wpre[w];
-  if (tile == ntiles - 1 && warp == kEnumWarps - 1 && lane == 0) out_n[0] = (int32_t)(base + c);
+  unsigned long long o = pre + incl - c;
+  for (int w = 0; w < warp; ++w) o += s_wpre[w];
+  if (tile == ntiles - 1 && warp == kEnumWarps - 1 && lane == 31) out_n[0] = (int32_t)(o + c);
+  if (c) {
+    const uint32_t x8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const long long wbase = sw0 * 32 + 8 * lane;
 #pragma unroll
-  for (int i = 0; i < kEnumPerWarp; ++i) {
-    const long long sw = sw0 + i;
-    const uint32_t x = words[i];
-    const unsigned pc = __popc(x);
-    const unsigned incl = warp_incl_scan(pc);
-    if (x) {
-      const long long w = sw * 32 + lane;
-      unsigned long long o = base + incl - pc;
-      rank2[w] = (o << 32) | (unsigned long long)x;
-      bits[w] = 0u;
-      uint32_t y = x;
-      while (y) {
-        const int bb = __ffs(y) - 1;
-        y &= y - 1;
-        out[o++] = (int32_t)(w * 32 + bb);
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t x = x8[i];
+      if (x) {
+        const long long w = wbase + i;
+        rank2[w] = (o << 32) | (unsigned long long)x;
+        bits[w] = 0u;
+        uint32_t y = x;
+        while (y) {
+          const int bb = __ffs(y) - 1;
+          y &= y - 1;
+          out[o++] = (int32_t)(w * 32 + bb);
+        }
       }
     }
-    base += __shfl_sync(GNS_FULL, incl, 31);
-    if (sw < nsw && lane == 0) sum[sw] = 0u;
   }
+  if (lane < kEnumPerWarp && sw0 + lane < nsw) sum[sw0 + lane] = 0u;
 }
 
 __device__ __forceinline__ int32_t bit_rank(const unsigned long long* __restrict__ rank2, int32_t v) {
@@ -1069,6 +1088,7 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   a.dsum = dd.sum;
   a.stream_len = g_stream_len;
   a.thread_len = g_thread_len;
+  a.warp_sort = g_warp_sort;
   a.desc = desc;
   a.b = *block;
   GNS_CUDA(cudaMemsetAsync(block->counts, 0, GNS_CNT_N * sizeof(int32_t), stream));
@@ -1125,6 +1145,10 @@ int gns_sample_tune(const char* name, int32_t value) {
   }
   if (!strcmp(name, "sampler_ctas") && value >= 0) {
     g_sampler_ctas = value;
+    return GNS_OK;
+  }
+  if (!strcmp(name, "warp_sort") && (value == 0 || value == 1)) {
+    g_warp_sort = value;
     return GNS_OK;
   }
   if (!strcmp(name, "count_items") && (value == 1 || value == 2 || value == 4)) {
