@@ -830,8 +830,8 @@ __global__ void __launch_bounds__(kSpmmBlock, 3) spmm_fwd_wide_kernel(const floa
 // chains of spmm_fwd_wide_kernel at D = 256, one float4 per lane per
 // neighbour row, G rows in flight).  Each warp ranks the row's edges itself;
 // per-element FMA order is unchanged (bit-identical).
-template <int G, bool MASK>
-__global__ void __launch_bounds__(kSpmmBlock, 4) spmm_fwd_wide_split_kernel(const float* __restrict__ h,
+template <int G, bool MASK, int MINB = 4>
+__global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_fwd_wide_split_kernel(const float* __restrict__ h,
                                                                              int64_t ld_h, int dim, BlockView bv,
                                                                              float* __restrict__ cat, int64_t ld_cat,
                                                                              int64_t pad_rows,
@@ -927,6 +927,7 @@ __global__ void __launch_bounds__(kSpmmBlock, 4) spmm_fwd_wide_split_kernel(cons
 // experiment knobs (gns_tune)
 static int g_tune_narrow = 2;  // narrow-row forward SpMM: 0 generic, 1 per-row narrow, 2+ chunk-staged
 static int g_tune_wide = 2;    // hidden-layer forward: 2 = column-split, 1 = spmm_fwd_wide_kernel, 0 = generic
+static int g_split_g = 4;      // column-split forward: neighbour rows in flight (2, 4, 8, 12, 16; 5 = 4 at 5 CTAs/SM)
 static int g_tune_bwd = 4;     // transposed SpMM (bits): >= 1 lane-staged (rows in flight / occupancy, see the dispatch), 0 = per-row
 
 // Forward SpMM grids: one wave of persistent CTAs (grid-stride rows).  Short
@@ -1853,6 +1854,10 @@ int gns_tune(const char* name, int32_t value) {
     g_tune_wide = value;
     return GNS_OK;
   }
+  if (!strcmp(name, "split_g") && (value == 2 || value == 4 || value == 5 || value == 8 || value == 12 || value == 16)) {
+    g_split_g = value;
+    return GNS_OK;
+  }
   if (!strcmp(name, "spmm_bwd") && value >= 0 && value <= 5) {
     g_tune_bwd = value;
     return GNS_OK;
@@ -1934,8 +1939,17 @@ int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block
   const int dv = dim / 4;
   if (g_tune_wide == 2 && dv > 32 && dv <= 128) {
     const long long tasks = rows * ((dv + 31) / 32);
-    spmm_fwd_wide_split_kernel<4, true><<<spmm_grid(spmm_fwd_wide_split_kernel<4, true>, tasks), kSpmmBlock, 0,
-                                           stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows, relu_bits);
+#define GNS_SPLIT(G, B)                                                                                     \
+  spmm_fwd_wide_split_kernel<G, true, B><<<spmm_grid(spmm_fwd_wide_split_kernel<G, true, B>, tasks), kSpmmBlock, \
+                                           0, stream>>>(h, ld_h, dim, bv, cat, ld_cat, pad_rows, relu_bits)
+    // (gns_tune "split_g": neighbour rows in flight per warp / resident CTAs per SM)
+    if (g_split_g == 2) GNS_SPLIT(2, 6);
+    else if (g_split_g == 5) GNS_SPLIT(4, 5);
+    else if (g_split_g == 8) GNS_SPLIT(8, 3);
+    else if (g_split_g == 12) GNS_SPLIT(12, 2);
+    else if (g_split_g == 16) GNS_SPLIT(16, 2);
+    else GNS_SPLIT(4, 4);
+#undef GNS_SPLIT
     return check_launch("spmm_fwd_bits");
   }
   if (g_tune_wide && dv > 32 && dv <= 64) {

@@ -597,8 +597,9 @@ def test_spmm_fwd_wide_equals_generic(P, dim):
             ns, nd = bg.src_nodes.numel(), bg.dst_nodes.numel()
             h = torch.randn(ns, dim, device="cuda")
             res = []
-            for v in (0, 1, 2):
+            for v, sg in ((0, 4), (1, 4), (2, 4), (2, 8), (2, 12), (2, 16)):
                 _lib.call("gns_tune", b"spmm_wide", v)
+                _lib.call("gns_tune", b"split_g", sg)
                 o = torch.full((nd + 3, 2 * dim), 5.0, device="cuda")
                 bits = torch.zeros(lib.gns_relu_bits_size(ns, dim) // 4, dtype=torch.int32, device="cuda")
                 _lib.call("gns_spmm_fwd_bits", h.data_ptr(), dim, dim, bg._c, nd, nd + 3, o.data_ptr(), 2 * dim,
@@ -609,6 +610,7 @@ def test_spmm_fwd_wide_equals_generic(P, dim):
                 assert torch.equal(res[0][1], res[v][1]), v
     finally:
         _lib.call("gns_tune", b"spmm_wide", 2)
+        _lib.call("gns_tune", b"split_g", 4)
 
 
 @pytest.mark.parametrize("dim", [16, 64, 128])
