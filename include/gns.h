@@ -452,14 +452,29 @@ GNS_API int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, cons
                      const int32_t* targets, void* grad_out, double* loss_out,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* The output layer's loss and gradients in one launch (the graphed step):
+ * gns_softmax_xent's rows and loss_out[0] plus grad_bias[c] = sum over rows
+ * of grad_out[:, c] (model.py:218-220; the output layer's dz is dlogits),
+ * both reduced in a fixed order.  num_classes <= 256.  The workspace
+ * (gns_softmax_xent_bias_workspace_size) must be zeroed once before the first
+ * call; every call leaves its counter at zero. */
+GNS_API size_t gns_softmax_xent_bias_workspace_size(int64_t max_rows, int64_t pad_rows, int32_t num_classes);
+GNS_API int gns_softmax_xent_bias(int32_t dtype, const void* logits, int64_t ld, const int32_t* n_dev,
+                                  int64_t max_rows, int64_t pad_rows, int32_t num_classes,
+                                  const int32_t* labels, const int32_t* targets, void* grad_out,
+                                  double* loss_out, void* grad_bias, void* ws, size_t ws_bytes,
+                                  void* stream);
+
 /* Bias-corrected Adam over a flat parameter buffer (model.py:229-242);
  * grad_scale multiplies the gradient first (1/W after an allreduce). */
 GNS_API int gns_adam(int32_t dtype, void* params, const void* grads, void* m, void* v,
              int64_t n, double lr, double beta1, double beta2, double eps,
              int64_t step, double grad_scale, void* stream);
 
-/* gns_adam with the step count on the device: uses t = *step_dev + 1 and
- * then increments *step_dev (graph-replay safe). */
+/* gns_adam with the step count on the device: step_dev points to two int64,
+ * the step count and a ticket that must be zero; uses t = step_dev[0] + 1,
+ * then the last CTA increments step_dev[0] and leaves the ticket at zero
+ * (graph-replay safe, one launch). */
 GNS_API int gns_adam_dev(int32_t dtype, void* params, const void* grads, void* m, void* v,
                          int64_t n, double lr, double beta1, double beta2, double eps,
                          int64_t* step_dev, double grad_scale, void* stream);

@@ -199,9 +199,15 @@ class CacheState:
     def cstruct(self):
         c = getattr(self, "_c", None)
         if c is None:
-            c = _lib.GnsCache(self.cached_indptr.data_ptr(), self.cached_indices.data_ptr(),
+            # the cached CSR arrays are prefixes of their buffers (_buf_cidx /
+            # _buf_cpos): pass the buffer bases, which stay put across
+            # in-place refreshes even when the prefix was empty (an empty
+            # view's data_ptr is 0 — a graph captured with it would keep 0)
+            cidx = getattr(self, "_buf_cidx", self.cached_indices)
+            cpos = self.cached_pos if self.cached_pos is None else getattr(self, "_buf_cpos", self.cached_pos)
+            c = _lib.GnsCache(self.cached_indptr.data_ptr(), cidx.data_ptr(),
                               self.nodes.mask_bits.data_ptr(), self.inclusion.data_ptr(),
-                              None if self.cached_pos is None else self.cached_pos.data_ptr())
+                              None if cpos is None or cpos.numel() == 0 else cpos.data_ptr())
             object.__setattr__(self, "_c", c)
         return c
 

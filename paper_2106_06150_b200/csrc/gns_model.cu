@@ -939,8 +939,10 @@ static inline int spmm_grid(Kernel k, long long rows) {
 }
 
 // ---- SpMM backward -------------------------------------------------------------
-__global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of) {
+__global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of,
+                              unsigned* __restrict__ ticket) {
   const int64_t ne = bv.counts[GNS_CNT_EDGES], nd = bv.counts[GNS_CNT_DST];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;   // the transposed SpMM's bias-gradient ticket
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne + nd; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < ne)
       atomicAdd(tcount + bv.edge_src[i], 1);
@@ -1262,7 +1264,9 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
                                                                       float* __restrict__ dh, int64_t ld_dh,
                                                                       int64_t pad_rows, float* __restrict__ colpart,
                                                                       const uint32_t* __restrict__ relu_bits,
-                                                                      const float* __restrict__ twn) {
+                                                                      const float* __restrict__ twn,
+                                                                      float* __restrict__ db,
+                                                                      unsigned* __restrict__ ticket) {
   constexpr int W = kSpmmBlock / 32;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t n = bv.counts[GNS_CNT_SRC];
@@ -1390,6 +1394,21 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
       for (int w = 0; w < W; ++w) t += red[w][col];
       colpart[(int64_t)blockIdx.x * dim + col] = t;
     }
+    // the last CTA to finish sums the CTA partials in CTA order (the bias
+    // gradient, deterministic) and leaves the ticket at zero
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) *ticket = 0u;
+    for (int col = threadIdx.x; col < dim; col += blockDim.x) {
+      float t = 0.f;
+      for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(colpart + (int64_t)b * dim + col);
+      db[col] = t;
+    }
   }
 }
 
@@ -1457,6 +1476,7 @@ static inline void colsum_launch(const T* part, int nrows, int ncols, T* out, cu
 
 struct BwdWs {
   void* colpart;
+  unsigned* ticket;   // last-CTA ticket of the fused bias-gradient reduction (reset by the transpose)
   int32_t* tcount;
   int32_t* tptr;
   int32_t* self_of;
@@ -1469,6 +1489,7 @@ struct BwdWs {
 static size_t bwd_ws(int64_t max_src, int64_t max_edges, int32_t dim, void* base, size_t cap, BwdWs* w) {
   Workspace ws(base, cap);
   w->colpart = (void*)ws.take<double>((size_t)num_sms() * 8 * (size_t)(dim > 0 ? dim : 1));
+  w->ticket = ws.take<unsigned>(1);
   w->tcount = ws.take<int32_t>(max_src + 1);
   w->tptr = ws.take<int32_t>(max_src + 1);
   w->self_of = ws.take<int32_t>(max_src + 1);
@@ -1512,6 +1533,95 @@ __global__ void xent_kernel(const T* __restrict__ logits, int64_t ld, const int3
     for (int c = lane; c < C; c += 32) grad[r * ld + c] = (T)0;
 }
 
+// Output layer in one launch (the graphed engine's training step): softmax
+// cross-entropy rows (xent_kernel's arithmetic, warp per row), the bias
+// gradient db[c] = sum_r dlogits[r][c] (model.py:218-220: the output layer's
+// dz is dlogits) as per-CTA column partials, and — in the last CTA to finish
+// (ticket counter, reset for the next launch) — the mean loss and db, each
+// summed in a fixed order (deterministic whichever CTA is last).  Replaces
+// xent + mean + dense_bwd_partial + colsum: three launches fewer on the
+// training branch.  Columns <= 32 * kXentCh.
+constexpr int kXentCh = 8;
+template <typename T>
+__global__ void __launch_bounds__(256) xent_bias_kernel(const T* __restrict__ logits, int64_t ld,
+                                                        const int32_t* __restrict__ n_dev, int C,
+                                                        const int32_t* __restrict__ labels,
+                                                        const int32_t* __restrict__ targets, T* __restrict__ grad,
+                                                        double* __restrict__ loss_out, T* __restrict__ grad_bias,
+                                                        double* __restrict__ row_loss, T* __restrict__ partial,
+                                                        unsigned* __restrict__ ticket, int64_t pad_rows) {
+  __shared__ T red[8][32 * kXentCh];
+  __shared__ double s_red[8];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t n = n_dev[0];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  T col[kXentCh];
+#pragma unroll
+  for (int i = 0; i < kXentCh; ++i) col[i] = (T)0;
+  for (int64_t r = gw; r < n; r += nw) {
+    const T* z = logits + r * ld;
+    T mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = max(mx, z[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(GNS_FULL, mx, o));
+    T s = 0;
+    for (int c = lane; c < C; c += 32) s += exp(z[c] - mx);
+    s = warp_sum(s);
+    const T lse = log(s);
+    const int lab = labels[targets[r]];
+    const T inv_n = (T)1 / (T)n;
+#pragma unroll
+    for (int i = 0; i < kXentCh; ++i) {
+      const int c = lane + 32 * i;
+      if (c < C) {
+        T lp = (z[c] - mx) - lse;
+        T g = exp(lp);
+        if (c == lab) g -= (T)1;
+        const T gv = g * inv_n;
+        grad[r * ld + c] = gv;
+        col[i] += gv;
+        if (c == lab) row_loss[r] = -(double)lp;
+      }
+    }
+  }
+  for (int64_t r = n + gw; r < pad_rows; r += nw)
+    for (int c = lane; c < C; c += 32) grad[r * ld + c] = (T)0;
+  // per-CTA column partials (warp order)
+#pragma unroll
+  for (int i = 0; i < kXentCh; ++i) red[wib][lane + 32 * i] = col[i];
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    T t = (T)0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][c];
+    partial[(int64_t)blockIdx.x * C + c] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *ticket = 0u;   // ready for the next launch (graph replay)
+  double acc = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += __ldcg(row_loss + i);
+  acc = warp_sum(acc);
+  if (lane == 0) s_red[wib] = acc;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    T t = (T)0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(partial + (int64_t)b * C + c);
+    grad_bias[c] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0;
+    for (int w = 0; w < 8; ++w) v += s_red[w];
+    loss_out[0] = n > 0 ? v / (double)n : 0.0;
+  }
+}
+
 __global__ void mean_kernel(const double* __restrict__ x, const int32_t* __restrict__ n_dev, double* __restrict__ out) {
   __shared__ double sh[32];
   const int64_t n = n_dev[0];
@@ -1545,11 +1655,12 @@ __global__ void adam_kernel(T* __restrict__ p, const T* __restrict__ g, T* __res
 // Adam with the step count read on the device (t = *step_dev + 1), so a step
 // captured in a CUDA graph stays correct at every replay; the bias
 // corrections are evaluated per thread in double exactly as gns_adam does on
-// the host, then step_inc_kernel advances the counter.
+// the host; the last CTA to finish advances the counter (step_dev[1] is its
+// ticket, zero between launches).
 template <typename T>
 __global__ void adam_dev_kernel(T* __restrict__ p, const T* __restrict__ g, T* __restrict__ m, T* __restrict__ v,
                                 int64_t n, double lr, double b1, double b2, double eps,
-                                const int64_t* __restrict__ step_dev, T gs) {
+                                int64_t* __restrict__ step_dev, T gs) {
   const double t = (double)(step_dev[0] + 1);
   const T bc1 = (T)(1.0 - pow(b1, t)), bc2 = (T)(1.0 - pow(b2, t));
   const T lr_ = (T)lr, b1_ = (T)b1, b2_ = (T)b2, eps_ = (T)eps;
@@ -1562,9 +1673,17 @@ __global__ void adam_dev_kernel(T* __restrict__ p, const T* __restrict__ g, T* _
     T mh = mi / bc1, vh = vi / bc2;
     p[i] -= lr_ * mh / (sqrt(vh) + eps_);
   }
+  // step_dev[1] is a ticket: the last CTA (every CTA has read step_dev[0] by
+  // then) advances the step count and resets the ticket
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* tk = reinterpret_cast<unsigned long long*>(step_dev + 1);
+    if (atomicAdd(tk, 1ull) == (unsigned long long)gridDim.x - 1) {
+      *tk = 0ull;
+      step_dev[0] += 1;
+    }
+  }
 }
-
-__global__ void step_inc_kernel(int64_t* step_dev) { step_dev[0] += 1; }
 
 }  // namespace gns
 
@@ -2003,7 +2122,7 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
   spmm_bwd_rows_kernel<CH, R, B><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,         \
                                                                 w.self_of, dh, ld_dh, pad_rows,                 \
                                                                 db ? (float*)w.colpart : nullptr, relu_bits,    \
-                                                                w.twn)
+                                                                w.twn, db, w.ticket)
   // knob: 1 = R2/4 CTAs per SM, 2 = R2/3, 3 = R4/3, 4 = R4/2, 5 = R8/2
   if (g_tune_bwd > 0 && dv <= 64) {
     if (dv <= 32) {
@@ -2019,9 +2138,7 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
     } else {
       GNS_BWDC(2, 8, 2);
     }
-    GNS_TRY(check_launch("spmm_bwd_bits"));
-    if (db) colsum_launch<float>((const float*)w.colpart, g2, dim, db, stream);
-    return check_launch("spmm_bwd_bits colsum");
+    return check_launch("spmm_bwd_bits");   // (bias gradient reduced in the kernel)
   }
 #undef GNS_BWDC
 #define GNS_BWDB(CH)                                                                                             \
@@ -2106,7 +2223,7 @@ int gns_block_transpose(const gns_block_t* block, int64_t max_dst, int64_t max_s
   GNS_CUDA(cudaMemsetAsync(w.tcount, 0, (max_src + 1) * sizeof(int32_t), stream));
   GNS_CUDA(cudaMemsetAsync(w.self_of, 0xff, (max_src + 1) * sizeof(int32_t), stream));
   int g1 = grid_for((max_edges + max_dst + 255) / 256, (long long)sms * 8);
-  tcount_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.self_of);
+  tcount_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.self_of, w.ticket);
   const unsigned ttiles = (unsigned)((max_src + kTsBlock * kTsItems - 1) / (kTsBlock * kTsItems)) + 1;
   tscan_reduce_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, (unsigned long long*)w.scan);
   tscan_apply_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, w.tptr, (unsigned long long*)w.scan);
@@ -2231,6 +2348,50 @@ int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, const int32_
   return check_launch("softmax_xent");
 }
 
+static int xent_bias_grid(int64_t max_rows, int64_t pad_rows) {
+  return grid_for(((max_rows > pad_rows ? max_rows : pad_rows) * 32 + 255) / 256, (long long)num_sms() * 8);
+}
+
+size_t gns_softmax_xent_bias_workspace_size(int64_t max_rows, int64_t pad_rows, int32_t num_classes) {
+  Workspace w(nullptr, 0);
+  w.take<double>(max_rows + 1);
+  w.take<double>((size_t)xent_bias_grid(max_rows, pad_rows) * (num_classes > 0 ? num_classes : 1));
+  w.take<unsigned>(1);
+  return w.off;
+}
+
+int gns_softmax_xent_bias(int32_t dtype, const void* logits, int64_t ld, const int32_t* n_dev, int64_t max_rows,
+                          int64_t pad_rows, int32_t num_classes, const int32_t* labels, const int32_t* targets,
+                          void* grad_out, double* loss_out, void* grad_bias, void* ws, size_t ws_bytes,
+                          void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (num_classes < 1 || num_classes > 32 * kXentCh) {
+    set_error("softmax_xent_bias: num_classes %d outside [1, %d]", num_classes, 32 * kXentCh);
+    return GNS_EINVAL;
+  }
+  if (ws_bytes < gns_softmax_xent_bias_workspace_size(max_rows, pad_rows, num_classes)) {
+    set_error("softmax_xent_bias: workspace %zu < %zu", ws_bytes,
+              gns_softmax_xent_bias_workspace_size(max_rows, pad_rows, num_classes));
+    return GNS_EINVAL;
+  }
+  Workspace w(ws, ws_bytes);
+  double* row_loss = w.take<double>(max_rows + 1);
+  const int grid = xent_bias_grid(max_rows, pad_rows);
+  void* partial = (void*)w.take<double>((size_t)grid * num_classes);
+  unsigned* ticket = w.take<unsigned>(1);
+  // the ticket must start at 0: the caller zeroes the workspace once (every
+  // launch leaves it at 0)
+  if (dtype == 0)
+    xent_bias_kernel<float><<<grid, 256, 0, stream>>>((const float*)logits, ld, n_dev, num_classes, labels, targets,
+                                                      (float*)grad_out, loss_out, (float*)grad_bias, row_loss,
+                                                      (float*)partial, ticket, pad_rows);
+  else
+    xent_bias_kernel<double><<<grid, 256, 0, stream>>>((const double*)logits, ld, n_dev, num_classes, labels,
+                                                       targets, (double*)grad_out, loss_out, (double*)grad_bias,
+                                                       row_loss, (double*)partial, ticket, pad_rows);
+  return check_launch("softmax_xent_bias");
+}
+
 int gns_adam(int32_t dtype, void* params, const void* grads, void* m, void* v, int64_t n, double lr, double beta1,
              double beta2, double eps, int64_t step, double grad_scale, void* stream_) {
   if (n <= 0) return GNS_OK;
@@ -2258,7 +2419,6 @@ int gns_adam_dev(int32_t dtype, void* params, const void* grads, void* m, void* 
   else
     adam_dev_kernel<double><<<grid, 256, 0, stream>>>((double*)params, (const double*)grads, (double*)m, (double*)v,
                                                       n, lr, beta1, beta2, eps, step_dev, grad_scale);
-  step_inc_kernel<<<1, 1, 0, stream>>>(step_dev);
   return check_launch("adam_dev");
 }
 

@@ -115,7 +115,7 @@ class GraphedTrainer:
         self.loss_host = [torch.zeros(S, dtype=torch.float64).pin_memory() for _ in range(2)]
         # Adam's step count lives on the device (gns_adam_dev), per-step losses
         # are kept for the host to read after a replay
-        self.adam_t = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.adam_t = torch.zeros(2, dtype=torch.int64, device=self.dev)   # [step count, gns_adam_dev ticket]
         self.step_loss = torch.zeros(S, dtype=torch.float64, device=self.dev)
         self._cur_j = 0
         # feature placement: "device" (whole table in HBM) or "mixed" (paper
@@ -141,6 +141,7 @@ class GraphedTrainer:
         # double-buffered cache: csets[cur] is the active CacheState; the
         # other set receives the next refresh epoch's cache (prefetch)
         self.csets = [None, None]
+        self._adopted = None       # a caller's CacheState set through `cache` (never written)
         self.cur = 0
         self._pf = None
         self.prefetch = os.environ.get("GNS_CACHE_PREFETCH", "1") == "1"
@@ -185,7 +186,10 @@ class GraphedTrainer:
 
     @cache.setter
     def cache(self, state):
-        """Adopt an externally built cache as the active set."""
+        """Adopt an externally built cache as the active set.  The caller's
+        CacheState is never written: later refreshes draw into buffers of the
+        engine's own (_own_set)."""
+        self._adopted = state
         self.csets[self.cur] = state
         self._free_execs(self.cur)
         if self.placement == "mixed" and state is not None:
@@ -219,7 +223,11 @@ class GraphedTrainer:
         self.tws = [[None] + [_lib.workspace(lib.gns_spmm_bwd_workspace_size(self.cap_src[li], self.cap_edges[li],
                                                                             dims[li]), dev, zero=True)
                               for li in range(1, L)] for _ in self.slots]
-        self.ws_xent = _lib.workspace(8 * max(self.cap_dst[L - 1], 1024), dev)
+        # the output layer's fused loss + dlogits + bias gradient (one launch;
+        # its ticket counter starts at zero and every launch leaves it there)
+        self.ws_xent = _lib.workspace(max(lib.gns_softmax_xent_bias_workspace_size(self.cap_dst[L - 1],
+                                                                                    self.npad[L - 1], dims[L]),
+                                          8 * max(self.cap_dst[L - 1], 1024)), dev, zero=True)
         self.use_switch = self.switch_chunk > 0 and self.switch_chunk % 2048 == 0 and \
             self.cap_dst[0] >= 2 * self.switch_chunk
         # split-K partial products of the input layer's weight gradient
@@ -261,7 +269,9 @@ class GraphedTrainer:
         if ev is not None:
             _lib.call("gns_record_event_external", ev[1].cuda_event, s)
 
-    def _train_rest(self, slot: int, with_adam: bool):
+    def _train_rest(self, slot: int, with_adam: bool, loss_out: torch.Tensor | None = None):
+        """The training step after the gather; the mean loss goes to
+        ``loss_out`` (a float64 device scalar; default model.loss_dev)."""
         m, sl, L, s = self.model, self.slots[slot], self.L, _lib.stream_ptr()
         blocks = [sl.layers[L - 1 - li] for li in range(L)]
         h = self.h0
@@ -301,14 +311,24 @@ class GraphedTrainer:
                 h = self.z[li]
             top = blocks[L - 1]
             logits = self.z[L - 1]
-            # dlogits straight into the output layer's dz (rows >= n zero)
-            _lib.call("gns_softmax_xent", 0, logits.data_ptr(), logits.stride(0),
-                      top.counts[_lib.CNT_DST:_lib.CNT_DST + 1].data_ptr(), self.cap_dst[L - 1], self.npad[L - 1],
-                      logits.shape[1], self.g.labels.data_ptr(), sl.seeds0.data_ptr(), self.dz[L - 1].data_ptr(),
-                      self.loss.data_ptr(), self.ws_xent.data_ptr(), self.ws_xent.numel(), s)
-            d_last = self.dims[L]
-            _lib.call("gns_dense_bwd_bias", 0, self.dz[L - 1].data_ptr(), None, d_last, None, self.cap_dst[L - 1],
-                      d_last, None, m.gbiases[L - 1].data_ptr(), self.ws_dense.data_ptr(), self.ws_dense.numel(), s)
+            # dlogits straight into the output layer's dz (rows >= n zero), the
+            # mean loss and the output bias gradient, in one launch
+            n_top = top.counts[_lib.CNT_DST:_lib.CNT_DST + 1]
+            loss_ptr = (self.loss if loss_out is None else loss_out).data_ptr()
+            if self.dims[L] <= 256:
+                _lib.call("gns_softmax_xent_bias", 0, logits.data_ptr(), logits.stride(0), n_top.data_ptr(),
+                          self.cap_dst[L - 1], self.npad[L - 1], logits.shape[1], self.g.labels.data_ptr(),
+                          sl.seeds0.data_ptr(), self.dz[L - 1].data_ptr(), loss_ptr,
+                          m.gbiases[L - 1].data_ptr(), self.ws_xent.data_ptr(), self.ws_xent.numel(), s)
+            else:
+                _lib.call("gns_softmax_xent", 0, logits.data_ptr(), logits.stride(0), n_top.data_ptr(),
+                          self.cap_dst[L - 1], self.npad[L - 1], logits.shape[1], self.g.labels.data_ptr(),
+                          sl.seeds0.data_ptr(), self.dz[L - 1].data_ptr(), loss_ptr,
+                          self.ws_xent.data_ptr(), self.ws_xent.numel(), s)
+                d_last = self.dims[L]
+                _lib.call("gns_dense_bwd_bias", 0, self.dz[L - 1].data_ptr(), None, d_last, None,
+                          self.cap_dst[L - 1], d_last, None, m.gbiases[L - 1].data_ptr(), self.ws_dense.data_ptr(),
+                          self.ws_dense.numel(), s)
             for li in range(L - 1, -1, -1):
                 if li == 0 and self.use_switch:
                     self._switched(n0, self.npad[0],
@@ -485,6 +505,7 @@ class GraphedTrainer:
         else:
             self._pf = None
             t = self.cur if self.cache is None else 1 - self.cur
+            self._own_set(t)
             if self.csets[t] is None:
                 if self.csets[1 - t] is None:
                     self.csets[t] = cache_mod.build_cache(self.g, self._probs, cs, epoch=epoch, rng_seed=seed,
@@ -505,6 +526,13 @@ class GraphedTrainer:
         if self.cfg.weight_policy == "gns-exact" and self._tables is None:
             self._tables = exact_tables(self.g, self.cfg, self._probs, cs)
 
+    def _own_set(self, t: int):
+        """Cache set ``t`` as a refresh target: replaced by fresh buffers if it
+        is an adopted (caller-owned) CacheState."""
+        if self.csets[t] is not None and self.csets[t] is self._adopted:
+            self.csets[t] = cache_mod.empty_like(self.csets[t], self.g)
+            self._free_execs(t)
+
     def _prefetch_begin(self, epoch: int):
         """Start drawing the cache of ``epoch`` into the idle set on the
         low-priority refresh stream (no host wait)."""
@@ -515,12 +543,22 @@ class GraphedTrainer:
         if self._probs is None:       # the active cache was adopted (cache setter)
             self._probs = cache_probs(self.g, self.cfg)
         t = 1 - self.cur
+        self._own_set(t)
         if self.csets[t] is None:
             self.csets[t] = cache_mod.empty_like(self.cache, self.g)
             self._free_execs(t)
         rs = self.refresh_stream
         rs.wait_stream(torch.cuda.current_stream())
-        p = cache_mod.refresh_begin(self.csets[t], self.g, self._probs, self._cache_size(), epoch,
+        # the refresh stream writes the idle set's buffers: tell the caching
+        # allocator, so memory freed with this engine (or a replaced set) is
+        # not handed out again before the refresh stream is done with it
+        st = self.csets[t]
+        for buf in (st._buf_ids, st.nodes.mask_bits, st._buf_counts, st.inclusion, st.cached_indptr, st._buf_cidx,
+                    st._buf_cpos):
+            buf.record_stream(rs)
+        if self.placement == "mixed" and self.tables[t] is not None:
+            self.tables[t].record_stream(rs)
+        p = cache_mod.refresh_begin(st, self.g, self._probs, self._cache_size(), epoch,
                                     [self.cfg.seed, _CACHE, epoch], stream=rs, positions=self._positions)
         self._pf = (t, p, 1)
 
@@ -632,10 +670,8 @@ class GraphedTrainer:
                 self._prof_events = ev_prof if j == 0 else None
                 if j > 0:
                     self._gather(sl)
-                self._train_rest(sl, with_adam=True)
-                # kernel copies (no copy-engine memcpy nodes on the critical path)
-                _lib.call("gns_copy_mapped", self.step_loss[j:j + 1].data_ptr(), self.model.loss_dev.data_ptr(),
-                          8, _lib.stream_ptr())
+                # the step's loss straight into its step_loss slot
+                self._train_rest(sl, with_adam=True, loss_out=self.step_loss[j:j + 1])
             if self.host_targets:   # every step's loss straight into pinned host memory
                 _lib.call("gns_copy_mapped", self.loss_host[p].data_ptr(), self.step_loss.data_ptr(), 8 * r,
                           _lib.stream_ptr())
@@ -659,6 +695,7 @@ class GraphedTrainer:
 
     def __del__(self):
         try:
+            self.refresh_stream.synchronize()   # a prefetch may still write the idle cache set
             self._free_execs()
         except Exception:
             pass
@@ -672,14 +709,33 @@ class GraphedTrainer:
         _lib.call("gns_graph_launch", self._execs[(p, r, self.cur)][1], _lib.stream_ptr(self.main))
 
     def prepare(self, steps: int):
-        """Capture every step graph a run of ``steps`` steps (within one
-        epoch) replays, so no capture happens inside a timed region."""
+        """Capture every step graph a run of ``steps`` steps replays, so no
+        capture happens inside a timed region: both graphs (p = 0, 1) for
+        every replay size the run can use (S; shorter groups at an epoch's
+        end), for the active cache set and — when the run may cross a cache
+        refresh — for the idle set it will switch to (allocated here)."""
         if not self._warmed:
             self._warm()
-        for r in {self.S, steps % self.S} - {0}:
-            for p in (0, 1):
-                if (p, r, self.cur) not in self._execs:
-                    self._capture(p, r)
+        sizes = set(range(1, self.S + 1)) if steps >= self.S else {steps % self.S}
+        sets = [self.cur]
+        # (the mixed placement's idle set gets its graphs at its first use:
+        # its HBM feature table and bitmap ranks are filled with the cache)
+        if self.cfg.strategy == "GNS" and self.cache is not None and self.placement != "mixed":
+            if steps >= len(self.batches(0)) or self.prefetch:
+                t = 1 - self.cur
+                if self.csets[t] is None:
+                    self.csets[t] = cache_mod.empty_like(self.cache, self.g)
+                sets.append(t)
+        cur = self.cur
+        try:
+            for cs in sets:
+                self.cur = cs
+                for r in sorted(sizes - {0}):
+                    for p in (0, 1):
+                        if (p, r, cs) not in self._execs:
+                            self._capture(p, r)
+        finally:
+            self.cur = cur
 
     @property
     def graphs(self):
@@ -730,7 +786,7 @@ class GraphedTrainer:
         torch.cuda.synchronize()
         if self._needs_refresh(epoch):
             self._refresh_cache(epoch)
-        self.adam_t.fill_(self.model.step_count)
+        self.adam_t[0].fill_(self.model.step_count)
         if self.epoch_perm is not None and self._perm_epoch != epoch:
             n = self.train_ids.numel()
             _lib.call("gns_epoch_targets", self.train_ids.data_ptr(), n, self.cfg.seed & 0xFFFFFFFF,

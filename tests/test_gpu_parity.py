@@ -1057,6 +1057,37 @@ def test_refresh_cache_grows_cached_csr_in_place(P):
         assert st.cstruct().cached_indices == before
 
 
+@pytest.mark.parametrize("placement", ["device", "mixed"])
+def test_engine_never_writes_an_adopted_cache(P, placement):
+    """A CacheState handed to the engine (``tr.cache = state``) is the
+    caller's: runs that cross several refresh epochs (prefetched into the
+    engine's own idle set, the timed-run graphs of both sets captured up
+    front by prepare) leave its contents untouched — regression: the second
+    refresh drew into the adopted buffers."""
+    og, g = _engine_graph(P, _hub_graph(3000, 43), train=0.5)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=300, cache_frac=0.05, cache_mode="degree",
+                          seed=3)
+    st = P.build_cache(g, P.degree_probs(g), O.cache_size_for(og, 0.05), rng_seed=[3, 33, 0])
+    before = {f: getattr(st, f).clone() for f in ("cached_indptr", "cached_indices", "inclusion")}
+    ids = st.nodes.ids.clone()
+    tr = GraphedTrainerCls(P)(g, cfg, (16, 16, 5), P.TrainConfig(), seed=0, feature_placement=placement)
+    tr.cache = st
+    nb = len(tr.batches(0))
+    tr.prepare(3 * nb)
+    tr.run(3 * nb + 1)
+    torch.cuda.synchronize()
+    assert tr.refresh_log and all(e > 0 for e, _ in tr.refresh_log)
+    assert torch.equal(st.nodes.ids, ids)
+    for f, v in before.items():
+        assert torch.equal(getattr(st, f), v), f
+    assert tr.cache is not st and tr.cache.epoch == 3
+
+
+def GraphedTrainerCls(P):
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    return GraphedTrainer
+
+
 def test_engine_device_errors_are_sticky(P):
     """A zero-inclusion cached draw in an engine step raises the reference's
     ValueError (sampling.py:255-256) at the end of the run, even though the
@@ -1636,3 +1667,50 @@ def test_numpy_generator_as_rng(P):
     a, b, c = draw(5), draw(5), draw(6)
     assert all(np.array_equal(x[f], y[f]) for x, y in zip(a, b) for f in FIELDS)
     assert not all(np.array_equal(x[f], y[f]) for x, y in zip(a, c) for f in ("src_nodes", "edge_src"))
+
+
+@pytest.mark.parametrize("dtype,C", [(torch.float32, 172), (torch.float64, 47), (torch.float32, 256)])
+def test_softmax_xent_bias_fused_equals_separate(P, dtype, C):
+    """gns_softmax_xent_bias (one launch: rows, mean loss, output bias
+    gradient) == gns_softmax_xent + gns_dense_bwd_bias: dlogits bit for bit,
+    the loss and bias gradient to the rounding of their (fixed, different)
+    summation orders; repeated launches reuse the ticket counter."""
+    from paper_2106_06150_b200 import _lib
+    lib = _lib.lib()
+    dt = 0 if dtype == torch.float32 else 1
+    gen = torch.Generator(device="cuda").manual_seed(C)
+    max_rows, pad = 1000, 1024
+    labels = torch.randint(0, C, (5000,), device="cuda", dtype=torch.int32, generator=gen)
+    targets = torch.randperm(5000, device="cuda", generator=gen)[:max_rows].sort().values.int()
+    ws = _lib.workspace(lib.gns_softmax_xent_bias_workspace_size(max_rows, pad, C), "cuda", zero=True)
+    ws2 = _lib.workspace(8 * 4096, "cuda")
+    wsd = _lib.workspace(lib.gns_dense_bwd_workspace_size(pad, C), "cuda")
+    for n in (1000, 777, 1):
+        logits = torch.randn((pad, C), dtype=dtype, device="cuda", generator=gen) * 3
+        n_dev = torch.tensor([n], dtype=torch.int32, device="cuda")
+        g1 = torch.full((pad, C), 7.0, dtype=dtype, device="cuda")
+        g2 = torch.full((pad, C), 7.0, dtype=dtype, device="cuda")
+        l1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        l2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        b1 = torch.zeros(C, dtype=dtype, device="cuda")
+        b2 = torch.zeros(C, dtype=dtype, device="cuda")
+        _lib.call("gns_softmax_xent", dt, logits.data_ptr(), C, n_dev.data_ptr(), max_rows, pad, C,
+                  labels.data_ptr(), targets.data_ptr(), g1.data_ptr(), l1.data_ptr(), ws2.data_ptr(), ws2.numel(),
+                  _lib.stream_ptr())
+        _lib.call("gns_dense_bwd_bias", dt, g1.data_ptr(), None, C, None, pad, C, None, b1.data_ptr(),
+                  wsd.data_ptr(), wsd.numel(), _lib.stream_ptr())
+        for _ in range(2):
+            _lib.call("gns_softmax_xent_bias", dt, logits.data_ptr(), C, n_dev.data_ptr(), max_rows, pad, C,
+                      labels.data_ptr(), targets.data_ptr(), g2.data_ptr(), l2.data_ptr(), b2.data_ptr(),
+                      ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+            assert torch.equal(g1, g2)
+            assert abs(float(l1) - float(l2)) <= 1e-13 * abs(float(l1))
+            ref = g1[:n].double().sum(0)
+            eps = 1e-6 if dtype == torch.float32 else 1e-13
+            tol = eps * g1[:n].double().abs().sum(0) + eps
+            assert torch.all((b2.double() - ref).abs() <= tol)
+            assert torch.all((b1.double() - ref).abs() <= tol)
+        # the loss is the reference's mean cross-entropy (model.py:189-200)
+        lp = torch.log_softmax(logits[:n].double(), 1)
+        want = -lp[torch.arange(n), labels[targets[:n].long()].long()].mean()
+        assert abs(float(l2) - float(want)) <= (1e-5 if dtype == torch.float32 else 1e-12) * max(1.0, abs(float(want)))
