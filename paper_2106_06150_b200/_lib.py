@@ -226,7 +226,7 @@ KERNELS_PER_CALL = {
     "gns_degree_probs": 1, "gns_random_walk_probs": 9, "gns_cache_draw": 15, "gns_inclusion": 1, "gns_cached_csr_count": 3,
     "gns_cached_csr_fill": 1, "gns_estimate_edge_inclusion": 0, "gns_sample_layer": 7, "gns_relabel": 4, "gns_unique_sorted": 3,
     "gns_epoch_targets": 1, "gns_epoch_targets_dev": 1, "gns_batch_targets_sorted": 1, "gns_batch_slice_sorted": 1, "gns_copy_mapped": 1, "gns_errors_accumulate": 1, "gns_gather_rows": 1, "gns_gather_rows_mixed": 1,
-    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_sum_rows": 1, "gns_graph_switch_begin": 1, "gns_graph_switch_handles": 1, "gns_graph_switch_node": 0, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2, "gns_spmm_fwd_bits": 1, "gns_spmm_bwd_transposed_bits": 1,
+    "gns_cache_refresh_rows": 1, "gns_bitmap_rank": 1, "gns_spmm_fwd": 1, "gns_spmm_fwd_gather": 1, "gns_sum_rows": 1, "gns_graph_switch_begin": 1, "gns_graph_switch_handles": 1, "gns_graph_switch_node": 0, "gns_spmm_bwd": 7, "gns_block_transpose": 5, "gns_spmm_bwd_transposed": 2, "gns_spmm_fwd_bits": 1, "gns_spmm_bwd_transposed_bits": 2,
     "gns_adam_dev": 1,
     "gns_softmax_xent": 2, "gns_softmax_xent_bias": 1, "gns_adam": 1, "gns_dense_bwd_bias": 2, "gns_gen_powerlaw_count": 6, "gns_gen_powerlaw_fill": 1, "gns_build_csr_count": 6, "gns_build_csr_fill": 1,
     "gns_gen_node_attrs": 1, "gns_gen_features": 2,

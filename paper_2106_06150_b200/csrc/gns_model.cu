@@ -939,10 +939,8 @@ static inline int spmm_grid(Kernel k, long long rows) {
 }
 
 // ---- SpMM backward -------------------------------------------------------------
-__global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of,
-                              unsigned* __restrict__ ticket) {
+__global__ void tcount_kernel(BlockView bv, int32_t* __restrict__ tcount, int32_t* __restrict__ self_of) {
   const int64_t ne = bv.counts[GNS_CNT_EDGES], nd = bv.counts[GNS_CNT_DST];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;   // the transposed SpMM's bias-gradient ticket
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ne + nd; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < ne)
       atomicAdd(tcount + bv.edge_src[i], 1);
@@ -1242,6 +1240,23 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
   }
 }
 
+// Column c of a [rows x ncols] row-major partial-sum matrix, summed in a
+// fixed order by one thread: 8 interleaved accumulators (row b into b & 7,
+// so 8 loads are in flight) combined in index order.  Deterministic.
+template <typename T>
+__device__ __forceinline__ T colsum_fixed(const T* __restrict__ part, int rows, int ncols, int c) {
+  T a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = (T)0;
+  int b = 0;
+  for (; b + 8 <= rows; b += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] += __ldcg(part + (int64_t)(b + j) * ncols + c);
+  }
+  for (int j = 0; b < rows; ++b, ++j) a[j] += __ldcg(part + (int64_t)b * ncols + c);
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
 // Lane-staged transposed SpMM (float32, relu' from the forward's bits; the
 // default for dim <= 256).  A warp owns kChunkRows consecutive source rows
 // and lane j holds row j's metadata: transpose bounds, self position and
@@ -1264,9 +1279,7 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
                                                                       float* __restrict__ dh, int64_t ld_dh,
                                                                       int64_t pad_rows, float* __restrict__ colpart,
                                                                       const uint32_t* __restrict__ relu_bits,
-                                                                      const float* __restrict__ twn,
-                                                                      float* __restrict__ db,
-                                                                      unsigned* __restrict__ ticket) {
+                                                                      const float* __restrict__ twn) {
   constexpr int W = kSpmmBlock / 32;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t n = bv.counts[GNS_CNT_SRC];
@@ -1394,21 +1407,6 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
       for (int w = 0; w < W; ++w) t += red[w][col];
       colpart[(int64_t)blockIdx.x * dim + col] = t;
     }
-    // the last CTA to finish sums the CTA partials in CTA order (the bias
-    // gradient, deterministic) and leaves the ticket at zero
-    __shared__ bool s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (threadIdx.x == 0) *ticket = 0u;
-    for (int col = threadIdx.x; col < dim; col += blockDim.x) {
-      float t = 0.f;
-      for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(colpart + (int64_t)b * dim + col);
-      db[col] = t;
-    }
   }
 }
 
@@ -1476,7 +1474,6 @@ static inline void colsum_launch(const T* part, int nrows, int ncols, T* out, cu
 
 struct BwdWs {
   void* colpart;
-  unsigned* ticket;   // last-CTA ticket of the fused bias-gradient reduction (reset by the transpose)
   int32_t* tcount;
   int32_t* tptr;
   int32_t* self_of;
@@ -1489,7 +1486,6 @@ struct BwdWs {
 static size_t bwd_ws(int64_t max_src, int64_t max_edges, int32_t dim, void* base, size_t cap, BwdWs* w) {
   Workspace ws(base, cap);
   w->colpart = (void*)ws.take<double>((size_t)num_sms() * 8 * (size_t)(dim > 0 ? dim : 1));
-  w->ticket = ws.take<unsigned>(1);
   w->tcount = ws.take<int32_t>(max_src + 1);
   w->tptr = ws.take<int32_t>(max_src + 1);
   w->self_of = ws.take<int32_t>(max_src + 1);
@@ -1609,11 +1605,7 @@ __global__ void __launch_bounds__(256) xent_bias_kernel(const T* __restrict__ lo
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += __ldcg(row_loss + i);
   acc = warp_sum(acc);
   if (lane == 0) s_red[wib] = acc;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    T t = (T)0;
-    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(partial + (int64_t)b * C + c);
-    grad_bias[c] = t;
-  }
+  for (int c = threadIdx.x; c < C; c += blockDim.x) grad_bias[c] = colsum_fixed(partial, gridDim.x, C, c);
   __syncthreads();
   if (threadIdx.x == 0) {
     double v = 0;
@@ -2122,7 +2114,7 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
   spmm_bwd_rows_kernel<CH, R, B><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,         \
                                                                 w.self_of, dh, ld_dh, pad_rows,                 \
                                                                 db ? (float*)w.colpart : nullptr, relu_bits,    \
-                                                                w.twn, db, w.ticket)
+                                                                w.twn)
   // knob: 1 = R2/4 CTAs per SM, 2 = R2/3, 3 = R4/3, 4 = R4/2, 5 = R8/2
   if (g_tune_bwd > 0 && dv <= 64) {
     if (dv <= 32) {
@@ -2138,7 +2130,11 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
     } else {
       GNS_BWDC(2, 8, 2);
     }
-    return check_launch("spmm_bwd_bits");   // (bias gradient reduced in the kernel)
+    GNS_TRY(check_launch("spmm_bwd_bits"));
+    // (a last-CTA reduction inside the kernel was measured slower: one SM
+    // summing ~300 partial rows is latency-bound; colsum spreads it)
+    if (db) colsum_launch<float>((const float*)w.colpart, g2, dim, db, stream);
+    return check_launch("spmm_bwd_bits colsum");
   }
 #undef GNS_BWDC
 #define GNS_BWDB(CH)                                                                                             \
@@ -2223,7 +2219,7 @@ int gns_block_transpose(const gns_block_t* block, int64_t max_dst, int64_t max_s
   GNS_CUDA(cudaMemsetAsync(w.tcount, 0, (max_src + 1) * sizeof(int32_t), stream));
   GNS_CUDA(cudaMemsetAsync(w.self_of, 0xff, (max_src + 1) * sizeof(int32_t), stream));
   int g1 = grid_for((max_edges + max_dst + 255) / 256, (long long)sms * 8);
-  tcount_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.self_of, w.ticket);
+  tcount_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.self_of);
   const unsigned ttiles = (unsigned)((max_src + kTsBlock * kTsItems - 1) / (kTsBlock * kTsItems)) + 1;
   tscan_reduce_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, (unsigned long long*)w.scan);
   tscan_apply_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, w.tptr, (unsigned long long*)w.scan);
@@ -2348,8 +2344,10 @@ int gns_softmax_xent(int32_t dtype, const void* logits, int64_t ld, const int32_
   return check_launch("softmax_xent");
 }
 
+// <= 64 CTAs: the last CTA's fixed-order column sums over the CTA partials
+// stay a few round trips (each warp takes several rows instead)
 static int xent_bias_grid(int64_t max_rows, int64_t pad_rows) {
-  return grid_for(((max_rows > pad_rows ? max_rows : pad_rows) * 32 + 255) / 256, (long long)num_sms() * 8);
+  return grid_for(((max_rows > pad_rows ? max_rows : pad_rows) * 32 + 255) / 256, 64);
 }
 
 size_t gns_softmax_xent_bias_workspace_size(int64_t max_rows, int64_t pad_rows, int32_t num_classes) {

@@ -315,7 +315,7 @@ class GraphedTrainer:
             # mean loss and the output bias gradient, in one launch
             n_top = top.counts[_lib.CNT_DST:_lib.CNT_DST + 1]
             loss_ptr = (self.loss if loss_out is None else loss_out).data_ptr()
-            if self.dims[L] <= 256:
+            if self.dims[L] <= 256 and os.environ.get("GNS_FUSED_XENT", "1") == "1":
                 _lib.call("gns_softmax_xent_bias", 0, logits.data_ptr(), logits.stride(0), n_top.data_ptr(),
                           self.cap_dst[L - 1], self.npad[L - 1], logits.shape[1], self.g.labels.data_ptr(),
                           sl.seeds0.data_ptr(), self.dz[L - 1].data_ptr(), loss_ptr,
