@@ -87,7 +87,8 @@ def launch_table(path, steps=5):
 def main():
     src, tag = sys.argv[1], sys.argv[2]
     os.makedirs(os.path.join(PROF, "bench"), exist_ok=True)
-    md = [f"# Profiles — round 1 (`{tag}`, {os.path.basename(src)})", ""]
+    rnd = tag[1:].split("_")[0].rstrip("abcdefghijklmnopqrstuvwxyz") if tag.startswith("r") else "?"
+    md = [f"# Profiles — round {rnd} (`{tag}`, {os.path.basename(src)})", ""]
     md.append("Produced by `scripts/round_profile.sh` on one B200 (gpurun) and summarised by "
               "`scripts/summarize_profiles.py`.  ncu numbers are serialised, cold-cache replays: "
               "compare shares, not absolutes, with the in-graph CUDA-event timings of bench.py.")
@@ -105,7 +106,7 @@ def main():
             f.write(json.dumps(d) + "\n")
         cpu = d.get("cpu_baseline") or {}
         md.append(f"| {cfg} | {d['value']:.1f} | {d['ms_per_step']:.3f} | {d['e2e']['value']:.1f} | "
-                  f"{d['roofline']['frac']:.3f} | {d['kernels']['gns_gather_rows']['frac']:.3f} | "
+                  f"{d['roofline']['frac']:.3f} | {d['kernels']['gather_rows']['frac']:.3f} | "
                   f"{(d.get('parity') or {}).get('bit_exact')} | {cpu.get('value', float('nan')):.3f} "
                   f"({cpu.get('cores')}) |")
     ref = last_json(os.path.join(src, "bench_papers100m_reference.log"))
@@ -119,18 +120,30 @@ def main():
     if os.path.exists(lp):
         shutil.copy(lp, os.path.join(PROF, f"{tag}_launches_papers100m.csv"))
         per_step, table = launch_table(lp)
-        md += ["", "## Launch list, papers100M-shaped (`ncu --metrics gpu__time_duration.sum`, 5 steps)", "",
+        md += ["", "## Launch list, papers100M-shaped (`ncu --metrics gpu__time_duration.sum`, 5 steps, "
+               "size-switched GEMMs off: ncu cannot replay graphs with conditional nodes)", "",
                f"Serialised cold sum {per_step:.0f} µs per step (the graph overlaps the sampling branch with "
                "training).", "", table]
     traffic = {}
-    for rep, title in (("ncu_full_step.ncu-rep", "training-branch SpMM kernels"),
-                       ("ncu_full_sampler.ncu-rep", "sampling-branch kernels"),
-                       ("ncu_full_gather.ncu-rep", "reference-API gather")):
+    for rep, title, keep in (("ncu_full_kernels.ncu-rep", "training-branch HBM kernels in the timed configuration "
+                              "(`scripts/kernel_ncu.py`: eager launches with the step graph's arguments)", None),
+                             ("ncu_full_sampler.ncu-rep", "sampling-branch kernels, one chain "
+                              "(`scripts/sampler_ncu.py`; selection tiers and enumeration kept)",
+                              "sample_warp|sample_stream|enumerate_apply"),
+                             ("ncu_full_step.ncu-rep", "training-branch SpMM kernels", None),
+                             ("ncu_full_gather.ncu-rep", "reference-API gather", None)):
         path = os.path.join(src, rep)
         if not os.path.exists(path):
             continue
-        shutil.copy(path, os.path.join(PROF, f"{tag}_{rep}"))
+        dst = os.path.join(PROF, f"{tag}_{rep}")
+        if keep:   # commit the main kernels only (the full report stays in gpurun_out/)
+            subprocess.run(["ncu", "-i", path, "-k", f"regex:{keep}", "--export", dst, "-f"], capture_output=True)
+        else:
+            shutil.copy(path, dst)
         rows = ncu_rows(path)
+        if keep:
+            import re
+            rows = [d for d in rows if re.search(keep, d.get("Kernel Name", ""))]
         md += ["", f"## `ncu --set full`: {title} (`profiles/{tag}_{rep}`)", "",
                "| kernel | grid | " + " | ".join(u for _, u, _ in METRICS[:-1]) + " |",
                "|---|---:|" + "---:|" * (len(METRICS) - 1)]
@@ -143,15 +156,18 @@ def main():
             md.append(f"| `{name}` | {d.get('launch__grid_size', '')} | " + " | ".join(vals) + " |")
             rd, wr = num(d, "dram__bytes_read.sum"), num(d, "dram__bytes_write.sum")
             if rd is not None and wr is not None:
-                if "spmm_fwd_narrow_kernel<0, 1" in d.get("Kernel Name", "") or "spmm_fwd_narrow_kernel<false, true" in \
-                        d.get("Kernel Name", ""):
+                kn = d.get("Kernel Name", "")
+                if "spmm_fwd_chunk_kernel<0, 1" in kn or "spmm_fwd_chunk_kernel<false, true" in kn:
                     traffic.setdefault("spmm_fwd_gather", int(rd + wr))
+                if "spmm_bwd_rows_kernel" in kn:
+                    traffic.setdefault("spmm_bwd_transposed", int(rd + wr))
                 if "gather_f32x4" in d.get("Kernel Name", ""):
                     traffic.setdefault("gather_f32x4_kernel", int(rd + wr))
     if traffic:
         with open(os.path.join(PROF, "traffic.json"), "w") as f:
             json.dump({"_note": f"dram__bytes_read.sum + dram__bytes_write.sum per launch, first launch of each "
-                                f"kernel in profiles/{tag}_ncu_full_*.ncu-rep (papers100M-shaped bench)",
+                                f"kernel in profiles/{tag}_ncu_full_kernels.ncu-rep (papers100M-shaped bench, "
+                                f"the timed configuration's arguments)",
                        "papers100m": traffic}, f, indent=1)
             f.write("\n")
     with open(os.path.join(PROF, "README.md"), "w") as f:
