@@ -36,6 +36,7 @@ constexpr int kStreamK = 8;       // streaming top-k tier: take <= 8 and <= stre
 static int g_stream_len = 32;     // (gns_tune "stream_len", <= 2047)
 static int g_thread_len = 0;      // (gns_tune "thread_len", <= 16; 0 = no sorting-network tier: measured best)
 static int g_stream_minb = 1;     // (gns_tune "stream_minb": 1, 3, 4) min resident CTAs/SM of the streaming tier
+static int g_stream_k5 = 1;       // (gns_tune "stream_k5": 0/1) fanout <= 5: keep 5 keys in the streaming tier
 static int g_warp_sort = 1;       // (gns_tune "warp_sort": 0/1) see LayerArgs::warp_sort
 static int g_sampler_ctas = 0;    // (gns_tune "sampler_ctas") cap grid-stride sampler grids at this many CTAs
                                   // per SM (0 = no cap): leaves SM room to the concurrent training branch
@@ -668,22 +669,27 @@ __device__ __forceinline__ void thread_select16(const LayerArgs& a, const Rng3& 
 // of the kStreamK smallest packed (key53 << 11 | position) values — the
 // reference's (key, position) lexsort order — so only ~kStreamK live keys
 // are held (the sorting-network tier holds 16 plus the candidates' ids).
-__device__ __forceinline__ void insert_sorted(uint64_t (&best)[kStreamK], uint64_t v) {
+template <int K>
+__device__ __forceinline__ void insert_sorted(uint64_t (&best)[K], uint64_t v) {
 #pragma unroll
-  for (int i = kStreamK - 1; i >= 1; --i) {
+  for (int i = K - 1; i >= 1; --i) {
     const uint64_t lo = best[i - 1];
     best[i] = v < lo ? lo : (v < best[i] ? v : best[i]);
   }
   best[0] = v < best[0] ? v : best[0];
 }
 
+// K = the kept-key count (>= take): kStreamK, or 5 for layers whose fanout
+// is <= 5 (the cache-only input layer: each insertion is a K-1 step
+// compare-select chain on 64-bit keys, as costly as the Philox pair itself)
+template <int K>
 __device__ __forceinline__ void thread_select_stream(const LayerArgs& a, const Rng3& rk, const RowInfo& ri,
                                                      int64_t r, const PhaseDesc& ph) {
   const uint32_t stream = stream_word(32, a.layer, ph.phase);
   const int len = ph.len;
-  uint64_t best[kStreamK];
+  uint64_t best[K];
 #pragma unroll
-  for (int i = 0; i < kStreamK; ++i) best[i] = ~0ull;
+  for (int i = 0; i < K; ++i) best[i] = ~0ull;
   for (int p0 = 0; p0 < len; p0 += 8) {
     // fill phase: the 8 neighbour ids and cache-bitmap words in flight at once
     int32_t idv[8];
@@ -705,8 +711,8 @@ __device__ __forceinline__ void thread_select_stream(const LayerArgs& a, const R
         ok0 = !((mw[2 * q] >> (idv[2 * q] & 31)) & 1u);
         ok1 = ok1 && !((mw[2 * q + 1] >> (idv[2 * q + 1] & 31)) & 1u);
       }
-      if (ok0) insert_sorted(best, (k0 << 11) | (uint64_t)p);
-      if (ok1) insert_sorted(best, (k1 << 11) | (uint64_t)(p + 1));
+      if (ok0) insert_sorted<K>(best, (k0 << 11) | (uint64_t)p);
+      if (ok1) insert_sorted<K>(best, (k1 << 11) | (uint64_t)(p + 1));
     }
   }
   // emit the first `take`, 4 at a time: every load of a chunk's edges
@@ -714,19 +720,20 @@ __device__ __forceinline__ void thread_select_stream(const LayerArgs& a, const R
   const int take = ph.take;
   const int64_t o0 = ph.out_base;
 #pragma unroll
-  for (int c0 = 0; c0 < kStreamK; c0 += 4) {
+  for (int c0 = 0; c0 < K; c0 += 4) {
     if (c0 >= take) break;
     int32_t u[4];
     double inc[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) u[i] = c0 + i < take ? __ldg(ph.ids + (uint32_t)(best[c0 + i] & 2047u)) : 0;
+    for (int i = 0; i < 4; ++i)
+      u[i] = (c0 + i < K && c0 + i < take) ? __ldg(ph.ids + (uint32_t)(best[(c0 + i) % K] & 2047u)) : 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       inc[i] = (c0 + i < take && ph.phase == 0 && !a.exact_q) ? __ldg(a.incl + u[i]) : 0.0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (c0 + i < take) {
-        const double w = a.exact_q ? exact_weight(a, ri, ph, (uint32_t)(best[c0 + i] & 2047u))
+        const double w = a.exact_q ? exact_weight(a, ri, ph, (uint32_t)(best[(c0 + i) % K] & 2047u))
                                    : edge_weight_of(a, ri, ph, inc[i]);
         mark_node(a.dbits, a.dsum, u[i]);
         a.b.edge_node[o0 + c0 + i] = u[i];
@@ -738,7 +745,7 @@ __device__ __forceinline__ void thread_select_stream(const LayerArgs& a, const R
   }
 }
 
-template <int MINB>
+template <int MINB, int K = kStreamK>
 __global__ void __launch_bounds__(256, MINB) sample_stream_kernel(const __grid_constant__ LayerArgs a) {
   const Rng3 rk = batch_rng(a);
   const int64_t nl = a.b.counts[GNS_CNT_STREAMROWS];
@@ -748,7 +755,7 @@ __global__ void __launch_bounds__(256, MINB) sample_stream_kernel(const __grid_c
     RowInfo ri = row_info(a, r);
     PhaseDesc pc, pf;
     make_phases(a, ri, r, pc, pf);
-    thread_select_stream(a, rk, ri, r, (item & 1) ? pf : pc);
+    thread_select_stream<K>(a, rk, ri, r, (item & 1) ? pf : pc);
   }
 }
 
@@ -1111,7 +1118,9 @@ int gns_sample_layer(const gns_graph_t* g, const gns_cache_t* cache, const int32
   // one wave of resident CTAs at most (grid-stride loops over the item lists)
   const long long cap = g_sampler_ctas ? (long long)sms * g_sampler_ctas : (1LL << 30);
   const long long titems = grid_for((2 * max_dst + 255) / 256, cap);
-  if (g_stream_minb == 4)
+  if (k <= 5 && g_stream_k5)   // every take of this layer is <= k <= 5
+    sample_stream_kernel<1, 5><<<resident_grid(sample_stream_kernel<1, 5>, 256, 0, titems), 256, 0, stream>>>(a);
+  else if (g_stream_minb == 4)
     sample_stream_kernel<4><<<resident_grid(sample_stream_kernel<4>, 256, 0, titems), 256, 0, stream>>>(a);
   else if (g_stream_minb == 3)
     sample_stream_kernel<3><<<resident_grid(sample_stream_kernel<3>, 256, 0, titems), 256, 0, stream>>>(a);
@@ -1145,6 +1154,10 @@ int gns_sample_tune(const char* name, int32_t value) {
   }
   if (!strcmp(name, "sampler_ctas") && value >= 0) {
     g_sampler_ctas = value;
+    return GNS_OK;
+  }
+  if (!strcmp(name, "stream_k5") && (value == 0 || value == 1)) {
+    g_stream_k5 = value;
     return GNS_OK;
   }
   if (!strcmp(name, "warp_sort") && (value == 0 || value == 1)) {

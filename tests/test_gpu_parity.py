@@ -207,7 +207,7 @@ def _mid_hub_graph(n=5000, seed=17):
 @pytest.mark.parametrize("tune", [{"thread_len": 16, "stream_len": 0}, {"thread_len": 16, "stream_len": 32},
                                   {"thread_len": 0, "stream_len": 64}, {"sampler_ctas": 1},
                                   {"warp_sort": 0}, {"stream_len": 0, "count_items": 1},
-                                  {"count_items": 2, "stream_minb": 4}])
+                                  {"count_items": 2, "stream_minb": 4}, {"stream_k5": 0}])
 def test_minibatch_selection_tiers_all_exact(P, tune):
     """Every routing of (row, phase) items over the selection tiers (sorting
     network, streaming top-k, warp, CTA) gives the reference's blocks."""
@@ -221,7 +221,7 @@ def test_minibatch_selection_tiers_all_exact(P, tune):
     oc = O.build_cache(og, O.degree_probs(og), cs, seed=3, epoch=0)
     targets = np.random.default_rng(2).choice(og.num_nodes, 400, replace=False)
     defaults = {"thread_len": 0, "stream_len": 32, "sampler_ctas": 0, "warp_sort": 1, "count_items": 4,
-                "stream_minb": 1}
+                "stream_minb": 1, "stream_k5": 1}
     try:
         for k, v in tune.items():
             _lib.call("gns_tune", k.encode(), v)
