@@ -591,23 +591,28 @@ def ours_arm(args, name, c, world, rank, local):
         nw = 4 * te.S * max(1, 48 // (4 * te.S))
         k2 = -(-k2 // te.S) * te.S   # whole replays in the timed region
         # rank r's host batches: r, r+W, ... of the permutation (pool.py:80)
+        S = te.S
         batches = [perm[((j * world + rank) % nbh) * BATCH:((j * world + rank) % nbh + 1) * BATCH]
-                   for j in range(k2 + nw)]
-        te.run_host(batches[:nw], epoch=0)
+                   for j in range(k2 + nw + S)]
+        # one continuous loop over host batches split at the timed window: each
+        # call samples the next call's first S batches ahead (lookahead), so
+        # the window holds exactly k2 target reads from pinned memory and k2
+        # loss reads, as a steady-state training loop does
+        te.run_host(batches[:nw], epoch=0, lookahead=batches[nw:nw + S])
         torch.cuda.synchronize()
         if distributed:
             dist.barrier()
         w0 = time.perf_counter()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(te.main)
-        te.run_host(batches[nw:], epoch=0)
+        te.run_host(batches[nw:nw + k2], epoch=0, base=nw, lookahead=batches[nw + k2:nw + k2 + S])
         s1.record(te.main)
         s1.synchronize()
         wall = gdist.max_over_ranks(time.perf_counter() - w0, device="cuda")
         got = []
-        if solo:   # the last replay's slots: its batches k2-S .. k2-1 (Philox batch = position)
-            for k in range(k2 - te.S, k2):
-                got.append((0, k, batches[nw + k], slot_blocks(te, te.slot_of(k))))
+        if solo:   # the last replay's slots: its batches k2-S .. k2-1 (Philox batch = nw + position)
+            for k in range(k2 - S, k2):
+                got.append((0, nw + k, batches[nw + k], slot_blocks(te, te.slot_of(k))))
         return {"value": k2 * world / wall, "unit": UNIT, "h2d_bytes_per_step": BATCH * 4 + 4 + 32,
                 "d2h_bytes_per_step": 8, "steps": k2, "device_ms_per_step": s0.elapsed_time(s1) / k2,
                 "path": f"GraphedTrainer(host_targets=True{tag}).run_host: pinned host targets read by a copy kernel "

@@ -140,6 +140,12 @@ class GraphedTrainer:
             self.tables[0] = torch.empty((max(cs, 1), hf.shape[1]), dtype=torch.float32, device=g.device)
         # double-buffered cache: csets[cur] is the active CacheState; the
         # other set receives the next refresh epoch's cache (prefetch)
+        # (epoch, batch indices, slot group, cache set) the last replay of the
+        # previous run_epoch call sampled ahead, and the first group's parity
+        # of the latest call (slot_of)
+        self._ready = None
+        self._q0 = 0
+        self.prologues = 0         # eager first-group samplings (run_epoch calls that could not continue)
         self.csets = [None, None]
         self._adopted = None       # a caller's CacheState set through `cache` (never written)
         self.cur = 0
@@ -190,6 +196,7 @@ class GraphedTrainer:
         CacheState is never written: later refreshes draw into buffers of the
         engine's own (_own_set)."""
         self._adopted = state
+        self._ready = None
         self.csets[self.cur] = state
         self._free_execs(self.cur)
         if self.placement == "mixed" and state is not None:
@@ -489,6 +496,7 @@ class GraphedTrainer:
         buffers moved."""
         if self.cfg.strategy != "GNS":
             return
+        self._ready = None      # batches sampled ahead used the previous cache
         if self._probs is None:
             self._probs = cache_probs(self.g, self.cfg)
         cs = self._cache_size()
@@ -623,8 +631,8 @@ class GraphedTrainer:
         return [p * self.S + j for j in range(self.S)]
 
     def slot_of(self, k: int) -> int:
-        """Sampler slot holding the k-th batch of a run_epoch call."""
-        return ((k // self.S) % 2) * self.S + k % self.S
+        """Sampler slot holding the k-th batch of the latest run_epoch call."""
+        return ((k // self.S + self._q0) % 2) * self.S + k % self.S
 
     def _warm(self):
         # outside capture: cuBLAS handles / workspaces, NCCL communicator
@@ -813,16 +821,35 @@ class GraphedTrainer:
         nre = self._next_refresh_epoch(epoch) if self.prefetch else None
         S = self.S
         groups = [idx[i:i + S] for i in range(0, len(idx), S)]
-        # prologue: sample the first group into group-0 slots
-        for j, sl in enumerate(self._group(0)):
-            self._set_step(sl, epoch, groups[0][j] if j < len(groups[0]) else None)
-        with torch.cuda.stream(self.main):
-            for sl in self._group(0):
-                self._sample_body(sl)
+        full = self.batches(epoch)
+        end = first + len(idx)
+        rd, self._ready = self._ready, None
+        if rd is not None and rd == (epoch, tuple(groups[0]), rd[2], self.cur) and len(groups[0]) == S:
+            # the previous call's last replay already sampled this call's
+            # first group (same epoch and cache set): no eager prologue
+            q0 = rd[2]
+        else:
+            # prologue: sample the first group into group-0 slots
+            q0 = 0
+            self.prologues += 1
+            for j, sl in enumerate(self._group(0)):
+                self._set_step(sl, epoch, groups[0][j] if j < len(groups[0]) else None)
+            with torch.cuda.stream(self.main):
+                for sl in self._group(0):
+                    self._sample_body(sl)
+        self._q0 = q0
         k = 0
         for gi, grp in enumerate(groups):
-            p = gi % 2
-            nxt = groups[gi + 1] if gi + 1 < len(groups) else []
+            p = (gi + q0) % 2
+            if gi + 1 < len(groups):
+                nxt = groups[gi + 1]
+            else:
+                # the batches after this call's last one (same epoch): sampled
+                # by the last replay so a continuing call starts without a
+                # prologue
+                nxt = full[end:end + S] if len(full[end:end + S]) == S else []
+                if nxt:
+                    self._ready = (epoch, tuple(nxt), 1 - p, self.cur)
             for j, sl in enumerate(self._group(1 - p)):
                 self._set_step(sl, epoch, nxt[j] if j < len(nxt) else None)
             with torch.cuda.stream(self.main):
@@ -847,19 +874,31 @@ class GraphedTrainer:
         self.check_errors()
         return len(idx)
 
-    def run_host(self, batches, epoch: int = 0, on_loss=None):
+    def run_host(self, batches, epoch: int = 0, on_loss=None, base: int = 0, lookahead=None):
         """End-to-end API with host buffers: ``batches`` are host int arrays of
         target ids; every step reads them from pinned memory (a copy kernel in
         the graph) and writes every step's loss into pinned memory (another
         copy kernel at the end of the replay), read by the host one replay
-        late.  Requires
-        ``host_targets=True``."""
+        late.  Requires ``host_targets=True``.
+
+        Batch ``batches[i]`` draws Philox batch key ``base + i``.  A continuous
+        loop over host batches passes the next call's first S arrays as
+        ``lookahead`` (with ``len(batches) % S == 0``): the last replay samples
+        them, and the next call — ``base`` advanced by ``len(batches)``, its
+        first S arrays those same objects — starts without the eager
+        prologue, as consecutive replays do within a call."""
         if not self.host_targets:
             raise ValueError("construct with host_targets=True")
         if not batches:
             return []
+        nref = len(self.refresh_log)
+        rd, self._ready = self._ready, None
         self._begin(epoch)
+        if len(self.refresh_log) != nref:
+            rd = None           # sampled ahead with the previous cache
         S = self.S
+        n = len(batches)
+        ahead = list(lookahead)[:S] if lookahead is not None and n % S == 0 else []
         losses = []
         # double-buffered loss read-back: replay g+1 is queued before the host
         # waits for replay g's losses, so the GPU never idles on the host
@@ -877,25 +916,35 @@ class GraphedTrainer:
         def put(slot, k):
             if self.done[slot] is not None:
                 self.done[slot].synchronize()
-            if k is None or k >= len(batches):
+            arr = batches[k] if k < n else (ahead[k - n] if k - n < len(ahead) else None)
+            if arr is None:
                 self.ntgt_host[slot][0] = 0
                 return
-            t = torch.as_tensor(batches[k], dtype=torch.int32)
+            t = torch.as_tensor(arr, dtype=torch.int32)
             self.tgt_host[slot][:t.numel()].copy_(t)
             self.ntgt_host[slot][0] = t.numel()
             h = self.step_host[slot]
             h[0] = (self.cfg.seed & 0xFFFFFFFF) | ((epoch & 0xFFFFFFFF) << 32)
-            h[1] = k & 0xFFFFFFFF
-        for j, sl in enumerate(self._group(0)):
-            put(sl, j)
-        with torch.cuda.stream(self.main):
-            for sl in self._group(0):
-                self._sample_body(sl)
-        for gi, b0 in enumerate(range(0, len(batches), S)):
-            p = gi % 2
-            r = min(S, len(batches) - b0)
+            h[1] = (base + k) & 0xFFFFFFFF
+        key = ("host", epoch, base, tuple(id(x) for x in batches[:S]), self.cur)
+        if rd is not None and n >= S and rd[:5] == key:
+            q0 = rd[5]      # sampled ahead by the previous call's last replay
+        else:
+            q0 = 0
+            self.prologues += 1
+            for j, sl in enumerate(self._group(0)):
+                put(sl, j)
+            with torch.cuda.stream(self.main):
+                for sl in self._group(0):
+                    self._sample_body(sl)
+        self._q0 = q0
+        for gi, b0 in enumerate(range(0, n, S)):
+            p = (gi + q0) % 2
+            r = min(S, n - b0)
             for j, sl in enumerate(self._group(1 - p)):
                 put(sl, b0 + S + j)
+            if b0 + S >= n and len(ahead) == S:
+                self._ready = ("host", epoch, base + n, tuple(id(x) for x in ahead), self.cur, 1 - p)
             with torch.cuda.stream(self.main):
                 self._replay(p, r)
                 ev = torch.cuda.Event()

@@ -1006,6 +1006,36 @@ def test_engine_epoch_slots_bit_exact_vs_oracle(P, S, period):
     assert seen == [(e, i) for e in range(3) for i in range(len(batches))]
 
 
+@pytest.mark.parametrize("S", [1, 2])
+def test_engine_continuing_runs_sample_ahead(P, S):
+    """run() calls that continue an epoch (bench: warm-up, then the timed
+    window) reuse the batches the previous call's last replay sampled ahead —
+    one eager prologue in all — and every trained batch, read from the slot
+    slot_of() names, stays bit-identical to the oracle."""
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    og, g = _engine_graph(P, _hub_graph(5000, 47), train=0.6)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=200, cache_frac=0.03, cache_mode="degree",
+                          seed=6)
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), P.TrainConfig(), seed=0, steps_per_graph=S)
+    nb = len(tr.batches(0))
+    assert nb >= 12
+    oc = O.build_cache(og, O.degree_probs(og), O.cache_size_for(og, cfg.cache_frac), seed=cfg.seed, epoch=0)
+    batches = O.epoch_targets(og, cfg.batch_size, cfg.seed, 0)
+    seen = []
+
+    def check(e, index, k):
+        mb = tr.slots[tr.slot_of(k)].snapshot()
+        ref = O.build_minibatch(og, oc, batches[index], cfg, O.PhiloxKeys(cfg.seed, e, index))
+        assert_mb_equal(mb, ref, f"S{S} i{index}")
+        seen.append(index)
+
+    pos = (0, 0)
+    for n in (5, 3, 4):
+        pos = tr.run(n, epoch=pos[0], first=pos[1], on_step=check)
+    assert seen == list(range(12))
+    assert tr.prologues == 1
+
+
 @pytest.mark.parametrize("n,pairs", [(4000, 0), (3000, 1024 * 7), (20000, 100000)])
 def test_cached_csr_flat_passes_equal_per_row(P, n, pairs):
     """The cached CSR from the flat (entry-parallel) passes — keep bits per
@@ -1237,6 +1267,42 @@ def test_graphed_trainer_run_host_matches_eager(P, S):
            for k, b in enumerate(batches)]
     assert len(got) == len(batches)
     np.testing.assert_allclose(got, ref, rtol=2e-3)
+
+
+@pytest.mark.parametrize("S", [1, 2])
+def test_run_host_lookahead_equals_one_call(P, S):
+    """run_host split into calls that sample the next call's first batches
+    ahead (``lookahead``, ``base``) trains exactly what one continuous call
+    trains: identical losses, one eager prologue, and the last trained batch
+    bit-identical to the oracle on Philox key base + position."""
+    og = _hub_graph(4000, 53)
+    rng = np.random.default_rng(2)
+    feats = rng.normal(size=(og.num_nodes, 16)).astype(np.float32)
+    labels = rng.integers(0, 5, og.num_nodes).astype(np.int32)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices, features=feats, labels=labels)
+    cfg = P.SamplerConfig(strategy="GNS", fanouts=(10, 5), batch_size=200, cache_frac=0.05, cache_mode="degree",
+                          seed=7)
+    tc = P.TrainConfig(lr=0.003)
+    batches = [rng.choice(og.num_nodes, 200, replace=False) for _ in range(12)]
+    from paper_2106_06150_b200.engine import GraphedTrainer
+    one = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0, host_targets=True, steps_per_graph=S)
+    ref = one.run_host(batches, epoch=0)
+    tr = GraphedTrainer(g, cfg, (16, 32, 5), tc, seed=0, host_targets=True, steps_per_graph=S)
+    got = tr.run_host(batches[:4], epoch=0, lookahead=batches[4:4 + S])
+    got += tr.run_host(batches[4:10], epoch=0, base=4, lookahead=batches[10:10 + S])
+    got += tr.run_host(batches[10:], epoch=0, base=10)
+    assert tr.prologues == 1 and one.prologues == 1
+    assert got == ref
+    ids = tr.cache.nodes.ids.cpu().numpy().astype(np.int64)
+    mask = np.zeros(og.num_nodes, dtype=bool)
+    mask[ids] = True
+    oc = O.OCache(ids=ids, mask=mask, inclusion=tr.cache.inclusion.cpu().numpy(),
+                  cached_indptr=tr.cache.cached_indptr.cpu().numpy(),
+                  cached_indices=tr.cache.cached_indices.cpu().numpy(), epoch=0)
+    k = len(batches[10:]) - 1
+    mb = tr.slots[tr.slot_of(k)].snapshot()
+    want = O.build_minibatch(og, oc, batches[10 + k], cfg, O.PhiloxKeys(cfg.seed, 0, 10 + k))
+    assert_mb_equal(mb, want, f"S{S}")
 
 
 # ---- random-walk cache distribution (SURVEY.md §8(f)1) -----------------------------
