@@ -190,12 +190,14 @@ __device__ __forceinline__ V ldv(const V* p) {
 // relu' bits of a float32 row as the forward reads it (MASK variants): word
 // blk*4+q, bit l <-> element 4*(blk*32+l)+q, so lane l of a backward warp
 // finds its chunk's four bits at the same bit position of four words.
-// Written by lanes 0..3 after four ballots; every lane must call it.
+// Four ballots, then one 16-byte store by lane 0 (words blk*4 .. blk*4+3;
+// rows are (dv+31)/32*4 words, so the store is aligned); every lane must
+// call it.  (A per-lane select of the ballot for lanes 0..3 compiled to a
+// jump table: ~2x the instructions per row read.)
 __device__ __forceinline__ void put_relu_bits(uint32_t* __restrict__ mrow, int blk, const float4& v, bool valid) {
   const unsigned b0 = __ballot_sync(GNS_FULL, valid && v.x > 0.f), b1 = __ballot_sync(GNS_FULL, valid && v.y > 0.f);
   const unsigned b2 = __ballot_sync(GNS_FULL, valid && v.z > 0.f), b3 = __ballot_sync(GNS_FULL, valid && v.w > 0.f);
-  const int lane = threadIdx.x & 31;
-  if (lane < 4) mrow[blk * 4 + lane] = lane == 0 ? b0 : lane == 1 ? b1 : lane == 2 ? b2 : b3;
+  if ((threadIdx.x & 31) == 0) reinterpret_cast<uint4*>(mrow)[blk] = make_uint4(b0, b1, b2, b3);
 }
 __device__ __forceinline__ void put_relu_bits(uint32_t*, int, const double2&, bool) {}
 
