@@ -156,6 +156,14 @@ __device__ __forceinline__ float4 vdiv(const float4& a, float d) {
 }
 __device__ __forceinline__ double2 vdiv(const double2& a, double d) { return make_double2(DDIV(a.x, d), DDIV(a.y, d)); }
 
+// Row r of a float32 row-major table: one IMAD.WIDE.U32 (32 x 32 -> 64 with
+// the 64-bit base as addend) instead of a 64 x 64-bit multiply (3 IMADs + 3
+// address ops per row).  Row ids are non-negative node / row indices and the
+// row pitch in bytes fits 32 bits (checked on the host: ld * 4 < 2^32).
+__device__ __forceinline__ const float4* row4(const float* __restrict__ base, int32_t r, uint32_t pitch_bytes) {
+  return reinterpret_cast<const float4*>(reinterpret_cast<const char*>(base) + (uint64_t)(uint32_t)r * pitch_bytes);
+}
+
 constexpr int kRowCap = 128;  // max edges per dst row (fanout <= 128)
 constexpr int kSpmmBlock = 256;
 
@@ -574,6 +582,7 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_chunk_kernel(
   const int64_t tm = (int64_t)(bv.row_scan[n] >> 32);
   const int dv = dim >> 2;
   const bool on = lane < dv;
+  const uint32_t pitch = (uint32_t)ld_h * 4u;   // row pitch in bytes (ld_h < 2^30: host check)
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
@@ -659,14 +668,14 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_chunk_kernel(
         const int bj = s_base[wib][j & 31];
         xs[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (on && j < rows && ((fast >> j) & 1))
-          xs[q] = ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)s_self[wib][j] * ld_h) + lane);
+          xs[q] = ldv<float4, RELU>(row4(h, s_self[wib][j], pitch) + lane);
 #pragma unroll
         for (int t = 0; t < MAXL; ++t) {
           // defined on every path: a conditionally kept old value would pin
           // the array in local memory across iterations
           x[q][t] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (on && t < Lj)
-            x[q][t] = ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)s_idx[wib][bj + t] * ld_h) + lane);
+            x[q][t] = ldv<float4, RELU>(row4(h, s_idx[wib][bj + t], pitch) + lane);
         }
       }
 #pragma unroll
@@ -697,7 +706,7 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_chunk_kernel(
       narrow_row_slow<RELU>(h, ld_h, eidx, bv.edge_weight, cbs, ncs, fbs, s_len[wib][j], lane, on, acc);
       float4* crow = reinterpret_cast<float4*>(cat + (r0 + j) * ld_cat);
       if (on) {
-        crow[lane] = ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)s_self[wib][j] * ld_h) + lane);
+        crow[lane] = ldv<float4, RELU>(row4(h, s_self[wib][j], pitch) + lane);
         crow[dv + lane] = vdiv_count(acc, s_rnorm[wib][j]);
       }
     }
@@ -842,6 +851,7 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_fwd_wide_split_kernel(c
   const int64_t n = bv.counts[GNS_CNT_DST];
   const int64_t tm = (int64_t)(bv.row_scan[n] >> 32);
   const int dv = dim >> 2;
+  const uint32_t pitch = (uint32_t)ld_h * 4u;   // row pitch in bytes (ld_h < 2^30: host check)
   const int nch = (dv + 31) >> 5;
   const int mw = nch * 4;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -901,7 +911,7 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_fwd_wide_split_kernel(c
         for (int u = 0; u < G; ++u) {
           const int32_t iu = __shfl_sync(GNS_FULL, idx, (t + u) & 31);
           x[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (t + u < m && on) x[u] = vrelu(reinterpret_cast<const float4*>(h + (int64_t)iu * ld_h)[c]);
+          if (t + u < m && on) x[u] = vrelu(row4(h, iu, pitch)[c]);
         }
 #pragma unroll
         for (int u = 0; u < G; ++u) {
@@ -1326,7 +1336,8 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
         // first item: the first edge's neighbour half, else the self half
         const bool edge = ej > bj;
         const float4* src = reinterpret_cast<const float4*>(
-            edge ? dcat + (int64_t)dj * ld_dcat + dim : dcat + (int64_t)(sj < 0 ? 0 : sj) * ld_dcat);
+            edge ? dcat + dim + (uint64_t)(uint32_t)dj * ((uint32_t)ld_dcat)
+                 : dcat + (uint64_t)(uint32_t)(sj < 0 ? 0 : sj) * ((uint32_t)ld_dcat));
         const bool any = edge || sj >= 0;
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
@@ -2000,6 +2011,10 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
     set_error("spmm_fwd_gather: dim/strides must be multiples of 4 floats, pointers 16-B aligned");
     return GNS_EINVAL;
   }
+  if (ld_table >= (1LL << 30)) {   // the kernels address rows with a 32-bit byte pitch
+    set_error("spmm_fwd_gather: row stride %lld floats >= 2^30", (long long)ld_table);
+    return GNS_EINVAL;
+  }
   const int sms = num_sms();
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
   BlockView bv = view_of(block);
@@ -2043,8 +2058,8 @@ int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block
                       int64_t pad_rows, float* cat, int64_t ld_cat, uint32_t* relu_bits, void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (max_dst <= 0 && pad_rows <= 0) return GNS_OK;
-  if (dim % 4 || ld_h % 4 || ld_cat % 4) {
-    set_error("spmm_fwd_bits: dim/strides must be multiples of 4");
+  if (dim % 4 || ld_h % 4 || ld_cat % 4 || ld_h >= (1LL << 30)) {
+    set_error("spmm_fwd_bits: dim/strides must be multiples of 4 (row stride < 2^30 floats)");
     return GNS_EINVAL;
   }
   long long rows = max_dst > pad_rows ? max_dst : pad_rows;
@@ -2101,8 +2116,8 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
     set_error("spmm_bwd_bits: workspace %zu < %zu", ws_bytes, need);
     return GNS_EINVAL;
   }
-  if (dim % 4 || ld_dcat % 4 || ld_dh % 4 || dim > 512) {
-    set_error("spmm_bwd_bits: dim/strides must be multiples of 4 and dim <= 512");
+  if (dim % 4 || ld_dcat % 4 || ld_dh % 4 || dim > 512 || ld_dcat >= (1LL << 30)) {
+    set_error("spmm_bwd_bits: dim/strides must be multiples of 4, dim <= 512, row stride < 2^30");
     return GNS_EINVAL;
   }
   BlockView bv = view_of(block);
