@@ -919,7 +919,10 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_fwd_wide_split_kernel(c
           const int32_t iu = __shfl_sync(GNS_FULL, idx, (t + u) & 31);
           if (t + u < m) {
             if (on) vfma<true>(acc, wu, x[u]);
-            if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)iu * mw, j, x[u], on);
+            if constexpr (MASK)
+              put_relu_bits(reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(relu_bits) +
+                                                        (uint64_t)(uint32_t)iu * (uint32_t)(mw * 4)),
+                            j, x[u], on);
           }
         }
       }
