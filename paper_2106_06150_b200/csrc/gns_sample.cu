@@ -823,17 +823,21 @@ __global__ void setbits_kernel(const int32_t* __restrict__ a, const int32_t* __r
   }
 }
 
-// Tile = 64 summary words (65536 node ids) per CTA, 8 per warp: the warp's
-// 256 bitmap words are read as 8 consecutive words per lane (two 16-B loads,
-// skipped when the lane's 8 summary bits are zero), so the output order —
-// ascending word — is lane-major and one warp scan of the lanes' popcounts
-// ranks every word (instead of one scan per summary word).
+// A warp walks kEnumSeg segments of 8 summary words (256 bitmap words each);
+// a segment's bitmap words are read as 8 consecutive words per lane (two
+// 16-B loads, skipped when the lane's 8 summary bits are zero), so the output
+// order — ascending word — is lane-major within a segment and one warp scan
+// ranks a segment's words.  Tile = 8 warps x kEnumSeg segments (256 summary
+// words, 262144 node ids per CTA): the per-CTA prefix / block sums are paid
+// once per 4 segments (the work of a sparse layer is mostly that fixed cost).
 constexpr int kEnumBlock = 256;
 constexpr int kEnumWarps = kEnumBlock / 32;
-constexpr int kEnumPerWarp = 8;
-constexpr int kEnumTileSw = kEnumWarps * kEnumPerWarp;
+constexpr int kEnumPerWarp = 8;   // summary words per segment
+constexpr int kEnumSeg = 4;       // segments per warp
+constexpr int kEnumTileSw = kEnumWarps * kEnumPerWarp * kEnumSeg;
 
-// lane's 8 bitmap words (bitmap words (sw0 * 32 + 8 * lane) ...) and their popcount
+// lane's 8 bitmap words of the segment at summary word sw0 (bitmap words
+// sw0 * 32 + 8 * lane ...) and their popcount
 __device__ __forceinline__ unsigned enum_lane_words(const uint32_t* __restrict__ bits,
                                                     const uint32_t* __restrict__ sum, int64_t nsw, long long sw0,
                                                     int lane, uint4& w0, uint4& w1) {
@@ -849,14 +853,21 @@ __device__ __forceinline__ unsigned enum_lane_words(const uint32_t* __restrict__
          __popc(w1.w);
 }
 
+__device__ __forceinline__ long long enum_seg0(long long tile, int warp, int g) {
+  return (tile * kEnumWarps + warp) * (long long)(kEnumPerWarp * kEnumSeg) + g * kEnumPerWarp;
+}
+
 __global__ void __launch_bounds__(kEnumBlock) enumerate_reduce_kernel(const uint32_t* __restrict__ bits,
                                                                       const uint32_t* __restrict__ sum, int64_t nsw,
                                                                       unsigned long long* tile_sums) {
   __shared__ unsigned long long s_w[kEnumWarps + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long sw0 = (long long)blockIdx.x * kEnumTileSw + warp * kEnumPerWarp;
-  uint4 w0, w1;
-  const unsigned c = enum_lane_words(bits, sum, nsw, sw0, lane, w0, w1);
+  unsigned c = 0;
+#pragma unroll
+  for (int g = 0; g < kEnumSeg; ++g) {
+    uint4 w0, w1;
+    c += enum_lane_words(bits, sum, nsw, enum_seg0(blockIdx.x, warp, g), lane, w0, w1);
+  }
   unsigned long long t = block_sum<kEnumBlock>((unsigned long long)c, s_w);
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = t;
 }
@@ -880,35 +891,51 @@ __global__ void __launch_bounds__(kEnumBlock) enumerate_apply_kernel(uint32_t* _
   unsigned long long pre = 0;
   for (long long j = threadIdx.x; j < tile; j += kEnumBlock) pre += tile_sums[j];
   pre = block_sum<kEnumBlock>(pre, s_w);
-  const long long sw0 = tile * kEnumTileSw + warp * kEnumPerWarp;
-  uint4 w0, w1;
-  const unsigned c = enum_lane_words(bits, sum, nsw, sw0, lane, w0, w1);
-  const unsigned incl = warp_incl_scan(c);
-  if (lane == 31) s_wpre[warp] = incl;
-  __syncthreads();
-  unsigned long long o = pre + incl - c;
-  for (int w = 0; w < warp; ++w) o += s_wpre[w];
-  if (tile == ntiles - 1 && warp == kEnumWarps - 1 && lane == 31) out_n[0] = (int32_t)(o + c);
-  if (c) {
-    const uint32_t x8[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-    const long long wbase = sw0 * 32 + 8 * lane;
+  uint4 w[kEnumSeg][2];
+  unsigned c[kEnumSeg], ct = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t x = x8[i];
-      if (x) {
-        const long long w = wbase + i;
-        rank2[w] = (o << 32) | (unsigned long long)x;
-        bits[w] = 0u;
-        uint32_t y = x;
-        while (y) {
-          const int bb = __ffs(y) - 1;
-          y &= y - 1;
-          out[o++] = (int32_t)(w * 32 + bb);
+  for (int g = 0; g < kEnumSeg; ++g) {
+    c[g] = enum_lane_words(bits, sum, nsw, enum_seg0(tile, warp, g), lane, w[g][0], w[g][1]);
+    ct += c[g];
+  }
+  const unsigned wtot = warp_sum(ct);
+  if (lane == 0) s_wpre[warp] = wtot;
+  __syncthreads();
+  unsigned long long base = pre;
+  for (int v = 0; v < warp; ++v) base += s_wpre[v];
+  if (tile == ntiles - 1 && warp == kEnumWarps - 1 && lane == 0) out_n[0] = (int32_t)(base + wtot);
+  if (wtot) {
+#pragma unroll
+    for (int g = 0; g < kEnumSeg; ++g) {
+      const unsigned incl = warp_incl_scan(c[g]);
+      unsigned long long o = base + incl - c[g];
+      base += __shfl_sync(GNS_FULL, incl, 31);
+      if (c[g]) {
+        const uint32_t x8[8] = {w[g][0].x, w[g][0].y, w[g][0].z, w[g][0].w,
+                                w[g][1].x, w[g][1].y, w[g][1].z, w[g][1].w};
+        const long long wbase = enum_seg0(tile, warp, g) * 32 + 8 * lane;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t x = x8[i];
+          if (x) {
+            const long long wd = wbase + i;
+            rank2[wd] = (o << 32) | (unsigned long long)x;
+            bits[wd] = 0u;
+            uint32_t y = x;
+            while (y) {
+              const int bb = __ffs(y) - 1;
+              y &= y - 1;
+              out[o++] = (int32_t)(wd * 32 + bb);
+            }
+          }
         }
       }
     }
   }
-  if (lane < kEnumPerWarp && sw0 + lane < nsw) sum[sw0 + lane] = 0u;
+  if (lane < kEnumPerWarp * kEnumSeg) {
+    const long long sw = enum_seg0(tile, warp, 0) + lane;
+    if (sw < nsw) sum[sw] = 0u;
+  }
 }
 
 __device__ __forceinline__ int32_t bit_rank(const unsigned long long* __restrict__ rank2, int32_t v) {
