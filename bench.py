@@ -355,7 +355,41 @@ def sampler_throughput(P, tr, g, cfg, n_batches=24):
     # per-edge output (src id, row, fp64 weight, flag = 17 B), relabel:
     # 4 (E + seeds) read + 4 src + 4 E written
     nbytes = 16 * seeds + 17 * edges + 4 * (edges + seeds) + 4 * srcs + 4 * edges
+    # K6 alone: gns_relabel on each layer of the last batch
+    # (mark seeds + sampled ids in the two-level bitmap, enumerate, rank),
+    # CUDA events, 20 launches per layer; recomputes the same src_nodes /
+    # edge_src.  Algorithmic bytes: the summary bitmap (N/256 B) scanned twice
+    # (tile counts, then ranks) with the 16-B bitmap pieces under set summary
+    # bits (<= 16 n_src B, twice) + ids read to mark and to rank (2 x 4 (n +
+    # E)) + rank words read per id (8 (n + E)) + edge_src / self_pos written
+    # (4 (n + E)) + src_nodes and rank words written (12 n_src).  A chain of
+    # four dependent launches: latency-bound, the fraction is low by design
+    k6 = []
+    N = g.num_nodes
+    with torch.cuda.stream(s):
+        for li, lb in enumerate(sl.layers):
+            if li == 0:
+                sd, nsd = sl.seeds0, sl.n_seeds0
+            else:
+                prev = sl.layers[li - 1]
+                sd, nsd = prev.src_nodes, prev.counts[_lib.CNT_SRC:_lib.CNT_SRC + 1]
+            cl = [int(x) for x in lb.counts.tolist()]
+            n_l, e_l, s_l = cl[_lib.CNT_DST], cl[_lib.CNT_EDGES], cl[_lib.CNT_SRC]
+            b = 2 * (N // 256 + 16 * s_l) + 8 * (n_l + e_l) + 8 * (n_l + e_l) + 4 * (n_l + e_l) + 12 * s_l
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for it in range(22):
+                if it == 2:
+                    a0.record(s)
+                _lib.call("gns_relabel", N, sd.data_ptr(), nsd.data_ptr(), lb.max_dst, lb.cblock, lb.max_edges,
+                          sl.ws_relabel.data_ptr(), sl.ws_relabel.numel(), _lib.stream_ptr(s))
+            a1.record(s)
+            a1.synchronize()
+            t_ms = a0.elapsed_time(a1) / 20
+            gbs = b / (t_ms / 1e3) / 1e9
+            k6.append({"layer": lb.layer, "dst": n_l, "edges": e_l, "src": s_l, "us": round(t_ms * 1e3, 1),
+                       "algorithmic_bytes": b, "achieved_gbs": round(gbs, 1), "frac": round(gbs / load_peaks()[0], 4)})
     return {"ms_per_batch": round(ms, 4), "mini_batches_per_s": round(1e3 / ms, 1),
+            "relabel_k6": k6,
             "sampled_edges_per_batch": edges, "sampled_edges_per_s": round(edges / (ms / 1e3), 1),
             "bytes_lower_bound_per_batch": nbytes, "achieved_gbs_lower_bound": round(nbytes / (ms / 1e3) / 1e9, 1),
             "how": f"one sampler chain (gns_batch_slice_sorted + 3 x gns_sample_layer), {n_batches} batches back to "
