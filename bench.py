@@ -412,7 +412,7 @@ def refresh_timing(P, tr, g, reps=3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
-        C.refresh_cache(st, g, probs, cs, 100 + r, [tr.cfg.seed, 33, 100 + r])
+        C.refresh_cache(st, g, probs, cs, 100 + r, [tr.cfg.seed, 33, 100 + r], positions=tr._positions)
         e1.record()
         e1.synchronize()
         if r:
@@ -425,8 +425,9 @@ def refresh_timing(P, tr, g, reps=3):
     return {"ms": round(ms, 3), "algorithmic_bytes": nbytes, "gbs": round(nbytes / (ms / 1e3) / 1e9, 1),
             "cache_size": cs, "cached_csr_nnz": nnz,
             "how": "cache.refresh_cache (gns_cache_draw + gns_inclusion + gns_cached_csr_count/fill) into a spare "
-                   "set, host-synchronised (the engine prefetches it on a low-priority stream during the "
-                   "previous epoch instead)"}
+                   "set exactly as the engine refreshes (cached-CSR positions only for gns-exact), "
+                   "host-synchronised (the engine prefetches it on a low-priority stream during the previous "
+                   "epoch instead)"}
 
 
 def main():
