@@ -530,11 +530,15 @@ def ours_arm(args, name, c, world, rank, local):
     spmm_ms, spmm_bytes, n_in, bwd_ms, bwd_bytes = [], [], [], [], []
     D, H = c["dim"], c["hidden"]
 
+    rep = {}
+
     def on_step(e, i, k):
-        if k % tr.S:          # the events time the first step of each replay
-            return
-        spmm_ms.append(tr.spmm0_ms())
-        bwd_ms.append(tr.bwd1_ms())
+        # the events time every step of a replay; their per-replay means
+        # (read once, at the replay's first step) pair with each step's bytes
+        if k % tr.S == 0:
+            rep["spmm"], rep["bwd"] = tr.spmm0_ms(), tr.bwd1_ms()
+        spmm_ms.append(rep["spmm"])
+        bwd_ms.append(rep["bwd"])
         sl = tr.slots[tr.slot_of(k)]
         cnt = sl.counts[len(FANOUTS) - 1].tolist()
         n_in.append(cnt[_lib.CNT_SRC])
@@ -555,10 +559,11 @@ def ours_arm(args, name, c, world, rank, local):
     g_res = gather_microbench(tr, D)
     spmm_k = kernel_line("gns_spmm_fwd_gather (input layer: feature gather fused with the mean aggregation)",
                          spmm_bytes, spmm_ms, peak, peak_kind,
-                         f"CUDA events around the kernel inside the captured step graph, {len(spmm_ms)} replays",
+                         f"CUDA events around the kernel inside the captured step graph, every step of "
+                         f"{len(spmm_ms) // tr.S} replays",
                          step_ms)
     bwd_k = kernel_line("gns_spmm_bwd_transposed_bits (model layer 1 backward, hidden 256)", bwd_bytes, bwd_ms,
-                        peak, peak_kind, f"CUDA events inside the captured step graph, {len(bwd_ms)} replays",
+                        peak, peak_kind, f"CUDA events inside the captured step graph, every step of {len(bwd_ms) // tr.S} replays",
                         step_ms)
     gather_k = kernel_line("gns_gather_rows (reference-API gather features[input_nodes], gather_f32x4_kernel)",
                            [b for b, _ in g_res], [t for _, t in g_res], peak, peak_kind,

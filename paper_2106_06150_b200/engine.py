@@ -598,33 +598,41 @@ class GraphedTrainer:
     def capture_profiled(self):
         """Re-capture with timing events around the input-feature gather
         (gns_gather_rows), the input-layer SpMM and layer 1's transposed
-        SpMM of the first step of each replay, so their durations can be read
+        SpMM of every step of each replay, so their durations can be read
         after a replay (bench.py's rooflines; not the headline)."""
-        self._prof_events = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-        for e in self._prof_events:      # materialise the driver events
-            e.record(self.main)
+        # one event set per step of a replay (the first step runs beside both
+        # sampling branches, the later ones mostly alone): the readers average
+        self._prof_steps = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(self.S)]
+        for evs in self._prof_steps:     # materialise the driver events
+            for e in evs:
+                e.record(self.main)
+        self._prof_events = self._prof_steps[0]
         torch.cuda.synchronize()
         self._free_execs()
 
+    def _prof_mean(self, a: int, b: int) -> float:
+        """Mean event interval (a -> b) over the steps of the last replay."""
+        steps = getattr(self, "_prof_steps", None) or [self._prof_events]
+        vals = []
+        for e in steps:
+            e[b].synchronize()
+            vals.append(float(e[a].elapsed_time(e[b])))
+        return sum(vals) / len(vals)
+
     def gather_ms(self) -> float:
-        e = self._prof_events
-        e[1].synchronize()
-        return float(e[0].elapsed_time(e[1]))
+        return self._prof_mean(0, 1)
 
     def spmm0_ms(self) -> float:
-        """Duration of the input-layer aggregation SpMM in the last replay."""
-        e = self._prof_events
-        e[3].synchronize()
-        return float(e[2].elapsed_time(e[3]))
+        """Duration of the input-layer aggregation SpMM in the last replay
+        (mean over its steps)."""
+        return self._prof_mean(2, 3)
 
     def bwd1_ms(self) -> float:
         """Duration of model layer 1's transposed SpMM (backward) in the last
         replay (0 for a one-layer model)."""
-        e = self._prof_events
         if self.L < 2:
             return 0.0
-        e[5].synchronize()
-        return float(e[4].elapsed_time(e[5]))
+        return self._prof_mean(4, 5)
 
     # -- capture / replay ---------------------------------------------------------------
     def _group(self, p: int):
@@ -674,8 +682,10 @@ class GraphedTrainer:
                     ev.record(side)
                 joins.append(ev)
             ev_prof, self._prof_events = self._prof_events, None
+            ev_steps = getattr(self, "_prof_steps", None) if ev_prof is not None else None
             for j, sl in enumerate(train):
-                self._prof_events = ev_prof if j == 0 else None
+                self._prof_events = (ev_steps[j] if ev_steps else ev_prof) if ev_prof is not None and \
+                    (ev_steps or j == 0) else None
                 if j > 0:
                     self._gather(sl)
                 # the step's loss straight into its step_loss slot
