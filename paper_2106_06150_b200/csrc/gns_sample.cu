@@ -14,12 +14,14 @@
 // fill phase the cache-bitmap probe and the neighbour-id load happen only for
 // positions whose key is under T, so a hub row costs Philox ALU, not HBM.
 //
-// Rows whose scan length exceeds kHubLen go to a CTA-per-row kernel.
+// Rows whose scan length exceeds kHubLen are taken by whole CTAs at the tail
+// of the warp-tier launch.
 //
-// Dedup/relabel: one bit per node id (N/8 bytes, L2-resident), atomicOr the
-// seeds and sampled neighbours, a single-pass scan over the bitmap words emits
-// the sorted unique src set and per-word ranks, and edge_src = word rank +
-// popc(prefix bits).  The bits are cleared by walking src_nodes.
+// Dedup/relabel: one bit per node id (N/8 bytes) plus a summary bit per
+// bitmap word, set by fire-and-forget atomicOr of the seeds and sampled
+// neighbours; two passes over the summary (tile counts, then ranks) emit the
+// sorted unique src set and per-word ranks and clear both levels as they go,
+// and edge_src = word rank + popc(prefix bits).
 #include <string.h>
 
 #include <algorithm>
