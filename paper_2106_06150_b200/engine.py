@@ -936,8 +936,11 @@ class GraphedTrainer:
             h = self.step_host[slot]
             h[0] = (self.cfg.seed & 0xFFFFFFFF) | ((epoch & 0xFFFFFFFF) << 32)
             h[1] = (base + k) & 0xFFFFFFFF
-        key = ("host", epoch, base, tuple(id(x) for x in batches[:S]), self.cur)
-        if rd is not None and n >= S and rd[:5] == key:
+        # (the arrays themselves are kept in _ready and compared by identity:
+        # holding them keeps their ids from being reused by new arrays)
+        same = (rd is not None and n >= S and rd[:3] == ("host", epoch, base) and rd[4] == self.cur
+                and len(rd[3]) == S and all(a is b for a, b in zip(rd[3], batches[:S])))
+        if same:
             q0 = rd[5]      # sampled ahead by the previous call's last replay
         else:
             q0 = 0
@@ -954,7 +957,7 @@ class GraphedTrainer:
             for j, sl in enumerate(self._group(1 - p)):
                 put(sl, b0 + S + j)
             if b0 + S >= n and len(ahead) == S:
-                self._ready = ("host", epoch, base + n, tuple(id(x) for x in ahead), self.cur, 1 - p)
+                self._ready = ("host", epoch, base + n, tuple(ahead), self.cur, 1 - p)
             with torch.cuda.stream(self.main):
                 self._replay(p, r)
                 ev = torch.cuda.Event()
