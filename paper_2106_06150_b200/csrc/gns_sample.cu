@@ -308,12 +308,15 @@ struct PhaseDesc {
   int64_t out_base;   // first output slot
 };
 
+// (float arithmetic: T only sets how many candidates pass the filter — the
+// exact (key, position) ranking and the bisection retry make the selection
+// independent of it — and fp64 sqrt/division cost ~40 instructions per item)
 __device__ __forceinline__ uint64_t initial_threshold(int take, int cnt) {
   if (take >= cnt) return kTwo53;
-  double mu = (double)take + 4.0 * sqrt((double)take) + 8.0;
-  if (mu >= (double)cnt) return kTwo53;
-  uint64_t t = (uint64_t)(mu / (double)cnt * 9007199254740992.0);
-  return t < 1 ? 1 : t;
+  const float mu = (float)take + 4.f * sqrtf((float)take) + 8.f;
+  if (mu >= (float)cnt) return kTwo53;
+  const uint64_t t = (uint64_t)(__fdividef(mu, (float)cnt) * 9007199254740992.0f);
+  return t < 1 ? 1 : (t > kTwo53 ? kTwo53 : t);
 }
 
 // gns-exact (sampling.py:238-250): w = 1 / q[global CSR position]
