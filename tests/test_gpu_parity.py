@@ -513,7 +513,31 @@ def test_spmm_fwd_f64_bit_exact(P, dim):
             assert np.array_equal(c[:, dim:], OM.spmm_mean_fwd(br, hr))
 
 
-@pytest.mark.parametrize("dim", [4, 64, 128, 200])
+@pytest.mark.parametrize("dim", [200, 768])
+def test_spmm_fwd_gather_wide_rows_long_lists(P, dim):
+    """Wide-row input layer (column-split warp tasks) with rows of > 32 edges
+    (ranked window by window): bit-identical to gather then aggregate."""
+    from paper_2106_06150_b200 import _lib
+    og = _hub_graph(4000, 29)
+    g = P.Graph.from_numpy(og.num_nodes, og.indptr, og.indices)
+    cfg = P.SamplerConfig(strategy="NS", fanouts=(70, 3), batch_size=200, seed=8)
+    targets = np.random.default_rng(8).choice(og.num_nodes, 200, replace=False)
+    mb = P.build_minibatch(g, None, targets, cfg, P.BatchRng(8, 0, 0))
+    feats = torch.randn(og.num_nodes, dim, device="cuda")
+    for bg in mb.blocks:
+        nd = bg.dst_nodes.numel()
+        h = feats[bg.src_nodes.long()].contiguous()
+        a = torch.full((nd + 3, 2 * dim), 7.0, device="cuda")
+        b = torch.full((nd + 3, 2 * dim), 9.0, device="cuda")
+        _lib.call("gns_spmm_fwd", 0, h.data_ptr(), dim, dim, 0, bg._c, nd, nd + 3, a.data_ptr(), 2 * dim,
+                  _lib.stream_ptr())
+        dst = bg.dst_nodes.int().contiguous()
+        _lib.call("gns_spmm_fwd_gather", feats.data_ptr(), dim, dim, bg._c, dst.data_ptr(), nd, nd + 3, 0, 0,
+                  b.data_ptr(), 2 * dim, _lib.stream_ptr())
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dim", [4, 64, 128, 200, 768, 1024])
 def test_spmm_fwd_gather_equals_gather_then_spmm(P, dim):
     """The fused input-layer kernel (feature table addressed by node id) is
     bit-identical to features[input_nodes] (model.py:146) followed by the
