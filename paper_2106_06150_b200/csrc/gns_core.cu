@@ -303,6 +303,9 @@ int gns_graph_instantiate(void* graph, int32_t use_node_priority, void** out_exe
   cudaGraphExec_t ex = nullptr;
   unsigned long long flags = use_node_priority ? cudaGraphInstantiateFlagUseNodePriority : 0;
   GNS_CUDA(cudaGraphInstantiateWithFlags(&ex, (cudaGraph_t)graph, flags));
+  // upload now (the caller synchronises after instantiating): the first
+  // launch — often inside a timed window — then skips the upload
+  GNS_CUDA(cudaGraphUpload(ex, (cudaStream_t)0));
   *out_exec = (void*)ex;
   return GNS_OK;
 }

@@ -146,6 +146,7 @@ class GraphedTrainer:
         self._ready = None
         self._q0 = 0
         self.prologues = 0         # eager first-group samplings (run_epoch calls that could not continue)
+        self._adam_mark = None     # model.step_count the device step count (adam_t[0]) matches after the queued replays
         self.csets = [None, None]
         self._adopted = None       # a caller's CacheState set through `cache` (never written)
         self.cur = 0
@@ -801,10 +802,20 @@ class GraphedTrainer:
         return epoch, first
 
     def _begin(self, epoch: int):
+        # fast path for a call continuing the previous one (same epoch, no
+        # refresh, Adam's device step count already the host's): nothing to
+        # synchronise or enqueue before the first replay
+        if (self.model.step_count == self._adam_mark and not self._needs_refresh(epoch)
+                and (self.epoch_perm is None or self._perm_epoch == epoch)):
+            # (work the caller queued on its current stream still precedes the
+            # replays, without blocking the host)
+            self.main.wait_stream(torch.cuda.current_stream())
+            return
         torch.cuda.synchronize()
         if self._needs_refresh(epoch):
             self._refresh_cache(epoch)
         self.adam_t[0].fill_(self.model.step_count)
+        self._adam_mark = self.model.step_count
         if self.epoch_perm is not None and self._perm_epoch != epoch:
             n = self.train_ids.numel()
             _lib.call("gns_epoch_targets", self.train_ids.data_ptr(), n, self.cfg.seed & 0xFFFFFFFF,
@@ -876,6 +887,7 @@ class GraphedTrainer:
                 else:
                     self._prefetch_poll()
             self.model.step_count += len(grp)
+            self._adam_mark = self.model.step_count
             for j, index in enumerate(grp):
                 self._cur_j = j
                 if on_step is not None:
@@ -965,6 +977,7 @@ class GraphedTrainer:
                 for sl in self._group(1 - p):
                     self.done[sl] = ev
             self.model.step_count += r
+            self._adam_mark = self.model.step_count
             pending.append((ev, lh[p], b0, r))
             if len(pending) > 1:
                 drain()
