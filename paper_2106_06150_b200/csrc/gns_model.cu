@@ -249,6 +249,68 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
     const int64_t cb = (int64_t)(s0 >> 32), ce = (int64_t)(s1 >> 32);
     const int64_t fb = tm + (int64_t)(s0 & 0xffffffffull), fe = tm + (int64_t)(s1 & 0xffffffffull);
     const int nc = (int)(ce - cb), L = nc + (int)(fe - fb);
+    if (L > kRowCap) {
+      // a row longer than the shared stage (full-neighbourhood blocks of
+      // hub rows, not sampled ones): the same ascending-source FMA sequence,
+      // each next source found by a warp arg-min over the row (O(L^2 / 32))
+      const T norm = (T)max(bv.dst_degree[r], 1);
+      const V* hs = reinterpret_cast<const V*>(h + (int64_t)(GATHER ? dst_ids[r] : bv.self_pos[r]) * ld_h);
+      V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
+      const int mw = ((dv + 31) >> 5) * 4;
+      for (int c0 = 0; c0 < dv; c0 += 32) {
+        const int c = c0 + lane;
+        V v;
+        vzero(v);
+        if (c < dv) {
+          v = ldv<V, RELU>(hs + c);
+          crow[c] = v;
+        }
+        if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)bv.self_pos[r] * mw, c0 >> 5, v, c < dv);
+      }
+      for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
+        V acc[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) vzero(acc[j]);
+        int64_t last = -1;
+        for (int t = 0; t < L; ++t) {
+          int32_t best = INT32_MAX;
+          T bw = 0;
+          for (int i = lane; i < L; i += 32) {
+            const int64_t e = i < nc ? cb + i : fb + (i - nc);
+            const int32_t v = eidx[e];
+            if ((int64_t)v > last && v < best) {
+              best = v;
+              bw = (T)bv.edge_weight[e];
+            }
+          }
+          int32_t mn = best;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(GNS_FULL, mn, o));
+          const int win = __ffs(__ballot_sync(GNS_FULL, best == mn)) - 1;
+          const T w0 = __shfl_sync(GNS_FULL, bw, win);
+          last = mn;
+          const V* r0 = reinterpret_cast<const V*>(h + (int64_t)mn * ld_h);
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int c = c0 + lane + 32 * j;
+            V x;
+            vzero(x);
+            if (c < dv) {
+              x = ldv<V, RELU>(r0 + c);
+              vfma<true>(acc[j], w0, x);
+            }
+            if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)mn * mw, (c0 >> 5) + j, x, c < dv);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int c = c0 + lane + 32 * j;
+          if (c < dv) crow[dv + c] = vdiv(acc[j], norm);
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     // load + rank-sort by src index (distinct within a row)
     int32_t my_idx[kRowCap / 32];
     T my_w[kRowCap / 32];

@@ -35,7 +35,7 @@ from . import _lib
 from .graph import Graph
 from .model import GraphSAGE, TrainConfig, init_params_numpy, micro_f1
 from .pool import SamplerPool
-from .sampling import BatchRng, MiniBatch, SamplerConfig, build_minibatch
+from .sampling import LayerBlock, MiniBatch, SamplerConfig
 
 
 @dataclass(eq=False)
@@ -226,15 +226,39 @@ def adam_step(params: ModelParams, grads: ParamGrads, state: AdamState, config: 
               config.eps, state.step, 1.0, _lib.stream_ptr())
 
 
+def full_block(g: Graph) -> LayerBlock:
+    """The whole graph as one block: dst = src = every node, the CSR's edges
+    with weight 1 (what an NS draw with fanout >= max degree keeps: weight
+    deg/take = 1), dst_degree = degree — the reference's full-neighbourhood
+    (A h)/max(deg, 1) aggregation (model.py:168-186).  Built straight from
+    the CSR (no sampler: rows of any degree); edge offsets must fit 32 bits."""
+    n, E = g.num_nodes, g.num_edges
+    if E >= 2 ** 32:
+        raise ValueError("full-batch blocks need < 2^32 edges")
+    dev = g.device
+    ar = torch.arange(n, dtype=torch.int32, device=dev)
+    deg = g.degrees
+    row = torch.repeat_interleave(ar, deg.long()) if E else torch.empty(0, dtype=torch.int32, device=dev)
+    counts = torch.zeros(_lib.CNT_N, dtype=torch.int32, device=dev)
+    counts[_lib.CNT_DST] = n
+    counts[_lib.CNT_SRC] = n
+    counts[_lib.CNT_EDGES] = E
+    # row_scan[r] = (cached prefix << 32) | fill prefix: no cached part here
+    b = LayerBlock(dst_nodes=ar, src_nodes=ar, edge_src=g.indices, edge_dst=row.to(torch.int32),
+                   edge_weight=torch.ones(E, dtype=torch.float64, device=dev),
+                   edge_cached=torch.zeros(E, dtype=torch.uint8, device=dev), dst_degree=deg, fanout=None,
+                   policy="uniform", self_pos=ar, edge_node=g.indices, row_scan=g.indptr.clone(), counts=counts)
+    b._c = _lib.GnsBlock(*(0 if t is None else t.data_ptr() for t in (
+        b.row_scan, b.dst_degree, b.self_pos, None, b.edge_node, b.edge_src, b.edge_dst, b.edge_weight,
+        b.edge_cached, b.src_nodes, b.counts)))
+    return b
+
+
 def full_batch_forward(g: Graph, params: ModelParams, features=None) -> torch.Tensor:
     """model.py:168-186: full-neighbourhood forward over every node (logits
-    for node ids 0..N-1).  NS blocks with fanout = max degree keep every
-    neighbour with weight deg/take = 1, i.e. the reference's dense
-    (A h)/max(deg, 1) aggregation."""
-    deg = g.indptr[1:] - g.indptr[:-1]
-    kmax = max(int(deg.max()) if g.num_nodes else 1, 1)
-    cfg = SamplerConfig(strategy="NS", fanouts=(kmax,) * params.num_layers, batch_size=max(g.num_nodes, 1))
-    mb = build_minibatch(g, None, np.arange(g.num_nodes), cfg, BatchRng())
+    for node ids 0..N-1), every layer over the whole-graph block."""
+    blk = full_block(g)
+    mb = MiniBatch(blocks=(blk,) * params.num_layers, targets=blk.dst_nodes, input_nodes=blk.src_nodes)
     return forward(mb, g if features is None else features, params)
 
 

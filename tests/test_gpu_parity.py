@@ -1804,3 +1804,32 @@ def test_softmax_xent_bias_fused_equals_separate(P, dtype, C):
         lp = torch.log_softmax(logits[:n].double(), 1)
         want = -lp[torch.arange(n), labels[targets[:n].long()].long()].mean()
         assert abs(float(l2) - float(want)) <= (1e-5 if dtype == torch.float32 else 1e-12) * max(1.0, abs(float(want)))
+
+
+def test_full_batch_forward_rows_of_any_degree(P):
+    """evaluate()'s full-neighbourhood forward (model.py:168-186) is built
+    from the CSR directly, so rows with more neighbours than the sampler's
+    fanout limit (128) work: float64 logits equal (A h)/max(deg, 1) layer by
+    layer (scipy order) on a graph with a 2000-neighbour hub."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(5)
+    n = 3000
+    e = np.concatenate([np.stack([np.zeros(2000, dtype=np.int64), rng.choice(np.arange(1, n), 2000, replace=False)], 1),
+                        rng.integers(0, n, size=(6000, 2))])
+    og = O.build_csr(e, n)
+    assert np.diff(og.indptr).max() > 128
+    feats = rng.normal(size=(n, 8)).astype(np.float32)
+    labels = rng.integers(0, 4, n).astype(np.int32)
+    g = P.Graph.from_numpy(n, og.indptr, og.indices, features=feats, labels=labels)
+    params = P.init_params((8, 16, 4), seed=0, dtype=torch.float64)
+    from paper_2106_06150_b200.train import full_batch_forward
+    logits = full_batch_forward(g, params).cpu().numpy()
+    w, b = params.model.export()
+    h = feats.astype(np.float64)
+    norm = np.maximum(np.diff(og.indptr), 1).astype(np.float64)
+    adj = sp.csr_matrix((np.ones(og.num_edges), og.indices, og.indptr), shape=(n, n))
+    for li in range(2):
+        agg = (adj @ h) / norm[:, None]
+        z = np.concatenate([h, agg], 1) @ w[li] + b[li]
+        h = np.maximum(z, 0) if li == 0 else z
+    np.testing.assert_allclose(logits, h, rtol=1e-10, atol=1e-10)
