@@ -432,6 +432,33 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
   }
 }
 
+// The next source index after `last` in a row (the row's edges in cached
+// then fill segments; indices distinct within a row) and its weight: a warp
+// arg-min over the row, O(L / 32) per lane — rows longer than the fast
+// paths' 32-edge windows are walked in ascending-source order in O(L^2 / 32)
+// (the rank-by-count loops these replace were O(L^3 / 32)).  Every lane calls
+// it; all lanes get the result (INT32_MAX past the end).
+__device__ __forceinline__ void next_src(const int32_t* __restrict__ eidx, const double* __restrict__ ew, int64_t cb,
+                                         int nc, int64_t fb, int L, int lane, int64_t last, int32_t& v_out,
+                                         float& w_out) {
+  int32_t best = INT32_MAX;
+  float bw = 0.f;
+  for (int i = lane; i < L; i += 32) {
+    const int64_t e = i < nc ? cb + i : fb + (i - nc);
+    const int32_t v = eidx[e];
+    if ((int64_t)v > last && v < best) {
+      best = v;
+      bw = (float)ew[e];
+    }
+  }
+  int32_t mn = best;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(GNS_FULL, mn, o));
+  const int win = __ffs(__ballot_sync(GNS_FULL, best == mn)) - 1;
+  v_out = mn;
+  w_out = __shfl_sync(GNS_FULL, bw, win);
+}
+
 // Narrow rows (float32, D <= 128: one 16-byte chunk per lane) with <= 32
 // edges per dst row — the input layer.  Per warp and dst row: lane i loads
 // edge i, the ranks by source index come from a shuffle count (no shared
@@ -511,29 +538,13 @@ __global__ void __launch_bounds__(kSpmmBlock, kMinBlocks) spmm_fwd_narrow_kernel
         }
       }
     } else {
-      // > 32 edges: sort through shared memory in 32-edge rounds is not
-      // worth a second path — rank each edge against all others directly
+      // > 32 edges (full-neighbourhood hub rows): the ascending walk
+      int64_t last = -1;
       for (int t = 0; t < L; ++t) {
-        // the t-th smallest source index among the row's edges
-        int32_t best = INT32_MAX;
-        float bw = 0.f;
-        for (int i = lane; i < L; i += 32) {
-          const int64_t e = i < nc ? cb + i : fb + (i - nc);
-          const int32_t v = eidx[e];
-          int rk = 0;
-          for (int j = 0; j < L; ++j) {
-            const int64_t ej = j < nc ? cb + j : fb + (j - nc);
-            rk += eidx[ej] < v;
-          }
-          if (rk == t) {
-            best = v;
-            bw = (float)bv.edge_weight[e];
-          }
-        }
-        const unsigned m = __ballot_sync(GNS_FULL, best != INT32_MAX);
-        const int sl = __ffs(m) - 1;
-        const int32_t iu = __shfl_sync(GNS_FULL, best, sl);
-        const float wu = __shfl_sync(GNS_FULL, bw, sl);
+        int32_t iu;
+        float wu;
+        next_src(eidx, bv.edge_weight, cb, nc, fb, L, lane, last, iu, wu);
+        last = iu;
         if (on) vfma<true>(acc, wu, ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)iu * ld_h) + lane));
       }
     }
@@ -593,31 +604,17 @@ __device__ __forceinline__ void sort_pairs(int32_t (&k)[MAXL], float (&v)[MAXL])
   }
 }
 
-// one dst row through the per-row (rank-by-count) path; every lane calls it
+// one dst row through the per-row (ascending walk) path; every lane calls it
 template <bool RELU>
 __device__ __noinline__ void narrow_row_slow(const float* __restrict__ h, int64_t ld_h, const int32_t* __restrict__ eidx,
                                                 const double* __restrict__ ew, int64_t cb, int nc, int64_t fb, int L,
                                                 int lane, bool on, float4& acc) {
+  int64_t last = -1;
   for (int t = 0; t < L; ++t) {
-    int32_t best = INT32_MAX;
-    float bw = 0.f;
-    for (int i = lane; i < L; i += 32) {
-      const int64_t e = i < nc ? cb + i : fb + (i - nc);
-      const int32_t v = eidx[e];
-      int rk = 0;
-      for (int j = 0; j < L; ++j) {
-        const int64_t ej = j < nc ? cb + j : fb + (j - nc);
-        rk += eidx[ej] < v;
-      }
-      if (rk == t) {
-        best = v;
-        bw = (float)ew[e];
-      }
-    }
-    const unsigned m = __ballot_sync(GNS_FULL, best != INT32_MAX);
-    const int sl = __ffs(m) - 1;
-    const int32_t iu = __shfl_sync(GNS_FULL, best, sl);
-    const float wu = __shfl_sync(GNS_FULL, bw, sl);
+    int32_t iu;
+    float wu;
+    next_src(eidx, ew, cb, nc, fb, L, lane, last, iu, wu);
+    last = iu;
     if (on) vfma<true>(acc, wu, ldv<float4, RELU>(reinterpret_cast<const float4*>(h + (int64_t)iu * ld_h) + lane));
   }
 }
@@ -819,9 +816,10 @@ __global__ void __launch_bounds__(kSpmmBlock, 3) spmm_fwd_wide_kernel(const floa
       for (int j = 0; j < CH; ++j) put_relu_bits(relu_bits + self * mw, j, xs[j], lane + 32 * j < dv);
     }
     float4* crow = reinterpret_cast<float4*>(cat + r * ld_cat);
+    int64_t last = -1;   // long rows: the walk's position
     for (int t0 = 0; t0 < L; t0 += 32) {
       // edges t0..t0+31 of the row in ascending source order: with L <= 32
-      // one round; longer rows rank each 32-edge window against all edges
+      // one round; longer rows take each 32-edge window from the ascending walk
       const int m = min(32, L - t0);
       int32_t idx = INT32_MAX;
       float w = 0.f;
@@ -841,19 +839,15 @@ __global__ void __launch_bounds__(kSpmmBlock, 3) spmm_fwd_wide_kernel(const floa
         idx = __shfl_sync(GNS_FULL, idx, src);
         w = __shfl_sync(GNS_FULL, w, src);
       } else {
-        // lane u < m finds the edge of rank t0 + u (distinct sources)
-        for (int i = 0; i < L; ++i) {
-          const int64_t e = i < nc ? cb + i : fb + (i - nc);
-          const int32_t v = bv.edge_src[e];
-          int rk = 0;
-          for (int j = lane; j < L; j += 32) {
-            const int64_t ej = j < nc ? cb + j : fb + (j - nc);
-            rk += bv.edge_src[ej] < v;
-          }
-          rk = warp_sum((unsigned)rk);
-          if (lane < m && rk == t0 + lane) {
+        // lane u < m takes the (t0 + u)-th source of the ascending walk
+        for (int u = 0; u < m; ++u) {
+          int32_t v;
+          float wv;
+          next_src(bv.edge_src, bv.edge_weight, cb, nc, fb, L, lane, last, v, wv);
+          last = v;
+          if (lane == u) {
             idx = v;
-            w = (float)bv.edge_weight[e];
+            w = wv;
           }
         }
       }
@@ -932,6 +926,7 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_fwd_wide_split_kernel(c
     float4 xs = make_float4(0.f, 0.f, 0.f, 0.f), acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (on) xs = vrelu(reinterpret_cast<const float4*>(h + self * ld_h)[c]);
     if constexpr (MASK) put_relu_bits(relu_bits + self * mw, j, xs, on);
+    int64_t last = -1;   // long rows: the walk's position
     for (int t0 = 0; t0 < L; t0 += 32) {
       const int m = min(32, L - t0);
       int32_t idx = INT32_MAX;
@@ -952,18 +947,15 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_fwd_wide_split_kernel(c
         idx = __shfl_sync(GNS_FULL, idx, src);
         w = __shfl_sync(GNS_FULL, w, src);
       } else {
-        for (int i = 0; i < L; ++i) {
-          const int64_t e = i < nc ? cb + i : fb + (i - nc);
-          const int32_t v = bv.edge_src[e];
-          int rk = 0;
-          for (int q = lane; q < L; q += 32) {
-            const int64_t eq = q < nc ? cb + q : fb + (q - nc);
-            rk += bv.edge_src[eq] < v;
-          }
-          rk = warp_sum((unsigned)rk);
-          if (lane < m && rk == t0 + lane) {
+        // lane u < m takes the (t0 + u)-th source of the ascending walk
+        for (int u = 0; u < m; ++u) {
+          int32_t v;
+          float wv;
+          next_src(bv.edge_src, bv.edge_weight, cb, nc, fb, L, lane, last, v, wv);
+          last = v;
+          if (lane == u) {
             idx = v;
-            w = (float)bv.edge_weight[e];
+            w = wv;
           }
         }
       }

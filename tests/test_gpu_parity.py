@@ -1833,3 +1833,62 @@ def test_full_batch_forward_rows_of_any_degree(P):
         z = np.concatenate([h, agg], 1) @ w[li] + b[li]
         h = np.maximum(z, 0) if li == 0 else z
     np.testing.assert_allclose(logits, h, rtol=1e-10, atol=1e-10)
+
+
+def _fp32_row_mean(indptr, indices, x):
+    """float32 (sum over a row's sources in ascending order) / max(deg, 1):
+    the kernels' FMA sequence with weight 1 (fma(1, x, acc) = x + acc, one
+    float32 rounding per add, as numpy's float32 add)."""
+    n = len(indptr) - 1
+    deg = np.diff(indptr)
+    row = np.repeat(np.arange(n), deg)
+    srt = indices[np.lexsort((indices, row))]
+    acc = np.zeros((n, x.shape[1]), np.float32)
+    for t in range(int(deg.max(initial=0))):
+        rows = np.nonzero(deg > t)[0]
+        acc[rows] = acc[rows] + x[srt[indptr[rows] + t]]
+    return acc / np.maximum(deg, 1).astype(np.float32)[:, None]
+
+
+@pytest.mark.parametrize("dim", [8, 64, 128, 256, 768])
+def test_spmm_fwd_full_block_long_rows_float32(P, dim):
+    """float32 aggregation over the whole-graph block (evaluate()'s
+    full-neighbourhood forward, model.py:168-186) with rows of 32, 33, 129
+    and 2000 edges: every fp32 path (plain, relu input, relu' bits, fused
+    gather) walks rows longer than a 32-edge window in ascending source order
+    and is bit-identical to the sequential float32 sum."""
+    from paper_2106_06150_b200 import _lib
+    from paper_2106_06150_b200.train import full_block
+    rng = np.random.default_rng(dim)
+    n = 3000
+    parts = [rng.integers(0, n, size=(6000, 2))]
+    for hub, d in ((0, 2000), (1, 129), (2, 33), (3, 32)):
+        nb = rng.choice(np.arange(4, n), d, replace=False)
+        parts.append(np.stack([np.full(d, hub), nb], 1))
+    og = O.build_csr(np.concatenate(parts), n)
+    deg = np.diff(og.indptr)
+    assert deg[0] >= 2000 and deg[1] >= 129
+    g = P.Graph.from_numpy(n, og.indptr, og.indices)
+    blk = full_block(g)
+    feats = rng.normal(size=(n, dim)).astype(np.float32)
+    h = torch.as_tensor(feats, device="cuda")
+    for relu in (0, 1):
+        x = np.maximum(feats, 0) if relu else feats
+        want = np.concatenate([x, _fp32_row_mean(og.indptr, og.indices, x)], 1)
+        out = torch.full((n + 3, 2 * dim), 7.0, device="cuda")
+        _lib.call("gns_spmm_fwd", 0, h.data_ptr(), dim, dim, relu, blk._c, n, n, out.data_ptr(), 2 * dim,
+                  _lib.stream_ptr())
+        assert np.array_equal(out[:n].cpu().numpy(), want), relu
+        if relu:
+            lib = _lib.lib()
+            bits = torch.zeros(lib.gns_relu_bits_size(n, dim) // 4, dtype=torch.int32, device="cuda")
+            o2 = torch.full((n, 2 * dim), 7.0, device="cuda")
+            _lib.call("gns_spmm_fwd_bits", h.data_ptr(), dim, dim, blk._c, n, n, o2.data_ptr(), 2 * dim,
+                      bits.data_ptr(), _lib.stream_ptr())
+            assert torch.equal(o2, out[:n])
+        else:
+            o3 = torch.full((n, 2 * dim), 9.0, device="cuda")
+            ids = torch.arange(n, dtype=torch.int32, device="cuda")
+            _lib.call("gns_spmm_fwd_gather", h.data_ptr(), dim, dim, blk._c, ids.data_ptr(), n, n, 0, 0,
+                      o3.data_ptr(), 2 * dim, _lib.stream_ptr())
+            assert torch.equal(o3, out[:n])
