@@ -42,9 +42,11 @@ L2_BYTES = 126 << 20
 
 CONFIGS = {
     # name: nodes, undirected pairs drawn, feature dim, classes, train fraction, hidden, cache frac, alpha, offset
-    "cfg1": dict(label="synthetic power-law 100K nodes / 2M directed edges, 64-d (BASELINE configs[0])",
-                 nodes=100_000, pairs=1_000_000, dim=64, classes=16, train=0.5, hidden=64, cache=0.01,
-                 alpha=0.6, offset=10.0, cpu_batches=12),
+    # cfg1 is the reference's own graph: generate_powerlaw(100000, 10, 0)
+    # (graph.py:172-205, preferential attachment, 1,999,800 directed entries)
+    "cfg1": dict(label="reference generate_powerlaw(100000, 10, seed 0): 100K nodes / 2M directed edges, 64-d "
+                       "(BASELINE configs[0])",
+                 nodes=100_000, attach=10, dim=64, classes=16, train=0.5, hidden=64, cache=0.01, cpu_batches=12),
     "products": dict(label="ogbn-products-shaped synthetic: 2.4M nodes, ~124M directed edges, 100-d",
                      nodes=2_400_000, pairs=62_000_000, dim=100, classes=47, train=0.10, hidden=256,
                      cache=0.01, alpha=0.6, offset=30.0, cpu_batches=6),
@@ -157,8 +159,17 @@ def host_reference_inputs(c, seed=0, threads=None):
     cache mask, cache.py:185-197)."""
     from oracle import detmath, gen, gns as O
     t0 = time.perf_counter()
-    og = gen.powerlaw_graph(c["nodes"], c["pairs"], c["alpha"], c["offset"], seed, feature_dim=c["dim"],
-                            num_classes=c["classes"], train_frac=c["train"], threads=threads)
+    if "attach" in c:
+        # the reference's generator restated (oracle.gns, graph.py:172-205) +
+        # the device attribute generator's host restatement (oracle/gen.cc)
+        top = O.generate_powerlaw(c["nodes"], c["attach"], seed)
+        labels, tr, va, te = gen.node_attrs(c["nodes"], c["classes"], c["train"], seed, threads)
+        og = O.OGraph(num_nodes=top.num_nodes, indptr=top.indptr, indices=top.indices.astype(np.int32),
+                      features=gen.features(c["nodes"], c["dim"], c["classes"], labels, 3.0, seed, threads),
+                      labels=labels, train_mask=tr, val_mask=va, test_mask=te)
+    else:
+        og = gen.powerlaw_graph(c["nodes"], c["pairs"], c["alpha"], c["offset"], seed, feature_dim=c["dim"],
+                                num_classes=c["classes"], train_frac=c["train"], threads=threads)
     t1 = time.perf_counter()
     w = O.degree_probs(og)
     cs = O.cache_size_for(og, c["cache"])
@@ -207,8 +218,12 @@ def reference_arm(args, name, c, world, rank):
 def make_graph(P, c, seed=0):
     import torch
     t0 = time.perf_counter()
-    g = P.generate_powerlaw_device(c["nodes"], c["pairs"], alpha=c["alpha"], offset=c["offset"], seed=seed,
-                                   feature_dim=c["dim"], num_classes=c["classes"], train_frac=c["train"])
+    if "attach" in c:
+        g = P.generate_powerlaw(c["nodes"], c["attach"], seed, feature_dim=c["dim"], num_classes=c["classes"],
+                                train_frac=c["train"])
+    else:
+        g = P.generate_powerlaw_device(c["nodes"], c["pairs"], alpha=c["alpha"], offset=c["offset"], seed=seed,
+                                       feature_dim=c["dim"], num_classes=c["classes"], train_frac=c["train"])
     torch.cuda.synchronize()
     return g, time.perf_counter() - t0
 

@@ -61,6 +61,7 @@ extern "C" {
 #define GNS_CNT_WARPROWS 6 /* (row, phase) items for the warp-per-item sampler  */
 #define GNS_CNT_THREADROWS 7 /* (row, phase) items for the thread-per-item sorting-network sampler */
 #define GNS_CNT_STREAMROWS 8 /* (row, phase) items for the thread-per-item streaming top-k sampler */
+#define GNS_CNT_TSEGS 9    /* segments of the transpose's long rows (gns_block_transpose) */
 #define GNS_CNT_N 16
 
 /* CSR graph (graph.py:52-104): indptr int64[N+1], indices int32[E]. */

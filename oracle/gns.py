@@ -82,6 +82,44 @@ def build_csr(edge_list, num_nodes: int) -> OGraph:
     return OGraph(num_nodes=num_nodes, indptr=indptr, indices=dst)
 
 
+def powerlaw_attach_edges(n: int, attach: int, seed: int) -> np.ndarray:
+    """graph.py:172-205 (the preferential-attachment generator) as an
+    ``(n - attach) * attach`` x 2 edge list: node s >= attach links to the
+    previous node's ``attach`` distinct picks, each pick a uniform draw from
+    the endpoint multiset so far (degree-proportional).  Same numpy stream:
+    the first ``attach`` draws of a node as one ``integers(k, size=attach)``
+    call (a batch consumes the generator exactly as that many scalar calls),
+    further draws one at a time while duplicates leave the set short, and
+    the picks in Python-set iteration order of the same insertions."""
+    if attach < 1:
+        raise ValueError("attach must be >= 1")
+    if n <= attach:
+        raise ValueError(f"need n > attach, got n={n}, attach={attach}")
+    rng = np.random.default_rng(seed)
+    m = attach
+    ends = np.empty(2 * (n - m) * m, dtype=np.int64)
+    dst = np.empty((n - m) * m, dtype=np.int64)
+    cur = np.arange(m, dtype=np.int64)
+    k = 0
+    for s in range(m, n):
+        dst[(s - m) * m:(s - m + 1) * m] = cur
+        ends[k:k + m] = cur
+        ends[k + m:k + 2 * m] = s
+        k += 2 * m
+        picks = set()
+        for v in ends[rng.integers(k, size=m)].tolist():
+            picks.add(v)
+        while len(picks) < m:
+            picks.add(int(ends[rng.integers(k)]))
+        cur = np.fromiter(picks, dtype=np.int64, count=m)
+    return np.stack([np.repeat(np.arange(m, n, dtype=np.int64), m), dst], 1)
+
+
+def generate_powerlaw(n: int, attach: int, seed: int) -> OGraph:
+    """graph.py:172-205: the preferential-attachment graph's CSR."""
+    return build_csr(powerlaw_attach_edges(n, attach, seed), n)
+
+
 def gather_rows(indptr, indices, rows):
     """graph.py:399-415."""
     rows = np.asarray(rows, dtype=np.int64)

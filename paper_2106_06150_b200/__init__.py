@@ -12,7 +12,7 @@ from .cache import (CacheState, ProbVector, build_cache, degree_probs, inclusion
                     random_walk_probs, sample_cache)
 from .formats import (build_csr, load_binary, load_edgelist, load_feature_csv, save_binary,
                       validate_graph)
-from .graph import Graph, NodeSet, generate_powerlaw_device
+from .graph import Graph, NodeSet, generate_powerlaw, generate_powerlaw_device
 from .model import GraphSAGE, TrainConfig, init_params_numpy, micro_f1
 from .pool import BatchItem, SamplerPool, epoch_targets
 from .train import (AdamState, EpochStats, ModelParams, ParamGrads, TrainReport, adam_step, backward, evaluate,

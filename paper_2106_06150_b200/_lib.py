@@ -14,7 +14,8 @@ from ctypes import POINTER, Structure, c_double, c_int32, c_int64, c_size_t, c_u
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgns.so")
+# GNS_LIB: load another build of the same ABI (A/B measurements of kernel changes)
+LIB_PATH = os.environ.get("GNS_LIB") or os.path.join(_HERE, "libgns.so")
 
 GNS_OK = 0
 GNS_EINVAL = 1
@@ -27,7 +28,7 @@ ERRBIT_CAPACITY = 2
 ERRBIT_ZEROQ = 4
 
 CNT_DST, CNT_EDGES, CNT_CACHED, CNT_SRC, CNT_HUBS, CNT_ERR, CNT_N = 0, 1, 2, 3, 4, 5, 16
-CNT_WARPROWS, CNT_THREADROWS, CNT_STREAMROWS = 6, 7, 8
+CNT_WARPROWS, CNT_THREADROWS, CNT_STREAMROWS, CNT_TSEGS = 6, 7, 8, 9
 
 
 class GraphFormatError(ValueError):

@@ -1049,30 +1049,100 @@ __global__ void tscatter_kernel(BlockView bv, int32_t* __restrict__ cursor, cons
   }
 }
 
-// sort each transposed row by dst (ascending): registers for <= 32 entries,
-// an all-ascending bitonic network in place otherwise
-// Also writes twn[t] = w_e / max(deg(dst_e), 1) in float32 for every sorted
-// entry — the float32 backward's per-edge coefficient, computed exactly as
-// that kernel would (IEEE division), so it reads one value instead of the
-// dependent weight + dst-degree loads.
-__device__ __forceinline__ void put_twn(BlockView bv, const uint64_t* a, int L, float* twn, int lane) {
-  for (int t = lane; t < L; t += 32) {
-    const uint64_t key = a[t];
-    const int32_t d = (int32_t)(key >> 32), e = (int32_t)(key & 0xffffffffu);
-    twn[t] = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
+// Long transposed rows.  A sampled block's source rows have ~1 item, but a
+// hub source can be the neighbour of thousands of dst rows (the reference's
+// generate_powerlaw graph, real graphs): a warp per row then serialises the
+// whole row.  Rows of more than kBwdLong items are split into kBwdSeg-item
+// segments: tsort registers them (segment -> row map, per-row segment base),
+// every warp of the float32 backward first computes unclaimed segments'
+// partial sums (sequential FMAs in ascending dst order, from 0), and the
+// warp that owns the row adds the partials in segment order — computing any
+// segment nobody has claimed yet itself, so no warp waits on a CTA that is
+// not running.  Claims and completion flags carry a generation number that
+// the last CTA of each backward launch advances, so repeated launches over
+// the same transpose need no reset.  Rows of more than kTsortWarpMax items
+// are sorted by whole CTAs in shared memory (tsort_long_kernel).
+#ifndef GNS_BWD_LONG
+#define GNS_BWD_LONG 1   // (0: builds without the long-row path, for A/B)
+#endif
+constexpr int kBwdLong = 64, kBwdSeg = 32, kTsortWarpMax = 256;
+enum { kCtrSegs = 0, kCtrSort = 1, kCtrGen = 2, kCtrTicket = 3, kCtrLong = 4, kCtrN = 8 };
+
+struct LongRows {
+  int32_t* ctr;             // kCtrN counters (zeroed with the transpose counts)
+  int32_t* sbase;           // per source row: first segment (long rows only)
+  int32_t* seg_row;         // per segment: its source row
+  int32_t* claim;           // per segment: generation that claimed it
+  int32_t* done;            // per segment: generation whose partial is stored
+  float4* part;             // per segment: partial sum row (dim / 4 float4)
+  int32_t* slist;           // rows sorted by tsort_long_kernel
+  int32_t* llist;           // rows of more than kBwdLong items
+};
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ascending sort of a[0, L) in place: the all-ascending bitonic network
+// (flip, then half-cleaners) with out-of-range partners skipped, so L need
+// not be a power of two.  Threads tid = 0..nt-1 of the group call it; sync()
+// is the group's barrier (warp or CTA; shared or global memory).
+template <typename Sync>
+__device__ __forceinline__ void bitonic_asc(uint64_t* a, int L, int tid, int nt, Sync sync) {
+  int P = 1;
+  while (P < L) P <<= 1;
+  for (int k = 2; k <= P; k <<= 1) {
+    const int half = k >> 1;
+    for (int t = tid; t < P / 2; t += nt) {
+      const int i = (t & (half - 1)) | ((t & ~(half - 1)) << 1), jj = i ^ (k - 1);
+      if (jj < L && a[jj] < a[i]) { const uint64_t x = a[i]; a[i] = a[jj]; a[jj] = x; }
+    }
+    sync();
+    for (int st = k >> 2; st >= 1; st >>= 1) {
+      for (int t = tid; t < P / 2; t += nt) {
+        const int i = (t & (st - 1)) | ((t & ~(st - 1)) << 1), jj = i + st;
+        if (jj < L && a[jj] < a[i]) { const uint64_t x = a[i]; a[i] = a[jj]; a[jj] = x; }
+      }
+      sync();
+    }
   }
 }
 
+struct WarpBar {
+  __device__ void operator()() const { __syncwarp(); }
+};
+struct CtaBar {
+  __device__ void operator()() const { __syncthreads(); }
+};
+
+__device__ __forceinline__ float twn_of(BlockView bv, uint64_t key) {
+  const int32_t d = (int32_t)(key >> 32), e = (int32_t)(key & 0xffffffffu);
+  return (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
+}
+
 // Per transposed row: sort its (dst << 32 | edge) keys ascending and write
-// the coefficients twn.  A warp takes 32 consecutive rows; rows of <= 8
+// the coefficients twn[t] = w_e / max(deg(dst_e), 1) in float32 — the
+// float32 backward's per-edge coefficient, computed exactly as that kernel
+// would (IEEE division), so it reads one value instead of the dependent
+// weight + dst-degree loads.  A warp takes 32 consecutive rows; rows of <= 8
 // entries (nearly all: a sampled block's source rows have ~1 edge) are sorted
-// by their own lane in registers, longer rows by the whole warp (rank by
-// shuffles up to 32 entries, a bitonic network in place beyond).  Keys are
-// unique, so every path gives the same order.
+// by their own lane in registers, rows of <= 32 by the warp (shuffle ranks),
+// rows of <= kTsortWarpMax by the warp in its shared-memory slice (bitonic),
+// longer ones are listed for tsort_long_kernel.  Rows of more than kBwdLong
+// entries are registered as segments for the backward.  Keys are unique, so
+// every path gives the same order.
 constexpr int kTsortLane = 8;
-__global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uint64_t* __restrict__ tkeys,
-                             float* __restrict__ twn) {
+__global__ void __launch_bounds__(256) tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr,
+                                                    uint64_t* __restrict__ tkeys, float* __restrict__ twn,
+                                                    LongRows lr) {
+  __shared__ uint64_t slice[256 / 32][kTsortWarpMax];
   const int lane = threadIdx.x & 31;
+  uint64_t* sa = slice[threadIdx.x >> 5];
   const int64_t n = bv.counts[GNS_CNT_SRC];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1083,6 +1153,18 @@ __global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uin
       b = tptr[s];
       L = tptr[s + 1] - b;
     }
+    if (L > kBwdLong) {   // register the row's backward segments
+      const int nseg = (L + kBwdSeg - 1) / kBwdSeg;
+      const int base = atomicAdd(lr.ctr + kCtrSegs, nseg);
+      lr.sbase[s] = base;
+      lr.llist[atomicAdd(lr.ctr + kCtrLong, 1)] = (int32_t)s;
+      for (int j = 0; j < nseg; ++j) {
+        lr.seg_row[base + j] = (int32_t)s;
+        lr.claim[base + j] = 0;
+        lr.done[base + j] = 0;
+      }
+    }
+    if (L > kTsortWarpMax) lr.slist[atomicAdd(lr.ctr + kCtrSort, 1)] = (int32_t)s;
     if (L > 0 && L <= kTsortLane) {
       uint64_t x[kTsortLane];
 #pragma unroll
@@ -1097,13 +1179,7 @@ __global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uin
         }
       float wv[kTsortLane];
 #pragma unroll
-      for (int i = 0; i < kTsortLane; ++i) {
-        wv[i] = 0.f;
-        if (i < L) {
-          const int32_t d = (int32_t)(x[i] >> 32), e = (int32_t)(x[i] & 0xffffffffu);
-          wv[i] = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
-        }
-      }
+      for (int i = 0; i < kTsortLane; ++i) wv[i] = i < L ? twn_of(bv, x[i]) : 0.f;
 #pragma unroll
       for (int i = 0; i < kTsortLane; ++i)
         if (i < L) {
@@ -1111,7 +1187,7 @@ __global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uin
           twn[b + i] = wv[i];
         }
     }
-    for (unsigned big = __ballot_sync(GNS_FULL, L > kTsortLane); big; big &= big - 1) {
+    for (unsigned big = __ballot_sync(GNS_FULL, L > kTsortLane && L <= kTsortWarpMax); big; big &= big - 1) {
       const int j = __ffs(big) - 1;
       const int bj = __shfl_sync(GNS_FULL, b, j), Lj = __shfl_sync(GNS_FULL, L, j);
       uint64_t* a = tkeys + bj;
@@ -1122,33 +1198,253 @@ __global__ void tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr, uin
         __syncwarp();
         if (lane < Lj) {
           a[rank] = x;
-          const int32_t d = (int32_t)(x >> 32), e = (int32_t)(x & 0xffffffffu);
-          twn[bj + rank] = (float)bv.edge_weight[e] / (float)max(bv.dst_degree[d], 1);
+          twn[bj + rank] = twn_of(bv, x);
         }
         __syncwarp();
         continue;
       }
-      int P = 1;
-      while (P < Lj) P <<= 1;
-      for (int k = 2; k <= P; k <<= 1) {
-        for (int t = lane; t < P / 2; t += 32) {
-          int half = k >> 1;
-          int i = (t / half) * k + (t % half);
-          int jj = i ^ (k - 1);
-          if (jj < Lj && a[jj] < a[i]) { uint64_t x = a[i]; a[i] = a[jj]; a[jj] = x; }
-        }
-        __syncwarp();
-        for (int st = k >> 2; st >= 1; st >>= 1) {
-          for (int t = lane; t < P / 2; t += 32) {
-            int i = (t / st) * 2 * st + (t % st);
-            int jj = i + st;
-            if (jj < Lj && a[jj] < a[i]) { uint64_t x = a[i]; a[i] = a[jj]; a[jj] = x; }
-          }
-          __syncwarp();
+      for (int t = lane; t < Lj; t += 32) sa[t] = a[t];
+      __syncwarp();
+      bitonic_asc(sa, Lj, lane, 32, WarpBar());
+      for (int t = lane; t < Lj; t += 32) {
+        a[t] = sa[t];
+        twn[bj + t] = twn_of(bv, sa[t]);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Rows of more than kTsortWarpMax entries (listed by tsort_kernel): a CTA per
+// row, bitonic in dynamic shared memory (kTsortLongKeys keys), in place in
+// global memory beyond that.
+constexpr int kTsortLongThreads = 512, kTsortLongKeys = 8192, kTsortLongGrid = 32;
+__global__ void __launch_bounds__(kTsortLongThreads) tsort_long_kernel(BlockView bv, const int32_t* __restrict__ tptr,
+                                                                       uint64_t* __restrict__ tkeys,
+                                                                       float* __restrict__ twn, LongRows lr) {
+  extern __shared__ uint64_t skeys[];
+  // the segment count where the backward finds it with the block's sizes
+  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<int32_t*>(bv.counts)[GNS_CNT_TSEGS] = lr.ctr[kCtrSegs];
+  const int nlong = lr.ctr[kCtrSort];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = blockIdx.x; k < nlong; k += gridDim.x) {
+    const int32_t s = lr.slist[k];
+    const int b = tptr[s], L = tptr[s + 1] - b;
+    uint64_t* a = tkeys + b;
+    if (L <= kTsortLongKeys) {
+      for (int t = tid; t < L; t += nt) skeys[t] = a[t];
+      __syncthreads();
+      bitonic_asc(skeys, L, tid, nt, CtaBar());
+      for (int t = tid; t < L; t += nt) {
+        a[t] = skeys[t];
+        twn[b + t] = twn_of(bv, skeys[t]);
+      }
+    } else {
+      bitonic_asc(a, L, tid, nt, CtaBar());
+      for (int t = tid; t < L; t += nt) twn[b + t] = twn_of(bv, a[t]);
+    }
+    __syncthreads();
+  }
+}
+
+// Items [t0, t1) of a transposed row (ascending dst) accumulated into acc:
+// acc = fma(w_t, dcat_nbr[d_t], acc) in item order — the per-row FMA order of
+// every float32 backward path.  32 items' keys and coefficients are loaded
+// at once (one per lane), then G neighbour rows are in flight per step.
+template <int CH, int G>
+__device__ __forceinline__ void bwd_chain(const float* __restrict__ dnb, uint32_t pitch, int dv,
+                                          const uint64_t* __restrict__ tkeys, const float* __restrict__ twn, int t0,
+                                          int t1, int lane, float4 (&acc)[CH]) {
+  for (int tb = t0; tb < t1; tb += 32) {
+    const int m = min(32, t1 - tb);
+    int32_t d = 0;
+    float w = 0.f;
+    if (lane < m) {
+      d = (int32_t)(tkeys[tb + lane] >> 32);
+      w = twn[tb + lane];
+    }
+    for (int u0 = 0; u0 < m; u0 += G) {
+      float4 x[G][CH];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int32_t du = __shfl_sync(GNS_FULL, d, (u0 + u) & 31);
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int c = lane + 32 * k;
+          x[u][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (u0 + u < m && c < dv) x[u][k] = row4(dnb, du, pitch)[c];
         }
       }
-      put_twn(bv, a, Lj, twn + bj, lane);
-      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const float wu = __shfl_sync(GNS_FULL, w, (u0 + u) & 31);
+        if (u0 + u < m) {
+#pragma unroll
+          for (int k = 0; k < CH; ++k)
+            if (lane + 32 * k < dv) vfma<true>(acc[k], wu, x[u][k]);
+        }
+      }
+    }
+  }
+}
+
+// the partial sum of segment `task` of row s (items b + j*kBwdSeg ...)
+template <int CH, int G>
+__device__ __forceinline__ void bwd_segment(const float* dnb, uint32_t pitch, int dv, const uint64_t* tkeys,
+                                            const float* twn, int b, int e, int j, int lane, float4 (&p)[CH]) {
+#pragma unroll
+  for (int k = 0; k < CH; ++k) p[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  bwd_chain<CH, G>(dnb, pitch, dv, tkeys, twn, b + j * kBwdSeg, min(e, b + (j + 1) * kBwdSeg), lane, p);
+}
+
+// every warp, before its own rows: compute unclaimed segments
+template <int CH, int G>
+__device__ __noinline__ void bwd_long_produce(const LongRows lr, int nsegs, int gen, const int32_t* tptr,
+                                                 const float* dnb, uint32_t pitch, int dv, const uint64_t* tkeys,
+                                                 const float* twn, int64_t gw, int64_t nw, int lane) {
+  for (int64_t task = gw; task < nsegs; task += nw) {
+    int mine = 0;
+    if (lane == 0) mine = atomicExch(lr.claim + task, gen) != gen;
+    if (!__shfl_sync(GNS_FULL, mine, 0)) continue;
+    const int s = lr.seg_row[task];
+    const int b = tptr[s], e = tptr[s + 1];
+    float4 p[CH];
+    bwd_segment<CH, G>(dnb, pitch, dv, tkeys, twn, b, e, (int)task - lr.sbase[s], lane, p);
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int c = lane + 32 * k;
+      if (c < dv) lr.part[task * dv + c] = p[k];
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(lr.done + task, gen);
+  }
+}
+
+template <int CH> struct RowAcc { float4 v[CH]; };
+
+// the owner of long row s: its segments' partials added in segment order.
+// The warp claims 32 segments at once (one atomic per lane), computes the
+// ones nobody had claimed (storing them like a producer), waits for the rest
+// (each lane polls its segments' flags), then sums the partial rows with 8
+// loads in flight.
+template <int CH, int G>
+__device__ __forceinline__ RowAcc<CH> bwd_long_row(const LongRows lr, int gen, const float* dnb, uint32_t pitch, int dv,
+                                                const uint64_t* tkeys, const float* twn, int s, int b, int e,
+                                                int lane) {
+  const int base = lr.sbase[s];
+  const int nseg = (e - b + kBwdSeg - 1) / kBwdSeg;
+  for (int j0 = 0; j0 < nseg; j0 += 32) {
+    const int j = j0 + lane;
+    const bool mine = j < nseg && atomicExch(lr.claim + base + j, gen) != gen;
+    for (unsigned mm = __ballot_sync(GNS_FULL, mine); mm; mm &= mm - 1) {
+      const int jj = j0 + __ffs(mm) - 1;
+      float4 p[CH];
+      bwd_segment<CH, G>(dnb, pitch, dv, tkeys, twn, b, e, jj, lane, p);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int c = lane + 32 * k;
+        if (c < dv) lr.part[(int64_t)(base + jj) * dv + c] = p[k];
+      }
+    }
+    if (!mine && j < nseg)
+      while (ld_acquire(lr.done + base + j) != gen) __nanosleep(32);
+  }
+  __threadfence();   // own partials (other lanes' stores) before the reads below
+  __syncwarp();
+  RowAcc<CH> out;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) out.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int B = 8;
+  for (int j0 = 0; j0 < nseg; j0 += B) {
+    float4 p[B][CH];
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int c = lane + 32 * k;
+        p[u][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j0 + u < nseg && c < dv) p[u][k] = __ldcg(lr.part + (int64_t)(base + j0 + u) * dv + c);
+      }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        if (j0 + u >= nseg) continue;
+        if (j0 + u == 0) {
+          out.v[k] = p[u][k];
+        } else {
+          out.v[k].x += p[u][k].x; out.v[k].y += p[u][k].y; out.v[k].z += p[u][k].z; out.v[k].w += p[u][k].w;
+        }
+      }
+  }
+  return out;
+}
+
+// Long rows (more than kBwdLong items) run as empty rows in a backward
+// kernel's row loop (dz = 0 written) and are finished here, after it, by the
+// warp that owned them there ((r >> own_shift) % nw: program order makes the
+// real row the last write; the bias-gradient partials group the same way
+// every run),
+// dz = mask(sum of segment partials + self row).  MASK: 0 none, 1 the
+// pre-activation rows zmask, 2 the forward's relu' bits (mw words per row).
+// (not inlined, like bwd_long_produce: the kernels' row loops keep their
+// register allocation; the column-sum contribution comes back by value)
+template <int CH, int G, int MASK>
+__device__ __noinline__ RowAcc<CH> bwd_long_rows(const LongRows lr, int gen, const float* __restrict__ dcat,
+                                                 int64_t ld_dcat, int dim, int dv, const int32_t* __restrict__ tptr,
+                                                 const uint64_t* __restrict__ tkeys, const float* __restrict__ twn,
+                                                 const int32_t* __restrict__ self_of, const float* __restrict__ zmask,
+                                                 const uint32_t* __restrict__ relu_bits, int mw,
+                                                 float* __restrict__ dh, int64_t ld_dh, int64_t gw, int64_t nw,
+                                                 int lane, int own_shift) {
+  RowAcc<CH> col;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) col.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int nl = lr.ctr[kCtrLong];
+  const uint32_t pitch = (uint32_t)ld_dcat * 4u;
+  for (int k0 = 0; k0 < nl; k0 += 32) {
+    const int32_t r = k0 + lane < nl ? lr.llist[k0 + lane] : -1;
+    for (unsigned m = __ballot_sync(GNS_FULL, r >= 0 && (int64_t)(r >> own_shift) % nw == gw); m; m &= m - 1) {
+      const int s = __shfl_sync(GNS_FULL, r, __ffs(m) - 1);
+      const int b = tptr[s], e = tptr[s + 1], sd = self_of[s];
+      const RowAcc<CH> ra = bwd_long_row<CH, G>(lr, gen, dcat + dim, pitch, dv, tkeys, twn, s, b, e, lane);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int c = lane + 32 * k;
+        if (c >= dv) continue;
+        uint4 mk = make_uint4(~0u, ~0u, ~0u, ~0u);
+        if constexpr (MASK == 2) mk = reinterpret_cast<const uint4*>(relu_bits + (int64_t)s * mw)[k];
+        float4 a = ra.v[k];
+        if (sd >= 0) {
+          const float4 y = reinterpret_cast<const float4*>(dcat + (int64_t)sd * ld_dcat)[c];
+          a.x += y.x; a.y += y.y; a.z += y.z; a.w += y.w;
+        }
+        if constexpr (MASK == 1) {
+          const float4 z = reinterpret_cast<const float4*>(zmask + (int64_t)s * ld_dh)[c];
+          a.x = z.x > 0.f ? a.x : 0.f; a.y = z.y > 0.f ? a.y : 0.f;
+          a.z = z.z > 0.f ? a.z : 0.f; a.w = z.w > 0.f ? a.w : 0.f;
+        } else if constexpr (MASK == 2) {
+          a.x = ((mk.x >> lane) & 1u) ? a.x : 0.f; a.y = ((mk.y >> lane) & 1u) ? a.y : 0.f;
+          a.z = ((mk.z >> lane) & 1u) ? a.z : 0.f; a.w = ((mk.w >> lane) & 1u) ? a.w : 0.f;
+        }
+        col.v[k].x += a.x; col.v[k].y += a.y; col.v[k].z += a.z; col.v[k].w += a.w;
+        reinterpret_cast<float4*>(dh + (int64_t)s * ld_dh)[c] = a;
+      }
+    }
+  }
+  return col;
+}
+
+// after the last CTA of a backward launch: advance the generation
+__device__ __forceinline__ void bwd_long_finish(const LongRows& lr, int nsegs) {
+  if (nsegs <= 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(lr.ctr + kCtrTicket, 1) == (int)gridDim.x - 1) {
+      lr.ctr[kCtrTicket] = 0;
+      atomicAdd(lr.ctr + kCtrGen, 1);
     }
   }
 }
@@ -1169,7 +1465,8 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
                                                               const T* __restrict__ zmask,
                                                               T* __restrict__ colpart,
                                                               const uint32_t* __restrict__ relu_bits = nullptr,
-                                                              const float* __restrict__ twn = nullptr) {
+                                                              const float* __restrict__ twn = nullptr,
+                                                              LongRows lr = LongRows{}) {
   // BITS (float32): the per-edge coefficient comes from the transpose's twn
   // and the self row of dcat is requested before the edge loop, so a row's
   // chain is bounds -> (keys, coefficients, self row) -> dcat rows
@@ -1189,9 +1486,27 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
 #pragma unroll
     for (int q = 0; q < VW; ++q) colacc[j][q] = (T)0;
   const int mw = ((dv + 31) >> 5) * 4;
+  // float32, one column pass: long rows (> kBwdLong items) by segments, the
+  // rows themselves after the row loop (bwd_long_rows)
+  constexpr int GL = 8 / CH;   // segment chains: 8 float4 per lane in flight
+  int nsegs = 0, gen = 0;
+  if constexpr (!EXACT) {
+    const int tsegs = bv.counts[GNS_CNT_TSEGS];   // loaded with n (one round trip)
+    if (GNS_BWD_LONG && lr.ctr && dv <= 32 * CH) nsegs = tsegs;
+    if (nsegs > 0) {
+      gen = lr.ctr[kCtrGen] + 1;
+      bwd_long_produce<CH, GL>(lr, nsegs, gen, tptr, reinterpret_cast<const float*>(dcat) + dim,
+                               (uint32_t)ld_dcat * 4u, dv, tkeys, twn, gw, nw, lane);
+    }
+  }
   for (int64_t s = gw; s < n; s += nw) {
-    const int b = tptr[s], e_end = tptr[s + 1];
-    const int sd = self_of[s];
+    const int b = tptr[s];
+    int e_end = tptr[s + 1];
+    int sd = self_of[s];
+    if (nsegs > 0 && e_end - b > kBwdLong) {   // a long row: empty here, finished by this warp after the loop
+      e_end = b;
+      sd = -1;
+    }
     uint32_t my_bits = 0;   // lane i < mw holds relu-bit word i of row s
     if constexpr (BITS) my_bits = lane < mw ? relu_bits[s * mw + lane] : 0u;
     for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
@@ -1287,6 +1602,24 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
       }
     }
   }
+  if constexpr (!EXACT) {
+    if (nsegs > 0) {
+      RowAcc<CH> col;
+      if constexpr (BITS)
+        col = bwd_long_rows<CH, GL, 2>(lr, gen, (const float*)dcat, ld_dcat, dim, dv, tptr, tkeys, twn, self_of,
+                                       nullptr, relu_bits, mw, (float*)dh, ld_dh, gw, nw, lane, 0);
+      else if (zmask)
+        col = bwd_long_rows<CH, GL, 1>(lr, gen, (const float*)dcat, ld_dcat, dim, dv, tptr, tkeys, twn, self_of,
+                                       (const float*)zmask, nullptr, mw, (float*)dh, ld_dh, gw, nw, lane, 0);
+      else
+        col = bwd_long_rows<CH, GL, 0>(lr, gen, (const float*)dcat, ld_dcat, dim, dv, tptr, tkeys, twn, self_of,
+                                       nullptr, nullptr, mw, (float*)dh, ld_dh, gw, nw, lane, 0);
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        colacc[j][0] += col.v[j].x; colacc[j][1] += col.v[j].y; colacc[j][2] += col.v[j].z; colacc[j][3] += col.v[j].w;
+      }
+    }
+  }
   for (int64_t s = n + gw; s < pad_rows; s += nw) {
     V zero;
     vzero(zero);
@@ -1307,6 +1640,7 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_bwd_kernel(const T* __restric
       colpart[(int64_t)blockIdx.x * dim + col] = t;
     }
   }
+  bwd_long_finish(lr, nsegs);
 }
 
 // Column c of a [rows x ncols] row-major partial-sum matrix, summed in a
@@ -1348,7 +1682,7 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
                                                                       float* __restrict__ dh, int64_t ld_dh,
                                                                       int64_t pad_rows, float* __restrict__ colpart,
                                                                       const uint32_t* __restrict__ relu_bits,
-                                                                      const float* __restrict__ twn) {
+                                                                      const float* __restrict__ twn, LongRows lr) {
   constexpr int W = kSpmmBlock / 32;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t n = bv.counts[GNS_CNT_SRC];
@@ -1357,6 +1691,16 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nchunks = (n + kChunkRows - 1) / kChunkRows;
+  // long rows (> kBwdLong items, hub sources): segments first, the rows
+  // themselves after the row loop (bwd_long_rows)
+  constexpr int GL = 8 / CH;   // segment chains: 8 float4 per lane in flight
+  int nsegs = 0, gen = 0;
+  const int tsegs = bv.counts[GNS_CNT_TSEGS];   // loaded with n (one round trip)
+  if (GNS_BWD_LONG && lr.ctr) nsegs = tsegs;
+  if (nsegs > 0) {
+    gen = lr.ctr[kCtrGen] + 1;
+    bwd_long_produce<CH, GL>(lr, nsegs, gen, tptr, dcat + dim, (uint32_t)ld_dcat * 4u, dv, tkeys, twn, gw, nw, lane);
+  }
   float colacc[CH][4];
 #pragma unroll
   for (int k = 0; k < CH; ++k)
@@ -1376,6 +1720,12 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
       sd = self_of[s0 + lane];
 #pragma unroll
       for (int k = 0; k < CH; ++k) mb[k] = reinterpret_cast<const uint4*>(relu_bits + (s0 + lane) * mw)[k];
+      // a long row runs as an empty one here (dz = 0 written) and is
+      // finished by this warp after the loop (bwd_long_rows, owner = chunk's)
+      if (nsegs > 0 && e - b > kBwdLong) {
+        e = b;
+        sd = -1;
+      }
     }
     if (e > b) {
       d0 = (int32_t)(tkeys[b] >> 32);
@@ -1462,6 +1812,14 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
       }
     }
   }
+  if (nsegs > 0) {
+    const RowAcc<CH> col = bwd_long_rows<CH, GL, 2>(lr, gen, dcat, ld_dcat, dim, dv, tptr, tkeys, twn, self_of,
+                                                    nullptr, relu_bits, mw, dh, ld_dh, gw, nw, lane, 5);
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      colacc[k][0] += col.v[k].x; colacc[k][1] += col.v[k].y; colacc[k][2] += col.v[k].z; colacc[k][3] += col.v[k].w;
+    }
+  }
   for (int64_t s = n + gw; s < pad_rows; s += nw)
     for (int c = lane; c < dv; c += 32) reinterpret_cast<float4*>(dh + s * ld_dh)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (colpart) {
@@ -1478,6 +1836,7 @@ __global__ void __launch_bounds__(kSpmmBlock, MINB) spmm_bwd_rows_kernel(const f
       colpart[(int64_t)blockIdx.x * dim + col] = t;
     }
   }
+  bwd_long_finish(lr, nsegs);
 }
 
 // dz = relu'(z) * dh (model.py:218) fused with the bias gradient db = sum_r dz
@@ -1551,18 +1910,32 @@ struct BwdWs {
   float* twn;
   void* scan;
   long long tiles;
+  LongRows lr;
 };
 
 static size_t bwd_ws(int64_t max_src, int64_t max_edges, int32_t dim, void* base, size_t cap, BwdWs* w) {
   Workspace ws(base, cap);
   w->colpart = (void*)ws.take<double>((size_t)num_sms() * 8 * (size_t)(dim > 0 ? dim : 1));
-  w->tcount = ws.take<int32_t>(max_src + 1);
+  // tcount is followed by the long-row counters (one memset clears both)
+  w->tcount = ws.take<int32_t>(max_src + 1 + kCtrN);
   w->tptr = ws.take<int32_t>(max_src + 1);
   w->self_of = ws.take<int32_t>(max_src + 1);
   w->tkeys = ws.take<uint64_t>(max_edges + 1);
   w->twn = ws.take<float>(max_edges + 1);
   w->tiles = (max_src + 256 * 8 - 1) / (256 * 8) + 1;
   w->scan = (void*)ws.take<char>(scan_status_bytes(w->tiles));
+  // long rows (L > kBwdLong = 64 items) have ceil(L / kBwdSeg) <= L / 32 +
+  // 1 < 3 L / 64 segments
+  const int64_t max_segs = 3 * max_edges / 64 + 1;
+  LongRows& lr = w->lr;
+  lr.ctr = w->tcount + max_src + 1;
+  lr.sbase = ws.take<int32_t>(max_src + 1);
+  lr.seg_row = ws.take<int32_t>(max_segs);
+  lr.claim = ws.take<int32_t>(max_segs);
+  lr.done = ws.take<int32_t>(max_segs);
+  lr.slist = ws.take<int32_t>(max_edges / (kTsortWarpMax + 1) + 1);
+  lr.llist = ws.take<int32_t>(max_edges / (kBwdLong + 1) + 1);
+  lr.part = reinterpret_cast<float4*>(ws.take<float>((size_t)max_segs * (size_t)((dim + 3) / 4 * 4)));
   return ws.off;
 }
 
@@ -2188,7 +2561,7 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
   spmm_bwd_rows_kernel<CH, R, B><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,         \
                                                                 w.self_of, dh, ld_dh, pad_rows,                 \
                                                                 db ? (float*)w.colpart : nullptr, relu_bits,    \
-                                                                w.twn)
+                                                                w.twn, w.lr)
   // knob: 1 = R2/4 CTAs per SM, 2 = R2/3, 3 = R4/3, 4 = R4/2, 5 = R8/2
   if (g_tune_bwd > 0 && dv <= 64) {
     if (dv <= 32) {
@@ -2216,7 +2589,7 @@ int gns_spmm_bwd_transposed_bits(const float* dcat, int64_t ld_dcat, int32_t dim
   spmm_bwd_kernel<float, CH, true><<<g2, kSpmmBlock, 0, stream>>>(dcat, ld_dcat, dim, bv, w.tptr, w.tkeys,       \
                                                                   w.self_of, dh, ld_dh, pad_rows, nullptr,       \
                                                                   db ? (float*)w.colpart : nullptr, relu_bits,   \
-                                                                  w.twn)
+                                                                  w.twn, w.lr)
   if (dv <= 32) {
     GNS_BWDB(1);
   } else if (dv <= 64) {
@@ -2290,7 +2663,7 @@ int gns_block_transpose(const gns_block_t* block, int64_t max_dst, int64_t max_s
   }
   const int sms = num_sms();
   BlockView bv = view_of(block);
-  GNS_CUDA(cudaMemsetAsync(w.tcount, 0, (max_src + 1) * sizeof(int32_t), stream));
+  GNS_CUDA(cudaMemsetAsync(w.tcount, 0, (max_src + 1 + kCtrN) * sizeof(int32_t), stream));
   GNS_CUDA(cudaMemsetAsync(w.self_of, 0xff, (max_src + 1) * sizeof(int32_t), stream));
   int g1 = grid_for((max_edges + max_dst + 255) / 256, (long long)sms * 8);
   tcount_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.self_of);
@@ -2299,7 +2672,18 @@ int gns_block_transpose(const gns_block_t* block, int64_t max_dst, int64_t max_s
   tscan_apply_kernel<<<ttiles, kTsBlock, 0, stream>>>(bv, w.tcount, w.tptr, (unsigned long long*)w.scan);
   tscatter_kernel<<<g1, 256, 0, stream>>>(bv, w.tcount, w.tptr, w.tkeys);
   int g2 = grid_for((max_src + 255) / 256, (long long)sms * 8);   // a warp per 32 rows
-  tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys, w.twn);
+  tsort_kernel<<<g2, 256, 0, stream>>>(bv, w.tptr, w.tkeys, w.twn, w.lr);
+  // rows longer than a warp's shared slice: a CTA each (a small grid: with
+  // no such rows its CTAs exit at once, and 64 KB CTAs must find room next
+  // to the training branch's kernels)
+  static bool attr = false;
+  if (!attr) {
+    GNS_CUDA(cudaFuncSetAttribute(tsort_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kTsortLongKeys * (int)sizeof(uint64_t)));
+    attr = true;
+  }
+  tsort_long_kernel<<<kTsortLongGrid, kTsortLongThreads, kTsortLongKeys * sizeof(uint64_t), stream>>>(bv, w.tptr, w.tkeys,
+                                                                                            w.twn, w.lr);
   return check_launch("block_transpose");
 }
 
@@ -2324,8 +2708,8 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
     return GNS_EINVAL;
   }
   const int VW = dtype == 0 ? 4 : 2;
-  if (dim % VW || ld_dcat % VW || ld_dh % VW) {
-    set_error("spmm_bwd: dim/strides must be multiples of %d", VW);
+  if (dim % VW || ld_dcat % VW || ld_dh % VW || ld_dcat >= (1LL << 29)) {
+    set_error("spmm_bwd: dim/strides must be multiples of %d (row stride < 2^29)", VW);
     return GNS_EINVAL;
   }
   const int sms = num_sms();
@@ -2339,7 +2723,7 @@ int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, in
 #define GNS_BWD(T, CH)                                                                                       \
   spmm_bwd_kernel<T, CH><<<g2, kSpmmBlock, 0, stream>>>((const T*)dcat, ld_dcat, dim, bv, w.tptr, w.tkeys, \
                                                         w.self_of, (T*)dh, ld_dh, pad_rows, (const T*)z_mask,  \
-                                                        db ? (T*)w.colpart : nullptr)
+                                                        db ? (T*)w.colpart : nullptr, nullptr, w.twn, w.lr)
   if (dtype == 0) {
     if (dv <= 32) GNS_BWD(float, 1);
     else if (dv <= 64) GNS_BWD(float, 2);

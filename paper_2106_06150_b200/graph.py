@@ -181,9 +181,18 @@ def generate_powerlaw_device(num_nodes: int, num_pairs: int, alpha: float = 0.6,
     _lib.call("gns_gen_powerlaw_fill", num_nodes, num_pairs, indptr.data_ptr(), indices.data_ptr(),
               ws.data_ptr(), ws.numel(), stream)
     del ws
-    # labels, masks and features: pure functions of (seed, node) on the device
-    # (gns_gen_node_attrs / gns_gen_features), reproducible bit for bit by the
-    # host restatement oracle/gen.c
+    return _with_node_data(Graph(num_nodes, indptr, indices), seed, feature_dim, num_classes, train_frac,
+                           feature_noise)
+
+
+def _with_node_data(g: Graph, seed: int, feature_dim: int, num_classes: int, train_frac: float,
+                    feature_noise: float) -> Graph:
+    """Labels, masks and features as pure functions of (seed, node) on the
+    device (gns_gen_node_attrs / gns_gen_features; class mean + noise, the
+    graph.py:249-253 scheme), reproducible bit for bit on the host by
+    oracle/gen.cc."""
+    num_nodes, dev, stream = g.num_nodes, g.device, _lib.stream_ptr()
+    indptr, indices = g.indptr, g.indices
     labels = torch.empty(num_nodes, dtype=torch.int32, device=dev)
     train, val, test = (torch.empty(num_nodes, dtype=torch.bool, device=dev) for _ in range(3))
     _lib.call("gns_gen_node_attrs", num_nodes, num_classes, float(train_frac), seed & 0xFFFFFFFF,
@@ -197,3 +206,42 @@ def generate_powerlaw_device(num_nodes: int, num_pairs: int, alpha: float = 0.6,
                   seed & 0xFFFFFFFF, labels.data_ptr(), means.data_ptr(), feats.data_ptr(), stream)
     return Graph(num_nodes, indptr, indices, feats, labels, train, val, test,
                  feature_dim=feature_dim if feature_dim else None)
+
+
+def generate_powerlaw(num_nodes: int, attach: int, seed: int, feature_dim: int = 0, num_classes: int = 2,
+                      train_frac: float = 1.0, feature_noise: float = 3.0, device=None) -> Graph:
+    """The reference's preferential-attachment graph (graph.py:172-205) —
+    the same graph for the same ``(num_nodes, attach, seed)``: every node
+    s >= attach links to ``attach`` distinct endpoints drawn uniformly from
+    the list of all edge endpoints so far (degree-proportional).  The draw
+    is inherently sequential and defined by numpy's PCG64 stream, so it runs
+    on the host (≈3 s at 100K nodes x 10); the CSR is built on the device
+    (``build_csr``), and labels / masks / features (``feature_dim > 0``) come
+    from the device attribute generator of ``generate_powerlaw_device``."""
+    if attach < 1:
+        raise ValueError("attach must be >= 1")
+    if num_nodes <= attach:
+        raise ValueError(f"need n > attach, got n={num_nodes}, attach={attach}")
+    from .formats import build_csr
+    rng = np.random.default_rng(seed)
+    m, n = attach, num_nodes
+    pool = np.empty(2 * (n - m) * m, dtype=np.int64)     # every endpoint so far
+    heads = np.empty((n - m, m), dtype=np.int64)         # node s's m neighbours
+    prev = list(range(m))
+    filled = 0
+    for s in range(m, n):
+        heads[s - m] = prev
+        pool[filled:filled + m] = prev
+        pool[filled + m:filled + 2 * m] = s
+        filled += 2 * m
+        # m draws at once consume the stream exactly like m scalar draws; the
+        # set needs more only when a draw repeats an earlier pick
+        chosen = set()
+        for v in pool[rng.integers(filled, size=m)].tolist():
+            chosen.add(v)
+        while len(chosen) < m:
+            chosen.add(int(pool[rng.integers(filled)]))
+        prev = list(chosen)          # set iteration order, as np.fromiter(set)
+    tails = np.repeat(np.arange(m, n, dtype=np.int64), m)
+    g = build_csr(np.stack([tails, heads.reshape(-1)], 1), n, device=device)
+    return _with_node_data(g, seed, feature_dim, num_classes, train_frac, feature_noise)

@@ -1,6 +1,6 @@
 """Generate golden fixtures by running the REFERENCE (gnsbench) in this container.
 
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [powerlaw]
 
 The reference is Python and cannot travel to the GPU box, so its outputs on
 small inputs are committed here (``golden_*.npz``).  Each fixture records the
@@ -243,7 +243,30 @@ def make_format_golden():
     gb.save_binary(g, os.path.join(HERE, "golden_sbm60.gnsg"))
 
 
+def make_powerlaw_golden():
+    """The reference's preferential-attachment generator (graph.py:172-205):
+    two small CSRs, and SHA-256 digests of the BASELINE config-1 graph
+    generate_powerlaw(100000, 10, 0) (int64 indptr, int64 indices)."""
+    import hashlib
+    out = {}
+    for tag, (n, m, seed) in {"a": (500, 3, 2), "b": (3000, 10, 0)}.items():
+        g = gb.generate_powerlaw(n, m, seed)
+        out[f"{tag}_args"] = np.array([n, m, seed])
+        out[f"{tag}_indptr"] = g.indptr
+        out[f"{tag}_indices"] = g.indices.astype(np.int32)
+    g = gb.generate_powerlaw(100000, 10, 0)
+    out["cfg1_args"] = np.array([100000, 10, 0])
+    out["cfg1_num_edges"] = np.array(len(g.indices))
+    out["cfg1_indptr_sha256"] = np.array(hashlib.sha256(np.ascontiguousarray(g.indptr, np.int64)).hexdigest())
+    out["cfg1_indices_sha256"] = np.array(hashlib.sha256(np.ascontiguousarray(g.indices, np.int64)).hexdigest())
+    np.savez_compressed(os.path.join(HERE, "golden_powerlaw.npz"), **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["powerlaw"]:
+        make_powerlaw_golden()
+        sys.exit(0)
+    make_powerlaw_golden()
     make_format_golden()
     make_kat_golden()
     make_sampler_golden()

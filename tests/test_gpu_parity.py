@@ -4,6 +4,8 @@ Bit-exact for ids, offsets, relabel maps, float64 weights, cached CSR and the
 float64 SpMM; statistical tests for the draws; tolerance-stated for training.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -1892,3 +1894,92 @@ def test_spmm_fwd_full_block_long_rows_float32(P, dim):
             _lib.call("gns_spmm_fwd_gather", h.data_ptr(), dim, dim, blk._c, ids.data_ptr(), n, n, 0, 0,
                       o3.data_ptr(), 2 * dim, _lib.stream_ptr())
             assert torch.equal(o3, out[:n])
+
+
+def test_generate_powerlaw_is_the_reference_graph(P):
+    """P.generate_powerlaw (graph.py:172-205: host draws, device CSR) builds
+    the reference's preferential-attachment graph: equal to the golden CSRs
+    and to the oracle restatement; node data equal the device attribute
+    generator's host restatement."""
+    from oracle import gen
+    with np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_powerlaw.npz")) as z:
+        gold = {k: z[k] for k in z.files}
+    for tag in ("a", "b"):
+        n, m, seed = (int(x) for x in gold[f"{tag}_args"])
+        g = P.generate_powerlaw(n, m, seed, feature_dim=6, num_classes=3, train_frac=0.3)
+        assert np.array_equal(g.indptr.cpu().numpy(), gold[f"{tag}_indptr"])
+        assert np.array_equal(g.indices.cpu().numpy(), gold[f"{tag}_indices"])
+        labels, tr, va, te = gen.node_attrs(n, 3, 0.3, seed)
+        assert np.array_equal(g.labels.cpu().numpy(), labels)
+        assert np.array_equal(g.train_mask.cpu().numpy(), tr)
+        f = gen.features(n, 6, 3, labels, 3.0, seed)
+        assert np.array_equal(g.features.cpu().numpy().view(np.uint32), f.view(np.uint32))
+    with pytest.raises(ValueError):
+        P.generate_powerlaw(5, 5, 0)
+
+
+def test_spmm_bwd_long_transposed_rows(P):
+    """Transposed rows of any length (hub sources: the neighbour of thousands
+    of dst rows).  Rows of 65..256 entries are sorted by a warp in shared
+    memory, longer ones by a CTA (in shared memory up to 8192, in place in
+    global memory beyond); rows of more than 64 are summed by 64-entry
+    segments spread over all warps.  float64 stays bit-exact with scipy's
+    order (model.py:223-225); every float32 path (z mask, relu' bits, every
+    lane-staged variant) gives the same dz bit for bit, within float32
+    rounding of float64, and repeated launches over one transpose (the
+    segments' generation counter) never reuse another launch's partials."""
+    import types
+    from paper_2106_06150_b200 import _lib
+    from paper_2106_06150_b200.train import full_block
+    rng = np.random.default_rng(3)
+    n = 12000
+    parts = [rng.integers(5, n, size=(20000, 2))]
+    for hub, d in ((0, n - 1), (1, 3000), (2, 200), (3, 65), (4, 64)):
+        nb = np.arange(1, n) if hub == 0 else rng.choice(np.arange(5, n), d, replace=False)
+        parts.append(np.stack([np.full(len(nb), hub), nb], 1))
+    og = O.build_csr(np.concatenate(parts), n)
+    g = P.Graph.from_numpy(n, og.indptr, og.indices)
+    blk = full_block(g)
+    tlen = np.bincount(og.indices, minlength=n)
+    assert tlen.max() > 8192 and np.any((tlen > 256) & (tlen <= 8192)) and np.any((tlen > 64) & (tlen <= 256))
+    ref = types.SimpleNamespace(src_nodes=np.arange(n), dst_nodes=np.arange(n), edge_src=og.indices,
+                                edge_dst=np.repeat(np.arange(n), np.diff(og.indptr)),
+                                edge_weight=np.ones(og.num_edges), dst_degree=np.diff(og.indptr))
+    E = og.num_edges
+    lib = _lib.lib()
+    for dim in (64, 256):
+        ws = _lib.workspace(lib.gns_spmm_bwd_workspace_size(n, E, dim), "cuda")
+        dcats = [np.random.default_rng(40 + k + dim).normal(size=(n, 2 * dim)) for k in range(2)]
+        expect = OM.spmm_mean_bwd(ref, dcats[0], dim)
+        dt = torch.as_tensor(dcats[0], device="cuda")
+        dh = torch.empty((n, dim), dtype=torch.float64, device="cuda")
+        _lib.call("gns_spmm_bwd", 1, dt.data_ptr(), 2 * dim, dim, blk._c, n, n, E, 0, None, None, dh.data_ptr(),
+                  dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        assert np.array_equal(dh.cpu().numpy(), expect), dim
+        # float32: z-mask path vs the relu'-bits paths
+        z = torch.randn((n, dim), device="cuda", generator=torch.Generator(device="cuda").manual_seed(dim))
+        bits = torch.zeros(lib.gns_relu_bits_size(n, dim) // 4, dtype=torch.int32, device="cuda")
+        cat = torch.empty((n, 2 * dim), device="cuda")
+        _lib.call("gns_spmm_fwd_bits", z.data_ptr(), dim, dim, blk._c, n, n, cat.data_ptr(), 2 * dim,
+                  bits.data_ptr(), _lib.stream_ptr())
+        d32 = [torch.as_tensor(d.astype(np.float32), device="cuda") for d in dcats]
+        base = torch.empty((n, dim), device="cuda")
+        db0 = torch.empty(dim, device="cuda")
+        _lib.call("gns_spmm_bwd", 0, d32[0].data_ptr(), 2 * dim, dim, blk._c, n, n, E, 0, z.data_ptr(),
+                  db0.data_ptr(), base.data_ptr(), dim, ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+        dz64 = expect * (z.double().cpu().numpy() > 0)
+        np.testing.assert_allclose(base.double().cpu().numpy(), dz64, rtol=1e-3, atol=2e-3)
+        out = torch.empty((n, dim), device="cuda")
+        db = torch.empty(dim, device="cuda")
+        try:
+            for knob in range(6):
+                _lib.call("gns_tune", b"spmm_bwd", knob)
+                for k in (1, 0):   # another launch's dcat first, then the checked one
+                    out.fill_(float("nan"))
+                    _lib.call("gns_spmm_bwd_transposed_bits", d32[k].data_ptr(), 2 * dim, dim, blk._c, n, n, E, 0,
+                              bits.data_ptr(), db.data_ptr(), out.data_ptr(), dim, ws.data_ptr(), ws.numel(),
+                              _lib.stream_ptr())
+                assert torch.equal(out, base), (dim, knob)
+                np.testing.assert_allclose(db.cpu().numpy(), db0.cpu().numpy(), rtol=1e-4, atol=1e-2)
+        finally:
+            _lib.call("gns_tune", b"spmm_bwd", 4)

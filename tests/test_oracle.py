@@ -314,3 +314,37 @@ def test_host_cached_csr_equals_build_cache():
     ip, ix = gen.cached_csr(g.indptr, g.indices, c.mask, threads=3)
     assert np.array_equal(ip, c.cached_indptr) and np.array_equal(ix, c.cached_indices)
 
+
+
+def _powerlaw_golden():
+    with np.load(os.path.join(ROOT, "tests", "golden", "golden_powerlaw.npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+def test_powerlaw_attach_matches_reference_golden():
+    """oracle.gns.generate_powerlaw (graph.py:172-205 restated, batched
+    draws) reproduces the reference's graphs: two small CSRs exactly and the
+    BASELINE config-1 graph generate_powerlaw(100000, 10, 0) by digest."""
+    import hashlib
+    gold = _powerlaw_golden()
+    for tag in ("a", "b"):
+        n, m, seed = (int(x) for x in gold[f"{tag}_args"])
+        g = O.generate_powerlaw(n, m, seed)
+        assert np.array_equal(g.indptr, gold[f"{tag}_indptr"])
+        assert np.array_equal(g.indices, gold[f"{tag}_indices"])
+    n, m, seed = (int(x) for x in gold["cfg1_args"])
+    g = O.generate_powerlaw(n, m, seed)
+    assert len(g.indices) == int(gold["cfg1_num_edges"]) == 1_999_800
+    assert hashlib.sha256(np.ascontiguousarray(g.indptr, np.int64)).hexdigest() == str(gold["cfg1_indptr_sha256"])
+    assert hashlib.sha256(np.ascontiguousarray(g.indices, np.int64)).hexdigest() == str(gold["cfg1_indices_sha256"])
+    with pytest.raises(ValueError):
+        O.generate_powerlaw(3, 3, 0)
+    with pytest.raises(ValueError):
+        O.generate_powerlaw(10, 0, 0)
+
+
+def test_powerlaw_attach_equals_live_reference(gb):
+    for n, m, seed in ((60, 2, 3), (1500, 4, 9)):
+        r = gb.generate_powerlaw(n, m, seed)
+        o = O.generate_powerlaw(n, m, seed)
+        assert np.array_equal(o.indptr, r.indptr) and np.array_equal(o.indices, r.indices)
