@@ -1065,7 +1065,7 @@ __global__ void tscatter_kernel(BlockView bv, int32_t* __restrict__ cursor, cons
 #ifndef GNS_BWD_LONG
 #define GNS_BWD_LONG 1   // (0: builds without the long-row path, for A/B)
 #endif
-constexpr int kBwdLong = 64, kBwdSeg = 32, kTsortWarpMax = 256;
+constexpr int kBwdLong = 16, kBwdSeg = 32, kTsortWarpMax = 256;
 enum { kCtrSegs = 0, kCtrSort = 1, kCtrGen = 2, kCtrTicket = 3, kCtrLong = 4, kCtrN = 8 };
 
 struct LongRows {
@@ -1924,9 +1924,9 @@ static size_t bwd_ws(int64_t max_src, int64_t max_edges, int32_t dim, void* base
   w->twn = ws.take<float>(max_edges + 1);
   w->tiles = (max_src + 256 * 8 - 1) / (256 * 8) + 1;
   w->scan = (void*)ws.take<char>(scan_status_bytes(w->tiles));
-  // long rows (L > kBwdLong = 64 items) have ceil(L / kBwdSeg) <= L / 32 +
-  // 1 < 3 L / 64 segments
-  const int64_t max_segs = 3 * max_edges / 64 + 1;
+  // a long row (L > kBwdLong items) has ceil(L / kBwdSeg) < L / kBwdSeg + 1
+  // segments, and there are fewer than E / kBwdLong long rows
+  const int64_t max_segs = max_edges / kBwdSeg + max_edges / (kBwdLong + 1) + 1;
   LongRows& lr = w->lr;
   lr.ctr = w->tcount + max_src + 1;
   lr.sbase = ws.take<int32_t>(max_src + 1);
