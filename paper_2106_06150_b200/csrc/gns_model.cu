@@ -224,6 +224,76 @@ __device__ __forceinline__ void put_relu_bits(uint32_t*, int, const double2&, bo
 // then reads 32 bytes per row instead of the whole pre-activation row.  Every
 // src row of a block is a dst (self) row or an edge source, so every row the
 // backward needs gets its bits.
+// A row longer than spmm_fwd_kernel's shared stage (full-neighbourhood
+// blocks of hub rows, not sampled ones): the same ascending-source FMA
+// sequence, each next source found by a warp arg-min over the row
+// (O(L^2 / 32)).  Its own kernel (spmm_fwd_long_kernel, launched after
+// spmm_fwd_kernel, which skips such rows): inlined into spmm_fwd_kernel this
+// path took it from 79 to 128 registers and the OAG input layer from 225 to
+// 275 us; a non-inlined call still cost spills.
+template <typename T, int CH, bool RELU, bool GATHER, bool MASK>
+__device__ __forceinline__ void spmm_fwd_row_long(const T* __restrict__ h, int64_t ld_h, int dv, BlockView bv,
+                                               T* __restrict__ cat, int64_t ld_cat, const int32_t* __restrict__ eidx,
+                                               const int32_t* __restrict__ dst_ids, uint32_t* __restrict__ relu_bits,
+                                               int64_t r, int64_t cb, int nc, int64_t fb, int L, int lane) {
+  using V = typename Vec<T>::type;
+  const T norm = (T)max(bv.dst_degree[r], 1);
+  const V* hs = reinterpret_cast<const V*>(h + (int64_t)(GATHER ? dst_ids[r] : bv.self_pos[r]) * ld_h);
+  V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
+  const int mw = ((dv + 31) >> 5) * 4;
+  for (int c0 = 0; c0 < dv; c0 += 32) {
+    const int c = c0 + lane;
+    V v;
+    vzero(v);
+    if (c < dv) {
+      v = ldv<V, RELU>(hs + c);
+      crow[c] = v;
+    }
+    if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)bv.self_pos[r] * mw, c0 >> 5, v, c < dv);
+  }
+  for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
+    V acc[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) vzero(acc[j]);
+    int64_t last = -1;
+    for (int t = 0; t < L; ++t) {
+      int32_t best = INT32_MAX;
+      T bw = 0;
+      for (int i = lane; i < L; i += 32) {
+        const int64_t e = i < nc ? cb + i : fb + (i - nc);
+        const int32_t v = eidx[e];
+        if ((int64_t)v > last && v < best) {
+          best = v;
+          bw = (T)bv.edge_weight[e];
+        }
+      }
+      int32_t mn = best;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(GNS_FULL, mn, o));
+      const int win = __ffs(__ballot_sync(GNS_FULL, best == mn)) - 1;
+      const T w0 = __shfl_sync(GNS_FULL, bw, win);
+      last = mn;
+      const V* r0 = reinterpret_cast<const V*>(h + (int64_t)mn * ld_h);
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = c0 + lane + 32 * j;
+        V x;
+        vzero(x);
+        if (c < dv) {
+          x = ldv<V, RELU>(r0 + c);
+          vfma<true>(acc[j], w0, x);
+        }
+        if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)mn * mw, (c0 >> 5) + j, x, c < dv);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int c = c0 + lane + 32 * j;
+      if (c < dv) crow[dv + c] = vdiv(acc[j], norm);
+    }
+  }
+}
+
 template <typename T, int CH, bool RELU, bool GATHER = false, bool MASK = false>
 __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restrict__ h, int64_t ld_h, int dim,
                                                               BlockView bv, T* __restrict__ cat, int64_t ld_cat,
@@ -249,65 +319,7 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
     const int64_t cb = (int64_t)(s0 >> 32), ce = (int64_t)(s1 >> 32);
     const int64_t fb = tm + (int64_t)(s0 & 0xffffffffull), fe = tm + (int64_t)(s1 & 0xffffffffull);
     const int nc = (int)(ce - cb), L = nc + (int)(fe - fb);
-    if (L > kRowCap) {
-      // a row longer than the shared stage (full-neighbourhood blocks of
-      // hub rows, not sampled ones): the same ascending-source FMA sequence,
-      // each next source found by a warp arg-min over the row (O(L^2 / 32))
-      const T norm = (T)max(bv.dst_degree[r], 1);
-      const V* hs = reinterpret_cast<const V*>(h + (int64_t)(GATHER ? dst_ids[r] : bv.self_pos[r]) * ld_h);
-      V* crow = reinterpret_cast<V*>(cat + r * ld_cat);
-      const int mw = ((dv + 31) >> 5) * 4;
-      for (int c0 = 0; c0 < dv; c0 += 32) {
-        const int c = c0 + lane;
-        V v;
-        vzero(v);
-        if (c < dv) {
-          v = ldv<V, RELU>(hs + c);
-          crow[c] = v;
-        }
-        if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)bv.self_pos[r] * mw, c0 >> 5, v, c < dv);
-      }
-      for (int c0 = 0; c0 < dv; c0 += 32 * CH) {
-        V acc[CH];
-#pragma unroll
-        for (int j = 0; j < CH; ++j) vzero(acc[j]);
-        int64_t last = -1;
-        for (int t = 0; t < L; ++t) {
-          int32_t best = INT32_MAX;
-          T bw = 0;
-          for (int i = lane; i < L; i += 32) {
-            const int64_t e = i < nc ? cb + i : fb + (i - nc);
-            const int32_t v = eidx[e];
-            if ((int64_t)v > last && v < best) {
-              best = v;
-              bw = (T)bv.edge_weight[e];
-            }
-          }
-          int32_t mn = best;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(GNS_FULL, mn, o));
-          const int win = __ffs(__ballot_sync(GNS_FULL, best == mn)) - 1;
-          const T w0 = __shfl_sync(GNS_FULL, bw, win);
-          last = mn;
-          const V* r0 = reinterpret_cast<const V*>(h + (int64_t)mn * ld_h);
-#pragma unroll
-          for (int j = 0; j < CH; ++j) {
-            const int c = c0 + lane + 32 * j;
-            V x;
-            vzero(x);
-            if (c < dv) {
-              x = ldv<V, RELU>(r0 + c);
-              vfma<true>(acc[j], w0, x);
-            }
-            if constexpr (MASK) put_relu_bits(relu_bits + (int64_t)mn * mw, (c0 >> 5) + j, x, c < dv);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          const int c = c0 + lane + 32 * j;
-          if (c < dv) crow[dv + c] = vdiv(acc[j], norm);
-        }
-      }
+    if (L > kRowCap) {   // longer than the shared stage: spmm_fwd_long_kernel
       __syncwarp();
       continue;
     }
@@ -429,6 +441,40 @@ __global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_kernel(const T* __restric
     V zero;
     vzero(zero);
     for (int c = lane; c < 2 * dv; c += 32) crow[c] = zero;
+  }
+}
+
+// rows of more than kRowCap edges (full-neighbourhood blocks), warp per row;
+// every other row was written by spmm_fwd_kernel
+template <typename T, int CH, bool RELU, bool GATHER = false, bool MASK = false>
+__global__ void __launch_bounds__(kSpmmBlock) spmm_fwd_long_kernel(const T* __restrict__ h, int64_t ld_h, int dim,
+                                                                   BlockView bv, T* __restrict__ cat, int64_t ld_cat,
+                                                                   const int32_t* __restrict__ edge_node = nullptr,
+                                                                   const int32_t* __restrict__ dst_ids = nullptr,
+                                                                   uint32_t* __restrict__ relu_bits = nullptr) {
+  const int32_t* __restrict__ eidx = GATHER ? edge_node : bv.edge_src;
+  const int lane = threadIdx.x & 31;
+  const int64_t n = bv.counts[GNS_CNT_DST];
+  const int64_t tm = (int64_t)(bv.row_scan[n] >> 32);
+  const int dv = dim / Vec<T>::W;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // lane-parallel length test over 32 rows at a time
+  for (int64_t r0 = gw * 32; r0 < n; r0 += nw * 32) {
+    int L = 0;
+    if (r0 + lane < n) {
+      const uint64_t s0 = bv.row_scan[r0 + lane], s1 = bv.row_scan[r0 + lane + 1];
+      L = (int)((s1 >> 32) - (s0 >> 32)) + (int)((s1 & 0xffffffffull) - (s0 & 0xffffffffull));
+    }
+    for (unsigned m = __ballot_sync(GNS_FULL, L > kRowCap); m; m &= m - 1) {
+      const int64_t r = r0 + __ffs(m) - 1;
+      const uint64_t s0 = bv.row_scan[r], s1 = bv.row_scan[r + 1];
+      const int64_t cb = (int64_t)(s0 >> 32), fb = tm + (int64_t)(s0 & 0xffffffffull);
+      const int nc = (int)((s1 >> 32) - (s0 >> 32));
+      const int Lr = nc + (int)((s1 & 0xffffffffull) - (s0 & 0xffffffffull));
+      spmm_fwd_row_long<T, CH, RELU, GATHER, MASK>(h, ld_h, dv, bv, cat, ld_cat, eidx, dst_ids, relu_bits, r, cb, nc,
+                                                   fb, Lr, lane);
+    }
   }
 }
 
@@ -1131,12 +1177,41 @@ __device__ __forceinline__ float twn_of(BlockView bv, uint64_t key) {
 // would (IEEE division), so it reads one value instead of the dependent
 // weight + dst-degree loads.  A warp takes 32 consecutive rows; rows of <= 8
 // entries (nearly all: a sampled block's source rows have ~1 edge) are sorted
-// by their own lane in registers, rows of <= 32 by the warp (shuffle ranks),
+// by their own lane in registers (a 16-wide lane tier for 9..16 was measured
+// no faster on cfg1 or papers100M), rows of <= 32 by the warp (shuffle ranks),
 // rows of <= kTsortWarpMax by the warp in its shared-memory slice (bitonic),
 // longer ones are listed for tsort_long_kernel.  Rows of more than kBwdLong
 // entries are registered as segments for the backward.  Keys are unique, so
 // every path gives the same order.
 constexpr int kTsortLane = 8;
+
+// one lane sorts its row of L <= N entries in registers (odd-even
+// transposition network) and writes the keys and coefficients back
+template <int N>
+__device__ __forceinline__ void lane_sort(BlockView bv, uint64_t* __restrict__ tkeys, float* __restrict__ twn, int b,
+                                          int L) {
+  uint64_t x[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = i < L ? tkeys[b + i] : ~0ull;
+#pragma unroll
+  for (int rnd = 0; rnd < N; ++rnd)
+#pragma unroll
+    for (int i = rnd & 1; i + 1 < N; i += 2) {
+      const uint64_t lo = x[i] < x[i + 1] ? x[i] : x[i + 1], hi = x[i] < x[i + 1] ? x[i + 1] : x[i];
+      x[i] = lo;
+      x[i + 1] = hi;
+    }
+  float wv[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) wv[i] = i < L ? twn_of(bv, x[i]) : 0.f;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (i < L) {
+      tkeys[b + i] = x[i];
+      twn[b + i] = wv[i];
+    }
+}
+
 __global__ void __launch_bounds__(256) tsort_kernel(BlockView bv, const int32_t* __restrict__ tptr,
                                                     uint64_t* __restrict__ tkeys, float* __restrict__ twn,
                                                     LongRows lr) {
@@ -1165,28 +1240,7 @@ __global__ void __launch_bounds__(256) tsort_kernel(BlockView bv, const int32_t*
       }
     }
     if (L > kTsortWarpMax) lr.slist[atomicAdd(lr.ctr + kCtrSort, 1)] = (int32_t)s;
-    if (L > 0 && L <= kTsortLane) {
-      uint64_t x[kTsortLane];
-#pragma unroll
-      for (int i = 0; i < kTsortLane; ++i) x[i] = i < L ? tkeys[b + i] : ~0ull;
-#pragma unroll
-      for (int rnd = 0; rnd < kTsortLane; ++rnd)   // odd-even transposition network
-#pragma unroll
-        for (int i = rnd & 1; i + 1 < kTsortLane; i += 2) {
-          const uint64_t lo = x[i] < x[i + 1] ? x[i] : x[i + 1], hi = x[i] < x[i + 1] ? x[i + 1] : x[i];
-          x[i] = lo;
-          x[i + 1] = hi;
-        }
-      float wv[kTsortLane];
-#pragma unroll
-      for (int i = 0; i < kTsortLane; ++i) wv[i] = i < L ? twn_of(bv, x[i]) : 0.f;
-#pragma unroll
-      for (int i = 0; i < kTsortLane; ++i)
-        if (i < L) {
-          tkeys[b + i] = x[i];
-          twn[b + i] = wv[i];
-        }
-    }
+    if (L > 0 && L <= kTsortLane) lane_sort<kTsortLane>(bv, tkeys, twn, b, L);
     for (unsigned big = __ballot_sync(GNS_FULL, L > kTsortLane && L <= kTsortWarpMax); big; big &= big - 1) {
       const int j = __ffs(big) - 1;
       const int bj = __shfl_sync(GNS_FULL, b, j), Lj = __shfl_sync(GNS_FULL, L, j);
@@ -2470,9 +2524,15 @@ int gns_spmm_fwd_gather(const float* table, int64_t ld_table, int32_t dim, const
     return check_launch("spmm_fwd_gather");
   }
 #define GNS_FWDG(CH)                                                                                          \
+  do {                                                                                                         \
   spmm_fwd_kernel<float, CH, false, true><<<spmm_grid(spmm_fwd_kernel<float, CH, false, true>, rows), kSpmmBlock, \
                                             0, stream>>>(table, ld_table, dim, bv, cat, ld_cat,             \
-                                                         pad_rows, block->edge_node, dst_ids, nullptr, pad_chunk)
+                                                         pad_rows, block->edge_node, dst_ids, nullptr, pad_chunk); \
+  if (max_row_edges <= 0 || max_row_edges > kRowCap)                                                          \
+    spmm_fwd_long_kernel<float, CH, false, true><<<spmm_grid(spmm_fwd_long_kernel<float, CH, false, true>,       \
+                                                             rows / 32 + 1), kSpmmBlock, 0, stream>>>(          \
+        table, ld_table, dim, bv, cat, ld_cat, block->edge_node, dst_ids, nullptr);  \
+  } while (0)
   if (dv <= 32) GNS_FWDG(1);
   else if (dv <= 64) GNS_FWDG(2);
   else GNS_FWDG(4);
@@ -2523,10 +2583,15 @@ int gns_spmm_fwd_bits(const float* h, int64_t ld_h, int32_t dim, const gns_block
     return check_launch("spmm_fwd_bits");
   }
 #define GNS_FWDB(CH)                                                                                             \
+  do {                                                                                                         \
   spmm_fwd_kernel<float, CH, true, false, true><<<spmm_grid(spmm_fwd_kernel<float, CH, true, false, true>, rows), \
                                                   kSpmmBlock, 0, stream>>>(h, ld_h, dim, bv, cat, ld_cat,       \
                                                                                 pad_rows, nullptr, nullptr,   \
-                                                                                relu_bits)
+                                                                                relu_bits);                   \
+  spmm_fwd_long_kernel<float, CH, true, false, true><<<spmm_grid(spmm_fwd_long_kernel<float, CH, true, false, true>, \
+                                                                 rows / 32 + 1), kSpmmBlock, 0, stream>>>(      \
+      h, ld_h, dim, bv, cat, ld_cat, nullptr, nullptr, relu_bits);  \
+  } while (0)
   if (dv <= 32) GNS_FWDB(1);
   else if (dv <= 64) GNS_FWDB(2);
   else GNS_FWDB(4);
@@ -2612,8 +2677,12 @@ int gns_spmm_fwd(int32_t dtype, const void* h, int64_t ld_h, int32_t dim, int32_
   BlockView bv = view_of(block);
   const bool relu = flags & GNS_SPMM_RELU_INPUT;
 #define GNS_FWD(T, CH, R)                                                                                      \
+  do {                                                                                                         \
   spmm_fwd_kernel<T, CH, R><<<spmm_grid(spmm_fwd_kernel<T, CH, R>, rows), kSpmmBlock, 0, stream>>>(                \
-      (const T*)h, ld_h, dim, bv, (T*)cat, ld_cat, pad_rows)
+      (const T*)h, ld_h, dim, bv, (T*)cat, ld_cat, pad_rows);                                                      \
+  spmm_fwd_long_kernel<T, CH, R><<<spmm_grid(spmm_fwd_long_kernel<T, CH, R>, rows / 32 + 1), kSpmmBlock, 0,        \
+                                   stream>>>((const T*)h, ld_h, dim, bv, (T*)cat, ld_cat);  \
+  } while (0)
   if (dtype == 0) {
     if (dim % 4 || ld_h % 4 || ld_cat % 4) {
       set_error("spmm_fwd(f32): dim/strides must be multiples of 4");

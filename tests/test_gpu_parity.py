@@ -1922,7 +1922,7 @@ def test_spmm_bwd_long_transposed_rows(P):
     """Transposed rows of any length (hub sources: the neighbour of thousands
     of dst rows).  Rows of 65..256 entries are sorted by a warp in shared
     memory, longer ones by a CTA (in shared memory up to 8192, in place in
-    global memory beyond); rows of more than 64 are summed by 64-entry
+    global memory beyond); rows of more than 16 are summed by 32-entry
     segments spread over all warps.  float64 stays bit-exact with scipy's
     order (model.py:223-225); every float32 path (z mask, relu' bits, every
     lane-staged variant) gives the same dz bit for bit, within float32
@@ -1933,9 +1933,9 @@ def test_spmm_bwd_long_transposed_rows(P):
     from paper_2106_06150_b200.train import full_block
     rng = np.random.default_rng(3)
     n = 12000
-    parts = [rng.integers(5, n, size=(20000, 2))]
-    for hub, d in ((0, n - 1), (1, 3000), (2, 200), (3, 65), (4, 64)):
-        nb = np.arange(1, n) if hub == 0 else rng.choice(np.arange(5, n), d, replace=False)
+    parts = [rng.integers(8, n, size=(20000, 2))]
+    for hub, d in ((0, n - 1), (1, 3000), (2, 200), (3, 65), (4, 64), (5, 33), (6, 17), (7, 16)):
+        nb = np.arange(1, n) if hub == 0 else rng.choice(np.arange(8, n), d, replace=False)
         parts.append(np.stack([np.full(len(nb), hub), nb], 1))
     og = O.build_csr(np.concatenate(parts), n)
     g = P.Graph.from_numpy(n, og.indptr, og.indices)
