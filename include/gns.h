@@ -409,7 +409,13 @@ GNS_API int gns_spmm_bwd(int32_t dtype, const void* dcat, int64_t ld_dcat, int32
  * transpose (per src row, its edges sorted by dst — scipy's csc order) in the
  * workspace; it depends only on the sampled block, so the engine runs it on
  * the sampling branch.  gns_spmm_bwd_transposed then runs the backward from a
- * workspace the transpose was built in (same sizes). */
+ * workspace the transpose was built in (same sizes).  Long transposed rows
+ * (hub sources, more than 16 entries) are also registered as 32-entry
+ * segments (count in block->counts[GNS_CNT_TSEGS]); the float32 backward
+ * sums them across warps, in a fixed segment order (float32 results are
+ * deterministic and identical across the float32 entry points; float64
+ * keeps scipy's sequential order).  The workspace carries a generation
+ * counter, so any number of backward launches may follow one transpose. */
 GNS_API int gns_block_transpose(const gns_block_t* block, int64_t max_dst, int64_t max_src,
                                 int64_t max_edges, int32_t dim, void* ws, size_t ws_bytes, void* stream);
 GNS_API int gns_spmm_bwd_transposed(int32_t dtype, const void* dcat, int64_t ld_dcat, int32_t dim,
